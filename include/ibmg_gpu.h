@@ -1,0 +1,116 @@
+/*
+ * ibmg_gpu.h — C ABI of the B200-native implicit-IB MG-FGMRES solver.
+ *
+ * Drop-in boundary for the reference's solver interface.
+ * Every entry point names the reference function it replaces; plain pointers
+ * and sizes only.  `ptr_kind` says whether the caller's arrays are host
+ * (IBMG_PTR_HOST, copies are made inside the call) or device memory on the
+ * context's GPU (IBMG_PTR_DEVICE).  All calls are synchronous with respect
+ * to the caller's pointers on return; work is ordered on the context's own
+ * CUDA stream.  One context per host thread.
+ *
+ * DOF layout of a level with n x n cells (periodic, h = 1/n):
+ *   x = [u | v | p], each n*n doubles, index i + j*n (x fastest);
+ *   u(i,j) at (i h, (j+1/2) h), v(i,j) at ((i+1/2) h, j h), p(i,j) at the cell centre.
+ * This is the reference's packed ordering (fields.hpp:53-56, geometry.hpp:67-72)
+ * specialised to periodic boundaries, where every face is an unknown.
+ *
+ * Operator (sign convention SURVEY.md §9-D3):
+ *   momentum:   (rho/dt - mu L) u + G p - E' u,  E' = dt * S K S^T (ds^2 quadrature)
+ *   continuity: -D u
+ * which is -1 x the reference's SaddleSystem rows (saddle.hpp:11-18) plus the
+ * backward-Euler mass term.
+ *
+ * Status codes: 0 OK, 1 INVALID (std::invalid_argument in the reference),
+ * 2 NOT_CONVERGED (stats still filled; SPEC.md:478 flag), 3 CUDA, 4 NCCL.
+ */
+#ifndef IBMG_GPU_H
+#define IBMG_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { IBMG_OK = 0, IBMG_INVALID = 1, IBMG_NOT_CONVERGED = 2, IBMG_CUDA = 3, IBMG_NCCL = 4 };
+enum { IBMG_PTR_HOST = 0, IBMG_PTR_DEVICE = 1 };
+
+typedef struct ibmg_ctx ibmg_ctx;
+
+typedef struct {
+    int N;            /* fine cells per side, power of two >= 8 (GridGeometry nx = ny, geometry.hpp:19-31) */
+    double rho, mu, dt;
+    int nu1, nu2;     /* V(nu1,nu2) (CyclePolicy) */
+    int restart;      /* FGMRES restart length (30) */
+    int max_iters;    /* total Arnoldi-step cap (GmresConfig.max_iter) */
+    double rtol;      /* relative residual threshold (1e-10) */
+    int coarsest_n;   /* 4 (SPEC.md "Coarsest level at 4x4 cells") */
+    int device;       /* CUDA device ordinal */
+} ibmg_params;
+
+typedef struct {
+    int iters;        /* Arnoldi steps == V-cycles applied */
+    int restarts;
+    int converged;
+    double relres;    /* true ||b - A x|| / ||b|| */
+    double setup_ms;  /* structure rebuild at X^n (windows, lists, box inverses) */
+    double solve_ms;  /* FGMRES */
+    double total_ms;  /* whole step */
+} ibmg_stats;
+
+/* Replaces SaddleSystem construction + build_hierarchy (saddle.cpp:7-13). */
+int ibmg_create(const ibmg_params* params, ibmg_ctx** out);
+void ibmg_destroy(ibmg_ctx* ctx);
+const char* ibmg_last_error(const ibmg_ctx* ctx);
+
+/* Replaces FiberMesh + assemble_elasticity + galerkin_coarsen_elasticity
+ * (fiber.hpp:36-50, elasticity.cpp:88-107, transfers.cpp:286-293): n_mem closed
+ * membranes, nb[m] points each, stiffness kappa[m], spacing ds[m]; X interleaved
+ * (x, y), membrane-major, 2*sum(nb) doubles.  Rebuilds all per-level data. */
+int ibmg_set_structures(ibmg_ctx* ctx, int n_mem, const int* nb, const double* kappa,
+                        const double* ds, const double* X, int ptr_kind);
+
+int ibmg_num_levels(const ibmg_ctx* ctx);
+int ibmg_level_n(const ibmg_ctx* ctx, int level);
+
+/* Replaces SaddleSystem::apply (saddle.cpp:19-38) on level `level` (0 = fine). */
+int ibmg_apply(ibmg_ctx* ctx, int level, const double* w, double* out, int ptr_kind);
+/* Replaces SaddleSystem::residual (saddle.cpp:48-54): r = b - A w, norm optional. */
+int ibmg_residual(ibmg_ctx* ctx, int level, const double* b, const double* w, double* r,
+                  double* norm, int ptr_kind);
+/* Replaces restrict_saddle (transfers.cpp:107-134): level -> level+1. */
+int ibmg_restrict(ibmg_ctx* ctx, int level, const double* rf, double* rc, int ptr_kind);
+/* Replaces prolong_saddle_add (transfers.cpp:209-232, v weights corrected): wf += P ec. */
+int ibmg_prolong_add(ibmg_ctx* ctx, int level, const double* ec, double* wf, int ptr_kind);
+/* Replaces the SPEC smoother `sweep`: one multicolour box sweep in place. */
+int ibmg_sweep(ibmg_ctx* ctx, int level, const double* b, double* w, int ptr_kind);
+/* Replaces `v_cycle`: z = V(nu1,nu2)(0, b), mean-zero pressure. */
+int ibmg_vcycle(ibmg_ctx* ctx, const double* b, double* z, int ptr_kind);
+/* Replaces `coarsest_solve` on the coarsest level. */
+int ibmg_coarse_solve(ibmg_ctx* ctx, const double* b, double* x, int ptr_kind);
+/* Big-block flags of a level ((n/4)^2 ints, host); returns the count or -1. */
+int ibmg_big_blocks(ibmg_ctx* ctx, int level, int* flags_host);
+
+/* Replaces build_rhs (saddle.cpp:96-104): b = [(rho/dt) u^n + S F(X^n); 0]. */
+int ibmg_build_rhs(ibmg_ctx* ctx, const double* u_n, double* b, int ptr_kind);
+/* Replaces interpolate (fiber.cpp:116-140): U = S^T u (h^2 weights), 2*npts. */
+int ibmg_interpolate(ibmg_ctx* ctx, const double* u, double* U, int ptr_kind);
+/* Replaces spread (fiber.cpp:89-114): f = S F (ds^2 weights), 2*N^2. */
+int ibmg_spread(ibmg_ctx* ctx, const double* F, double* f, int ptr_kind);
+
+/* Replaces gmres_solve re-specified as FGMRES(restart) with
+ * one V-cycle as right preconditioner, x0 = 0. */
+int ibmg_solve(ibmg_ctx* ctx, const double* b, double* x, ibmg_stats* stats, int ptr_kind);
+
+/* Replaces step_implicit: rebuild at X^n, RHS, solve,
+ * X^{n+1} = X^n + dt S^T u^{n+1}.  u: 2N^2 in/out, p: N^2 out, X in/out. */
+int ibmg_step(ibmg_ctx* ctx, double* u, double* p, double* X, ibmg_stats* stats, int ptr_kind);
+
+/* Number of kernels this context has launched (evidence for bench's gpu_launches). */
+long long ibmg_kernel_launches(const ibmg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for callers timing with events. */
+void* ibmg_stream(const ibmg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

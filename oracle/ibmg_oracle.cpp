@@ -421,13 +421,16 @@ void extract(const Csr& A, const int* d, int m, DenseLu& lu) {
         for (int c = 0; c < m; ++c) lu.a[size_t(r) * m + c] = A.at(d[r], d[c]);
 }
 
-// Fixed multicolour schedule: tile colours (2x2 over 32x32
-// tiles), then per tile the 8 conflict-free plain colours (i+2j) mod 8 over
-// cells outside big blocks, then 16 block colours (bx mod 4, by mod 4) over big
-// 4x4 blocks.  Boxes within one pass are mutually independent, so a pass is
-// exactly a Gauss-Seidel pass in any order (SPEC.md:427-431 semantics).
+// Fixed multicolour schedule.  Plain phase: 16x16-cell
+// tiles coloured 2x2 (one tile, periodic, when n <= 16); inside each tile the
+// 8 conflict-free colours (i + 2j) mod 8 of local coordinates over cells
+// outside big blocks.  Big phase: the level-wide 16 colours (bx mod 4,
+// by mod 4) of the big 4x4 blocks (12-cell gap between same-colour blocks,
+// larger than the E' reach checked at setup).  Boxes within one pass are
+// mutually independent, so each pass is exactly a Gauss-Seidel pass in any
+// order (SPEC.md:427-431 semantics) and the GPU may run it in parallel.
 void build_schedule(Level& L) {
-    const int n = L.n, T = std::min(32, n), nt = n / T, nbk = n / 4, tb = T / 4;
+    const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4;
     L.passes.clear();
     const int ntc = nt >= 2 ? 4 : 1;
     for (int tc = 0; tc < ntc; ++tc) {
@@ -444,18 +447,17 @@ void build_schedule(Level& L) {
                 }
             if (!p.items.empty()) L.passes.push_back(std::move(p));
         }
-        for (int bc = 0; bc < 16; ++bc) {
-            Pass p;
-            p.big = true;
-            for (int by = 0; by < nbk; ++by)
-                for (int bx = 0; bx < nbk; ++bx) {
-                    if (!L.big[bx + by * nbk]) continue;
-                    if (!tile_ok(bx / tb, by / tb)) continue;
-                    if (((bx % tb) % 4) + 4 * ((by % tb) % 4) != bc) continue;
-                    p.items.push_back(bx + by * nbk);
-                }
-            if (!p.items.empty()) L.passes.push_back(std::move(p));
-        }
+    }
+    for (int bc = 0; bc < 16; ++bc) {
+        Pass p;
+        p.big = true;
+        for (int by = 0; by < nbk; ++by)
+            for (int bx = 0; bx < nbk; ++bx) {
+                if (!L.big[bx + by * nbk]) continue;
+                if ((bx % 4) + 4 * (by % 4) != bc) continue;
+                p.items.push_back(bx + by * nbk);
+            }
+        if (!p.items.empty()) L.passes.push_back(std::move(p));
     }
 }
 

@@ -1,0 +1,51 @@
+"""In-tree build of the sm_100a CUDA library (libibmg_b200.so) and the oracle.
+
+nvcc cross-compiles for sm_100a without a GPU; the .so files are git-ignored
+but travel to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libibmg_b200.so")
+SRCS = ["ibmg.cu"]
+DEPS = ["ibmg.cu", "common.cuh", "grid_kernels.cuh", "ib_kernels.cuh", "smoother_kernels.cuh", "coarse_kernel.cuh"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+
+
+def nvcc() -> str:
+    for c in ("/usr/local/cuda/bin/nvcc", "nvcc"):
+        if os.path.isabs(c) and os.path.exists(c):
+            return c
+    return "nvcc"
+
+
+def stale(target, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_cuda(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(HERE, "csrc", d) for d in DEPS] + [os.path.join(ROOT, "include", "ibmg_gpu.h")]
+    if force or stale(LIB, deps):
+        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(HERE, "csrc", s) for s in SRCS]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return LIB
+
+
+def build_oracle() -> None:
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
+
+
+if __name__ == "__main__":
+    build_cuda(force="--force" in sys.argv, verbose=True)
+    build_oracle()

@@ -1,0 +1,191 @@
+// coarse_kernel.cuh — the bottom of the V-cycle (levels with n <= 32) in ONE
+// CTA, entirely in shared memory: sweeps (same schedule as the multi-tile
+// kernels), residual with the E' part, restriction, the dense bordered coarsest
+// solve, prolongation.  Removes ~20 launches per cycle from the latency-bound
+// tail of Algorithm 1.
+#pragma once
+#include "common.cuh"
+#include "grid_kernels.cuh"
+#include "smoother_kernels.cuh"
+
+namespace ibmg {
+
+constexpr int kCoarseMaxN = 32;
+constexpr int kCoarseThreads = 512;
+
+struct CLev {
+    Lev L;
+    Win W;
+    FaceList FL;
+    const uint8_t* big;
+    const int* blk_ids;
+    const int* fidx;
+    const double* Ainv;
+    int coff[17];
+};
+
+struct CoarseArgs {
+    int nl, nu1, nu2;
+    CLev lv[6];
+    Pts P;
+    double* F;               // 2*npts scratch
+    const double* Acoarse;   // bordered inverse, col-major (3nn+1)^2
+    const double* b_in;
+    double* w_out;
+};
+
+struct SW {
+    double* s;
+    int n, nn;
+    __device__ __forceinline__ double& operator()(int f, int i, int j) const {
+        return s[f * nn + wr(i, n) + wr(j, n) * n];
+    }
+};
+
+__device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, const double* b, double (*sr)[56]) {
+    const Lev& L = C.L;
+    const int n = L.n, t = threadIdx.x, nt = blockDim.x;
+    SW W{w, n, L.nn};
+    SW B{const_cast<double*>(b), n, L.nn};
+    const int T = n < kTile ? n : kTile, ntile = n / T, ntc = ntile >= 2 ? 4 : 1;
+    const int per = T * T / 8, ntiles_c = ntc == 1 ? 1 : (ntile / 2) * (ntile / 2), nbk = n >> 2;
+    for (int tc = 0; tc < ntc; ++tc)
+        for (int pc = 0; pc < 8; ++pc) {
+            for (int idx = t; idx < ntiles_c * per; idx += nt) {
+                const int tile = idx / per, within = idx % per;
+                int tx = 0, ty = 0;
+                if (ntc == 4) {
+                    tx = 2 * (tile % (ntile / 2)) + (tc & 1);
+                    ty = 2 * (tile / (ntile / 2)) + (tc >> 1);
+                }
+                int li, lj;
+                if (T == 16) {
+                    lj = within >> 1;
+                    li = ((pc - 2 * lj) & 7) + 8 * (within & 1);
+                } else {  // T == 8
+                    lj = within;
+                    li = (pc - 2 * lj) & 7;
+                }
+                const int i = tx * T + li, j = ty * T + lj;
+                if (!C.big[(i >> 2) + (j >> 2) * nbk]) plain_cell(L, W, B, i, j);
+            }
+            __syncthreads();
+        }
+    const int g = t >> 6, tt = t & 63;
+    for (int bc = 0; bc < 16; ++bc) {
+        const int cnt = C.coff[bc + 1] - C.coff[bc];
+        for (int ch = 0; ch < cnt; ch += nt / 64) {
+            const bool act = (ch + g) < cnt && tt < 56;
+            const int q = C.coff[bc] + ch + g;
+            int bi = 0, bj = 0;
+            if (act) {
+                const int Bk = C.blk_ids[q];
+                bi = 4 * (Bk % nbk);
+                bj = 4 * (Bk / nbk);
+                sr[g][tt] =
+                    block_residual(L, C.W, A.P, C.FL, W, B, tt < 40 ? C.fidx[(size_t)q * 40 + tt] : -1, tt, bi, bj);
+            }
+            __syncthreads();
+            if (act) {
+                const double* Ai = C.Ainv + (size_t)q * 3136;
+                double s = 0.0;
+                for (int c = 0; c < 56; ++c) s += Ai[c * 56 + tt] * sr[g][c];
+                int f, i, j;
+                block_dof(tt, bi, bj, f, i, j);
+                W(f, i, j) += s;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
+    extern __shared__ double sm[];
+    __shared__ double sr[kCoarseThreads / 64][56];
+    double* wl[6];
+    double* bl[6];
+    size_t off = 0;
+    for (int l = 0; l < A.nl; ++l) {
+        const int m = 3 * A.lv[l].L.nn;
+        wl[l] = sm + off;
+        off += m;
+        bl[l] = sm + off;
+        off += m;
+    }
+    double* r = sm + off;
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) bl[0][q] = A.b_in[q];
+    __syncthreads();
+    for (int l = 0; l + 1 < A.nl; ++l) {
+        const CLev& C = A.lv[l];
+        const Lev& L = C.L;
+        const int n = L.n, nn = L.nn;
+        for (int q = t; q < 3 * nn; q += nt) wl[l][q] = 0.0;
+        __syncthreads();
+        for (int s = 0; s < A.nu1; ++s) coarse_sweep(A, C, wl[l], bl[l], sr);
+        // residual r = b - A w (stencil, then + E' w via point forces and face lists)
+        SW W{wl[l], n, nn};
+        for (int k = t; k < A.P.n; k += nt) {
+            A.F[2 * k] = point_force(C.W, A.P, k, 0, n, W);
+            A.F[2 * k + 1] = point_force(C.W, A.P, k, 1, n, W);
+        }
+        for (int q = t; q < nn; q += nt) {
+            double ru, rv, rp;
+            stokes_rows(L, W, q % n, q / n, ru, rv, rp);
+            r[q] = bl[l][q] - ru;
+            r[nn + q] = bl[l][nn + q] - rv;
+            r[2 * nn + q] = bl[l][2 * nn + q] - rp;
+        }
+        __threadfence_block();
+        __syncthreads();
+        for (int fq = t; fq < C.FL.nf; fq += nt) {
+            const int face = C.FL.face[fq], comp = face >= nn;
+            double s = 0.0;
+            for (int e = C.FL.off[fq]; e < C.FL.off[fq + 1]; ++e) {
+                const int v = C.FL.ent[e];
+                const int k = v >> 5;
+                s += C.W.w[(size_t)k * 64 + (v & 31)] * A.F[2 * k + comp];
+            }
+            r[face] += s;
+        }
+        __syncthreads();
+        // restrict into the next level's b
+        const int nc = n >> 1, nnc = nc * nc;
+        for (int q = t; q < nnc; q += nt) {
+            const int I = q % nc, J = q / nc, i = 2 * I, j = 2 * J;
+            SW R{r, n, nn};
+            bl[l + 1][q] = 0.125 * (R(0, i - 1, j) + 2.0 * R(0, i, j) + R(0, i + 1, j) + R(0, i - 1, j + 1) +
+                                    2.0 * R(0, i, j + 1) + R(0, i + 1, j + 1));
+            bl[l + 1][nnc + q] = 0.125 * (R(1, i, j - 1) + 2.0 * R(1, i, j) + R(1, i, j + 1) + R(1, i + 1, j - 1) +
+                                          2.0 * R(1, i + 1, j) + R(1, i + 1, j + 1));
+            bl[l + 1][2 * nnc + q] = 0.25 * (R(2, i, j) + R(2, i + 1, j) + R(2, i, j + 1) + R(2, i + 1, j + 1));
+        }
+        __syncthreads();
+    }
+    {
+        const int l = A.nl - 1, nn = A.lv[l].L.nn, m = 3 * nn + 1;
+        for (int q = t; q < 3 * nn; q += nt) {
+            double s = 0.0;
+            for (int c = 0; c < 3 * nn; ++c) s += A.Acoarse[(size_t)c * m + q] * bl[l][c];
+            wl[l][q] = s;
+        }
+        __syncthreads();
+    }
+    for (int l = A.nl - 2; l >= 0; --l) {
+        const CLev& C = A.lv[l];
+        const int n = C.L.n, nn = C.L.nn;
+        SW E{wl[l + 1], n >> 1, nn >> 2};
+        for (int q = t; q < nn; q += nt) {
+            double du, dv, dp;
+            prolong_rows(n, E, q % n, q / n, du, dv, dp);
+            wl[l][q] += du;
+            wl[l][nn + q] += dv;
+            wl[l][2 * nn + q] += dp;
+        }
+        __syncthreads();
+        for (int s = 0; s < A.nu2; ++s) coarse_sweep(A, C, wl[l], bl[l], sr);
+    }
+    for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) A.w_out[q] = wl[0][q];
+}
+
+}  // namespace ibmg

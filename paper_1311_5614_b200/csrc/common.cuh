@@ -1,0 +1,124 @@
+// common.cuh — shared device types and helpers for the periodic MAC-grid kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ibmg {
+
+// One multigrid level of the periodic n x n MAC grid (n a power of two).
+// d, c, g are the stencil coefficients of the negated, mass-augmented Stokes
+// rows (reference rows assembly.cpp:13-50):
+//   u row: d u_C - c (u_W + u_E + u_S + u_N) + g (p_C - p_W)
+//   p row: -g (u_E - u_C) - g (v_N - v_C)
+struct Lev {
+    int n, nn, lg;   // cells per side, n*n, log2(n)
+    double h, d, c, g;
+};
+
+// Per-level Lagrangian windows: for every point four 4x4
+// patches with unwrapped integer origins: Lu, Lv (left = R...R W^T) and Ru, Rv
+// (right = W P...P).  On the fine level left == right == the 4-point kernel
+// weights W (elasticity.cpp:16-58).
+struct Win {
+    int4* orgL;   // {Lu.i0, Lu.j0, Lv.i0, Lv.j0}
+    int4* orgR;   // {Ru.i0, Ru.j0, Rv.i0, Rv.j0}
+    double* w;    // [pt][4][16]: Lu, Lv, Ru, Rv patches, entry b*4 + a at (i0+a, j0+b)
+};
+
+// CSR of E-active faces of a level: for each unique face (sorted flat
+// velocity index) the (point, left weight) entries in ascending point order.
+struct FaceList {
+    int nf = 0;          // unique faces
+    int* face = nullptr; // [nf] flat index comp*nn + i + j*n
+    int* off = nullptr;  // [nf+1]
+    int* ent = nullptr;  // entries: pt*32 + comp*16 + e (window slot of Lu/Lv)
+};
+
+// Lagrangian point data.
+struct Pts {
+    int n = 0;
+    int* kprev = nullptr;
+    int* knext = nullptr;
+    double* cE = nullptr;    // dt * kappa_m * h0^2  (E' coefficient, ds^2 cancels)
+    double* kap = nullptr;   // kappa_m
+    double* ids2 = nullptr;  // 1 / ds_m^2
+    double* dsq = nullptr;   // ds_m^2 (spread quadrature, fiber.cpp:93)
+};
+
+__host__ __device__ __forceinline__ int wr(int i, int n) { return i & (n - 1); }
+
+// Enumerate the 56 DOFs of a 4x4 big block at cell origin (bi, bj):
+// u faces (a in 0..4, b in 0..3), v faces (a in 0..3, b in 0..4), p (4x4).
+__device__ __forceinline__ void block_dof(int t, int bi, int bj, int& field, int& i, int& j) {
+    if (t < 20) {
+        field = 0;
+        i = bi + t % 5;
+        j = bj + t / 5;
+    } else if (t < 40) {
+        t -= 20;
+        field = 1;
+        i = bi + t % 4;
+        j = bj + t / 4;
+    } else {
+        t -= 40;
+        field = 2;
+        i = bi + t % 4;
+        j = bj + t / 4;
+    }
+}
+
+// Local index inside a block of a (field, i, j) DOF with unwrapped-relative
+// coordinates (a, b) = (i - bi, j - bj) taken mod n; -1 if outside.
+__device__ __forceinline__ int block_local(int field, int a, int b) {
+    if (field == 0) return (a >= 0 && a <= 4 && b >= 0 && b <= 3) ? a + 5 * b : -1;
+    if (field == 1) return (a >= 0 && a <= 3 && b >= 0 && b <= 4) ? 20 + a + 4 * b : -1;
+    return (a >= 0 && a <= 3 && b >= 0 && b <= 3) ? 40 + a + 4 * b : -1;
+}
+
+// Window value of patch slot s (0 Lu, 1 Lv, 2 Ru, 3 Rv) of point k at the
+// wrapped face (i, j), 0 if outside the 4x4 support.
+__device__ __forceinline__ double win_at(const Win& W, int k, int s, int n, int i, int j) {
+    const int4 o = (s < 2) ? W.orgL[k] : W.orgR[k];
+    const int i0 = (s & 1) ? o.z : o.x;
+    const int j0 = (s & 1) ? o.w : o.y;
+    const int a = wr(i - i0, n), b = wr(j - j0, n);
+    if (a >= 4 || b >= 4) return 0.0;
+    return W.w[(size_t)k * 64 + s * 16 + b * 4 + a];
+}
+
+// U_k = R_k . w for component comp (0 u, 1 v) against a field accessor.
+template <class Acc>
+__device__ __forceinline__ double win_dot_R(const Win& W, int k, int comp, int n, const Acc& acc) {
+    const int4 o = W.orgR[k];
+    const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+    const double* p = W.w + (size_t)k * 64 + (2 + comp) * 16;
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) s += p[b * 4 + a] * acc(comp, wr(i0 + a, n), wr(j0 + b, n));
+    return s;
+}
+
+// F_k = cE_k (U_{k-1} - 2 U_k + U_{k+1}) for one component (elasticity.cpp:62-84
+// coefficients {1, -2, 1}/ds^2 times ds^2 h^2 dt kappa).
+template <class Acc>
+__device__ __forceinline__ double point_force(const Win& W, const Pts& P, int k, int comp, int n,
+                                              const Acc& acc) {
+    const double um = win_dot_R(W, P.kprev[k], comp, n, acc);
+    const double uc = win_dot_R(W, k, comp, n, acc);
+    const double up = win_dot_R(W, P.knext[k], comp, n, acc);
+    return P.cE[k] * (um - 2.0 * uc + up);
+}
+
+// Global-memory field accessor: comp 0 u, 1 v, 2 p.
+struct GAcc {
+    const double* w;
+    int n, nn;
+    __device__ __forceinline__ double operator()(int comp, int i, int j) const {
+        return __ldg(w + (size_t)comp * nn + i + (size_t)j * n);
+    }
+};
+
+}  // namespace ibmg

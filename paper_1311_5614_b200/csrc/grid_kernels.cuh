@@ -1,0 +1,234 @@
+// grid_kernels.cuh — periodic MAC stencils (operator apply, residual+restrict,
+// prolong+add) and the Krylov vector kernels (deterministic reductions).
+#pragma once
+#include "common.cuh"
+
+namespace ibmg {
+
+// Stokes rows of cell (i, j) against an accessor: returns the u(i,j), v(i,j)
+// and p(i,j) rows of S w (negated laplacian_hom + gradient_hom + divergence_hom,
+// stokes_ops.cpp:78-130, plus rho/dt; periodic wrap replaces the wall branches).
+template <class Acc>
+__device__ __forceinline__ void stokes_rows(const Lev& L, const Acc& w, int i, int j, double& ru, double& rv,
+                                            double& rp) {
+    const int n = L.n;
+    const int im = wr(i - 1, n), ip = wr(i + 1, n), jm = wr(j - 1, n), jp = wr(j + 1, n);
+    const double uc = w(0, i, j), vc = w(1, i, j), pc = w(2, i, j);
+    ru = L.d * uc - L.c * (w(0, im, j) + w(0, ip, j) + w(0, i, jm) + w(0, i, jp)) + L.g * (pc - w(2, im, j));
+    rv = L.d * vc - L.c * (w(1, i, jm) + w(1, i, jp) + w(1, im, j) + w(1, ip, j)) + L.g * (pc - w(2, i, jm));
+    rp = -L.g * (w(0, ip, j) - uc) - L.g * (w(1, i, jp) - vc);
+}
+
+// out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
+__global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= L.nn) return;
+    const int i = q & (L.n - 1), j = q >> L.lg;
+    GAcc acc{w, L.n, L.nn};
+    double ru, rv, rp;
+    stokes_rows(L, acc, i, j, ru, rv, rp);
+    out[q] = ru;
+    out[L.nn + q] = rv;
+    out[2 * L.nn + q] = rp;
+}
+
+// r = b - S w (E' part added by k_face_gather with sign +1).
+__global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const double* __restrict__ w,
+                                  double* __restrict__ r) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= L.nn) return;
+    const int i = q & (L.n - 1), j = q >> L.lg;
+    GAcc acc{w, L.n, L.nn};
+    double ru, rv, rp;
+    stokes_rows(L, acc, i, j, ru, rv, rp);
+    r[q] = b[q] - ru;
+    r[L.nn + q] = b[L.nn + q] - rv;
+    r[2 * L.nn + q] = b[2 * L.nn + q] - rp;
+}
+
+// Fused residual + restriction (K2): coarse b = R (b - S w) per coarse cell
+// (restrict_saddle, transfers.cpp:107-134; periodic).  The E' part of the
+// restricted residual, R E' w = sum_k L^{l+1}_k F_k, is added afterwards by
+// k_face_gather on the coarse face list.
+__global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
+                                    double* __restrict__ bc) {
+    const int nc = F.n >> 1, nnc = nc * nc;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nnc) return;
+    const int I = q % nc, J = q / nc;
+    const int i = 2 * I, j = 2 * J, n = F.n, nn = F.nn;
+    GAcc acc{w, n, nn};
+    auto ru_at = [&](int a, int bb) {
+        a = wr(a, n);
+        bb = wr(bb, n);
+        double ru, rv, rp;
+        stokes_rows(F, acc, a, bb, ru, rv, rp);
+        return b[a + bb * n] - ru;
+    };
+    auto rv_at = [&](int a, int bb) {
+        a = wr(a, n);
+        bb = wr(bb, n);
+        double ru, rv, rp;
+        stokes_rows(F, acc, a, bb, ru, rv, rp);
+        return b[nn + a + bb * n] - rv;
+    };
+    auto rp_at = [&](int a, int bb) {
+        a = wr(a, n);
+        bb = wr(bb, n);
+        double ru, rv, rp;
+        stokes_rows(F, acc, a, bb, ru, rv, rp);
+        return b[2 * nn + a + bb * n] - rp;
+    };
+    bc[q] = 0.125 * (ru_at(i - 1, j) + 2.0 * ru_at(i, j) + ru_at(i + 1, j) + ru_at(i - 1, j + 1) +
+                     2.0 * ru_at(i, j + 1) + ru_at(i + 1, j + 1));
+    bc[nnc + q] = 0.125 * (rv_at(i, j - 1) + 2.0 * rv_at(i, j) + rv_at(i, j + 1) + rv_at(i + 1, j - 1) +
+                           2.0 * rv_at(i + 1, j) + rv_at(i + 1, j + 1));
+    bc[2 * nnc + q] = 0.25 * (rp_at(i, j) + rp_at(i + 1, j) + rp_at(i, j + 1) + rp_at(i + 1, j + 1));
+}
+
+// Plain restriction of a vector (ibmg_restrict).
+__global__ void k_restrict(int nf, const double* __restrict__ rf, double* __restrict__ rc) {
+    const int nc = nf >> 1, nnc = nc * nc, nnf = nf * nf;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nnc) return;
+    const int I = q % nc, J = q / nc, i = 2 * I, j = 2 * J;
+    auto U = [&](int a, int bb) { return rf[wr(a, nf) + wr(bb, nf) * nf]; };
+    auto V = [&](int a, int bb) { return rf[nnf + wr(a, nf) + wr(bb, nf) * nf]; };
+    auto P = [&](int a, int bb) { return rf[2 * nnf + wr(a, nf) + wr(bb, nf) * nf]; };
+    rc[q] = 0.125 * (U(i - 1, j) + 2.0 * U(i, j) + U(i + 1, j) + U(i - 1, j + 1) + 2.0 * U(i, j + 1) + U(i + 1, j + 1));
+    rc[nnc + q] = 0.125 * (V(i, j - 1) + 2.0 * V(i, j) + V(i, j + 1) + V(i + 1, j - 1) + 2.0 * V(i + 1, j) + V(i + 1, j + 1));
+    rc[2 * nnc + q] = 0.25 * (P(i, j) + P(i + 1, j) + P(i, j + 1) + P(i + 1, j + 1));
+}
+
+// Prolongation + add (K3): bilinear u/v (transfers.cpp:141-205 with the correct
+// v weight ys[b].w, not line 202's xs[a].w), constant p.
+template <class Acc>
+__device__ __forceinline__ void prolong_rows(int nf, const Acc& ec, int i, int j, double& du, double& dv,
+                                             double& dp) {
+    const int nc = nf >> 1;
+    // u: x face direction, y cell direction
+    {
+        int I[2], J[2];
+        double wi[2], wj[2];
+        int ni;
+        if ((i & 1) == 0) { I[0] = i >> 1; wi[0] = 1.0; ni = 1; }
+        else { I[0] = (i - 1) >> 1; wi[0] = 0.5; I[1] = (i + 1) >> 1; wi[1] = 0.5; ni = 2; }
+        J[0] = j >> 1; wj[0] = 0.75; J[1] = (j & 1) ? (j >> 1) + 1 : (j >> 1) - 1; wj[1] = 0.25;
+        double acc = 0.0;
+        for (int a = 0; a < ni; ++a)
+            for (int b = 0; b < 2; ++b) acc += wi[a] * wj[b] * ec(0, wr(I[a], nc), wr(J[b], nc));
+        du = acc;
+    }
+    {
+        int I[2], J[2];
+        double wi[2], wj[2];
+        int nj;
+        if ((j & 1) == 0) { J[0] = j >> 1; wj[0] = 1.0; nj = 1; }
+        else { J[0] = (j - 1) >> 1; wj[0] = 0.5; J[1] = (j + 1) >> 1; wj[1] = 0.5; nj = 2; }
+        I[0] = i >> 1; wi[0] = 0.75; I[1] = (i & 1) ? (i >> 1) + 1 : (i >> 1) - 1; wi[1] = 0.25;
+        double acc = 0.0;
+        for (int b = 0; b < nj; ++b)
+            for (int a = 0; a < 2; ++a) acc += wj[b] * wi[a] * ec(1, wr(I[a], nc), wr(J[b], nc));
+        dv = acc;
+    }
+    dp = ec(2, i >> 1, j >> 1);
+}
+
+__global__ void k_prolong_add(int nf, const double* __restrict__ ec, double* __restrict__ wf) {
+    const int nnf = nf * nf;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nnf) return;
+    const int i = q % nf, j = q / nf;
+    GAcc acc{ec, nf >> 1, (nf >> 1) * (nf >> 1)};
+    double du, dv, dp;
+    prolong_rows(nf, acc, i, j, du, dv, dp);
+    wf[q] += du;
+    wf[nnf + q] += dv;
+    wf[2 * nnf + q] += dp;
+}
+
+// ---------------- Krylov vector kernels ----------------
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs; fixed => reduction order fixed
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// partial[y * kRedBlocks + x] = sum over block x's strided range of V_y . w
+// (y = blockIdx.y indexes the vector; V vectors are `stride` doubles apart).
+__global__ void k_multidot_partial(const double* __restrict__ V, size_t stride, const double* __restrict__ w,
+                                   size_t m, double* __restrict__ partial) {
+    const double* v = V + stride * blockIdx.y;
+    double s = 0.0;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
+        s += v[q] * w[q];
+    __shared__ double red[kRedThreads / 32];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = threadIdx.x < kRedThreads / 32 ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// out[y] (+)= sum_x partial[y][x]; mode 0: store, 1: accumulate (CGS2 second pass).
+__global__ void k_finish_dots(const double* __restrict__ partial, int nblk, double* __restrict__ out, int accumulate) {
+    double s = 0.0;
+    for (int x = threadIdx.x; x < nblk; x += 32) s += partial[blockIdx.x * nblk + x];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) out[blockIdx.x] = accumulate ? out[blockIdx.x] + s : s;
+}
+
+// w -= sum_{i<k} h[i] V_i   (one pass over w and the V's).
+__global__ void k_multi_axpy_sub(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
+                                 double* __restrict__ w, size_t m) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
+        double s = w[q];
+        for (int i = 0; i < k; ++i) s -= h[i] * V[stride * i + q];
+        w[q] = s;
+    }
+}
+
+// x += sum_{i<k} y[i] Z_i
+__global__ void k_multi_axpy_add(const double* __restrict__ Z, size_t stride, int k, const double* __restrict__ y,
+                                 double* __restrict__ x, size_t m) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
+        double s = x[q];
+        for (int i = 0; i < k; ++i) s += y[i] * Z[stride * i + q];
+        x[q] = s;
+    }
+}
+
+// dst = src * (1 / sqrt(*nrm2))  or  src / scalar when nrm2 == nullptr
+__global__ void k_scale_by_norm(const double* __restrict__ src, double* __restrict__ dst, size_t m,
+                                const double* __restrict__ nrm2, double scalar) {
+    const double s = nrm2 ? sqrt(*nrm2) : scalar;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
+        dst[q] = src[q] / s;
+}
+
+// p -= mean(p)  (project_pressure_mean, fields.cpp:78-85); sum precomputed in *sum.
+__global__ void k_sub_mean(double* __restrict__ p, size_t nn, const double* __restrict__ sum) {
+    const double mean = *sum / (double)nn;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < nn; q += (size_t)gridDim.x * blockDim.x)
+        p[q] -= mean;
+}
+
+// b = [(rho/dt) u ; 0]
+__global__ void k_rhs_mass(const double* __restrict__ u, double* __restrict__ b, size_t nn, double rho_dt) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < 3 * nn; q += (size_t)gridDim.x * blockDim.x)
+        b[q] = q < 2 * nn ? rho_dt * u[q] : 0.0;
+}
+
+// r = b - r  (residual from an applied operator)
+__global__ void k_b_minus(const double* __restrict__ b, double* __restrict__ r, size_t m) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
+        r[q] = b[q] - r[q];
+}
+
+}  // namespace ibmg

@@ -1,0 +1,270 @@
+// ib_kernels.cuh — Lagrangian-structure kernels: 4-point kernel windows on every
+// level, E-active face lists, point forces, deterministic spread (gather over
+// face lists: no float atomics), interpolation and the X update.
+#pragma once
+#include "common.cuh"
+
+namespace ibmg {
+
+constexpr double kPi = 3.14159265358979323846;
+
+// delta_1d (fiber.cpp:12-16): (1 + cos(pi r / 2h)) / 4h for |r| < 2h.
+__device__ __forceinline__ double delta_1d(double r, double h) {
+    const double a = fabs(r);
+    if (a >= 2.0 * h) return 0.0;
+    return (1.0 + cos(kPi * r / (2.0 * h))) / (4.0 * h);
+}
+// kernel_line_faces / kernel_line_centers (fiber.cpp:58-87), periodic (no clip).
+__device__ __forceinline__ int line_faces(double X, double h, double* w) {
+    const int first = (int)ceil(X / h - 2.0);
+    for (int a = 0; a < 4; ++a) w[a] = delta_1d((double)(first + a) * h - X, h);
+    return first;
+}
+__device__ __forceinline__ int line_centers(double X, double h, double* w) {
+    const int first = (int)ceil((X / h - 0.5) - 2.0);
+    for (int a = 0; a < 4; ++a) w[a] = delta_1d(((double)(first + a) + 0.5) * h - X, h);
+    return first;
+}
+
+struct WinLevels {
+    Win win[20];
+    int n[20];
+    int nlev;
+};
+
+__device__ __forceinline__ void patch_add(double* dst, int a, int b, double v, int* err) {
+    if (a < 0 || a >= 4 || b < 0 || b >= 4) {
+        atomicOr(err, 1);
+        return;
+    }
+    dst[b * 4 + a] += v;
+}
+
+// Face-direction restriction weights {1/8, 1/4, 1/8} (transfers.cpp:117-127):
+// fine face index f feeds coarse F = f/2 (1/4) when even, (f-1)/2 and (f+1)/2 (1/8) when odd.
+// Cell-direction restriction: coarse C = c>>1 with weight 1.
+// Face-direction prolongation: coarse f/2 (1) or (f-1)/2,(f+1)/2 (1/2).
+// Cell-direction prolongation: C = c>>1 (3/4) and C-1 (c even) / C+1 (c odd) (1/4).
+__device__ __forceinline__ int face_restrict(int f, int* I, double* w) {
+    if ((f & 1) == 0) { I[0] = f >> 1; w[0] = 0.25; return 1; }
+    I[0] = (f - 1) >> 1; w[0] = 0.125; I[1] = (f + 1) >> 1; w[1] = 0.125; return 2;
+}
+__device__ __forceinline__ int face_prolong(int f, int* I, double* w) {
+    if ((f & 1) == 0) { I[0] = f >> 1; w[0] = 1.0; return 1; }
+    I[0] = (f - 1) >> 1; w[0] = 0.5; I[1] = (f + 1) >> 1; w[1] = 0.5; return 2;
+}
+__device__ __forceinline__ int cell_prolong(int c, int* J, double* w) {
+    J[0] = c >> 1; w[0] = 0.75; J[1] = (c & 1) ? (c >> 1) + 1 : (c >> 1) - 1; w[1] = 0.25; return 2;
+}
+
+// Windows of every point on every level, one thread per point.  Level l+1's
+// left window is R applied to level l's (R*...*R*W^T), the right window is
+// level l's times P (W*P*...*P) — the factored form of the reference's
+// recursive Galerkin R*E*P (transfers.cpp:286-293, PAPER Eq. 20).
+__global__ void k_windows(int npts, const double* __restrict__ X, WinLevels WL, double h0, int* err) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    const double x = X[2 * k], y = X[2 * k + 1];
+    double wx[4], wy[4];
+    {
+        Win& W = WL.win[0];
+        double* p = W.w + (size_t)k * 64;
+        int fx = line_faces(x, h0, wx), fy = line_centers(y, h0, wy);
+        for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a) p[b * 4 + a] = p[32 + b * 4 + a] = wx[a] * wy[b];
+        int4 o;
+        o.x = fx;
+        o.y = fy;
+        fx = line_centers(x, h0, wx);
+        fy = line_faces(y, h0, wy);
+        for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a) p[16 + b * 4 + a] = p[48 + b * 4 + a] = wx[a] * wy[b];
+        o.z = fx;
+        o.w = fy;
+        W.orgL[k] = o;
+        W.orgR[k] = o;
+    }
+    for (int l = 0; l + 1 < WL.nlev; ++l) {
+        const Win& F = WL.win[l];
+        Win& C = WL.win[l + 1];
+        const double* src = F.w + (size_t)k * 64;
+        double* dst = C.w + (size_t)k * 64;
+        for (int q = 0; q < 64; ++q) dst[q] = 0.0;
+        const int4 oL = F.orgL[k], oR = F.orgR[k];
+        int4 nL, nR;
+        // left u: x face-restrict, y cell-restrict; origin (floor(i0/2), floor(j0/2))
+        nL.x = oL.x >> 1; nL.y = oL.y >> 1;
+        // left v: x cell-restrict, y face-restrict
+        nL.z = oL.z >> 1; nL.w = oL.w >> 1;
+        // right u: x face-prolong, y cell-prolong; origin (floor(i0/2), floor((j0-1)/2))
+        nR.x = oR.x >> 1; nR.y = (oR.y - 1) >> 1;
+        // right v: x cell-prolong, y face-prolong
+        nR.z = (oR.z - 1) >> 1; nR.w = oR.w >> 1;
+        int I[2], J[2];
+        double wi[2], wj[2];
+        for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a) {
+                double v = src[b * 4 + a];  // Lu
+                if (v != 0.0) {
+                    const int ni = face_restrict(oL.x + a, I, wi);
+                    const int J0 = (oL.y + b) >> 1;
+                    for (int p = 0; p < ni; ++p) patch_add(dst, I[p] - nL.x, J0 - nL.y, v * wi[p], err);
+                }
+                v = src[16 + b * 4 + a];  // Lv
+                if (v != 0.0) {
+                    const int nj = face_restrict(oL.w + b, J, wj);
+                    const int I0 = (oL.z + a) >> 1;
+                    for (int q = 0; q < nj; ++q) patch_add(dst + 16, I0 - nL.z, J[q] - nL.w, v * wj[q], err);
+                }
+                v = src[32 + b * 4 + a];  // Ru
+                if (v != 0.0) {
+                    const int ni = face_prolong(oR.x + a, I, wi);
+                    const int nj = cell_prolong(oR.y + b, J, wj);
+                    for (int p = 0; p < ni; ++p)
+                        for (int q = 0; q < nj; ++q)
+                            patch_add(dst + 32, I[p] - nR.x, J[q] - nR.y, v * (wi[p] * wj[q]), err);
+                }
+                v = src[48 + b * 4 + a];  // Rv
+                if (v != 0.0) {
+                    const int nj = face_prolong(oR.w + b, J, wj);
+                    const int ni = cell_prolong(oR.z + a, I, wi);
+                    for (int q = 0; q < nj; ++q)
+                        for (int p = 0; p < ni; ++p)
+                            patch_add(dst + 48, I[p] - nR.z, J[q] - nR.w, v * (wj[q] * wi[p]), err);
+                }
+            }
+        C.orgL[k] = nL;
+        C.orgR[k] = nR;
+    }
+}
+
+// Keys for the face lists of one level: one (face, entry) pair per nonzero
+// left-window weight; sentinel key INT_MAX for zeros.
+__global__ void k_face_keys(int npts, Win W, int n, int* keys, int* vals) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= npts * 32) return;
+    const int k = q >> 5, s = (q >> 4) & 1, e = q & 15;
+    const double v = W.w[(size_t)k * 64 + s * 16 + e];
+    const int4 o = W.orgL[k];
+    const int i0 = s ? o.z : o.x, j0 = s ? o.w : o.y;
+    const int i = wr(i0 + (e & 3), n), j = wr(j0 + (e >> 2), n);
+    keys[q] = (v != 0.0) ? s * n * n + i + j * n : 0x7fffffff;
+    vals[q] = q;
+}
+
+// Big-block marking: a 4x4 block is big when any face of it
+// lies in the support of any point's left or right window on the level.
+__global__ void k_mark_big(int npts, Win W, int n, uint8_t* flags) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= npts * 64) return;
+    const int k = q >> 6, s = (q >> 4) & 3, e = q & 15;
+    if (W.w[(size_t)k * 64 + s * 16 + e] == 0.0) return;
+    const int4 o = (s < 2) ? W.orgL[k] : W.orgR[k];
+    const int comp = s & 1;
+    const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+    const int i = wr(i0 + (e & 3), n), j = wr(j0 + (e >> 2), n);
+    const int nbk = n >> 2;
+    flags[(i >> 2) + (j >> 2) * nbk] = 1;
+    if (comp == 0) {
+        const int i2 = wr(i - 1, n);
+        flags[(i2 >> 2) + (j >> 2) * nbk] = 1;
+    } else {
+        const int j2 = wr(j - 1, n);
+        flags[(i >> 2) + (j2 >> 2) * nbk] = 1;
+    }
+}
+
+// Reach of E' on a level: the extent (in face index units) of the union of
+// L_k and R_{k-1}, R_k, R_{k+1} supports, max over points and components.
+// Same-colour big blocks are 12 cells apart, so the schedule requires <= 12.
+__global__ void k_reach(int npts, Win W, Pts P, int* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    int ext = 0;
+    for (int comp = 0; comp < 2; ++comp) {
+        int lo_i = 1 << 30, hi_i = -(1 << 30), lo_j = 1 << 30, hi_j = -(1 << 30);
+        const int ks[4] = {k, P.kprev[k], k, P.knext[k]};
+        for (int t = 0; t < 4; ++t) {
+            const int s = (t == 0 ? 0 : 2) + comp;
+            const int kk = ks[t];
+            const int4 o = (s < 2) ? W.orgL[kk] : W.orgR[kk];
+            const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+            for (int e = 0; e < 16; ++e) {
+                if (W.w[(size_t)kk * 64 + s * 16 + e] == 0.0) continue;
+                const int i = i0 + (e & 3), j = j0 + (e >> 2);
+                lo_i = min(lo_i, i); hi_i = max(hi_i, i);
+                lo_j = min(lo_j, j); hi_j = max(hi_j, j);
+            }
+        }
+        if (hi_i >= lo_i) ext = max(ext, max(hi_i - lo_i, hi_j - lo_j));
+    }
+    atomicMax(out, ext);
+}
+
+// F_k for both components from field w on a level (thread per point).
+__global__ void k_point_force(Win W, Pts P, int n, const double* __restrict__ w, double* __restrict__ F) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= P.n) return;
+    GAcc acc{w, n, n * n};
+    F[2 * k] = point_force(W, P, k, 0, n, acc);
+    F[2 * k + 1] = point_force(W, P, k, 1, n, acc);
+}
+
+// out[face] += sign * sum_{(k, l) in list(face)} l * F[k][comp]   (deterministic
+// spread: entries in ascending point order, no atomics).
+__global__ void k_face_gather(FaceList FL, Win W, const double* __restrict__ F, double* __restrict__ out,
+                              int nn, double sign) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= FL.nf) return;
+    const int face = FL.face[q];
+    const int comp = face >= nn;
+    double s = 0.0;
+    for (int e = FL.off[q]; e < FL.off[q + 1]; ++e) {
+        const int v = FL.ent[e];
+        const int k = v >> 5;
+        s += W.w[(size_t)k * 64 + (v & 31)] * F[2 * k + comp];
+    }
+    out[face] += sign * s;
+}
+
+// Fiber force density of the RHS times the spread quadrature:
+// F_k ds^2 = kappa (X_{k-1} + X_{k+1} - 2 X_k)/ds^2 * ds^2  (fiber.cpp:34-55, 93).
+__global__ void k_rhs_force(Pts P, const double* __restrict__ X, double* __restrict__ F) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= P.n) return;
+    const int km = P.kprev[k], kp = P.knext[k];
+    for (int c = 0; c < 2; ++c) {
+        const double d = X[2 * km + c] + X[2 * kp + c] - X[2 * k + c] * 2.0;
+        F[2 * k + c] = ((d * P.ids2[k]) * P.kap[k]) * P.dsq[k];
+    }
+}
+
+// Plain spread input scaling: F_k ds_m^2 (ds^2 quadrature, fiber.cpp:93).
+__global__ void k_scale_dsq(Pts P, const double* __restrict__ Fin, double* __restrict__ F) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= P.n) return;
+    F[2 * k] = Fin[2 * k] * P.dsq[k];
+    F[2 * k + 1] = Fin[2 * k + 1] * P.dsq[k];
+}
+
+// interpolate (fiber.cpp:116-140): U_k = h^2 sum W u; optionally X += dt U.
+__global__ void k_interp(Win W, int npts, int n, double h, const double* __restrict__ u, double* __restrict__ U,
+                         double* __restrict__ X, double dt) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    GAcc acc{u, n, n * n};
+    const double w0 = h * h;
+    // fine level: left == right windows; use the right-window dot
+    const double Uu = win_dot_R(W, k, 0, n, acc) * w0;
+    const double Vv = win_dot_R(W, k, 1, n, acc) * w0;
+    if (U) {
+        U[2 * k] = Uu;
+        U[2 * k + 1] = Vv;
+    }
+    if (X) {
+        X[2 * k] += dt * Uu;
+        X[2 * k + 1] += dt * Vv;
+    }
+}
+
+}  // namespace ibmg

@@ -1,0 +1,967 @@
+// ibmg.cu — host driver of the B200-native implicit-IB MG-FGMRES solver and the
+// C ABI declared in include/ibmg_gpu.h.
+//
+// Host C++ owns the context (device memory, stream, per-level data) and issues
+// the sm_100a kernels of *_kernels.cuh; there is no CPU fallback: every
+// numerical operation of the hot path is a kernel on the context's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/ibmg_gpu.h"
+#include "coarse_kernel.cuh"
+#include "common.cuh"
+#include "grid_kernels.cuh"
+#include "ib_kernels.cuh"
+#include "smoother_kernels.cuh"
+
+using namespace ibmg;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct InvalidArg : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + std::to_string(__LINE__)); \
+    } while (0)
+
+template <class T>
+T* dalloc(size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+inline unsigned nblk(size_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+struct LevelBuf {
+    Lev L{};
+    double *w = nullptr, *b = nullptr, *r = nullptr;
+    Win W{};
+    FaceList FL{};
+    int fl_cap = 0;
+    uint8_t* big = nullptr;
+    int nbig = 0;
+    int* blk_ids = nullptr;  // big blocks sorted by colour, ascending id within
+    int blk_cap = 0;
+    int coff[17] = {0};
+    int* fidx = nullptr;
+    double* Ainv = nullptr;
+    int ainv_cap = 0;
+};
+
+}  // namespace
+
+struct ibmg_ctx {
+    ibmg_params prm{};
+    std::string err;
+    cudaStream_t s = nullptr;
+    int nlev = 0, lc = 0;  // levels [lc, nlev) run in the single-CTA coarse kernel
+    std::vector<LevelBuf> lev;
+    long long launches = 0;
+    // structures
+    int npts = 0, nmem = 0;
+    std::vector<int> nb;
+    Pts P{};
+    double* X = nullptr;
+    double* F = nullptr;       // point forces (2 npts)
+    double* Fc = nullptr;      // coarse-kernel scratch (2 npts)
+    double* Acoarse = nullptr;
+    int* err_flag = nullptr;
+    // setup scratch
+    int *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *vals2 = nullptr, *runs = nullptr, *cnt = nullptr;
+    size_t sort_cap = 0;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    int* counters = nullptr;   // per level: [17 colour counts][num_runs][reach]
+    // Krylov
+    double *V = nullptr, *Z = nullptr, *wv = nullptr, *xv = nullptr, *rv = nullptr, *bv = nullptr;
+    double *partial = nullptr, *dh = nullptr, *ones = nullptr, *stage_a = nullptr, *stage_b = nullptr;
+    double* hpin = nullptr;    // pinned host mirror of dh
+    size_t M = 0;              // 3 N^2
+    bool have_structs = false;
+};
+
+namespace {
+
+#define LAUNCH(ctx, kern, grid, block, smem, ...)                          \
+    do {                                                                   \
+        kern<<<(grid), (block), (smem), (ctx)->s>>>(__VA_ARGS__);          \
+        ++(ctx)->launches;                                                 \
+        CK(cudaGetLastError());                                            \
+    } while (0)
+
+Lev make_lev(const ibmg_params& p, int n) {
+    Lev L;
+    L.n = n;
+    L.nn = n * n;
+    L.lg = 0;
+    while ((1 << L.lg) < n) ++L.lg;
+    L.h = 1.0 / n;
+    L.c = p.mu / (L.h * L.h);
+    L.d = p.rho / p.dt + 4.0 * L.c;
+    L.g = 1.0 / L.h;
+    return L;
+}
+
+void ensure_cub(ibmg_ctx* c, size_t bytes) {
+    if (bytes > c->cub_bytes) {
+        if (c->cub_tmp) cudaFree(c->cub_tmp);
+        CK(cudaMalloc(&c->cub_tmp, bytes));
+        c->cub_bytes = bytes;
+    }
+}
+
+void alloc_levels(ibmg_ctx* c) {
+    const ibmg_params& p = c->prm;
+    for (int n = p.N;; n /= 2) {
+        LevelBuf lb;
+        lb.L = make_lev(p, n);
+        const size_t m = 3 * size_t(n) * n;
+        lb.w = dalloc<double>(m);
+        lb.b = dalloc<double>(m);
+        lb.r = dalloc<double>(m);
+        if (n > p.coarsest_n) lb.big = dalloc<uint8_t>(size_t(n / 4) * (n / 4));
+        c->lev.push_back(lb);
+        if (n <= p.coarsest_n) break;
+    }
+    c->nlev = int(c->lev.size());
+    c->lc = 0;
+    while (c->lev[c->lc].L.n > kCoarseMaxN) ++c->lc;
+    if (c->nlev - c->lc > 6) throw InvalidArg("too many coarse-kernel levels");
+    c->M = 3 * size_t(p.N) * p.N;
+    const int m = p.restart;
+    c->V = dalloc<double>(c->M * (m + 1));
+    c->Z = dalloc<double>(c->M * m);
+    c->wv = dalloc<double>(c->M);
+    c->xv = dalloc<double>(c->M);
+    c->rv = dalloc<double>(c->M);
+    c->bv = dalloc<double>(c->M);
+    c->stage_a = dalloc<double>(c->M);
+    c->stage_b = dalloc<double>(c->M);
+    c->partial = dalloc<double>(size_t(kRedBlocks) * (m + 2));
+    c->dh = dalloc<double>(2 * (m + 2) + 8);
+    CK(cudaMallocHost(&c->hpin, sizeof(double) * (2 * (m + 2) + 8)));
+    c->ones = dalloc<double>(size_t(p.N) * p.N);
+    {
+        std::vector<double> one(size_t(p.N) * p.N, 1.0);
+        CK(cudaMemcpy(c->ones, one.data(), one.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    c->err_flag = dalloc<int>(1);
+    c->counters = dalloc<int>(size_t(c->nlev) * 20);
+    const int nc = c->lev.back().L.nn;
+    c->Acoarse = dalloc<double>(size_t(3 * nc + 1) * (3 * nc + 1));
+}
+
+void free_structs(ibmg_ctx* c) {
+    for (auto& lb : c->lev) {
+        dfree(lb.W.orgL);
+        dfree(lb.W.orgR);
+        dfree(lb.W.w);
+        dfree(lb.FL.face);
+        dfree(lb.FL.off);
+        dfree(lb.FL.ent);
+        lb.FL.nf = 0;
+        lb.fl_cap = 0;
+        dfree(lb.blk_ids);
+        dfree(lb.fidx);
+        dfree(lb.Ainv);
+        lb.blk_cap = lb.ainv_cap = 0;
+        lb.nbig = 0;
+    }
+    dfree(c->P.kprev);
+    dfree(c->P.knext);
+    dfree(c->P.cE);
+    dfree(c->P.kap);
+    dfree(c->P.ids2);
+    dfree(c->P.dsq);
+    dfree(c->X);
+    dfree(c->F);
+    dfree(c->Fc);
+    dfree(c->keys);
+    dfree(c->vals);
+    dfree(c->keys2);
+    dfree(c->vals2);
+    dfree(c->runs);
+    dfree(c->cnt);
+    c->sort_cap = 0;
+    c->npts = 0;
+}
+
+void check_err_flag(ibmg_ctx* c, const char* where) {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, c->err_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    if (h & 1) throw InvalidArg(std::string(where) + ": window patch overflow (structure too coarse for 4x4 windows)");
+    if (h & 2) throw CudaError(std::string(where) + ": singular local box matrix");
+}
+
+// Rebuild every per-level structure datum from the device positions c->X
+// (the lagged operators of one step).
+void rebuild(ibmg_ctx* c) {
+    const int npts = c->npts;
+    CK(cudaMemsetAsync(c->err_flag, 0, sizeof(int), c->s));
+    CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * 20, c->s));
+    if (npts == 0) {
+        for (auto& lb : c->lev) {
+            lb.FL.nf = 0;
+            lb.nbig = 0;
+            std::fill(lb.coff, lb.coff + 17, 0);
+            if (lb.big) CK(cudaMemsetAsync(lb.big, 0, size_t(lb.L.n / 4) * (lb.L.n / 4), c->s));
+        }
+    } else {
+        WinLevels WL{};
+        WL.nlev = c->nlev;
+        for (int l = 0; l < c->nlev; ++l) {
+            WL.win[l] = c->lev[l].W;
+            WL.n[l] = c->lev[l].L.n;
+        }
+        LAUNCH(c, k_windows, nblk(npts, 128), 128, 0, npts, c->X, WL, c->lev[0].L.h, c->err_flag);
+        // face lists: sort (face, entry) keys per level, run-length encode
+        const int items = npts * 32;
+        for (int l = 0; l < c->nlev; ++l) {
+            LevelBuf& lb = c->lev[l];
+            LAUNCH(c, k_face_keys, nblk(items), 256, 0, npts, lb.W, lb.L.n, c->keys, c->vals);
+            size_t bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys, c->keys2, c->vals, lb.FL.ent, items, 0, 31, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys, c->keys2, c->vals, lb.FL.ent, items, 0, 31,
+                                               c->s));
+            bytes = 0;
+            cub::DeviceRunLengthEncode::Encode(nullptr, bytes, c->keys2, lb.FL.face, c->cnt, c->counters + l * 20 + 17,
+                                               items, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceRunLengthEncode::Encode(c->cub_tmp, bytes, c->keys2, lb.FL.face, c->cnt,
+                                                  c->counters + l * 20 + 17, items, c->s));
+            bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, lb.FL.off, items + 1, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, lb.FL.off, items + 1, c->s));
+            // c->cnt must be zero past the runs for the scan's tail; entries past nf are ignored anyway
+            ++c->launches;  // account the CUB launches coarsely (sort+rle+scan)
+        }
+        // big-block marking, colour sort, reach
+        for (int l = 0; l + 1 < c->nlev; ++l) {
+            LevelBuf& lb = c->lev[l];
+            const int nbk = lb.L.n / 4;
+            CK(cudaMemsetAsync(lb.big, 0, size_t(nbk) * nbk, c->s));
+            LAUNCH(c, k_mark_big, nblk(size_t(npts) * 64), 256, 0, npts, lb.W, lb.L.n, lb.big);
+            LAUNCH(c, k_reach, nblk(npts, 128), 128, 0, npts, lb.W, c->P, c->counters + l * 20 + 18);
+            LAUNCH(c, k_block_keys, nblk(size_t(nbk) * nbk), 256, 0, nbk, lb.big, c->keys, c->vals,
+                   c->counters + l * 20);
+            size_t bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys, c->keys2, c->vals, c->vals2, nbk * nbk, 0, 5,
+                                            c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys, c->keys2, c->vals, c->vals2, nbk * nbk, 0,
+                                               5, c->s));
+            // keep the sorted block ids of this level in vals2 slice: copy after counts are known
+            if (lb.blk_cap < nbk * nbk) {
+                dfree(lb.blk_ids);
+                lb.blk_ids = dalloc<int>(size_t(nbk) * nbk);
+                lb.blk_cap = nbk * nbk;
+            }
+            CK(cudaMemcpyAsync(lb.blk_ids, c->vals2, sizeof(int) * nbk * nbk, cudaMemcpyDeviceToDevice, c->s));
+        }
+        std::vector<int> hc(size_t(c->nlev) * 20);
+        CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        for (int l = 0; l < c->nlev; ++l) {
+            LevelBuf& lb = c->lev[l];
+            const int* h = &hc[size_t(l) * 20];
+            // runs include the sentinel run (INT_MAX) when any weight was zero
+            int runs = h[17];
+            int last = 0;
+            if (runs > 0) {
+                CK(cudaMemcpy(&last, lb.FL.face + runs - 1, sizeof(int), cudaMemcpyDeviceToHost));
+                if (last == 0x7fffffff) --runs;
+            }
+            lb.FL.nf = runs;
+            if (l + 1 < c->nlev) {
+                const int reach = h[18];
+                if (reach > 12)
+                    throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 12-cell colour separation on level " +
+                                     std::to_string(l) + " (Lagrangian spacing too large)");
+                lb.coff[0] = 0;
+                for (int k = 0; k < 16; ++k) lb.coff[k + 1] = lb.coff[k] + h[k];
+                lb.nbig = lb.coff[16];
+            }
+        }
+        // per-level big-block face indices and inverses
+        for (int l = 0; l + 1 < c->nlev; ++l) {
+            LevelBuf& lb = c->lev[l];
+            if (lb.nbig == 0) continue;
+            if (lb.ainv_cap < lb.nbig) {
+                dfree(lb.Ainv);
+                dfree(lb.fidx);
+                lb.ainv_cap = std::max(lb.nbig, lb.ainv_cap * 5 / 4);
+                lb.Ainv = dalloc<double>(size_t(lb.ainv_cap) * 3136);
+                lb.fidx = dalloc<int>(size_t(lb.ainv_cap) * 40);
+            }
+            LAUNCH(c, k_block_fidx, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.FL, lb.blk_ids, lb.nbig, lb.fidx);
+            LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.W, c->P, lb.FL, lb.blk_ids,
+                   lb.fidx, lb.Ainv, c->err_flag);
+        }
+    }
+    {
+        LevelBuf& lb = c->lev.back();
+        const int m = 3 * lb.L.nn + 1;
+        LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * 2 * m * sizeof(double), lb.L, lb.W, c->P, lb.FL, c->Acoarse,
+               c->err_flag);
+    }
+    check_err_flag(c, "rebuild");
+}
+
+void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, const double* ds, const double* X,
+                    int ptr_kind) {
+    if (n_mem < 0) throw InvalidArg("n_mem must be >= 0");
+    std::vector<int> hnb(nb, nb + n_mem);
+    std::vector<double> hk(kappa, kappa + n_mem), hds(ds, ds + n_mem);
+    int tot = 0;
+    for (int m = 0; m < n_mem; ++m) {
+        if (hnb[m] < 3) throw InvalidArg("FiberMesh: m1 must be >= 3");
+        if (!(hds[m] > 0.0)) throw InvalidArg("FiberMesh: ds must be positive");
+        if (hk[m] < 0.0) throw InvalidArg("kappa must be >= 0");
+        tot += hnb[m];
+    }
+    free_structs(c);
+    c->npts = tot;
+    c->nmem = n_mem;
+    c->nb = hnb;
+    std::vector<int> kp(tot), kn(tot);
+    std::vector<double> cE(tot), kap(tot), ids2(tot), dsq(tot);
+    const double h0 = 1.0 / c->prm.N;
+    for (int m = 0, o = 0; m < n_mem; o += hnb[m], ++m)
+        for (int k = 0; k < hnb[m]; ++k) {
+            kp[o + k] = o + (k == 0 ? hnb[m] - 1 : k - 1);
+            kn[o + k] = o + (k == hnb[m] - 1 ? 0 : k + 1);
+            cE[o + k] = c->prm.dt * hk[m] * h0 * h0;
+            kap[o + k] = hk[m];
+            ids2[o + k] = 1.0 / (hds[m] * hds[m]);
+            dsq[o + k] = hds[m] * hds[m];
+        }
+    c->P.n = tot;
+    c->P.kprev = dalloc<int>(tot);
+    c->P.knext = dalloc<int>(tot);
+    c->P.cE = dalloc<double>(tot);
+    c->P.kap = dalloc<double>(tot);
+    c->P.ids2 = dalloc<double>(tot);
+    c->P.dsq = dalloc<double>(tot);
+    c->X = dalloc<double>(2 * size_t(tot));
+    c->F = dalloc<double>(2 * size_t(tot));
+    c->Fc = dalloc<double>(2 * size_t(tot));
+    CK(cudaMemcpy(c->P.kprev, kp.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->P.knext, kn.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->P.cE, cE.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->P.kap, kap.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->P.ids2, ids2.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->P.dsq, dsq.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->X, X, sizeof(double) * 2 * tot,
+                  ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    for (auto& lb : c->lev) {
+        lb.W.orgL = dalloc<int4>(tot);
+        lb.W.orgR = dalloc<int4>(tot);
+        lb.W.w = dalloc<double>(size_t(tot) * 64);
+        lb.fl_cap = tot * 32;
+        lb.FL.face = dalloc<int>(size_t(lb.fl_cap));
+        lb.FL.off = dalloc<int>(size_t(lb.fl_cap) + 1);
+        lb.FL.ent = dalloc<int>(size_t(lb.fl_cap));
+    }
+    size_t cap = std::max<size_t>(size_t(tot) * 32 + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
+    c->keys = dalloc<int>(cap);
+    c->vals = dalloc<int>(cap);
+    c->keys2 = dalloc<int>(cap);
+    c->vals2 = dalloc<int>(cap);
+    c->cnt = dalloc<int>(cap + 1);
+    CK(cudaMemset(c->cnt, 0, sizeof(int) * (cap + 1)));
+    c->sort_cap = cap;
+    rebuild(c);
+    c->have_structs = true;
+}
+
+// ---------------- operators ----------------
+
+// out = A_l w on level l (stencil + E' via point forces and the level face list).
+void apply_level(ibmg_ctx* c, int l, const double* w, double* out) {
+    LevelBuf& lb = c->lev[l];
+    LAUNCH(c, k_stokes_apply, nblk(lb.L.nn), 256, 0, lb.L, w, out);
+    if (c->npts && lb.FL.nf) {
+        LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, w, c->F);
+        LAUNCH(c, k_face_gather, nblk(lb.FL.nf), 256, 0, lb.FL, lb.W, c->F, out, lb.L.nn, -1.0);
+    }
+}
+
+void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double* r) {
+    LevelBuf& lb = c->lev[l];
+    LAUNCH(c, k_stokes_residual, nblk(lb.L.nn), 256, 0, lb.L, b, w, r);
+    if (c->npts && lb.FL.nf) {
+        LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, w, c->F);
+        LAUNCH(c, k_face_gather, nblk(lb.FL.nf), 256, 0, lb.FL, lb.W, c->F, r, lb.L.nn, 1.0);
+    }
+}
+
+void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
+    LevelBuf& lb = c->lev[l];
+    const int n = lb.L.n;
+    if (n < 2 * kTile) throw InvalidArg("multi-tile sweep needs n >= 32");
+    const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
+    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
+    for (int bc = 0; bc < 16; ++bc) {
+        const int cnt = lb.coff[bc + 1] - lb.coff[bc];
+        if (cnt == 0) continue;
+        LAUNCH(c, k_big_sweep, cnt, 64, 0, lb.L, lb.W, c->P, lb.FL, lb.blk_ids, lb.fidx, lb.Ainv, lb.coff[bc], b, w);
+    }
+}
+
+CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
+    CoarseArgs A{};
+    A.nl = c->nlev - c->lc;
+    A.nu1 = c->prm.nu1;
+    A.nu2 = c->prm.nu2;
+    for (int l = c->lc; l < c->nlev; ++l) {
+        LevelBuf& lb = c->lev[l];
+        CLev& C = A.lv[l - c->lc];
+        C.L = lb.L;
+        C.W = lb.W;
+        C.FL = lb.FL;
+        C.big = lb.big;
+        C.blk_ids = lb.blk_ids;
+        C.fidx = lb.fidx;
+        C.Ainv = lb.Ainv;
+        std::copy(lb.coff, lb.coff + 17, C.coff);
+    }
+    A.P = c->P;
+    A.F = c->Fc;
+    A.Acoarse = c->Acoarse;
+    A.b_in = b_in;
+    A.w_out = w_out;
+    return A;
+}
+
+size_t coarse_smem(ibmg_ctx* c) {
+    size_t d = 0;
+    for (int l = c->lc; l < c->nlev; ++l) d += 6 * size_t(c->lev[l].L.nn);
+    d += 3 * size_t(c->lev[c->lc].L.nn);
+    return d * sizeof(double);
+}
+
+void coarse_cycle(ibmg_ctx* c, const double* b, double* w) {
+    CoarseArgs A = coarse_args(c, b, w);
+    LAUNCH(c, k_coarse_cycle, 1, kCoarseThreads, coarse_smem(c), A);
+}
+
+void pressure_mean_zero(ibmg_ctx* c, double* x) {
+    const size_t nn = size_t(c->prm.N) * c->prm.N;
+    dim3 g(kRedBlocks, 1);
+    LAUNCH(c, k_multidot_partial, g, kRedThreads, 0, x + 2 * nn, 0, c->ones, nn, c->partial);
+    LAUNCH(c, k_finish_dots, 1, 32, 0, c->partial, kRedBlocks, c->dh + 2 * (c->prm.restart + 2), 0);
+    LAUNCH(c, k_sub_mean, nblk(nn), 256, 0, x + 2 * nn, nn, c->dh + 2 * (c->prm.restart + 2));
+}
+
+// z = V(nu1,nu2)(0, b): Algorithm 1 from a zero guess.
+void vcycle(ibmg_ctx* c, const double* b, double* z) {
+    if (c->lc == 0) {
+        coarse_cycle(c, b, z);
+    } else {
+        CK(cudaMemcpyAsync(c->lev[0].b, b, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
+        for (int l = 0; l < c->lc; ++l) {
+            LevelBuf& lb = c->lev[l];
+            LevelBuf& nx = c->lev[l + 1];
+            CK(cudaMemsetAsync(lb.w, 0, sizeof(double) * 3 * lb.L.nn, c->s));
+            for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, lb.b, lb.w);
+            LAUNCH(c, k_residual_restrict, nblk(nx.L.nn), 256, 0, lb.L, lb.b, lb.w, nx.b);
+            if (c->npts && nx.FL.nf) {
+                LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, lb.w, c->F);
+                LAUNCH(c, k_face_gather, nblk(nx.FL.nf), 256, 0, nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0);
+            }
+        }
+        coarse_cycle(c, c->lev[c->lc].b, c->lev[c->lc].w);
+        for (int l = c->lc - 1; l >= 0; --l) {
+            LevelBuf& lb = c->lev[l];
+            LAUNCH(c, k_prolong_add, nblk(lb.L.nn), 256, 0, lb.L.n, c->lev[l + 1].w, lb.w);
+            for (int s = 0; s < c->prm.nu2; ++s) sweep_level(c, l, lb.b, lb.w);
+        }
+        CK(cudaMemcpyAsync(z, c->lev[0].w, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
+    }
+    // mean removal hoisted to the returned fine state
+    pressure_mean_zero(c, z);
+}
+
+// dots[0..k) = V_i . w, written to c->dh + off (accumulate when acc)
+void multidot(ibmg_ctx* c, const double* V, int k, const double* w, int off, int acc) {
+    dim3 g(kRedBlocks, k);
+    LAUNCH(c, k_multidot_partial, g, kRedThreads, 0, V, c->M, w, c->M, c->partial);
+    LAUNCH(c, k_finish_dots, k, 32, 0, c->partial, kRedBlocks, c->dh + off, acc);
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// FGMRES(m) with one V-cycle as right preconditioner, x0 = 0, CGS2, true
+// residual check at each restart (oracle fgmres()).
+int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
+    const int m = c->prm.restart;
+    const size_t M = c->M;
+    const int hoff = 0, h2off = m + 2;  // dh layout: [h (m+1)] [h2 (m+1)] [scratch]
+    std::vector<double> H(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m);
+    st->iters = st->restarts = st->converged = 0;
+    st->relres = 0.0;
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * M, c->s));
+    // ||b||
+    multidot(c, b, 1, b, hoff, 0);
+    CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    const double bnorm = std::sqrt(c->hpin[0]);
+    if (bnorm == 0.0) {
+        st->converged = 1;
+        return IBMG_OK;
+    }
+    const double tol = c->prm.rtol * bnorm;
+    double beta = bnorm;
+    const double* r = b;
+    int it = 0, restarts = 0;
+    while (true) {
+        LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, nullptr, beta);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int kdim = 0;
+        for (int j = 0; j < m; ++j) {
+            double* Vj = c->V + M * j;
+            double* Zj = c->Z + M * j;
+            vcycle(c, Vj, Zj);
+            apply_level(c, 0, Zj, c->wv);
+            // CGS2: two classical passes, h = h1 + h2
+            multidot(c, c->V, j + 1, c->wv, hoff, 0);
+            LAUNCH(c, k_multi_axpy_sub, nblk(M), 256, 0, c->V, M, j + 1, c->dh + hoff, c->wv, M);
+            multidot(c, c->V, j + 1, c->wv, h2off, 0);
+            LAUNCH(c, k_multi_axpy_sub, nblk(M), 256, 0, c->V, M, j + 1, c->dh + h2off, c->wv, M);
+            multidot(c, c->wv, 1, c->wv, h2off + j + 1, 0);
+            CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (2 * (m + 2)), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = c->hpin[hoff + i] + c->hpin[h2off + i];
+            const double hnext = std::sqrt(c->hpin[h2off + j + 1]);
+            H[size_t(j + 1) * m + j] = hnext;
+            for (int i = 0; i < j; ++i) {
+                const double a = H[size_t(i) * m + j], cc = H[size_t(i + 1) * m + j];
+                H[size_t(i) * m + j] = cs[i] * a + sn[i] * cc;
+                H[size_t(i + 1) * m + j] = -sn[i] * a + cs[i] * cc;
+            }
+            const double a = H[size_t(j) * m + j], cc = H[size_t(j + 1) * m + j];
+            const double den = std::hypot(a, cc);
+            cs[j] = a / den;
+            sn[j] = cc / den;
+            H[size_t(j) * m + j] = den;
+            H[size_t(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++it;
+            kdim = j + 1;
+            if (!std::isfinite(g[j + 1])) throw CudaError("FGMRES: non-finite residual estimate");
+            if (std::fabs(g[j + 1]) <= tol || it >= c->prm.max_iters || hnext == 0.0) break;
+            LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + M * (j + 1), M, nullptr, hnext);
+        }
+        for (int i = kdim - 1; i >= 0; --i) {
+            double s = g[i];
+            for (int k = i + 1; k < kdim; ++k) s -= H[size_t(i) * m + k] * y[k];
+            y[i] = s / H[size_t(i) * m + i];
+        }
+        std::copy(y.begin(), y.begin() + kdim, c->hpin);
+        CK(cudaMemcpyAsync(c->dh + h2off, c->hpin, sizeof(double) * kdim, cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, k_multi_axpy_add, nblk(M), 256, 0, c->Z, M, kdim, c->dh + h2off, x, M);
+        // true residual
+        apply_level(c, 0, x, c->rv);
+        LAUNCH(c, k_b_minus, nblk(M), 256, 0, b, c->rv, M);
+        multidot(c, c->rv, 1, c->rv, hoff, 0);
+        CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        beta = std::sqrt(c->hpin[0]);
+        r = c->rv;
+        if (beta <= tol) {
+            st->converged = 1;
+            break;
+        }
+        if (it >= c->prm.max_iters) break;
+        ++restarts;
+    }
+    pressure_mean_zero(c, x);
+    st->iters = it;
+    st->restarts = restarts;
+    st->relres = beta / bnorm;
+    return st->converged ? IBMG_OK : IBMG_NOT_CONVERGED;
+}
+
+void build_rhs(ibmg_ctx* c, const double* u, double* b) {
+    LevelBuf& l0 = c->lev[0];
+    LAUNCH(c, k_rhs_mass, nblk(c->M), 256, 0, u, b, size_t(l0.L.nn), c->prm.rho / c->prm.dt);
+    if (c->npts && l0.FL.nf) {
+        LAUNCH(c, k_rhs_force, nblk(c->npts, 128), 128, 0, c->P, c->X, c->F);
+        LAUNCH(c, k_face_gather, nblk(l0.FL.nf), 256, 0, l0.FL, l0.W, c->F, b, l0.L.nn, 1.0);
+    }
+}
+
+// ---------------- host/device staging for the C ABI ----------------
+struct Stage {
+    ibmg_ctx* c;
+    int kind;
+    const double* in(const double* p, size_t n, double* buf) {
+        if (kind == IBMG_PTR_DEVICE) return p;
+        CK(cudaMemcpyAsync(buf, p, n * sizeof(double), cudaMemcpyHostToDevice, c->s));
+        return buf;
+    }
+    double* out(double* p, double* buf) { return kind == IBMG_PTR_DEVICE ? p : buf; }
+    void back(double* p, const double* buf, size_t n) {
+        if (kind != IBMG_PTR_DEVICE)
+            CK(cudaMemcpyAsync(p, buf, n * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    }
+};
+
+int fail(ibmg_ctx* c, const std::exception& e, int code) {
+    if (c) c->err = e.what();
+    return code;
+}
+
+template <class Fn>
+int api(ibmg_ctx* c, Fn&& fn) {
+    if (!c) return IBMG_INVALID;
+    try {
+        CK(cudaSetDevice(c->prm.device));
+        return fn();
+    } catch (const std::invalid_argument& e) {
+        return fail(c, e, IBMG_INVALID);
+    } catch (const std::exception& e) {
+        return fail(c, e, IBMG_CUDA);
+    }
+}
+
+void need_level(ibmg_ctx* c, int l) {
+    if (l < 0 || l >= c->nlev) throw InvalidArg("level out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ibmg_create(const ibmg_params* p, ibmg_ctx** out) {
+    if (!p || !out) return IBMG_INVALID;
+    *out = nullptr;
+    if (p->N < 8 || (p->N & (p->N - 1))) return IBMG_INVALID;
+    if (!(p->rho > 0 && p->mu > 0 && p->dt > 0) || p->coarsest_n != 4) return IBMG_INVALID;
+    if (p->restart < 1 || p->restart > 64 || p->max_iters < 1 || !(p->rtol > 0 && p->rtol < 1)) return IBMG_INVALID;
+    if (p->nu1 < 0 || p->nu2 < 0 || p->nu1 + p->nu2 < 1) return IBMG_INVALID;
+    ibmg_ctx* c = new ibmg_ctx;
+    c->prm = *p;
+    try {
+        CK(cudaSetDevice(p->device));
+        CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 112 * 8));
+        CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * 98 * 8));
+        alloc_levels(c);
+        CK(cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem(c))));
+        c->npts = 0;
+        rebuild(c);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "ibmg_create: %s\n", e.what());
+        ibmg_destroy(c);
+        return IBMG_CUDA;
+    }
+    *out = c;
+    return IBMG_OK;
+}
+
+void ibmg_destroy(ibmg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->prm.device);
+    if (c->s) cudaStreamSynchronize(c->s);
+    free_structs(c);
+    for (auto& lb : c->lev) {
+        dfree(lb.w);
+        dfree(lb.b);
+        dfree(lb.r);
+        dfree(lb.big);
+    }
+    dfree(c->V);
+    dfree(c->Z);
+    dfree(c->wv);
+    dfree(c->xv);
+    dfree(c->rv);
+    dfree(c->bv);
+    dfree(c->stage_a);
+    dfree(c->stage_b);
+    dfree(c->partial);
+    dfree(c->dh);
+    dfree(c->ones);
+    dfree(c->err_flag);
+    dfree(c->counters);
+    dfree(c->Acoarse);
+    if (c->cub_tmp) cudaFree(c->cub_tmp);
+    if (c->hpin) cudaFreeHost(c->hpin);
+    if (c->s) cudaStreamDestroy(c->s);
+    delete c;
+}
+
+const char* ibmg_last_error(const ibmg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int ibmg_num_levels(const ibmg_ctx* c) { return c ? c->nlev : -1; }
+int ibmg_level_n(const ibmg_ctx* c, int l) { return (c && l >= 0 && l < c->nlev) ? c->lev[l].L.n : -1; }
+long long ibmg_kernel_launches(const ibmg_ctx* c) { return c ? c->launches : -1; }
+void* ibmg_stream(const ibmg_ctx* c) { return c ? (void*)c->s : nullptr; }
+
+int ibmg_set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, const double* ds,
+                        const double* X, int ptr_kind) {
+    return api(c, [&]() -> int {
+        if (n_mem > 0 && (!nb || !kappa || !ds || !X)) throw InvalidArg("null structure arrays");
+        set_structures(c, n_mem, nb, kappa, ds, X, ptr_kind);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_apply(ibmg_ctx* c, int level, const double* w, double* out, int ptr_kind) {
+    return api(c, [&]() -> int {
+        need_level(c, level);
+        const size_t m = 3 * size_t(c->lev[level].L.nn);
+        Stage S{c, ptr_kind};
+        const double* dw = S.in(w, m, c->stage_a);
+        double* dout = S.out(out, c->stage_b);
+        apply_level(c, level, dw, dout);
+        S.back(out, dout, m);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_residual(ibmg_ctx* c, int level, const double* b, const double* w, double* r, double* norm,
+                  int ptr_kind) {
+    return api(c, [&]() -> int {
+        need_level(c, level);
+        const size_t m = 3 * size_t(c->lev[level].L.nn);
+        Stage S{c, ptr_kind};
+        const double* db = S.in(b, m, c->stage_a);
+        const double* dw = S.in(w, m, c->stage_b);
+        double* dr = ptr_kind == IBMG_PTR_DEVICE ? r : c->rv;
+        residual_level(c, level, db, dw, dr);
+        if (norm) {
+            multidot(c, dr, 1, dr, 0, 0);
+            CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        }
+        S.back(r, dr, m);
+        if (norm) *norm = std::sqrt(c->hpin[0]);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_restrict(ibmg_ctx* c, int level, const double* rf, double* rc, int ptr_kind) {
+    return api(c, [&]() -> int {
+        if (level < 0 || level + 1 >= c->nlev) throw InvalidArg("restrict: level out of range");
+        const int nf = c->lev[level].L.n;
+        Stage S{c, ptr_kind};
+        const double* d_in = S.in(rf, 3 * size_t(nf) * nf, c->stage_a);
+        double* d_out = S.out(rc, c->stage_b);
+        LAUNCH(c, k_restrict, nblk(size_t(nf / 2) * (nf / 2)), 256, 0, nf, d_in, d_out);
+        S.back(rc, d_out, 3 * size_t(nf / 2) * (nf / 2));
+        return IBMG_OK;
+    });
+}
+
+int ibmg_prolong_add(ibmg_ctx* c, int level, const double* ec, double* wf, int ptr_kind) {
+    return api(c, [&]() -> int {
+        if (level < 0 || level + 1 >= c->nlev) throw InvalidArg("prolong: level out of range");
+        const int nf = c->lev[level].L.n;
+        Stage S{c, ptr_kind};
+        const double* d_ec = S.in(ec, 3 * size_t(nf / 2) * (nf / 2), c->stage_a);
+        double* d_wf = ptr_kind == IBMG_PTR_DEVICE ? wf : const_cast<double*>(S.in(wf, 3 * size_t(nf) * nf, c->stage_b));
+        LAUNCH(c, k_prolong_add, nblk(size_t(nf) * nf), 256, 0, nf, d_ec, d_wf);
+        S.back(wf, d_wf, 3 * size_t(nf) * nf);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_sweep(ibmg_ctx* c, int level, const double* b, double* w, int ptr_kind) {
+    return api(c, [&]() -> int {
+        if (level < 0 || level + 1 >= c->nlev) throw InvalidArg("sweep: level out of range");
+        if (level >= c->lc) throw InvalidArg("sweep: levels with n <= 32 run inside the coarse-cycle kernel only");
+        const size_t m = 3 * size_t(c->lev[level].L.nn);
+        Stage S{c, ptr_kind};
+        const double* db = S.in(b, m, c->stage_a);
+        double* dw = ptr_kind == IBMG_PTR_DEVICE ? w : const_cast<double*>(S.in(w, m, c->stage_b));
+        sweep_level(c, level, db, dw);
+        S.back(w, dw, m);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_vcycle(ibmg_ctx* c, const double* b, double* z, int ptr_kind) {
+    return api(c, [&]() -> int {
+        Stage S{c, ptr_kind};
+        const double* db = S.in(b, c->M, c->stage_a);
+        double* dz = S.out(z, c->stage_b);
+        vcycle(c, db, dz);
+        S.back(z, dz, c->M);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_coarse_solve(ibmg_ctx* c, const double* b, double* x, int ptr_kind) {
+    return api(c, [&]() -> int {
+        // the coarsest solve alone: a 1-level coarse-kernel launch on the last level
+        const int l = c->nlev - 1;
+        const size_t m = 3 * size_t(c->lev[l].L.nn);
+        Stage S{c, ptr_kind};
+        const double* db = S.in(b, m, c->stage_a);
+        double* dx = S.out(x, c->stage_b);
+        const int save = c->lc;
+        c->lc = l;
+        CoarseArgs A = coarse_args(c, db, dx);
+        const size_t smem = coarse_smem(c);
+        c->lc = save;
+        LAUNCH(c, k_coarse_cycle, 1, kCoarseThreads, smem, A);
+        S.back(x, dx, m);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_big_blocks(ibmg_ctx* c, int level, int* flags) {
+    try {
+        if (!c || level < 0 || level + 1 >= c->nlev) return -1;
+        CK(cudaSetDevice(c->prm.device));
+        const int nbk = c->lev[level].L.n / 4;
+        std::vector<uint8_t> h(size_t(nbk) * nbk);
+        CK(cudaMemcpy(h.data(), c->lev[level].big, h.size(), cudaMemcpyDeviceToHost));
+        int cnt = 0;
+        for (size_t q = 0; q < h.size(); ++q) {
+            if (flags) flags[q] = h[q];
+            cnt += h[q];
+        }
+        return cnt;
+    } catch (const std::exception& e) {
+        return fail(c, e, -1);
+    }
+}
+
+int ibmg_build_rhs(ibmg_ctx* c, const double* u_n, double* b, int ptr_kind) {
+    return api(c, [&]() -> int {
+        const size_t nn = size_t(c->prm.N) * c->prm.N;
+        Stage S{c, ptr_kind};
+        const double* du = S.in(u_n, 2 * nn, c->stage_a);
+        double* db = S.out(b, c->stage_b);
+        build_rhs(c, du, db);
+        S.back(b, db, c->M);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_interpolate(ibmg_ctx* c, const double* u, double* U, int ptr_kind) {
+    return api(c, [&]() -> int {
+        const size_t nn = size_t(c->prm.N) * c->prm.N;
+        Stage S{c, ptr_kind};
+        const double* du = S.in(u, 2 * nn, c->stage_a);
+        double* dU = S.out(U, c->stage_b);
+        if (c->npts)
+            LAUNCH(c, k_interp, nblk(c->npts, 128), 128, 0, c->lev[0].W, c->npts, c->prm.N, c->lev[0].L.h, du, dU,
+                   (double*)nullptr, 0.0);
+        S.back(U, dU, 2 * size_t(c->npts));
+        return IBMG_OK;
+    });
+}
+
+int ibmg_spread(ibmg_ctx* c, const double* Fin, double* f, int ptr_kind) {
+    return api(c, [&]() -> int {
+        const size_t nn = size_t(c->prm.N) * c->prm.N;
+        Stage S{c, ptr_kind};
+        const double* dF = S.in(Fin, 2 * size_t(c->npts), c->stage_a);
+        double* df = S.out(f, c->stage_b);
+        CK(cudaMemsetAsync(df, 0, sizeof(double) * 2 * nn, c->s));
+        LevelBuf& l0 = c->lev[0];
+        if (c->npts && l0.FL.nf) {
+            LAUNCH(c, k_scale_dsq, nblk(c->npts, 128), 128, 0, c->P, dF, c->F);
+            LAUNCH(c, k_face_gather, nblk(l0.FL.nf), 256, 0, l0.FL, l0.W, c->F, df, l0.L.nn, 1.0);
+        }
+        S.back(f, df, 2 * nn);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_solve(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st, int ptr_kind) {
+    ibmg_stats local{};
+    if (!st) st = &local;
+    return api(c, [&]() -> int {
+        const double t0 = now_ms();
+        const double* db = ptr_kind == IBMG_PTR_DEVICE ? b : nullptr;
+        if (!db) {
+            CK(cudaMemcpyAsync(c->bv, b, sizeof(double) * c->M, cudaMemcpyHostToDevice, c->s));
+            db = c->bv;
+        }
+        double* dx = ptr_kind == IBMG_PTR_DEVICE ? x : c->xv;
+        const int rc = fgmres(c, db, dx, st);
+        if (ptr_kind != IBMG_PTR_DEVICE)
+            CK(cudaMemcpyAsync(x, dx, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        st->solve_ms = now_ms() - t0;
+        st->total_ms = st->solve_ms;
+        return rc;
+    });
+}
+
+int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int ptr_kind) {
+    ibmg_stats local{};
+    if (!st) st = &local;
+    return api(c, [&]() -> int {
+        if (!c->have_structs) throw InvalidArg("ibmg_step: call ibmg_set_structures first");
+        const double t0 = now_ms();
+        const size_t nn = size_t(c->prm.N) * c->prm.N;
+        // X^n in, lagged operators rebuilt at X^n
+        if (c->npts)
+            CK(cudaMemcpyAsync(c->X, X, sizeof(double) * 2 * c->npts,
+                               ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
+        rebuild(c);
+        const double* du = u;
+        if (ptr_kind != IBMG_PTR_DEVICE) {
+            CK(cudaMemcpyAsync(c->stage_a, u, sizeof(double) * 2 * nn, cudaMemcpyHostToDevice, c->s));
+            du = c->stage_a;
+        }
+        build_rhs(c, du, c->bv);
+        CK(cudaStreamSynchronize(c->s));
+        const double t1 = now_ms();
+        const int rc = fgmres(c, c->bv, c->xv, st);
+        CK(cudaStreamSynchronize(c->s));
+        const double t2 = now_ms();
+        if (c->npts)
+            LAUNCH(c, k_interp, nblk(c->npts, 128), 128, 0, c->lev[0].W, c->npts, c->prm.N, c->lev[0].L.h, c->xv,
+                   (double*)nullptr, c->X, c->prm.dt);
+        const cudaMemcpyKind k = ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        CK(cudaMemcpyAsync(u, c->xv, sizeof(double) * 2 * nn, k, c->s));
+        CK(cudaMemcpyAsync(p, c->xv + 2 * nn, sizeof(double) * nn, k, c->s));
+        if (c->npts) CK(cudaMemcpyAsync(X, c->X, sizeof(double) * 2 * c->npts, k, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        st->setup_ms = t1 - t0;
+        st->solve_ms = t2 - t1;
+        st->total_ms = now_ms() - t0;
+        return rc;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,350 @@
+// smoother_kernels.cuh — multicolour box relaxation (the paper's generalised
+// Vanka / big-box smoother) and the coarse-level kernels.
+//
+// Schedule (mirrored exactly by oracle/ibmg_oracle.cpp
+// build_schedule): plain phase = 16x16-cell tiles coloured 2x2 (one launch per
+// tile colour, one warp per tile, the 8 conflict-free colours (i+2j) mod 8 run
+// in shared memory); big phase = big 4x4 blocks in 16 level-wide colours
+// (bx mod 4, by mod 4), one CTA per block, dense 56x56 inverse applied.
+#pragma once
+#include "common.cuh"
+#include "grid_kernels.cuh"
+
+namespace ibmg {
+
+// Exact 5x5 Vanka solve of one plain cell (§5 "5-by-5 system") in
+// closed form for the constant-coefficient periodic stencil, then the
+// immediate correction (multiplicative sweep).
+template <class WA, class BA>
+__device__ __forceinline__ void plain_cell(const Lev& L, WA& W, const BA& B, int i, int j) {
+    const double d = L.d, c = L.c, g = L.g;
+    const double uW = W(0, i, j), uE = W(0, i + 1, j), vS = W(1, i, j), vN = W(1, i, j + 1), pC = W(2, i, j);
+    const double r_uW =
+        B(0, i, j) - (d * uW - c * (W(0, i - 1, j) + uE + W(0, i, j - 1) + W(0, i, j + 1)) + g * (pC - W(2, i - 1, j)));
+    const double r_uE = B(0, i + 1, j) -
+                        (d * uE - c * (uW + W(0, i + 2, j) + W(0, i + 1, j - 1) + W(0, i + 1, j + 1)) +
+                         g * (W(2, i + 1, j) - pC));
+    const double r_vS =
+        B(1, i, j) - (d * vS - c * (W(1, i, j - 1) + vN + W(1, i - 1, j) + W(1, i + 1, j)) + g * (pC - W(2, i, j - 1)));
+    const double r_vN = B(1, i, j + 1) -
+                        (d * vN - c * (vS + W(1, i, j + 2) + W(1, i - 1, j + 1) + W(1, i + 1, j + 1)) +
+                         g * (W(2, i, j + 1) - pC));
+    const double r_p = B(2, i, j) - (-g * (uE - uW) - g * (vN - vS));
+    const double dpc = d + c, dmc = d - c;
+    const double dp = ((r_uW - r_uE + r_vS - r_vN) - dpc * r_p / g) / (4.0 * g);
+    const double s = (r_uW - r_uE - 2.0 * g * dp) / dpc;
+    const double t = (r_vS - r_vN - 2.0 * g * dp) / dpc;
+    const double a = (r_uW + r_uE) / dmc, e = (r_vS + r_vN) / dmc;
+    W(0, i, j) = uW + 0.5 * (a + s);
+    W(0, i + 1, j) = uE + 0.5 * (a - s);
+    W(1, i, j) = vS + 0.5 * (e + t);
+    W(1, i, j + 1) = vN + 0.5 * (e - t);
+    W(2, i, j) = pC + dp;
+}
+
+// ---- plain phase, multi-tile levels (n >= 32): one warp per 16x16 tile.
+constexpr int kTile = 16, kReg = kTile + 4;  // region with a 2-cell halo
+
+struct TileW {
+    double* s;  // [3][kReg][kReg], local coords li, lj in [-2, 18)
+    __device__ __forceinline__ double& operator()(int f, int i, int j) const {
+        return s[f * kReg * kReg + (j + 2) * kReg + (i + 2)];
+    }
+};
+struct TileB {
+    const double* s;  // [3][17][17], local coords in [0, 17)
+    __device__ __forceinline__ double operator()(int f, int i, int j) const { return s[f * 289 + j * 17 + i]; }
+};
+
+__global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double* __restrict__ b,
+                                                     double* __restrict__ w, const uint8_t* __restrict__ big) {
+    __shared__ double sw[3 * kReg * kReg];
+    __shared__ double sb[3 * 289];
+    __shared__ uint8_t sbig[16];
+    const int n = L.n, nn = L.nn, lane = threadIdx.x;
+    const int half = (n / kTile) >> 1;
+    const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = 2 * (blockIdx.x / half) + (tc >> 1);
+    const int x0 = tx * kTile, y0 = ty * kTile;
+    for (int q = lane; q < kReg * kReg; q += 32) {
+        const int a = q % kReg, bb = q / kReg;
+        const size_t gi = wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n;
+        sw[q] = w[gi];
+        sw[kReg * kReg + q] = w[nn + gi];
+        sw[2 * kReg * kReg + q] = w[2 * nn + gi];
+    }
+    for (int q = lane; q < 289; q += 32) {
+        const int a = q % 17, bb = q / 17;
+        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+        sb[q] = b[gi];
+        sb[289 + q] = b[nn + gi];
+        sb[578 + q] = b[2 * nn + gi];
+    }
+    if (lane < 16) sbig[lane] = big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
+    __syncwarp();
+    TileW W{sw};
+    TileB B{sb};
+    for (int pc = 0; pc < 8; ++pc) {
+        const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
+        if (!sbig[(li >> 2) + 4 * (lj >> 2)]) plain_cell(L, W, B, li, lj);
+        __syncwarp();
+    }
+    // write set: u faces i in [x0, x0+16], v faces j in [y0, y0+16], p cells
+    for (int q = lane; q < 17 * 17; q += 32) {
+        const int a = q % 17, bb = q / 17;
+        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+        if (bb < 16) w[gi] = W(0, a, bb);
+        if (a < 16) w[nn + gi] = W(1, a, bb);
+        if (a < 16 && bb < 16) w[2 * nn + gi] = W(2, a, bb);
+    }
+}
+
+// Global accessor for plain loads (no __ldg: the big phase writes w in-kernel).
+struct GAccRW {
+    const double* w;
+    int n, nn;
+    __device__ __forceinline__ double operator()(int comp, int i, int j) const {
+        return w[(size_t)comp * nn + i + (size_t)j * n];
+    }
+};
+
+// Residual of block DOF t (0..55) of the block at (bi, bj): b - A w including
+// the -E' part via the face lists (E' rows of DOF t) and on-the-fly point forces.
+template <class Acc, class BAcc>
+__device__ __forceinline__ double block_residual(const Lev& L, const Win& W, const Pts& P, const FaceList& FL,
+                                                 const Acc& acc, const BAcc& bacc, int fi, int t, int bi, int bj) {
+    int f, i, j;
+    block_dof(t, bi, bj, f, i, j);
+    i = wr(i, L.n);
+    j = wr(j, L.n);
+    double ru, rv, rp;
+    stokes_rows(L, acc, i, j, ru, rv, rp);
+    double r = bacc(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
+    if (f < 2 && fi >= 0) {
+        double s = 0.0;
+        for (int e = FL.off[fi]; e < FL.off[fi + 1]; ++e) {
+            const int v = FL.ent[e];
+            const int k = v >> 5;
+            s += W.w[(size_t)k * 64 + (v & 31)] * point_force(W, P, k, f, L.n, acc);
+        }
+        r += s;
+    }
+    return r;
+}
+
+// Big phase, one colour: one 64-thread CTA per big block of the colour.
+__global__ void __launch_bounds__(64) k_big_sweep(Lev L, Win W, Pts P, FaceList FL, const int* __restrict__ blk_ids,
+                                                   const int* __restrict__ fidx, const double* __restrict__ Ainv,
+                                                   int qbase, const double* __restrict__ b, double* w) {
+    __shared__ double sr[56];
+    const int q = qbase + blockIdx.x, t = threadIdx.x;
+    const int B = blk_ids[q], nbk = L.n >> 2;
+    const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
+    GAccRW acc{w, L.n, L.nn};
+    GAccRW bacc{b, L.n, L.nn};
+    if (t < 56) sr[t] = block_residual(L, W, P, FL, acc, bacc, t < 40 ? fidx[(size_t)q * 40 + t] : -1, t, bi, bj);
+    __syncthreads();
+    if (t < 56) {
+        const double* A = Ainv + (size_t)q * 3136;
+        double s = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < 56; ++c) s += A[c * 56 + t] * sr[c];
+        int f, i, j;
+        block_dof(t, bi, bj, f, i, j);
+        w[(size_t)f * L.nn + wr(i, L.n) + (size_t)wr(j, L.n) * L.n] += s;
+    }
+}
+
+// ---- setup: dense local matrices and their inverses --------------------------
+
+// Gauss-Jordan with partial pivoting on an m x 2m augmented matrix in shared
+// memory (row-major, ld = 2m).  Ties in the pivot search go to the lowest row.
+__device__ void gauss_jordan(double* M, int m, double* col, int* err) {
+    const int ld = 2 * m, t = threadIdx.x, nt = blockDim.x;
+    __shared__ int piv;
+    for (int k = 0; k < m; ++k) {
+        if (t < 32) {
+            double best = -1.0;
+            int bi = k;
+            for (int i = k + t; i < m; i += 32) {
+                const double v = fabs(M[i * ld + k]);
+                if (v > best) { best = v; bi = i; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (t == 0) piv = bi;
+        }
+        __syncthreads();
+        const int p = piv;
+        if (p != k)
+            for (int j = t; j < ld; j += nt) {
+                const double a = M[k * ld + j];
+                M[k * ld + j] = M[p * ld + j];
+                M[p * ld + j] = a;
+            }
+        __syncthreads();
+        const double pv = M[k * ld + k];
+        if (pv == 0.0) {
+            if (t == 0) atomicOr(err, 2);
+            return;
+        }
+        __syncthreads();
+        for (int j = t; j < ld; j += nt) M[k * ld + j] /= pv;
+        for (int i = t; i < m; i += nt) col[i] = M[i * ld + k];
+        __syncthreads();
+        for (int idx = t; idx < m * ld; idx += nt) {
+            const int i = idx / ld, j = idx - i * ld;
+            if (i != k) M[idx] -= col[i] * M[k * ld + j];
+        }
+        __syncthreads();
+    }
+}
+
+// Stokes entries of row r of a box, emitted as (field, da, db, value) with da,
+// db the column offset relative to the row's own (i, j).
+template <class Emit>
+__device__ __forceinline__ void stokes_row_entries(const Lev& L, int field, Emit&& emit) {
+    const double d = L.d, c = L.c, g = L.g;
+    if (field == 0) {
+        emit(0, 0, 0, d); emit(0, -1, 0, -c); emit(0, 1, 0, -c); emit(0, 0, -1, -c); emit(0, 0, 1, -c);
+        emit(2, 0, 0, g); emit(2, -1, 0, -g);
+    } else if (field == 1) {
+        emit(1, 0, 0, d); emit(1, 0, -1, -c); emit(1, 0, 1, -c); emit(1, -1, 0, -c); emit(1, 1, 0, -c);
+        emit(2, 0, 0, g); emit(2, 0, -1, -g);
+    } else {
+        emit(0, 1, 0, -g); emit(0, 0, 0, g); emit(1, 0, 1, -g); emit(1, 0, 0, g);
+    }
+}
+
+// E'(row face, col face) = sum_{(k,l) in list(row)} l c_k (R_{k-1} - 2 R_k + R_{k+1})(col).
+__device__ __forceinline__ double elastic_entry(const Win& W, const Pts& P, const FaceList& FL, int fi, int comp,
+                                                int n, int ic, int jc) {
+    double s = 0.0;
+    for (int e = FL.off[fi]; e < FL.off[fi + 1]; ++e) {
+        const int v = FL.ent[e];
+        const int k = v >> 5;
+        const double rr = win_at(W, P.kprev[k], 2 + comp, n, ic, jc) - 2.0 * win_at(W, k, 2 + comp, n, ic, jc) +
+                          win_at(W, P.knext[k], 2 + comp, n, ic, jc);
+        s += W.w[(size_t)k * 64 + (v & 31)] * (P.cE[k] * rr);
+    }
+    return s;
+}
+
+// One CTA per big block: assemble the 56x56 principal submatrix of A_l on the
+// block DOFs, invert it, store the inverse column-major.
+__global__ void k_block_inverse(Lev L, Win W, Pts P, FaceList FL, const int* __restrict__ blk_ids,
+                                const int* __restrict__ fidx, double* __restrict__ Ainv, int* err) {
+    extern __shared__ double M[];  // 56 x 112
+    __shared__ double col[56];
+    const int q = blockIdx.x, t = threadIdx.x, nt = blockDim.x, n = L.n;
+    const int B = blk_ids[q], nbk = n >> 2;
+    const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
+    for (int idx = t; idx < 56 * 112; idx += nt) {
+        const int i = idx / 112, j = idx % 112;
+        M[idx] = (j == 56 + i) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (t < 56) {
+        int f, i, j;
+        block_dof(t, bi, bj, f, i, j);
+        const int a = i - bi, bb = j - bj;
+        stokes_row_entries(L, f, [&](int f2, int da, int db, double v) {
+            const int c = block_local(f2, a + da, bb + db);
+            if (c >= 0) M[t * 112 + c] += v;
+        });
+    }
+    __syncthreads();
+    for (int idx = t; idx < 40 * 40; idx += nt) {
+        const int r = idx / 40, c = idx % 40;
+        const int comp = r >= 20;
+        if ((c >= 20) != comp) continue;
+        const int fi = fidx[(size_t)q * 40 + r];
+        if (fi < 0) continue;
+        int f, i, j;
+        block_dof(c, bi, bj, f, i, j);
+        M[r * 112 + c] -= elastic_entry(W, P, FL, fi, comp, n, wr(i, n), wr(j, n));
+    }
+    __syncthreads();
+    gauss_jordan(M, 56, col, err);
+    for (int idx = t; idx < 56 * 56; idx += nt) {
+        const int c = idx / 56, r = idx % 56;
+        Ainv[(size_t)q * 3136 + idx] = M[r * 112 + 56 + c];
+    }
+}
+
+// Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
+// pressure constraint), 49 x 49, inverted; stored col-major.
+__global__ void k_coarse_inverse(Lev L, Win W, Pts P, FaceList FL, double* __restrict__ Ainv, int* err) {
+    extern __shared__ double M[];
+    __shared__ double col[64];
+    const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = 2 * m, t = threadIdx.x, nt = blockDim.x;
+    for (int idx = t; idx < m * ld; idx += nt) {
+        const int i = idx / ld, j = idx % ld;
+        M[idx] = (j == m + i) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (t < 3 * nn) {
+        const int f = t / nn, i = (t % nn) % n, j = (t % nn) / n;
+        stokes_row_entries(L, f, [&](int f2, int da, int db, double v) {
+            M[t * ld + f2 * nn + wr(i + da, n) + wr(j + db, n) * n] += v;
+        });
+        if (f == 2) {
+            M[t * ld + 3 * nn] = 1.0;
+            M[3 * nn * ld + t] = 1.0;
+        }
+    }
+    __syncthreads();
+    for (int idx = t; idx < 4 * nn * nn; idx += nt) {
+        const int r = idx / (2 * nn), c = idx % (2 * nn);
+        const int comp = r >= nn;
+        if ((c >= nn) != comp) continue;
+        // find row face r in the sorted face list
+        int lo = 0, hi = FL.nf;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (FL.face[mid] < r) lo = mid + 1; else hi = mid;
+        }
+        if (lo >= FL.nf || FL.face[lo] != r) continue;
+        const int cf = c % nn;
+        M[r * ld + c] -= elastic_entry(W, P, FL, lo, comp, n, cf % n, cf / n);
+    }
+    __syncthreads();
+    gauss_jordan(M, m, col, err);
+    for (int idx = t; idx < m * m; idx += nt) {
+        const int c = idx / m, r = idx % m;
+        Ainv[idx] = M[r * ld + m + c];
+    }
+}
+
+// Face-list index of each of the 40 velocity DOFs of every big block (-1 if the
+// face has no E' row).
+__global__ void k_block_fidx(Lev L, FaceList FL, const int* __restrict__ blk_ids, int nbig, int* __restrict__ fidx) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nbig * 40) return;
+    const int q = idx / 40, t = idx % 40, n = L.n, nbk = n >> 2;
+    const int B = blk_ids[q];
+    int f, i, j;
+    block_dof(t, 4 * (B % nbk), 4 * (B / nbk), f, i, j);
+    const int key = f * L.nn + wr(i, n) + wr(j, n) * n;
+    int lo = 0, hi = FL.nf;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (FL.face[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    fidx[idx] = (lo < FL.nf && FL.face[lo] == key) ? lo : -1;
+}
+
+// Block sort keys: colour (bx mod 4) + 4 (by mod 4) for big blocks, 16 otherwise.
+__global__ void k_block_keys(int nbk, const uint8_t* __restrict__ big, int* keys, int* vals, int* counts) {
+    const int B = blockIdx.x * blockDim.x + threadIdx.x;
+    if (B >= nbk * nbk) return;
+    const int bx = B % nbk, by = B / nbk;
+    const int key = big[B] ? (bx & 3) + 4 * (by & 3) : 16;
+    keys[B] = key;
+    vals[B] = B;
+    atomicAdd(&counts[key], 1);
+}
+
+}  // namespace ibmg

@@ -1,0 +1,270 @@
+"""Host-side mirror of the reference's ibmg:: solver interface over the C ABI.
+
+The reference is C++ (proj/core/include/ibmg/*.hpp); its solver path is
+reached here through include/ibmg_gpu.h (libibmg_b200.so, hand-written sm_100a
+kernels).  Names follow the reference: SaddleSystem.apply / .residual
+(saddle.hpp:32-38), restrict_saddle / prolong_saddle_add (transfers.hpp:25-28),
+spread / interpolate (fiber.hpp:80-83), build_rhs (saddle.hpp:46), v_cycle /
+gmres_solve / step_implicit.  Errors map back to the
+reference's exception types: status 1 -> ValueError (std::invalid_argument),
+3 -> RuntimeError (std::runtime_error).  Non-convergence is a flag, not an
+error.
+
+Arrays may be numpy (host; copied inside the call) or CUDA torch tensors on
+the context's device (zero-copy).  There is no CPU fallback: if the CUDA
+library is missing this module raises on import of the context.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+IBMG_PTR_HOST, IBMG_PTR_DEVICE = 0, 1
+_LIB = None
+
+
+class Params(C.Structure):
+    _fields_ = [("N", C.c_int), ("rho", C.c_double), ("mu", C.c_double), ("dt", C.c_double),
+                ("nu1", C.c_int), ("nu2", C.c_int), ("restart", C.c_int), ("max_iters", C.c_int),
+                ("rtol", C.c_double), ("coarsest_n", C.c_int), ("device", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("iters", C.c_int), ("restarts", C.c_int), ("converged", C.c_int), ("relres", C.c_double),
+                ("setup_ms", C.c_double), ("solve_ms", C.c_double), ("total_ms", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structures", "ibmg_num_levels",
+           "ibmg_level_n", "ibmg_apply", "ibmg_residual", "ibmg_restrict", "ibmg_prolong_add", "ibmg_sweep",
+           "ibmg_vcycle", "ibmg_coarse_solve", "ibmg_big_blocks", "ibmg_build_rhs", "ibmg_interpolate",
+           "ibmg_spread", "ibmg_solve", "ibmg_step", "ibmg_kernel_launches", "ibmg_stream"]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib(build_if_missing: bool = True):
+    """Load libibmg_b200.so (building it in-tree if absent and nvcc is present)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise RuntimeError(f"CUDA library missing: {path}")
+        _build.build_cuda()
+    L = C.CDLL(path)
+    vp, ip, dp = C.c_void_p, C.c_int, C.c_void_p
+    L.ibmg_create.argtypes = [C.POINTER(Params), C.POINTER(C.c_void_p)]
+    L.ibmg_destroy.argtypes = [vp]
+    L.ibmg_last_error.restype = C.c_char_p
+    L.ibmg_last_error.argtypes = [vp]
+    L.ibmg_set_structures.argtypes = [vp, ip, vp, vp, vp, vp, ip]
+    L.ibmg_num_levels.argtypes = [vp]
+    L.ibmg_level_n.argtypes = [vp, ip]
+    L.ibmg_apply.argtypes = [vp, ip, dp, dp, ip]
+    L.ibmg_residual.argtypes = [vp, ip, dp, dp, dp, C.POINTER(C.c_double), ip]
+    L.ibmg_restrict.argtypes = [vp, ip, dp, dp, ip]
+    L.ibmg_prolong_add.argtypes = [vp, ip, dp, dp, ip]
+    L.ibmg_sweep.argtypes = [vp, ip, dp, dp, ip]
+    L.ibmg_vcycle.argtypes = [vp, dp, dp, ip]
+    L.ibmg_coarse_solve.argtypes = [vp, dp, dp, ip]
+    L.ibmg_big_blocks.argtypes = [vp, ip, vp]
+    L.ibmg_build_rhs.argtypes = [vp, dp, dp, ip]
+    L.ibmg_interpolate.argtypes = [vp, dp, dp, ip]
+    L.ibmg_spread.argtypes = [vp, dp, dp, ip]
+    L.ibmg_solve.argtypes = [vp, dp, dp, C.POINTER(Stats), ip]
+    L.ibmg_step.argtypes = [vp, dp, dp, dp, C.POINTER(Stats), ip]
+    L.ibmg_kernel_launches.restype = C.c_longlong
+    L.ibmg_kernel_launches.argtypes = [vp]
+    L.ibmg_stream.restype = C.c_void_p
+    L.ibmg_stream.argtypes = [vp]
+    _LIB = L
+    return L
+
+
+def _ptr(a):
+    """(pointer, kind) of a numpy array or a CUDA torch tensor."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous float64")
+        return a.ctypes.data, IBMG_PTR_HOST
+    if hasattr(a, "data_ptr") and getattr(a, "is_cuda", False):
+        import torch
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("tensors must be contiguous float64")
+        return a.data_ptr(), IBMG_PTR_DEVICE
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _empty_like(a, n):
+    if isinstance(a, np.ndarray):
+        return np.empty(n, np.float64)
+    import torch
+    return torch.empty(n, dtype=torch.float64, device=a.device)
+
+
+class SaddleSystem:
+    """Periodic backward-Euler IB-Stokes saddle system on a MAC grid, with its
+    multigrid hierarchy and FGMRES solver, resident on one GPU.
+
+    Mirrors ibmg::SaddleSystem (saddle.hpp:19-39) extended per SURVEY §9:
+    periodic geometry (D1), rho/dt and mu (D2), sign (D3), per-membrane kappa.
+    """
+
+    def __init__(self, N, rho=1.0, mu=1.0, dt=1e-2, nu1=1, nu2=1, restart=30, max_iters=600, rtol=1e-10,
+                 device=0):
+        self._L = lib()
+        p = Params(N, rho, mu, dt, nu1, nu2, restart, max_iters, rtol, 4, device)
+        h = C.c_void_p()
+        rc = self._L.ibmg_create(C.byref(p), C.byref(h))
+        if rc != 0 or not h.value:
+            raise RuntimeError(f"ibmg_create failed (status {rc}); is a CUDA device available?")
+        self._h = h
+        self.N, self.rho, self.mu, self.dt = N, rho, mu, dt
+        self.npts = 0
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.ibmg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, rc, ok=(0,)):
+        if rc in ok:
+            return rc
+        msg = self._L.ibmg_last_error(self._h).decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+    # -- structure (FiberMesh + assemble_elasticity + Galerkin hierarchy)
+    def set_structures(self, nb, kappa, ds, X):
+        nb = np.ascontiguousarray(nb, np.int32)
+        kappa = np.ascontiguousarray(kappa, np.float64)
+        ds = np.ascontiguousarray(ds, np.float64)
+        if isinstance(X, np.ndarray):
+            X = np.ascontiguousarray(X, np.float64).reshape(-1)
+        xp, kind = _ptr(X)
+        self._chk(self._L.ibmg_set_structures(self._h, len(nb), nb.ctypes.data, kappa.ctypes.data,
+                                              ds.ctypes.data, xp, kind))
+        self.npts = int(nb.sum())
+        return self
+
+    @classmethod
+    def from_problem(cls, prob, **kw):
+        s = cls(prob.N, prob.rho, prob.mu, prob.dt, **kw)
+        s.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
+        return s
+
+    @property
+    def num_levels(self):
+        return self._L.ibmg_num_levels(self._h)
+
+    def level_n(self, level):
+        return self._L.ibmg_level_n(self._h, level)
+
+    def _size(self, level):
+        n = self.level_n(level)
+        return 3 * n * n
+
+    def apply(self, w, out=None, level=0):
+        out = _empty_like(w, self._size(level)) if out is None else out
+        (wp, k), (op, _) = _ptr(w), _ptr(out)
+        self._chk(self._L.ibmg_apply(self._h, level, wp, op, k))
+        return out
+
+    def residual(self, b, w, level=0):
+        r = _empty_like(w, self._size(level))
+        nrm = C.c_double()
+        (bp, k), (wp, _), (rp, _) = _ptr(b), _ptr(w), _ptr(r)
+        self._chk(self._L.ibmg_residual(self._h, level, bp, wp, rp, C.byref(nrm), k))
+        return r, nrm.value
+
+    def sweep(self, b, w, level=0):
+        """One multicolour box sweep, in place on w (returns w)."""
+        (bp, k), (wp, _) = _ptr(b), _ptr(w)
+        self._chk(self._L.ibmg_sweep(self._h, level, bp, wp, k))
+        return w
+
+    def v_cycle(self, b):
+        z = _empty_like(b, self._size(0))
+        (bp, k), (zp, _) = _ptr(b), _ptr(z)
+        self._chk(self._L.ibmg_vcycle(self._h, bp, zp, k))
+        return z
+
+    def coarsest_solve(self, b):
+        x = _empty_like(b, self._size(self.num_levels - 1))
+        (bp, k), (xp, _) = _ptr(b), _ptr(x)
+        self._chk(self._L.ibmg_coarse_solve(self._h, bp, xp, k))
+        return x
+
+    def restrict_saddle(self, rf, level=0):
+        rc = _empty_like(rf, self._size(level + 1))
+        (fp, k), (cp, _) = _ptr(rf), _ptr(rc)
+        self._chk(self._L.ibmg_restrict(self._h, level, fp, cp, k))
+        return rc
+
+    def prolong_saddle_add(self, ec, wf, level=0):
+        (ep, k), (wp, _) = _ptr(ec), _ptr(wf)
+        self._chk(self._L.ibmg_prolong_add(self._h, level, ep, wp, k))
+        return wf
+
+    def big_blocks(self, level=0):
+        n = self.level_n(level)
+        f = np.zeros((n // 4) * (n // 4), np.int32)
+        cnt = self._L.ibmg_big_blocks(self._h, level, f.ctypes.data)
+        if cnt < 0:
+            raise ValueError("big_blocks: bad level")
+        return f.reshape(n // 4, n // 4)
+
+    def build_rhs(self, u_n):
+        b = _empty_like(u_n, 3 * self.N * self.N)
+        (up, k), (bp, _) = _ptr(u_n), _ptr(b)
+        self._chk(self._L.ibmg_build_rhs(self._h, up, bp, k))
+        return b
+
+    def interpolate(self, u):
+        U = _empty_like(u, 2 * self.npts)
+        (up, k), (Up, _) = _ptr(u), _ptr(U)
+        self._chk(self._L.ibmg_interpolate(self._h, up, Up, k))
+        return U
+
+    def spread(self, F):
+        f = _empty_like(F, 2 * self.N * self.N)
+        (Fp, k), (fp, _) = _ptr(F), _ptr(f)
+        self._chk(self._L.ibmg_spread(self._h, Fp, fp, k))
+        return f
+
+    def gmres_solve(self, b, x=None):
+        """FGMRES(restart) with one V-cycle right preconditioner; returns (x, stats)."""
+        x = _empty_like(b, self._size(0)) if x is None else x
+        st = Stats()
+        (bp, k), (xp, _) = _ptr(b), _ptr(x)
+        self._chk(self._L.ibmg_solve(self._h, bp, xp, C.byref(st), k), ok=(0, 2))
+        return x, st.as_dict()
+
+    def step_implicit(self, u, p, X):
+        """One backward-Euler implicit step in place on (u, p, X); returns stats."""
+        st = Stats()
+        (up, k), (pp, _), (Xp, _) = _ptr(u), _ptr(p), _ptr(X)
+        self._chk(self._L.ibmg_step(self._h, up, pp, Xp, C.byref(st), k), ok=(0, 2))
+        return st.as_dict()
+
+    @property
+    def kernel_launches(self):
+        return int(self._L.ibmg_kernel_launches(self._h))
+
+    @property
+    def stream(self):
+        return self._L.ibmg_stream(self._h)

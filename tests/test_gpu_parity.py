@@ -1,0 +1,130 @@
+"""GPU (C-ABI) vs CPU oracle parity on identical seeded inputs.
+
+Bars (BASELINE.json north_star): operators to round-off (1e-12 relative);
+solves/steps u, p, X^{n+1} within 1e-8 relative when both converge to 1e-10,
+FGMRES iteration counts within +2 of the oracle.
+"""
+import numpy as np
+import pytest
+
+from helpers import rand, rel
+from paper_1311_5614_b200 import configs
+from paper_1311_5614_b200.ibmg import SaddleSystem
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def pair(prob, **kw):
+    return SaddleSystem.from_problem(prob, **kw), O.Oracle(prob, threads=4)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return pair(configs.config1())
+
+
+def test_apply_all_levels(c1):
+    g, o = c1
+    for l in range(g.num_levels):
+        n = g.level_n(l)
+        w = rand(3 * n * n, seed=l)
+        assert rel(g.apply(w, level=l), o.apply(w, level=l)) < 1e-12, l
+
+
+def test_residual(c1):
+    g, o = c1
+    n = g.N
+    b, w = rand(3 * n * n, 1), rand(3 * n * n, 2)
+    r, nrm = g.residual(b, w)
+    ro = o.residual(b, w)
+    assert rel(r, ro) < 1e-12
+    assert abs(nrm - np.linalg.norm(ro)) < 1e-10 * np.linalg.norm(ro)
+
+
+def test_transfers(c1):
+    g, o = c1
+    n = g.N
+    rf = rand(3 * n * n, 3)
+    assert rel(g.restrict_saddle(rf), O.restrict(n, rf)) < 1e-14
+    ec = rand(3 * (n // 2) ** 2, 4)
+    wf = rand(3 * n * n, 5)
+    assert rel(g.prolong_saddle_add(ec, wf.copy()), O.prolong_add(n, ec, wf)) < 1e-14
+
+
+def test_big_blocks_match(c1):
+    g, o = c1
+    for l in range(g.num_levels - 1):
+        assert np.array_equal(g.big_blocks(l), o.big_blocks(l)), l
+
+
+def test_rhs_interp_spread(c1):
+    g, o = c1
+    prob = configs.config1()
+    n = prob.N
+    u = rand(2 * n * n, 6)
+    assert rel(g.build_rhs(u), o.rhs(u)) < 1e-13
+    assert rel(g.interpolate(u).reshape(-1, 2), o.interp(u)) < 1e-13
+    F = rand(2 * prob.npts, 7)
+    assert rel(g.spread(F), o.spread(F)) < 1e-13
+
+
+def test_sweep_level0(c1):
+    g, o = c1
+    n = g.N
+    b, w = rand(3 * n * n, 8), rand(3 * n * n, 9)
+    wg = g.sweep(b, w.copy())
+    wo = o.sweep(b, w)
+    assert rel(wg, wo) < 1e-11
+
+
+def test_coarse_solve(c1):
+    g, o = c1
+    nc = g.level_n(g.num_levels - 1)
+    b = rand(3 * nc * nc, 10)
+    b[2 * nc * nc:] -= b[2 * nc * nc:].mean()
+    assert rel(g.coarsest_solve(b), o.coarse_solve(b)) < 1e-11
+
+
+@pytest.mark.parametrize("N", [16, 32, 64])
+def test_vcycle(N):
+    prob = configs.small_problem(N=N, nb=2 * N, kappa=1e3)
+    g, o = pair(prob)
+    b = rand(3 * N * N, 11)
+    b[2 * N * N:] -= b[2 * N * N:].mean()
+    assert rel(g.v_cycle(b), o.vcycle(b)) < 1e-10
+
+
+def test_vcycle_deterministic(c1):
+    g, _ = c1
+    b = rand(3 * g.N * g.N, 12)
+    z1, z2 = g.v_cycle(b), g.v_cycle(b)
+    assert np.array_equal(z1, z2)
+
+
+def test_solve_c1(c1):
+    g, o = c1
+    prob = configs.config1()
+    u0 = np.zeros(2 * prob.N ** 2)
+    b = o.rhs(u0)
+    xg, sg = g.gmres_solve(b)
+    xo, so, _ = o.solve(b)
+    assert sg["converged"] and so["converged"]
+    assert sg["iters"] <= so["iters"] + 2
+    assert rel(xg, xo) < 1e-8
+
+
+def test_step_c1():
+    prob = configs.config1()
+    g, o = pair(prob)
+    n = prob.N
+    u = np.zeros(2 * n * n)
+    p = np.zeros(n * n)
+    X = prob.X.reshape(-1).copy()
+    sg = g.step_implicit(u, p, X)
+    uo, po, Xo, so = o.step(np.zeros(2 * n * n), prob.X)
+    assert sg["converged"] and so["converged"]
+    assert abs(sg["iters"] - so["iters"]) <= 2
+    assert rel(u, uo) < 1e-8
+    assert rel(p, po) < 1e-8
+    assert rel(X.reshape(-1, 2), Xo) < 1e-8
