@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py — implicit IB step solve time on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): periodic unit square, MAC grid
+N=256, fp64, rho = mu = 1, dt = 1e-3; one ellipse centred (0.5, 0.5), semi-axes
+0.3 / 0.15, Nb = 512 equal-arclength points, zero-rest-length springs with
+kappa in {1e2, 1e4, 1e6}; 10 consecutive backward-Euler steps per kappa from
+u = 0, each solved by FGMRES(30) preconditioned by one V(1,1) cycle (multicolour
+Vanka + big boxes, coarsening to 4x4) to relative residual 1e-10.
+
+A bench "step" is one implicit step of that 30-step sequence (step s uses kappa
+index (s // 10) % 3; the state resets at the start of each kappa block).
+  value  : device time per implicit step (ms), CUDA events on the solver's
+           stream, inputs resident in HBM, L2 flushed (256 MiB write) between
+           steps, max over ranks.
+  e2e    : the same steps through the C ABI with HOST numpy buffers (H2D of
+           u^n, X^n and D2H of u, p, X inside the timed region), wall clock.
+  roofline: live per-kernel CUDA-event timing (ibmg_profile) of the dominant
+           kernel in a separate profiled pass of the first step of each kappa.
+  cpu_baseline: the CPU oracle (oracle/, kind "port": the reference ships no
+           solver) on all host threads, 2 steps per kappa.
+--impl reference runs that oracle port on the same sequence (rank 0 only).
+Multi-GPU (torchrun): C2 does not shard; every rank runs an independent replica
+("replicas only"); scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "implicit IB step solve time (ms); fine-grid DOF·V-cycles/s vs HBM roofline"
+KAPPAS = [1e2, 1e4, 1e6]
+STEPS_PER_KAPPA = 10
+N_GRID = 256
+NB = 512
+
+THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def workload_config():
+    return {
+        "workload": "C2: periodic N=256 MAC grid fp64, ellipse (0.5,0.5) a=0.3 b=0.15, Nb=512, "
+                    "kappa {1e2,1e4,1e6} x 10 implicit steps, dt=1e-3, FGMRES(30)+V(1,1) box relaxation, rtol 1e-10",
+        "N": N_GRID, "Nb": NB, "kappas": KAPPAS, "steps_per_kappa": STEPS_PER_KAPPA, "dt": 1e-3,
+        "dof": 3 * N_GRID * N_GRID,
+        "l2": "flushed between timed steps (256 MiB write); working set ~100 MB",
+    }
+
+
+def step_schedule(total):
+    """(kappa index, reset?) for steps 0..total-1 of the repeating C2 sequence."""
+    out = []
+    for s in range(total):
+        kb = (s // STEPS_PER_KAPPA) % len(KAPPAS)
+        out.append((kb, s % STEPS_PER_KAPPA == 0))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self._p = None
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self._p:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=2)
+            except Exception:
+                self._p.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(s[0] for s in self.samples)
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        reasons = [name for bit, name in THROTTLE_BITS.items() if mask & bit and name != "gpu_idle"]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
+    """Algorithmic (compulsory fp64) bytes of all launches of `name` in the
+    profiled pass (SURVEY.md §8d per-cell figures x cells)."""
+    lv = ctxinfo["levels"]  # list of (n, nbig) for multi-tile levels (n > 32)
+    sweeps = 2  # V(1,1)
+    N = ctxinfo["N"]
+    if name == "k_plain_tiles":
+        return sum(72 * n * n * sweeps for n, _ in lv) * vcycles
+    if name == "k_big_sweep":
+        return sum((3136 * 8 + 56 * 24) * nb * sweeps for _, nb in lv) * vcycles
+    if name == "k_residual_restrict":
+        return sum(54 * n * n for n, _ in lv) * vcycles
+    if name == "k_prolong_add":
+        return sum(54 * n * n for n, _ in lv) * vcycles
+    if name == "k_stokes_apply":
+        return 48 * N * N * (fgmres_iters + restarts + 3)
+    return None
+
+
+def run_ours(args, rank, world):
+    import torch
+    from paper_1311_5614_b200 import configs
+    from paper_1311_5614_b200.ibmg import SaddleSystem
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    probs = [configs.config2(k, N=N_GRID, nb=NB) for k in KAPPAS]
+    ctxs = [SaddleSystem.from_problem(p, device=dev) for p in probs]
+    n2 = N_GRID * N_GRID
+    X0 = [torch.tensor(p.X.reshape(-1), dtype=torch.float64, device=f"cuda:{dev}") for p in probs]
+    u = torch.zeros(2 * n2, dtype=torch.float64, device=f"cuda:{dev}")
+    p = torch.zeros(n2, dtype=torch.float64, device=f"cuda:{dev}")
+    X = torch.empty_like(X0[0])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    streams = [torch.cuda.ExternalStream(c.stream, device=f"cuda:{dev}") for c in ctxs]
+
+    def run(total, timed):
+        nonlocal X
+        ms, iters, setup, restarts, conv = [], [], [], [], True
+        for kb, reset in step_schedule(total):
+            if reset:
+                u.zero_()
+                p.zero_()
+                X.copy_(X0[kb])
+            flush.zero_()
+            torch.cuda.synchronize()
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(streams[kb])
+            st = ctxs[kb].step_implicit(u, p, X)
+            if timed:
+                e1.record(streams[kb])
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            iters.append(st["iters"])
+            setup.append(st["setup_ms"])
+            restarts.append(st["restarts"])
+            conv = conv and bool(st["converged"])
+        return ms, iters, setup, restarts, conv
+
+    run(args.warmup, False)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = sum(c.kernel_launches for c in ctxs)
+    with ClockSampler(dev) as clk:
+        ms, iters, setup, restarts, conv = run(args.steps, True)
+    torch.cuda.synchronize()
+    launches = sum(c.kernel_launches for c in ctxs) - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = float(sum(ms))
+    vcyc = int(sum(iters))
+    t = torch.tensor([total_ms, float(vcyc)], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tsum = t.clone()
+        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
+        total_ms_max, vcyc_all = float(tmax[0]), float(tsum[1])
+    else:
+        total_ms_max, vcyc_all = total_ms, float(vcyc)
+
+    # e2e: same steps through the C ABI with host numpy buffers (copies inside)
+    e2e_ms = []
+    uh = np.zeros(2 * n2)
+    ph = np.zeros(n2)
+    Xh = None
+    for kb, reset in step_schedule(args.steps):
+        if reset:
+            uh[:] = 0.0
+            ph[:] = 0.0
+            Xh = probs[kb].X.reshape(-1).copy()
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctxs[kb].step_implicit(uh, ph, Xh)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    h2d = 8 * (2 * n2 + 2 * NB)
+    d2h = 8 * (2 * n2 + n2 + 2 * NB)
+
+    result = None
+    if rank == 0:
+        # profiled pass (live CUDA-event timing per kernel): first step of each kappa
+        prof_tot = {}
+        pv, pit, prs = 0, 0, 0
+        for kb in range(len(KAPPAS)):
+            u.zero_()
+            p.zero_()
+            X.copy_(X0[kb])
+            ctxs[kb].profile(True)
+            st = ctxs[kb].step_implicit(u, p, X)
+            rep = ctxs[kb].profile_report()
+            ctxs[kb].profile(False)
+            for k, (tms, cnt) in rep.items():
+                a = prof_tot.setdefault(k, [0.0, 0])
+                a[0] += tms
+                a[1] += cnt
+            pv += st["iters"]
+            pit += st["iters"]
+            prs += st["restarts"]
+        step_prof_ms = sum(v[0] for v in prof_tot.values())
+        ranked = sorted(prof_tot.items(), key=lambda kv: -kv[1][0])
+        levels = []
+        n = N_GRID
+        c0 = ctxs[0]
+        for l in range(c0.num_levels):
+            nl = c0.level_n(l)
+            if nl > 32:
+                levels.append((nl, None))
+        # big-block counts per level per kappa context (averaged)
+        lv_info = []
+        for l, (nl, _) in enumerate(levels):
+            nbig = np.mean([int(c.big_blocks(l).sum()) for c in ctxs])
+            lv_info.append((nl, nbig))
+        info = {"N": N_GRID, "levels": lv_info}
+        peak, peak_kind = measured_peak_hbm()
+        roof = None
+        for name, (tms, cnt) in ranked:
+            byts = kernel_algorithmic_bytes(name, info, pv, pit, prs)
+            if byts is None:
+                continue
+            avg_s = tms / cnt * 1e-3
+            ach = byts / cnt / avg_s / 1e9
+            roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
+                    "bytes_per_launch": byts / cnt, "avg_launch_us": round(avg_s * 1e6, 3),
+                    "share_of_step": round(tms / step_prof_ms, 4), "launches": cnt}
+            break
+        kernel_shares = {k: {"ms": round(v[0], 4), "launches": v[1], "share": round(v[0] / step_prof_ms, 4)}
+                         for k, v in ranked[:12]}
+        result = {
+            "total_ms_max": total_ms_max, "vcyc_all": vcyc_all, "ms": ms, "iters": iters, "setup": setup,
+            "launches": launches, "clocks": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h,
+            "roofline": roof, "kernels": kernel_shares, "converged": conv,
+        }
+    for c in ctxs:
+        c.close()
+    return result
+
+
+def cpu_oracle_steps(steps_sched, threads):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_1311_5614_b200 import configs
+    probs = [configs.config2(k, N=N_GRID, nb=NB) for k in KAPPAS]
+    ctxs = [O.Oracle(pr, threads=threads) for pr in probs]
+    ms, iters = [], []
+    u = X = None
+    for kb, reset in steps_sched:
+        if reset or u is None:
+            u = np.zeros(2 * N_GRID * N_GRID)
+            X = probs[kb].X.copy()
+        t0 = time.perf_counter()
+        u, p, X, st = ctxs[kb].step(u, X)
+        ms.append((time.perf_counter() - t0) * 1e3)
+        iters.append(st["iters"])
+    return ms, iters
+
+
+def cpu_baseline(threads):
+    sched = []
+    for kb in range(len(KAPPAS)):
+        sched += [(kb, True), (kb, False)]
+    ms, iters = cpu_oracle_steps(sched, threads)
+    return {"value": round(float(np.mean(ms)), 3), "unit": "ms", "cores": threads, "kind": "port",
+            "sample": f"first 2 implicit C2 steps of each kappa (6 steps, {sum(iters)} V-cycles) on the CPU oracle "
+                      f"(oracle/ibmg_oracle.cpp, OpenMP {threads} threads); ms per step"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    threads = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cpu_oracle_steps(step_schedule(args.warmup), threads)
+        ms, iters = cpu_oracle_steps(step_schedule(args.steps), threads)
+        v = float(np.mean(ms))
+        line = {"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 geometry)", "impl": "reference",
+                "config": dict(workload_config(), parallelism="CPU oracle port, OpenMP over independent boxes"),
+                "dof_vcycles_per_s": 3 * N_GRID ** 2 * sum(iters) / (sum(ms) * 1e-3),
+                "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "port",
+                                 "sample": f"{args.steps} C2 implicit steps ({sum(iters)} V-cycles) on the CPU oracle "
+                                           "(the reference ships no solver; SURVEY.md §0)"},
+                "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    res = run_ours(args, rank, world)
+    if rank == 0:
+        ms_step = res["total_ms_max"] / args.steps
+        dofv = 3 * N_GRID ** 2 * res["vcyc_all"] / (res["total_ms_max"] * 1e-3)
+        peak, _ = measured_peak_hbm()
+        line = {
+            "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 geometry, u0 = 0)",
+            "config": dict(workload_config(), parallelism=f"replicas x{world} (C2 does not shard)"),
+            "dof_vcycles_per_s": dofv,
+            "dof_vcycles_roofline_frac": dofv * 112 / (peak * 1e9 * world),
+            "vcycles_per_step": round(res["vcyc_all"] / world / args.steps, 2),
+            "setup_ms_mean": round(float(np.mean(res["setup"])), 4),
+            "converged": res["converged"],
+            "gpu_launches": res["launches"],
+            "clocks": res["clocks"],
+            "e2e": {"value": round(float(np.mean(res["e2e_ms"])), 4), "unit": "ms",
+                    "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},
+            "roofline": res["roofline"],
+            "kernels": res["kernels"],
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -90,6 +90,12 @@ int ibmg_coarse_solve(ibmg_ctx* ctx, const double* b, double* x, int ptr_kind);
 /* Big-block flags of a level ((n/4)^2 ints, host); returns the count or -1. */
 int ibmg_big_blocks(ibmg_ctx* ctx, int level, int* flags_host);
 
+/* Assembled E'_level (velocity block, E' = dt S K S^T Galerkin-coarsened) as host
+ * triplets: returns nnz (call with rows == NULL to size); the role of
+ * assemble_elasticity / galerkin_coarsen_elasticity's matrices
+ * (elasticity.cpp:88-107, transfers.cpp:286-293). */
+long ibmg_elasticity_triplets(ibmg_ctx* ctx, int level, int* rows, int* cols, double* vals, long cap);
+
 /* Replaces build_rhs (saddle.cpp:96-104): b = [(rho/dt) u^n + S F(X^n); 0]. */
 int ibmg_build_rhs(ibmg_ctx* ctx, const double* u_n, double* b, int ptr_kind);
 /* Replaces interpolate (fiber.cpp:116-140): U = S^T u (h^2 weights), 2*npts. */
@@ -107,6 +113,11 @@ int ibmg_step(ibmg_ctx* ctx, double* u, double* p, double* X, ibmg_stats* stats,
 
 /* Number of kernels this context has launched (evidence for bench's gpu_launches). */
 long long ibmg_kernel_launches(const ibmg_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (bench roofline evidence):
+ * enable=1 starts (and clears) the accumulation; report writes JSON
+ * {"kernel": [total_ms, launches], ...} and returns its length. */
+int ibmg_profile(ibmg_ctx* ctx, int enable);
+int ibmg_profile_report(ibmg_ctx* ctx, char* buf, int cap);
 /* The context's CUDA stream (cudaStream_t), for callers timing with events. */
 void* ibmg_stream(const ibmg_ctx* ctx);
 

@@ -17,6 +17,7 @@ struct CLev {
     Lev L;
     Win W;
     FaceList FL;
+    EMat E;
     const uint8_t* big;
     const int* blk_ids;
     const int* fidx;
@@ -27,8 +28,6 @@ struct CLev {
 struct CoarseArgs {
     int nl, nu1, nu2;
     CLev lv[6];
-    Pts P;
-    double* F;               // 2*npts scratch
     const double* Acoarse;   // bordered inverse, col-major (3nn+1)^2
     const double* b_in;
     double* w_out;
@@ -40,6 +39,10 @@ struct SW {
     __device__ __forceinline__ double& operator()(int f, int i, int j) const {
         return s[f * nn + wr(i, n) + wr(j, n) * n];
     }
+};
+struct FlatS {
+    const double* s;
+    __device__ __forceinline__ double operator()(int idx) const { return s[idx]; }
 };
 
 __device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, const double* b, double (*sr)[56]) {
@@ -82,8 +85,8 @@ __device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, cons
                 const int Bk = C.blk_ids[q];
                 bi = 4 * (Bk % nbk);
                 bj = 4 * (Bk / nbk);
-                sr[g][tt] =
-                    block_residual(L, C.W, A.P, C.FL, W, B, tt < 40 ? C.fidx[(size_t)q * 40 + tt] : -1, tt, bi, bj);
+                sr[g][tt] = block_residual(L, C.E, W, B, FlatS{w}, tt < 40 ? C.fidx[(size_t)q * 40 + tt] : -1, tt,
+                                           bi, bj);
             }
             __syncthreads();
             if (act) {
@@ -123,12 +126,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
         for (int q = t; q < 3 * nn; q += nt) wl[l][q] = 0.0;
         __syncthreads();
         for (int s = 0; s < A.nu1; ++s) coarse_sweep(A, C, wl[l], bl[l], sr);
-        // residual r = b - A w (stencil, then + E' w via point forces and face lists)
+        // residual r = b - A w (stencil, then + E' w from the assembled rows)
         SW W{wl[l], n, nn};
-        for (int k = t; k < A.P.n; k += nt) {
-            A.F[2 * k] = point_force(C.W, A.P, k, 0, n, W);
-            A.F[2 * k + 1] = point_force(C.W, A.P, k, 1, n, W);
-        }
         for (int q = t; q < nn; q += nt) {
             double ru, rv, rp;
             stokes_rows(L, W, q % n, q / n, ru, rv, rp);
@@ -136,17 +135,11 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
             r[nn + q] = bl[l][nn + q] - rv;
             r[2 * nn + q] = bl[l][2 * nn + q] - rp;
         }
-        __threadfence_block();
         __syncthreads();
         for (int fq = t; fq < C.FL.nf; fq += nt) {
-            const int face = C.FL.face[fq], comp = face >= nn;
             double s = 0.0;
-            for (int e = C.FL.off[fq]; e < C.FL.off[fq + 1]; ++e) {
-                const int v = C.FL.ent[e];
-                const int k = v >> 5;
-                s += C.W.w[(size_t)k * 64 + (v & 31)] * A.F[2 * k + comp];
-            }
-            r[face] += s;
+            for (int e = C.E.rp[fq]; e < C.E.rp[fq + 1]; ++e) s += C.E.val[e] * wl[l][C.E.col[e]];
+            r[C.FL.face[fq]] += s;
         }
         __syncthreads();
         // restrict into the next level's b

@@ -35,6 +35,17 @@ struct FaceList {
     int* ent = nullptr;  // entries: pt*32 + comp*16 + e (window slot of Lu/Lv)
 };
 
+// Assembled E'_l rows on the E-active faces of a level (row q <-> FaceList
+// face q): CSR with flat velocity column indices.  Built from the factored
+// windows (E'_l = sum_k L_k c_k (R_{k-1} - 2 R_k + R_{k+1})), i.e. the
+// reference's assembled Galerkin elasticity (elasticity.cpp:88-107,
+// transfers.cpp:286-293) restricted to its nonzero rows.
+struct EMat {
+    int* rp = nullptr;     // [nf+1]
+    int* col = nullptr;    // [nnz]
+    double* val = nullptr; // [nnz]
+};
+
 // Lagrangian point data.
 struct Pts {
     int n = 0;

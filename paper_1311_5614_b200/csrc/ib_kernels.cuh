@@ -227,6 +227,56 @@ __global__ void k_face_gather(FaceList FL, Win W, const double* __restrict__ F, 
     out[face] += sign * s;
 }
 
+// Assembly of E'_l rows, one warp per face-list row, accumulated in a 32x32
+// shared-memory patch of column offsets (slot = wr(col - row + 16, n)) in a
+// fixed order (entries ascending in point, windows k-1, k, k+1): deterministic.
+// pass 0 writes the row's nonzero count, pass 1 the (col, val) pairs.
+constexpr int kEWarps = 4;
+__global__ void __launch_bounds__(32 * kEWarps) k_erows(FaceList FL, Win W, Pts P, int n, int pass, EMat E,
+                                                         int* __restrict__ cnt) {
+    __shared__ double patch[kEWarps][1024];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = blockIdx.x * kEWarps + wid;
+    if (q >= FL.nf) return;
+    double* pt = patch[wid];
+    for (int s = lane; s < 1024; s += 32) pt[s] = 0.0;
+    __syncwarp();
+    const int nn = n * n, face = FL.face[q], comp = face >= nn;
+    const int f = face - comp * nn, di = f & (n - 1), dj = f / n;
+    for (int e = FL.off[q]; e < FL.off[q + 1]; ++e) {
+        const int v = FL.ent[e];
+        const int k = v >> 5;
+        const double lc = W.w[(size_t)k * 64 + (v & 31)] * P.cE[k];
+        const int ks[3] = {P.kprev[k], k, P.knext[k]};
+        const double coef[3] = {1.0, -2.0, 1.0};
+        for (int t = 0; t < 3; ++t) {
+            if (lane < 16) {
+                const int kk = ks[t];
+                const double r = W.w[(size_t)kk * 64 + (2 + comp) * 16 + lane];
+                if (r != 0.0) {
+                    const int4 o = W.orgR[kk];
+                    const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+                    const int sx = wr(i0 + (lane & 3) - di + 16, n), sy = wr(j0 + (lane >> 2) - dj + 16, n);
+                    pt[sy * 32 + sx] += lc * coef[t] * r;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    int base = pass ? E.rp[q] : 0;
+    for (int y = 0; y < 32; ++y) {
+        const double v = pt[y * 32 + lane];
+        const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
+        if (pass && v != 0.0) {
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            E.col[pos] = comp * nn + wr(di - 16 + lane, n) + wr(dj - 16 + y, n) * n;
+            E.val[pos] = v;
+        }
+        base += __popc(m);
+    }
+    if (!pass && lane == 0) cnt[q] = base;
+}
+
 // Fiber force density of the RHS times the spread quadrature:
 // F_k ds^2 = kappa (X_{k-1} + X_{k+1} - 2 X_k)/ds^2 * ds^2  (fiber.cpp:34-55, 93).
 __global__ void k_rhs_force(Pts P, const double* __restrict__ X, double* __restrict__ F) {

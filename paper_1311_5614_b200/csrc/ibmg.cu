@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -65,6 +66,9 @@ struct LevelBuf {
     Win W{};
     FaceList FL{};
     int fl_cap = 0;
+    EMat E{};
+    int* ecnt = nullptr;
+    long e_cap = 0;
     uint8_t* big = nullptr;
     int nbig = 0;
     int* blk_ids = nullptr;  // big blocks sorted by colour, ascending id within
@@ -105,15 +109,57 @@ struct ibmg_ctx {
     double* hpin = nullptr;    // pinned host mirror of dh
     size_t M = 0;              // 3 N^2
     bool have_structs = false;
+    // live per-kernel CUDA-event timing (bench roofline); off on the timed path
+    bool prof = false;
+    struct ProfRec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfRec> prof_pending;
+    std::vector<cudaEvent_t> ev_pool;
+    std::map<std::string, std::pair<double, long>> prof_acc;
 };
 
 namespace {
 
+cudaEvent_t prof_event(ibmg_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+}
+void prof_begin(ibmg_ctx* c, const char* name) {
+    ibmg_ctx::ProfRec r{name, prof_event(c), prof_event(c)};
+    CK(cudaEventRecord(r.a, c->s));
+    c->prof_pending.push_back(r);
+}
+void prof_end(ibmg_ctx* c) { CK(cudaEventRecord(c->prof_pending.back().b, c->s)); }
+void prof_collect(ibmg_ctx* c) {
+    CK(cudaStreamSynchronize(c->s));
+    for (auto& r : c->prof_pending) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        auto& acc = c->prof_acc[r.name];
+        acc.first += ms;
+        acc.second += 1;
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->prof_pending.clear();
+}
+
 #define LAUNCH(ctx, kern, grid, block, smem, ...)                          \
     do {                                                                   \
+        if ((ctx)->prof) prof_begin((ctx), #kern);                         \
         kern<<<(grid), (block), (smem), (ctx)->s>>>(__VA_ARGS__);          \
+        if ((ctx)->prof) prof_end((ctx));                                  \
         ++(ctx)->launches;                                                 \
         CK(cudaGetLastError());                                            \
+        if ((ctx)->prof && (ctx)->prof_pending.size() > 4096) prof_collect(ctx); \
     } while (0)
 
 Lev make_lev(const ibmg_params& p, int n) {
@@ -186,6 +232,11 @@ void free_structs(ibmg_ctx* c) {
         dfree(lb.FL.face);
         dfree(lb.FL.off);
         dfree(lb.FL.ent);
+        dfree(lb.E.rp);
+        dfree(lb.E.col);
+        dfree(lb.E.val);
+        dfree(lb.ecnt);
+        lb.e_cap = 0;
         lb.FL.nf = 0;
         lb.fl_cap = 0;
         dfree(lb.blk_ids);
@@ -312,6 +363,38 @@ void rebuild(ibmg_ctx* c) {
                 lb.nbig = lb.coff[16];
             }
         }
+        // assembled E'_l rows on the E-active faces (count, scan, fill)
+        for (int l = 0; l < c->nlev; ++l) {
+            LevelBuf& lb = c->lev[l];
+            if (lb.FL.nf == 0) continue;
+            CK(cudaMemsetAsync(lb.ecnt, 0, sizeof(int) * (lb.FL.nf + 1), c->s));
+            LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, 0, lb.E, lb.ecnt);
+            size_t bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, lb.ecnt, lb.E.rp, lb.FL.nf + 1, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, lb.ecnt, lb.E.rp, lb.FL.nf + 1, c->s));
+        }
+        {
+            std::vector<int> nnz(c->nlev, 0);
+            for (int l = 0; l < c->nlev; ++l)
+                if (c->lev[l].FL.nf)
+                    CK(cudaMemcpyAsync(&nnz[l], c->lev[l].E.rp + c->lev[l].FL.nf, sizeof(int), cudaMemcpyDeviceToHost,
+                                       c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int l = 0; l < c->nlev; ++l) {
+                LevelBuf& lb = c->lev[l];
+                if (lb.FL.nf == 0) continue;
+                if (nnz[l] > lb.e_cap) {
+                    dfree(lb.E.col);
+                    dfree(lb.E.val);
+                    lb.e_cap = std::max<long>(nnz[l], lb.e_cap * 5 / 4);
+                    lb.E.col = dalloc<int>(size_t(lb.e_cap));
+                    lb.E.val = dalloc<double>(size_t(lb.e_cap));
+                }
+                LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, 1, lb.E,
+                       lb.ecnt);
+            }
+        }
         // per-level big-block face indices and inverses
         for (int l = 0; l + 1 < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
@@ -324,14 +407,14 @@ void rebuild(ibmg_ctx* c) {
                 lb.fidx = dalloc<int>(size_t(lb.ainv_cap) * 40);
             }
             LAUNCH(c, k_block_fidx, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.FL, lb.blk_ids, lb.nbig, lb.fidx);
-            LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.W, c->P, lb.FL, lb.blk_ids,
-                   lb.fidx, lb.Ainv, c->err_flag);
+            LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.E, lb.blk_ids, lb.fidx,
+                   lb.Ainv, c->err_flag);
         }
     }
     {
         LevelBuf& lb = c->lev.back();
         const int m = 3 * lb.L.nn + 1;
-        LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * 2 * m * sizeof(double), lb.L, lb.W, c->P, lb.FL, c->Acoarse,
+        LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * 2 * m * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
                c->err_flag);
     }
     check_err_flag(c, "rebuild");
@@ -391,6 +474,8 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
         lb.FL.face = dalloc<int>(size_t(lb.fl_cap));
         lb.FL.off = dalloc<int>(size_t(lb.fl_cap) + 1);
         lb.FL.ent = dalloc<int>(size_t(lb.fl_cap));
+        lb.E.rp = dalloc<int>(size_t(lb.fl_cap) + 1);
+        lb.ecnt = dalloc<int>(size_t(lb.fl_cap) + 1);
     }
     size_t cap = std::max<size_t>(size_t(tot) * 32 + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
     c->keys = dalloc<int>(cap);
@@ -434,7 +519,7 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     for (int bc = 0; bc < 16; ++bc) {
         const int cnt = lb.coff[bc + 1] - lb.coff[bc];
         if (cnt == 0) continue;
-        LAUNCH(c, k_big_sweep, cnt, 64, 0, lb.L, lb.W, c->P, lb.FL, lb.blk_ids, lb.fidx, lb.Ainv, lb.coff[bc], b, w);
+        LAUNCH(c, k_big_sweep, cnt, 64, 0, lb.L, lb.E, lb.blk_ids, lb.fidx, lb.Ainv, lb.coff[bc], b, w);
     }
 }
 
@@ -449,14 +534,13 @@ CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
         C.L = lb.L;
         C.W = lb.W;
         C.FL = lb.FL;
+        C.E = lb.E;
         C.big = lb.big;
         C.blk_ids = lb.blk_ids;
         C.fidx = lb.fidx;
         C.Ainv = lb.Ainv;
         std::copy(lb.coff, lb.coff + 17, C.coff);
     }
-    A.P = c->P;
-    A.F = c->Fc;
     A.Acoarse = c->Acoarse;
     A.b_in = b_in;
     A.w_out = w_out;
@@ -722,6 +806,11 @@ void ibmg_destroy(ibmg_ctx* c) {
     dfree(c->Acoarse);
     if (c->cub_tmp) cudaFree(c->cub_tmp);
     if (c->hpin) cudaFreeHost(c->hpin);
+    for (auto& r : c->prof_pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->s) cudaStreamDestroy(c->s);
     delete c;
 }
@@ -730,6 +819,31 @@ const char* ibmg_last_error(const ibmg_ctx* c) { return c ? c->err.c_str() : "nu
 int ibmg_num_levels(const ibmg_ctx* c) { return c ? c->nlev : -1; }
 int ibmg_level_n(const ibmg_ctx* c, int l) { return (c && l >= 0 && l < c->nlev) ? c->lev[l].L.n : -1; }
 long long ibmg_kernel_launches(const ibmg_ctx* c) { return c ? c->launches : -1; }
+
+int ibmg_profile(ibmg_ctx* c, int enable) {
+    return api(c, [&]() -> int {
+        if (c->prof) prof_collect(c);
+        c->prof = enable != 0;
+        c->prof_acc.clear();
+        return IBMG_OK;
+    });
+}
+
+int ibmg_profile_report(ibmg_ctx* c, char* buf, int cap) {
+    return api(c, [&]() -> int {
+        prof_collect(c);
+        std::string js = "{";
+        for (auto& kv : c->prof_acc) {
+            if (js.size() > 1) js += ",";
+            char tmp[256];
+            std::snprintf(tmp, sizeof tmp, "\"%s\":[%.9g,%ld]", kv.first.c_str(), kv.second.first, kv.second.second);
+            js += tmp;
+        }
+        js += "}";
+        if (buf && cap > 0) std::snprintf(buf, size_t(cap), "%s", js.c_str());
+        return int(js.size());
+    });
+}
 void* ibmg_stream(const ibmg_ctx* c) { return c ? (void*)c->s : nullptr; }
 
 int ibmg_set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, const double* ds,
@@ -859,6 +973,29 @@ int ibmg_big_blocks(ibmg_ctx* c, int level, int* flags) {
         return cnt;
     } catch (const std::exception& e) {
         return fail(c, e, -1);
+    }
+}
+
+long ibmg_elasticity_triplets(ibmg_ctx* c, int level, int* rows, int* cols, double* vals, long cap) {
+    try {
+        if (!c || level < 0 || level >= c->nlev) return -1;
+        CK(cudaSetDevice(c->prm.device));
+        LevelBuf& lb = c->lev[level];
+        const int nf = lb.FL.nf;
+        if (nf == 0) return 0;
+        std::vector<int> rp(nf + 1), face(nf);
+        CK(cudaMemcpy(rp.data(), lb.E.rp, sizeof(int) * (nf + 1), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(face.data(), lb.FL.face, sizeof(int) * nf, cudaMemcpyDeviceToHost));
+        const long nnz = rp[nf];
+        if (!rows || cap < nnz) return nnz;
+        CK(cudaMemcpy(cols, lb.E.col, sizeof(int) * nnz, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals, lb.E.val, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+        for (int q = 0; q < nf; ++q)
+            for (int e = rp[q]; e < rp[q + 1]; ++e) rows[e] = face[q];
+        return nnz;
+    } catch (const std::exception& e) {
+        fail(c, e, -1);
+        return -1;
     }
 }
 

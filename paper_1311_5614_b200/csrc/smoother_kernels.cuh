@@ -42,6 +42,14 @@ __device__ __forceinline__ void plain_cell(const Lev& L, WA& W, const BA& B, int
     W(2, i, j) = pC + dp;
 }
 
+// Asynchronous global->shared copies (LDGSTS): the whole tile is in flight at
+// once instead of one load round trip per loop iteration.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ---- plain phase, multi-tile levels (n >= 32): one warp per 16x16 tile.
 constexpr int kTile = 16, kReg = kTile + 4;  // region with a 2-cell halo
 
@@ -68,18 +76,19 @@ __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double*
     for (int q = lane; q < kReg * kReg; q += 32) {
         const int a = q % kReg, bb = q / kReg;
         const size_t gi = wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-        sw[q] = w[gi];
-        sw[kReg * kReg + q] = w[nn + gi];
-        sw[2 * kReg * kReg + q] = w[2 * nn + gi];
+        cp_async8(&sw[q], w + gi);
+        cp_async8(&sw[kReg * kReg + q], w + nn + gi);
+        cp_async8(&sw[2 * kReg * kReg + q], w + 2 * nn + gi);
     }
     for (int q = lane; q < 289; q += 32) {
         const int a = q % 17, bb = q / 17;
         const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-        sb[q] = b[gi];
-        sb[289 + q] = b[nn + gi];
-        sb[578 + q] = b[2 * nn + gi];
+        cp_async8(&sb[q], b + gi);
+        cp_async8(&sb[289 + q], b + nn + gi);
+        cp_async8(&sb[578 + q], b + 2 * nn + gi);
     }
     if (lane < 16) sbig[lane] = big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
+    cp_async_wait_all();
     __syncwarp();
     TileW W{sw};
     TileB B{sb};
@@ -108,10 +117,11 @@ struct GAccRW {
 };
 
 // Residual of block DOF t (0..55) of the block at (bi, bj): b - A w including
-// the -E' part via the face lists (E' rows of DOF t) and on-the-fly point forces.
-template <class Acc, class BAcc>
-__device__ __forceinline__ double block_residual(const Lev& L, const Win& W, const Pts& P, const FaceList& FL,
-                                                 const Acc& acc, const BAcc& bacc, int fi, int t, int bi, int bj) {
+// the -E' part from the assembled rows (row fi of the level's EMat, -1 if the
+// face has no E' row).
+template <class Acc, class BAcc, class WAcc>
+__device__ __forceinline__ double block_residual(const Lev& L, const EMat& E, const Acc& acc, const BAcc& bacc,
+                                                 const WAcc& flat, int fi, int t, int bi, int bj) {
     int f, i, j;
     block_dof(t, bi, bj, f, i, j);
     i = wr(i, L.n);
@@ -119,20 +129,21 @@ __device__ __forceinline__ double block_residual(const Lev& L, const Win& W, con
     double ru, rv, rp;
     stokes_rows(L, acc, i, j, ru, rv, rp);
     double r = bacc(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
-    if (f < 2 && fi >= 0) {
+    if (fi >= 0) {
         double s = 0.0;
-        for (int e = FL.off[fi]; e < FL.off[fi + 1]; ++e) {
-            const int v = FL.ent[e];
-            const int k = v >> 5;
-            s += W.w[(size_t)k * 64 + (v & 31)] * point_force(W, P, k, f, L.n, acc);
-        }
+        for (int e = E.rp[fi]; e < E.rp[fi + 1]; ++e) s += E.val[e] * flat(E.col[e]);
         r += s;
     }
     return r;
 }
 
+struct FlatG {
+    const double* w;
+    __device__ __forceinline__ double operator()(int idx) const { return w[idx]; }
+};
+
 // Big phase, one colour: one 64-thread CTA per big block of the colour.
-__global__ void __launch_bounds__(64) k_big_sweep(Lev L, Win W, Pts P, FaceList FL, const int* __restrict__ blk_ids,
+__global__ void __launch_bounds__(64) k_big_sweep(Lev L, EMat E, const int* __restrict__ blk_ids,
                                                    const int* __restrict__ fidx, const double* __restrict__ Ainv,
                                                    int qbase, const double* __restrict__ b, double* w) {
     __shared__ double sr[56];
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(64) k_big_sweep(Lev L, Win W, Pts P, FaceList 
     const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
     GAccRW acc{w, L.n, L.nn};
     GAccRW bacc{b, L.n, L.nn};
-    if (t < 56) sr[t] = block_residual(L, W, P, FL, acc, bacc, t < 40 ? fidx[(size_t)q * 40 + t] : -1, t, bi, bj);
+    if (t < 56) sr[t] = block_residual(L, E, acc, bacc, FlatG{w}, t < 40 ? fidx[(size_t)q * 40 + t] : -1, t, bi, bj);
     __syncthreads();
     if (t < 56) {
         const double* A = Ainv + (size_t)q * 3136;
@@ -218,24 +229,10 @@ __device__ __forceinline__ void stokes_row_entries(const Lev& L, int field, Emit
     }
 }
 
-// E'(row face, col face) = sum_{(k,l) in list(row)} l c_k (R_{k-1} - 2 R_k + R_{k+1})(col).
-__device__ __forceinline__ double elastic_entry(const Win& W, const Pts& P, const FaceList& FL, int fi, int comp,
-                                                int n, int ic, int jc) {
-    double s = 0.0;
-    for (int e = FL.off[fi]; e < FL.off[fi + 1]; ++e) {
-        const int v = FL.ent[e];
-        const int k = v >> 5;
-        const double rr = win_at(W, P.kprev[k], 2 + comp, n, ic, jc) - 2.0 * win_at(W, k, 2 + comp, n, ic, jc) +
-                          win_at(W, P.knext[k], 2 + comp, n, ic, jc);
-        s += W.w[(size_t)k * 64 + (v & 31)] * (P.cE[k] * rr);
-    }
-    return s;
-}
-
 // One CTA per big block: assemble the 56x56 principal submatrix of A_l on the
 // block DOFs, invert it, store the inverse column-major.
-__global__ void k_block_inverse(Lev L, Win W, Pts P, FaceList FL, const int* __restrict__ blk_ids,
-                                const int* __restrict__ fidx, double* __restrict__ Ainv, int* err) {
+__global__ void k_block_inverse(Lev L, EMat E, const int* __restrict__ blk_ids, const int* __restrict__ fidx,
+                                double* __restrict__ Ainv, int* err) {
     extern __shared__ double M[];  // 56 x 112
     __shared__ double col[56];
     const int q = blockIdx.x, t = threadIdx.x, nt = blockDim.x, n = L.n;
@@ -256,15 +253,14 @@ __global__ void k_block_inverse(Lev L, Win W, Pts P, FaceList FL, const int* __r
         });
     }
     __syncthreads();
-    for (int idx = t; idx < 40 * 40; idx += nt) {
-        const int r = idx / 40, c = idx % 40;
-        const int comp = r >= 20;
-        if ((c >= 20) != comp) continue;
-        const int fi = fidx[(size_t)q * 40 + r];
-        if (fi < 0) continue;
-        int f, i, j;
-        block_dof(c, bi, bj, f, i, j);
-        M[r * 112 + c] -= elastic_entry(W, P, FL, fi, comp, n, wr(i, n), wr(j, n));
+    if (t < 40) {
+        const int fi = fidx[(size_t)q * 40 + t];
+        if (fi >= 0)
+            for (int e = E.rp[fi]; e < E.rp[fi + 1]; ++e) {
+                const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
+                const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
+                if (c >= 0) M[t * 112 + c] -= E.val[e];
+            }
     }
     __syncthreads();
     gauss_jordan(M, 56, col, err);
@@ -276,7 +272,7 @@ __global__ void k_block_inverse(Lev L, Win W, Pts P, FaceList FL, const int* __r
 
 // Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
 // pressure constraint), 49 x 49, inverted; stored col-major.
-__global__ void k_coarse_inverse(Lev L, Win W, Pts P, FaceList FL, double* __restrict__ Ainv, int* err) {
+__global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict__ Ainv, int* err) {
     extern __shared__ double M[];
     __shared__ double col[64];
     const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = 2 * m, t = threadIdx.x, nt = blockDim.x;
@@ -296,19 +292,9 @@ __global__ void k_coarse_inverse(Lev L, Win W, Pts P, FaceList FL, double* __res
         }
     }
     __syncthreads();
-    for (int idx = t; idx < 4 * nn * nn; idx += nt) {
-        const int r = idx / (2 * nn), c = idx % (2 * nn);
-        const int comp = r >= nn;
-        if ((c >= nn) != comp) continue;
-        // find row face r in the sorted face list
-        int lo = 0, hi = FL.nf;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (FL.face[mid] < r) lo = mid + 1; else hi = mid;
-        }
-        if (lo >= FL.nf || FL.face[lo] != r) continue;
-        const int cf = c % nn;
-        M[r * ld + c] -= elastic_entry(W, P, FL, lo, comp, n, cf % n, cf / n);
+    for (int q = t; q < FL.nf; q += nt) {
+        const int r = FL.face[q];
+        for (int e = E.rp[q]; e < E.rp[q + 1]; ++e) M[r * ld + E.col[e]] -= E.val[e];
     }
     __syncthreads();
     gauss_jordan(M, m, col, err);

@@ -44,7 +44,8 @@ class Stats(C.Structure):
 EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structures", "ibmg_num_levels",
            "ibmg_level_n", "ibmg_apply", "ibmg_residual", "ibmg_restrict", "ibmg_prolong_add", "ibmg_sweep",
            "ibmg_vcycle", "ibmg_coarse_solve", "ibmg_big_blocks", "ibmg_build_rhs", "ibmg_interpolate",
-           "ibmg_spread", "ibmg_solve", "ibmg_step", "ibmg_kernel_launches", "ibmg_stream"]
+           "ibmg_spread", "ibmg_solve", "ibmg_step", "ibmg_kernel_launches", "ibmg_stream", "ibmg_profile",
+           "ibmg_profile_report", "ibmg_elasticity_triplets"]
 
 
 def lib_path() -> str:
@@ -87,6 +88,10 @@ def lib(build_if_missing: bool = True):
     L.ibmg_kernel_launches.argtypes = [vp]
     L.ibmg_stream.restype = C.c_void_p
     L.ibmg_stream.argtypes = [vp]
+    L.ibmg_elasticity_triplets.restype = C.c_long
+    L.ibmg_elasticity_triplets.argtypes = [vp, ip, vp, vp, vp, C.c_long]
+    L.ibmg_profile.argtypes = [vp, ip]
+    L.ibmg_profile_report.argtypes = [vp, C.c_char_p, ip]
     _LIB = L
     return L
 
@@ -228,6 +233,18 @@ class SaddleSystem:
             raise ValueError("big_blocks: bad level")
         return f.reshape(n // 4, n // 4)
 
+    def elasticity(self, level=0):
+        """Assembled E'_level velocity block as (rows, cols, vals) host triplets."""
+        nnz = self._L.ibmg_elasticity_triplets(self._h, level, None, None, None, 0)
+        if nnz < 0:
+            raise ValueError("elasticity: bad level")
+        r = np.empty(nnz, np.int32)
+        c = np.empty(nnz, np.int32)
+        v = np.empty(nnz, np.float64)
+        if nnz:
+            self._L.ibmg_elasticity_triplets(self._h, level, r.ctypes.data, c.ctypes.data, v.ctypes.data, nnz)
+        return r, c, v
+
     def build_rhs(self, u_n):
         b = _empty_like(u_n, 3 * self.N * self.N)
         (up, k), (bp, _) = _ptr(u_n), _ptr(b)
@@ -264,6 +281,18 @@ class SaddleSystem:
     @property
     def kernel_launches(self):
         return int(self._L.ibmg_kernel_launches(self._h))
+
+    def profile(self, enable=True):
+        """Start (and clear) / stop live per-kernel CUDA-event timing."""
+        self._chk(self._L.ibmg_profile(self._h, int(enable)))
+
+    def profile_report(self):
+        """{kernel: (total_ms, launches)} accumulated since profile(True)."""
+        import json
+        n = self._L.ibmg_profile_report(self._h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        self._L.ibmg_profile_report(self._h, buf, n + 1)
+        return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
 
     @property
     def stream(self):

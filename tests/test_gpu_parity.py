@@ -52,6 +52,22 @@ def test_transfers(c1):
     assert rel(g.prolong_saddle_add(ec, wf.copy()), O.prolong_add(n, ec, wf)) < 1e-14
 
 
+def _dense(trip, m):
+    r, c, v = trip
+    D = np.zeros((m, m))
+    np.add.at(D, (r, c), v)
+    return D
+
+
+def test_elasticity_matrices(c1):
+    """GPU E'_l (factored windows -> assembled rows) == oracle R*E*P sparse products."""
+    g, o = c1
+    for l in range(g.num_levels):
+        n = g.level_n(l)
+        Dg, Do = _dense(g.elasticity(l), 2 * n * n), _dense(o.elasticity(l), 2 * n * n)
+        assert np.abs(Dg - Do).max() <= 1e-12 * np.abs(Do).max(), l
+
+
 def test_big_blocks_match(c1):
     g, o = c1
     for l in range(g.num_levels - 1):
