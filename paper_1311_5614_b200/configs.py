@@ -38,7 +38,7 @@ class Problem:
         return 3 * self.N * self.N
 
 
-def _arclength_series(a: float, b: float, modes: int = 256):
+def _arclength_series(a: float, b: float, modes: int = 64):
     """Fourier series of s'(t) = sqrt(a^2 sin^2 t + b^2 cos^2 t) (even, pi-periodic)."""
     m = 4 * modes
     t = 2 * np.pi * np.arange(m) / m
@@ -48,28 +48,25 @@ def _arclength_series(a: float, b: float, modes: int = 256):
 
 
 def ellipse_points(cx, cy, a, b, nb, theta0=0.0, rot=0.0):
-    """nb points at equal arclength on an ellipse (D5); returns (X (nb,2), ds, L)."""
+    """nb points at equal arclength on an ellipse (D5); returns (X (nb,2), ds, L).
+
+    The arclength s(t) = int_0^t sqrt(a^2 sin^2 + b^2 cos^2) is evaluated from
+    its Fourier series (spectrally accurate) and s(t_q) = q L / nb is solved by
+    vectorised Newton iteration to machine precision."""
     c = _arclength_series(a, b)
     k = np.arange(1, len(c))
     L = 2 * np.pi * c[0].real
-
-    def S(t):  # cumulative arclength from 0
-        return c[0].real * t + np.sum(2 * (c[1:] * (np.exp(1j * k * t) - 1) / (1j * k)).real)
-
-    def dS(t):
-        return math.sqrt((a * math.sin(t)) ** 2 + (b * math.cos(t)) ** 2)
-
-    th = np.empty(nb)
-    for q in range(nb):
-        target = q * L / nb
-        t = 2 * np.pi * q / nb
-        for _ in range(50):
-            f = S(t) - target
-            t -= f / dS(t)
-            if abs(f) < 1e-15 * max(1.0, L):
-                break
-        th[q] = t
-    th += theta0
+    target = np.arange(nb) * (L / nb)
+    t = 2 * np.pi * np.arange(nb) / nb
+    coef = 2 * c[1:] / (1j * k)
+    for _ in range(60):
+        e = np.exp(1j * np.outer(t, k))
+        S = c[0].real * t + ((e - 1.0) @ coef).real
+        f = S - target
+        t = t - f / np.sqrt((a * np.sin(t)) ** 2 + (b * np.cos(t)) ** 2)
+        if np.max(np.abs(f)) < 1e-15 * max(1.0, L):
+            break
+    th = t + theta0
     x = a * np.cos(th)
     y = b * np.sin(th)
     cr, sr = math.cos(rot), math.sin(rot)

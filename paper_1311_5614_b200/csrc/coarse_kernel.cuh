@@ -45,7 +45,7 @@ struct FlatS {
     __device__ __forceinline__ double operator()(int idx) const { return s[idx]; }
 };
 
-__device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, const double* b, double (*sr)[56]) {
+__device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, const double* b, BigScratch* sbig) {
     const Lev& L = C.L;
     const int n = L.n, t = threadIdx.x, nt = blockDim.x;
     SW W{w, n, L.nn};
@@ -74,37 +74,27 @@ __device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, cons
             }
             __syncthreads();
         }
-    const int g = t >> 6, tt = t & 63;
+    // big phase: 4 groups of 128 threads, each relaxing its own blocks of the
+    // colour (independent by the colouring), named barrier per group
+    const int g = t / kGroup, gt = t % kGroup;
+    FlatS flat{w};
     for (int bc = 0; bc < 16; ++bc) {
         const int cnt = C.coff[bc + 1] - C.coff[bc];
-        for (int ch = 0; ch < cnt; ch += nt / 64) {
-            const bool act = (ch + g) < cnt && tt < 56;
-            const int q = C.coff[bc] + ch + g;
-            int bi = 0, bj = 0;
-            if (act) {
-                const int Bk = C.blk_ids[q];
-                bi = 4 * (Bk % nbk);
-                bj = 4 * (Bk / nbk);
-                sr[g][tt] = block_residual(L, C.E, W, B, FlatS{w}, tt < 40 ? C.fidx[(size_t)q * 40 + tt] : -1, tt,
-                                           bi, bj);
-            }
-            __syncthreads();
-            if (act) {
-                const double* Ai = C.Ainv + (size_t)q * 3136;
-                double s = 0.0;
-                for (int c = 0; c < 56; ++c) s += Ai[c * 56 + tt] * sr[g][c];
-                int f, i, j;
-                block_dof(tt, bi, bj, f, i, j);
-                W(f, i, j) += s;
-            }
-            __syncthreads();
+        if (cnt == 0) continue;
+        for (int qq = g; qq < cnt; qq += nt / kGroup) {
+            const int q = C.coff[bc] + qq;
+            const int Bk = C.blk_ids[q];
+            big_block_group(L, C.E, C.fidx + (size_t)q * 40, C.Ainv + (size_t)q * 3136, 4 * (Bk % nbk),
+                            4 * (Bk / nbk), W, flat, B, [&](int f, int i, int j, double d) { W(f, i, j) += d; },
+                            sbig[g], gt, [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); });
         }
+        __syncthreads();
     }
 }
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
     extern __shared__ double sm[];
-    __shared__ double sr[kCoarseThreads / 64][56];
+    __shared__ BigScratch sr[kCoarseThreads / kGroup];
     double* wl[6];
     double* bl[6];
     size_t off = 0;

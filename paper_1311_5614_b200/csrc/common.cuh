@@ -14,6 +14,8 @@ namespace ibmg {
 struct Lev {
     int n, nn, lg;   // cells per side, n*n, log2(n)
     double h, d, c, g;
+    // closed-form 5x5 Vanka constants: 1/(d+c), 1/(d-c), (d+c)/g, 1/(4g)
+    double idpc, idmc, dpc_g, i4g;
 };
 
 // Per-level Lagrangian windows: for every point four 4x4

@@ -172,6 +172,10 @@ Lev make_lev(const ibmg_params& p, int n) {
     L.c = p.mu / (L.h * L.h);
     L.d = p.rho / p.dt + 4.0 * L.c;
     L.g = 1.0 / L.h;
+    L.idpc = 1.0 / (L.d + L.c);
+    L.idmc = 1.0 / (L.d - L.c);
+    L.dpc_g = (L.d + L.c) / L.g;
+    L.i4g = 1.0 / (4.0 * L.g);
     return L;
 }
 
@@ -519,7 +523,7 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     for (int bc = 0; bc < 16; ++bc) {
         const int cnt = lb.coff[bc + 1] - lb.coff[bc];
         if (cnt == 0) continue;
-        LAUNCH(c, k_big_sweep, cnt, 64, 0, lb.L, lb.E, lb.blk_ids, lb.fidx, lb.Ainv, lb.coff[bc], b, w);
+        LAUNCH(c, k_big_sweep, cnt, kGroup, 0, lb.L, lb.E, lb.blk_ids, lb.fidx, lb.Ainv, lb.coff[bc], b, w);
     }
 }
 

@@ -30,11 +30,10 @@ __device__ __forceinline__ void plain_cell(const Lev& L, WA& W, const BA& B, int
                         (d * vN - c * (vS + W(1, i, j + 2) + W(1, i - 1, j + 1) + W(1, i + 1, j + 1)) +
                          g * (W(2, i, j + 1) - pC));
     const double r_p = B(2, i, j) - (-g * (uE - uW) - g * (vN - vS));
-    const double dpc = d + c, dmc = d - c;
-    const double dp = ((r_uW - r_uE + r_vS - r_vN) - dpc * r_p / g) / (4.0 * g);
-    const double s = (r_uW - r_uE - 2.0 * g * dp) / dpc;
-    const double t = (r_vS - r_vN - 2.0 * g * dp) / dpc;
-    const double a = (r_uW + r_uE) / dmc, e = (r_vS + r_vN) / dmc;
+    const double dp = ((r_uW - r_uE + r_vS - r_vN) - L.dpc_g * r_p) * L.i4g;
+    const double s = (r_uW - r_uE - 2.0 * g * dp) * L.idpc;
+    const double t = (r_vS - r_vN - 2.0 * g * dp) * L.idpc;
+    const double a = (r_uW + r_uE) * L.idmc, e = (r_vS + r_vN) * L.idmc;
     W(0, i, j) = uW + 0.5 * (a + s);
     W(0, i + 1, j) = uE + 0.5 * (a - s);
     W(1, i, j) = vS + 0.5 * (e + t);
@@ -142,27 +141,105 @@ struct FlatG {
     __device__ __forceinline__ double operator()(int idx) const { return w[idx]; }
 };
 
-// Big phase, one colour: one 64-thread CTA per big block of the colour.
-__global__ void __launch_bounds__(64) k_big_sweep(Lev L, EMat E, const int* __restrict__ blk_ids,
-                                                   const int* __restrict__ fidx, const double* __restrict__ Ainv,
-                                                   int qbase, const double* __restrict__ b, double* w) {
-    __shared__ double sr[56];
-    const int q = qbase + blockIdx.x, t = threadIdx.x;
+// One big-block relaxation by a group of 128 threads (4 warps).  Latency
+// structure (the routine is a handful of dependent memory rounds):
+//  (1) Stokes residual of the 56 DOFs and, in parallel, the E' row dots of the
+//      40 velocity DOFs (warp per row, lanes over nonzeros; all (col, val)
+//      loads of 5 rows issued before the dependent w gathers);
+//  (2) the 56x56 inverse applied by 112 threads (2 column halves, loads
+//      prefetched 14 at a time), reduced in a fixed order (deterministic).
+// `gsync` is the group barrier (__syncthreads or a named barrier).
+constexpr int kGroup = 128;
+struct BigScratch {
+    double sr[56], se[40], part[2][56];
+};
+
+template <class Acc, class Flat, class BAcc, class WAdd, class Sync>
+__device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, const int* __restrict__ fidx_q,
+                                                const double* __restrict__ A_q, int bi, int bj, const Acc& acc,
+                                                const Flat& flat, const BAcc& bacc, WAdd&& wadd, BigScratch& S,
+                                                int gt, Sync&& gsync) {
+    const int wid = gt >> 5, lane = gt & 31;
+    if (gt < 56) {
+        int f, i, j;
+        block_dof(gt, bi, bj, f, i, j);
+        i = wr(i, L.n);
+        j = wr(j, L.n);
+        double ru, rv, rp;
+        stokes_rows(L, acc, i, j, ru, rv, rp);
+        S.sr[gt] = bacc(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        int beg[5], end[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const int fi = fidx_q[wid + 4 * (5 * half + k)];
+            beg[k] = fi >= 0 ? E.rp[fi] : 0;
+            end[k] = fi >= 0 ? E.rp[fi + 1] : 0;
+        }
+        int cl[5][2];
+        double vl[5][2];
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = beg[k] + lane + 32 * h;
+                const bool ok = e < end[k];
+                cl[k][h] = ok ? E.col[e] : 0;
+                vl[k][h] = ok ? E.val[e] : 0.0;
+            }
+        double ps[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) ps[k] = vl[k][0] * flat(cl[k][0]) + vl[k][1] * flat(cl[k][1]);
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+            for (int e = beg[k] + lane + 64; e < end[k]; e += 32) ps[k] += E.val[e] * flat(E.col[e]);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const double v = warp_sum(ps[k]);
+            if (lane == 0) S.se[wid + 4 * (5 * half + k)] = v;
+        }
+    }
+    gsync();
+    if (gt < 112) {
+        const int row = gt % 56, g = gt / 56;
+        const double* A = A_q + (size_t)(28 * g) * 56 + row;
+        double s = 0.0;
+#pragma unroll
+        for (int c0 = 0; c0 < 28; c0 += 14) {
+            double av[14];
+#pragma unroll
+            for (int c = 0; c < 14; ++c) av[c] = A[(c0 + c) * 56];
+#pragma unroll
+            for (int c = 0; c < 14; ++c) {
+                const int cc = 28 * g + c0 + c;
+                s += av[c] * (cc < 40 ? S.sr[cc] + S.se[cc] : S.sr[cc]);
+            }
+        }
+        S.part[g][row] = s;
+    }
+    gsync();
+    if (gt < 56) {
+        int f, i, j;
+        block_dof(gt, bi, bj, f, i, j);
+        wadd(f, wr(i, L.n), wr(j, L.n), S.part[0][gt] + S.part[1][gt]);
+    }
+}
+
+// Big phase, one colour: one 128-thread CTA per big block of the colour.
+__global__ void __launch_bounds__(kGroup) k_big_sweep(Lev L, EMat E, const int* __restrict__ blk_ids,
+                                                       const int* __restrict__ fidx, const double* __restrict__ Ainv,
+                                                       int qbase, const double* __restrict__ b, double* w) {
+    __shared__ BigScratch S;
+    const int q = qbase + blockIdx.x;
     const int B = blk_ids[q], nbk = L.n >> 2;
-    const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
     GAccRW acc{w, L.n, L.nn};
     GAccRW bacc{b, L.n, L.nn};
-    if (t < 56) sr[t] = block_residual(L, E, acc, bacc, FlatG{w}, t < 40 ? fidx[(size_t)q * 40 + t] : -1, t, bi, bj);
-    __syncthreads();
-    if (t < 56) {
-        const double* A = Ainv + (size_t)q * 3136;
-        double s = 0.0;
-#pragma unroll 8
-        for (int c = 0; c < 56; ++c) s += A[c * 56 + t] * sr[c];
-        int f, i, j;
-        block_dof(t, bi, bj, f, i, j);
-        w[(size_t)f * L.nn + wr(i, L.n) + (size_t)wr(j, L.n) * L.n] += s;
-    }
+    big_block_group(L, E, fidx + (size_t)q * 40, Ainv + (size_t)q * 3136, 4 * (B % nbk), 4 * (B / nbk), acc,
+                    FlatG{w}, bacc,
+                    [&](int f, int i, int j, double d) { w[(size_t)f * L.nn + i + (size_t)j * L.n] += d; }, S,
+                    threadIdx.x, [] { __syncthreads(); });
 }
 
 // ---- setup: dense local matrices and their inverses --------------------------
