@@ -424,13 +424,19 @@ void extract(const Csr& A, const int* d, int m, DenseLu& lu) {
 // Fixed multicolour schedule.  Plain phase: 16x16-cell
 // tiles coloured 2x2 (one tile, periodic, when n <= 16); inside each tile the
 // 8 conflict-free colours (i + 2j) mod 8 of local coordinates over cells
-// outside big blocks.  Big phase: the level-wide 16 colours (bx mod 4,
-// by mod 4) of the big 4x4 blocks (12-cell gap between same-colour blocks,
-// larger than the E' reach checked at setup).  Boxes within one pass are
-// mutually independent, so each pass is exactly a Gauss-Seidel pass in any
-// order (SPEC.md:427-431 semantics) and the GPU may run it in parallel.
+// outside big blocks.  Big 4x4 blocks:
+//  * levels with n >= 64 (multi-tile GPU kernel): inside each tile, right after
+//    its plain colours, the tile's big blocks one at a time in local block
+//    order (bx + 4 by).  Same-colour tiles are 16 cells apart, beyond the E'
+//    reach (<= 12, checked at setup), so tiles of one colour are independent;
+//  * levels with n <= 32 (single-CTA coarse kernel): after all plain passes,
+//    the level-wide 16 colours (bx mod 4, by mod 4) (12-cell gap).
+// Boxes within one pass are mutually independent, so each pass is exactly a
+// Gauss-Seidel pass in any order (SPEC.md:427-431 semantics) and the GPU may
+// run it in parallel.
 void build_schedule(Level& L) {
-    const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4;
+    const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4, tb = T / 4;
+    const bool tile_local_big = n >= 64;
     L.passes.clear();
     const int ntc = nt >= 2 ? 4 : 1;
     for (int tc = 0; tc < ntc; ++tc) {
@@ -447,7 +453,20 @@ void build_schedule(Level& L) {
                 }
             if (!p.items.empty()) L.passes.push_back(std::move(p));
         }
+        if (!tile_local_big) continue;
+        for (int lb = 0; lb < tb * tb; ++lb) {
+            Pass p;
+            p.big = true;
+            for (int by = 0; by < nbk; ++by)
+                for (int bx = 0; bx < nbk; ++bx) {
+                    if (!L.big[bx + by * nbk] || !tile_ok(bx / tb, by / tb)) continue;
+                    if ((bx % tb) + tb * (by % tb) != lb) continue;
+                    p.items.push_back(bx + by * nbk);
+                }
+            if (!p.items.empty()) L.passes.push_back(std::move(p));
+        }
     }
+    if (tile_local_big) return;
     for (int bc = 0; bc < 16; ++bc) {
         Pass p;
         p.big = true;

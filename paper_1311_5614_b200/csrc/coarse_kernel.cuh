@@ -20,7 +20,7 @@ struct CLev {
     EMat E;
     const uint8_t* big;
     const int* blk_ids;
-    const int* fidx;
+    const int2* rr;
     const double* Ainv;
     int coff[17];
 };
@@ -84,7 +84,7 @@ __device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, cons
         for (int qq = g; qq < cnt; qq += nt / kGroup) {
             const int q = C.coff[bc] + qq;
             const int Bk = C.blk_ids[q];
-            big_block_group(L, C.E, C.fidx + (size_t)q * 40, C.Ainv + (size_t)q * 3136, 4 * (Bk % nbk),
+            big_block_group(L, C.E, C.rr + (size_t)q * 40, C.Ainv + (size_t)q * 3136, 4 * (Bk % nbk),
                             4 * (Bk / nbk), W, flat, B, [&](int f, int i, int j, double d) { W(f, i, j) += d; },
                             sbig[g], gt, [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); });
         }

@@ -74,7 +74,8 @@ struct LevelBuf {
     int* blk_ids = nullptr;  // big blocks sorted by colour, ascending id within
     int blk_cap = 0;
     int coff[17] = {0};
-    int* fidx = nullptr;
+    int2* rr = nullptr;
+    int* bq = nullptr;
     double* Ainv = nullptr;
     int ainv_cap = 0;
 };
@@ -196,13 +197,17 @@ void alloc_levels(ibmg_ctx* c) {
         lb.w = dalloc<double>(m);
         lb.b = dalloc<double>(m);
         lb.r = dalloc<double>(m);
-        if (n > p.coarsest_n) lb.big = dalloc<uint8_t>(size_t(n / 4) * (n / 4));
+        if (n > p.coarsest_n) {
+            lb.big = dalloc<uint8_t>(size_t(n / 4) * (n / 4));
+            lb.bq = dalloc<int>(size_t(n / 4) * (n / 4));
+        }
         c->lev.push_back(lb);
         if (n <= p.coarsest_n) break;
     }
     c->nlev = int(c->lev.size());
     c->lc = 0;
     while (c->lev[c->lc].L.n > kCoarseMaxN) ++c->lc;
+    static_assert(kCoarseMaxN * 2 == 4 * kTile, "multi-tile levels (tile-local big phase) are exactly n >= 64");
     if (c->nlev - c->lc > 6) throw InvalidArg("too many coarse-kernel levels");
     c->M = 3 * size_t(p.N) * p.N;
     const int m = p.restart;
@@ -244,7 +249,7 @@ void free_structs(ibmg_ctx* c) {
         lb.FL.nf = 0;
         lb.fl_cap = 0;
         dfree(lb.blk_ids);
-        dfree(lb.fidx);
+        dfree(lb.rr);
         dfree(lb.Ainv);
         lb.blk_cap = lb.ainv_cap = 0;
         lb.nbig = 0;
@@ -405,13 +410,14 @@ void rebuild(ibmg_ctx* c) {
             if (lb.nbig == 0) continue;
             if (lb.ainv_cap < lb.nbig) {
                 dfree(lb.Ainv);
-                dfree(lb.fidx);
+                dfree(lb.rr);
                 lb.ainv_cap = std::max(lb.nbig, lb.ainv_cap * 5 / 4);
                 lb.Ainv = dalloc<double>(size_t(lb.ainv_cap) * 3136);
-                lb.fidx = dalloc<int>(size_t(lb.ainv_cap) * 40);
+                lb.rr = dalloc<int2>(size_t(lb.ainv_cap) * 40);
             }
-            LAUNCH(c, k_block_fidx, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.FL, lb.blk_ids, lb.nbig, lb.fidx);
-            LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.E, lb.blk_ids, lb.fidx,
+            LAUNCH(c, k_block_rows, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.FL, lb.E, lb.blk_ids, lb.nbig, lb.rr,
+                   lb.bq);
+            LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.E, lb.blk_ids, lb.rr,
                    lb.Ainv, c->err_flag);
         }
     }
@@ -517,14 +523,10 @@ void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double
 void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     LevelBuf& lb = c->lev[l];
     const int n = lb.L.n;
-    if (n < 2 * kTile) throw InvalidArg("multi-tile sweep needs n >= 32");
+    if (n < 4 * kTile) throw InvalidArg("multi-tile sweep needs n >= 64");
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
-    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
-    for (int bc = 0; bc < 16; ++bc) {
-        const int cnt = lb.coff[bc + 1] - lb.coff[bc];
-        if (cnt == 0) continue;
-        LAUNCH(c, k_big_sweep, cnt, kGroup, 0, lb.L, lb.E, lb.blk_ids, lb.fidx, lb.Ainv, lb.coff[bc], b, w);
-    }
+    for (int tc = 0; tc < 4; ++tc)
+        LAUNCH(c, k_tile_sweep, per, kTileThreads, 0, lb.L, tc, b, w, lb.big, lb.bq, lb.E, lb.rr, lb.Ainv);
 }
 
 CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
@@ -541,7 +543,7 @@ CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
         C.E = lb.E;
         C.big = lb.big;
         C.blk_ids = lb.blk_ids;
-        C.fidx = lb.fidx;
+        C.rr = lb.rr;
         C.Ainv = lb.Ainv;
         std::copy(lb.coff, lb.coff + 17, C.coff);
     }
@@ -793,6 +795,7 @@ void ibmg_destroy(ibmg_ctx* c) {
         dfree(lb.b);
         dfree(lb.r);
         dfree(lb.big);
+        dfree(lb.bq);
     }
     dfree(c->V);
     dfree(c->Z);

@@ -155,11 +155,19 @@ struct BigScratch {
 };
 
 template <class Acc, class Flat, class BAcc, class WAdd, class Sync>
-__device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, const int* __restrict__ fidx_q,
+__device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, const int2* __restrict__ rr_q,
                                                 const double* __restrict__ A_q, int bi, int bj, const Acc& acc,
                                                 const Flat& flat, const BAcc& bacc, WAdd&& wadd, BigScratch& S,
                                                 int gt, Sync&& gsync) {
     const int wid = gt >> 5, lane = gt & 31;
+    // inverse columns of this thread, issued first (independent of w)
+    double av[28];
+    const int row = gt % 56, cg = gt / 56;
+    if (gt < 112) {
+        const double* A = A_q + (size_t)(28 * cg) * 56 + row;
+#pragma unroll
+        for (int c = 0; c < 28; ++c) av[c] = A[c * 56];
+    }
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
@@ -174,9 +182,9 @@ __device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, con
         int beg[5], end[5];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            const int fi = fidx_q[wid + 4 * (5 * half + k)];
-            beg[k] = fi >= 0 ? E.rp[fi] : 0;
-            end[k] = fi >= 0 ? E.rp[fi + 1] : 0;
+            const int2 r = rr_q[wid + 4 * (5 * half + k)];
+            beg[k] = r.x;
+            end[k] = r.y;
         }
         int cl[5][2];
         double vl[5][2];
@@ -186,12 +194,13 @@ __device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, con
             for (int h = 0; h < 2; ++h) {
                 const int e = beg[k] + lane + 32 * h;
                 const bool ok = e < end[k];
-                cl[k][h] = ok ? E.col[e] : 0;
+                cl[k][h] = ok ? E.col[e] : -1;
                 vl[k][h] = ok ? E.val[e] : 0.0;
             }
         double ps[5];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) ps[k] = vl[k][0] * flat(cl[k][0]) + vl[k][1] * flat(cl[k][1]);
+        for (int k = 0; k < 5; ++k)
+            ps[k] = (cl[k][0] >= 0 ? vl[k][0] * flat(cl[k][0]) : 0.0) + (cl[k][1] >= 0 ? vl[k][1] * flat(cl[k][1]) : 0.0);
 #pragma unroll
         for (int k = 0; k < 5; ++k)
             for (int e = beg[k] + lane + 64; e < end[k]; e += 32) ps[k] += E.val[e] * flat(E.col[e]);
@@ -203,43 +212,116 @@ __device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, con
     }
     gsync();
     if (gt < 112) {
-        const int row = gt % 56, g = gt / 56;
-        const double* A = A_q + (size_t)(28 * g) * 56 + row;
         double s = 0.0;
 #pragma unroll
-        for (int c0 = 0; c0 < 28; c0 += 14) {
-            double av[14];
-#pragma unroll
-            for (int c = 0; c < 14; ++c) av[c] = A[(c0 + c) * 56];
-#pragma unroll
-            for (int c = 0; c < 14; ++c) {
-                const int cc = 28 * g + c0 + c;
-                s += av[c] * (cc < 40 ? S.sr[cc] + S.se[cc] : S.sr[cc]);
-            }
+        for (int c = 0; c < 28; ++c) {
+            const int cc = 28 * cg + c;
+            s += av[c] * (cc < 40 ? S.sr[cc] + S.se[cc] : S.sr[cc]);
         }
-        S.part[g][row] = s;
+        S.part[cg][row] = s;
     }
     gsync();
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
-        wadd(f, wr(i, L.n), wr(j, L.n), S.part[0][gt] + S.part[1][gt]);
+        wadd(f, i, j, S.part[0][gt] + S.part[1][gt]);
     }
 }
 
-// Big phase, one colour: one 128-thread CTA per big block of the colour.
-__global__ void __launch_bounds__(kGroup) k_big_sweep(Lev L, EMat E, const int* __restrict__ blk_ids,
-                                                       const int* __restrict__ fidx, const double* __restrict__ Ainv,
-                                                       int qbase, const double* __restrict__ b, double* w) {
+// One sweep phase of a multi-tile level (n >= 64): one 128-thread CTA per tile
+// of tile colour tc.  The 20x20 region (2-cell halo) of w and the tile's b are
+// staged in shared memory with cp.async; warp 0 runs the 8 plain colour
+// passes; then the whole CTA relaxes the tile's big blocks one by one in local
+// order (tile-local big phase); the write set goes back once.
+struct TileFlat {  // flat velocity index -> shared region if inside, else global
+    const double* s;
+    const double* g;
+    int n, nn, x0, y0;
+    __device__ __forceinline__ double operator()(int idx) const {
+        const int comp = idx >= nn, f = idx - comp * nn;
+        const int li = wr((f & (n - 1)) - x0 + 2, n), lj = wr(f / n - y0 + 2, n);
+        if (li < kReg && lj < kReg) return s[comp * kReg * kReg + lj * kReg + li];
+        return g[idx];
+    }
+};
+struct TileGW {  // wrapped global coords -> shared region (all stencil reads are inside)
+    double* s;
+    int n, x0, y0;
+    __device__ __forceinline__ double& operator()(int f, int i, int j) const {
+        return s[f * kReg * kReg + wr(j - y0 + 2, n) * kReg + wr(i - x0 + 2, n)];
+    }
+};
+struct TileGB {
+    const double* s;
+    int n, x0, y0;
+    __device__ __forceinline__ double operator()(int f, int i, int j) const {
+        return s[f * 289 + wr(j - y0, n) * 17 + wr(i - x0, n)];
+    }
+};
+
+constexpr int kTileThreads = 128;
+__global__ void __launch_bounds__(kTileThreads) k_tile_sweep(Lev L, int tc, const double* __restrict__ b,
+                                                              double* __restrict__ w, const uint8_t* __restrict__ big,
+                                                              const int* __restrict__ bq, EMat E,
+                                                              const int2* __restrict__ rr,
+                                                              const double* __restrict__ Ainv) {
+    __shared__ double sw[3 * kReg * kReg];
+    __shared__ double sb[3 * 289];
+    __shared__ int sq[16];
     __shared__ BigScratch S;
-    const int q = qbase + blockIdx.x;
-    const int B = blk_ids[q], nbk = L.n >> 2;
-    GAccRW acc{w, L.n, L.nn};
-    GAccRW bacc{b, L.n, L.nn};
-    big_block_group(L, E, fidx + (size_t)q * 40, Ainv + (size_t)q * 3136, 4 * (B % nbk), 4 * (B / nbk), acc,
-                    FlatG{w}, bacc,
-                    [&](int f, int i, int j, double d) { w[(size_t)f * L.nn + i + (size_t)j * L.n] += d; }, S,
-                    threadIdx.x, [] { __syncthreads(); });
+    const int n = L.n, nn = L.nn, t = threadIdx.x;
+    const int half = (n / kTile) >> 1;
+    const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = 2 * (blockIdx.x / half) + (tc >> 1);
+    const int x0 = tx * kTile, y0 = ty * kTile, nbk = n >> 2;
+    for (int q = t; q < kReg * kReg; q += kTileThreads) {
+        const int a = q % kReg, bb = q / kReg;
+        const size_t gi = wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n;
+        cp_async8(&sw[q], w + gi);
+        cp_async8(&sw[kReg * kReg + q], w + nn + gi);
+        cp_async8(&sw[2 * kReg * kReg + q], w + 2 * nn + gi);
+    }
+    for (int q = t; q < 289; q += kTileThreads) {
+        const int a = q % 17, bb = q / 17;
+        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+        cp_async8(&sb[q], b + gi);
+        cp_async8(&sb[289 + q], b + nn + gi);
+        cp_async8(&sb[578 + q], b + 2 * nn + gi);
+    }
+    if (t < 16) {
+        const int B = (x0 >> 2) + (t & 3) + ((y0 >> 2) + (t >> 2)) * nbk;
+        sq[t] = big[B] ? bq[B] : -1;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (t < 32) {
+        TileW W{sw};
+        TileB B{sb};
+        for (int pc = 0; pc < 8; ++pc) {
+            const int lj = t >> 1, li = ((pc - 2 * lj) & 7) + 8 * (t & 1);
+            if (sq[(li >> 2) + 4 * (lj >> 2)] < 0) plain_cell(L, W, B, li, lj);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    TileGW GW{sw, n, x0, y0};
+    TileGB GB{sb, n, x0, y0};
+    TileFlat FL{sw, w, n, nn, x0, y0};
+    for (int lb = 0; lb < 16; ++lb) {
+        const int q = sq[lb];
+        if (q < 0) continue;
+        big_block_group(L, E, rr + (size_t)q * 40, Ainv + (size_t)q * 3136, x0 + 4 * (lb & 3), y0 + 4 * (lb >> 2), GW,
+                        FL, GB, [&](int f, int i, int j, double d) { GW(f, i, j) += d; }, S, t,
+                        [] { __syncthreads(); });
+        __syncthreads();
+    }
+    for (int q = t; q < 17 * 17; q += kTileThreads) {
+        const int a = q % 17, bb = q / 17;
+        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+        TileW W{sw};
+        if (bb < 16) w[gi] = W(0, a, bb);
+        if (a < 16) w[nn + gi] = W(1, a, bb);
+        if (a < 16 && bb < 16) w[2 * nn + gi] = W(2, a, bb);
+    }
 }
 
 // ---- setup: dense local matrices and their inverses --------------------------
@@ -308,7 +390,7 @@ __device__ __forceinline__ void stokes_row_entries(const Lev& L, int field, Emit
 
 // One CTA per big block: assemble the 56x56 principal submatrix of A_l on the
 // block DOFs, invert it, store the inverse column-major.
-__global__ void k_block_inverse(Lev L, EMat E, const int* __restrict__ blk_ids, const int* __restrict__ fidx,
+__global__ void k_block_inverse(Lev L, EMat E, const int* __restrict__ blk_ids, const int2* __restrict__ rr,
                                 double* __restrict__ Ainv, int* err) {
     extern __shared__ double M[];  // 56 x 112
     __shared__ double col[56];
@@ -331,13 +413,12 @@ __global__ void k_block_inverse(Lev L, EMat E, const int* __restrict__ blk_ids, 
     }
     __syncthreads();
     if (t < 40) {
-        const int fi = fidx[(size_t)q * 40 + t];
-        if (fi >= 0)
-            for (int e = E.rp[fi]; e < E.rp[fi + 1]; ++e) {
+        const int2 r = rr[(size_t)q * 40 + t];
+        for (int e = r.x; e < r.y; ++e) {
                 const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
-                const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
-                if (c >= 0) M[t * 112 + c] -= E.val[e];
-            }
+            const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
+            if (c >= 0) M[t * 112 + c] -= E.val[e];
+        }
     }
     __syncthreads();
     gauss_jordan(M, 56, col, err);
@@ -381,13 +462,15 @@ __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict_
     }
 }
 
-// Face-list index of each of the 40 velocity DOFs of every big block (-1 if the
-// face has no E' row).
-__global__ void k_block_fidx(Lev L, FaceList FL, const int* __restrict__ blk_ids, int nbig, int* __restrict__ fidx) {
+// E' row range (begin, end) of each of the 40 velocity DOFs of every big block
+// ((0, 0) if the face has no E' row), and the block -> list position map bq.
+__global__ void k_block_rows(Lev L, FaceList FL, EMat E, const int* __restrict__ blk_ids, int nbig,
+                             int2* __restrict__ rr, int* __restrict__ bq) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nbig * 40) return;
     const int q = idx / 40, t = idx % 40, n = L.n, nbk = n >> 2;
     const int B = blk_ids[q];
+    if (t == 0) bq[B] = q;
     int f, i, j;
     block_dof(t, 4 * (B % nbk), 4 * (B / nbk), f, i, j);
     const int key = f * L.nn + wr(i, n) + wr(j, n) * n;
@@ -396,7 +479,7 @@ __global__ void k_block_fidx(Lev L, FaceList FL, const int* __restrict__ blk_ids
         const int mid = (lo + hi) >> 1;
         if (FL.face[mid] < key) lo = mid + 1; else hi = mid;
     }
-    fidx[idx] = (lo < FL.nf && FL.face[lo] == key) ? lo : -1;
+    rr[idx] = (lo < FL.nf && FL.face[lo] == key) ? make_int2(E.rp[lo], E.rp[lo + 1]) : make_int2(0, 0);
 }
 
 // Block sort keys: colour (bx mod 4) + 4 (by mod 4) for big blocks, 16 otherwise.
