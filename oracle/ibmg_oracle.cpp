@@ -421,22 +421,41 @@ void extract(const Csr& A, const int* d, int m, DenseLu& lu) {
         for (int c = 0; c < m; ++c) lu.a[size_t(r) * m + c] = A.at(d[r], d[c]);
 }
 
+// Deterministic greedy colouring of the big 4x4 blocks:
+// blocks in ascending id (bx + by*nbk) take the smallest colour unused by
+// already-coloured big blocks within Chebyshev block distance 2 (periodic).
+// Same-colour blocks are then >= 8 cells apart, beyond the E' reach (<= 7,
+// checked at setup), so a colour class is a set of independent boxes.
+// Mirrored exactly by the GPU host (paper_1311_5614_b200/csrc/ibmg.cu).
+std::vector<int> greedy_block_colours(const std::vector<char>& big, int nbk, int* ncol) {
+    std::vector<int> col(big.size(), -1);
+    *ncol = 0;
+    for (int by = 0; by < nbk; ++by)
+        for (int bx = 0; bx < nbk; ++bx) {
+            if (!big[bx + by * nbk]) continue;
+            unsigned long long used = 0;
+            for (int dy = -2; dy <= 2; ++dy)
+                for (int dx = -2; dx <= 2; ++dx) {
+                    const int c = col[wrap(bx + dx, nbk) + wrap(by + dy, nbk) * nbk];
+                    if (c >= 0) used |= 1ull << c;
+                }
+            int k = 0;
+            while (used >> k & 1ull) ++k;
+            col[bx + by * nbk] = k;
+            *ncol = std::max(*ncol, k + 1);
+        }
+    return col;
+}
+
 // Fixed multicolour schedule.  Plain phase: 16x16-cell
 // tiles coloured 2x2 (one tile, periodic, when n <= 16); inside each tile the
 // 8 conflict-free colours (i + 2j) mod 8 of local coordinates over cells
-// outside big blocks.  Big 4x4 blocks:
-//  * levels with n >= 64 (multi-tile GPU kernel): inside each tile, right after
-//    its plain colours, the tile's big blocks one at a time in local block
-//    order (bx + 4 by).  Same-colour tiles are 16 cells apart, beyond the E'
-//    reach (<= 12, checked at setup), so tiles of one colour are independent;
-//  * levels with n <= 32 (single-CTA coarse kernel): after all plain passes,
-//    the level-wide 16 colours (bx mod 4, by mod 4) (12-cell gap).
-// Boxes within one pass are mutually independent, so each pass is exactly a
-// Gauss-Seidel pass in any order (SPEC.md:427-431 semantics) and the GPU may
-// run it in parallel.
+// outside big blocks.  Big phase: the greedy colour classes of the big blocks
+// in colour order.  Boxes within one pass are mutually independent, so each
+// pass is exactly a Gauss-Seidel pass in any order (SPEC.md:427-431
+// semantics) and the GPU runs it in parallel.
 void build_schedule(Level& L) {
-    const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4, tb = T / 4;
-    const bool tile_local_big = n >= 64;
+    const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4;
     L.passes.clear();
     const int ntc = nt >= 2 ? 4 : 1;
     for (int tc = 0; tc < ntc; ++tc) {
@@ -453,29 +472,14 @@ void build_schedule(Level& L) {
                 }
             if (!p.items.empty()) L.passes.push_back(std::move(p));
         }
-        if (!tile_local_big) continue;
-        for (int lb = 0; lb < tb * tb; ++lb) {
-            Pass p;
-            p.big = true;
-            for (int by = 0; by < nbk; ++by)
-                for (int bx = 0; bx < nbk; ++bx) {
-                    if (!L.big[bx + by * nbk] || !tile_ok(bx / tb, by / tb)) continue;
-                    if ((bx % tb) + tb * (by % tb) != lb) continue;
-                    p.items.push_back(bx + by * nbk);
-                }
-            if (!p.items.empty()) L.passes.push_back(std::move(p));
-        }
     }
-    if (tile_local_big) return;
-    for (int bc = 0; bc < 16; ++bc) {
+    int ncol = 0;
+    const std::vector<int> col = greedy_block_colours(L.big, nbk, &ncol);
+    for (int bc = 0; bc < ncol; ++bc) {
         Pass p;
         p.big = true;
-        for (int by = 0; by < nbk; ++by)
-            for (int bx = 0; bx < nbk; ++bx) {
-                if (!L.big[bx + by * nbk]) continue;
-                if ((bx % 4) + 4 * (by % 4) != bc) continue;
-                p.items.push_back(bx + by * nbk);
-            }
+        for (int q = 0; q < nbk * nbk; ++q)
+            if (col[q] == bc) p.items.push_back(q);
         if (!p.items.empty()) L.passes.push_back(std::move(p));
     }
 }

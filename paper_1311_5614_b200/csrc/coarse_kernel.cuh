@@ -1,8 +1,10 @@
-// coarse_kernel.cuh — the bottom of the V-cycle (levels with n <= 32) in ONE
-// CTA, entirely in shared memory: sweeps (same schedule as the multi-tile
-// kernels), residual with the E' part, restriction, the dense bordered coarsest
-// solve, prolongation.  Removes ~20 launches per cycle from the latency-bound
-// tail of Algorithm 1.
+// coarse_kernel.cuh — the bottom of the V-cycle (levels with n <= 16) in ONE
+// CTA, entirely in shared memory: sweeps (same schedule as the oracle), the
+// residual with the E' part, restriction, the dense bordered coarsest solve,
+// prolongation.  Removes the latency-bound tail of Algorithm 1
+// from the launch stream.  At n <= 16 every big-block
+// colour holds one block, so the big phase is a sequence whose slabs are
+// double-buffered into shared memory ahead of use.
 #pragma once
 #include "common.cuh"
 #include "grid_kernels.cuh"
@@ -10,24 +12,21 @@
 
 namespace ibmg {
 
-constexpr int kCoarseMaxN = 32;
-constexpr int kCoarseThreads = 512;
+constexpr int kCoarseMaxN = 16;
+constexpr int kCoarseThreads = 128;
 
 struct CLev {
     Lev L;
-    Win W;
     FaceList FL;
     EMat E;
     const uint8_t* big;
-    const int* blk_ids;
-    const int2* rr;
-    const double* Ainv;
-    int coff[17];
+    Slabs SL;
+    int nbig;
 };
 
 struct CoarseArgs {
     int nl, nu1, nu2;
-    CLev lv[6];
+    CLev lv[4];
     const double* Acoarse;   // bordered inverse, col-major (3nn+1)^2
     const double* b_in;
     double* w_out;
@@ -40,63 +39,53 @@ struct SW {
         return s[f * nn + wr(i, n) + wr(j, n) * n];
     }
 };
-struct FlatS {
-    const double* s;
-    __device__ __forceinline__ double operator()(int idx) const { return s[idx]; }
-};
 
-__device__ void coarse_sweep(const CoarseArgs& A, const CLev& C, double* w, const double* b, BigScratch* sbig) {
+__device__ void coarse_sweep(const CLev& C, double* w, const double* b, SlabSlot* slot, BigScratch& S) {
     const Lev& L = C.L;
-    const int n = L.n, t = threadIdx.x, nt = blockDim.x;
+    const int n = L.n, t = threadIdx.x, nt = blockDim.x, nbk = n >> 2;
     SW W{w, n, L.nn};
     SW B{const_cast<double*>(b), n, L.nn};
-    const int T = n < kTile ? n : kTile, ntile = n / T, ntc = ntile >= 2 ? 4 : 1;
-    const int per = T * T / 8, ntiles_c = ntc == 1 ? 1 : (ntile / 2) * (ntile / 2), nbk = n >> 2;
-    for (int tc = 0; tc < ntc; ++tc)
-        for (int pc = 0; pc < 8; ++pc) {
-            for (int idx = t; idx < ntiles_c * per; idx += nt) {
-                const int tile = idx / per, within = idx % per;
-                int tx = 0, ty = 0;
-                if (ntc == 4) {
-                    tx = 2 * (tile % (ntile / 2)) + (tc & 1);
-                    ty = 2 * (tile / (ntile / 2)) + (tc >> 1);
-                }
-                int li, lj;
-                if (T == 16) {
-                    lj = within >> 1;
-                    li = ((pc - 2 * lj) & 7) + 8 * (within & 1);
-                } else {  // T == 8
-                    lj = within;
-                    li = (pc - 2 * lj) & 7;
-                }
-                const int i = tx * T + li, j = ty * T + lj;
-                if (!C.big[(i >> 2) + (j >> 2) * nbk]) plain_cell(L, W, B, i, j);
+    // start streaming the first big block's slab while the plain passes run
+    if (C.nbig > 0) slab_issue(slot[0], C.SL, 0, t, nt);
+    cp_async_commit();
+    const int per = n * n / 8;  // single tile (n <= 16): cells of one colour
+    for (int pc = 0; pc < 8; ++pc) {
+        for (int idx = t; idx < per; idx += nt) {
+            int li, lj;
+            if (n == 16) {
+                lj = idx >> 1;
+                li = ((pc - 2 * lj) & 7) + 8 * (idx & 1);
+            } else {  // n == 8
+                lj = idx;
+                li = (pc - 2 * lj) & 7;
             }
-            __syncthreads();
-        }
-    // big phase: 4 groups of 128 threads, each relaxing its own blocks of the
-    // colour (independent by the colouring), named barrier per group
-    const int g = t / kGroup, gt = t % kGroup;
-    FlatS flat{w};
-    for (int bc = 0; bc < 16; ++bc) {
-        const int cnt = C.coff[bc + 1] - C.coff[bc];
-        if (cnt == 0) continue;
-        for (int qq = g; qq < cnt; qq += nt / kGroup) {
-            const int q = C.coff[bc] + qq;
-            const int Bk = C.blk_ids[q];
-            big_block_group(L, C.E, C.rr + (size_t)q * 40, C.Ainv + (size_t)q * 3136, 4 * (Bk % nbk),
-                            4 * (Bk / nbk), W, flat, B, [&](int f, int i, int j, double d) { W(f, i, j) += d; },
-                            sbig[g], gt, [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); });
+            if (!C.big[(li >> 2) + (lj >> 2) * nbk]) plain_cell(L, W, B, li, lj);
         }
         __syncthreads();
     }
+    // big phase: each level-wide colour holds one block here; list order = pass order
+    for (int q = 0; q < C.nbig; ++q) {
+        if (q + 1 < C.nbig) slab_issue(slot[(q + 1) & 1], C.SL, q + 1, t, nt);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const SlabSlot& sl = slot[q & 1];
+        const int Bk = sl.rp[47];  // owner block id (k_slab_count)
+        big_block_slab(L, sl, 4 * (Bk % nbk), 4 * (Bk / nbk), W, (const double*)w, (const double*)w, B,
+                       [&](int f, int i, int j, double d) { W(f, i, j) += d; }, S, t);
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
-    extern __shared__ double sm[];
-    __shared__ BigScratch sr[kCoarseThreads / kGroup];
-    double* wl[6];
-    double* bl[6];
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
+    double* sm = reinterpret_cast<double*>(dsm + 2 * sizeof(SlabSlot));
+    __shared__ BigScratch S;
+    double* wl[4];
+    double* bl[4];
     size_t off = 0;
     for (int l = 0; l < A.nl; ++l) {
         const int m = 3 * A.lv[l].L.nn;
@@ -115,7 +104,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
         const int n = L.n, nn = L.nn;
         for (int q = t; q < 3 * nn; q += nt) wl[l][q] = 0.0;
         __syncthreads();
-        for (int s = 0; s < A.nu1; ++s) coarse_sweep(A, C, wl[l], bl[l], sr);
+        for (int s = 0; s < A.nu1; ++s) coarse_sweep(C, wl[l], bl[l], slot, S);
         // residual r = b - A w (stencil, then + E' w from the assembled rows)
         SW W{wl[l], n, nn};
         for (int q = t; q < nn; q += nt) {
@@ -132,7 +121,6 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
             r[C.FL.face[fq]] += s;
         }
         __syncthreads();
-        // restrict into the next level's b
         const int nc = n >> 1, nnc = nc * nc;
         for (int q = t; q < nnc; q += nt) {
             const int I = q % nc, J = q / nc, i = 2 * I, j = 2 * J;
@@ -166,7 +154,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
             wl[l][2 * nn + q] += dp;
         }
         __syncthreads();
-        for (int s = 0; s < A.nu2; ++s) coarse_sweep(A, C, wl[l], bl[l], sr);
+        for (int s = 0; s < A.nu2; ++s) coarse_sweep(C, wl[l], bl[l], slot, S);
     }
     for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) A.w_out[q] = wl[0][q];
 }

@@ -60,6 +60,8 @@ void dfree(T*& p) {
 
 inline unsigned nblk(size_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
+constexpr int kMaxColours = 32;
+
 struct LevelBuf {
     Lev L{};
     double *w = nullptr, *b = nullptr, *r = nullptr;
@@ -73,9 +75,18 @@ struct LevelBuf {
     int nbig = 0;
     int* blk_ids = nullptr;  // big blocks sorted by colour, ascending id within
     int blk_cap = 0;
-    int coff[17] = {0};
+    int coff[kMaxColours + 1] = {0};
+    int ncol = 0;
     int2* rr = nullptr;
     int* bq = nullptr;
+    // per-block slabs (inverse + encoded E' rows) and big-tile lists
+    int* sl_rp = nullptr;
+    int* sl_off = nullptr;
+    int blk_slab_cap = 0;
+    int* sl_col = nullptr;
+    double* sl_val = nullptr;
+    long sl_cap = 0;
+
     double* Ainv = nullptr;
     int ainv_cap = 0;
 };
@@ -110,6 +121,7 @@ struct ibmg_ctx {
     double* hpin = nullptr;    // pinned host mirror of dh
     size_t M = 0;              // 3 N^2
     bool have_structs = false;
+    int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
     // live per-kernel CUDA-event timing (bench roofline); off on the timed path
     bool prof = false;
     struct ProfRec {
@@ -163,6 +175,10 @@ void prof_collect(ibmg_ctx* c) {
         if ((ctx)->prof && (ctx)->prof_pending.size() > 4096) prof_collect(ctx); \
     } while (0)
 
+// per-level counters: [0..16] colour counts, 17 runs, 18 reach, 19 max slab
+// entries, [20..27] tile-key counts, 28 slab total
+constexpr int kCtr = 32;
+
 Lev make_lev(const ibmg_params& p, int n) {
     Lev L;
     L.n = n;
@@ -207,8 +223,8 @@ void alloc_levels(ibmg_ctx* c) {
     c->nlev = int(c->lev.size());
     c->lc = 0;
     while (c->lev[c->lc].L.n > kCoarseMaxN) ++c->lc;
-    static_assert(kCoarseMaxN * 2 == 4 * kTile, "multi-tile levels (tile-local big phase) are exactly n >= 64");
-    if (c->nlev - c->lc > 6) throw InvalidArg("too many coarse-kernel levels");
+    static_assert(kCoarseMaxN == kTile, "multi-tile levels (tile-local big phase) are exactly n >= 32");
+    if (c->nlev - c->lc > 4) throw InvalidArg("too many coarse-kernel levels");
     c->M = 3 * size_t(p.N) * p.N;
     const int m = p.restart;
     c->V = dalloc<double>(c->M * (m + 1));
@@ -228,7 +244,7 @@ void alloc_levels(ibmg_ctx* c) {
         CK(cudaMemcpy(c->ones, one.data(), one.size() * sizeof(double), cudaMemcpyHostToDevice));
     }
     c->err_flag = dalloc<int>(1);
-    c->counters = dalloc<int>(size_t(c->nlev) * 20);
+    c->counters = dalloc<int>(size_t(c->nlev) * kCtr);
     const int nc = c->lev.back().L.nn;
     c->Acoarse = dalloc<double>(size_t(3 * nc + 1) * (3 * nc + 1));
 }
@@ -251,6 +267,12 @@ void free_structs(ibmg_ctx* c) {
         dfree(lb.blk_ids);
         dfree(lb.rr);
         dfree(lb.Ainv);
+        dfree(lb.sl_rp);
+        dfree(lb.sl_off);
+        dfree(lb.sl_col);
+        dfree(lb.sl_val);
+        lb.sl_cap = 0;
+        lb.blk_slab_cap = 0;
         lb.blk_cap = lb.ainv_cap = 0;
         lb.nbig = 0;
     }
@@ -273,6 +295,51 @@ void free_structs(ibmg_ctx* c) {
     c->npts = 0;
 }
 
+// Deterministic greedy colouring of the big blocks, the same
+// rule as the oracle (oracle/ibmg_oracle.cpp greedy_block_colours): ascending
+// block id, smallest colour unused within Chebyshev block distance 2
+// (periodic).  Produces the colour-major block list and colour offsets.
+void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb) {
+    const int nbk = lb.L.n / 4;
+    std::vector<uint8_t> big(size_t(nbk) * nbk);
+    CK(cudaMemcpy(big.data(), lb.big, big.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> col(big.size(), -1);
+    int ncol = 0, nbig = 0;
+    for (int by = 0; by < nbk; ++by)
+        for (int bx = 0; bx < nbk; ++bx) {
+            if (!big[bx + by * nbk]) continue;
+            unsigned long long used = 0;
+            for (int dy = -2; dy <= 2; ++dy)
+                for (int dx = -2; dx <= 2; ++dx) {
+                    const int k = col[wr(bx + dx, nbk) + wr(by + dy, nbk) * nbk];
+                    if (k >= 0) used |= 1ull << k;
+                }
+            int k = 0;
+            while (used >> k & 1ull) ++k;
+            col[bx + by * nbk] = k;
+            ncol = std::max(ncol, k + 1);
+            ++nbig;
+        }
+    if (ncol > kMaxColours) throw InvalidArg("too many big-block colours");
+    std::vector<int> cnt(ncol + 1, 0), ids(nbig);
+    for (int k : col)
+        if (k >= 0) ++cnt[k + 1];
+    for (int k = 0; k < ncol; ++k) cnt[k + 1] += cnt[k];
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+    for (int q = 0; q < nbk * nbk; ++q)
+        if (col[q] >= 0) ids[pos[col[q]]++] = q;
+    lb.ncol = ncol;
+    lb.nbig = nbig;
+    std::fill(lb.coff, lb.coff + kMaxColours + 1, nbig);
+    for (int k = 0; k <= ncol; ++k) lb.coff[k] = cnt[k];
+    if (lb.blk_cap < nbig) {
+        dfree(lb.blk_ids);
+        lb.blk_cap = std::max(nbig, 64);
+        lb.blk_ids = dalloc<int>(size_t(lb.blk_cap));
+    }
+    if (nbig) CK(cudaMemcpy(lb.blk_ids, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice));
+}
+
 void check_err_flag(ibmg_ctx* c, const char* where) {
     int h = 0;
     CK(cudaMemcpyAsync(&h, c->err_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s));
@@ -286,12 +353,13 @@ void check_err_flag(ibmg_ctx* c, const char* where) {
 void rebuild(ibmg_ctx* c) {
     const int npts = c->npts;
     CK(cudaMemsetAsync(c->err_flag, 0, sizeof(int), c->s));
-    CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * 20, c->s));
+    CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * kCtr, c->s));
     if (npts == 0) {
         for (auto& lb : c->lev) {
             lb.FL.nf = 0;
             lb.nbig = 0;
-            std::fill(lb.coff, lb.coff + 17, 0);
+            lb.ncol = 0;
+            std::fill(lb.coff, lb.coff + kMaxColours + 1, 0);
             if (lb.big) CK(cudaMemsetAsync(lb.big, 0, size_t(lb.L.n / 4) * (lb.L.n / 4), c->s));
         }
     } else {
@@ -313,11 +381,11 @@ void rebuild(ibmg_ctx* c) {
             CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys, c->keys2, c->vals, lb.FL.ent, items, 0, 31,
                                                c->s));
             bytes = 0;
-            cub::DeviceRunLengthEncode::Encode(nullptr, bytes, c->keys2, lb.FL.face, c->cnt, c->counters + l * 20 + 17,
+            cub::DeviceRunLengthEncode::Encode(nullptr, bytes, c->keys2, lb.FL.face, c->cnt, c->counters + l * kCtr + 17,
                                                items, c->s);
             ensure_cub(c, bytes);
             CK(cub::DeviceRunLengthEncode::Encode(c->cub_tmp, bytes, c->keys2, lb.FL.face, c->cnt,
-                                                  c->counters + l * 20 + 17, items, c->s));
+                                                  c->counters + l * kCtr + 17, items, c->s));
             bytes = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, lb.FL.off, items + 1, c->s);
             ensure_cub(c, bytes);
@@ -331,29 +399,14 @@ void rebuild(ibmg_ctx* c) {
             const int nbk = lb.L.n / 4;
             CK(cudaMemsetAsync(lb.big, 0, size_t(nbk) * nbk, c->s));
             LAUNCH(c, k_mark_big, nblk(size_t(npts) * 64), 256, 0, npts, lb.W, lb.L.n, lb.big);
-            LAUNCH(c, k_reach, nblk(npts, 128), 128, 0, npts, lb.W, c->P, c->counters + l * 20 + 18);
-            LAUNCH(c, k_block_keys, nblk(size_t(nbk) * nbk), 256, 0, nbk, lb.big, c->keys, c->vals,
-                   c->counters + l * 20);
-            size_t bytes = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys, c->keys2, c->vals, c->vals2, nbk * nbk, 0, 5,
-                                            c->s);
-            ensure_cub(c, bytes);
-            CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys, c->keys2, c->vals, c->vals2, nbk * nbk, 0,
-                                               5, c->s));
-            // keep the sorted block ids of this level in vals2 slice: copy after counts are known
-            if (lb.blk_cap < nbk * nbk) {
-                dfree(lb.blk_ids);
-                lb.blk_ids = dalloc<int>(size_t(nbk) * nbk);
-                lb.blk_cap = nbk * nbk;
-            }
-            CK(cudaMemcpyAsync(lb.blk_ids, c->vals2, sizeof(int) * nbk * nbk, cudaMemcpyDeviceToDevice, c->s));
+            LAUNCH(c, k_reach, nblk(npts, 128), 128, 0, npts, lb.W, c->P, c->counters + l * kCtr + 18);
         }
-        std::vector<int> hc(size_t(c->nlev) * 20);
+        std::vector<int> hc(size_t(c->nlev) * kCtr);
         CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
         CK(cudaStreamSynchronize(c->s));
         for (int l = 0; l < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
-            const int* h = &hc[size_t(l) * 20];
+            const int* h = &hc[size_t(l) * kCtr];
             // runs include the sentinel run (INT_MAX) when any weight was zero
             int runs = h[17];
             int last = 0;
@@ -364,12 +417,10 @@ void rebuild(ibmg_ctx* c) {
             lb.FL.nf = runs;
             if (l + 1 < c->nlev) {
                 const int reach = h[18];
-                if (reach > 12)
-                    throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 12-cell colour separation on level " +
+                if (reach > 7)
+                    throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 8-cell same-colour gap on level " +
                                      std::to_string(l) + " (Lagrangian spacing too large)");
-                lb.coff[0] = 0;
-                for (int k = 0; k < 16; ++k) lb.coff[k + 1] = lb.coff[k] + h[k];
-                lb.nbig = lb.coff[16];
+                colour_big_blocks(c, lb);
             }
         }
         // assembled E'_l rows on the E-active faces (count, scan, fill)
@@ -419,6 +470,44 @@ void rebuild(ibmg_ctx* c) {
                    lb.bq);
             LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.E, lb.blk_ids, lb.rr,
                    lb.Ainv, c->err_flag);
+            if (lb.sl_off == nullptr || lb.ainv_cap > lb.blk_slab_cap) {
+                dfree(lb.sl_rp);
+                dfree(lb.sl_off);
+                lb.sl_rp = dalloc<int>(size_t(lb.ainv_cap) * 48);
+                lb.sl_off = dalloc<int>(size_t(lb.ainv_cap) + 1);
+                lb.blk_slab_cap = lb.ainv_cap;
+            }
+            CK(cudaMemsetAsync(c->cnt, 0, sizeof(int) * (lb.nbig + 1), c->s));
+            LAUNCH(c, k_slab_count, nblk(lb.nbig, 128), 128, 0, lb.nbig, lb.blk_ids, lb.rr, lb.sl_rp, c->cnt,
+                   c->counters + l * kCtr + 19);
+            size_t bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, lb.sl_off, lb.nbig + 1, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, lb.sl_off, lb.nbig + 1, c->s));
+            CK(cudaMemcpyAsync(c->counters + l * kCtr + 28, lb.sl_off + lb.nbig, sizeof(int), cudaMemcpyDeviceToDevice,
+                               c->s));
+        }
+        {
+            std::vector<int> hc(size_t(c->nlev) * kCtr);
+            CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int l = 0; l + 1 < c->nlev; ++l) {
+                LevelBuf& lb = c->lev[l];
+                if (lb.nbig == 0) continue;
+                const int* h = &hc[size_t(l) * kCtr];
+                if (h[19] > kSlabCap)
+                    throw InvalidArg("E' rows of a big block exceed the shared-memory slab (" + std::to_string(h[19]) +
+                                     " > " + std::to_string(kSlabCap) + " entries) on level " + std::to_string(l));
+                if (h[28] > lb.sl_cap) {
+                    dfree(lb.sl_col);
+                    dfree(lb.sl_val);
+                    lb.sl_cap = std::max<long>(h[28], lb.sl_cap * 5 / 4);
+                    lb.sl_col = dalloc<int>(size_t(lb.sl_cap));
+                    lb.sl_val = dalloc<double>(size_t(lb.sl_cap));
+                }
+                LAUNCH(c, k_slab_fill, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.nbig, lb.blk_ids, lb.rr, lb.E,
+                       lb.sl_off, lb.sl_rp, lb.sl_col, lb.sl_val, 0);
+            }
         }
     }
     {
@@ -520,13 +609,31 @@ void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double
     }
 }
 
+Slabs slabs(const LevelBuf& lb) { return Slabs{lb.Ainv, lb.sl_rp, lb.sl_off, lb.sl_col, lb.sl_val}; }
+
+// One multicolour sweep of a multi-tile level (n >= 32): the plain phase as
+// 4 tile-colour launches (one warp per 16x16 tile), then the big phase as one
+// cooperative persistent launch over the 16 level-wide colours.
 void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     LevelBuf& lb = c->lev[l];
     const int n = lb.L.n;
-    if (n < 4 * kTile) throw InvalidArg("multi-tile sweep needs n >= 64");
+    if (n < 2 * kTile) throw InvalidArg("multi-tile sweep needs n >= 32");
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
-    for (int tc = 0; tc < 4; ++tc)
-        LAUNCH(c, k_tile_sweep, per, kTileThreads, 0, lb.L, tc, b, w, lb.big, lb.bq, lb.E, lb.rr, lb.Ainv);
+    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
+    if (lb.nbig == 0) return;
+    BigColours BC;
+    BC.ncol = lb.ncol;
+    int widest = 1;
+    for (int k = 0; k <= kMaxColours; ++k) BC.off[k] = lb.coff[k];
+    for (int k = 0; k < lb.ncol; ++k) widest = std::max(widest, lb.coff[k + 1] - lb.coff[k]);
+    const int grid = std::min(widest, c->big_grid_max);
+    Lev L = lb.L;
+    Slabs SL = slabs(lb);
+    void* args[] = {&L, &SL, &BC, (void*)&b, (void*)&w};
+    if (c->prof) prof_begin(c, "k_big_phase");
+    CK(cudaLaunchCooperativeKernel((const void*)k_big_phase, dim3(grid), dim3(kBigThreads), args, kBigSmem, c->s));
+    if (c->prof) prof_end(c);
+    ++c->launches;
 }
 
 CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
@@ -538,14 +645,11 @@ CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
         LevelBuf& lb = c->lev[l];
         CLev& C = A.lv[l - c->lc];
         C.L = lb.L;
-        C.W = lb.W;
         C.FL = lb.FL;
         C.E = lb.E;
         C.big = lb.big;
-        C.blk_ids = lb.blk_ids;
-        C.rr = lb.rr;
-        C.Ainv = lb.Ainv;
-        std::copy(lb.coff, lb.coff + 17, C.coff);
+        C.SL = slabs(lb);
+        C.nbig = lb.nbig;
     }
     A.Acoarse = c->Acoarse;
     A.b_in = b_in;
@@ -557,7 +661,7 @@ size_t coarse_smem(ibmg_ctx* c) {
     size_t d = 0;
     for (int l = c->lc; l < c->nlev; ++l) d += 6 * size_t(c->lev[l].L.nn);
     d += 3 * size_t(c->lev[c->lc].L.nn);
-    return d * sizeof(double);
+    return 2 * sizeof(SlabSlot) + d * sizeof(double);
 }
 
 void coarse_cycle(ibmg_ctx* c, const double* b, double* w) {
@@ -772,6 +876,13 @@ int ibmg_create(const ibmg_params* p, ibmg_ctx** out) {
         CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
         CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 112 * 8));
         CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * 98 * 8));
+        CK(cudaFuncSetAttribute(k_big_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
+        {
+            int per_sm = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_phase, kBigThreads, kBigSmem));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+            c->big_grid_max = std::max(1, per_sm * sms);
+        }
         alloc_levels(c);
         CK(cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem(c))));
         c->npts = 0;
@@ -924,7 +1035,7 @@ int ibmg_prolong_add(ibmg_ctx* c, int level, const double* ec, double* wf, int p
 int ibmg_sweep(ibmg_ctx* c, int level, const double* b, double* w, int ptr_kind) {
     return api(c, [&]() -> int {
         if (level < 0 || level + 1 >= c->nlev) throw InvalidArg("sweep: level out of range");
-        if (level >= c->lc) throw InvalidArg("sweep: levels with n <= 32 run inside the coarse-cycle kernel only");
+        if (level >= c->lc) throw InvalidArg("sweep: levels with n <= 16 run inside the coarse-cycle kernel only");
         const size_t m = 3 * size_t(c->lev[level].L.nn);
         Stage S{c, ptr_kind};
         const double* db = S.in(b, m, c->stage_a);

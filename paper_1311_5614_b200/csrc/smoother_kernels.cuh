@@ -7,8 +7,12 @@
 // in shared memory); big phase = big 4x4 blocks in 16 level-wide colours
 // (bx mod 4, by mod 4), one CTA per block, dense 56x56 inverse applied.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "grid_kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ibmg {
 
@@ -65,9 +69,8 @@ struct TileB {
 
 __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double* __restrict__ b,
                                                      double* __restrict__ w, const uint8_t* __restrict__ big) {
-    __shared__ double sw[3 * kReg * kReg];
-    __shared__ double sb[3 * 289];
-    __shared__ uint8_t sbig[16];
+    __shared__ __align__(16) double sw[3 * kReg * kReg];
+    __shared__ __align__(16) double sb[3 * 289];
     const int n = L.n, nn = L.nn, lane = threadIdx.x;
     const int half = (n / kTile) >> 1;
     const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = 2 * (blockIdx.x / half) + (tc >> 1);
@@ -86,14 +89,15 @@ __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double*
         cp_async8(&sb[289 + q], b + nn + gi);
         cp_async8(&sb[578 + q], b + 2 * nn + gi);
     }
-    if (lane < 16) sbig[lane] = big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
+    const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
+    const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
     cp_async_wait_all();
     __syncwarp();
     TileW W{sw};
     TileB B{sb};
     for (int pc = 0; pc < 8; ++pc) {
         const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
-        if (!sbig[(li >> 2) + 4 * (lj >> 2)]) plain_cell(L, W, B, li, lj);
+        if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
         __syncwarp();
     }
     // write set: u faces i in [x0, x0+16], v faces j in [y0, y0+16], p cells
@@ -141,86 +145,103 @@ struct FlatG {
     __device__ __forceinline__ double operator()(int idx) const { return w[idx]; }
 };
 
-// One big-block relaxation by a group of 128 threads (4 warps).  Latency
-// structure (the routine is a handful of dependent memory rounds):
-//  (1) Stokes residual of the 56 DOFs and, in parallel, the E' row dots of the
-//      40 velocity DOFs (warp per row, lanes over nonzeros; all (col, val)
-//      loads of 5 rows issued before the dependent w gathers);
-//  (2) the 56x56 inverse applied by 112 threads (2 column halves, loads
-//      prefetched 14 at a time), reduced in a fixed order (deterministic).
-// `gsync` is the group barrier (__syncthreads or a named barrier).
 constexpr int kGroup = 128;
 struct BigScratch {
-    double sr[56], se[40], part[2][56];
+    double sr[56], se[40], part[2][56], epart[3][40];
 };
 
-template <class Acc, class Flat, class BAcc, class WAdd, class Sync>
-__device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, const int2* __restrict__ rr_q,
-                                                const double* __restrict__ A_q, int bi, int bj, const Acc& acc,
-                                                const Flat& flat, const BAcc& bacc, WAdd&& wadd, BigScratch& S,
-                                                int gt, Sync&& gsync) {
-    const int wid = gt >> 5, lane = gt & 31;
-    // inverse columns of this thread, issued first (independent of w)
-    double av[28];
-    const int row = gt % 56, cg = gt / 56;
-    if (gt < 112) {
-        const double* A = A_q + (size_t)(28 * cg) * 56 + row;
-#pragma unroll
-        for (int c = 0; c < 28; ++c) av[c] = A[c * 56];
-    }
+// ---- per-block "slab": all w-independent data of one big block, packed at
+// setup so it can be streamed into shared memory with cp.async ahead of use:
+// the 56x56 inverse (col-major), the 40 E' row pointers (relative, padded to
+// 48 ints) and the rows' (col, val) entries with columns pre-encoded as
+// shared-memory indices (>= 0) or global flat indices (-(flat+1)).
+constexpr int kSlabCap = 2560;  // entries per block held in shared memory
+struct SlabSlot {
+    double A[3136];
+    double val[kSlabCap];
+    int col[kSlabCap];
+    int rp[48];
+};
+static_assert(sizeof(SlabSlot) % 16 == 0, "slot alignment");
+
+struct Slabs {
+    const double* Ainv;  // [nbig][3136]
+    const int* rp;       // [nbig][48]
+    const int* off;      // [nbig+1] entry offsets (multiples of 4)
+    const int* col;
+    const double* val;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void slab_issue(SlabSlot& slot, const Slabs& SL, int q, int t, int nt) {
+    const char* A = reinterpret_cast<const char*>(SL.Ainv + (size_t)q * 3136);
+    char* dA = reinterpret_cast<char*>(slot.A);
+    for (int c = t; c < 3136 * 8 / 16; c += nt) cp_async16(dA + 16 * c, A + 16 * c);
+    if (t < 12) cp_async16(reinterpret_cast<char*>(slot.rp) + 16 * t, reinterpret_cast<const char*>(SL.rp + (size_t)q * 48) + 16 * t);
+    const int o = SL.off[q], cnt = SL.off[q + 1] - o;
+    const char* cv = reinterpret_cast<const char*>(SL.val + o);
+    const char* cc = reinterpret_cast<const char*>(SL.col + o);
+    for (int c = t; c < cnt / 2; c += nt) cp_async16(reinterpret_cast<char*>(slot.val) + 16 * c, cv + 16 * c);
+    for (int c = t; c < cnt / 4; c += nt) cp_async16(reinterpret_cast<char*>(slot.col) + 16 * c, cc + 16 * c);
+}
+
+// One big-block relaxation from a shared-memory slab by 128 threads: Stokes
+// residual of the 56 DOFs + E' row dots (3 threads per row) -> 56x56 inverse
+// (2 column halves) -> correction.  Only shared-memory traffic except E'
+// columns outside the staged region (global, not modified by this launch).
+template <class WA, class LocA, class GlobA, class BA, class WAdd>
+__device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slot, int bi, int bj, const WA& W,
+                                               const LocA& wloc, const GlobA& wglob, const BA& Bv, WAdd&& wadd,
+                                               BigScratch& S, int gt) {
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
         i = wr(i, L.n);
         j = wr(j, L.n);
         double ru, rv, rp;
-        stokes_rows(L, acc, i, j, ru, rv, rp);
-        S.sr[gt] = bacc(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
+        stokes_rows(L, W, i, j, ru, rv, rp);
+        S.sr[gt] = Bv(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
     }
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-        int beg[5], end[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const int2 r = rr_q[wid + 4 * (5 * half + k)];
-            beg[k] = r.x;
-            end[k] = r.y;
+    // E' row dots: 3 threads per row (strided entries), fixed-order combine
+    if (gt < 120) {
+        const int r = gt % 40, p = gt / 40;
+        double s0 = 0.0, s1 = 0.0;
+        const int e1 = slot.rp[r + 1];
+        int e = slot.rp[r] + p;
+        for (; e + 3 < e1; e += 6) {
+            const int c0 = slot.col[e], c1 = slot.col[e + 3];
+            s0 += slot.val[e] * (c0 >= 0 ? wloc[c0] : wglob[-c0 - 1]);
+            s1 += slot.val[e + 3] * (c1 >= 0 ? wloc[c1] : wglob[-c1 - 1]);
         }
-        int cl[5][2];
-        double vl[5][2];
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int e = beg[k] + lane + 32 * h;
-                const bool ok = e < end[k];
-                cl[k][h] = ok ? E.col[e] : -1;
-                vl[k][h] = ok ? E.val[e] : 0.0;
-            }
-        double ps[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-            ps[k] = (cl[k][0] >= 0 ? vl[k][0] * flat(cl[k][0]) : 0.0) + (cl[k][1] >= 0 ? vl[k][1] * flat(cl[k][1]) : 0.0);
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-            for (int e = beg[k] + lane + 64; e < end[k]; e += 32) ps[k] += E.val[e] * flat(E.col[e]);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const double v = warp_sum(ps[k]);
-            if (lane == 0) S.se[wid + 4 * (5 * half + k)] = v;
+        if (e < e1) {
+            const int c0 = slot.col[e];
+            s0 += slot.val[e] * (c0 >= 0 ? wloc[c0] : wglob[-c0 - 1]);
         }
+        S.epart[p][r] = s0 + s1;
     }
-    gsync();
+    __syncthreads();
     if (gt < 112) {
-        double s = 0.0;
+        const int row = gt % 56, cg = gt / 56;
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < 28; ++c) {
+        for (int c = 0; c < 28; c += 2) {
             const int cc = 28 * cg + c;
-            s += av[c] * (cc < 40 ? S.sr[cc] + S.se[cc] : S.sr[cc]);
+            const double r0 = cc < 40 ? S.sr[cc] + ((S.epart[0][cc] + S.epart[1][cc]) + S.epart[2][cc]) : S.sr[cc];
+            const double r1 = cc + 1 < 40 ? S.sr[cc + 1] + ((S.epart[0][cc + 1] + S.epart[1][cc + 1]) + S.epart[2][cc + 1])
+                                          : S.sr[cc + 1];
+            s0 += slot.A[cc * 56 + row] * r0;
+            s1 += slot.A[(cc + 1) * 56 + row] * r1;
         }
-        S.part[cg][row] = s;
+        S.part[cg][row] = s0 + s1;
     }
-    gsync();
+    __syncthreads();
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
@@ -228,100 +249,88 @@ __device__ __forceinline__ void big_block_group(const Lev& L, const EMat& E, con
     }
 }
 
-// One sweep phase of a multi-tile level (n >= 64): one 128-thread CTA per tile
-// of tile colour tc.  The 20x20 region (2-cell halo) of w and the tile's b are
-// staged in shared memory with cp.async; warp 0 runs the 8 plain colour
-// passes; then the whole CTA relaxes the tile's big blocks one by one in local
-// order (tile-local big phase); the write set goes back once.
-struct TileFlat {  // flat velocity index -> shared region if inside, else global
-    const double* s;
-    const double* g;
-    int n, nn, x0, y0;
-    __device__ __forceinline__ double operator()(int idx) const {
-        const int comp = idx >= nn, f = idx - comp * nn;
-        const int li = wr((f & (n - 1)) - x0 + 2, n), lj = wr(f / n - y0 + 2, n);
-        if (li < kReg && lj < kReg) return s[comp * kReg * kReg + lj * kReg + li];
-        return g[idx];
+// Global accessors that bypass L1 (ld.global.cg): the big phase reads values
+// other CTAs wrote before the last grid barrier.
+struct GAccCG {
+    const double* w;
+    int n, nn;
+    __device__ __forceinline__ double operator()(int comp, int i, int j) const {
+        return __ldcg(w + (size_t)comp * nn + i + (size_t)j * n);
     }
 };
-struct TileGW {  // wrapped global coords -> shared region (all stencil reads are inside)
-    double* s;
-    int n, x0, y0;
-    __device__ __forceinline__ double& operator()(int f, int i, int j) const {
-        return s[f * kReg * kReg + wr(j - y0 + 2, n) * kReg + wr(i - x0 + 2, n)];
+struct GAccB {
+    const double* b;
+    int n, nn;
+    __device__ __forceinline__ double operator()(int comp, int i, int j) const {
+        return __ldg(b + (size_t)comp * nn + i + (size_t)j * n);
     }
 };
-struct TileGB {
-    const double* s;
-    int n, x0, y0;
-    __device__ __forceinline__ double operator()(int f, int i, int j) const {
-        return s[f * 289 + wr(j - y0, n) * 17 + wr(i - x0, n)];
-    }
+struct FlatCG {
+    const double* w;
+    __device__ __forceinline__ double operator[](int idx) const { return __ldcg(w + idx); }
 };
 
-constexpr int kTileThreads = 128;
-__global__ void __launch_bounds__(kTileThreads) k_tile_sweep(Lev L, int tc, const double* __restrict__ b,
-                                                              double* __restrict__ w, const uint8_t* __restrict__ big,
-                                                              const int* __restrict__ bq, EMat E,
-                                                              const int2* __restrict__ rr,
-                                                              const double* __restrict__ Ainv) {
-    __shared__ double sw[3 * kReg * kReg];
-    __shared__ double sb[3 * 289];
-    __shared__ int sq[16];
+struct BigColours {
+    int ncol;
+    int off[33];
+};
+
+// The big phase of one sweep on a level as ONE cooperative persistent kernel:
+// the greedy colour classes run in order with a grid barrier between them;
+// each CTA takes the colour's blocks grid-stride, and the slab of its next
+// block (possibly in the next colour) streams into the second shared-memory
+// slot while the current block is solved.
+constexpr int kBigThreads = 128;
+constexpr size_t kBigSmem = 2 * sizeof(SlabSlot);
+__global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC,
+                                                            const double* __restrict__ b, double* w) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
     __shared__ BigScratch S;
-    const int n = L.n, nn = L.nn, t = threadIdx.x;
-    const int half = (n / kTile) >> 1;
-    const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = 2 * (blockIdx.x / half) + (tc >> 1);
-    const int x0 = tx * kTile, y0 = ty * kTile, nbk = n >> 2;
-    for (int q = t; q < kReg * kReg; q += kTileThreads) {
-        const int a = q % kReg, bb = q / kReg;
-        const size_t gi = wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-        cp_async8(&sw[q], w + gi);
-        cp_async8(&sw[kReg * kReg + q], w + nn + gi);
-        cp_async8(&sw[2 * kReg * kReg + q], w + 2 * nn + gi);
-    }
-    for (int q = t; q < 289; q += kTileThreads) {
-        const int a = q % 17, bb = q / 17;
-        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-        cp_async8(&sb[q], b + gi);
-        cp_async8(&sb[289 + q], b + nn + gi);
-        cp_async8(&sb[578 + q], b + 2 * nn + gi);
-    }
-    if (t < 16) {
-        const int B = (x0 >> 2) + (t & 3) + ((y0 >> 2) + (t >> 2)) * nbk;
-        sq[t] = big[B] ? bq[B] : -1;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if (t < 32) {
-        TileW W{sw};
-        TileB B{sb};
-        for (int pc = 0; pc < 8; ++pc) {
-            const int lj = t >> 1, li = ((pc - 2 * lj) & 7) + 8 * (t & 1);
-            if (sq[(li >> 2) + 4 * (lj >> 2)] < 0) plain_cell(L, W, B, li, lj);
-            __syncwarp();
+    cg::grid_group grid = cg::this_grid();
+    const int t = threadIdx.x, G = gridDim.x, nbk = L.n >> 2;
+    auto next_item = [&](int c, int q, int& nc, int& nq) {
+        // the item after (c, q) for this CTA; c = -1 starts the enumeration
+        nq = (c < 0) ? -1 : q + G;
+        nc = (c < 0) ? 0 : c;
+        while (nc < BC.ncol) {
+            if (nq < 0) nq = BC.off[nc] + (int)blockIdx.x;
+            if (nq < BC.off[nc + 1]) return;
+            ++nc;
+            nq = -1;
         }
+    };
+    int c, q;
+    next_item(-1, 0, c, q);
+    if (c < BC.ncol) slab_issue(slot[0], SL, q, t, kBigThreads);
+    cp_async_commit();
+    GAccCG W{w, L.n, L.nn};
+    GAccB B{b, L.n, L.nn};
+    int k = 0;
+    for (int colour = 0; colour < BC.ncol; ++colour) {
+        while (c == colour) {
+            int nc, nq;
+            next_item(c, q, nc, nq);
+            if (nc < BC.ncol) slab_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
+            cp_async_commit();
+            cp_async_wait<1>();
+            __syncthreads();
+            const SlabSlot& sl = slot[k & 1];
+            const int Bk = sl.rp[47];
+            big_block_slab(L, sl, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, FlatCG{w}, B,
+                           [&](int f, int i, int j, double d) {
+                               double* p = w + (size_t)f * L.nn + i + (size_t)j * L.n;
+                               __stcg(p, __ldcg(p) + d);
+                           },
+                           S, t);
+            __syncthreads();
+            ++k;
+            c = nc;
+            q = nq;
+        }
+        if (BC.off[colour + 1] > BC.off[colour]) grid.sync();
     }
-    __syncthreads();
-    TileGW GW{sw, n, x0, y0};
-    TileGB GB{sb, n, x0, y0};
-    TileFlat FL{sw, w, n, nn, x0, y0};
-    for (int lb = 0; lb < 16; ++lb) {
-        const int q = sq[lb];
-        if (q < 0) continue;
-        big_block_group(L, E, rr + (size_t)q * 40, Ainv + (size_t)q * 3136, x0 + 4 * (lb & 3), y0 + 4 * (lb >> 2), GW,
-                        FL, GB, [&](int f, int i, int j, double d) { GW(f, i, j) += d; }, S, t,
-                        [] { __syncthreads(); });
-        __syncthreads();
-    }
-    for (int q = t; q < 17 * 17; q += kTileThreads) {
-        const int a = q % 17, bb = q / 17;
-        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-        TileW W{sw};
-        if (bb < 16) w[gi] = W(0, a, bb);
-        if (a < 16) w[nn + gi] = W(1, a, bb);
-        if (a < 16 && bb < 16) w[2 * nn + gi] = W(2, a, bb);
-    }
+    cp_async_wait<0>();
 }
 
 // ---- setup: dense local matrices and their inverses --------------------------
@@ -480,6 +489,49 @@ __global__ void k_block_rows(Lev L, FaceList FL, EMat E, const int* __restrict__
         if (FL.face[mid] < key) lo = mid + 1; else hi = mid;
     }
     rr[idx] = (lo < FL.nf && FL.face[lo] == key) ? make_int2(E.rp[lo], E.rp[lo + 1]) : make_int2(0, 0);
+}
+
+// Slab packing (setup): row pointers + padded entry counts, then the entries
+// with pre-encoded columns.  tile_mode: columns inside the 20x20 region of the
+// block's 16x16 tile become shared-memory indices comp*400 + lj*20 + li, others
+// -(flat+1); otherwise (single-CTA coarse levels) the flat index itself.
+__global__ void k_slab_count(int nbig, const int* __restrict__ blk_ids, const int2* __restrict__ rr,
+                             int* __restrict__ rp, int* __restrict__ cnt, int* __restrict__ maxcnt) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nbig) return;
+    int rel = 0;
+    for (int t = 0; t < 40; ++t) {
+        rp[(size_t)q * 48 + t] = rel;
+        const int2 r = rr[(size_t)q * 40 + t];
+        rel += r.y - r.x;
+    }
+    for (int t = 40; t < 47; ++t) rp[(size_t)q * 48 + t] = rel;
+    rp[(size_t)q * 48 + 47] = blk_ids[q];  // owner block id (used by the coarse kernel)
+    cnt[q] = (rel + 3) & ~3;
+    atomicMax(maxcnt, rel);
+}
+
+__global__ void k_slab_fill(Lev L, int nbig, const int* __restrict__ blk_ids, const int2* __restrict__ rr, EMat E,
+                            const int* __restrict__ off, const int* __restrict__ rp, int* __restrict__ col,
+                            double* __restrict__ val, int tile_mode) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nbig * 40) return;
+    const int q = idx / 40, t = idx % 40, n = L.n, nn = L.nn, nbk = n >> 2;
+    const int B = blk_ids[q];
+    const int x0 = ((B % nbk) >> 2) * 16, y0 = ((B / nbk) >> 2) * 16;
+    const int2 r = rr[idx];
+    int o = off[q] + rp[(size_t)q * 48 + t];
+    for (int e = r.x; e < r.y; ++e, ++o) {
+        const int c = E.col[e];
+        int enc = c;
+        if (tile_mode) {
+            const int comp = c >= nn, f = c - comp * nn;
+            const int li = wr((f & (n - 1)) - x0 + 2, n), lj = wr(f / n - y0 + 2, n);
+            enc = (li < kReg && lj < kReg) ? comp * kReg * kReg + lj * kReg + li : -(c + 1);
+        }
+        col[o] = enc;
+        val[o] = E.val[e];
+    }
 }
 
 // Block sort keys: colour (bx mod 4) + 4 (by mod 4) for big blocks, 16 otherwise.
