@@ -42,10 +42,25 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+FACADE_SRC = os.path.join(ROOT, "tests", "cpp", "facade_step.cpp")
+FACADE_BIN = os.path.join(ROOT, "tests", "cpp", "facade_step")
+
+
+def build_facade_test() -> str:
+    """C++ caller of the ibmg::b200 facade (include/ibmg/b200.hpp) linked to the library."""
+    deps = [FACADE_SRC, LIB, os.path.join(ROOT, "include", "ibmg", "b200.hpp")]
+    if stale(FACADE_BIN, deps):
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+        subprocess.check_call([cxx, "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"), "-o", FACADE_BIN,
+                               FACADE_SRC, "-L", HERE, "-libmg_b200", "-Wl,-rpath," + HERE])
+    return FACADE_BIN
+
+
 def build_oracle() -> None:
     subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
 
 
 if __name__ == "__main__":
     build_cuda(force="--force" in sys.argv, verbose=True)
+    build_facade_test()
     build_oracle()
