@@ -39,10 +39,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "implicit IB step solve time (ms); fine-grid DOF·V-cycles/s vs HBM roofline"
-KAPPAS = [1e2, 1e4, 1e6]
-STEPS_PER_KAPPA = 10
-N_GRID = 256
-NB = 512
+
+
+def workloads():
+    """name -> (list of problem blocks, steps per block, description).  A bench
+    step is one implicit step; the state resets at the start of each block."""
+    from paper_1311_5614_b200 import configs
+    return {
+        "C2": ([configs.config2(k) for k in (1e2, 1e4, 1e6)], 10,
+               "C2: periodic N=256 MAC grid fp64, ellipse (0.5,0.5) a=0.3 b=0.15, Nb=512, "
+               "kappa {1e2,1e4,1e6} x 10 implicit steps, dt=1e-3, FGMRES(30)+V(1,1) box relaxation, rtol 1e-10"),
+        "C3": ([configs.config3()], 5,
+               "C3: periodic N=1024 MAC grid fp64, 16 circles (seed 0, r~U[0.03,0.06], ds=h/2, kappa 10^U[3,6]), "
+               "5 implicit steps, dt=1e-3, FGMRES(30)+V(1,1) box relaxation, rtol 1e-10"),
+        "C1": ([configs.config1()], 1,
+               "C1: periodic N=64, ellipse Nb=128, kappa=1e2, dt=1e-2, one implicit step"),
+    }
+
+
+WL = {}
 
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                  0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -50,22 +65,20 @@ THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_p
 
 
 def workload_config():
+    probs, per, desc = WL["blocks"], WL["per"], WL["desc"]
+    N = probs[0].N
     return {
-        "workload": "C2: periodic N=256 MAC grid fp64, ellipse (0.5,0.5) a=0.3 b=0.15, Nb=512, "
-                    "kappa {1e2,1e4,1e6} x 10 implicit steps, dt=1e-3, FGMRES(30)+V(1,1) box relaxation, rtol 1e-10",
-        "N": N_GRID, "Nb": NB, "kappas": KAPPAS, "steps_per_kappa": STEPS_PER_KAPPA, "dt": 1e-3,
-        "dof": 3 * N_GRID * N_GRID,
-        "l2": "flushed between timed steps (256 MiB write); working set ~100 MB",
+        "workload": desc, "name": WL["name"], "N": N, "Nb": [p.npts for p in probs],
+        "kappas": [p.kappa if len(p.kappa) > 1 else p.kappa[0] for p in probs], "steps_per_block": per,
+        "dt": probs[0].dt, "dof": 3 * N * N,
+        "l2": "flushed between timed steps (256 MiB write)",
     }
 
 
 def step_schedule(total):
-    """(kappa index, reset?) for steps 0..total-1 of the repeating C2 sequence."""
-    out = []
-    for s in range(total):
-        kb = (s // STEPS_PER_KAPPA) % len(KAPPAS)
-        out.append((kb, s % STEPS_PER_KAPPA == 0))
-    return out
+    """(block index, reset?) for steps 0..total-1 of the repeating workload sequence."""
+    per, nblocks = WL["per"], len(WL["blocks"])
+    return [((s // per) % nblocks, s % per == 0) for s in range(total)]
 
 
 class ClockSampler:
@@ -129,13 +142,13 @@ def measured_peak_hbm():
 def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     """Algorithmic (compulsory fp64) bytes of all launches of `name` in the
     profiled pass (SURVEY.md §8d per-cell figures x cells)."""
-    lv = ctxinfo["levels"]  # list of (n, nbig) for multi-tile levels (n > 32)
+    lv = ctxinfo["levels"]  # list of (n, nbig) for multi-tile levels (n >= 32)
     sweeps = 2  # V(1,1)
     N = ctxinfo["N"]
-    if name == "k_plain_tiles":
+    if name == "k_plain_tiles":  # 4 tile-colour launches cover every cell once per sweep
         return sum(72 * n * n * sweeps for n, _ in lv) * vcycles
-    if name == "k_big_sweep":
-        return sum((3136 * 8 + 56 * 24) * nb * sweeps for _, nb in lv) * vcycles
+    if name == "k_big_phase":  # inverse + E' slab (~2000 entries x 12 B) + block w/b traffic
+        return sum((3136 * 8 + 2000 * 12 + 56 * 24) * nb * sweeps for _, nb in lv) * vcycles
     if name == "k_residual_restrict":
         return sum(54 * n * n for n, _ in lv) * vcycles
     if name == "k_prolong_add":
@@ -147,18 +160,19 @@ def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
 
 def run_ours(args, rank, world):
     import torch
-    from paper_1311_5614_b200 import configs
     from paper_1311_5614_b200.ibmg import SaddleSystem
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    probs = [configs.config2(k, N=N_GRID, nb=NB) for k in KAPPAS]
+    probs = WL["blocks"]
+    N_GRID = probs[0].N
     ctxs = [SaddleSystem.from_problem(p, device=dev) for p in probs]
     n2 = N_GRID * N_GRID
+    NBs = [p.npts for p in probs]
     X0 = [torch.tensor(p.X.reshape(-1), dtype=torch.float64, device=f"cuda:{dev}") for p in probs]
     u = torch.zeros(2 * n2, dtype=torch.float64, device=f"cuda:{dev}")
     p = torch.zeros(n2, dtype=torch.float64, device=f"cuda:{dev}")
-    X = torch.empty_like(X0[0])
+    X = torch.empty(max(x.numel() for x in X0), dtype=torch.float64, device=f"cuda:{dev}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     streams = [torch.cuda.ExternalStream(c.stream, device=f"cuda:{dev}") for c in ctxs]
 
@@ -166,16 +180,17 @@ def run_ours(args, rank, world):
         nonlocal X
         ms, iters, setup, restarts, conv = [], [], [], [], True
         for kb, reset in step_schedule(total):
+            Xk = X[: X0[kb].numel()]
             if reset:
                 u.zero_()
                 p.zero_()
-                X.copy_(X0[kb])
+                Xk.copy_(X0[kb])
             flush.zero_()
             torch.cuda.synchronize()
             if timed:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(streams[kb])
-            st = ctxs[kb].step_implicit(u, p, X)
+            st = ctxs[kb].step_implicit(u, p, Xk)
             if timed:
                 e1.record(streams[kb])
                 e1.synchronize()
@@ -224,20 +239,21 @@ def run_ours(args, rank, world):
         t0 = time.perf_counter()
         ctxs[kb].step_implicit(uh, ph, Xh)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    h2d = 8 * (2 * n2 + 2 * NB)
-    d2h = 8 * (2 * n2 + n2 + 2 * NB)
+    h2d = 8 * (2 * n2 + 2 * int(np.mean(NBs)))
+    d2h = 8 * (2 * n2 + n2 + 2 * int(np.mean(NBs)))
 
     result = None
     if rank == 0:
         # profiled pass (live CUDA-event timing per kernel): first step of each kappa
         prof_tot = {}
         pv, pit, prs = 0, 0, 0
-        for kb in range(len(KAPPAS)):
+        for kb in range(len(probs)):
             u.zero_()
             p.zero_()
-            X.copy_(X0[kb])
+            Xk = X[: X0[kb].numel()]
+            Xk.copy_(X0[kb])
             ctxs[kb].profile(True)
-            st = ctxs[kb].step_implicit(u, p, X)
+            st = ctxs[kb].step_implicit(u, p, Xk)
             rep = ctxs[kb].profile_report()
             ctxs[kb].profile(False)
             for k, (tms, cnt) in rep.items():
@@ -250,11 +266,10 @@ def run_ours(args, rank, world):
         step_prof_ms = sum(v[0] for v in prof_tot.values())
         ranked = sorted(prof_tot.items(), key=lambda kv: -kv[1][0])
         levels = []
-        n = N_GRID
         c0 = ctxs[0]
         for l in range(c0.num_levels):
             nl = c0.level_n(l)
-            if nl > 32:
+            if nl >= 32:
                 levels.append((nl, None))
         # big-block counts per level per kappa context (averaged)
         lv_info = []
@@ -290,8 +305,8 @@ def run_ours(args, rank, world):
 def cpu_oracle_steps(steps_sched, threads):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    from paper_1311_5614_b200 import configs
-    probs = [configs.config2(k, N=N_GRID, nb=NB) for k in KAPPAS]
+    probs = WL["blocks"]
+    N_GRID = probs[0].N
     ctxs = [O.Oracle(pr, threads=threads) for pr in probs]
     ms, iters = [], []
     u = X = None
@@ -308,12 +323,13 @@ def cpu_oracle_steps(steps_sched, threads):
 
 def cpu_baseline(threads):
     sched = []
-    for kb in range(len(KAPPAS)):
-        sched += [(kb, True), (kb, False)]
+    per = 2 if WL["name"] == "C2" else 1
+    for kb in range(len(WL["blocks"])):
+        sched += [(kb, True)] + [(kb, False)] * (per - 1)
     ms, iters = cpu_oracle_steps(sched, threads)
     return {"value": round(float(np.mean(ms)), 3), "unit": "ms", "cores": threads, "kind": "port",
-            "sample": f"first 2 implicit C2 steps of each kappa (6 steps, {sum(iters)} V-cycles) on the CPU oracle "
-                      f"(oracle/ibmg_oracle.cpp, OpenMP {threads} threads); ms per step"}
+            "sample": f"first {per} implicit {WL['name']} step(s) of each block ({len(sched)} steps, {sum(iters)} "
+                      f"V-cycles) on the CPU oracle (oracle/ibmg_oracle.cpp, OpenMP {threads} threads); ms per step"}
 
 
 def main():
@@ -323,7 +339,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3"])
     args = ap.parse_args()
+    blocks, per, desc = workloads()[args.config]
+    WL.update(name=args.config, blocks=blocks, per=per, desc=desc)
+    N_GRID = blocks[0].N
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     threads = os.cpu_count() or 1
@@ -338,7 +358,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 geometry)", "impl": "reference",
                 "config": dict(workload_config(), parallelism="CPU oracle port, OpenMP over independent boxes"),
-                "dof_vcycles_per_s": 3 * N_GRID ** 2 * sum(iters) / (sum(ms) * 1e-3),
+                "dof_vcycles_per_s": 3 * WL["blocks"][0].N ** 2 * sum(iters) / (sum(ms) * 1e-3),
                 "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "port",
                                  "sample": f"{args.steps} C2 implicit steps ({sum(iters)} V-cycles) on the CPU oracle "
                                            "(the reference ships no solver; SURVEY.md §0)"},
@@ -355,12 +375,13 @@ def main():
     if rank == 0:
         ms_step = res["total_ms_max"] / args.steps
         dofv = 3 * N_GRID ** 2 * res["vcyc_all"] / (res["total_ms_max"] * 1e-3)
+        line_extra = {}
         peak, _ = measured_peak_hbm()
         line = {
             "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 geometry, u0 = 0)",
-            "config": dict(workload_config(), parallelism=f"replicas x{world} (C2 does not shard)"),
+            "config": dict(workload_config(), parallelism=f"replicas x{world} ({args.config} runs one problem per GPU)"),
             "dof_vcycles_per_s": dofv,
             "dof_vcycles_roofline_frac": dofv * 112 / (peak * 1e9 * world),
             "vcycles_per_step": round(res["vcyc_all"] / world / args.steps, 2),

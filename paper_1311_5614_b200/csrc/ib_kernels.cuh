@@ -176,7 +176,7 @@ __global__ void k_mark_big(int npts, Win W, int n, uint8_t* flags) {
 
 // Reach of E' on a level: the extent (in face index units) of the union of
 // L_k and R_{k-1}, R_k, R_{k+1} supports, max over points and components.
-// Same-colour big blocks are 12 cells apart, so the schedule requires <= 12.
+// Same-colour big blocks are >= 8 cells apart, so the schedule requires <= 7.
 __global__ void k_reach(int npts, Win W, Pts P, int* out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= npts) return;
@@ -210,66 +210,80 @@ __global__ void k_point_force(Win W, Pts P, int n, const double* __restrict__ w,
     F[2 * k + 1] = point_force(W, P, k, 1, n, acc);
 }
 
-// out[face] += sign * sum_{(k, l) in list(face)} l * F[k][comp]   (deterministic
-// spread: entries in ascending point order, no atomics).
+// out[face] += sign * sum_{(k, l) in list(face)} l * F[k][comp]: one warp per
+// face (lists run to hundreds of entries on coarse levels), lanes strided over
+// the entries, fixed butterfly reduction (deterministic spread: no atomics).
 __global__ void k_face_gather(FaceList FL, Win W, const double* __restrict__ F, double* __restrict__ out,
                               int nn, double sign) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (q >= FL.nf) return;
     const int face = FL.face[q];
     const int comp = face >= nn;
     double s = 0.0;
-    for (int e = FL.off[q]; e < FL.off[q + 1]; ++e) {
+    for (int e = FL.off[q] + lane; e < FL.off[q + 1]; e += 32) {
         const int v = FL.ent[e];
         const int k = v >> 5;
         s += W.w[(size_t)k * 64 + (v & 31)] * F[2 * k + comp];
     }
-    out[face] += sign * s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[face] += sign * s;
 }
 
-// Assembly of E'_l rows, one warp per face-list row, accumulated in a 32x32
-// shared-memory patch of column offsets (slot = wr(col - row + 16, n)) in a
-// fixed order (entries ascending in point, windows k-1, k, k+1): deterministic.
-// pass 0 writes the row's nonzero count, pass 1 the (col, val) pairs.
-constexpr int kEWarps = 4;
+// Assembly of E'_l rows, one warp per face-list row, accumulated in a 16x16
+// shared-memory patch of column offsets (slot = wr(col - row + 8, n); the E'
+// reach is <= 7, checked at setup) in a fixed order (entry pairs ascending in
+// point, windows k-1, k, k+1, lower half-warp first): deterministic.  pass 0
+// writes the row's nonzero count, pass 1 the (col, val) pairs.
+constexpr int kEWarps = 8;
 __global__ void __launch_bounds__(32 * kEWarps) k_erows(FaceList FL, Win W, Pts P, int n, int pass, EMat E,
                                                          int* __restrict__ cnt) {
-    __shared__ double patch[kEWarps][1024];
+    __shared__ double patch[kEWarps][256];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = blockIdx.x * kEWarps + wid;
     if (q >= FL.nf) return;
     double* pt = patch[wid];
-    for (int s = lane; s < 1024; s += 32) pt[s] = 0.0;
+    for (int s = lane; s < 256; s += 32) pt[s] = 0.0;
     __syncwarp();
     const int nn = n * n, face = FL.face[q], comp = face >= nn;
     const int f = face - comp * nn, di = f & (n - 1), dj = f / n;
-    for (int e = FL.off[q]; e < FL.off[q + 1]; ++e) {
-        const int v = FL.ent[e];
+    const int half = lane >> 4, e16 = lane & 15;
+    for (int e0 = FL.off[q]; e0 < FL.off[q + 1]; e0 += 2) {
+        const int e = e0 + half;
+        const bool act = e < FL.off[q + 1];
+        const int v = act ? FL.ent[e] : 0;
         const int k = v >> 5;
-        const double lc = W.w[(size_t)k * 64 + (v & 31)] * P.cE[k];
+        const double lc = act ? W.w[(size_t)k * 64 + (v & 31)] * P.cE[k] : 0.0;
         const int ks[3] = {P.kprev[k], k, P.knext[k]};
         const double coef[3] = {1.0, -2.0, 1.0};
         for (int t = 0; t < 3; ++t) {
-            if (lane < 16) {
+            int slot = -1;
+            double add = 0.0;
+            if (act) {
                 const int kk = ks[t];
-                const double r = W.w[(size_t)kk * 64 + (2 + comp) * 16 + lane];
+                const double r = W.w[(size_t)kk * 64 + (2 + comp) * 16 + e16];
                 if (r != 0.0) {
                     const int4 o = W.orgR[kk];
                     const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
-                    const int sx = wr(i0 + (lane & 3) - di + 16, n), sy = wr(j0 + (lane >> 2) - dj + 16, n);
-                    pt[sy * 32 + sx] += lc * coef[t] * r;
+                    const int sx = wr(i0 + (e16 & 3) - di + 8, n), sy = wr(j0 + (e16 >> 2) - dj + 8, n);
+                    slot = (sx < 16 && sy < 16) ? sy * 16 + sx : -1;
+                    add = lc * coef[t] * r;
                 }
             }
+            if (half == 0 && slot >= 0) pt[slot] += add;
+            __syncwarp();
+            if (half == 1 && slot >= 0) pt[slot] += add;
             __syncwarp();
         }
     }
     int base = pass ? E.rp[q] : 0;
-    for (int y = 0; y < 32; ++y) {
-        const double v = pt[y * 32 + lane];
+    for (int y = 0; y < 8; ++y) {
+        const int s = y * 32 + lane;
+        const double v = pt[s];
         const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
         if (pass && v != 0.0) {
             const int pos = base + __popc(m & ((1u << lane) - 1u));
-            E.col[pos] = comp * nn + wr(di - 16 + lane, n) + wr(dj - 16 + y, n) * n;
+            E.col[pos] = comp * nn + wr(di - 8 + (s & 15), n) + wr(dj - 8 + (s >> 4), n) * n;
             E.val[pos] = v;
         }
         base += __popc(m);

@@ -60,6 +60,11 @@ void dfree(T*& p) {
 
 inline unsigned nblk(size_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
+// Capacity policy for per-step (structure-dependent) buffers: 1.5x headroom
+// so the lagged rebuild of later steps (moving structures) never reallocates
+// inside a timed step in practice (cudaFree synchronises the device).
+inline long grow_cap(long need, long cap) { return std::max<long>(need + need / 2 + 64, cap + cap / 2); }
+
 constexpr int kMaxColours = 32;
 
 struct LevelBuf {
@@ -334,7 +339,7 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb) {
     for (int k = 0; k <= ncol; ++k) lb.coff[k] = cnt[k];
     if (lb.blk_cap < nbig) {
         dfree(lb.blk_ids);
-        lb.blk_cap = std::max(nbig, 64);
+        lb.blk_cap = grow_cap(nbig, lb.blk_cap);
         lb.blk_ids = dalloc<int>(size_t(lb.blk_cap));
     }
     if (nbig) CK(cudaMemcpy(lb.blk_ids, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice));
@@ -447,7 +452,7 @@ void rebuild(ibmg_ctx* c) {
                 if (nnz[l] > lb.e_cap) {
                     dfree(lb.E.col);
                     dfree(lb.E.val);
-                    lb.e_cap = std::max<long>(nnz[l], lb.e_cap * 5 / 4);
+                    lb.e_cap = grow_cap(nnz[l], lb.e_cap);
                     lb.E.col = dalloc<int>(size_t(lb.e_cap));
                     lb.E.val = dalloc<double>(size_t(lb.e_cap));
                 }
@@ -462,7 +467,7 @@ void rebuild(ibmg_ctx* c) {
             if (lb.ainv_cap < lb.nbig) {
                 dfree(lb.Ainv);
                 dfree(lb.rr);
-                lb.ainv_cap = std::max(lb.nbig, lb.ainv_cap * 5 / 4);
+                lb.ainv_cap = int(grow_cap(lb.nbig, lb.ainv_cap));
                 lb.Ainv = dalloc<double>(size_t(lb.ainv_cap) * 3136);
                 lb.rr = dalloc<int2>(size_t(lb.ainv_cap) * 40);
             }
@@ -501,7 +506,7 @@ void rebuild(ibmg_ctx* c) {
                 if (h[28] > lb.sl_cap) {
                     dfree(lb.sl_col);
                     dfree(lb.sl_val);
-                    lb.sl_cap = std::max<long>(h[28], lb.sl_cap * 5 / 4);
+                    lb.sl_cap = grow_cap(h[28], lb.sl_cap);
                     lb.sl_col = dalloc<int>(size_t(lb.sl_cap));
                     lb.sl_val = dalloc<double>(size_t(lb.sl_cap));
                 }
@@ -596,7 +601,7 @@ void apply_level(ibmg_ctx* c, int l, const double* w, double* out) {
     LAUNCH(c, k_stokes_apply, nblk(lb.L.nn), 256, 0, lb.L, w, out);
     if (c->npts && lb.FL.nf) {
         LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, w, c->F);
-        LAUNCH(c, k_face_gather, nblk(lb.FL.nf), 256, 0, lb.FL, lb.W, c->F, out, lb.L.nn, -1.0);
+        LAUNCH(c, k_face_gather, nblk(size_t(lb.FL.nf) * 32), 256, 0, lb.FL, lb.W, c->F, out, lb.L.nn, -1.0);
     }
 }
 
@@ -605,7 +610,7 @@ void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double
     LAUNCH(c, k_stokes_residual, nblk(lb.L.nn), 256, 0, lb.L, b, w, r);
     if (c->npts && lb.FL.nf) {
         LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, w, c->F);
-        LAUNCH(c, k_face_gather, nblk(lb.FL.nf), 256, 0, lb.FL, lb.W, c->F, r, lb.L.nn, 1.0);
+        LAUNCH(c, k_face_gather, nblk(size_t(lb.FL.nf) * 32), 256, 0, lb.FL, lb.W, c->F, r, lb.L.nn, 1.0);
     }
 }
 
@@ -691,7 +696,7 @@ void vcycle(ibmg_ctx* c, const double* b, double* z) {
             LAUNCH(c, k_residual_restrict, nblk(nx.L.nn), 256, 0, lb.L, lb.b, lb.w, nx.b);
             if (c->npts && nx.FL.nf) {
                 LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, lb.w, c->F);
-                LAUNCH(c, k_face_gather, nblk(nx.FL.nf), 256, 0, nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0);
+                LAUNCH(c, k_face_gather, nblk(size_t(nx.FL.nf) * 32), 256, 0, nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0);
             }
         }
         coarse_cycle(c, c->lev[c->lc].b, c->lev[c->lc].w);
@@ -815,7 +820,7 @@ void build_rhs(ibmg_ctx* c, const double* u, double* b) {
     LAUNCH(c, k_rhs_mass, nblk(c->M), 256, 0, u, b, size_t(l0.L.nn), c->prm.rho / c->prm.dt);
     if (c->npts && l0.FL.nf) {
         LAUNCH(c, k_rhs_force, nblk(c->npts, 128), 128, 0, c->P, c->X, c->F);
-        LAUNCH(c, k_face_gather, nblk(l0.FL.nf), 256, 0, l0.FL, l0.W, c->F, b, l0.L.nn, 1.0);
+        LAUNCH(c, k_face_gather, nblk(size_t(l0.FL.nf) * 32), 256, 0, l0.FL, l0.W, c->F, b, l0.L.nn, 1.0);
     }
 }
 
@@ -1153,7 +1158,7 @@ int ibmg_spread(ibmg_ctx* c, const double* Fin, double* f, int ptr_kind) {
         LevelBuf& l0 = c->lev[0];
         if (c->npts && l0.FL.nf) {
             LAUNCH(c, k_scale_dsq, nblk(c->npts, 128), 128, 0, c->P, dF, c->F);
-            LAUNCH(c, k_face_gather, nblk(l0.FL.nf), 256, 0, l0.FL, l0.W, c->F, df, l0.L.nn, 1.0);
+            LAUNCH(c, k_face_gather, nblk(size_t(l0.FL.nf) * 32), 256, 0, l0.FL, l0.W, c->F, df, l0.L.nn, 1.0);
         }
         S.back(f, df, 2 * nn);
         return IBMG_OK;

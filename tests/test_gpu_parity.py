@@ -144,3 +144,30 @@ def test_step_c1():
     assert rel(u, uo) < 1e-8
     assert rel(p, po) < 1e-8
     assert rel(X.reshape(-1, 2), Xo) < 1e-8
+
+
+def test_solve_c2_stiff():
+    """kappa = 1e6 (the stiff regime the big boxes target): parity at rtol 1e-10."""
+    prob = configs.config2(1e6)
+    g, o = pair(prob)
+    b = o.rhs(np.zeros(2 * prob.N ** 2))
+    xg, sg = g.gmres_solve(b)
+    xo, so, _ = o.solve(b)
+    assert sg["converged"] and so["converged"]
+    assert sg["iters"] <= so["iters"] + 2
+    assert rel(xg, xo) < 1e-8
+
+
+def test_step_c3():
+    """C3: 16 membranes (seed 0), N = 1024, one implicit step."""
+    prob = configs.config3()
+    g = SaddleSystem.from_problem(prob)
+    o = O.Oracle(prob, threads=16)
+    n = prob.N
+    u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+    sg = g.step_implicit(u, p, X)
+    uo, po, Xo, so = o.step(np.zeros(2 * n * n), prob.X)
+    assert sg["converged"] and so["converged"]
+    assert abs(sg["iters"] - so["iters"]) <= 2
+    assert rel(u, uo) < 1e-8 and rel(p, po) < 1e-8
+    assert rel(X.reshape(-1, 2), Xo) < 1e-8
