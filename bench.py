@@ -52,6 +52,9 @@ def workloads():
         "C3": ([configs.config3()], 5,
                "C3: periodic N=1024 MAC grid fp64, 16 circles (seed 0, r~U[0.03,0.06], ds=h/2, kappa 10^U[3,6]), "
                "5 implicit steps, dt=1e-3, FGMRES(30)+V(1,1) box relaxation, rtol 1e-10"),
+        "C4": ([configs.config4()], 1,
+               "C4: periodic N=8192 MAC grid fp64, 256 circular/elliptic membranes (seed 1, r~U[0.005,0.015], aspect "
+               "U[1,2], ds=h/2, kappa 10^U[3,6]), one implicit step, dt=1e-4, FGMRES(30)+V(1,1), rtol 1e-10, 1 GPU"),
         "C1": ([configs.config1()], 1,
                "C1: periodic N=64, ellipse Nb=128, kappa=1e2, dt=1e-2, one implicit step"),
     }
@@ -339,7 +342,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     args = ap.parse_args()
     blocks, per, desc = workloads()[args.config]
     WL.update(name=args.config, blocks=blocks, per=per, desc=desc)

@@ -184,6 +184,68 @@ __global__ void k_finish_dots(const double* __restrict__ partial, int nblk, doub
     if (threadIdx.x == 0) out[blockIdx.x] = accumulate ? out[blockIdx.x] + s : s;
 }
 
+// Fused CGS2 sweeps over the Krylov basis (one read of w and of each V_i per
+// sweep; K accumulators in registers):
+//   MODE 0: partial[i] = V_i . w
+//   MODE 1: w -= sum_i h[i] V_i, then partial[i] = V_i . w_new
+//   MODE 2: w -= sum_i h[i] V_i, then partial[0] = w_new . w_new
+// Per-block partial sums are reduced in a fixed order (warp butterfly, then
+// the warps in index order), so the dots are deterministic.
+constexpr int kCgsBlocks = 592;  // 4 per SM; fixed => reduction order fixed
+template <int MODE, int KMAX>
+__global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 ? 2 : 1))
+    k_cgs_sweep(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
+                double* __restrict__ w, size_t m, double* __restrict__ partial) {
+    constexpr int NACC = MODE == 2 ? 1 : KMAX;
+    __shared__ double hs[KMAX];
+    __shared__ double red[kRedThreads / 32][NACC];
+    if (MODE > 0 && threadIdx.x < KMAX) hs[threadIdx.x] = threadIdx.x < k ? h[threadIdx.x] : 0.0;
+    __syncthreads();
+    double acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
+        double x = w[q];
+        if (MODE == 0) {
+            // batches of 8 independent loads issued back to back, then the FMAs
+#pragma unroll
+            for (int i0 = 0; i0 < KMAX; i0 += 8) {
+                double v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = (i0 + i < k) ? __ldcs(V + stride * (i0 + i) + q) : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i0 + i] += v[i] * x;
+            }
+        } else {
+            double v[KMAX];
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i) v[i] = (i < k) ? __ldcs(V + stride * i + q) : 0.0;
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i) x -= hs[i] * v[i];
+            w[q] = x;
+            if (MODE == 2) {
+                acc[0] += x * x;
+            } else {
+#pragma unroll
+                for (int i = 0; i < NACC; ++i) acc[i] += v[i] * x;
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) {
+        const double t = warp_sum(acc[i]);
+        if (lane == 0) red[wid][i] = t;
+    }
+    __syncthreads();
+    const int kk = MODE == 2 ? 1 : k;
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+        double t = 0.0;
+        for (int ww = 0; ww < kRedThreads / 32; ++ww) t += red[ww][i];
+        partial[(size_t)i * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 // w -= sum_{i<k} h[i] V_i   (one pass over w and the V's).
 __global__ void k_multi_axpy_sub(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
                                  double* __restrict__ w, size_t m) {
