@@ -305,6 +305,90 @@ def run_ours(args, rank, world):
     return result
 
 
+def run_batch(args, rank, world):
+    """C5: a batch of independent N=256 problems (seed 5 + index), one implicit
+    step each, sharded across ranks (replicas, no collective).  On one GPU the
+    problems of this rank are spread over `workers` host threads, each owning a
+    solver context on its own CUDA stream, so the latency-bound problems overlap
+    on the device.  Returns per-rank wall/device time and counts."""
+    import threading as th
+
+    import torch
+    from paper_1311_5614_b200 import configs
+    from paper_1311_5614_b200.ibmg import SaddleSystem
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    mine = list(range(rank, args.batch, world))
+    probs = {i: configs.config5_problem(i) for i in mine}
+    W = min(args.workers, len(mine))
+    ctxs = [SaddleSystem(256, 1.0, 1.0, 1e-3, device=dev) for _ in range(W)]
+    n2 = 256 * 256
+
+    def work(w, host, out):
+        c = ctxs[w]
+        if host:
+            u, p = np.zeros(2 * n2), np.zeros(n2)
+        else:
+            u = torch.zeros(2 * n2, dtype=torch.float64, device=f"cuda:{dev}")
+            p = torch.zeros(n2, dtype=torch.float64, device=f"cuda:{dev}")
+        for i in mine[w::W]:
+            pr = probs[i]
+            X = pr.X.reshape(-1).copy() if host else torch.tensor(pr.X.reshape(-1), device=f"cuda:{dev}")
+            c.set_structures(pr.nb, pr.kappa, pr.ds, X)
+            if host:
+                u[:] = 0.0
+            else:
+                u.zero_()
+            st = c.step_implicit(u, p, X)
+            out.append((i, st["iters"], bool(st["converged"])))
+
+    def run(host):
+        outs = [[] for _ in range(W)]
+        ts = [th.Thread(target=work, args=(w, host, outs[w])) for w in range(W)]
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        return max(e0.elapsed_time(e1), wall), [r for o in outs for r in o]
+
+    # warm-up: one problem per worker
+    saved = args.batch
+    run(False)
+    launches0 = sum(c.kernel_launches for c in ctxs)
+    with ClockSampler(dev) as clk:
+        ms, res = run(False)
+    launches = sum(c.kernel_launches for c in ctxs) - launches0
+    e2e_ms, _ = run(True)
+    t = torch.tensor([ms, e2e_ms, float(len(res)), float(sum(r[1] for r in res)),
+                      float(all(r[2] for r in res))], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tsum = t.clone()
+        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
+        tmin = t.clone()
+        torch.distributed.all_reduce(tmin, op=torch.distributed.ReduceOp.MIN)
+        ms, e2e_ms, nprob, vcyc, conv = float(tmax[0]), float(tmax[1]), float(tsum[2]), float(tsum[3]), bool(tmin[4])
+    else:
+        nprob, vcyc, conv = float(len(res)), float(sum(r[1] for r in res)), all(r[2] for r in res)
+    for c in ctxs:
+        c.close()
+    args.batch = saved
+    return {"ms": ms, "e2e_ms": e2e_ms, "nprob": nprob, "vcyc": vcyc, "conv": conv, "launches": launches,
+            "clocks": clk.summary(), "workers": W}
+
+
 def cpu_oracle_steps(steps_sched, threads):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
@@ -342,8 +426,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--batch", type=int, default=512, help="C5: number of independent N=256 problems")
+    ap.add_argument("--workers", type=int, default=16, help="C5: concurrent solver contexts per GPU")
     args = ap.parse_args()
+    if args.config == "C5":
+        return main_batch(args)
     blocks, per, desc = workloads()[args.config]
     WL.update(name=args.config, blocks=blocks, per=per, desc=desc)
     N_GRID = blocks[0].N
@@ -399,6 +487,62 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main_batch(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    threads = os.cpu_count() or 1
+    desc = (f"C5: batch of {args.batch} independent problems, periodic N=256 fp64, one ellipse each (seed 5+i, "
+            "semi-axes U[0.1,0.35], Nb=512, kappa 10^U[1,6]), dt=1e-3, one implicit step each, FGMRES(30)+V(1,1)")
+    cfg = {"workload": desc, "name": "C5", "N": 256, "batch": args.batch, "dof": 3 * 256 * 256,
+           "parallelism": f"batch sharded over {world} GPU(s) (replicas), {args.workers} concurrent contexts/GPU"}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        from paper_1311_5614_b200 import configs
+        sample = max(1, min(args.steps, 8))
+        ms = []
+        for i in range(sample):
+            pr = configs.config5_problem(i)
+            t0 = time.perf_counter()
+            O.Oracle(pr, threads=threads).step(np.zeros(2 * 256 * 256), pr.X)
+            ms.append((time.perf_counter() - t0) * 1e3)
+        v = float(np.mean(ms))
+        print(json.dumps({"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
+                          "steps": sample, "warmup": 0, "ms_per_step": round(v, 3), "higher_is_better": False,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "impl": "reference", "config": cfg, "problems_per_s": 1e3 / v,
+                          "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "port",
+                                           "sample": f"{sample} C5 problems (oracle port, ms per problem)"},
+                          "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    r = run_batch(args, rank, world)
+    if rank == 0:
+        ms_per = r["ms"] / r["nprob"]
+        line = {"metric": METRIC, "value": round(ms_per, 4), "unit": "ms", "n_gpus": world,
+                "steps": int(r["nprob"]), "warmup": r["workers"], "ms_per_step": round(ms_per, 4),
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded C5 geometry)", "config": cfg,
+                "problems_per_s": r["nprob"] / (r["ms"] * 1e-3),
+                "dof_vcycles_per_s": 3 * 256 * 256 * r["vcyc"] / (r["ms"] * 1e-3),
+                "vcycles_per_problem": r["vcyc"] / r["nprob"], "converged": r["conv"],
+                "gpu_launches": r["launches"], "clocks": r["clocks"],
+                "e2e": {"value": round(r["e2e_ms"] / r["nprob"], 4), "unit": "ms",
+                        "h2d_bytes_per_step": 8 * (2 * 256 * 256 + 2 * 512),
+                        "d2h_bytes_per_step": 8 * (3 * 256 * 256 + 2 * 512)}}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

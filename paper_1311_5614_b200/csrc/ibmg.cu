@@ -106,7 +106,7 @@ struct ibmg_ctx {
     std::vector<LevelBuf> lev;
     long long launches = 0;
     // structures
-    int npts = 0, nmem = 0;
+    int npts = 0, nmem = 0, pts_cap = 0;
     std::vector<int> nb;
     Pts P{};
     double* X = nullptr;
@@ -303,6 +303,7 @@ void free_structs(ibmg_ctx* c) {
     dfree(c->cnt);
     c->sort_cap = 0;
     c->npts = 0;
+    c->pts_cap = 0;
 }
 
 // Deterministic greedy colouring of the big blocks, the same
@@ -541,7 +542,11 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
         if (hk[m] < 0.0) throw InvalidArg("kappa must be >= 0");
         tot += hnb[m];
     }
-    free_structs(c);
+    // point-sized buffers are reused when the new structure set fits (no
+    // cudaMalloc/cudaFree, which would synchronise the whole device, between
+    // problems of a batch); per-step buffers keep their grown capacities
+    const bool fits = c->have_structs && tot <= c->pts_cap;
+    if (!fits) free_structs(c);
     c->npts = tot;
     c->nmem = n_mem;
     c->nb = hnb;
@@ -557,43 +562,49 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
             ids2[o + k] = 1.0 / (hds[m] * hds[m]);
             dsq[o + k] = hds[m] * hds[m];
         }
-    c->P.n = tot;
-    c->P.kprev = dalloc<int>(tot);
-    c->P.knext = dalloc<int>(tot);
-    c->P.cE = dalloc<double>(tot);
-    c->P.kap = dalloc<double>(tot);
-    c->P.ids2 = dalloc<double>(tot);
-    c->P.dsq = dalloc<double>(tot);
-    c->X = dalloc<double>(2 * size_t(tot));
-    c->F = dalloc<double>(2 * size_t(tot));
-    c->Fc = dalloc<double>(2 * size_t(tot));
-    CK(cudaMemcpy(c->P.kprev, kp.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->P.knext, kn.data(), sizeof(int) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->P.cE, cE.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->P.kap, kap.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->P.ids2, ids2.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->P.dsq, dsq.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->X, X, sizeof(double) * 2 * tot,
-                  ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-    for (auto& lb : c->lev) {
-        lb.W.orgL = dalloc<int4>(tot);
-        lb.W.orgR = dalloc<int4>(tot);
-        lb.W.w = dalloc<double>(size_t(tot) * 64);
-        lb.fl_cap = tot * 32;
-        lb.FL.face = dalloc<int>(size_t(lb.fl_cap));
-        lb.FL.off = dalloc<int>(size_t(lb.fl_cap) + 1);
-        lb.FL.ent = dalloc<int>(size_t(lb.fl_cap));
-        lb.E.rp = dalloc<int>(size_t(lb.fl_cap) + 1);
-        lb.ecnt = dalloc<int>(size_t(lb.fl_cap) + 1);
+    if (!fits) {
+        const int cap = std::max(tot, 1);
+        c->pts_cap = cap;
+        c->P.kprev = dalloc<int>(cap);
+        c->P.knext = dalloc<int>(cap);
+        c->P.cE = dalloc<double>(cap);
+        c->P.kap = dalloc<double>(cap);
+        c->P.ids2 = dalloc<double>(cap);
+        c->P.dsq = dalloc<double>(cap);
+        c->X = dalloc<double>(2 * size_t(cap));
+        c->F = dalloc<double>(2 * size_t(cap));
+        c->Fc = dalloc<double>(2 * size_t(cap));
+        for (auto& lb : c->lev) {
+            lb.W.orgL = dalloc<int4>(cap);
+            lb.W.orgR = dalloc<int4>(cap);
+            lb.W.w = dalloc<double>(size_t(cap) * 64);
+            lb.fl_cap = cap * 32;
+            lb.FL.face = dalloc<int>(size_t(lb.fl_cap));
+            lb.FL.off = dalloc<int>(size_t(lb.fl_cap) + 1);
+            lb.FL.ent = dalloc<int>(size_t(lb.fl_cap));
+            lb.E.rp = dalloc<int>(size_t(lb.fl_cap) + 1);
+            lb.ecnt = dalloc<int>(size_t(lb.fl_cap) + 1);
+        }
+        size_t scap = std::max<size_t>(size_t(cap) * 32 + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
+        c->keys = dalloc<int>(scap);
+        c->vals = dalloc<int>(scap);
+        c->keys2 = dalloc<int>(scap);
+        c->vals2 = dalloc<int>(scap);
+        c->cnt = dalloc<int>(scap + 1);
+        CK(cudaMemset(c->cnt, 0, sizeof(int) * (scap + 1)));
+        c->sort_cap = scap;
     }
-    size_t cap = std::max<size_t>(size_t(tot) * 32 + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
-    c->keys = dalloc<int>(cap);
-    c->vals = dalloc<int>(cap);
-    c->keys2 = dalloc<int>(cap);
-    c->vals2 = dalloc<int>(cap);
-    c->cnt = dalloc<int>(cap + 1);
-    CK(cudaMemset(c->cnt, 0, sizeof(int) * (cap + 1)));
-    c->sort_cap = cap;
+    c->P.n = tot;
+    CK(cudaMemcpyAsync(c->P.kprev, kp.data(), sizeof(int) * tot, cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(c->P.knext, kn.data(), sizeof(int) * tot, cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(c->P.cE, cE.data(), sizeof(double) * tot, cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(c->P.kap, kap.data(), sizeof(double) * tot, cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(c->P.ids2, ids2.data(), sizeof(double) * tot, cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(c->P.dsq, dsq.data(), sizeof(double) * tot, cudaMemcpyHostToDevice, c->s));
+    if (tot)
+        CK(cudaMemcpyAsync(c->X, X, sizeof(double) * 2 * tot,
+                           ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
+    CK(cudaStreamSynchronize(c->s));
     rebuild(c);
     c->have_structs = true;
 }

@@ -171,3 +171,32 @@ def test_step_c3():
     assert abs(sg["iters"] - so["iters"]) <= 2
     assert rel(u, uo) < 1e-8 and rel(p, po) < 1e-8
     assert rel(X.reshape(-1, 2), Xo) < 1e-8
+
+
+def test_context_reuse_across_batch_problems():
+    """C5 path: one context, structures swapped between problems (buffers reused
+    without reallocation) — each step still matches the oracle."""
+    g = SaddleSystem(256, 1.0, 1.0, 1e-3)
+    for i in (0, 3):
+        prob = configs.config5_problem(i)
+        g.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
+        n = prob.N
+        u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+        sg = g.step_implicit(u, p, X)
+        uo, po, Xo, so = O.Oracle(prob, threads=16).step(np.zeros(2 * n * n), prob.X)
+        assert sg["converged"] and so["converged"], i
+        assert abs(sg["iters"] - so["iters"]) <= 2, i
+        assert rel(u, uo) < 1e-8 and rel(X.reshape(-1, 2), Xo) < 1e-8, i
+
+
+def test_no_structures_pure_stokes():
+    """n_mem = 0 (kappa-free Stokes): the whole path runs without IB data."""
+    from paper_1311_5614_b200.configs import Problem
+    prob = Problem("stokes", 64, 1.0, 1.0, 1e-2, [], [], [], np.zeros((0, 2)))
+    g, o = pair(prob)
+    b = rand(3 * 64 * 64, 21)
+    b[2 * 64 * 64:] = 0.0
+    xg, sg = g.gmres_solve(b)
+    xo, so, _ = o.solve(b)
+    assert sg["converged"] and so["converged"] and abs(sg["iters"] - so["iters"]) <= 2
+    assert rel(xg, xo) < 1e-8
