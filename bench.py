@@ -215,17 +215,9 @@ def run_ours(args, rank, world):
     launches = sum(c.kernel_launches for c in ctxs) - launches0
     if world > 1:
         torch.distributed.barrier()
-    total_ms = float(sum(ms))
-    vcyc = int(sum(iters))
-    t = torch.tensor([total_ms, float(vcyc)], dtype=torch.float64, device=f"cuda:{dev}")
-    if world > 1:
-        tmax = t.clone()
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-        tsum = t.clone()
-        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
-        total_ms_max, vcyc_all = float(tmax[0]), float(tsum[1])
-    else:
-        total_ms_max, vcyc_all = total_ms, float(vcyc)
+    from paper_1311_5614_b200 import dist as D
+    tmax, tsum, _ = D.reduce_stats([float(sum(ms)), float(sum(iters))], device=f"cuda:{dev}")
+    total_ms_max, vcyc_all = float(tmax[0]), float(tsum[1])
 
     # e2e: same steps through the C ABI with host numpy buffers (copies inside)
     e2e_ms = []
@@ -319,7 +311,8 @@ def run_batch(args, rank, world):
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    mine = list(range(rank, args.batch, world))
+    from paper_1311_5614_b200 import dist as D
+    mine = D.shard(args.batch, rank, world)
     probs = {i: configs.config5_problem(i) for i in mine}
     W = min(args.workers, len(mine))
     ctxs = [SaddleSystem(256, 1.0, 1.0, 1e-3, device=dev) for _ in range(W)]
@@ -370,18 +363,9 @@ def run_batch(args, rank, world):
         ms, res = run(False)
     launches = sum(c.kernel_launches for c in ctxs) - launches0
     e2e_ms, _ = run(True)
-    t = torch.tensor([ms, e2e_ms, float(len(res)), float(sum(r[1] for r in res)),
-                      float(all(r[2] for r in res))], dtype=torch.float64, device=f"cuda:{dev}")
-    if world > 1:
-        tmax = t.clone()
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-        tsum = t.clone()
-        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
-        tmin = t.clone()
-        torch.distributed.all_reduce(tmin, op=torch.distributed.ReduceOp.MIN)
-        ms, e2e_ms, nprob, vcyc, conv = float(tmax[0]), float(tmax[1]), float(tsum[2]), float(tsum[3]), bool(tmin[4])
-    else:
-        nprob, vcyc, conv = float(len(res)), float(sum(r[1] for r in res)), all(r[2] for r in res)
+    tmax, tsum, tmin = D.reduce_stats([ms, e2e_ms, len(res), sum(r[1] for r in res), all(r[2] for r in res)],
+                                      device=f"cuda:{dev}")
+    ms, e2e_ms, nprob, vcyc, conv = float(tmax[0]), float(tmax[1]), float(tsum[2]), float(tsum[3]), bool(tmin[4])
     for c in ctxs:
         c.close()
     args.batch = saved
