@@ -291,6 +291,83 @@ __global__ void __launch_bounds__(32 * kEWarps) k_erows(FaceList FL, Win W, Pts 
     if (!pass && lane == 0) cnt[q] = base;
 }
 
+// Long-row variant of k_erows for coarse levels (a face there can collect
+// ~1e5 point entries): one 512-thread CTA per row, its 16 warps take
+// interleaved entry pairs into private 16x16 patches which are then summed in
+// warp order (deterministic), then compacted like k_erows.
+constexpr int kELongWarps = 16;
+__global__ void __launch_bounds__(32 * kELongWarps) k_erows_long(FaceList FL, Win W, Pts P, int n, int pass, EMat E,
+                                                                  int* __restrict__ cnt) {
+    __shared__ double patch[kELongWarps][256];
+    __shared__ double fin[256];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, q = blockIdx.x;
+    double* pt = patch[wid];
+    for (int s = lane; s < 256; s += 32) pt[s] = 0.0;
+    __syncwarp();
+    const int nn = n * n, face = FL.face[q], comp = face >= nn;
+    const int f = face - comp * nn, di = f & (n - 1), dj = f / n;
+    const int half = lane >> 4, e16 = lane & 15;
+    for (int e0 = FL.off[q] + 2 * wid; e0 < FL.off[q + 1]; e0 += 2 * kELongWarps) {
+        const int e = e0 + half;
+        const bool act = e < FL.off[q + 1];
+        const int v = act ? FL.ent[e] : 0;
+        const int k = v >> 5;
+        const double lc = act ? W.w[(size_t)k * 64 + (v & 31)] * P.cE[k] : 0.0;
+        const int ks[3] = {P.kprev[k], k, P.knext[k]};
+        const double coef[3] = {1.0, -2.0, 1.0};
+        for (int t = 0; t < 3; ++t) {
+            int slot = -1;
+            double add = 0.0;
+            if (act) {
+                const int kk = ks[t];
+                const double r = W.w[(size_t)kk * 64 + (2 + comp) * 16 + e16];
+                if (r != 0.0) {
+                    const int4 o = W.orgR[kk];
+                    const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+                    const int sx = wr(i0 + (e16 & 3) - di + 8, n), sy = wr(j0 + (e16 >> 2) - dj + 8, n);
+                    slot = (sx < 16 && sy < 16) ? sy * 16 + sx : -1;
+                    add = lc * coef[t] * r;
+                }
+            }
+            if (half == 0 && slot >= 0) pt[slot] += add;
+            __syncwarp();
+            if (half == 1 && slot >= 0) pt[slot] += add;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) {
+        double s = 0.0;
+        for (int w = 0; w < kELongWarps; ++w) s += patch[w][threadIdx.x];
+        fin[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (wid != 0) return;
+    int base = pass ? E.rp[q] : 0;
+    for (int y = 0; y < 8; ++y) {
+        const int s = y * 32 + lane;
+        const double v = fin[s];
+        const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
+        if (pass && v != 0.0) {
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            E.col[pos] = comp * nn + wr(di - 8 + (s & 15), n) + wr(dj - 8 + (s >> 4), n) * n;
+            E.val[pos] = v;
+        }
+        base += __popc(m);
+    }
+    if (!pass && lane == 0) cnt[q] = base;
+}
+
+// Longest face list of a level (runs counted by RLE; the INT_MAX sentinel run excluded).
+__global__ void k_rowlen_max(const int* __restrict__ face, const int* __restrict__ off, const int* __restrict__ nruns,
+                             int* __restrict__ out) {
+    const int nr = *nruns;
+    int m = 0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nr; q += gridDim.x * blockDim.x)
+        if (face[q] != 0x7fffffff) m = max(m, off[q + 1] - off[q]);
+    atomicMax(out, m);
+}
+
 // Fiber force density of the RHS times the spread quadrature:
 // F_k ds^2 = kappa (X_{k-1} + X_{k+1} - 2 X_k)/ds^2 * ds^2  (fiber.cpp:34-55, 93).
 __global__ void k_rhs_force(Pts P, const double* __restrict__ X, double* __restrict__ F) {

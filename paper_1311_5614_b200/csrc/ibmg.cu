@@ -75,6 +75,7 @@ struct LevelBuf {
     int fl_cap = 0;
     EMat E{};
     int* ecnt = nullptr;
+    int maxrow = 0;          // longest face list (selects the E'-row assembly kernel)
     long e_cap = 0;
     uint8_t* big = nullptr;
     int nbig = 0;
@@ -359,6 +360,15 @@ void check_err_flag(ibmg_ctx* c, const char* where) {
     if (h & 2) throw CudaError(std::string(where) + ": singular local box matrix");
 }
 
+// E'_l row assembly: warp per row, or CTA per row on levels whose face lists
+// run long (coarse levels, where each face collects many points).
+void erows(ibmg_ctx* c, LevelBuf& lb, int pass) {
+    if (lb.maxrow > 256)
+        LAUNCH(c, k_erows_long, lb.FL.nf, 32 * kELongWarps, 0, lb.FL, lb.W, c->P, lb.L.n, pass, lb.E, lb.ecnt);
+    else
+        LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, pass, lb.E, lb.ecnt);
+}
+
 // Rebuild every per-level structure datum from the device positions c->X
 // (the lagged operators of one step).
 void rebuild(ibmg_ctx* c) {
@@ -401,7 +411,8 @@ void rebuild(ibmg_ctx* c) {
             cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, lb.FL.off, items + 1, c->s);
             ensure_cub(c, bytes);
             CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, lb.FL.off, items + 1, c->s));
-            // c->cnt must be zero past the runs for the scan's tail; entries past nf are ignored anyway
+            LAUNCH(c, k_rowlen_max, 64, 256, 0, lb.FL.face, lb.FL.off, c->counters + l * kCtr + 17,
+                   c->counters + l * kCtr + 29);
             ++c->launches;  // account the CUB launches coarsely (sort+rle+scan)
         }
         // big-block marking, colour sort, reach
@@ -426,6 +437,7 @@ void rebuild(ibmg_ctx* c) {
                 if (last == 0x7fffffff) --runs;
             }
             lb.FL.nf = runs;
+            lb.maxrow = h[29];
             if (l + 1 < c->nlev) {
                 const int reach = h[18];
                 if (reach > 7)
@@ -439,7 +451,7 @@ void rebuild(ibmg_ctx* c) {
             LevelBuf& lb = c->lev[l];
             if (lb.FL.nf == 0) continue;
             CK(cudaMemsetAsync(lb.ecnt, 0, sizeof(int) * (lb.FL.nf + 1), c->s));
-            LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, 0, lb.E, lb.ecnt);
+            erows(c, lb, 0);
             size_t bytes = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, bytes, lb.ecnt, lb.E.rp, lb.FL.nf + 1, c->s);
             ensure_cub(c, bytes);
@@ -462,8 +474,7 @@ void rebuild(ibmg_ctx* c) {
                     lb.E.col = dalloc<int>(size_t(lb.e_cap));
                     lb.E.val = dalloc<double>(size_t(lb.e_cap));
                 }
-                LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, 1, lb.E,
-                       lb.ecnt);
+                erows(c, lb, 1);
             }
         }
         // per-level big-block face indices and inverses
