@@ -1,10 +1,10 @@
-// coarse_kernel.cuh — the bottom of the V-cycle (levels with n <= 16) in ONE
+// coarse_kernel.cuh — the bottom of the V-cycle (levels with n <= 32) in ONE
 // CTA, entirely in shared memory: sweeps (same schedule as the oracle), the
 // residual with the E' part, restriction, the dense bordered coarsest solve,
 // prolongation.  Removes the latency-bound tail of Algorithm 1
-// from the launch stream.  At n <= 16 every big-block
-// colour holds one block, so the big phase is a sequence whose slabs are
-// double-buffered into shared memory ahead of use.
+// from the launch stream.  The big phase runs its colour
+// classes in order, the blocks of a class one after another (a valid order of
+// an independent set), their slabs double-buffered into shared memory.
 #pragma once
 #include "common.cuh"
 #include "grid_kernels.cuh"
@@ -12,7 +12,7 @@
 
 namespace ibmg {
 
-constexpr int kCoarseMaxN = 16;
+constexpr int kCoarseMaxN = 32;
 constexpr int kCoarseThreads = 128;
 
 struct CLev {
@@ -48,22 +48,27 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, SlabSlot
     // start streaming the first big block's slab while the plain passes run
     if (C.nbig > 0) slab_issue(slot[0], C.SL, 0, t, nt);
     cp_async_commit();
-    const int per = n * n / 8;  // single tile (n <= 16): cells of one colour
-    for (int pc = 0; pc < 8; ++pc) {
-        for (int idx = t; idx < per; idx += nt) {
-            int li, lj;
-            if (n == 16) {
-                lj = idx >> 1;
-                li = ((pc - 2 * lj) & 7) + 8 * (idx & 1);
-            } else {  // n == 8
-                lj = idx;
-                li = (pc - 2 * lj) & 7;
+    // plain phase: 16x16 tiles in 2x2 tile colours (n = 32) or one periodic tile
+    const int T = n < kTile ? n : kTile, ntile = n / T, ntc = ntile >= 2 ? 4 : 1;
+    const int per = T * T / 8;
+    for (int tc = 0; tc < ntc; ++tc)
+        for (int pc = 0; pc < 8; ++pc) {
+            for (int idx = t; idx < per; idx += nt) {  // one tile per colour at n <= 32
+                const int tx = ntc == 4 ? (tc & 1) : 0, ty = ntc == 4 ? (tc >> 1) : 0;
+                int li, lj;
+                if (T == 16) {
+                    lj = idx >> 1;
+                    li = ((pc - 2 * lj) & 7) + 8 * (idx & 1);
+                } else {  // T == 8
+                    lj = idx;
+                    li = (pc - 2 * lj) & 7;
+                }
+                const int i = tx * T + li, j = ty * T + lj;
+                if (!C.big[(i >> 2) + (j >> 2) * nbk]) plain_cell(L, W, B, i, j);
             }
-            if (!C.big[(li >> 2) + (lj >> 2) * nbk]) plain_cell(L, W, B, li, lj);
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    // big phase: each level-wide colour holds one block here; list order = pass order
+    // big phase: colour classes in order, list order within a class
     for (int q = 0; q < C.nbig; ++q) {
         if (q + 1 < C.nbig) slab_issue(slot[(q + 1) & 1], C.SL, q + 1, t, nt);
         cp_async_commit();

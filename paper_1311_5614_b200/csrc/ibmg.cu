@@ -230,7 +230,7 @@ void alloc_levels(ibmg_ctx* c) {
     c->nlev = int(c->lev.size());
     c->lc = 0;
     while (c->lev[c->lc].L.n > kCoarseMaxN) ++c->lc;
-    static_assert(kCoarseMaxN == kTile, "multi-tile levels (tile-local big phase) are exactly n >= 32");
+    static_assert(kCoarseMaxN == 2 * kTile, "multi-tile kernels run the levels n >= 64");
     if (c->nlev - c->lc > 4) throw InvalidArg("too many coarse-kernel levels");
     c->M = 3 * size_t(p.N) * p.N;
     const int m = p.restart;
@@ -490,8 +490,6 @@ void rebuild(ibmg_ctx* c) {
             }
             LAUNCH(c, k_block_rows, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.FL, lb.E, lb.blk_ids, lb.nbig, lb.rr,
                    lb.bq);
-            LAUNCH(c, k_block_inverse, lb.nbig, 256, 56 * 112 * sizeof(double), lb.L, lb.E, lb.blk_ids, lb.rr,
-                   lb.Ainv, c->err_flag);
             if (lb.sl_off == nullptr || lb.ainv_cap > lb.blk_slab_cap) {
                 dfree(lb.sl_rp);
                 dfree(lb.sl_off);
@@ -508,6 +506,26 @@ void rebuild(ibmg_ctx* c) {
             CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, lb.sl_off, lb.nbig + 1, c->s));
             CK(cudaMemcpyAsync(c->counters + l * kCtr + 28, lb.sl_off + lb.nbig, sizeof(int), cudaMemcpyDeviceToDevice,
                                c->s));
+        }
+        {
+            // all levels' box inverses in one launch (each CTA is a latency-bound
+            // 56-step Gauss-Jordan; one launch overlaps the levels)
+            BInvLevels BL{};
+            int tot = 0;
+            for (int l = 0; l + 1 < c->nlev; ++l) {
+                LevelBuf& lb = c->lev[l];
+                if (lb.nbig == 0) continue;
+                const int k = BL.nlev++;
+                BL.L[k] = lb.L;
+                BL.E[k] = lb.E;
+                BL.blk_ids[k] = lb.blk_ids;
+                BL.rr[k] = lb.rr;
+                BL.Ainv[k] = lb.Ainv;
+                BL.start[k] = tot;
+                tot += lb.nbig;
+            }
+            BL.start[BL.nlev] = tot;
+            if (tot) LAUNCH(c, k_block_inverse, tot, 256, 56 * 112 * sizeof(double), BL, c->err_flag);
         }
         {
             std::vector<int> hc(size_t(c->nlev) * kCtr);
@@ -649,7 +667,7 @@ Slabs slabs(const LevelBuf& lb) { return Slabs{lb.Ainv, lb.sl_rp, lb.sl_off, lb.
 void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     LevelBuf& lb = c->lev[l];
     const int n = lb.L.n;
-    if (n < 2 * kTile) throw InvalidArg("multi-tile sweep needs n >= 32");
+    if (n < 4 * kTile) throw InvalidArg("multi-tile sweep needs n >= 64");
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
     for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
     if (lb.nbig == 0) return;
@@ -1086,7 +1104,7 @@ int ibmg_prolong_add(ibmg_ctx* c, int level, const double* ec, double* wf, int p
 int ibmg_sweep(ibmg_ctx* c, int level, const double* b, double* w, int ptr_kind) {
     return api(c, [&]() -> int {
         if (level < 0 || level + 1 >= c->nlev) throw InvalidArg("sweep: level out of range");
-        if (level >= c->lc) throw InvalidArg("sweep: levels with n <= 16 run inside the coarse-cycle kernel only");
+        if (level >= c->lc) throw InvalidArg("sweep: levels with n <= 32 run inside the coarse-cycle kernel only");
         const size_t m = 3 * size_t(c->lev[level].L.nn);
         Stage S{c, ptr_kind};
         const double* db = S.in(b, m, c->stage_a);

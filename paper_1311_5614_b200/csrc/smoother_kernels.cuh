@@ -399,11 +399,27 @@ __device__ __forceinline__ void stokes_row_entries(const Lev& L, int field, Emit
 
 // One CTA per big block: assemble the 56x56 principal submatrix of A_l on the
 // block DOFs, invert it, store the inverse column-major.
-__global__ void k_block_inverse(Lev L, EMat E, const int* __restrict__ blk_ids, const int2* __restrict__ rr,
-                                double* __restrict__ Ainv, int* err) {
+struct BInvLevels {
+    Lev L[20];
+    EMat E[20];
+    const int* blk_ids[20];
+    const int2* rr[20];
+    double* Ainv[20];
+    int start[21];
+    int nlev;
+};
+
+__global__ void k_block_inverse(BInvLevels BL, int* err) {
     extern __shared__ double M[];  // 56 x 112
     __shared__ double col[56];
-    const int q = blockIdx.x, t = threadIdx.x, nt = blockDim.x, n = L.n;
+    int lv = 0;
+    while (lv + 1 < BL.nlev && (int)blockIdx.x >= BL.start[lv + 1]) ++lv;
+    const Lev L = BL.L[lv];
+    const EMat E = BL.E[lv];
+    const int* __restrict__ blk_ids = BL.blk_ids[lv];
+    const int2* __restrict__ rr = BL.rr[lv];
+    double* __restrict__ Ainv = BL.Ainv[lv];
+    const int q = blockIdx.x - BL.start[lv], t = threadIdx.x, nt = blockDim.x, n = L.n;
     const int B = blk_ids[q], nbk = n >> 2;
     const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
     for (int idx = t; idx < 56 * 112; idx += nt) {
