@@ -142,6 +142,16 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
+def measured_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
+    (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[config][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     """Algorithmic (compulsory fp64) bytes of all launches of `name` in the
     profiled pass (SURVEY.md §8d per-cell figures x cells)."""
@@ -281,7 +291,8 @@ def run_ours(args, rank, world):
             avg_s = tms / cnt * 1e-3
             ach = byts / cnt / avg_s / 1e9
             roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
+                    "frac": round(ach / peak, 4), "traffic": measured_traffic(WL["name"], name),
+                    "traffic_unit": "B/launch (ncu, profiles/traffic.json)", "peak_source": peak_kind,
                     "bytes_per_launch": byts / cnt, "avg_launch_us": round(avg_s * 1e6, 3),
                     "share_of_step": round(tms / step_prof_ms, 4), "launches": cnt}
             break
