@@ -13,7 +13,7 @@
 namespace ibmg {
 
 constexpr int kCoarseMaxN = 32;
-constexpr int kCoarseThreads = 128;
+constexpr int kCoarseThreads = 512;  // 4 groups of 128 for the big phase
 
 struct CLev {
     Lev L;
@@ -21,7 +21,8 @@ struct CLev {
     EMat E;
     const uint8_t* big;
     Slabs SL;
-    int nbig;
+    int nbig, ncol;
+    int coff[33];
 };
 
 struct CoarseArgs {
@@ -40,14 +41,11 @@ struct SW {
     }
 };
 
-__device__ void coarse_sweep(const CLev& C, double* w, const double* b, SlabSlot* slot, BigScratch& S) {
+__device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* slot, BigScratch* S) {
     const Lev& L = C.L;
     const int n = L.n, t = threadIdx.x, nt = blockDim.x, nbk = n >> 2;
     SW W{w, n, L.nn};
     SW B{const_cast<double*>(b), n, L.nn};
-    // start streaming the first big block's slab while the plain passes run
-    if (C.nbig > 0) slab_issue(slot[0], C.SL, 0, t, nt);
-    cp_async_commit();
     // plain phase: 16x16 tiles in 2x2 tile colours (n = 32) or one periodic tile
     const int T = n < kTile ? n : kTile, ntile = n / T, ntc = ntile >= 2 ? 4 : 1;
     const int per = T * T / 8;
@@ -68,27 +66,33 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, SlabSlot
             }
             __syncthreads();
         }
-    // big phase: colour classes in order, list order within a class
-    for (int q = 0; q < C.nbig; ++q) {
-        if (q + 1 < C.nbig) slab_issue(slot[(q + 1) & 1], C.SL, q + 1, t, nt);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        const SlabSlot& sl = slot[q & 1];
-        const int Bk = sl.rp[47];  // owner block id (k_slab_count)
-        big_block_slab(L, sl, 4 * (Bk % nbk), 4 * (Bk / nbk), W, (const double*)w, (const double*)w, B,
-                       [&](int f, int i, int j, double d) { W(f, i, j) += d; }, S, t);
+    // big phase: colour classes in order; the blocks of a class (independent)
+    // are shared by 4 groups of 128 threads, each with its own E'-row slot
+    const int g = t / kGroup, gt = t % kGroup, G = nt / kGroup;
+    for (int colour = 0; colour < C.ncol; ++colour) {
+        const int cnt = C.coff[colour + 1] - C.coff[colour];
+        for (int base = 0; base < cnt; base += G) {
+            if (base + g < cnt) {
+                const int q = C.coff[colour] + base + g;
+                eslot_issue(slot[g], C.SL, q, gt, kGroup);
+                cp_async_commit();
+                cp_async_wait<0>();
+                asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup));
+                const int Bk = slot[g].rp[47];
+                big_block_es(L, slot[g], C.SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W,
+                             (const double*)w, B, [&](int f, int i, int j, double d) { W(f, i, j) += d; }, S[g], gt,
+                             [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); });
+            }
+        }
         __syncthreads();
     }
-    cp_async_wait<0>();
-    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
-    double* sm = reinterpret_cast<double*>(dsm + 2 * sizeof(SlabSlot));
-    __shared__ BigScratch S;
+    ESlot* slot = reinterpret_cast<ESlot*>(dsm);
+    double* sm = reinterpret_cast<double*>(dsm + (kCoarseThreads / kGroup) * sizeof(ESlot));
+    __shared__ BigScratch S[kCoarseThreads / kGroup];
     double* wl[4];
     double* bl[4];
     size_t off = 0;

@@ -700,6 +700,8 @@ CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
         C.big = lb.big;
         C.SL = slabs(lb);
         C.nbig = lb.nbig;
+        C.ncol = lb.ncol;
+        std::copy(lb.coff, lb.coff + kMaxColours + 1, C.coff);
     }
     A.Acoarse = c->Acoarse;
     A.b_in = b_in;
@@ -711,7 +713,7 @@ size_t coarse_smem(ibmg_ctx* c) {
     size_t d = 0;
     for (int l = c->lc; l < c->nlev; ++l) d += 6 * size_t(c->lev[l].L.nn);
     d += 3 * size_t(c->lev[c->lc].L.nn);
-    return 2 * sizeof(SlabSlot) + d * sizeof(double);
+    return (kCoarseThreads / kGroup) * sizeof(ESlot) + d * sizeof(double);
 }
 
 void coarse_cycle(ibmg_ctx* c, const double* b, double* w) {

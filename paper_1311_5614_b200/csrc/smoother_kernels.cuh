@@ -249,6 +249,75 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
     }
 }
 
+// E'-row part of a slab only (the coarse kernel keeps 4 of these in shared
+// memory, one per 128-thread group; the inverse is read from L2 into registers).
+struct ESlot {
+    double val[kSlabCap];
+    int col[kSlabCap];
+    int rp[48];
+};
+static_assert(sizeof(ESlot) % 16 == 0, "slot alignment");
+
+__device__ __forceinline__ void eslot_issue(ESlot& slot, const Slabs& SL, int q, int t, int nt) {
+    if (t < 12) cp_async16(reinterpret_cast<char*>(slot.rp) + 16 * t, reinterpret_cast<const char*>(SL.rp + (size_t)q * 48) + 16 * t);
+    const int o = SL.off[q], cnt = SL.off[q + 1] - o;
+    const char* cv = reinterpret_cast<const char*>(SL.val + o);
+    const char* cc = reinterpret_cast<const char*>(SL.col + o);
+    for (int c = t; c < cnt / 2; c += nt) cp_async16(reinterpret_cast<char*>(slot.val) + 16 * c, cv + 16 * c);
+    for (int c = t; c < cnt / 4; c += nt) cp_async16(reinterpret_cast<char*>(slot.col) + 16 * c, cc + 16 * c);
+}
+
+// big_block_slab with the E' rows from an ESlot and the inverse streamed from
+// global memory straight into registers (issued first, overlapping the
+// residual).  `gsync` is the group barrier.
+template <class WA, class LocA, class BA, class WAdd, class Sync>
+__device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, const double* __restrict__ A_q, int bi,
+                                             int bj, const WA& W, const LocA& wloc, const BA& Bv, WAdd&& wadd,
+                                             BigScratch& S, int gt, Sync&& gsync) {
+    double av[28];
+    const int row = gt % 56, cg = gt / 56;
+    if (gt < 112) {
+        const double* A = A_q + (size_t)(28 * cg) * 56 + row;
+#pragma unroll
+        for (int c = 0; c < 28; ++c) av[c] = __ldg(A + c * 56);
+    }
+    if (gt < 56) {
+        int f, i, j;
+        block_dof(gt, bi, bj, f, i, j);
+        i = wr(i, L.n);
+        j = wr(j, L.n);
+        double ru, rv, rp;
+        stokes_rows(L, W, i, j, ru, rv, rp);
+        S.sr[gt] = Bv(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
+    }
+    if (gt < 120) {
+        const int r = gt % 40, p = gt / 40;
+        double s0 = 0.0;
+        for (int e = slot.rp[r] + p; e < slot.rp[r + 1]; e += 3) s0 += slot.val[e] * wloc[slot.col[e]];
+        S.epart[p][r] = s0;
+    }
+    gsync();
+    if (gt < 112) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 28; c += 2) {
+            const int cc = 28 * cg + c;
+            const double r0 = cc < 40 ? S.sr[cc] + ((S.epart[0][cc] + S.epart[1][cc]) + S.epart[2][cc]) : S.sr[cc];
+            const double r1 = cc + 1 < 40 ? S.sr[cc + 1] + ((S.epart[0][cc + 1] + S.epart[1][cc + 1]) + S.epart[2][cc + 1])
+                                          : S.sr[cc + 1];
+            s0 += av[c] * r0;
+            s1 += av[c + 1] * r1;
+        }
+        S.part[cg][row] = s0 + s1;
+    }
+    gsync();
+    if (gt < 56) {
+        int f, i, j;
+        block_dof(gt, bi, bj, f, i, j);
+        wadd(f, i, j, S.part[0][gt] + S.part[1][gt]);
+    }
+}
+
 // Global accessors that bypass L1 (ld.global.cg): the big phase reads values
 // other CTAs wrote before the last grid barrier.
 struct GAccCG {
