@@ -66,6 +66,7 @@ inline unsigned nblk(size_t n, int t = 256) { return unsigned((n + t - 1) / t); 
 inline long grow_cap(long need, long cap) { return std::max<long>(need + need / 2 + 64, cap + cap / 2); }
 
 constexpr int kMaxColours = 32;
+constexpr int kDataflowMaxN = 512;  // levels swept by the single dataflow kernel
 
 struct LevelBuf {
     Lev L{};
@@ -83,6 +84,14 @@ struct LevelBuf {
     int blk_cap = 0;
     int coff[kMaxColours + 1] = {0};
     int ncol = 0;
+    // barrier-free big phase: predecessor CSR (list positions) + completion epochs
+    int* pred = nullptr;
+    int* poff = nullptr;
+    unsigned* flags = nullptr;
+    long pred_cap = 0;
+    int poff_cap = 0;
+    unsigned epoch = 0;
+    unsigned* tflags = nullptr;  // per-tile completion epochs (dataflow sweep)
     int2* rr = nullptr;
     int* bq = nullptr;
     // per-block slabs (inverse + encoded E' rows) and big-tile lists
@@ -129,6 +138,8 @@ struct ibmg_ctx {
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
     bool have_structs = false;
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
+    int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
+    unsigned long long* trace = nullptr;  // debug task timeline of the dataflow sweep
     // live per-kernel CUDA-event timing (bench roofline); off on the timed path
     bool prof = false;
     struct ProfRec {
@@ -223,6 +234,10 @@ void alloc_levels(ibmg_ctx* c) {
         if (n > p.coarsest_n) {
             lb.big = dalloc<uint8_t>(size_t(n / 4) * (n / 4));
             lb.bq = dalloc<int>(size_t(n / 4) * (n / 4));
+            if (n >= 4 * kTile) {
+                lb.tflags = dalloc<unsigned>(size_t(n / kTile) * (n / kTile));
+                CK(cudaMemset(lb.tflags, 0, sizeof(unsigned) * (n / kTile) * (n / kTile)));
+            }
         }
         c->lev.push_back(lb);
         if (n <= p.coarsest_n) break;
@@ -284,6 +299,11 @@ void free_structs(ibmg_ctx* c) {
         dfree(lb.sl_val);
         lb.sl_cap = 0;
         lb.blk_slab_cap = 0;
+        dfree(lb.pred);
+        dfree(lb.poff);
+        dfree(lb.flags);
+        lb.pred_cap = 0;
+        lb.poff_cap = 0;
         lb.blk_cap = lb.ainv_cap = 0;
         lb.nbig = 0;
     }
@@ -350,6 +370,42 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb) {
         lb.blk_ids = dalloc<int>(size_t(lb.blk_cap));
     }
     if (nbig) CK(cudaMemcpy(lb.blk_ids, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice));
+    // dependency lists for the barrier-free big phase: the predecessors of a
+    // block are the big blocks within Chebyshev block distance 2 (periodic)
+    // with a smaller colour (list positions); same-colour blocks never conflict
+    std::vector<int> pos_of(size_t(nbk) * nbk, -1);
+    for (int q = 0; q < nbig; ++q) pos_of[ids[q]] = q;
+    std::vector<int> poff(nbig + 1, 0), pred;
+    pred.reserve(size_t(nbig) * 12);
+    for (int q = 0; q < nbig; ++q) {
+        const int B = ids[q], bx = B % nbk, by = B / nbk, cq = col[B];
+        for (int dy = -2; dy <= 2; ++dy)
+            for (int dx = -2; dx <= 2; ++dx) {
+                const int B2 = wr(bx + dx, nbk) + wr(by + dy, nbk) * nbk;
+                if (B2 != B && col[B2] >= 0 && col[B2] < cq) {
+                    // distinct offsets may alias on tiny periodic levels: keep each predecessor once
+                    const int p = pos_of[B2];
+                    bool dup = false;
+                    for (int k = poff[q]; k < int(pred.size()); ++k) dup |= pred[k] == p;
+                    if (!dup) pred.push_back(p);
+                }
+            }
+        poff[q + 1] = int(pred.size());
+    }
+    if (lb.pred_cap < long(pred.size()) + 1 || lb.poff_cap < nbig + 1) {
+        dfree(lb.pred);
+        dfree(lb.poff);
+        dfree(lb.flags);
+        lb.pred_cap = grow_cap(long(pred.size()) + 1, lb.pred_cap);
+        lb.poff_cap = int(grow_cap(nbig + 1, lb.poff_cap));
+        lb.pred = dalloc<int>(size_t(lb.pred_cap));
+        lb.poff = dalloc<int>(size_t(lb.poff_cap));
+        lb.flags = dalloc<unsigned>(size_t(lb.poff_cap));
+        CK(cudaMemset(lb.flags, 0, sizeof(unsigned) * lb.poff_cap));
+        lb.epoch = 0;
+    }
+    if (!pred.empty()) CK(cudaMemcpy(lb.pred, pred.data(), sizeof(int) * pred.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(lb.poff, poff.data(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice));
 }
 
 void check_err_flag(ibmg_ctx* c, const char* where) {
@@ -668,18 +724,30 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     LevelBuf& lb = c->lev[l];
     const int n = lb.L.n;
     if (n < 4 * kTile) throw InvalidArg("multi-tile sweep needs n >= 64");
-    const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
-    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
-    if (lb.nbig == 0) return;
     BigColours BC;
     BC.ncol = lb.ncol;
     int widest = 1;
     for (int k = 0; k <= kMaxColours; ++k) BC.off[k] = lb.coff[k];
     for (int k = 0; k < lb.ncol; ++k) widest = std::max(widest, lb.coff[k + 1] - lb.coff[k]);
-    const int grid = std::min(widest, c->big_grid_max);
     Lev L = lb.L;
     Slabs SL = slabs(lb);
-    void* args[] = {&L, &SL, &BC, (void*)&b, (void*)&w};
+    if (n <= kDataflowMaxN) {
+        // latency regime: the whole sweep as one dataflow kernel
+        DfArgs A{L, SL, BC, BigDeps{lb.pred, lb.poff, lb.flags, ++lb.epoch}, lb.tflags, lb.big, b, w, c->trace};
+        void* args[] = {&A};
+        if (c->prof) prof_begin(c, "k_sweep_df");
+        CK(cudaLaunchCooperativeKernel((const void*)k_sweep_df, dim3(c->df_grid_max), dim3(32 * kDfWarps), args,
+                                       kDfSmem, c->s));
+        if (c->prof) prof_end(c);
+        ++c->launches;
+        return;
+    }
+    const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
+    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
+    if (lb.nbig == 0) return;
+    const int grid = std::min(widest, c->big_grid_max);
+    BigDeps DP{lb.pred, lb.poff, lb.flags, ++lb.epoch};
+    void* args[] = {&L, &SL, &BC, &DP, (void*)&b, (void*)&w};
     if (c->prof) prof_begin(c, "k_big_phase");
     CK(cudaLaunchCooperativeKernel((const void*)k_big_phase, dim3(grid), dim3(kBigThreads), args, kBigSmem, c->s));
     if (c->prof) prof_end(c);
@@ -953,6 +1021,9 @@ int ibmg_create(const ibmg_params* p, ibmg_ctx** out) {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_phase, kBigThreads, kBigSmem));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
             c->big_grid_max = std::max(1, per_sm * sms);
+            CK(cudaFuncSetAttribute(k_sweep_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df, 32 * kDfWarps, kDfSmem));
+            c->df_grid_max = std::max(1, per_sm * sms);
         }
         alloc_levels(c);
         CK(cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem(c))));
@@ -978,6 +1049,7 @@ void ibmg_destroy(ibmg_ctx* c) {
         dfree(lb.r);
         dfree(lb.big);
         dfree(lb.bq);
+        dfree(lb.tflags);
     }
     dfree(c->V);
     dfree(c->Z);
@@ -1162,6 +1234,33 @@ int ibmg_big_blocks(ibmg_ctx* c, int level, int* flags) {
         return cnt;
     } catch (const std::exception& e) {
         return fail(c, e, -1);
+    }
+}
+
+// Debug: run one dataflow sweep on `level` with per-task globaltimer stamps and
+// copy them out (tiles: 4 words each, then big blocks: 6 words each).  Returns
+// the number of words, or -1.  Not part of the solver path.
+long ibmg_debug_sweep_trace(ibmg_ctx* c, int level, const double* b, double* w, unsigned long long* out, long cap) {
+    try {
+        if (!c || level < 0 || level >= c->lc) return -1;
+        CK(cudaSetDevice(c->prm.device));
+        LevelBuf& lb = c->lev[level];
+        const int nt = lb.L.n / kTile;
+        const long words = 4L * nt * nt + 6L * lb.nbig;
+        if (!out) return words;
+        unsigned long long* d = dalloc<unsigned long long>(size_t(words));
+        CK(cudaMemset(d, 0, sizeof(unsigned long long) * words));
+        c->trace = d;
+        sweep_level(c, level, b, w);
+        c->trace = nullptr;
+        CK(cudaStreamSynchronize(c->s));
+        CK(cudaMemcpy(out, d, sizeof(unsigned long long) * std::min(words, cap), cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        return words;
+    } catch (const std::exception& e) {
+        c->trace = nullptr;
+        fail(c, e, -1);
+        return -1;
     }
 }
 

@@ -209,22 +209,28 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
         stokes_rows(L, W, i, j, ru, rv, rp);
         S.sr[gt] = Bv(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
     }
-    // E' row dots: 3 threads per row (strided entries), fixed-order combine
+    // E' row dots: 3 threads per row (strided entries), the column gathers
+    // batched 8 at a time (independent loads in flight), fixed-order combine
     if (gt < 120) {
         const int r = gt % 40, p = gt / 40;
-        double s0 = 0.0, s1 = 0.0;
         const int e1 = slot.rp[r + 1];
-        int e = slot.rp[r] + p;
-        for (; e + 3 < e1; e += 6) {
-            const int c0 = slot.col[e], c1 = slot.col[e + 3];
-            s0 += slot.val[e] * (c0 >= 0 ? wloc[c0] : wglob[-c0 - 1]);
-            s1 += slot.val[e + 3] * (c1 >= 0 ? wloc[c1] : wglob[-c1 - 1]);
+        double s0 = 0.0;
+        for (int e = slot.rp[r] + p; e < e1; e += 24) {
+            int cc[8];
+            double vv[8], xx[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int em = e + 3 * m;
+                cc[m] = em < e1 ? slot.col[em] : 0x7fffffff;
+                vv[m] = em < e1 ? slot.val[em] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                xx[m] = cc[m] == 0x7fffffff ? 0.0 : (cc[m] >= 0 ? wloc[cc[m]] : wglob[-cc[m] - 1]);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) s0 += vv[m] * xx[m];
         }
-        if (e < e1) {
-            const int c0 = slot.col[e];
-            s0 += slot.val[e] * (c0 >= 0 ? wloc[c0] : wglob[-c0 - 1]);
-        }
-        S.epart[p][r] = s0 + s1;
+        S.epart[p][r] = s0;
     }
     __syncthreads();
     if (gt < 112) {
@@ -344,19 +350,38 @@ struct BigColours {
     int off[33];
 };
 
-// The big phase of one sweep on a level as ONE cooperative persistent kernel:
-// the greedy colour classes run in order with a grid barrier between them;
-// each CTA takes the colour's blocks grid-stride, and the slab of its next
-// block (possibly in the next colour) streams into the second shared-memory
-// slot while the current block is solved.
+struct BigDeps {
+    const int* pred;   // predecessor list positions (CSR by block)
+    const int* poff;
+    unsigned* flags;   // completion epoch per block
+    unsigned epoch;    // this launch's epoch (monotone per level)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// The big phase of one sweep on a level as ONE cooperative persistent kernel
+// without grid barriers: each CTA takes its blocks in colour order; a block
+// waits (acquire) until its predecessors — the conflicting big blocks of
+// smaller colour — have published this epoch (release), so the result is
+// exactly the colour-ordered Gauss-Seidel schedule while blocks that do not
+// depend on each other run ahead.  The cooperative launch makes all CTAs
+// co-resident, and dependencies only point to smaller colours, so the waits
+// cannot deadlock.  The slab of the CTA's next block streams into the second
+// shared-memory slot while the current one is solved.
 constexpr int kBigThreads = 128;
 constexpr size_t kBigSmem = 2 * sizeof(SlabSlot);
-__global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC,
+__global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC, BigDeps DP,
                                                             const double* __restrict__ b, double* w) {
     extern __shared__ __align__(16) unsigned char dsm[];
     SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
     __shared__ BigScratch S;
-    cg::grid_group grid = cg::this_grid();
     const int t = threadIdx.x, G = gridDim.x, nbk = L.n >> 2;
     auto next_item = [&](int c, int q, int& nc, int& nq) {
         // the item after (c, q) for this CTA; c = -1 starts the enumeration
@@ -376,28 +401,206 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
     GAccCG W{w, L.n, L.nn};
     GAccB B{b, L.n, L.nn};
     int k = 0;
-    for (int colour = 0; colour < BC.ncol; ++colour) {
-        while (c == colour) {
-            int nc, nq;
-            next_item(c, q, nc, nq);
-            if (nc < BC.ncol) slab_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
-            cp_async_commit();
-            cp_async_wait<1>();
-            __syncthreads();
-            const SlabSlot& sl = slot[k & 1];
-            const int Bk = sl.rp[47];
-            big_block_slab(L, sl, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, FlatCG{w}, B,
-                           [&](int f, int i, int j, double d) {
-                               double* p = w + (size_t)f * L.nn + i + (size_t)j * L.n;
-                               __stcg(p, __ldcg(p) + d);
-                           },
-                           S, t);
-            __syncthreads();
-            ++k;
-            c = nc;
-            q = nq;
+    while (c < BC.ncol) {
+        int nc, nq;
+        next_item(c, q, nc, nq);
+        if (nc < BC.ncol) slab_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
+        cp_async_commit();
+        // wait for the predecessors of block q (one thread per predecessor)
+        for (int e = DP.poff[q] + t; e < DP.poff[q + 1]; e += kBigThreads)
+            while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(32);
+        cp_async_wait<1>();
+        __syncthreads();
+        const SlabSlot& sl = slot[k & 1];
+        const int Bk = sl.rp[47];
+        big_block_slab(L, sl, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, FlatCG{w}, B,
+                       [&](int f, int i, int j, double d) {
+                           double* p = w + (size_t)f * L.nn + i + (size_t)j * L.n;
+                           __stcg(p, __ldcg(p) + d);
+                       },
+                       S, t);
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            st_release(DP.flags + q, DP.epoch);
         }
-        if (BC.off[colour + 1] > BC.off[colour]) grid.sync();
+        ++k;
+        c = nc;
+        q = nq;
+    }
+    cp_async_wait<0>();
+}
+
+
+// ---- dataflow sweep (latency regime, 64 <= n <= 512) ------------------------
+// One sweep of a level as ONE cooperative persistent kernel executing a task
+// DAG: the plain tiles (warp tasks, tile-colour-major order),
+// then the big blocks (CTA tasks, colour order).  A tile waits for its adjacent
+// tiles of smaller tile colour; a big block waits for its conflicting big
+// blocks of smaller colour and for every plain tile within 8 cells of it (its
+// E' reach + stencil).  Each waiter polls completion epochs with acquire loads;
+// each finisher publishes with a release store.  Every dependency points to an
+// earlier task and all CTAs are co-resident, so the DAG cannot deadlock, and
+// the result is exactly the colour-ordered schedule of the oracle.
+constexpr int kDfWarps = 4;
+struct DfArgs {
+    Lev L;
+    Slabs SL;
+    BigColours BC;
+    BigDeps DP;
+    unsigned* tflags;        // per-tile completion epochs
+    const uint8_t* big;
+    const double* b;
+    double* w;
+    unsigned long long* trace;  // debug: per-task globaltimer stamps (nullptr in production)
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr size_t kDfTileBytes = (3 * kReg * kReg + 3 * 289) * sizeof(double);
+constexpr size_t kDfSmem = 2 * sizeof(SlabSlot) + kDfWarps * ((kDfTileBytes + 15) / 16 * 16);
+
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+__global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
+    __shared__ BigScratch S;
+    const Lev& L = A.L;
+    const int n = L.n, nn = L.nn, t = threadIdx.x, wid = t >> 5, lane = t & 31, G = gridDim.x;
+    const int nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1, nbk = n >> 2;
+    double* sw = reinterpret_cast<double*>(dsm + 2 * sizeof(SlabSlot) + wid * ((kDfTileBytes + 15) / 16 * 16));
+    double* sb = sw + 3 * kReg * kReg;
+    const unsigned epoch = A.DP.epoch;
+    // first big slab streams in while the plain tasks run
+    int c = 0, q = -1;
+    auto next_item = [&](int cc, int qq, int& nc, int& nq) {
+        nq = (cc < 0) ? -1 : qq + G;
+        nc = (cc < 0) ? 0 : cc;
+        while (nc < A.BC.ncol) {
+            if (nq < 0) nq = A.BC.off[nc] + (int)blockIdx.x;
+            if (nq < A.BC.off[nc + 1]) return;
+            ++nc;
+            nq = -1;
+        }
+    };
+    next_item(-1, 0, c, q);
+    if (c < A.BC.ncol) slab_issue(slot[0], A.SL, q, t, 32 * kDfWarps);
+    cp_async_commit();
+    // ---- plain tasks: warp per tile
+    for (int task = blockIdx.x * kDfWarps + wid; task < ntiles; task += G * kDfWarps) {
+        const int tc = task / per, i = task % per;
+        const int tx = 2 * (i % half) + (tc & 1), ty = 2 * (i / half) + (tc >> 1);
+        const int x0 = tx * kTile, y0 = ty * kTile;
+        const unsigned long long t_a = A.trace ? gtimer() : 0;
+        if (lane < 8) {  // adjacent tiles of smaller tile colour
+            const int d = lane < 4 ? lane : lane + 1;  // skip the centre of the 3x3
+            const int ax = wr(tx + d % 3 - 1, nt), ay = wr(ty + d / 3 - 1, nt);
+            const int ac = (ax & 1) + 2 * (ay & 1);
+            if (ac < tc)
+                while (ld_acquire(A.tflags + ax + ay * nt) != epoch) __nanosleep(20);
+        }
+        __syncwarp();
+        const unsigned long long t_b = A.trace ? gtimer() : 0;
+        for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs, L2 only
+            const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
+            const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
+            const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
+            cp_async16_cg(&sw[f * kReg * kReg + bb * kReg + 2 * a2], A.w + (size_t)f * nn + gi);
+        }
+        for (int qq = lane; qq < 289; qq += 32) {
+            const int a = qq % 17, bb = qq / 17;
+            const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+            cp_async8(&sb[qq], A.b + gi);
+            cp_async8(&sb[289 + qq], A.b + nn + gi);
+            cp_async8(&sb[578 + qq], A.b + 2 * nn + gi);
+        }
+        cp_async_commit();
+        const bool isbig = lane < 16 && A.big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * nbk];
+        const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
+        cp_async_wait<0>();
+        __syncwarp();
+        TileW W{sw};
+        TileB B{sb};
+        for (int pc = 0; pc < 8; ++pc) {
+            const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
+            if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
+            __syncwarp();
+        }
+        for (int qq = lane; qq < 17 * 17; qq += 32) {
+            const int a = qq % 17, bb = qq / 17;
+            const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+            if (bb < 16) __stcg(A.w + gi, W(0, a, bb));
+            if (a < 16) __stcg(A.w + nn + gi, W(1, a, bb));
+            if (a < 16 && bb < 16) __stcg(A.w + 2 * nn + gi, W(2, a, bb));
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            st_release(A.tflags + tx + ty * nt, epoch);
+            if (A.trace) {
+                unsigned long long* r = A.trace + 4 * task;
+                r[0] = t_a;
+                r[1] = t_b;
+                r[2] = gtimer();
+                r[3] = blockIdx.x;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- big tasks: CTA per block, colour order
+    GAccCG Wg{A.w, n, nn};
+    GAccB Bg{A.b, n, nn};
+    int k = 0;
+    while (c < A.BC.ncol) {
+        int nc, nq;
+        next_item(c, q, nc, nq);
+        if (nc < A.BC.ncol) slab_issue(slot[(k + 1) & 1], A.SL, nq, t, 32 * kDfWarps);
+        cp_async_commit();
+        const int Bk = A.SL.rp[(size_t)q * 48 + 47];
+        const int bi = 4 * (Bk % nbk), bj = 4 * (Bk / nbk);
+        const unsigned long long t_a = A.trace ? gtimer() : 0;
+        for (int e = A.DP.poff[q] + t; e < A.DP.poff[q + 1]; e += 32 * kDfWarps)
+            while (ld_acquire(A.DP.flags + A.DP.pred[e]) != epoch) __nanosleep(20);
+        if (t < 9) {  // plain tiles within 8 cells of the block
+            const int tx0 = (bi - 8) >> 4, ty0 = (bj - 8) >> 4;
+            const int tx = tx0 + t % 3, ty = ty0 + t / 3;
+            if (tx * kTile <= bi + 11 && ty * kTile <= bj + 11)
+                while (ld_acquire(A.tflags + wr(tx, nt) + wr(ty, nt) * nt) != epoch) __nanosleep(20);
+        }
+        __syncthreads();
+        const unsigned long long t_b = A.trace ? gtimer() : 0;
+        cp_async_wait<1>();
+        __syncthreads();
+        const unsigned long long t_c = A.trace ? gtimer() : 0;
+        big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg,
+                       [&](int f, int i, int j, double d) {
+                           double* p = A.w + (size_t)f * nn + i + (size_t)j * n;
+                           __stcg(p, __ldcg(p) + d);
+                       },
+                       S, t);
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            st_release(A.DP.flags + q, epoch);
+            if (A.trace) {
+                unsigned long long* r = A.trace + 4 * ntiles + 6 * q;
+                r[0] = t_a;
+                r[1] = t_b;
+                r[2] = t_c;
+                r[3] = gtimer();
+                r[4] = c;
+                r[5] = blockIdx.x;
+            }
+        }
+        ++k;
+        c = nc;
+        q = nq;
     }
     cp_async_wait<0>();
 }

@@ -1,0 +1,39 @@
+"""Task timeline of one dataflow sweep (debug): where the critical path goes."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1311_5614_b200 import configs  # noqa: E402
+from paper_1311_5614_b200.ibmg import SaddleSystem  # noqa: E402
+
+prob = configs.config2(1e4)
+g = SaddleSystem.from_problem(prob)
+L = g._L
+b = torch.tensor(g.build_rhs(np.zeros(2 * 256 * 256)), device="cuda")
+w = torch.zeros_like(b)
+for level in (0, 1):
+    n = g.level_n(level)
+    nb = 3 * n * n
+    bl, wl = b[:nb].clone(), w[:nb].clone()
+    words = L.ibmg_debug_sweep_trace(g._h, level, bl.data_ptr(), wl.data_ptr(), None, 0)
+    out = np.zeros(words, np.uint64)
+    for rep in range(3):  # warm, then measure
+        L.ibmg_debug_sweep_trace(g._h, level, bl.data_ptr(), wl.data_ptr(), out.ctypes.data, words)
+    nt = (n // 16) ** 2
+    tiles = out[: 4 * nt].reshape(-1, 4).astype(np.int64)
+    bigs = out[4 * nt:].reshape(-1, 6).astype(np.int64)
+    t0 = min(tiles[:, 0].min(), bigs[:, 0].min() if len(bigs) else 1 << 62)
+    print(f"level {level} n={n}: tiles={nt} big={len(bigs)}")
+    print("  tile wait / work (us): mean %.2f / %.2f, last tile done at %.2f" % (
+        np.mean(tiles[:, 1] - tiles[:, 0]) / 1e3, np.mean(tiles[:, 2] - tiles[:, 1]) / 1e3, (tiles[:, 2].max() - t0) / 1e3))
+    if len(bigs):
+        print("  big wait-deps / wait-slab / solve (us): mean %.2f / %.2f / %.2f; end at %.2f" % (
+            np.mean(bigs[:, 1] - bigs[:, 0]) / 1e3, np.mean(bigs[:, 2] - bigs[:, 1]) / 1e3,
+            np.mean(bigs[:, 3] - bigs[:, 2]) / 1e3, (bigs[:, 3].max() - t0) / 1e3))
+        for col in range(int(bigs[:, 4].max()) + 1):
+            m = bigs[:, 4] == col
+            print(f"    colour {col}: {m.sum():3d} blocks, start {(bigs[m,0].min()-t0)/1e3:7.2f} done {(bigs[m,3].max()-t0)/1e3:7.2f} us")
