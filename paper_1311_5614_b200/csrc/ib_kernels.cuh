@@ -62,79 +62,72 @@ __device__ __forceinline__ int cell_prolong(int c, int* J, double* w) {
 // level l's times P (W*P*...*P) — the factored form of the reference's
 // recursive Galerkin R*E*P (transfers.cpp:286-293, PAPER Eq. 20).
 __global__ void k_windows(int npts, const double* __restrict__ X, WinLevels WL, double h0, int* err) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= npts) return;
+    // one thread per (point, patch s): s = 0 Lu, 1 Lv, 2 Ru, 3 Rv; the 16-entry
+    // patch and its origin stay in registers from level to level
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= 4 * npts) return;
+    const int k = idx >> 2, s = idx & 3, comp = s & 1;
     const double x = X[2 * k], y = X[2 * k + 1];
-    double wx[4], wy[4];
-    {
-        Win& W = WL.win[0];
-        double* p = W.w + (size_t)k * 64;
-        int fx = line_faces(x, h0, wx), fy = line_centers(y, h0, wy);
-        for (int b = 0; b < 4; ++b)
-            for (int a = 0; a < 4; ++a) p[b * 4 + a] = p[32 + b * 4 + a] = wx[a] * wy[b];
-        int4 o;
-        o.x = fx;
-        o.y = fy;
-        fx = line_centers(x, h0, wx);
-        fy = line_faces(y, h0, wy);
-        for (int b = 0; b < 4; ++b)
-            for (int a = 0; a < 4; ++a) p[16 + b * 4 + a] = p[48 + b * 4 + a] = wx[a] * wy[b];
-        o.z = fx;
-        o.w = fy;
-        W.orgL[k] = o;
-        W.orgR[k] = o;
+    double wx[4], wy[4], cur[16];
+    int ox, oy;
+    if (comp == 0) {
+        ox = line_faces(x, h0, wx);
+        oy = line_centers(y, h0, wy);
+    } else {
+        ox = line_centers(x, h0, wx);
+        oy = line_faces(y, h0, wy);
     }
-    for (int l = 0; l + 1 < WL.nlev; ++l) {
-        const Win& F = WL.win[l];
-        Win& C = WL.win[l + 1];
-        const double* src = F.w + (size_t)k * 64;
-        double* dst = C.w + (size_t)k * 64;
-        for (int q = 0; q < 64; ++q) dst[q] = 0.0;
-        const int4 oL = F.orgL[k], oR = F.orgR[k];
-        int4 nL, nR;
-        // left u: x face-restrict, y cell-restrict; origin (floor(i0/2), floor(j0/2))
-        nL.x = oL.x >> 1; nL.y = oL.y >> 1;
-        // left v: x cell-restrict, y face-restrict
-        nL.z = oL.z >> 1; nL.w = oL.w >> 1;
-        // right u: x face-prolong, y cell-prolong; origin (floor(i0/2), floor((j0-1)/2))
-        nR.x = oR.x >> 1; nR.y = (oR.y - 1) >> 1;
-        // right v: x cell-prolong, y face-prolong
-        nR.z = (oR.z - 1) >> 1; nR.w = oR.w >> 1;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) cur[b * 4 + a] = wx[a] * wy[b];
+    for (int l = 0;; ++l) {
+        Win& W = WL.win[l];
+        double* p = W.w + (size_t)k * 64 + s * 16;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[e] = cur[e];
+        int* org = reinterpret_cast<int*>(s < 2 ? &W.orgL[k] : &W.orgR[k]) + 2 * comp;
+        org[0] = ox;
+        org[1] = oy;
+        if (l + 1 >= WL.nlev) break;
+        double nxt[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) nxt[e] = 0.0;
+        int nx, ny;
+        if (s == 0) { nx = ox >> 1; ny = oy >> 1; }             // left u: face-restrict x, cell-restrict y
+        else if (s == 1) { nx = ox >> 1; ny = oy >> 1; }        // left v: cell-restrict x, face-restrict y
+        else if (s == 2) { nx = ox >> 1; ny = (oy - 1) >> 1; }  // right u: face-prolong x, cell-prolong y
+        else { nx = (ox - 1) >> 1; ny = oy >> 1; }              // right v: cell-prolong x, face-prolong y
         int I[2], J[2];
         double wi[2], wj[2];
         for (int b = 0; b < 4; ++b)
             for (int a = 0; a < 4; ++a) {
-                double v = src[b * 4 + a];  // Lu
-                if (v != 0.0) {
-                    const int ni = face_restrict(oL.x + a, I, wi);
-                    const int J0 = (oL.y + b) >> 1;
-                    for (int p = 0; p < ni; ++p) patch_add(dst, I[p] - nL.x, J0 - nL.y, v * wi[p], err);
-                }
-                v = src[16 + b * 4 + a];  // Lv
-                if (v != 0.0) {
-                    const int nj = face_restrict(oL.w + b, J, wj);
-                    const int I0 = (oL.z + a) >> 1;
-                    for (int q = 0; q < nj; ++q) patch_add(dst + 16, I0 - nL.z, J[q] - nL.w, v * wj[q], err);
-                }
-                v = src[32 + b * 4 + a];  // Ru
-                if (v != 0.0) {
-                    const int ni = face_prolong(oR.x + a, I, wi);
-                    const int nj = cell_prolong(oR.y + b, J, wj);
-                    for (int p = 0; p < ni; ++p)
-                        for (int q = 0; q < nj; ++q)
-                            patch_add(dst + 32, I[p] - nR.x, J[q] - nR.y, v * (wi[p] * wj[q]), err);
-                }
-                v = src[48 + b * 4 + a];  // Rv
-                if (v != 0.0) {
-                    const int nj = face_prolong(oR.w + b, J, wj);
-                    const int ni = cell_prolong(oR.z + a, I, wi);
-                    for (int q = 0; q < nj; ++q)
-                        for (int p = 0; p < ni; ++p)
-                            patch_add(dst + 48, I[p] - nR.z, J[q] - nR.w, v * (wj[q] * wi[p]), err);
+                const double v = cur[b * 4 + a];
+                if (v == 0.0) continue;
+                if (s == 0) {
+                    const int ni = face_restrict(ox + a, I, wi);
+                    const int J0 = (oy + b) >> 1;
+                    for (int p2 = 0; p2 < ni; ++p2) patch_add(nxt, I[p2] - nx, J0 - ny, v * wi[p2], err);
+                } else if (s == 1) {
+                    const int nj = face_restrict(oy + b, J, wj);
+                    const int I0 = (ox + a) >> 1;
+                    for (int q2 = 0; q2 < nj; ++q2) patch_add(nxt, I0 - nx, J[q2] - ny, v * wj[q2], err);
+                } else if (s == 2) {
+                    const int ni = face_prolong(ox + a, I, wi);
+                    const int nj = cell_prolong(oy + b, J, wj);
+                    for (int p2 = 0; p2 < ni; ++p2)
+                        for (int q2 = 0; q2 < nj; ++q2) patch_add(nxt, I[p2] - nx, J[q2] - ny, v * (wi[p2] * wj[q2]), err);
+                } else {
+                    const int nj = face_prolong(oy + b, J, wj);
+                    const int ni = cell_prolong(ox + a, I, wi);
+                    for (int q2 = 0; q2 < nj; ++q2)
+                        for (int p2 = 0; p2 < ni; ++p2) patch_add(nxt, I[p2] - nx, J[q2] - ny, v * (wj[q2] * wi[p2]), err);
                 }
             }
-        C.orgL[k] = nL;
-        C.orgR[k] = nR;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) cur[e] = nxt[e];
+        ox = nx;
+        oy = ny;
     }
 }
 
@@ -358,7 +351,8 @@ __global__ void __launch_bounds__(32 * kELongWarps) k_erows_long(FaceList FL, Wi
     if (!pass && lane == 0) cnt[q] = base;
 }
 
-// Longest face list of a level (runs counted by RLE; the INT_MAX sentinel run excluded).
+// Longest face list of a level (runs counted by RLE; the INT_MAX sentinel run
+// excluded) into out[0]; out[1] = 1 when the last run is that sentinel.
 __global__ void k_rowlen_max(const int* __restrict__ face, const int* __restrict__ off, const int* __restrict__ nruns,
                              int* __restrict__ out) {
     const int nr = *nruns;
@@ -366,6 +360,7 @@ __global__ void k_rowlen_max(const int* __restrict__ face, const int* __restrict
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nr; q += gridDim.x * blockDim.x)
         if (face[q] != 0x7fffffff) m = max(m, off[q + 1] - off[q]);
     atomicMax(out, m);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[1] = (nr > 0 && face[nr - 1] == 0x7fffffff) ? 1 : 0;
 }
 
 // Fiber force density of the RHS times the spread quadrature:

@@ -193,8 +193,8 @@ void prof_collect(ibmg_ctx* c) {
         if ((ctx)->prof && (ctx)->prof_pending.size() > 4096) prof_collect(ctx); \
     } while (0)
 
-// per-level counters: [0..16] colour counts, 17 runs, 18 reach, 19 max slab
-// entries, [20..27] tile-key counts, 28 slab total
+// per-level counters: 17 face-list runs, 18 reach, 19 max slab entries,
+// 28 slab total, 29 longest face list, 30 sentinel-run flag
 constexpr int kCtr = 32;
 
 Lev make_lev(const ibmg_params& p, int n) {
@@ -331,11 +331,9 @@ void free_structs(ibmg_ctx* c) {
 // rule as the oracle (oracle/ibmg_oracle.cpp greedy_block_colours): ascending
 // block id, smallest colour unused within Chebyshev block distance 2
 // (periodic).  Produces the colour-major block list and colour offsets.
-void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb) {
+void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const uint8_t* big) {
     const int nbk = lb.L.n / 4;
-    std::vector<uint8_t> big(size_t(nbk) * nbk);
-    CK(cudaMemcpy(big.data(), lb.big, big.size(), cudaMemcpyDeviceToHost));
-    std::vector<int> col(big.size(), -1);
+    std::vector<int> col(size_t(nbk) * nbk, -1);
     int ncol = 0, nbig = 0;
     for (int by = 0; by < nbk; ++by)
         for (int bx = 0; bx < nbk; ++bx) {
@@ -369,7 +367,7 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb) {
         lb.blk_cap = grow_cap(nbig, lb.blk_cap);
         lb.blk_ids = dalloc<int>(size_t(lb.blk_cap));
     }
-    if (nbig) CK(cudaMemcpy(lb.blk_ids, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice));
+    if (nbig) CK(cudaMemcpyAsync(lb.blk_ids, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, c->s));
     // dependency lists for the barrier-free big phase: the predecessors of a
     // block are the big blocks within Chebyshev block distance 2 (periodic)
     // with a smaller colour (list positions); same-colour blocks never conflict
@@ -404,8 +402,11 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb) {
         CK(cudaMemset(lb.flags, 0, sizeof(unsigned) * lb.poff_cap));
         lb.epoch = 0;
     }
-    if (!pred.empty()) CK(cudaMemcpy(lb.pred, pred.data(), sizeof(int) * pred.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(lb.poff, poff.data(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice));
+    if (!pred.empty())
+        CK(cudaMemcpyAsync(lb.pred, pred.data(), sizeof(int) * pred.size(), cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(lb.poff, poff.data(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice, c->s));
+    // the host vectors die here: the async copies must complete first
+    CK(cudaStreamSynchronize(c->s));
 }
 
 void check_err_flag(ibmg_ctx* c, const char* where) {
@@ -419,7 +420,7 @@ void check_err_flag(ibmg_ctx* c, const char* where) {
 // E'_l row assembly: warp per row, or CTA per row on levels whose face lists
 // run long (coarse levels, where each face collects many points).
 void erows(ibmg_ctx* c, LevelBuf& lb, int pass) {
-    if (lb.maxrow > 256)
+    if (lb.maxrow > 32)
         LAUNCH(c, k_erows_long, lb.FL.nf, 32 * kELongWarps, 0, lb.FL, lb.W, c->P, lb.L.n, pass, lb.E, lb.ecnt);
     else
         LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, pass, lb.E, lb.ecnt);
@@ -446,7 +447,7 @@ void rebuild(ibmg_ctx* c) {
             WL.win[l] = c->lev[l].W;
             WL.n[l] = c->lev[l].L.n;
         }
-        LAUNCH(c, k_windows, nblk(npts, 128), 128, 0, npts, c->X, WL, c->lev[0].L.h, c->err_flag);
+        LAUNCH(c, k_windows, nblk(size_t(npts) * 4, 128), 128, 0, npts, c->X, WL, c->lev[0].L.h, c->err_flag);
         // face lists: sort (face, entry) keys per level, run-length encode
         const int items = npts * 32;
         for (int l = 0; l < c->nlev; ++l) {
@@ -481,17 +482,19 @@ void rebuild(ibmg_ctx* c) {
         }
         std::vector<int> hc(size_t(c->nlev) * kCtr);
         CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
+        // big-block flags of every level in the same round trip (for the host colouring)
+        std::vector<std::vector<uint8_t>> bigh(c->nlev);
+        for (int l = 0; l + 1 < c->nlev; ++l) {
+            const int nbk = c->lev[l].L.n / 4;
+            bigh[l].resize(size_t(nbk) * nbk);
+            CK(cudaMemcpyAsync(bigh[l].data(), c->lev[l].big, bigh[l].size(), cudaMemcpyDeviceToHost, c->s));
+        }
         CK(cudaStreamSynchronize(c->s));
         for (int l = 0; l < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
             const int* h = &hc[size_t(l) * kCtr];
             // runs include the sentinel run (INT_MAX) when any weight was zero
-            int runs = h[17];
-            int last = 0;
-            if (runs > 0) {
-                CK(cudaMemcpy(&last, lb.FL.face + runs - 1, sizeof(int), cudaMemcpyDeviceToHost));
-                if (last == 0x7fffffff) --runs;
-            }
+            const int runs = h[17] - h[30];  // h[30]: the last run is the INT_MAX sentinel (k_rowlen_max)
             lb.FL.nf = runs;
             lb.maxrow = h[29];
             if (l + 1 < c->nlev) {
@@ -499,7 +502,7 @@ void rebuild(ibmg_ctx* c) {
                 if (reach > 7)
                     throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 8-cell same-colour gap on level " +
                                      std::to_string(l) + " (Lagrangian spacing too large)");
-                colour_big_blocks(c, lb);
+                colour_big_blocks(c, lb, bigh[l].data());
             }
         }
         // assembled E'_l rows on the E-active faces (count, scan, fill)
@@ -581,7 +584,7 @@ void rebuild(ibmg_ctx* c) {
                 tot += lb.nbig;
             }
             BL.start[BL.nlev] = tot;
-            if (tot) LAUNCH(c, k_block_inverse, tot, 256, 56 * 112 * sizeof(double), BL, c->err_flag);
+            if (tot) LAUNCH(c, k_block_inverse, tot, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
         }
         {
             std::vector<int> hc(size_t(c->nlev) * kCtr);
@@ -609,7 +612,7 @@ void rebuild(ibmg_ctx* c) {
     {
         LevelBuf& lb = c->lev.back();
         const int m = 3 * lb.L.nn + 1;
-        LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * 2 * m * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
+        LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
                c->err_flag);
     }
     check_err_flag(c, "rebuild");
@@ -1013,8 +1016,8 @@ int ibmg_create(const ibmg_params* p, ibmg_ctx** out) {
     try {
         CK(cudaSetDevice(p->device));
         CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
-        CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 112 * 8));
-        CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * 98 * 8));
+        CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
+        CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * gj_ld(49) * 8));
         CK(cudaFuncSetAttribute(k_big_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
         {
             int per_sm = 0, sms = 0;

@@ -52,6 +52,13 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // ---- plain phase, multi-tile levels (n >= 32): one warp per 16x16 tile.
 constexpr int kTile = 16, kReg = kTile + 4;  // region with a 2-cell halo
@@ -67,34 +74,37 @@ struct TileB {
     __device__ __forceinline__ double operator()(int f, int i, int j) const { return s[f * 289 + j * 17 + i]; }
 };
 
+struct TileBG {  // b read through L1 (read-only in the kernel): local coords of the tile
+    const double* b;
+    int n, nn, x0, y0;
+    __device__ __forceinline__ double operator()(int f, int i, int j) const {
+        return __ldg(b + (size_t)f * nn + wr(x0 + i, n) + (size_t)wr(y0 + j, n) * n);
+    }
+};
+
+// Plain phase of one tile colour on a large level (n > 512, bandwidth regime):
+// one warp per 16x16 tile; only the w region (2-cell halo) is staged in shared
+// memory (9.6 KB per warp -> ~23 resident warps per SM), b is read through L1.
 __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double* __restrict__ b,
                                                      double* __restrict__ w, const uint8_t* __restrict__ big) {
     __shared__ __align__(16) double sw[3 * kReg * kReg];
-    __shared__ __align__(16) double sb[3 * 289];
     const int n = L.n, nn = L.nn, lane = threadIdx.x;
     const int half = (n / kTile) >> 1;
     const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = 2 * (blockIdx.x / half) + (tc >> 1);
     const int x0 = tx * kTile, y0 = ty * kTile;
-    for (int q = lane; q < kReg * kReg; q += 32) {
-        const int a = q % kReg, bb = q / kReg;
-        const size_t gi = wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-        cp_async8(&sw[q], w + gi);
-        cp_async8(&sw[kReg * kReg + q], w + nn + gi);
-        cp_async8(&sw[2 * kReg * kReg + q], w + 2 * nn + gi);
+    for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs
+        const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
+        const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
+        const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
+        cp_async16(&sw[f * kReg * kReg + bb * kReg + 2 * a2], w + (size_t)f * nn + gi);
     }
-    for (int q = lane; q < 289; q += 32) {
-        const int a = q % 17, bb = q / 17;
-        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-        cp_async8(&sb[q], b + gi);
-        cp_async8(&sb[289 + q], b + nn + gi);
-        cp_async8(&sb[578 + q], b + 2 * nn + gi);
-    }
+    cp_async_commit();
     const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
     const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
-    cp_async_wait_all();
+    cp_async_wait<0>();
     __syncwarp();
     TileW W{sw};
-    TileB B{sb};
+    TileBG B{b, n, nn, x0, y0};
     for (int pc = 0; pc < 8; ++pc) {
         const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
         if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
@@ -172,13 +182,6 @@ struct Slabs {
     const double* val;
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void slab_issue(SlabSlot& slot, const Slabs& SL, int q, int t, int nt) {
     const char* A = reinterpret_cast<const char*>(SL.Ainv + (size_t)q * 3136);
@@ -609,9 +612,17 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
 
 // Gauss-Jordan with partial pivoting on an m x 2m augmented matrix in shared
 // memory (row-major, ld = 2m).  Ties in the pivot search go to the lowest row.
+// Row stride of the augmented matrices: 2m + 1 (odd) keeps the per-row
+// accesses of a warp on distinct shared-memory banks.
+__host__ __device__ constexpr int gj_ld(int m) { return 2 * m + 1; }
+
 __device__ void gauss_jordan(double* M, int m, double* col, int* err) {
-    const int ld = 2 * m, t = threadIdx.x, nt = blockDim.x;
+    // thread mapping for the elimination: row r = t % 64, column quarter t / 64
+    // (no division per element); rows >= m idle.  Requires blockDim = 256, m <= 64.
+    const int ld = gj_ld(m), t = threadIdx.x;
+    const int r = t & 63, cq = t >> 6, q = (2 * m + 3) / 4, c0 = cq * q, c1 = min(2 * m, c0 + q);
     __shared__ int piv;
+    __shared__ double pinv;
     for (int k = 0; k < m; ++k) {
         if (t < 32) {
             double best = -1.0;
@@ -625,29 +636,32 @@ __device__ void gauss_jordan(double* M, int m, double* col, int* err) {
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
             }
-            if (t == 0) piv = bi;
+            if (t == 0) {
+                piv = bi;
+                pinv = M[bi * ld + k];
+            }
         }
         __syncthreads();
         const int p = piv;
-        if (p != k)
-            for (int j = t; j < ld; j += nt) {
-                const double a = M[k * ld + j];
-                M[k * ld + j] = M[p * ld + j];
-                M[p * ld + j] = a;
-            }
-        __syncthreads();
-        const double pv = M[k * ld + k];
+        const double pv = pinv;
         if (pv == 0.0) {
             if (t == 0) atomicOr(err, 2);
             return;
         }
+        // swap rows k and p and scale the new pivot row in one pass
+        for (int j = t; j < 2 * m; j += blockDim.x) {
+            const double a = M[k * ld + j], bp = M[p * ld + j];
+            M[k * ld + j] = bp / pv;
+            if (p != k) M[p * ld + j] = a;
+        }
         __syncthreads();
-        for (int j = t; j < ld; j += nt) M[k * ld + j] /= pv;
-        for (int i = t; i < m; i += nt) col[i] = M[i * ld + k];
+        if (t < m) col[t] = M[t * ld + k];
         __syncthreads();
-        for (int idx = t; idx < m * ld; idx += nt) {
-            const int i = idx / ld, j = idx - i * ld;
-            if (i != k) M[idx] -= col[i] * M[k * ld + j];
+        if (r < m && r != k) {
+            const double f = col[r];
+            double* Mr = M + r * ld;
+            const double* Mk = M + k * ld;
+            for (int j = c0; j < c1; ++j) Mr[j] -= f * Mk[j];
         }
         __syncthreads();
     }
@@ -682,7 +696,7 @@ struct BInvLevels {
 };
 
 __global__ void k_block_inverse(BInvLevels BL, int* err) {
-    extern __shared__ double M[];  // 56 x 112
+    extern __shared__ double M[];  // 56 x gj_ld(56)
     __shared__ double col[56];
     int lv = 0;
     while (lv + 1 < BL.nlev && (int)blockIdx.x >= BL.start[lv + 1]) ++lv;
@@ -694,8 +708,9 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
     const int q = blockIdx.x - BL.start[lv], t = threadIdx.x, nt = blockDim.x, n = L.n;
     const int B = blk_ids[q], nbk = n >> 2;
     const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
-    for (int idx = t; idx < 56 * 112; idx += nt) {
-        const int i = idx / 112, j = idx % 112;
+    constexpr int LD = gj_ld(56);
+    for (int idx = t; idx < 56 * LD; idx += nt) {
+        const int i = idx / LD, j = idx % LD;
         M[idx] = (j == 56 + i) ? 1.0 : 0.0;
     }
     __syncthreads();
@@ -705,7 +720,7 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
         const int a = i - bi, bb = j - bj;
         stokes_row_entries(L, f, [&](int f2, int da, int db, double v) {
             const int c = block_local(f2, a + da, bb + db);
-            if (c >= 0) M[t * 112 + c] += v;
+            if (c >= 0) M[t * LD + c] += v;
         });
     }
     __syncthreads();
@@ -714,14 +729,14 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
         for (int e = r.x; e < r.y; ++e) {
                 const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
             const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
-            if (c >= 0) M[t * 112 + c] -= E.val[e];
+            if (c >= 0) M[t * LD + c] -= E.val[e];
         }
     }
     __syncthreads();
     gauss_jordan(M, 56, col, err);
     for (int idx = t; idx < 56 * 56; idx += nt) {
         const int c = idx / 56, r = idx % 56;
-        Ainv[(size_t)q * 3136 + idx] = M[r * 112 + 56 + c];
+        Ainv[(size_t)q * 3136 + idx] = M[r * LD + 56 + c];
     }
 }
 
@@ -730,7 +745,7 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
 __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict__ Ainv, int* err) {
     extern __shared__ double M[];
     __shared__ double col[64];
-    const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = 2 * m, t = threadIdx.x, nt = blockDim.x;
+    const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = gj_ld(m), t = threadIdx.x, nt = blockDim.x;
     for (int idx = t; idx < m * ld; idx += nt) {
         const int i = idx / ld, j = idx % ld;
         M[idx] = (j == m + i) ? 1.0 : 0.0;
