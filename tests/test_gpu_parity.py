@@ -200,3 +200,66 @@ def test_no_structures_pure_stokes():
     xo, so, _ = o.solve(b)
     assert sg["converged"] and so["converged"] and abs(sg["iters"] - so["iters"]) <= 2
     assert rel(xg, xo) < 1e-8
+
+
+def test_consecutive_steps_track_oracle():
+    """Three implicit steps (lagged rebuild at the moving X^n each step)."""
+    prob = configs.config2(1e4, N=64, nb=128)
+    g, o = pair(prob)
+    n = prob.N
+    u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+    uo, Xo = np.zeros(2 * n * n), prob.X.copy()
+    for s in range(3):
+        sg = g.step_implicit(u, p, X)
+        uo, po, Xo, so = o.step(uo, Xo)
+        assert sg["converged"] and so["converged"], s
+        assert abs(sg["iters"] - so["iters"]) <= 2, s
+    assert rel(u, uo) < 1e-8 and rel(p, po) < 1e-8
+    assert rel(X.reshape(-1, 2), Xo) < 1e-8
+
+
+def test_membrane_across_periodic_boundary():
+    """An ellipse centred near the corner: windows, face lists and big blocks wrap."""
+    prob = configs.small_problem(N=64, nb=160, kappa=1e4, dt=1e-2, a=0.2, b=0.12, cx=0.03, cy=0.97, rot=0.4)
+    g, o = pair(prob)
+    for l in range(g.num_levels - 1):
+        assert np.array_equal(g.big_blocks(l), o.big_blocks(l)), l
+    n = prob.N
+    u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+    sg = g.step_implicit(u, p, X)
+    uo, po, Xo, so = o.step(np.zeros(2 * n * n), prob.X)
+    assert sg["converged"] and so["converged"] and abs(sg["iters"] - so["iters"]) <= 2
+    assert rel(u, uo) < 1e-8 and rel(X.reshape(-1, 2), Xo) < 1e-8
+
+
+def test_not_converged_is_a_flag():
+    """hitting max_iters returns the best iterate flagged, no error."""
+    prob = configs.config1()
+    g = SaddleSystem.from_problem(prob, max_iters=3)
+    b = g.build_rhs(np.zeros(2 * prob.N ** 2))
+    x, st = g.gmres_solve(b)
+    assert st["converged"] == 0 and st["iters"] == 3 and 0 < st["relres"] < 1
+
+
+def test_step_bitwise_deterministic():
+    prob = configs.config2(1e6, N=128, nb=256)
+    outs = []
+    for _ in range(2):
+        g = SaddleSystem.from_problem(prob)
+        n = prob.N
+        u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+        g.step_implicit(u, p, X)
+        outs.append((u, p, X))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_invalid_arguments_raise_value_error():
+    with pytest.raises(RuntimeError):
+        SaddleSystem(12)  # not a power of two -> ibmg_create status 1
+    prob = configs.config1()
+    g = SaddleSystem.from_problem(prob)
+    with pytest.raises(ValueError):
+        g.set_structures([2], [1.0], [0.01], np.zeros((2, 2)))  # FiberMesh: m1 >= 3
+    with pytest.raises(ValueError):
+        g.sweep(np.zeros(3 * 64 * 64), np.zeros(3 * 64 * 64), level=3)  # coarse-kernel level
