@@ -299,10 +299,21 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
         stokes_rows(L, W, i, j, ru, rv, rp);
         S.sr[gt] = Bv(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
     }
-    if (gt < 120) {
+    if (gt < 120) {  // E' row dots: 3 threads per row, gathers batched 8 at a time
         const int r = gt % 40, p = gt / 40;
+        const int e1 = slot.rp[r + 1];
         double s0 = 0.0;
-        for (int e = slot.rp[r] + p; e < slot.rp[r + 1]; e += 3) s0 += slot.val[e] * wloc[slot.col[e]];
+        for (int e = slot.rp[r] + p; e < e1; e += 24) {
+            double vv[8], xx[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int em = e + 3 * m;
+                vv[m] = em < e1 ? slot.val[em] : 0.0;
+                xx[m] = em < e1 ? wloc[slot.col[em]] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) s0 += vv[m] * xx[m];
+        }
         S.epart[p][r] = s0;
     }
     gsync();
@@ -376,14 +387,15 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // exactly the colour-ordered Gauss-Seidel schedule while blocks that do not
 // depend on each other run ahead.  The cooperative launch makes all CTAs
 // co-resident, and dependencies only point to smaller colours, so the waits
-// cannot deadlock.  The slab of the CTA's next block streams into the second
-// shared-memory slot while the current one is solved.
+// cannot deadlock.  Only the E' rows of the CTA's next block are
+// double-buffered in shared memory (2 x 31 KB -> 3 CTAs/SM); the 25 KB inverse
+// streams straight into registers at the start of each block.
 constexpr int kBigThreads = 128;
-constexpr size_t kBigSmem = 2 * sizeof(SlabSlot);
+constexpr size_t kBigSmem = 2 * sizeof(ESlot);
 __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC, BigDeps DP,
                                                             const double* __restrict__ b, double* w) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
+    ESlot* slot = reinterpret_cast<ESlot*>(dsm);
     __shared__ BigScratch S;
     const int t = threadIdx.x, G = gridDim.x, nbk = L.n >> 2;
     auto next_item = [&](int c, int q, int& nc, int& nq) {
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
     };
     int c, q;
     next_item(-1, 0, c, q);
-    if (c < BC.ncol) slab_issue(slot[0], SL, q, t, kBigThreads);
+    if (c < BC.ncol) eslot_issue(slot[0], SL, q, t, kBigThreads);
     cp_async_commit();
     GAccCG W{w, L.n, L.nn};
     GAccB B{b, L.n, L.nn};
@@ -407,21 +419,21 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
     while (c < BC.ncol) {
         int nc, nq;
         next_item(c, q, nc, nq);
-        if (nc < BC.ncol) slab_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
+        if (nc < BC.ncol) eslot_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
         cp_async_commit();
         // wait for the predecessors of block q (one thread per predecessor)
         for (int e = DP.poff[q] + t; e < DP.poff[q + 1]; e += kBigThreads)
             while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(32);
         cp_async_wait<1>();
         __syncthreads();
-        const SlabSlot& sl = slot[k & 1];
+        const ESlot& sl = slot[k & 1];
         const int Bk = sl.rp[47];
-        big_block_slab(L, sl, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, FlatCG{w}, B,
-                       [&](int f, int i, int j, double d) {
-                           double* p = w + (size_t)f * L.nn + i + (size_t)j * L.n;
-                           __stcg(p, __ldcg(p) + d);
-                       },
-                       S, t);
+        big_block_es(L, sl, SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, B,
+                     [&](int f, int i, int j, double d) {
+                         double* p = w + (size_t)f * L.nn + i + (size_t)j * L.n;
+                         __stcg(p, __ldcg(p) + d);
+                     },
+                     S, t, [] { __syncthreads(); });
         __syncthreads();
         if (t == 0) {
             __threadfence();
