@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
         cp_async_commit();
         // wait for the predecessors of block q (one thread per predecessor)
         for (int e = DP.poff[q] + t; e < DP.poff[q + 1]; e += kBigThreads)
-            while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(32);
+            while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(8);
         cp_async_wait<1>();
         __syncthreads();
         const ESlot& sl = slot[k & 1];
@@ -435,8 +435,7 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
                      },
                      S, t, [] { __syncthreads(); });
         __syncthreads();
-        if (t == 0) {
-            __threadfence();
+        if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(DP.flags + q, DP.epoch);
         }
         ++k;
@@ -518,7 +517,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
             const int ax = wr(tx + d % 3 - 1, nt), ay = wr(ty + d / 3 - 1, nt);
             const int ac = (ax & 1) + 2 * (ay & 1);
             if (ac < tc)
-                while (ld_acquire(A.tflags + ax + ay * nt) != epoch) __nanosleep(20);
+                while (ld_acquire(A.tflags + ax + ay * nt) != epoch) __nanosleep(8);
         }
         __syncwarp();
         const unsigned long long t_b = A.trace ? gtimer() : 0;
@@ -555,8 +554,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
             if (a < 16 && bb < 16) __stcg(A.w + 2 * nn + gi, W(2, a, bb));
         }
         __syncwarp();
-        if (lane == 0) {
-            __threadfence();
+        if (lane == 0) {  // warp-synchronous stores + st.release.gpu (cumulative) publish the tile
             st_release(A.tflags + tx + ty * nt, epoch);
             if (A.trace) {
                 unsigned long long* r = A.trace + 4 * task;
@@ -581,12 +579,12 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         const int bi = 4 * (Bk % nbk), bj = 4 * (Bk / nbk);
         const unsigned long long t_a = A.trace ? gtimer() : 0;
         for (int e = A.DP.poff[q] + t; e < A.DP.poff[q + 1]; e += 32 * kDfWarps)
-            while (ld_acquire(A.DP.flags + A.DP.pred[e]) != epoch) __nanosleep(20);
+            while (ld_acquire(A.DP.flags + A.DP.pred[e]) != epoch) __nanosleep(8);
         if (t < 9) {  // plain tiles within 8 cells of the block
             const int tx0 = (bi - 8) >> 4, ty0 = (bj - 8) >> 4;
             const int tx = tx0 + t % 3, ty = ty0 + t / 3;
             if (tx * kTile <= bi + 11 && ty * kTile <= bj + 11)
-                while (ld_acquire(A.tflags + wr(tx, nt) + wr(ty, nt) * nt) != epoch) __nanosleep(20);
+                while (ld_acquire(A.tflags + wr(tx, nt) + wr(ty, nt) * nt) != epoch) __nanosleep(8);
         }
         __syncthreads();
         const unsigned long long t_b = A.trace ? gtimer() : 0;
@@ -600,8 +598,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
                        },
                        S, t);
         __syncthreads();
-        if (t == 0) {
-            __threadfence();
+        if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(A.DP.flags + q, epoch);
             if (A.trace) {
                 unsigned long long* r = A.trace + 4 * ntiles + 6 * q;
