@@ -80,7 +80,7 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
                 asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup));
                 const int Bk = slot[g].rp[47];
                 big_block_es(L, slot[g], C.SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W,
-                             (const double*)w, B, [&](int f, int i, int j, double d) { W(f, i, j) += d; }, S[g], gt,
+                             (const double*)w, B, [&](int f, int i, int j, double old, double d) { W(f, i, j) = old + d; }, S[g], gt,
                              [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); });
             }
         }

@@ -19,6 +19,21 @@ __device__ __forceinline__ void stokes_rows(const Lev& L, const Acc& w, int i, i
     rp = -L.g * (w(0, ip, j) - uc) - L.g * (w(1, i, jp) - vc);
 }
 
+// One Stokes row (field f of cell (i, j)) only: the loads of the other two rows
+// are not issued (the box solves need one row per DOF).
+template <class Acc>
+__device__ __forceinline__ double stokes_row(const Lev& L, const Acc& w, int f, int i, int j) {
+    const int n = L.n;
+    const int im = wr(i - 1, n), ip = wr(i + 1, n), jm = wr(j - 1, n), jp = wr(j + 1, n);
+    if (f == 0)
+        return L.d * w(0, i, j) - L.c * (w(0, im, j) + w(0, ip, j) + w(0, i, jm) + w(0, i, jp)) +
+               L.g * (w(2, i, j) - w(2, im, j));
+    if (f == 1)
+        return L.d * w(1, i, j) - L.c * (w(1, i, jm) + w(1, i, jp) + w(1, im, j) + w(1, ip, j)) +
+               L.g * (w(2, i, j) - w(2, i, jm));
+    return -L.g * (w(0, ip, j) - w(0, i, j)) - L.g * (w(1, i, jp) - w(1, i, j));
+}
+
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
 __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;

@@ -60,6 +60,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---- plain phase, multi-tile levels (n >= 32): one warp per 16x16 tile.
 constexpr int kTile = 16, kReg = kTile + 4;  // region with a 2-cell halo
 
@@ -157,7 +163,7 @@ struct FlatG {
 
 constexpr int kGroup = 128;
 struct BigScratch {
-    double sr[56], se[40], part[2][56], epart[3][40];
+    double sr[56], se[40], part[2][56], epart[3][40], wold[56];
 };
 
 // ---- per-block "slab": all w-independent data of one big block, packed at
@@ -195,22 +201,22 @@ __device__ __forceinline__ void slab_issue(SlabSlot& slot, const Slabs& SL, int 
     for (int c = t; c < cnt / 4; c += nt) cp_async16(reinterpret_cast<char*>(slot.col) + 16 * c, cc + 16 * c);
 }
 
-// One big-block relaxation from a shared-memory slab by 128 threads: Stokes
+// One big-block relaxation from a shared-memory slab by 128 threads (flat
+// column encoding: every E' column is indexed through `wloc`): Stokes
 // residual of the 56 DOFs + E' row dots (3 threads per row) -> 56x56 inverse
 // (2 column halves) -> correction.  Only shared-memory traffic except E'
 // columns outside the staged region (global, not modified by this launch).
 template <class WA, class LocA, class GlobA, class BA, class WAdd>
 __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slot, int bi, int bj, const WA& W,
                                                const LocA& wloc, const GlobA& wglob, const BA& Bv, WAdd&& wadd,
-                                               BigScratch& S, int gt) {
+                                               BigScratch& S, int gt, unsigned long long* dbg = nullptr) {
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
         i = wr(i, L.n);
         j = wr(j, L.n);
-        double ru, rv, rp;
-        stokes_rows(L, W, i, j, ru, rv, rp);
-        S.sr[gt] = Bv(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
+        S.sr[gt] = Bv(f, i, j) - stokes_row(L, W, f, i, j);
+        S.wold[gt] = W(f, i, j);  // current value, reused for the correction (no re-read)
     }
     // E' row dots: 3 threads per row (strided entries), the column gathers
     // batched 8 at a time (independent loads in flight), fixed-order combine
@@ -218,23 +224,27 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
         const int r = gt % 40, p = gt / 40;
         const int e1 = slot.rp[r + 1];
         double s0 = 0.0;
-        for (int e = slot.rp[r] + p; e < e1; e += 24) {
-            int cc[8];
-            double vv[8], xx[8];
+        for (int e = slot.rp[r] + p; e < e1; e += 72) {  // one round of up to 24 gathers per thread
+            int cc[24];
+            double vv[24], xx[24];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < 24; ++m) {  // branch-free: clamp the index, mask the value
                 const int em = e + 3 * m;
-                cc[m] = em < e1 ? slot.col[em] : 0x7fffffff;
-                vv[m] = em < e1 ? slot.val[em] : 0.0;
+                const bool ok = em < e1;
+                cc[m] = slot.col[ok ? em : e];
+                vv[m] = ok ? slot.val[em] : 0.0;
             }
 #pragma unroll
-            for (int m = 0; m < 8; ++m)
-                xx[m] = cc[m] == 0x7fffffff ? 0.0 : (cc[m] >= 0 ? wloc[cc[m]] : wglob[-cc[m] - 1]);
+            for (int m = 0; m < 24; ++m) xx[m] = wloc[cc[m]];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) s0 += vv[m] * xx[m];
+            for (int m = 0; m < 24; ++m) s0 += vv[m] * xx[m];
         }
         S.epart[p][r] = s0;
     }
+    if (dbg && gt == 0) dbg[0] = gtimer();
+    __syncthreads();
+    if (dbg && gt == 0) dbg[1] = gtimer();
+    if (gt < 40) S.sr[gt] += (S.epart[0][gt] + S.epart[1][gt]) + S.epart[2][gt];  // combined residual
     __syncthreads();
     if (gt < 112) {
         const int row = gt % 56, cg = gt / 56;
@@ -242,19 +252,17 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
 #pragma unroll
         for (int c = 0; c < 28; c += 2) {
             const int cc = 28 * cg + c;
-            const double r0 = cc < 40 ? S.sr[cc] + ((S.epart[0][cc] + S.epart[1][cc]) + S.epart[2][cc]) : S.sr[cc];
-            const double r1 = cc + 1 < 40 ? S.sr[cc + 1] + ((S.epart[0][cc + 1] + S.epart[1][cc + 1]) + S.epart[2][cc + 1])
-                                          : S.sr[cc + 1];
-            s0 += slot.A[cc * 56 + row] * r0;
-            s1 += slot.A[(cc + 1) * 56 + row] * r1;
+            s0 += slot.A[cc * 56 + row] * S.sr[cc];
+            s1 += slot.A[(cc + 1) * 56 + row] * S.sr[cc + 1];
         }
         S.part[cg][row] = s0 + s1;
     }
     __syncthreads();
+    if (dbg && gt == 0) dbg[2] = gtimer();
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
-        wadd(f, i, j, S.part[0][gt] + S.part[1][gt]);
+        wadd(f, wr(i, L.n), wr(j, L.n), S.wold[gt], S.part[0][gt] + S.part[1][gt]);
     }
 }
 
@@ -295,38 +303,36 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
         block_dof(gt, bi, bj, f, i, j);
         i = wr(i, L.n);
         j = wr(j, L.n);
-        double ru, rv, rp;
-        stokes_rows(L, W, i, j, ru, rv, rp);
-        S.sr[gt] = Bv(f, i, j) - (f == 0 ? ru : f == 1 ? rv : rp);
+        S.sr[gt] = Bv(f, i, j) - stokes_row(L, W, f, i, j);
+        S.wold[gt] = W(f, i, j);  // current value, reused for the correction (no re-read)
     }
     if (gt < 120) {  // E' row dots: 3 threads per row, gathers batched 8 at a time
         const int r = gt % 40, p = gt / 40;
         const int e1 = slot.rp[r + 1];
         double s0 = 0.0;
-        for (int e = slot.rp[r] + p; e < e1; e += 24) {
-            double vv[8], xx[8];
+        for (int e = slot.rp[r] + p; e < e1; e += 72) {  // one round of up to 24 gathers per thread
+            double vv[24], xx[24];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < 24; ++m) {
                 const int em = e + 3 * m;
                 vv[m] = em < e1 ? slot.val[em] : 0.0;
                 xx[m] = em < e1 ? wloc[slot.col[em]] : 0.0;
             }
 #pragma unroll
-            for (int m = 0; m < 8; ++m) s0 += vv[m] * xx[m];
+            for (int m = 0; m < 24; ++m) s0 += vv[m] * xx[m];
         }
         S.epart[p][r] = s0;
     }
+    gsync();
+    if (gt < 40) S.sr[gt] += (S.epart[0][gt] + S.epart[1][gt]) + S.epart[2][gt];  // combined residual
     gsync();
     if (gt < 112) {
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (int c = 0; c < 28; c += 2) {
             const int cc = 28 * cg + c;
-            const double r0 = cc < 40 ? S.sr[cc] + ((S.epart[0][cc] + S.epart[1][cc]) + S.epart[2][cc]) : S.sr[cc];
-            const double r1 = cc + 1 < 40 ? S.sr[cc + 1] + ((S.epart[0][cc + 1] + S.epart[1][cc + 1]) + S.epart[2][cc + 1])
-                                          : S.sr[cc + 1];
-            s0 += av[c] * r0;
-            s1 += av[c + 1] * r1;
+            s0 += av[c] * S.sr[cc];
+            s1 += av[c + 1] * S.sr[cc + 1];
         }
         S.part[cg][row] = s0 + s1;
     }
@@ -334,7 +340,7 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
-        wadd(f, i, j, S.part[0][gt] + S.part[1][gt]);
+        wadd(f, wr(i, L.n), wr(j, L.n), S.wold[gt], S.part[0][gt] + S.part[1][gt]);
     }
 }
 
@@ -429,9 +435,8 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
         const ESlot& sl = slot[k & 1];
         const int Bk = sl.rp[47];
         big_block_es(L, sl, SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, B,
-                     [&](int f, int i, int j, double d) {
-                         double* p = w + (size_t)f * L.nn + i + (size_t)j * L.n;
-                         __stcg(p, __ldcg(p) + d);
+                     [&](int f, int i, int j, double old, double d) {
+                         __stcg(w + (size_t)f * L.nn + i + (size_t)j * L.n, old + d);
                      },
                      S, t, [] { __syncthreads(); });
         __syncthreads();
@@ -468,11 +473,6 @@ struct DfArgs {
     double* w;
     unsigned long long* trace;  // debug: per-task globaltimer stamps (nullptr in production)
 };
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 constexpr size_t kDfTileBytes = (3 * kReg * kReg + 3 * 289) * sizeof(double);
 constexpr size_t kDfSmem = 2 * sizeof(SlabSlot) + kDfWarps * ((kDfTileBytes + 15) / 16 * 16);
 
@@ -591,17 +591,17 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         cp_async_wait<1>();
         __syncthreads();
         const unsigned long long t_c = A.trace ? gtimer() : 0;
+        unsigned long long* dbgp = A.trace ? A.trace + 4 * ntiles + 9 * q + 6 : nullptr;
         big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg,
-                       [&](int f, int i, int j, double d) {
-                           double* p = A.w + (size_t)f * nn + i + (size_t)j * n;
-                           __stcg(p, __ldcg(p) + d);
+                       [&](int f, int i, int j, double old, double d) {
+                           __stcg(A.w + (size_t)f * nn + i + (size_t)j * n, old + d);
                        },
-                       S, t);
+                       S, t, dbgp);
         __syncthreads();
         if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(A.DP.flags + q, epoch);
             if (A.trace) {
-                unsigned long long* r = A.trace + 4 * ntiles + 6 * q;
+                unsigned long long* r = A.trace + 4 * ntiles + 9 * q;
                 r[0] = t_a;
                 r[1] = t_b;
                 r[2] = t_c;

@@ -25,7 +25,7 @@ for level in (0, 1):
         L.ibmg_debug_sweep_trace(g._h, level, bl.data_ptr(), wl.data_ptr(), out.ctypes.data, words)
     nt = (n // 16) ** 2
     tiles = out[: 4 * nt].reshape(-1, 4).astype(np.int64)
-    bigs = out[4 * nt:].reshape(-1, 6).astype(np.int64)
+    bigs = out[4 * nt:].reshape(-1, 9).astype(np.int64)
     t0 = min(tiles[:, 0].min(), bigs[:, 0].min() if len(bigs) else 1 << 62)
     print(f"level {level} n={n}: tiles={nt} big={len(bigs)}")
     print("  tile wait / work (us): mean %.2f / %.2f, last tile done at %.2f" % (
@@ -34,6 +34,9 @@ for level in (0, 1):
         print("  big wait-deps / wait-slab / solve (us): mean %.2f / %.2f / %.2f; end at %.2f" % (
             np.mean(bigs[:, 1] - bigs[:, 0]) / 1e3, np.mean(bigs[:, 2] - bigs[:, 1]) / 1e3,
             np.mean(bigs[:, 3] - bigs[:, 2]) / 1e3, (bigs[:, 3].max() - t0) / 1e3))
+        print("  solve phases (us): residual %.2f | sync %.2f | matvec+sync %.2f | write+publish %.2f" % (
+            np.mean(bigs[:, 6] - bigs[:, 2]) / 1e3, np.mean(bigs[:, 7] - bigs[:, 6]) / 1e3,
+            np.mean(bigs[:, 8] - bigs[:, 7]) / 1e3, np.mean(bigs[:, 3] - bigs[:, 8]) / 1e3))
         for col in range(int(bigs[:, 4].max()) + 1):
             m = bigs[:, 4] == col
             print(f"    colour {col}: {m.sum():3d} blocks, start {(bigs[m,0].min()-t0)/1e3:7.2f} done {(bigs[m,3].max()-t0)/1e3:7.2f} us")
