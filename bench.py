@@ -158,10 +158,13 @@ def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     lv = ctxinfo["levels"]  # list of (n, nbig) for multi-tile levels (n >= 32)
     sweeps = 2  # V(1,1)
     N = ctxinfo["N"]
-    if name == "k_plain_tiles":  # 4 tile-colour launches cover every cell once per sweep
-        return sum(72 * n * n * sweeps for n, _ in lv) * vcycles
-    if name == "k_big_phase":  # inverse + E' slab (~2000 entries x 12 B) + block w/b traffic
-        return sum((3136 * 8 + 2000 * 12 + 56 * 24) * nb * sweeps for _, nb in lv) * vcycles
+    big_bytes = 3136 * 8 + 2000 * 12 + 56 * 24  # inverse + E' slab (~2000 entries x 12 B) + block w/b traffic
+    if name == "k_plain_tiles":  # levels n > 512: 4 tile-colour launches cover every cell once per sweep
+        return sum(72 * n * n * sweeps for n, _ in lv if n > 512) * vcycles
+    if name == "k_big_phase":
+        return sum(big_bytes * nb * sweeps for n, nb in lv if n > 512) * vcycles
+    if name == "k_sweep_df":  # levels 64 <= n <= 512: the whole sweep (plain cells + big blocks)
+        return sum((72 * n * n + big_bytes * nb) * sweeps for n, nb in lv if 64 <= n <= 512) * vcycles
     if name == "k_residual_restrict":
         return sum(54 * n * n for n, _ in lv) * vcycles
     if name == "k_prolong_add":
@@ -327,6 +330,9 @@ def run_batch(args, rank, world):
     probs = {i: configs.config5_problem(i) for i in mine}
     W = min(args.workers, len(mine))
     ctxs = [SaddleSystem(256, 1.0, 1.0, 1e-3, device=dev) for _ in range(W)]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    for c in ctxs:  # share the SMs among the concurrent contexts
+        c.set_grid_limit(max(8, (2 * sms) // W))
     n2 = 256 * 256
 
     def work(w, host, out):

@@ -139,6 +139,7 @@ struct ibmg_ctx {
     bool have_structs = false;
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
+    int grid_limit = 0;     // optional cap on the persistent kernels' grids (concurrent contexts)
     unsigned long long* trace = nullptr;  // debug task timeline of the dataflow sweep
     // live per-kernel CUDA-event timing (bench roofline); off on the timed path
     bool prof = false;
@@ -739,7 +740,7 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
         DfArgs A{L, SL, BC, BigDeps{lb.pred, lb.poff, lb.flags, ++lb.epoch}, lb.tflags, lb.big, b, w, c->trace};
         void* args[] = {&A};
         if (c->prof) prof_begin(c, "k_sweep_df");
-        CK(cudaLaunchCooperativeKernel((const void*)k_sweep_df, dim3(c->df_grid_max), dim3(32 * kDfWarps), args,
+        CK(cudaLaunchCooperativeKernel((const void*)k_sweep_df, dim3(c->grid_limit > 0 ? std::min(c->grid_limit, c->df_grid_max) : c->df_grid_max), dim3(32 * kDfWarps), args,
                                        kDfSmem, c->s));
         if (c->prof) prof_end(c);
         ++c->launches;
@@ -748,7 +749,7 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
     for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big);
     if (lb.nbig == 0) return;
-    const int grid = std::min(widest, c->big_grid_max);
+    const int grid = std::min(widest, c->grid_limit > 0 ? std::min(c->grid_limit, c->big_grid_max) : c->big_grid_max);
     BigDeps DP{lb.pred, lb.poff, lb.flags, ++lb.epoch};
     void* args[] = {&L, &SL, &BC, &DP, (void*)&b, (void*)&w};
     if (c->prof) prof_begin(c, "k_big_phase");
@@ -1083,6 +1084,14 @@ const char* ibmg_last_error(const ibmg_ctx* c) { return c ? c->err.c_str() : "nu
 int ibmg_num_levels(const ibmg_ctx* c) { return c ? c->nlev : -1; }
 int ibmg_level_n(const ibmg_ctx* c, int l) { return (c && l >= 0 && l < c->nlev) ? c->lev[l].L.n : -1; }
 long long ibmg_kernel_launches(const ibmg_ctx* c) { return c ? c->launches : -1; }
+
+int ibmg_set_grid_limit(ibmg_ctx* c, int max_ctas) {
+    return api(c, [&]() -> int {
+        if (max_ctas < 0) throw InvalidArg("grid limit must be >= 0");
+        c->grid_limit = max_ctas;
+        return IBMG_OK;
+    });
+}
 
 int ibmg_profile(ibmg_ctx* c, int enable) {
     return api(c, [&]() -> int {
