@@ -100,6 +100,10 @@ long ibmg_elasticity_triplets(ibmg_ctx* ctx, int level, int* rows, int* cols, do
  * per-task globaltimer stamps (device b, w); returns the trace length in words. */
 long ibmg_debug_sweep_trace(ibmg_ctx* ctx, int level, const double* b, double* w, unsigned long long* out, long cap);
 
+/* Debug only: one coarse-cycle launch (device b, w at the first coarse-kernel
+ * level) with thread-0 globaltimer phase stamps; returns the stamp count. */
+long ibmg_debug_coarse_trace(ibmg_ctx* ctx, const double* b, double* w, unsigned long long* out, long cap);
+
 /* Replaces build_rhs (saddle.cpp:96-104): b = [(rho/dt) u^n + S F(X^n); 0]. */
 int ibmg_build_rhs(ibmg_ctx* ctx, const double* u_n, double* b, int ptr_kind);
 /* Replaces interpolate (fiber.cpp:116-140): U = S^T u (h^2 weights), 2*npts. */

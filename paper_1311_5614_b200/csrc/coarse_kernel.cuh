@@ -27,6 +27,7 @@ struct CLev {
 
 struct CoarseArgs {
     int nl, nu1, nu2;
+    unsigned long long* trace;  // debug: phase stamps by thread 0 (nullptr in production)
     CLev lv[4];
     const double* Acoarse;   // bordered inverse, col-major (3nn+1)^2
     const double* b_in;
@@ -41,7 +42,13 @@ struct SW {
     }
 };
 
-__device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* slot, BigScratch* S) {
+__device__ __forceinline__ void cmark(unsigned long long* tr, int& n) {
+    if (tr && threadIdx.x == 0) tr[n] = gtimer();
+    ++n;
+}
+
+__device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* slot, BigScratch* S,
+                             unsigned long long* tr, int& nm) {
     const Lev& L = C.L;
     const int n = L.n, t = threadIdx.x, nt = blockDim.x, nbk = n >> 2;
     SW W{w, n, L.nn};
@@ -66,26 +73,55 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
             }
             __syncthreads();
         }
+    cmark(tr, nm);  // plain phase done
     // big phase: colour classes in order; the blocks of a class (independent)
-    // are shared by 4 groups of 128 threads, each with its own E'-row slot
+    // are shared by 4 groups of 128 threads, each with its own E'-row slot.  A
+    // group refills its slot with its next block (possibly of a later colour)
+    // as soon as the current block's rows are consumed, so the load overlaps
+    // the rest of the solve and the colour barrier.
     const int g = t / kGroup, gt = t % kGroup, G = nt / kGroup;
+    auto next_of = [&](int c, int q, int& nc, int& nq) {  // this group's item after (c, q); c < 0 starts
+        nq = (c < 0) ? -1 : q + G;
+        nc = (c < 0) ? 0 : c;
+        while (nc < C.ncol) {
+            if (nq < 0) nq = C.coff[nc] + g;
+            if (nq < C.coff[nc + 1]) return;
+            ++nc;
+            nq = -1;
+        }
+    };
+    int cc, qq;
+    next_of(-1, 0, cc, qq);
+    if (cc < C.ncol) eslot_issue(slot[g], C.SL, qq, gt, kGroup);
+    cp_async_commit();
+    double av[28];  // this thread's part of the group's next inverse (prefetched)
+    if (cc < C.ncol) load_inverse_part(av, C.SL.Ainv + (size_t)qq * 3136, gt);
     for (int colour = 0; colour < C.ncol; ++colour) {
         const int cnt = C.coff[colour + 1] - C.coff[colour];
         for (int base = 0; base < cnt; base += G) {
-            if (base + g < cnt) {
-                const int q = C.coff[colour] + base + g;
-                eslot_issue(slot[g], C.SL, q, gt, kGroup);
-                cp_async_commit();
+            if (cc == colour && qq == C.coff[colour] + base + g) {
                 cp_async_wait<0>();
                 asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup));
                 const int Bk = slot[g].rp[47];
-                big_block_es(L, slot[g], C.SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W,
-                             (const double*)w, B, [&](int f, int i, int j, double old, double d) { W(f, i, j) = old + d; }, S[g], gt,
-                             [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); });
+                int nc, nq;
+                next_of(cc, qq, nc, nq);
+                big_block_es(L, slot[g], nullptr, 4 * (Bk % nbk), 4 * (Bk / nbk), W,
+                             (const double*)w, B,
+                             [&](int f, int i, int j, double old, double d) { W(f, i, j) = old + d; }, S[g], gt,
+                             [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); },
+                             [&] {
+                                 if (nc < C.ncol) eslot_issue(slot[g], C.SL, nq, gt, kGroup);
+                                 cp_async_commit();
+                             },
+                             av, nc < C.ncol ? C.SL.Ainv + (size_t)nq * 3136 : nullptr);
+                cc = nc;
+                qq = nq;
             }
         }
         __syncthreads();
     }
+    cp_async_wait<0>();
+    cmark(tr, nm);  // big phase done
 }
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
@@ -105,6 +141,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
     }
     double* r = sm + off;
     const int t = threadIdx.x, nt = blockDim.x;
+    int nm = 0;
+    cmark(A.trace, nm);
     for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) bl[0][q] = A.b_in[q];
     __syncthreads();
     for (int l = 0; l + 1 < A.nl; ++l) {
@@ -113,7 +151,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
         const int n = L.n, nn = L.nn;
         for (int q = t; q < 3 * nn; q += nt) wl[l][q] = 0.0;
         __syncthreads();
-        for (int s = 0; s < A.nu1; ++s) coarse_sweep(C, wl[l], bl[l], slot, S);
+        for (int s = 0; s < A.nu1; ++s) coarse_sweep(C, wl[l], bl[l], slot, S, A.trace, nm);
         // residual r = b - A w (stencil, then + E' w from the assembled rows)
         SW W{wl[l], n, nn};
         for (int q = t; q < nn; q += nt) {
@@ -141,6 +179,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
             bl[l + 1][2 * nnc + q] = 0.25 * (R(2, i, j) + R(2, i + 1, j) + R(2, i, j + 1) + R(2, i + 1, j + 1));
         }
         __syncthreads();
+        cmark(A.trace, nm);  // residual + restriction done
     }
     {
         const int l = A.nl - 1, nn = A.lv[l].L.nn, m = 3 * nn + 1;
@@ -150,6 +189,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
             wl[l][q] = s;
         }
         __syncthreads();
+        cmark(A.trace, nm);  // coarsest solve done
     }
     for (int l = A.nl - 2; l >= 0; --l) {
         const CLev& C = A.lv[l];
@@ -163,9 +203,11 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
             wl[l][2 * nn + q] += dp;
         }
         __syncthreads();
-        for (int s = 0; s < A.nu2; ++s) coarse_sweep(C, wl[l], bl[l], slot, S);
+        cmark(A.trace, nm);  // prolongation done
+        for (int s = 0; s < A.nu2; ++s) coarse_sweep(C, wl[l], bl[l], slot, S, A.trace, nm);
     }
     for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) A.w_out[q] = wl[0][q];
+    cmark(A.trace, nm);
 }
 
 }  // namespace ibmg

@@ -1252,6 +1252,28 @@ int ibmg_big_blocks(ibmg_ctx* c, int level, int* flags) {
 // Debug: run one dataflow sweep on `level` with per-task globaltimer stamps and
 // copy them out (tiles: 4 words each, then big blocks: 6 words each).  Returns
 // the number of words, or -1.  Not part of the solver path.
+// Debug: one coarse-cycle launch with phase stamps (thread 0, globaltimer):
+// [start, per level down: plain, big, restrict; coarsest; per level up:
+// prolong, plain, big; end].  Returns the number of stamps, or -1.
+long ibmg_debug_coarse_trace(ibmg_ctx* c, const double* b, double* w, unsigned long long* out, long cap) {
+    try {
+        if (!c) return -1;
+        CK(cudaSetDevice(c->prm.device));
+        unsigned long long* d = dalloc<unsigned long long>(64);
+        CK(cudaMemset(d, 0, sizeof(unsigned long long) * 64));
+        CoarseArgs A = coarse_args(c, b, w);
+        A.trace = d;
+        LAUNCH(c, k_coarse_cycle, 1, kCoarseThreads, coarse_smem(c), A);
+        CK(cudaStreamSynchronize(c->s));
+        if (out) CK(cudaMemcpy(out, d, sizeof(unsigned long long) * std::min<long>(64, cap), cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        return 64;
+    } catch (const std::exception& e) {
+        fail(c, e, -1);
+        return -1;
+    }
+}
+
 long ibmg_debug_sweep_trace(ibmg_ctx* c, int level, const double* b, double* w, unsigned long long* out, long cap) {
     try {
         if (!c || level < 0 || level >= c->lc) return -1;

@@ -287,17 +287,33 @@ __device__ __forceinline__ void eslot_issue(ESlot& slot, const Slabs& SL, int q,
 // big_block_slab with the E' rows from an ESlot and the inverse streamed from
 // global memory straight into registers (issued first, overlapping the
 // residual).  `gsync` is the group barrier.
-template <class WA, class LocA, class BA, class WAdd, class Sync>
-__device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, const double* __restrict__ A_q, int bi,
-                                             int bj, const WA& W, const LocA& wloc, const BA& Bv, WAdd&& wadd,
-                                             BigScratch& S, int gt, Sync&& gsync) {
-    double av[28];
-    const int row = gt % 56, cg = gt / 56;
+struct NoOp {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// `after_rows` runs right after the first group barrier, when the slot's E'
+// rows have been consumed (callers refill the slot with the next block there).
+__device__ __forceinline__ void load_inverse_part(double (&av)[28], const double* __restrict__ A_q, int gt) {
     if (gt < 112) {
-        const double* A = A_q + (size_t)(28 * cg) * 56 + row;
+        const double* A = A_q + (size_t)(28 * (gt / 56)) * 56 + gt % 56;
 #pragma unroll
         for (int c = 0; c < 28; ++c) av[c] = __ldg(A + c * 56);
     }
+}
+
+// The inverse arrives in `av` (this thread's 28 entries): loaded here when
+// A_q != nullptr, else preloaded by the caller; A_next != nullptr prefetches
+// the next block's part into `av` after the apply, hiding its L2 latency
+// behind the write-back and the colour barrier.
+template <class WA, class LocA, class BA, class WAdd, class Sync, class After = NoOp>
+__device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, const double* __restrict__ A_q, int bi,
+                                             int bj, const WA& W, const LocA& wloc, const BA& Bv, WAdd&& wadd,
+                                             BigScratch& S, int gt, Sync&& gsync, After after_rows = After{},
+                                             double* avp = nullptr, const double* __restrict__ A_next = nullptr) {
+    double avl[28];
+    double (&av)[28] = avp ? *reinterpret_cast<double(*)[28]>(avp) : avl;
+    const int row = gt % 56, cg = gt / 56;
+    if (A_q) load_inverse_part(av, A_q, gt);
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
@@ -324,6 +340,7 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
         S.epart[p][r] = s0;
     }
     gsync();
+    after_rows();
     if (gt < 40) S.sr[gt] += (S.epart[0][gt] + S.epart[1][gt]) + S.epart[2][gt];  // combined residual
     gsync();
     if (gt < 112) {
@@ -336,6 +353,7 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
         }
         S.part[cg][row] = s0 + s1;
     }
+    if (A_next) load_inverse_part(av, A_next, gt);
     gsync();
     if (gt < 56) {
         int f, i, j;

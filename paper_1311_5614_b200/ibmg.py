@@ -45,7 +45,8 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_level_n", "ibmg_apply", "ibmg_residual", "ibmg_restrict", "ibmg_prolong_add", "ibmg_sweep",
            "ibmg_vcycle", "ibmg_coarse_solve", "ibmg_big_blocks", "ibmg_build_rhs", "ibmg_interpolate",
            "ibmg_spread", "ibmg_solve", "ibmg_step", "ibmg_kernel_launches", "ibmg_stream", "ibmg_profile",
-           "ibmg_profile_report", "ibmg_elasticity_triplets", "ibmg_debug_sweep_trace", "ibmg_set_grid_limit"]
+           "ibmg_profile_report", "ibmg_elasticity_triplets", "ibmg_debug_sweep_trace", "ibmg_set_grid_limit",
+           "ibmg_debug_coarse_trace"]
 
 
 def lib_path() -> str:
@@ -93,6 +94,8 @@ def lib(build_if_missing: bool = True):
     L.ibmg_elasticity_triplets.restype = C.c_long
     L.ibmg_elasticity_triplets.argtypes = [vp, ip, vp, vp, vp, C.c_long]
     L.ibmg_set_grid_limit.argtypes = [vp, ip]
+    L.ibmg_debug_coarse_trace.restype = C.c_long
+    L.ibmg_debug_coarse_trace.argtypes = [vp, vp, vp, vp, C.c_long]
     L.ibmg_profile.argtypes = [vp, ip]
     L.ibmg_profile_report.argtypes = [vp, C.c_char_p, ip]
     _LIB = L

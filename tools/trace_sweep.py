@@ -40,3 +40,14 @@ for level in (0, 1):
         for col in range(int(bigs[:, 4].max()) + 1):
             m = bigs[:, 4] == col
             print(f"    colour {col}: {m.sum():3d} blocks, start {(bigs[m,0].min()-t0)/1e3:7.2f} done {(bigs[m,3].max()-t0)/1e3:7.2f} us")
+
+# coarse kernel phases (levels n <= 32)
+lc = next(l for l in range(g.num_levels) if g.level_n(l) <= 32)
+nc = g.level_n(lc)
+bc = torch.tensor(np.random.default_rng(0).uniform(-1, 1, 3 * nc * nc), device="cuda")
+wc = torch.zeros_like(bc)
+out = np.zeros(64, np.uint64)
+for rep in range(3):
+    L.ibmg_debug_coarse_trace(g._h, bc.data_ptr(), wc.data_ptr(), out.ctypes.data, 64)
+st = out[out > 0].astype(np.int64)
+print("coarse kernel phases (us):", np.round(np.diff(st) / 1e3, 2).tolist(), "total %.1f" % ((st[-1] - st[0]) / 1e3))
