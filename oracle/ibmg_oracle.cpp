@@ -421,29 +421,117 @@ void extract(const Csr& A, const int* d, int m, DenseLu& lu) {
         for (int c = 0; c < m; ++c) lu.a[size_t(r) * m + c] = A.at(d[r], d[c]);
 }
 
-// Deterministic greedy colouring of the big 4x4 blocks:
-// blocks in ascending id (bx + by*nbk) take the smallest colour unused by
-// already-coloured big blocks within Chebyshev block distance 2 (periodic).
-// Same-colour blocks are then >= 8 cells apart, beyond the E' reach (<= 7,
-// checked at setup), so a colour class is a set of independent boxes.
-// Mirrored exactly by the GPU host (paper_1311_5614_b200/csrc/ibmg.cu).
-std::vector<int> greedy_block_colours(const std::vector<char>& big, int nbk, int* ncol) {
-    std::vector<int> col(big.size(), -1);
-    *ncol = 0;
-    for (int by = 0; by < nbk; ++by)
-        for (int bx = 0; bx < nbk; ++bx) {
-            if (!big[bx + by * nbk]) continue;
-            unsigned long long used = 0;
-            for (int dy = -2; dy <= 2; ++dy)
-                for (int dx = -2; dx <= 2; ++dx) {
-                    const int c = col[wrap(bx + dx, nbk) + wrap(by + dy, nbk) * nbk];
-                    if (c >= 0) used |= 1ull << c;
-                }
-            int k = 0;
-            while (used >> k & 1ull) ++k;
-            col[bx + by * nbk] = k;
-            *ncol = std::max(*ncol, k + 1);
+// Canonical periodic block offset in [-nbk/2, nbk/2).
+inline int canon(int d, int nbk) { return wrap(d + nbk / 2, nbk) - nbk / 2; }
+
+// Big-block conflict graph.  Two big blocks conflict (may
+// not share a colour, and the later waits for the earlier) when their
+// canonical periodic offset has Chebyshev length 1 (shared faces, stencil
+// coupling), or length 2 and E'_l couples their boxes: some point k has a
+// nonzero left-window entry on a face of one box and one of k-1, k, k+1 a
+// nonzero right-window entry of the same component on a face of the other
+// (E'_l = sum_k L_k c_k (R_{k-1} - 2 R_k + R_{k+1}); the E' reach <= 7
+// excludes length >= 3).  The length-2 couplings are bit (dx+2) + 5 (dy+2) of
+// mask[A]; mirrored by k_block_pairs + colour_big_blocks on the GPU.
+std::vector<unsigned> block_pair_masks(const Level& L, const std::vector<int>& kprev, const std::vector<int>& knext) {
+    const int n = L.n, nn = n * n, nbk = n / 4;
+    std::vector<unsigned> mask(size_t(nbk) * nbk, 0u);
+    auto owners = [&](const SpVec& win, std::vector<int>& out) {
+        for (auto& e : win) {
+            const int f = e.first % nn, i = f % n, j = f / n;
+            const bool is_u = e.first < nn;
+            const int i2 = is_u ? wrap(i - 1, n) : i, j2 = is_u ? j : wrap(j - 1, n);
+            out.push_back((i / 4) + (j / 4) * nbk);
+            out.push_back((i2 / 4) + (j2 / 4) * nbk);
         }
+    };
+    const int npts = int(L.Lu.size());
+    std::vector<int> la, ra;
+    for (int k = 0; k < npts; ++k)
+        for (int comp = 0; comp < 2; ++comp) {
+            la.clear();
+            ra.clear();
+            owners(comp ? L.Lv[k] : L.Lu[k], la);
+            for (int kk : {kprev[k], k, knext[k]}) owners(comp ? L.Rv[kk] : L.Ru[kk], ra);
+            for (int A : la)
+                for (int B : ra) {
+                    const int dx = canon(B % nbk - A % nbk, nbk), dy = canon(B / nbk - A / nbk, nbk);
+                    if (std::max(std::abs(dx), std::abs(dy)) != 2) continue;
+                    const int ex = canon(A % nbk - B % nbk, nbk), ey = canon(A / nbk - B / nbk, nbk);
+                    mask[A] |= 1u << ((dx + 2) + 5 * (dy + 2));
+                    mask[B] |= 1u << ((ex + 2) + 5 * (ey + 2));
+                }
+        }
+    return mask;
+}
+
+// Deterministic colouring of the big blocks over the conflict graph above
+// (neighbours listed in offset order dy, dx ascending): DSatur — the block
+// with the most distinct neighbour colours, then the highest conflict degree,
+// then the most recently queued, takes its smallest free colour — when the
+// level has <= kDsaturMax big blocks, else greedy in ascending block id.
+// Mirrored exactly by the GPU host (paper_1311_5614_b200/csrc/ibmg.cu).
+constexpr int kDsaturMax = 4096;
+std::vector<int> colour_blocks(const std::vector<char>& big, const std::vector<unsigned>& mask, int nbk, int* ncol) {
+    std::vector<int> ids, pos(big.size(), -1);
+    for (int q = 0; q < int(big.size()); ++q)
+        if (big[q]) {
+            pos[q] = int(ids.size());
+            ids.push_back(q);
+        }
+    const int nb = int(ids.size());
+    std::vector<std::vector<int>> adj(nb);
+    for (int v = 0; v < nb; ++v) {
+        const int A = ids[v], ax = A % nbk, ay = A / nbk;
+        for (int dy = -2; dy <= 2; ++dy)
+            for (int dx = -2; dx <= 2; ++dx) {
+                const int B = wrap(ax + dx, nbk) + wrap(ay + dy, nbk) * nbk;
+                if (B == A || !big[B]) continue;
+                const int cx = canon(B % nbk - ax, nbk), cy = canon(B / nbk - ay, nbk);
+                const int len = std::max(std::abs(cx), std::abs(cy));
+                if (len > 2 || (len == 2 && !(mask[A] >> ((cx + 2) + 5 * (cy + 2)) & 1u))) continue;
+                if (std::find(adj[v].begin(), adj[v].end(), pos[B]) == adj[v].end()) adj[v].push_back(pos[B]);
+            }
+    }
+    std::vector<int> col(big.size(), -1), cv(nb, -1);
+    std::vector<unsigned long long> used(nb, 0ull);
+    *ncol = 0;
+    auto take = [&](int v) {
+        int k = 0;
+        while (used[v] >> k & 1ull) ++k;
+        cv[v] = k;
+        col[ids[v]] = k;
+        *ncol = std::max(*ncol, k + 1);
+        return k;
+    };
+    if (nb > kDsaturMax) {
+        for (int v = 0; v < nb; ++v) {
+            const int k = take(v);
+            for (int u : adj[v]) used[u] |= 1ull << k;
+        }
+        return col;
+    }
+    // bucket queue on saturation * 32 + degree, last pushed first within a
+    // bucket (stale entries skipped), as the GPU host
+    std::vector<int> sat(nb, 0);
+    std::vector<std::vector<int>> bucket(32 * 32);
+    auto key = [&](int v) { return sat[v] * 32 + int(adj[v].size()); };
+    for (int v = 0; v < nb; ++v) bucket[key(v)].push_back(v);
+    for (int done = 0; done < nb;) {
+        int top = 32 * 32 - 1;
+        while (bucket[top].empty()) --top;
+        const int v = bucket[top].back();
+        bucket[top].pop_back();
+        if (cv[v] >= 0 || key(v) != top) continue;
+        const int k = take(v);
+        ++done;
+        for (int u : adj[v]) {
+            if (cv[u] >= 0 || (used[u] >> k & 1ull)) continue;
+            used[u] |= 1ull << k;
+            ++sat[u];
+            bucket[key(u)].push_back(u);
+        }
+    }
     return col;
 }
 
@@ -454,7 +542,7 @@ std::vector<int> greedy_block_colours(const std::vector<char>& big, int nbk, int
 // in colour order.  Boxes within one pass are mutually independent, so each
 // pass is exactly a Gauss-Seidel pass in any order (SPEC.md:427-431
 // semantics) and the GPU runs it in parallel.
-void build_schedule(Level& L) {
+void build_schedule(Level& L, const std::vector<int>& kprev, const std::vector<int>& knext) {
     const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4;
     L.passes.clear();
     const int ntc = nt >= 2 ? 4 : 1;
@@ -474,7 +562,7 @@ void build_schedule(Level& L) {
         }
     }
     int ncol = 0;
-    const std::vector<int> col = greedy_block_colours(L.big, nbk, &ncol);
+    const std::vector<int> col = colour_blocks(L.big, block_pair_masks(L, kprev, knext), nbk, &ncol);
     for (int bc = 0; bc < ncol; ++bc) {
         Pass p;
         p.big = true;
@@ -539,6 +627,13 @@ void build(Ctx& C) {
     }
     const int nl = int(C.lev.size());
     const int npts = C.npts;
+    // closed-curve neighbours of every point (membrane-local, periodic in s1)
+    std::vector<int> kprev(npts), knext(npts);
+    for (size_t m = 0; m < C.nb.size(); ++m)
+        for (int k = 0; k < C.nb[m]; ++k) {
+            kprev[C.off[m] + k] = C.off[m] + (k == 0 ? C.nb[m] - 1 : k - 1);
+            knext[C.off[m] + k] = C.off[m] + (k == C.nb[m] - 1 ? 0 : k + 1);
+        }
     // fine windows + E' (elasticity.cpp:62-107, with per-membrane kappa and dt)
     {
         Level& L = C.lev[0];
@@ -612,7 +707,7 @@ void build(Ctx& C) {
             continue;
         }
         mark_big(L, npts);
-        build_schedule(L);
+        build_schedule(L, kprev, knext);
         L.blk.assign(L.big.size(), DenseLu{});
         int d[56];
         for (size_t bkk = 0; bkk < L.big.size(); ++bkk) {

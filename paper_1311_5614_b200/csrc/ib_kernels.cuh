@@ -167,31 +167,102 @@ __global__ void k_mark_big(int npts, Win W, int n, uint8_t* flags) {
     }
 }
 
-// Reach of E' on a level: the extent (in face index units) of the union of
-// L_k and R_{k-1}, R_k, R_{k+1} supports, max over points and components.
-// Same-colour big blocks are >= 8 cells apart, so the schedule requires <= 7.
-__global__ void k_reach(int npts, Win W, Pts P, int* out) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= npts) return;
-    int ext = 0;
-    for (int comp = 0; comp < 2; ++comp) {
-        int lo_i = 1 << 30, hi_i = -(1 << 30), lo_j = 1 << 30, hi_j = -(1 << 30);
-        const int ks[4] = {k, P.kprev[k], k, P.knext[k]};
-        for (int t = 0; t < 4; ++t) {
-            const int s = (t == 0 ? 0 : 2) + comp;
-            const int kk = ks[t];
-            const int4 o = (s < 2) ? W.orgL[kk] : W.orgR[kk];
-            const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
-            for (int e = 0; e < 16; ++e) {
-                if (W.w[(size_t)kk * 64 + s * 16 + e] == 0.0) continue;
-                const int i = i0 + (e & 3), j = j0 + (e >> 2);
-                lo_i = min(lo_i, i); hi_i = max(hi_i, i);
-                lo_j = min(lo_j, j); hi_j = max(hi_j, j);
-            }
-        }
-        if (hi_i >= lo_i) ext = max(ext, max(hi_i - lo_i, hi_j - lo_j));
+// Nonzero support of window slot s of point k: unwrapped extent (for the
+// E' reach) and its owner blocks (a face belongs to the cell on its high side
+// and the one below/left) as a 2x2 occupancy over the unwrapped base block
+// (bx0, by0): the owners of a 4x4 patch span at most 5 cells per axis, i.e.
+// at most two blocks.
+struct WinSupport {
+    int bx0, by0;
+    unsigned occ;  // bit dx + 2 dy
+};
+__device__ __forceinline__ WinSupport window_support(const Win& W, int k, int s, int& lo_i, int& hi_i, int& lo_j,
+                                                     int& hi_j) {
+    const int4 o = (s < 2) ? W.orgL[k] : W.orgR[k];
+    const int comp = s & 1;
+    const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+    WinSupport r{(i0 - (comp ? 0 : 1)) >> 2, (j0 - comp) >> 2, 0u};
+    const double* p = W.w + (size_t)k * 64 + s * 16;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        if (p[e] == 0.0) continue;
+        const int i = i0 + (e & 3), j = j0 + (e >> 2);
+        lo_i = min(lo_i, i);
+        hi_i = max(hi_i, i);
+        lo_j = min(lo_j, j);
+        hi_j = max(hi_j, j);
+        const int i2 = comp ? i : i - 1, j2 = comp ? j - 1 : j;
+        r.occ |= 1u << (((i >> 2) - r.bx0) + 2 * ((j >> 2) - r.by0));
+        r.occ |= 1u << (((i2 >> 2) - r.bx0) + 2 * ((j2 >> 2) - r.by0));
     }
-    atomicMax(out, ext);
+    return r;
+}
+
+__device__ __forceinline__ int canon_off(int d, int nbk) { return wr(d + nbk / 2, nbk) - nbk / 2; }
+
+// Per point k and component comp (oracle block_pair_masks):
+//  * the length-2 couplings of the big-block conflict graph: every pair (A, B)
+//    of boxes with A owning a nonzero left-window entry of k and B a nonzero
+//    right-window entry of k-1, k or k+1 at canonical Chebyshev offset 2 sets
+//    bit (dx+2) + 5 (dy+2) in mask[A] and the mirrored bit in mask[B];
+//  * the E' reach: the extent (face index units) of the union of the L_k and
+//    R_{k-1}, R_k, R_{k+1} supports, max into *reach (same-colour blocks are
+//    >= 8 cells apart only when it is <= 7, checked at setup).
+__global__ void k_block_pairs(int npts, Win W, Pts P, int n, unsigned* __restrict__ mask, int* __restrict__ reach) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= npts * 2) return;
+    const int k = q >> 1, comp = q & 1, nbk = n >> 2;
+    int lo_i = 1 << 30, hi_i = -(1 << 30), lo_j = 1 << 30, hi_j = -(1 << 30);
+    const WinSupport Ls = window_support(W, k, comp, lo_i, hi_i, lo_j, hi_j);
+    const WinSupport Rs[3] = {window_support(W, P.kprev[k], 2 + comp, lo_i, hi_i, lo_j, hi_j),
+                              window_support(W, k, 2 + comp, lo_i, hi_i, lo_j, hi_j),
+                              window_support(W, P.knext[k], 2 + comp, lo_i, hi_i, lo_j, hi_j)};
+    if (hi_i >= lo_i) atomicMax(reach, max(hi_i - lo_i, hi_j - lo_j));
+    for (int x = 0; x < 4; ++x) {
+        if (!(Ls.occ >> x & 1u)) continue;
+        const int ax = Ls.bx0 + (x & 1), ay = Ls.by0 + (x >> 1);
+        const int A = wr(ax, nbk) + wr(ay, nbk) * nbk;
+        for (int r = 0; r < 3; ++r)
+            for (int y = 0; y < 4; ++y) {
+                if (!(Rs[r].occ >> y & 1u)) continue;
+                const int bx = Rs[r].bx0 + (y & 1), by = Rs[r].by0 + (y >> 1);
+                const int dx = canon_off(bx - ax, nbk), dy = canon_off(by - ay, nbk);
+                if (max(abs(dx), abs(dy)) != 2) continue;
+                const int B = wr(bx, nbk) + wr(by, nbk) * nbk;
+                const int ex = canon_off(ax - bx, nbk), ey = canon_off(ay - by, nbk);
+                atomicOr(mask + A, 1u << ((dx + 2) + 5 * (dy + 2)));
+                atomicOr(mask + B, 1u << ((ex + 2) + 5 * (ey + 2)));
+            }
+    }
+}
+
+// Conflict masks of the big blocks (oracle colour_blocks),
+// in place over the k_block_pairs output: for a big block A, bit
+// (dx+2) + 5 (dy+2) for every offset (dx, dy) != 0 in [-2, 2]^2 whose block
+// B = A + (dx, dy) (periodic) is big, is not A itself, and conflicts with A —
+// canonical Chebyshev offset 1, or 2 with the pair bit set — and bit 12
+// (the zero offset) marking A big; 0 for blocks that are not big.
+__global__ void k_block_conflicts(int n, const uint8_t* __restrict__ big, unsigned* __restrict__ mask) {
+    const int nbk = n >> 2;
+    const int A = blockIdx.x * blockDim.x + threadIdx.x;
+    if (A >= nbk * nbk) return;
+    if (!big[A]) {
+        mask[A] = 0u;
+        return;
+    }
+    const unsigned pairs = mask[A];
+    const int ax = A % nbk, ay = A / nbk;
+    unsigned m = 1u << 12;
+    for (int dy = -2; dy <= 2; ++dy)
+        for (int dx = -2; dx <= 2; ++dx) {
+            const int B = wr(ax + dx, nbk) + wr(ay + dy, nbk) * nbk;
+            if (B == A || !big[B]) continue;
+            const int cx = canon_off(dx, nbk), cy = canon_off(dy, nbk);
+            const int len = max(abs(cx), abs(cy));
+            if (len > 2 || (len == 2 && !(pairs >> ((cx + 2) + 5 * (cy + 2)) & 1u))) continue;
+            m |= 1u << ((dx + 2) + 5 * (dy + 2));
+        }
+    mask[A] = m;
 }
 
 // F_k for both components from field w on a level (thread per point).

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <map>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -79,6 +80,7 @@ struct LevelBuf {
     int maxrow = 0;          // longest face list (selects the E'-row assembly kernel)
     long e_cap = 0;
     uint8_t* big = nullptr;
+    unsigned* cmask = nullptr;  // length-2 conflict bits per block (k_block_pairs)
     int nbig = 0;
     int* blk_ids = nullptr;  // big blocks sorted by colour, ascending id within
     int blk_cap = 0;
@@ -104,6 +106,9 @@ struct LevelBuf {
 
     double* Ainv = nullptr;
     int ainv_cap = 0;
+    std::vector<int> h_ids, h_pred, h_poff;  // host sources of the async uploads above
+    std::vector<int> h_pos;                  // block -> list position scratch (colouring)
+    unsigned* h_cm = nullptr;                // pinned mirror of cmask
 };
 
 }  // namespace
@@ -234,6 +239,8 @@ void alloc_levels(ibmg_ctx* c) {
         lb.r = dalloc<double>(m);
         if (n > p.coarsest_n) {
             lb.big = dalloc<uint8_t>(size_t(n / 4) * (n / 4));
+            lb.cmask = dalloc<unsigned>(size_t(n / 4) * (n / 4));
+            CK(cudaMallocHost(&lb.h_cm, sizeof(unsigned) * (n / 4) * (n / 4)));
             lb.bq = dalloc<int>(size_t(n / 4) * (n / 4));
             if (n >= 4 * kTile) {
                 lb.tflags = dalloc<unsigned>(size_t(n / kTile) * (n / kTile));
@@ -332,33 +339,97 @@ void free_structs(ibmg_ctx* c) {
 // rule as the oracle (oracle/ibmg_oracle.cpp greedy_block_colours): ascending
 // block id, smallest colour unused within Chebyshev block distance 2
 // (periodic).  Produces the colour-major block list and colour offsets.
-void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const uint8_t* big) {
-    const int nbk = lb.L.n / 4;
-    std::vector<int> col(size_t(nbk) * nbk, -1);
-    int ncol = 0, nbig = 0;
-    for (int by = 0; by < nbk; ++by)
-        for (int bx = 0; bx < nbk; ++bx) {
-            if (!big[bx + by * nbk]) continue;
-            unsigned long long used = 0;
-            for (int dy = -2; dy <= 2; ++dy)
-                for (int dx = -2; dx <= 2; ++dx) {
-                    const int k = col[wr(bx + dx, nbk) + wr(by + dy, nbk) * nbk];
-                    if (k >= 0) used |= 1ull << k;
-                }
-            int k = 0;
-            while (used >> k & 1ull) ++k;
-            col[bx + by * nbk] = k;
-            ncol = std::max(ncol, k + 1);
-            ++nbig;
+// Colouring of the big blocks over their conflict graph (
+// oracle colour_blocks, mirrored exactly).  cm[] is the k_block_conflicts
+// mask (bit 12: big; other bits: conflicting neighbour at that offset).
+// Levels with <= kDsaturMax big blocks: DSatur — repeatedly colour the block
+// with the most distinct neighbour colours, then the highest conflict degree
+// (a bucket queue on saturation * 32 + degree, last pushed first within a
+// bucket), with its smallest free colour; larger levels: greedy in ascending
+// block id.  The predecessors of a block (barrier-free big phase) are its
+// conflicting neighbours of smaller colour; same-colour blocks never conflict.
+constexpr int kDsaturMax = 4096;
+void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
+    const int nbk = lb.L.n / 4, lgb = lb.L.lg - 2;
+    std::vector<int>& pos_of = lb.h_pos;  // persistent, all -1 between calls
+    if (pos_of.size() != size_t(nbk) * nbk) pos_of.assign(size_t(nbk) * nbk, -1);
+    std::vector<int> vid;
+    for (int q = 0; q < nbk * nbk; ++q)
+        if (cm[q]) {
+            pos_of[q] = int(vid.size());
+            vid.push_back(q);
         }
+    const int nbig = int(vid.size());
+    std::vector<int> aoff(nbig + 1, 0), adj;
+    adj.reserve(size_t(nbig) * 12);
+    for (int v = 0; v < nbig; ++v) {
+        const int A = vid[v], ax = A & (nbk - 1), ay = A >> lgb;
+        for (unsigned m = cm[A] & ~(1u << 12); m; m &= m - 1) {
+            const int bit = __builtin_ctz(m), dx = bit % 5 - 2, dy = bit / 5 - 2;
+            const int u = pos_of[wr(ax + dx, nbk) + (wr(ay + dy, nbk) << lgb)];
+            // distinct offsets alias on tiny periodic levels: keep each neighbour once
+            if (nbk >= 5 || std::find(adj.begin() + aoff[v], adj.end(), u) == adj.end()) adj.push_back(u);
+        }
+        aoff[v + 1] = int(adj.size());
+    }
+    for (int q : vid) pos_of[q] = -1;
+    std::vector<int> cv(nbig, -1);
+    std::vector<unsigned long long> used(nbig, 0ull);
+    int ncol = 0;
+    auto take = [&](int v) {
+        int k = 0;
+        while (used[v] >> k & 1ull) ++k;
+        cv[v] = k;
+        ncol = std::max(ncol, k + 1);
+        return k;
+    };
+    if (nbig > kDsaturMax) {
+        for (int v = 0; v < nbig; ++v) {
+            const int k = take(v);
+            for (int e = aoff[v]; e < aoff[v + 1]; ++e) used[adj[e]] |= 1ull << k;
+        }
+    } else {
+        // bucket queue with intrusive LIFO lists; stale entries are skipped
+        std::vector<int> sat(nbig, 0), head(32 * 32, -1), ev, en;
+        ev.reserve(size_t(nbig) * 4);
+        en.reserve(size_t(nbig) * 4);
+        auto key = [&](int v) { return sat[v] * 32 + (aoff[v + 1] - aoff[v]); };
+        int top = 0;
+        auto push = [&](int v) {
+            const int b = key(v);
+            ev.push_back(v);
+            en.push_back(head[b]);
+            head[b] = int(ev.size()) - 1;
+            top = std::max(top, b);
+        };
+        for (int v = 0; v < nbig; ++v) push(v);
+        for (int done = 0; done < nbig;) {
+            while (head[top] < 0) --top;
+            const int e = head[top];
+            head[top] = en[e];
+            const int v = ev[e];
+            if (cv[v] >= 0 || key(v) != top) continue;
+            const int k = take(v);
+            ++done;
+            for (int q = aoff[v]; q < aoff[v + 1]; ++q) {
+                const int u = adj[q];
+                if (cv[u] >= 0 || (used[u] >> k & 1ull)) continue;
+                used[u] |= 1ull << k;
+                ++sat[u];
+                push(u);
+            }
+        }
+    }
     if (ncol > kMaxColours) throw InvalidArg("too many big-block colours");
-    std::vector<int> cnt(ncol + 1, 0), ids(nbig);
-    for (int k : col)
-        if (k >= 0) ++cnt[k + 1];
+    // list order: by colour, ascending block id within a colour
+    std::vector<int> cnt(ncol + 1, 0), ids(nbig), lpos(nbig);
+    for (int v = 0; v < nbig; ++v) ++cnt[cv[v] + 1];
     for (int k = 0; k < ncol; ++k) cnt[k + 1] += cnt[k];
     std::vector<int> pos(cnt.begin(), cnt.end() - 1);
-    for (int q = 0; q < nbk * nbk; ++q)
-        if (col[q] >= 0) ids[pos[col[q]]++] = q;
+    for (int v = 0; v < nbig; ++v) {
+        lpos[v] = pos[cv[v]]++;
+        ids[lpos[v]] = vid[v];
+    }
     lb.ncol = ncol;
     lb.nbig = nbig;
     std::fill(lb.coff, lb.coff + kMaxColours + 1, nbig);
@@ -368,27 +439,17 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const uint8_t* big) {
         lb.blk_cap = grow_cap(nbig, lb.blk_cap);
         lb.blk_ids = dalloc<int>(size_t(lb.blk_cap));
     }
-    if (nbig) CK(cudaMemcpyAsync(lb.blk_ids, ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, c->s));
-    // dependency lists for the barrier-free big phase: the predecessors of a
-    // block are the big blocks within Chebyshev block distance 2 (periodic)
-    // with a smaller colour (list positions); same-colour blocks never conflict
-    std::vector<int> pos_of(size_t(nbk) * nbk, -1);
-    for (int q = 0; q < nbig; ++q) pos_of[ids[q]] = q;
+    // predecessor CSR over list positions, ascending
+    std::vector<int> vof(nbig);
+    for (int v = 0; v < nbig; ++v) vof[lpos[v]] = v;
     std::vector<int> poff(nbig + 1, 0), pred;
-    pred.reserve(size_t(nbig) * 12);
+    pred.reserve(adj.size() / 2 + 1);
     for (int q = 0; q < nbig; ++q) {
-        const int B = ids[q], bx = B % nbk, by = B / nbk, cq = col[B];
-        for (int dy = -2; dy <= 2; ++dy)
-            for (int dx = -2; dx <= 2; ++dx) {
-                const int B2 = wr(bx + dx, nbk) + wr(by + dy, nbk) * nbk;
-                if (B2 != B && col[B2] >= 0 && col[B2] < cq) {
-                    // distinct offsets may alias on tiny periodic levels: keep each predecessor once
-                    const int p = pos_of[B2];
-                    bool dup = false;
-                    for (int k = poff[q]; k < int(pred.size()); ++k) dup |= pred[k] == p;
-                    if (!dup) pred.push_back(p);
-                }
-            }
+        const int v = vof[q];
+        const size_t first = pred.size();
+        for (int e = aoff[v]; e < aoff[v + 1]; ++e)
+            if (cv[adj[e]] < cv[v]) pred.push_back(lpos[adj[e]]);
+        std::sort(pred.begin() + first, pred.end());
         poff[q + 1] = int(pred.size());
     }
     if (lb.pred_cap < long(pred.size()) + 1 || lb.poff_cap < nbig + 1) {
@@ -403,11 +464,15 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const uint8_t* big) {
         CK(cudaMemset(lb.flags, 0, sizeof(unsigned) * lb.poff_cap));
         lb.epoch = 0;
     }
-    if (!pred.empty())
-        CK(cudaMemcpyAsync(lb.pred, pred.data(), sizeof(int) * pred.size(), cudaMemcpyHostToDevice, c->s));
-    CK(cudaMemcpyAsync(lb.poff, poff.data(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice, c->s));
-    // the host vectors die here: the async copies must complete first
-    CK(cudaStreamSynchronize(c->s));
+    // the host copies stay alive in the level until the next rebuild (which
+    // starts after rebuild()'s final synchronisation), so no sync here
+    lb.h_ids = std::move(ids);
+    lb.h_pred = std::move(pred);
+    lb.h_poff = std::move(poff);
+    if (nbig) CK(cudaMemcpyAsync(lb.blk_ids, lb.h_ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, c->s));
+    if (!lb.h_pred.empty())
+        CK(cudaMemcpyAsync(lb.pred, lb.h_pred.data(), sizeof(int) * lb.h_pred.size(), cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(lb.poff, lb.h_poff.data(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice, c->s));
 }
 
 void check_err_flag(ibmg_ctx* c, const char* where) {
@@ -429,8 +494,20 @@ void erows(ibmg_ctx* c, LevelBuf& lb, int pass) {
 
 // Rebuild every per-level structure datum from the device positions c->X
 // (the lagged operators of one step).
+// IBMG_SETUP_TRACE=1: host wall-clock marks through rebuild() on stderr
+struct SetupTrace {
+    bool on = std::getenv("IBMG_SETUP_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) const {
+        if (on)
+            std::fprintf(stderr, "[setup] %-28s %8.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 void rebuild(ibmg_ctx* c) {
     const int npts = c->npts;
+    const SetupTrace tr;
     CK(cudaMemsetAsync(c->err_flag, 0, sizeof(int), c->s));
     CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * kCtr, c->s));
     if (npts == 0) {
@@ -479,18 +556,22 @@ void rebuild(ibmg_ctx* c) {
             const int nbk = lb.L.n / 4;
             CK(cudaMemsetAsync(lb.big, 0, size_t(nbk) * nbk, c->s));
             LAUNCH(c, k_mark_big, nblk(size_t(npts) * 64), 256, 0, npts, lb.W, lb.L.n, lb.big);
-            LAUNCH(c, k_reach, nblk(npts, 128), 128, 0, npts, lb.W, c->P, c->counters + l * kCtr + 18);
+            CK(cudaMemsetAsync(lb.cmask, 0, sizeof(unsigned) * nbk * nbk, c->s));
+            LAUNCH(c, k_block_pairs, nblk(size_t(npts) * 2, 128), 128, 0, npts, lb.W, c->P, lb.L.n, lb.cmask,
+                   c->counters + l * kCtr + 18);
+            LAUNCH(c, k_block_conflicts, nblk(size_t(nbk) * nbk), 256, 0, lb.L.n, lb.big, lb.cmask);
         }
         std::vector<int> hc(size_t(c->nlev) * kCtr);
         CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
-        // big-block flags of every level in the same round trip (for the host colouring)
-        std::vector<std::vector<uint8_t>> bigh(c->nlev);
+        // conflict masks (big flag in bit 12) of every level in the same round trip
         for (int l = 0; l + 1 < c->nlev; ++l) {
             const int nbk = c->lev[l].L.n / 4;
-            bigh[l].resize(size_t(nbk) * nbk);
-            CK(cudaMemcpyAsync(bigh[l].data(), c->lev[l].big, bigh[l].size(), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaMemcpyAsync(c->lev[l].h_cm, c->lev[l].cmask, sizeof(unsigned) * nbk * nbk, cudaMemcpyDeviceToHost,
+                               c->s));
         }
+        tr.mark("launched marks");
         CK(cudaStreamSynchronize(c->s));
+        tr.mark("synced marks");
         for (int l = 0; l < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
             const int* h = &hc[size_t(l) * kCtr];
@@ -503,9 +584,11 @@ void rebuild(ibmg_ctx* c) {
                 if (reach > 7)
                     throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 8-cell same-colour gap on level " +
                                      std::to_string(l) + " (Lagrangian spacing too large)");
-                colour_big_blocks(c, lb, bigh[l].data());
+                colour_big_blocks(c, lb, lb.h_cm);
+                tr.mark(("coloured level " + std::to_string(l) + " nbig " + std::to_string(lb.nbig)).c_str());
             }
         }
+        tr.mark("coloured");
         // assembled E'_l rows on the E-active faces (count, scan, fill)
         for (int l = 0; l < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
@@ -523,7 +606,9 @@ void rebuild(ibmg_ctx* c) {
                 if (c->lev[l].FL.nf)
                     CK(cudaMemcpyAsync(&nnz[l], c->lev[l].E.rp + c->lev[l].FL.nf, sizeof(int), cudaMemcpyDeviceToHost,
                                        c->s));
+            tr.mark("launched erows count");
             CK(cudaStreamSynchronize(c->s));
+            tr.mark("synced nnz");
             for (int l = 0; l < c->nlev; ++l) {
                 LevelBuf& lb = c->lev[l];
                 if (lb.FL.nf == 0) continue;
@@ -590,7 +675,9 @@ void rebuild(ibmg_ctx* c) {
         {
             std::vector<int> hc(size_t(c->nlev) * kCtr);
             CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
+            tr.mark("launched inverses");
             CK(cudaStreamSynchronize(c->s));
+            tr.mark("synced slab sizes");
             for (int l = 0; l + 1 < c->nlev; ++l) {
                 LevelBuf& lb = c->lev[l];
                 if (lb.nbig == 0) continue;
@@ -616,7 +703,9 @@ void rebuild(ibmg_ctx* c) {
         LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
                c->err_flag);
     }
+    tr.mark("launched slabs");
     check_err_flag(c, "rebuild");
+    tr.mark("done");
 }
 
 void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, const double* ds, const double* X,
@@ -1052,6 +1141,8 @@ void ibmg_destroy(ibmg_ctx* c) {
         dfree(lb.b);
         dfree(lb.r);
         dfree(lb.big);
+        dfree(lb.cmask);
+        if (lb.h_cm) cudaFreeHost(lb.h_cm);
         dfree(lb.bq);
         dfree(lb.tflags);
     }
