@@ -114,17 +114,6 @@ __device__ __forceinline__ double win_dot_R(const Win& W, int k, int comp, int n
     return s;
 }
 
-// F_k = cE_k (U_{k-1} - 2 U_k + U_{k+1}) for one component (elasticity.cpp:62-84
-// coefficients {1, -2, 1}/ds^2 times ds^2 h^2 dt kappa).
-template <class Acc>
-__device__ __forceinline__ double point_force(const Win& W, const Pts& P, int k, int comp, int n,
-                                              const Acc& acc) {
-    const double um = win_dot_R(W, P.kprev[k], comp, n, acc);
-    const double uc = win_dot_R(W, k, comp, n, acc);
-    const double up = win_dot_R(W, P.knext[k], comp, n, acc);
-    return P.cE[k] * (um - 2.0 * uc + up);
-}
-
 // Global-memory field accessor: comp 0 u, 1 v, 2 p.
 struct GAcc {
     const double* w;

@@ -34,9 +34,49 @@ __device__ __forceinline__ double stokes_row(const Lev& L, const Acc& w, int f, 
     return -L.g * (w(0, ip, j) - w(0, i, j)) - L.g * (w(1, i, jp) - w(1, i, j));
 }
 
+// Point-force CTAs of a grid launch: the first `nblk` CTAs of
+// K1/K2 compute F_k = cE_k (U_{k-1} - 2 U_k + U_{k+1}), U_k = R_k . w
+// (elasticity.cpp:62-84 in window form), one warp per point: lane
+// comp * 16 + tap loads one window weight and one field value for each of
+// k-1, k, k+1, then fixed xor-tree sums over the 16 taps (deterministic).
+// The face gather that follows adds L_k F_k.  nblk = 0: no point CTAs.
+struct PForce {
+    Win W;
+    Pts P;
+    int n;
+    const double* w;
+    double* F;
+    int nblk;
+};
+constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point
+
+__device__ __forceinline__ void point_force_warp(const PForce& pf) {
+    const int k = blockIdx.x * kPfPerCta + (threadIdx.x >> 5);
+    if (k >= pf.P.n) return;
+    const int lane = threadIdx.x & 31, comp = lane >> 4, e = lane & 15;
+    const int n = pf.n;
+    const double* wc = pf.w + (size_t)comp * n * n;
+    const int ks[3] = {pf.P.kprev[k], k, pf.P.knext[k]};
+    double u[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const int kk = ks[t];
+        const int4 o = pf.W.orgR[kk];
+        const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+        u[t] = pf.W.w[(size_t)kk * 64 + (2 + comp) * 16 + e] *
+               __ldg(wc + wr(i0 + (e & 3), n) + (size_t)wr(j0 + (e >> 2), n) * n);
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) u[t] += __shfl_xor_sync(0xffffffffu, u[t], o);
+    if (e == 0) pf.F[2 * k + comp] = pf.P.cE[k] * (u[0] - 2.0 * u[1] + u[2]);
+}
+
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
-__global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out, PForce pf) {
+    if ((int)blockIdx.x < pf.nblk) return point_force_warp(pf);
+    const int q = (blockIdx.x - pf.nblk) * blockDim.x + threadIdx.x;
     if (q >= L.nn) return;
     const int i = q & (L.n - 1), j = q >> L.lg;
     GAcc acc{w, L.n, L.nn};
@@ -49,8 +89,9 @@ __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __re
 
 // r = b - S w (E' part added by k_face_gather with sign +1).
 __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const double* __restrict__ w,
-                                  double* __restrict__ r) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+                                  double* __restrict__ r, PForce pf) {
+    if ((int)blockIdx.x < pf.nblk) return point_force_warp(pf);
+    const int q = (blockIdx.x - pf.nblk) * blockDim.x + threadIdx.x;
     if (q >= L.nn) return;
     const int i = q & (L.n - 1), j = q >> L.lg;
     GAcc acc{w, L.n, L.nn};
@@ -66,9 +107,10 @@ __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const dou
 // restricted residual, R E' w = sum_k L^{l+1}_k F_k, is added afterwards by
 // k_face_gather on the coarse face list.
 __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
-                                    double* __restrict__ bc) {
+                                    double* __restrict__ bc, PForce pf) {
+    if ((int)blockIdx.x < pf.nblk) return point_force_warp(pf);
     const int nc = F.n >> 1, nnc = nc * nc;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = (blockIdx.x - pf.nblk) * blockDim.x + threadIdx.x;
     if (q >= nnc) return;
     const int I = q % nc, J = q / nc;
     const int i = 2 * I, j = 2 * J, n = F.n, nn = F.nn;

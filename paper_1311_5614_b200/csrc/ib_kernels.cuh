@@ -265,15 +265,6 @@ __global__ void k_block_conflicts(int n, const uint8_t* __restrict__ big, unsign
     mask[A] = m;
 }
 
-// F_k for both components from field w on a level (thread per point).
-__global__ void k_point_force(Win W, Pts P, int n, const double* __restrict__ w, double* __restrict__ F) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= P.n) return;
-    GAcc acc{w, n, n * n};
-    F[2 * k] = point_force(W, P, k, 0, n, acc);
-    F[2 * k + 1] = point_force(W, P, k, 1, n, acc);
-}
-
 // out[face] += sign * sum_{(k, l) in list(face)} l * F[k][comp]: one warp per
 // face (lists run to hundreds of entries on coarse levels), lanes strided over
 // the entries, fixed butterfly reduction (deterministic spread: no atomics).

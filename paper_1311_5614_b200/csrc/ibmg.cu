@@ -789,23 +789,29 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
 
 // ---------------- operators ----------------
 
+// Point-force CTAs for a grid launch on level l's windows against field w;
+// none when the level has no E'-active faces.
+PForce pforce(ibmg_ctx* c, const LevelBuf& lb, const double* w, bool active) {
+    PForce pf{lb.W, c->P, lb.L.n, w, c->F, 0};
+    if (c->npts && active) pf.nblk = int(nblk(c->npts, kPfPerCta));
+    return pf;
+}
+
 // out = A_l w on level l (stencil + E' via point forces and the level face list).
 void apply_level(ibmg_ctx* c, int l, const double* w, double* out) {
     LevelBuf& lb = c->lev[l];
-    LAUNCH(c, k_stokes_apply, nblk(lb.L.nn), 256, 0, lb.L, w, out);
-    if (c->npts && lb.FL.nf) {
-        LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, w, c->F);
+    const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
+    LAUNCH(c, k_stokes_apply, pf.nblk + nblk(lb.L.nn), 256, 0, lb.L, w, out, pf);
+    if (pf.nblk)
         LAUNCH(c, k_face_gather, nblk(size_t(lb.FL.nf) * 32), 256, 0, lb.FL, lb.W, c->F, out, lb.L.nn, -1.0);
-    }
 }
 
 void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double* r) {
     LevelBuf& lb = c->lev[l];
-    LAUNCH(c, k_stokes_residual, nblk(lb.L.nn), 256, 0, lb.L, b, w, r);
-    if (c->npts && lb.FL.nf) {
-        LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, w, c->F);
+    const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
+    LAUNCH(c, k_stokes_residual, pf.nblk + nblk(lb.L.nn), 256, 0, lb.L, b, w, r, pf);
+    if (pf.nblk)
         LAUNCH(c, k_face_gather, nblk(size_t(lb.FL.nf) * 32), 256, 0, lb.FL, lb.W, c->F, r, lb.L.nn, 1.0);
-    }
 }
 
 Slabs slabs(const LevelBuf& lb) { return Slabs{lb.Ainv, lb.sl_rp, lb.sl_off, lb.sl_col, lb.sl_val}; }
@@ -901,11 +907,10 @@ void vcycle(ibmg_ctx* c, const double* b, double* z) {
             LevelBuf& nx = c->lev[l + 1];
             CK(cudaMemsetAsync(lb.w, 0, sizeof(double) * 3 * lb.L.nn, c->s));
             for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, lb.b, lb.w);
-            LAUNCH(c, k_residual_restrict, nblk(nx.L.nn), 256, 0, lb.L, lb.b, lb.w, nx.b);
-            if (c->npts && nx.FL.nf) {
-                LAUNCH(c, k_point_force, nblk(c->npts, 128), 128, 0, lb.W, c->P, lb.L.n, lb.w, c->F);
+            const PForce pf = pforce(c, lb, lb.w, nx.FL.nf > 0);
+            LAUNCH(c, k_residual_restrict, pf.nblk + nblk(nx.L.nn), 256, 0, lb.L, lb.b, lb.w, nx.b, pf);
+            if (pf.nblk)
                 LAUNCH(c, k_face_gather, nblk(size_t(nx.FL.nf) * 32), 256, 0, nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0);
-            }
         }
         coarse_cycle(c, c->lev[c->lc].b, c->lev[c->lc].w);
         for (int l = c->lc - 1; l >= 0; --l) {
