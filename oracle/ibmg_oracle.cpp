@@ -536,14 +536,16 @@ std::vector<int> colour_blocks(const std::vector<char>& big, const std::vector<u
 }
 
 // Fixed multicolour schedule.  Plain phase: 16x16-cell
-// tiles coloured 2x2 (one tile, periodic, when n <= 16); inside each tile the
+// tiles coloured 2x2 (one tile, periodic, when n <= 32); inside each tile the
 // 8 conflict-free colours (i + 2j) mod 8 of local coordinates over cells
 // outside big blocks.  Big phase: the greedy colour classes of the big blocks
 // in colour order.  Boxes within one pass are mutually independent, so each
 // pass is exactly a Gauss-Seidel pass in any order (SPEC.md:427-431
 // semantics) and the GPU runs it in parallel.
 void build_schedule(Level& L, const std::vector<int>& kprev, const std::vector<int>& knext) {
-    const int n = L.n, T = std::min(16, n), nt = n / T, nbk = n / 4;
+    // levels n <= 32 (one CTA on the GPU) colour the whole periodic level
+    // (i + 2j) mod 8 — valid across the seam since 8 | n — instead of tiling
+    const int n = L.n, T = n <= 32 ? n : 16, nt = n / T, nbk = n / 4;
     L.passes.clear();
     const int ntc = nt >= 2 ? 4 : 1;
     for (int tc = 0; tc < ntc; ++tc) {

@@ -53,26 +53,16 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
     const int n = L.n, t = threadIdx.x, nt = blockDim.x, nbk = n >> 2;
     SW W{w, n, L.nn};
     SW B{const_cast<double*>(b), n, L.nn};
-    // plain phase: 16x16 tiles in 2x2 tile colours (n = 32) or one periodic tile
-    const int T = n < kTile ? n : kTile, ntile = n / T, ntc = ntile >= 2 ? 4 : 1;
-    const int per = T * T / 8;
-    for (int tc = 0; tc < ntc; ++tc)
-        for (int pc = 0; pc < 8; ++pc) {
-            for (int idx = t; idx < per; idx += nt) {  // one tile per colour at n <= 32
-                const int tx = ntc == 4 ? (tc & 1) : 0, ty = ntc == 4 ? (tc >> 1) : 0;
-                int li, lj;
-                if (T == 16) {
-                    lj = idx >> 1;
-                    li = ((pc - 2 * lj) & 7) + 8 * (idx & 1);
-                } else {  // T == 8
-                    lj = idx;
-                    li = (pc - 2 * lj) & 7;
-                }
-                const int i = tx * T + li, j = ty * T + lj;
-                if (!C.big[(i >> 2) + (j >> 2) * nbk]) plain_cell(L, W, B, i, j);
-            }
-            __syncthreads();
+    // plain phase: the whole periodic level in the 8 colours (i + 2j) mod 8
+    // (oracle build_schedule: one tile when n <= 32), n^2/8 cells per pass
+    const int per = L.nn >> 3, row = n >> 3;
+    for (int pc = 0; pc < 8; ++pc) {
+        for (int idx = t; idx < per; idx += nt) {
+            const int j = idx / row, i = ((pc - 2 * j) & 7) + 8 * (idx % row);
+            if (!C.big[(i >> 2) + (j >> 2) * nbk]) plain_cell(L, W, B, i, j);
         }
+        __syncthreads();
+    }
     cmark(tr, nm);  // plain phase done
     // big phase: colour classes in order; the blocks of a class (independent)
     // are shared by 4 groups of 128 threads, each with its own E'-row slot.  A

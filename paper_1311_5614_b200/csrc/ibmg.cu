@@ -1376,7 +1376,7 @@ long ibmg_debug_sweep_trace(ibmg_ctx* c, int level, const double* b, double* w, 
         CK(cudaSetDevice(c->prm.device));
         LevelBuf& lb = c->lev[level];
         const int nt = lb.L.n / kTile;
-        const long words = 4L * nt * nt + 9L * lb.nbig;
+        const long words = 6L * nt * nt + 9L * lb.nbig;
         if (!out) return words;
         unsigned long long* d = dalloc<unsigned long long>(size_t(words));
         CK(cudaMemset(d, 0, sizeof(unsigned long long) * words));

@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
         cp_async_wait<0>();
         __syncwarp();
+        const unsigned long long t_s = A.trace ? gtimer() : 0;
         TileW W{sw};
         TileB B{sb};
         for (int pc = 0; pc < 8; ++pc) {
@@ -564,6 +565,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
             if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
             __syncwarp();
         }
+        const unsigned long long t_p = A.trace ? gtimer() : 0;
         for (int qq = lane; qq < 17 * 17; qq += 32) {
             const int a = qq % 17, bb = qq / 17;
             const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
@@ -575,11 +577,13 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         if (lane == 0) {  // warp-synchronous stores + st.release.gpu (cumulative) publish the tile
             st_release(A.tflags + tx + ty * nt, epoch);
             if (A.trace) {
-                unsigned long long* r = A.trace + 4 * task;
+                unsigned long long* r = A.trace + 6 * task;
                 r[0] = t_a;
                 r[1] = t_b;
                 r[2] = gtimer();
                 r[3] = blockIdx.x;
+                r[4] = t_s;
+                r[5] = t_p;
             }
         }
     }
@@ -609,7 +613,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         cp_async_wait<1>();
         __syncthreads();
         const unsigned long long t_c = A.trace ? gtimer() : 0;
-        unsigned long long* dbgp = A.trace ? A.trace + 4 * ntiles + 9 * q + 6 : nullptr;
+        unsigned long long* dbgp = A.trace ? A.trace + 6 * ntiles + 9 * q + 6 : nullptr;
         big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg,
                        [&](int f, int i, int j, double old, double d) {
                            __stcg(A.w + (size_t)f * nn + i + (size_t)j * n, old + d);
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(A.DP.flags + q, epoch);
             if (A.trace) {
-                unsigned long long* r = A.trace + 4 * ntiles + 9 * q;
+                unsigned long long* r = A.trace + 6 * ntiles + 9 * q;
                 r[0] = t_a;
                 r[1] = t_b;
                 r[2] = t_c;

@@ -15,7 +15,7 @@ g = SaddleSystem.from_problem(prob)
 L = g._L
 b = torch.tensor(g.build_rhs(np.zeros(2 * 256 * 256)), device="cuda")
 w = torch.zeros_like(b)
-for level in (0, 1):
+for level in (0, 1, 2):
     n = g.level_n(level)
     nb = 3 * n * n
     bl, wl = b[:nb].clone(), w[:nb].clone()
@@ -24,12 +24,21 @@ for level in (0, 1):
     for rep in range(3):  # warm, then measure
         L.ibmg_debug_sweep_trace(g._h, level, bl.data_ptr(), wl.data_ptr(), out.ctypes.data, words)
     nt = (n // 16) ** 2
-    tiles = out[: 4 * nt].reshape(-1, 4).astype(np.int64)
-    bigs = out[4 * nt:].reshape(-1, 9).astype(np.int64)
+    tiles = out[: 6 * nt].reshape(-1, 6).astype(np.int64)
+    bigs = out[6 * nt:].reshape(-1, 9).astype(np.int64)
     t0 = min(tiles[:, 0].min(), bigs[:, 0].min() if len(bigs) else 1 << 62)
     print(f"level {level} n={n}: tiles={nt} big={len(bigs)}")
     print("  tile wait / work (us): mean %.2f / %.2f, last tile done at %.2f" % (
         np.mean(tiles[:, 1] - tiles[:, 0]) / 1e3, np.mean(tiles[:, 2] - tiles[:, 1]) / 1e3, (tiles[:, 2].max() - t0) / 1e3))
+    print("  tile task phases (us): stage %.2f | 8 passes %.2f | write+publish %.2f" % (
+        np.mean(tiles[:, 4] - tiles[:, 1]) / 1e3, np.mean(tiles[:, 5] - tiles[:, 4]) / 1e3,
+        np.mean(tiles[:, 2] - tiles[:, 5]) / 1e3))
+    per = nt // 4
+    for tc in range(4):
+        m = slice(tc * per, (tc + 1) * per)
+        print("    tile colour %d: start %.2f, deps met %.2f, done %.2f us (work mean %.2f)" % (
+            tc, (tiles[m, 0].min() - t0) / 1e3, (tiles[m, 1].max() - t0) / 1e3, (tiles[m, 2].max() - t0) / 1e3,
+            np.mean(tiles[m, 2] - tiles[m, 1]) / 1e3))
     if len(bigs):
         print("  big wait-deps / wait-slab / solve (us): mean %.2f / %.2f / %.2f; end at %.2f" % (
             np.mean(bigs[:, 1] - bigs[:, 0]) / 1e3, np.mean(bigs[:, 2] - bigs[:, 1]) / 1e3,
