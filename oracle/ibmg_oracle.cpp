@@ -790,13 +790,16 @@ void vcycle_rec(Ctx& C, int l) {
     for (int s = 0; s < C.prm.nu2; ++s) sweep(L, L.b.data(), L.w.data());
 }
 
-void vcycle(Ctx& C, const double* b, double* z) {
+// project = false inside FGMRES: a constant pressure is in the null space of
+// the periodic operator (G 1 = 0; E' and the mass term act on velocity), so
+// A z does not see z's pressure mean and the solution's mean is removed once
+// at the end.  The stand-alone V-cycle projects.
+void vcycle(Ctx& C, const double* b, double* z, bool project = true) {
     Level& L = C.lev[0];
     std::copy(b, b + L.b.size(), L.b.begin());
     vcycle_rec(C, 0);
-    // mean removal hoisted to the returned fine state
     std::copy(L.w.begin(), L.w.end(), z);
-    project_pressure_mean(z, L.n);
+    if (project) project_pressure_mean(z, L.n);
 }
 
 double dotv(const std::vector<double>& a, const std::vector<double>& b) {  // fields.cpp:87-92
@@ -835,7 +838,7 @@ int fgmres(Ctx& C, const double* bptr, double* xptr, orc_stats* st, double* hist
         g[0] = beta;
         int j = 0, kdim = 0;
         for (; j < m; ++j) {
-            vcycle(C, V[j].data(), Z[j].data());
+            vcycle(C, V[j].data(), Z[j].data(), false);
             apply_level(L, Z[j].data(), w.data());
             for (int pass = 0; pass < 2; ++pass) {
                 for (int i = 0; i <= j; ++i) h1[i] = dotv(V[i], w);

@@ -252,7 +252,8 @@ constexpr int kCgsBlocks = 592;  // 4 per SM; fixed => reduction order fixed
 template <int MODE, int KMAX>
 __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 ? 2 : 1))
     k_cgs_sweep(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
-                double* __restrict__ w, size_t m, double* __restrict__ partial) {
+                double* __restrict__ w, size_t m, double* __restrict__ partial, double* __restrict__ out,
+                unsigned* __restrict__ ticket) {
     constexpr int NACC = MODE == 2 ? 1 : KMAX;
     __shared__ double hs[KMAX];
     __shared__ double red[kRedThreads / 32][NACC];
@@ -301,6 +302,22 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
         for (int ww = 0; ww < kRedThreads / 32; ++ww) t += red[ww][i];
         partial[(size_t)i * gridDim.x + blockIdx.x] = t;
     }
+    // the last CTA to finish sums the partials in the fixed k_finish_dots
+    // order (lane-strided, then a warp butterfly), one warp per dot
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = wid; i < kk; i += kRedThreads / 32) {
+        double t = 0.0;
+        for (int x = lane; x < (int)gridDim.x; x += 32) t += __ldcg(partial + (size_t)i * gridDim.x + x);
+        t = warp_sum(t);
+        if (lane == 0) out[i] = t;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // w -= sum_{i<k} h[i] V_i   (one pass over w and the V's).

@@ -138,6 +138,7 @@ struct ibmg_ctx {
     // Krylov
     double *V = nullptr, *Z = nullptr, *wv = nullptr, *xv = nullptr, *rv = nullptr, *bv = nullptr;
     double *partial = nullptr, *dh = nullptr, *ones = nullptr, *stage_a = nullptr, *stage_b = nullptr;
+    unsigned* ticket = nullptr;  // last-CTA ticket of the fused CGS sweeps
     double* hpin = nullptr;    // pinned host mirror of dh
     size_t M = 0;              // 3 N^2
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
@@ -270,6 +271,8 @@ void alloc_levels(ibmg_ctx* c) {
     c->stage_a = dalloc<double>(c->M);
     c->stage_b = dalloc<double>(c->M);
     c->partial = dalloc<double>(size_t(std::max(kRedBlocks, kCgsBlocks)) * (m + 2));
+    c->ticket = dalloc<unsigned>(1);
+    CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     c->dh = dalloc<double>(2 * (m + 2) + 8);
     CK(cudaMallocHost(&c->hpin, sizeof(double) * (2 * (m + 2) + 8)));
     c->ones = dalloc<double>(size_t(p.N) * p.N);
@@ -897,31 +900,36 @@ void pressure_mean_zero(ibmg_ctx* c, double* x) {
 }
 
 // z = V(nu1,nu2)(0, b): Algorithm 1 from a zero guess.
-void vcycle(ibmg_ctx* c, const double* b, double* z) {
+// Level 0 reads b and works in z directly.  project = false inside FGMRES: a
+// constant pressure is in the null space of the periodic operator, so the
+// mean is removed once from the solution instead (oracle
+// vcycle).
+void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true) {
     if (c->lc == 0) {
         coarse_cycle(c, b, z);
     } else {
-        CK(cudaMemcpyAsync(c->lev[0].b, b, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
+        const bool alias = b == z;
+        if (alias) CK(cudaMemcpyAsync(c->lev[0].b, b, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
+        auto bl = [&](int l) -> const double* { return l == 0 && !alias ? b : c->lev[l].b; };
+        auto wl = [&](int l) -> double* { return l == 0 ? z : c->lev[l].w; };
         for (int l = 0; l < c->lc; ++l) {
             LevelBuf& lb = c->lev[l];
             LevelBuf& nx = c->lev[l + 1];
-            CK(cudaMemsetAsync(lb.w, 0, sizeof(double) * 3 * lb.L.nn, c->s));
-            for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, lb.b, lb.w);
-            const PForce pf = pforce(c, lb, lb.w, nx.FL.nf > 0);
-            LAUNCH(c, k_residual_restrict, pf.nblk + nblk(nx.L.nn), 256, 0, lb.L, lb.b, lb.w, nx.b, pf);
+            CK(cudaMemsetAsync(wl(l), 0, sizeof(double) * 3 * lb.L.nn, c->s));
+            for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
+            const PForce pf = pforce(c, lb, wl(l), nx.FL.nf > 0);
+            LAUNCH(c, k_residual_restrict, pf.nblk + nblk(nx.L.nn), 256, 0, lb.L, bl(l), wl(l), nx.b, pf);
             if (pf.nblk)
                 LAUNCH(c, k_face_gather, nblk(size_t(nx.FL.nf) * 32), 256, 0, nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0);
         }
-        coarse_cycle(c, c->lev[c->lc].b, c->lev[c->lc].w);
+        coarse_cycle(c, c->lev[c->lc].b, wl(c->lc));
         for (int l = c->lc - 1; l >= 0; --l) {
             LevelBuf& lb = c->lev[l];
-            LAUNCH(c, k_prolong_add, nblk(lb.L.nn), 256, 0, lb.L.n, c->lev[l + 1].w, lb.w);
-            for (int s = 0; s < c->prm.nu2; ++s) sweep_level(c, l, lb.b, lb.w);
+            LAUNCH(c, k_prolong_add, nblk(lb.L.nn), 256, 0, lb.L.n, wl(l + 1), wl(l));
+            for (int s = 0; s < c->prm.nu2; ++s) sweep_level(c, l, bl(l), wl(l));
         }
-        CK(cudaMemcpyAsync(z, c->lev[0].w, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
     }
-    // mean removal hoisted to the returned fine state
-    pressure_mean_zero(c, z);
+    if (project) pressure_mean_zero(c, z);
 }
 
 // dots[0..k) = V_i . w, written to c->dh + off (accumulate when acc)
@@ -931,12 +939,12 @@ void multidot(ibmg_ctx* c, const double* V, int k, const double* w, int off, int
     LAUNCH(c, k_finish_dots, k, 32, 0, c->partial, kRedBlocks, c->dh + off, acc);
 }
 
-// One fused CGS2 sweep over V_0..V_{k-1} (k_cgs_sweep) + the fixed-order finish
-// of its per-block partials into c->dh + off.
+// One fused CGS2 sweep over V_0..V_{k-1} (k_cgs_sweep); its last CTA finishes
+// the per-block partials into c->dh + off in a fixed order.
 template <int MODE, int KMAX>
 void cgs_launch(ibmg_ctx* c, int k, const double* h, double* w, int off) {
-    LAUNCH(c, (k_cgs_sweep<MODE, KMAX>), kCgsBlocks, kRedThreads, 0, c->V, c->Mst, k, h, w, c->M, c->partial);
-    LAUNCH(c, k_finish_dots, MODE == 2 ? 1 : k, 32, 0, c->partial, kCgsBlocks, c->dh + off, 0);
+    LAUNCH(c, (k_cgs_sweep<MODE, KMAX>), kCgsBlocks, kRedThreads, 0, c->V, c->Mst, k, h, w, c->M, c->partial,
+           c->dh + off, c->ticket);
 }
 template <int MODE>
 void cgs_mode(ibmg_ctx* c, int k, const double* h, double* w, int off) {
@@ -987,7 +995,7 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
         for (int j = 0; j < m; ++j) {
             double* Vj = c->V + c->Mst * j;
             double* Zj = c->Z + c->Mst * j;
-            vcycle(c, Vj, Zj);
+            vcycle(c, Vj, Zj, false);
             apply_level(c, 0, Zj, c->wv);
             // CGS2 in three fused sweeps: h1 = V^T w | w -= V h1, h2 = V^T w | w -= V h2, ||w||^2
             cgs_sweep(c, 0, j + 1, nullptr, c->wv, hoff);
@@ -1160,6 +1168,7 @@ void ibmg_destroy(ibmg_ctx* c) {
     dfree(c->stage_a);
     dfree(c->stage_b);
     dfree(c->partial);
+    dfree(c->ticket);
     dfree(c->dh);
     dfree(c->ones);
     dfree(c->err_flag);
