@@ -123,4 +123,23 @@ struct GAcc {
     }
 };
 
+// out[face q] += sign * sum_{(k, l) in list(q)} l * F[k][comp]: one warp per
+// face (lists run to hundreds of entries on coarse levels), lanes strided over
+// the entries, fixed butterfly reduction (deterministic spread: no atomics).
+__device__ __forceinline__ void face_gather_warp(const FaceList& FL, const Win& W, const double* __restrict__ F,
+                                                 double* __restrict__ out, int nn, double sign, int q, int lane) {
+    if (q >= FL.nf) return;
+    const int face = FL.face[q];
+    const int comp = face >= nn;
+    double s = 0.0;
+    for (int e = FL.off[q] + lane; e < FL.off[q + 1]; e += 32) {
+        const int v = FL.ent[e];
+        const int k = v >> 5;
+        s += W.w[(size_t)k * 64 + (v & 31)] * F[2 * k + comp];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[face] += sign * s;
+}
+
 }  // namespace ibmg

@@ -34,12 +34,17 @@ __device__ __forceinline__ double stokes_row(const Lev& L, const Acc& w, int f, 
     return -L.g * (w(0, ip, j) - w(0, i, j)) - L.g * (w(1, i, jp) - w(1, i, j));
 }
 
-// Point-force CTAs of a grid launch: the first `nblk` CTAs of
-// K1/K2 compute F_k = cE_k (U_{k-1} - 2 U_k + U_{k+1}), U_k = R_k . w
-// (elasticity.cpp:62-84 in window form), one warp per point: lane
-// comp * 16 + tap loads one window weight and one field value for each of
-// k-1, k, k+1, then fixed xor-tree sums over the 16 taps (deterministic).
-// The face gather that follows adds L_k F_k.  nblk = 0: no point CTAs.
+// Point-force + face-gather CTAs of a grid launch.  A launch
+// of K1/K2 is [pf.nblk point CTAs | grid CTAs | G.nblk gather CTAs]:
+//  * point CTAs compute F_k = cE_k (U_{k-1} - 2 U_k + U_{k+1}), U_k = R_k . w
+//    (elasticity.cpp:62-84 in window form), one warp per point: lane
+//    comp * 16 + tap loads one window weight and one field value for each of
+//    k-1, k, k+1, then fixed xor-tree sums over the 16 taps (deterministic);
+//  * grid CTAs write the stencil part of the output;
+//  * gather CTAs wait until every earlier CTA of the launch has signalled a
+//    monotone counter (CTAs are dispatched in index order, so waiting only on
+//    lower indices always makes progress) and add sign * L_k F_k per face.
+// nblk = 0: no point / gather CTAs.
 struct PForce {
     Win W;
     Pts P;
@@ -48,10 +53,21 @@ struct PForce {
     double* F;
     int nblk;
 };
-constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point
+struct Gather {
+    FaceList FL;
+    Win W;
+    const double* F;
+    double* out;
+    int nn;
+    double sign;
+    int nblk;
+    unsigned long long* cnt;    // monotone per-context counter
+    unsigned long long target;  // its value once this launch's producers are done
+};
+constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point / per face
 
-__device__ __forceinline__ void point_force_warp(const PForce& pf) {
-    const int k = blockIdx.x * kPfPerCta + (threadIdx.x >> 5);
+__device__ __forceinline__ void point_force_warp(const PForce& pf, int bid) {
+    const int k = bid * kPfPerCta + (threadIdx.x >> 5);
     if (k >= pf.P.n) return;
     const int lane = threadIdx.x & 31, comp = lane >> 4, e = lane & 15;
     const int n = pf.n;
@@ -73,44 +89,74 @@ __device__ __forceinline__ void point_force_warp(const PForce& pf) {
     if (e == 0) pf.F[2 * k + comp] = pf.P.cE[k] * (u[0] - 2.0 * u[1] + u[2]);
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Dispatch of a fused launch; `grid(b)` runs grid CTA b.
+template <class GridFn>
+__device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, int ngrid, GridFn&& grid) {
+    const int bid = blockIdx.x;
+    if (bid >= pf.nblk + ngrid) {  // gather CTA
+        if (threadIdx.x == 0)
+            while (ld_acquire_u64(G.cnt) < G.target) __nanosleep(32);
+        __syncthreads();
+        const int q = (bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5);
+        face_gather_warp(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, threadIdx.x & 31);
+        return;
+    }
+    if (bid < pf.nblk) point_force_warp(pf, bid);
+    else grid(bid - pf.nblk);
+    if (G.nblk) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(G.cnt, 1ull);
+        }
+    }
+}
+
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
-__global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out, PForce pf) {
-    if ((int)blockIdx.x < pf.nblk) return point_force_warp(pf);
-    const int q = (blockIdx.x - pf.nblk) * blockDim.x + threadIdx.x;
-    if (q >= L.nn) return;
-    const int i = q & (L.n - 1), j = q >> L.lg;
-    GAcc acc{w, L.n, L.nn};
-    double ru, rv, rp;
-    stokes_rows(L, acc, i, j, ru, rv, rp);
-    out[q] = ru;
-    out[L.nn + q] = rv;
-    out[2 * L.nn + q] = rp;
+__global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out, PForce pf, Gather G,
+                               int ngrid) {
+    fused_launch(pf, G, ngrid, [&](int b) {
+        const int q = b * blockDim.x + threadIdx.x;
+        if (q >= L.nn) return;
+        const int i = q & (L.n - 1), j = q >> L.lg;
+        GAcc acc{w, L.n, L.nn};
+        double ru, rv, rp;
+        stokes_rows(L, acc, i, j, ru, rv, rp);
+        out[q] = ru;
+        out[L.nn + q] = rv;
+        out[2 * L.nn + q] = rp;
+    });
 }
 
 // r = b - S w (E' part added by k_face_gather with sign +1).
 __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const double* __restrict__ w,
-                                  double* __restrict__ r, PForce pf) {
-    if ((int)blockIdx.x < pf.nblk) return point_force_warp(pf);
-    const int q = (blockIdx.x - pf.nblk) * blockDim.x + threadIdx.x;
-    if (q >= L.nn) return;
-    const int i = q & (L.n - 1), j = q >> L.lg;
-    GAcc acc{w, L.n, L.nn};
-    double ru, rv, rp;
-    stokes_rows(L, acc, i, j, ru, rv, rp);
-    r[q] = b[q] - ru;
-    r[L.nn + q] = b[L.nn + q] - rv;
-    r[2 * L.nn + q] = b[2 * L.nn + q] - rp;
+                                  double* __restrict__ r, PForce pf, Gather G, int ngrid) {
+    fused_launch(pf, G, ngrid, [&](int blk) {
+        const int q = blk * blockDim.x + threadIdx.x;
+        if (q >= L.nn) return;
+        const int i = q & (L.n - 1), j = q >> L.lg;
+        GAcc acc{w, L.n, L.nn};
+        double ru, rv, rp;
+        stokes_rows(L, acc, i, j, ru, rv, rp);
+        r[q] = b[q] - ru;
+        r[L.nn + q] = b[L.nn + q] - rv;
+        r[2 * L.nn + q] = b[2 * L.nn + q] - rp;
+    });
 }
 
 // Fused residual + restriction (K2): coarse b = R (b - S w) per coarse cell
 // (restrict_saddle, transfers.cpp:107-134; periodic).  The E' part of the
 // restricted residual, R E' w = sum_k L^{l+1}_k F_k, is added afterwards by
 // k_face_gather on the coarse face list.
-__global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
-                                    double* __restrict__ bc, PForce pf) {
-    if ((int)blockIdx.x < pf.nblk) return point_force_warp(pf);
+__device__ __forceinline__ void residual_restrict_cell(const Lev& F, const double* __restrict__ b,
+                                                       const double* __restrict__ w, double* __restrict__ bc, int q) {
     const int nc = F.n >> 1, nnc = nc * nc;
-    const int q = (blockIdx.x - pf.nblk) * blockDim.x + threadIdx.x;
     if (q >= nnc) return;
     const int I = q % nc, J = q / nc;
     const int i = 2 * I, j = 2 * J, n = F.n, nn = F.nn;
@@ -141,6 +187,11 @@ __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const d
     bc[nnc + q] = 0.125 * (rv_at(i, j - 1) + 2.0 * rv_at(i, j) + rv_at(i, j + 1) + rv_at(i + 1, j - 1) +
                            2.0 * rv_at(i + 1, j) + rv_at(i + 1, j + 1));
     bc[2 * nnc + q] = 0.25 * (rp_at(i, j) + rp_at(i + 1, j) + rp_at(i, j + 1) + rp_at(i + 1, j + 1));
+}
+
+__global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
+                                    double* __restrict__ bc, PForce pf, Gather G, int ngrid) {
+    fused_launch(pf, G, ngrid, [&](int blk) { residual_restrict_cell(F, b, w, bc, blk * blockDim.x + threadIdx.x); });
 }
 
 // Plain restriction of a vector (ibmg_restrict).

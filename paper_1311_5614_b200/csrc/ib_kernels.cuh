@@ -265,24 +265,10 @@ __global__ void k_block_conflicts(int n, const uint8_t* __restrict__ big, unsign
     mask[A] = m;
 }
 
-// out[face] += sign * sum_{(k, l) in list(face)} l * F[k][comp]: one warp per
-// face (lists run to hundreds of entries on coarse levels), lanes strided over
-// the entries, fixed butterfly reduction (deterministic spread: no atomics).
+// Stand-alone face gather (spread of given forces): face_gather_warp per warp.
 __global__ void k_face_gather(FaceList FL, Win W, const double* __restrict__ F, double* __restrict__ out,
                               int nn, double sign) {
-    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (q >= FL.nf) return;
-    const int face = FL.face[q];
-    const int comp = face >= nn;
-    double s = 0.0;
-    for (int e = FL.off[q] + lane; e < FL.off[q + 1]; e += 32) {
-        const int v = FL.ent[e];
-        const int k = v >> 5;
-        s += W.w[(size_t)k * 64 + (v & 31)] * F[2 * k + comp];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[face] += sign * s;
+    face_gather_warp(FL, W, F, out, nn, sign, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
 }
 
 // Assembly of E'_l rows, one warp per face-list row, accumulated in a 16x16

@@ -139,6 +139,8 @@ struct ibmg_ctx {
     double *V = nullptr, *Z = nullptr, *wv = nullptr, *xv = nullptr, *rv = nullptr, *bv = nullptr;
     double *partial = nullptr, *dh = nullptr, *ones = nullptr, *stage_a = nullptr, *stage_b = nullptr;
     unsigned* ticket = nullptr;  // last-CTA ticket of the fused CGS sweeps
+    unsigned long long* tail_cnt = nullptr;  // producer counter of the fused gathers
+    unsigned long long tail_base = 0;        // its value after the last enqueued launch
     double* hpin = nullptr;    // pinned host mirror of dh
     size_t M = 0;              // 3 N^2
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
@@ -273,6 +275,8 @@ void alloc_levels(ibmg_ctx* c) {
     c->partial = dalloc<double>(size_t(std::max(kRedBlocks, kCgsBlocks)) * (m + 2));
     c->ticket = dalloc<unsigned>(1);
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
+    c->tail_cnt = dalloc<unsigned long long>(1);
+    CK(cudaMemset(c->tail_cnt, 0, sizeof(unsigned long long)));
     c->dh = dalloc<double>(2 * (m + 2) + 8);
     CK(cudaMallocHost(&c->hpin, sizeof(double) * (2 * (m + 2) + 8)));
     c->ones = dalloc<double>(size_t(p.N) * p.N);
@@ -800,21 +804,33 @@ PForce pforce(ibmg_ctx* c, const LevelBuf& lb, const double* w, bool active) {
     return pf;
 }
 
-// out = A_l w on level l (stencil + E' via point forces and the level face list).
+// Gather CTAs adding sign * L_k F_k on level `to`'s face list into out, after
+// the launch's pf.nblk + ngrid producer CTAs (grid_kernels.cuh fused_launch).
+Gather gather(ibmg_ctx* c, const LevelBuf& to, double* out, double sign, const PForce& pf, int ngrid) {
+    Gather G{to.FL, to.W, c->F, out, to.L.nn, sign, 0, c->tail_cnt, 0ull};
+    if (pf.nblk) {
+        G.nblk = int(nblk(to.FL.nf, kPfPerCta));
+        c->tail_base += (unsigned long long)(pf.nblk + ngrid);
+        G.target = c->tail_base;
+    }
+    return G;
+}
+
+// out = A_l w on level l: stencil, point forces and the face gather in one launch.
 void apply_level(ibmg_ctx* c, int l, const double* w, double* out) {
     LevelBuf& lb = c->lev[l];
     const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
-    LAUNCH(c, k_stokes_apply, pf.nblk + nblk(lb.L.nn), 256, 0, lb.L, w, out, pf);
-    if (pf.nblk)
-        LAUNCH(c, k_face_gather, nblk(size_t(lb.FL.nf) * 32), 256, 0, lb.FL, lb.W, c->F, out, lb.L.nn, -1.0);
+    const int ng = int(nblk(lb.L.nn));
+    const Gather G = gather(c, lb, out, -1.0, pf, ng);
+    LAUNCH(c, k_stokes_apply, pf.nblk + ng + G.nblk, 256, 0, lb.L, w, out, pf, G, ng);
 }
 
 void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double* r) {
     LevelBuf& lb = c->lev[l];
     const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
-    LAUNCH(c, k_stokes_residual, pf.nblk + nblk(lb.L.nn), 256, 0, lb.L, b, w, r, pf);
-    if (pf.nblk)
-        LAUNCH(c, k_face_gather, nblk(size_t(lb.FL.nf) * 32), 256, 0, lb.FL, lb.W, c->F, r, lb.L.nn, 1.0);
+    const int ng = int(nblk(lb.L.nn));
+    const Gather G = gather(c, lb, r, 1.0, pf, ng);
+    LAUNCH(c, k_stokes_residual, pf.nblk + ng + G.nblk, 256, 0, lb.L, b, w, r, pf, G, ng);
 }
 
 Slabs slabs(const LevelBuf& lb) { return Slabs{lb.Ainv, lb.sl_rp, lb.sl_off, lb.sl_col, lb.sl_val}; }
@@ -918,9 +934,9 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true) {
             CK(cudaMemsetAsync(wl(l), 0, sizeof(double) * 3 * lb.L.nn, c->s));
             for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
             const PForce pf = pforce(c, lb, wl(l), nx.FL.nf > 0);
-            LAUNCH(c, k_residual_restrict, pf.nblk + nblk(nx.L.nn), 256, 0, lb.L, bl(l), wl(l), nx.b, pf);
-            if (pf.nblk)
-                LAUNCH(c, k_face_gather, nblk(size_t(nx.FL.nf) * 32), 256, 0, nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0);
+            const int ng = int(nblk(nx.L.nn));
+            const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
+            LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, bl(l), wl(l), nx.b, pf, G, ng);
         }
         coarse_cycle(c, c->lev[c->lc].b, wl(c->lc));
         for (int l = c->lc - 1; l >= 0; --l) {
@@ -1169,6 +1185,7 @@ void ibmg_destroy(ibmg_ctx* c) {
     dfree(c->stage_b);
     dfree(c->partial);
     dfree(c->ticket);
+    dfree(c->tail_cnt);
     dfree(c->dh);
     dfree(c->ones);
     dfree(c->err_flag);
