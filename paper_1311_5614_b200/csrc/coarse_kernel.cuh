@@ -13,7 +13,7 @@
 namespace ibmg {
 
 constexpr int kCoarseMaxN = 32;
-constexpr int kCoarseThreads = 512;  // 4 groups of 128 for the big phase
+constexpr int kCoarseThreads = 384;  // 3 groups of 128 for the big phase (170 regs per thread)
 
 struct CLev {
     Lev L;
@@ -95,7 +95,7 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
                 const int Bk = slot[g].rp[47];
                 int nc, nq;
                 next_of(cc, qq, nc, nq);
-                big_block_es(L, slot[g], nullptr, 4 * (Bk % nbk), 4 * (Bk / nbk), W,
+                big_block_es<1>(L, slot[g], nullptr, 4 * (Bk % nbk), 4 * (Bk / nbk), W,
                              (const double*)w, B,
                              [&](int f, int i, int j, double old, double d) { W(f, i, j) = old + d; }, S[g], gt,
                              [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); },

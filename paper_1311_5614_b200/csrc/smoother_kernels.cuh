@@ -305,7 +305,11 @@ __device__ __forceinline__ void load_inverse_part(double (&av)[28], const double
 // A_q != nullptr, else preloaded by the caller; A_next != nullptr prefetches
 // the next block's part into `av` after the apply, hiding its L2 latency
 // behind the write-back and the colour barrier.
-template <class WA, class LocA, class BA, class WAdd, class Sync, class After = NoOp>
+// EDOT 0: E' row dots by 3 threads per row, 24 gathers in flight per thread
+// (latency: one block per CTA, long fine-level rows).  EDOT 1: one thread per
+// row (threads 64..103, a warp apart from the stencil rows), 8 at a time —
+// fewer instructions where several groups share an SM (coarse kernel).
+template <int EDOT = 0, class WA, class LocA, class BA, class WAdd, class Sync, class After = NoOp>
 __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, const double* __restrict__ A_q, int bi,
                                              int bj, const WA& W, const LocA& wloc, const BA& Bv, WAdd&& wadd,
                                              BigScratch& S, int gt, Sync&& gsync, After after_rows = After{},
@@ -322,7 +326,7 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
         S.sr[gt] = Bv(f, i, j) - stokes_row(L, W, f, i, j);
         S.wold[gt] = W(f, i, j);  // current value, reused for the correction (no re-read)
     }
-    if (gt < 120) {  // E' row dots: 3 threads per row, gathers batched 8 at a time
+    if (EDOT == 0 && gt < 120) {  // E' row dots: 3 threads per row, 24 gathers per round
         const int r = gt % 40, p = gt / 40;
         const int e1 = slot.rp[r + 1];
         double s0 = 0.0;
@@ -339,9 +343,30 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
         }
         S.epart[p][r] = s0;
     }
+    if (EDOT == 1 && gt >= 64 && gt < 104) {  // E' row dots: one thread per row
+        const int r = gt - 64;
+        const int e1 = slot.rp[r + 1];
+        double s0 = 0.0, s1 = 0.0;
+        for (int e = slot.rp[r]; e < e1; e += 8) {
+            double vv[8], xx[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int em = e + m;
+                vv[m] = em < e1 ? slot.val[em] : 0.0;
+                xx[m] = em < e1 ? wloc[slot.col[em]] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; m += 2) {
+                s0 += vv[m] * xx[m];
+                s1 += vv[m + 1] * xx[m + 1];
+            }
+        }
+        S.epart[0][r] = s0 + s1;
+    }
     gsync();
     after_rows();
-    if (gt < 40) S.sr[gt] += (S.epart[0][gt] + S.epart[1][gt]) + S.epart[2][gt];  // combined residual
+    if (gt < 40)  // combined residual
+        S.sr[gt] += EDOT == 0 ? (S.epart[0][gt] + S.epart[1][gt]) + S.epart[2][gt] : S.epart[0][gt];
     gsync();
     if (gt < 112) {
         double s0 = 0.0, s1 = 0.0;
