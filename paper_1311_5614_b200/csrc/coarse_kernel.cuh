@@ -42,6 +42,15 @@ struct SW {
     }
 };
 
+// Pointers into the dynamic shared memory lose their address space when kept
+// in local arrays or passed to a non-inlined function; asserting it again lets
+// the compiler emit LDS/STS (short scoreboard) instead of generic LD/ST.
+template <class T>
+__device__ __forceinline__ T* in_smem(T* p) {
+    __builtin_assume(__isShared(p));
+    return p;
+}
+
 __device__ __forceinline__ void cmark(unsigned long long* tr, int& n) {
     if (tr && threadIdx.x == 0) tr[n] = gtimer();
     ++n;
@@ -49,6 +58,10 @@ __device__ __forceinline__ void cmark(unsigned long long* tr, int& n) {
 
 __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* slot, BigScratch* S,
                              unsigned long long* tr, int& nm) {
+    w = in_smem(w);
+    b = in_smem(b);
+    slot = in_smem(slot);
+    S = in_smem(S);
     const Lev& L = C.L;
     const int n = L.n, t = threadIdx.x, nt = blockDim.x, nbk = n >> 2;
     SW W{w, n, L.nn};
