@@ -131,18 +131,49 @@ __global__ void k_windows(int npts, const double* __restrict__ X, WinLevels WL, 
     }
 }
 
-// Keys for the face lists of one level: one (face, entry) pair per nonzero
-// left-window weight; sentinel key INT_MAX for zeros.
-__global__ void k_face_keys(int npts, Win W, int n, int* keys, int* vals) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= npts * 32) return;
-    const int k = q >> 5, s = (q >> 4) & 1, e = q & 15;
+// Face lists of every level in one sort: level-major face
+// numbering key = base[l] + face (face < 2 n_l^2; 2 n_l^2 is the level's
+// sentinel for zero window weights), value = entry pt*32 + comp*16 + e.
+struct FaceBase {
+    int nlev;
+    unsigned base[21];
+    int n[20];
+};
+__global__ void k_face_keys(int npts, WinLevels WL, FaceBase FB, unsigned* keys, int* vals) {
+    const long items = (long)npts * 32;
+    const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= items * FB.nlev) return;
+    const int l = int(q / items), r = int(q - l * items);
+    const int k = r >> 5, s = (r >> 4) & 1, e = r & 15, n = FB.n[l];
+    const Win& W = WL.win[l];
     const double v = W.w[(size_t)k * 64 + s * 16 + e];
     const int4 o = W.orgL[k];
     const int i0 = s ? o.z : o.x, j0 = s ? o.w : o.y;
     const int i = wr(i0 + (e & 3), n), j = wr(j0 + (e >> 2), n);
-    keys[q] = (v != 0.0) ? s * n * n + i + j * n : 0x7fffffff;
-    vals[q] = q;
+    keys[q] = FB.base[l] + unsigned((v != 0.0) ? s * n * n + i + j * n : 2 * n * n);
+    vals[q] = r;
+}
+
+// Per run of the sorted keys: the level-local face index, the level's first
+// run (counter 20), its number of faces (17) and longest list (29); the
+// sentinel run of a level is not a face.
+__global__ void k_face_levels(const unsigned* __restrict__ ukeys, const int* __restrict__ nruns,
+                              const int* __restrict__ off, FaceBase FB, int* __restrict__ face,
+                              int* __restrict__ counters, int ctr_stride) {
+    const int nr = *nruns;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nr; q += gridDim.x * blockDim.x) {
+        const unsigned key = ukeys[q];
+        int l = 0;
+        while (l + 1 < FB.nlev && key >= FB.base[l + 1]) ++l;
+        const int loc = int(key - FB.base[l]), n = FB.n[l];
+        face[q] = loc;
+        int* ctr = counters + l * ctr_stride;
+        if (q == 0 || ukeys[q - 1] < FB.base[l]) ctr[20] = q;
+        if (loc != 2 * n * n) {
+            atomicAdd(ctr + 17, 1);
+            atomicMax(ctr + 29, off[q + 1] - off[q]);
+        }
+    }
 }
 
 // Big-block marking: a 4x4 block is big when any face of it
@@ -397,18 +428,6 @@ __global__ void __launch_bounds__(32 * kELongWarps) k_erows_long(FaceList FL, Wi
         base += __popc(m);
     }
     if (!pass && lane == 0) cnt[q] = base;
-}
-
-// Longest face list of a level (runs counted by RLE; the INT_MAX sentinel run
-// excluded) into out[0]; out[1] = 1 when the last run is that sentinel.
-__global__ void k_rowlen_max(const int* __restrict__ face, const int* __restrict__ off, const int* __restrict__ nruns,
-                             int* __restrict__ out) {
-    const int nr = *nruns;
-    int m = 0;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nr; q += gridDim.x * blockDim.x)
-        if (face[q] != 0x7fffffff) m = max(m, off[q + 1] - off[q]);
-    atomicMax(out, m);
-    if (blockIdx.x == 0 && threadIdx.x == 0) out[1] = (nr > 0 && face[nr - 1] == 0x7fffffff) ? 1 : 0;
 }
 
 // Fiber force density of the RHS times the spread quadrature:

@@ -131,6 +131,7 @@ struct ibmg_ctx {
     int* err_flag = nullptr;
     // setup scratch
     int *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *vals2 = nullptr, *runs = nullptr, *cnt = nullptr;
+    int *fl_face = nullptr, *fl_off = nullptr, *fl_ent = nullptr;  // batched face lists (all levels)
     size_t sort_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -202,9 +203,11 @@ void prof_collect(ibmg_ctx* c) {
         if ((ctx)->prof && (ctx)->prof_pending.size() > 4096) prof_collect(ctx); \
     } while (0)
 
-// per-level counters: 17 face-list runs, 18 reach, 19 max slab entries,
-// 28 slab total, 29 longest face list, 30 sentinel-run flag
+// per-level counters: 17 faces, 18 reach, 19 max slab entries, 20 first run of
+// the level in the shared face-list arrays, 28 slab total, 29 longest face
+// list; level 0's slot 31 holds the total run count of the batched face lists
 constexpr int kCtr = 32;
+constexpr int kCtrRuns = 31;
 
 Lev make_lev(const ibmg_params& p, int n) {
     Lev L;
@@ -295,9 +298,7 @@ void free_structs(ibmg_ctx* c) {
         dfree(lb.W.orgL);
         dfree(lb.W.orgR);
         dfree(lb.W.w);
-        dfree(lb.FL.face);
-        dfree(lb.FL.off);
-        dfree(lb.FL.ent);
+        lb.FL.face = lb.FL.off = lb.FL.ent = nullptr;  // views into c->fl_*
         dfree(lb.E.rp);
         dfree(lb.E.col);
         dfree(lb.E.val);
@@ -335,6 +336,9 @@ void free_structs(ibmg_ctx* c) {
     dfree(c->vals);
     dfree(c->keys2);
     dfree(c->vals2);
+    dfree(c->fl_face);
+    dfree(c->fl_off);
+    dfree(c->fl_ent);
     dfree(c->runs);
     dfree(c->cnt);
     c->sort_cap = 0;
@@ -533,29 +537,42 @@ void rebuild(ibmg_ctx* c) {
             WL.n[l] = c->lev[l].L.n;
         }
         LAUNCH(c, k_windows, nblk(size_t(npts) * 4, 128), 128, 0, npts, c->X, WL, c->lev[0].L.h, c->err_flag);
-        // face lists: sort (face, entry) keys per level, run-length encode
-        const int items = npts * 32;
-        for (int l = 0; l < c->nlev; ++l) {
-            LevelBuf& lb = c->lev[l];
-            LAUNCH(c, k_face_keys, nblk(items), 256, 0, npts, lb.W, lb.L.n, c->keys, c->vals);
+        // face lists of all levels: one sort of level-major (face, entry) keys,
+        // one run-length encode, one scan, then per-run level bookkeeping
+        {
+            FaceBase FB{};
+            FB.nlev = c->nlev;
+            unsigned acc = 0;
+            for (int l = 0; l < c->nlev; ++l) {
+                const int n = c->lev[l].L.n;
+                FB.base[l] = acc;
+                FB.n[l] = n;
+                acc += 2u * unsigned(n) * unsigned(n) + 1u;
+            }
+            FB.base[c->nlev] = acc;
+            int end_bit = 1;
+            while (end_bit < 32 && (acc >> end_bit) != 0) ++end_bit;
+            if (long(npts) * 32 * c->nlev >= (1L << 31)) throw InvalidArg("too many Lagrangian points for the face lists");
+            const int tot = npts * 32 * c->nlev;
+            unsigned* keys = reinterpret_cast<unsigned*>(c->keys);
+            unsigned* keys2 = reinterpret_cast<unsigned*>(c->keys2);
+            int* nruns = c->counters + kCtrRuns;
+            LAUNCH(c, k_face_keys, nblk(size_t(tot)), 256, 0, npts, WL, FB, keys, c->vals);
             size_t bytes = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys, c->keys2, c->vals, lb.FL.ent, items, 0, 31, c->s);
+            cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, c->vals, c->fl_ent, tot, 0, end_bit, c->s);
             ensure_cub(c, bytes);
-            CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys, c->keys2, c->vals, lb.FL.ent, items, 0, 31,
+            CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, keys, keys2, c->vals, c->fl_ent, tot, 0, end_bit,
                                                c->s));
             bytes = 0;
-            cub::DeviceRunLengthEncode::Encode(nullptr, bytes, c->keys2, lb.FL.face, c->cnt, c->counters + l * kCtr + 17,
-                                               items, c->s);
+            cub::DeviceRunLengthEncode::Encode(nullptr, bytes, keys2, keys, c->cnt, nruns, tot, c->s);
             ensure_cub(c, bytes);
-            CK(cub::DeviceRunLengthEncode::Encode(c->cub_tmp, bytes, c->keys2, lb.FL.face, c->cnt,
-                                                  c->counters + l * kCtr + 17, items, c->s));
+            CK(cub::DeviceRunLengthEncode::Encode(c->cub_tmp, bytes, keys2, keys, c->cnt, nruns, tot, c->s));
             bytes = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, lb.FL.off, items + 1, c->s);
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, c->fl_off, tot + 1, c->s);
             ensure_cub(c, bytes);
-            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, lb.FL.off, items + 1, c->s));
-            LAUNCH(c, k_rowlen_max, 64, 256, 0, lb.FL.face, lb.FL.off, c->counters + l * kCtr + 17,
-                   c->counters + l * kCtr + 29);
-            ++c->launches;  // account the CUB launches coarsely (sort+rle+scan)
+            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, c->fl_off, tot + 1, c->s));
+            LAUNCH(c, k_face_levels, 296, 256, 0, keys, nruns, c->fl_off, FB, c->fl_face, c->counters, kCtr);
+            c->launches += 2;  // account the CUB launches coarsely (sort+rle+scan)
         }
         // big-block marking, colour sort, reach
         for (int l = 0; l + 1 < c->nlev; ++l) {
@@ -582,10 +599,11 @@ void rebuild(ibmg_ctx* c) {
         for (int l = 0; l < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
             const int* h = &hc[size_t(l) * kCtr];
-            // runs include the sentinel run (INT_MAX) when any weight was zero
-            const int runs = h[17] - h[30];  // h[30]: the last run is the INT_MAX sentinel (k_rowlen_max)
-            lb.FL.nf = runs;
+            lb.FL.nf = h[17];
             lb.maxrow = h[29];
+            lb.FL.face = c->fl_face + h[20];
+            lb.FL.off = c->fl_off + h[20];
+            lb.FL.ent = c->fl_ent;
             if (l + 1 < c->nlev) {
                 const int reach = h[18];
                 if (reach > 7)
@@ -764,13 +782,15 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
             lb.W.orgR = dalloc<int4>(cap);
             lb.W.w = dalloc<double>(size_t(cap) * 64);
             lb.fl_cap = cap * 32;
-            lb.FL.face = dalloc<int>(size_t(lb.fl_cap));
-            lb.FL.off = dalloc<int>(size_t(lb.fl_cap) + 1);
-            lb.FL.ent = dalloc<int>(size_t(lb.fl_cap));
             lb.E.rp = dalloc<int>(size_t(lb.fl_cap) + 1);
             lb.ecnt = dalloc<int>(size_t(lb.fl_cap) + 1);
         }
-        size_t scap = std::max<size_t>(size_t(cap) * 32 + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
+        // batched face lists of all levels (views per level)
+        const size_t ftot = size_t(cap) * 32 * c->nlev;
+        c->fl_face = dalloc<int>(ftot);
+        c->fl_off = dalloc<int>(ftot + 1);
+        c->fl_ent = dalloc<int>(ftot);
+        size_t scap = std::max<size_t>(ftot + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
         c->keys = dalloc<int>(scap);
         c->vals = dalloc<int>(scap);
         c->keys2 = dalloc<int>(scap);
