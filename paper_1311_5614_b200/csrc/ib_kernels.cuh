@@ -302,28 +302,36 @@ __global__ void k_face_gather(FaceList FL, Win W, const double* __restrict__ F, 
     face_gather_warp(FL, W, F, out, nn, sign, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
 }
 
-// Assembly of E'_l rows, one warp per face-list row, accumulated in a 16x16
-// shared-memory patch of column offsets (slot = wr(col - row + 8, n); the E'
-// reach is <= 7, checked at setup) in a fixed order (entry pairs ascending in
-// point, windows k-1, k, k+1, lower half-warp first): deterministic.  pass 0
-// writes the row's nonzero count, pass 1 the (col, val) pairs.
-constexpr int kEWarps = 8;
-__global__ void __launch_bounds__(32 * kEWarps) k_erows(FaceList FL, Win W, Pts P, int n, int pass, EMat E,
-                                                         int* __restrict__ cnt) {
-    __shared__ double patch[kEWarps][256];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q = blockIdx.x * kEWarps + wid;
-    if (q >= FL.nf) return;
-    double* pt = patch[wid];
-    for (int s = lane; s < 256; s += 32) pt[s] = 0.0;
-    __syncwarp();
-    const int nn = n * n, face = FL.face[q], comp = face >= nn;
-    const int f = face - comp * nn, di = f & (n - 1), dj = f / n;
+// Assembly of E'_l rows for the face lists of all levels in
+// one launch: a row is the run q of the batched face lists (k_face_keys);
+// entry pairs accumulate into a 16x16 shared-memory patch of column offsets
+// (slot = wr(col - row + 8, n); the E' reach is <= 7, checked at setup) in a
+// fixed order (entry pairs ascending in point, windows k-1, k, k+1, lower
+// half-warp first): deterministic.  pass 0 writes the row's nonzero count,
+// pass 1 the (col, val) pairs at rp[q].  Levels whose face lists run long
+// (coarse levels: a face there collects many points) take a CTA per row, the
+// 16 warps on interleaved entry pairs with private patches summed in warp
+// order; the others a warp per row.
+constexpr int kEWarps = 16;
+struct ERows {
+    int nlev;
+    Win W[20];
+    int n[20];
+    int start[21];   // first run of each level; start[nlev] = total runs
+    int islong[20];  // CTA per row on this level
+    int lstart[21];  // prefix over the long levels' run counts (CTA part)
+    int nwarp_cta;   // CTAs of the warp part
+};
+
+// Accumulate entry pairs e0, e0 + stride, ... of a row into the patch pt.
+__device__ __forceinline__ void erow_accumulate(double* pt, const int* __restrict__ ent, int e_begin, int e_end,
+                                                int stride, const Win& W, const Pts& P, int n, int comp, int di,
+                                                int dj, int lane) {
     const int half = lane >> 4, e16 = lane & 15;
-    for (int e0 = FL.off[q]; e0 < FL.off[q + 1]; e0 += 2) {
+    for (int e0 = e_begin; e0 < e_end; e0 += stride) {
         const int e = e0 + half;
-        const bool act = e < FL.off[q + 1];
-        const int v = act ? FL.ent[e] : 0;
+        const bool act = e < e_end;
+        const int v = act ? ent[e] : 0;
         const int k = v >> 5;
         const double lc = act ? W.w[(size_t)k * 64 + (v & 31)] * P.cE[k] : 0.0;
         const int ks[3] = {P.kprev[k], k, P.knext[k]};
@@ -348,86 +356,71 @@ __global__ void __launch_bounds__(32 * kEWarps) k_erows(FaceList FL, Win W, Pts 
             __syncwarp();
         }
     }
-    int base = pass ? E.rp[q] : 0;
+}
+
+// Compact a finished patch (one warp): count (pass 0) or (col, val) pairs.
+__device__ __forceinline__ void erow_emit(const double* pt, int q, int pass, int n, int comp, int di, int dj,
+                                          int* __restrict__ cnt, const int* __restrict__ rp, int* __restrict__ col,
+                                          double* __restrict__ val, int lane) {
+    const int nn = n * n;
+    int base = pass ? rp[q] : 0;
     for (int y = 0; y < 8; ++y) {
         const int s = y * 32 + lane;
         const double v = pt[s];
         const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
         if (pass && v != 0.0) {
             const int pos = base + __popc(m & ((1u << lane) - 1u));
-            E.col[pos] = comp * nn + wr(di - 8 + (s & 15), n) + wr(dj - 8 + (s >> 4), n) * n;
-            E.val[pos] = v;
+            col[pos] = comp * nn + wr(di - 8 + (s & 15), n) + wr(dj - 8 + (s >> 4), n) * n;
+            val[pos] = v;
         }
         base += __popc(m);
     }
     if (!pass && lane == 0) cnt[q] = base;
 }
 
-// Long-row variant of k_erows for coarse levels (a face there can collect
-// ~1e5 point entries): one 512-thread CTA per row, its 16 warps take
-// interleaved entry pairs into private 16x16 patches which are then summed in
-// warp order (deterministic), then compacted like k_erows.
-constexpr int kELongWarps = 16;
-__global__ void __launch_bounds__(32 * kELongWarps) k_erows_long(FaceList FL, Win W, Pts P, int n, int pass, EMat E,
-                                                                  int* __restrict__ cnt) {
-    __shared__ double patch[kELongWarps][256];
+__global__ void __launch_bounds__(32 * kEWarps) k_erows(ERows R, const int* __restrict__ face,
+                                                         const int* __restrict__ off, const int* __restrict__ ent,
+                                                         Pts P, int pass, int* __restrict__ cnt,
+                                                         const int* __restrict__ rp, int* __restrict__ col,
+                                                         double* __restrict__ val) {
+    __shared__ double patch[kEWarps][256];
     __shared__ double fin[256];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, q = blockIdx.x;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool cta_row = (int)blockIdx.x >= R.nwarp_cta;
+    int q, l = 0;
+    if (!cta_row) {
+        q = blockIdx.x * kEWarps + wid;
+        if (q >= R.start[R.nlev]) return;
+        while (q >= R.start[l + 1]) ++l;
+        if (R.islong[l]) return;
+    } else {
+        const int cq = blockIdx.x - R.nwarp_cta;
+        while (cq >= R.lstart[l + 1]) ++l;
+        q = R.start[l] + (cq - R.lstart[l]);
+    }
+    const int n = R.n[l], nn = n * n, fc = face[q];
+    if (fc == 2 * nn) {  // the level's sentinel run (zero window weights): no row
+        if (!pass && lane == 0 && (!cta_row || wid == 0)) cnt[q] = 0;
+        return;
+    }
+    const int comp = fc >= nn, f = fc - comp * nn, di = f & (n - 1), dj = f / n;
     double* pt = patch[wid];
     for (int s = lane; s < 256; s += 32) pt[s] = 0.0;
     __syncwarp();
-    const int nn = n * n, face = FL.face[q], comp = face >= nn;
-    const int f = face - comp * nn, di = f & (n - 1), dj = f / n;
-    const int half = lane >> 4, e16 = lane & 15;
-    for (int e0 = FL.off[q] + 2 * wid; e0 < FL.off[q + 1]; e0 += 2 * kELongWarps) {
-        const int e = e0 + half;
-        const bool act = e < FL.off[q + 1];
-        const int v = act ? FL.ent[e] : 0;
-        const int k = v >> 5;
-        const double lc = act ? W.w[(size_t)k * 64 + (v & 31)] * P.cE[k] : 0.0;
-        const int ks[3] = {P.kprev[k], k, P.knext[k]};
-        const double coef[3] = {1.0, -2.0, 1.0};
-        for (int t = 0; t < 3; ++t) {
-            int slot = -1;
-            double add = 0.0;
-            if (act) {
-                const int kk = ks[t];
-                const double r = W.w[(size_t)kk * 64 + (2 + comp) * 16 + e16];
-                if (r != 0.0) {
-                    const int4 o = W.orgR[kk];
-                    const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
-                    const int sx = wr(i0 + (e16 & 3) - di + 8, n), sy = wr(j0 + (e16 >> 2) - dj + 8, n);
-                    slot = (sx < 16 && sy < 16) ? sy * 16 + sx : -1;
-                    add = lc * coef[t] * r;
-                }
-            }
-            if (half == 0 && slot >= 0) pt[slot] += add;
-            __syncwarp();
-            if (half == 1 && slot >= 0) pt[slot] += add;
-            __syncwarp();
-        }
+    if (!cta_row) {
+        erow_accumulate(pt, ent, off[q], off[q + 1], 2, R.W[l], P, n, comp, di, dj, lane);
+        erow_emit(pt, q, pass, n, comp, di, dj, cnt, rp, col, val, lane);
+        return;
     }
+    erow_accumulate(pt, ent, off[q] + 2 * wid, off[q + 1], 2 * kEWarps, R.W[l], P, n, comp, di, dj, lane);
     __syncthreads();
     if (threadIdx.x < 256) {
         double s = 0.0;
-        for (int w = 0; w < kELongWarps; ++w) s += patch[w][threadIdx.x];
+        for (int w = 0; w < kEWarps; ++w) s += patch[w][threadIdx.x];
         fin[threadIdx.x] = s;
     }
     __syncthreads();
-    if (wid != 0) return;
-    int base = pass ? E.rp[q] : 0;
-    for (int y = 0; y < 8; ++y) {
-        const int s = y * 32 + lane;
-        const double v = fin[s];
-        const unsigned m = __ballot_sync(0xffffffffu, v != 0.0);
-        if (pass && v != 0.0) {
-            const int pos = base + __popc(m & ((1u << lane) - 1u));
-            E.col[pos] = comp * nn + wr(di - 8 + (s & 15), n) + wr(dj - 8 + (s >> 4), n) * n;
-            E.val[pos] = v;
-        }
-        base += __popc(m);
-    }
-    if (!pass && lane == 0) cnt[q] = base;
+    if (wid == 0) erow_emit(fin, q, pass, n, comp, di, dj, cnt, rp, col, val, lane);
 }
 
 // Fiber force density of the RHS times the spread quadrature:

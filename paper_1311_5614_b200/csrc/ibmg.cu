@@ -76,9 +76,7 @@ struct LevelBuf {
     FaceList FL{};
     int fl_cap = 0;
     EMat E{};
-    int* ecnt = nullptr;
     int maxrow = 0;          // longest face list (selects the E'-row assembly kernel)
-    long e_cap = 0;
     uint8_t* big = nullptr;
     unsigned* cmask = nullptr;  // length-2 conflict bits per block (k_block_pairs)
     int nbig = 0;
@@ -132,6 +130,10 @@ struct ibmg_ctx {
     // setup scratch
     int *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *vals2 = nullptr, *runs = nullptr, *cnt = nullptr;
     int *fl_face = nullptr, *fl_off = nullptr, *fl_ent = nullptr;  // batched face lists (all levels)
+    int *e_cnt = nullptr, *e_rp = nullptr, *e_col = nullptr;       // batched E' rows (all levels)
+    double* e_val = nullptr;
+    long e_cap = 0;
+    int* hpin_i = nullptr;  // pinned int scratch (row counts)
     size_t sort_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -282,6 +284,7 @@ void alloc_levels(ibmg_ctx* c) {
     CK(cudaMemset(c->tail_cnt, 0, sizeof(unsigned long long)));
     c->dh = dalloc<double>(2 * (m + 2) + 8);
     CK(cudaMallocHost(&c->hpin, sizeof(double) * (2 * (m + 2) + 8)));
+    CK(cudaMallocHost(&c->hpin_i, sizeof(int) * 16));
     c->ones = dalloc<double>(size_t(p.N) * p.N);
     {
         std::vector<double> one(size_t(p.N) * p.N, 1.0);
@@ -299,11 +302,8 @@ void free_structs(ibmg_ctx* c) {
         dfree(lb.W.orgR);
         dfree(lb.W.w);
         lb.FL.face = lb.FL.off = lb.FL.ent = nullptr;  // views into c->fl_*
-        dfree(lb.E.rp);
-        dfree(lb.E.col);
-        dfree(lb.E.val);
-        dfree(lb.ecnt);
-        lb.e_cap = 0;
+        lb.E.rp = lb.E.col = nullptr;  // views into c->e_*
+        lb.E.val = nullptr;
         lb.FL.nf = 0;
         lb.fl_cap = 0;
         dfree(lb.blk_ids);
@@ -339,6 +339,11 @@ void free_structs(ibmg_ctx* c) {
     dfree(c->fl_face);
     dfree(c->fl_off);
     dfree(c->fl_ent);
+    dfree(c->e_cnt);
+    dfree(c->e_rp);
+    dfree(c->e_col);
+    dfree(c->e_val);
+    c->e_cap = 0;
     dfree(c->runs);
     dfree(c->cnt);
     c->sort_cap = 0;
@@ -494,15 +499,6 @@ void check_err_flag(ibmg_ctx* c, const char* where) {
     if (h & 2) throw CudaError(std::string(where) + ": singular local box matrix");
 }
 
-// E'_l row assembly: warp per row, or CTA per row on levels whose face lists
-// run long (coarse levels, where each face collects many points).
-void erows(ibmg_ctx* c, LevelBuf& lb, int pass) {
-    if (lb.maxrow > 32)
-        LAUNCH(c, k_erows_long, lb.FL.nf, 32 * kELongWarps, 0, lb.FL, lb.W, c->P, lb.L.n, pass, lb.E, lb.ecnt);
-    else
-        LAUNCH(c, k_erows, nblk(lb.FL.nf, kEWarps), 32 * kEWarps, 0, lb.FL, lb.W, c->P, lb.L.n, pass, lb.E, lb.ecnt);
-}
-
 // Rebuild every per-level structure datum from the device positions c->X
 // (the lagged operators of one step).
 // IBMG_SETUP_TRACE=1: host wall-clock marks through rebuild() on stderr
@@ -614,37 +610,51 @@ void rebuild(ibmg_ctx* c) {
             }
         }
         tr.mark("coloured");
-        // assembled E'_l rows on the E-active faces (count, scan, fill)
-        for (int l = 0; l < c->nlev; ++l) {
-            LevelBuf& lb = c->lev[l];
-            if (lb.FL.nf == 0) continue;
-            CK(cudaMemsetAsync(lb.ecnt, 0, sizeof(int) * (lb.FL.nf + 1), c->s));
-            erows(c, lb, 0);
-            size_t bytes = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, bytes, lb.ecnt, lb.E.rp, lb.FL.nf + 1, c->s);
-            ensure_cub(c, bytes);
-            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, lb.ecnt, lb.E.rp, lb.FL.nf + 1, c->s));
-        }
+        // assembled E'_l rows of every level (count, one scan, fill): row q is
+        // run q of the batched face lists; per-level views follow
         {
-            std::vector<int> nnz(c->nlev, 0);
-            for (int l = 0; l < c->nlev; ++l)
-                if (c->lev[l].FL.nf)
-                    CK(cudaMemcpyAsync(&nnz[l], c->lev[l].E.rp + c->lev[l].FL.nf, sizeof(int), cudaMemcpyDeviceToHost,
-                                       c->s));
+            ERows R{};
+            R.nlev = c->nlev;
+            const int total = hc[kCtrRuns];
+            for (int l = 0; l < c->nlev; ++l) {
+                R.W[l] = c->lev[l].W;
+                R.n[l] = c->lev[l].L.n;
+                R.start[l] = hc[size_t(l) * kCtr + 20];
+                R.islong[l] = c->lev[l].maxrow > 32;
+            }
+            R.start[c->nlev] = total;
+            for (int l = 0; l < c->nlev; ++l) {
+                if (R.start[l + 1] < R.start[l]) throw CudaError("face lists: level runs out of order");
+                R.lstart[l + 1] = R.lstart[l] + (R.islong[l] ? R.start[l + 1] - R.start[l] : 0);
+            }
+            R.nwarp_cta = int(nblk(size_t(total), kEWarps));
+            const int grid = R.nwarp_cta + R.lstart[c->nlev];
+            CK(cudaMemsetAsync(c->e_cnt + total, 0, sizeof(int), c->s));
+            LAUNCH(c, k_erows, grid, 32 * kEWarps, 0, R, c->fl_face, c->fl_off, c->fl_ent, c->P, 0, c->e_cnt,
+                   c->e_rp, c->e_col, c->e_val);
+            size_t bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->e_cnt, c->e_rp, total + 1, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->e_cnt, c->e_rp, total + 1, c->s));
+            CK(cudaMemcpyAsync(c->hpin_i, c->e_rp + total, sizeof(int), cudaMemcpyDeviceToHost, c->s));
             tr.mark("launched erows count");
             CK(cudaStreamSynchronize(c->s));
             tr.mark("synced nnz");
+            const long nnz = c->hpin_i[0];
+            if (nnz > c->e_cap) {
+                dfree(c->e_col);
+                dfree(c->e_val);
+                c->e_cap = grow_cap(nnz, c->e_cap);
+                c->e_col = dalloc<int>(size_t(c->e_cap));
+                c->e_val = dalloc<double>(size_t(c->e_cap));
+            }
+            LAUNCH(c, k_erows, grid, 32 * kEWarps, 0, R, c->fl_face, c->fl_off, c->fl_ent, c->P, 1, c->e_cnt,
+                   c->e_rp, c->e_col, c->e_val);
             for (int l = 0; l < c->nlev; ++l) {
                 LevelBuf& lb = c->lev[l];
-                if (lb.FL.nf == 0) continue;
-                if (nnz[l] > lb.e_cap) {
-                    dfree(lb.E.col);
-                    dfree(lb.E.val);
-                    lb.e_cap = grow_cap(nnz[l], lb.e_cap);
-                    lb.E.col = dalloc<int>(size_t(lb.e_cap));
-                    lb.E.val = dalloc<double>(size_t(lb.e_cap));
-                }
-                erows(c, lb, 1);
+                lb.E.rp = c->e_rp + R.start[l];
+                lb.E.col = c->e_col;
+                lb.E.val = c->e_val;
             }
         }
         // per-level big-block face indices and inverses
@@ -782,14 +792,14 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
             lb.W.orgR = dalloc<int4>(cap);
             lb.W.w = dalloc<double>(size_t(cap) * 64);
             lb.fl_cap = cap * 32;
-            lb.E.rp = dalloc<int>(size_t(lb.fl_cap) + 1);
-            lb.ecnt = dalloc<int>(size_t(lb.fl_cap) + 1);
         }
         // batched face lists of all levels (views per level)
         const size_t ftot = size_t(cap) * 32 * c->nlev;
         c->fl_face = dalloc<int>(ftot);
         c->fl_off = dalloc<int>(ftot + 1);
         c->fl_ent = dalloc<int>(ftot);
+        c->e_cnt = dalloc<int>(ftot + 1);
+        c->e_rp = dalloc<int>(ftot + 1);
         size_t scap = std::max<size_t>(ftot + 1, size_t(c->prm.N / 4) * (c->prm.N / 4));
         c->keys = dalloc<int>(scap);
         c->vals = dalloc<int>(scap);
@@ -1213,6 +1223,7 @@ void ibmg_destroy(ibmg_ctx* c) {
     dfree(c->Acoarse);
     if (c->cub_tmp) cudaFree(c->cub_tmp);
     if (c->hpin) cudaFreeHost(c->hpin);
+    if (c->hpin_i) cudaFreeHost(c->hpin_i);
     for (auto& r : c->prof_pending) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -1450,12 +1461,12 @@ long ibmg_elasticity_triplets(ibmg_ctx* c, int level, int* rows, int* cols, doub
         std::vector<int> rp(nf + 1), face(nf);
         CK(cudaMemcpy(rp.data(), lb.E.rp, sizeof(int) * (nf + 1), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(face.data(), lb.FL.face, sizeof(int) * nf, cudaMemcpyDeviceToHost));
-        const long nnz = rp[nf];
+        const long r0 = rp[0], nnz = rp[nf] - r0;  // positions in the all-level arrays
         if (!rows || cap < nnz) return nnz;
-        CK(cudaMemcpy(cols, lb.E.col, sizeof(int) * nnz, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(vals, lb.E.val, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cols, lb.E.col + r0, sizeof(int) * nnz, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals, lb.E.val + r0, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
         for (int q = 0; q < nf; ++q)
-            for (int e = rp[q]; e < rp[q + 1]; ++e) rows[e] = face[q];
+            for (int e = rp[q]; e < rp[q + 1]; ++e) rows[e - r0] = face[q];
         return nnz;
     } catch (const std::exception& e) {
         fail(c, e, -1);
