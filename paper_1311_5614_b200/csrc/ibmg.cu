@@ -96,11 +96,9 @@ struct LevelBuf {
     int* bq = nullptr;
     // per-block slabs (inverse + encoded E' rows) and big-tile lists
     int* sl_rp = nullptr;
-    int* sl_off = nullptr;
-    int blk_slab_cap = 0;
+    int* sl_off = nullptr;      // views into the all-level slab arrays (ctx)
     int* sl_col = nullptr;
     double* sl_val = nullptr;
-    long sl_cap = 0;
 
     double* Ainv = nullptr;
     int ainv_cap = 0;
@@ -133,6 +131,10 @@ struct ibmg_ctx {
     int *e_cnt = nullptr, *e_rp = nullptr, *e_col = nullptr;       // batched E' rows (all levels)
     double* e_val = nullptr;
     long e_cap = 0;
+    int *sl_off = nullptr, *sl_col = nullptr;  // slabs of all levels' big blocks
+    double* sl_val = nullptr;
+    int slo_cap = 0;
+    long sl_cap = 0;
     int* hpin_i = nullptr;  // pinned int scratch (row counts)
     size_t sort_cap = 0;
     void* cub_tmp = nullptr;
@@ -210,6 +212,7 @@ void prof_collect(ibmg_ctx* c) {
 // list; level 0's slot 31 holds the total run count of the batched face lists
 constexpr int kCtr = 32;
 constexpr int kCtrRuns = 31;
+constexpr int kCtrSlabTot = 30;  // level 0 slot 30: total slab entries of all levels
 
 Lev make_lev(const ibmg_params& p, int n) {
     Lev L;
@@ -310,11 +313,8 @@ void free_structs(ibmg_ctx* c) {
         dfree(lb.rr);
         dfree(lb.Ainv);
         dfree(lb.sl_rp);
-        dfree(lb.sl_off);
-        dfree(lb.sl_col);
-        dfree(lb.sl_val);
-        lb.sl_cap = 0;
-        lb.blk_slab_cap = 0;
+        lb.sl_off = lb.sl_col = nullptr;
+        lb.sl_val = nullptr;
         dfree(lb.pred);
         dfree(lb.poff);
         dfree(lb.flags);
@@ -344,6 +344,11 @@ void free_structs(ibmg_ctx* c) {
     dfree(c->e_col);
     dfree(c->e_val);
     c->e_cap = 0;
+    dfree(c->sl_off);
+    dfree(c->sl_col);
+    dfree(c->sl_val);
+    c->slo_cap = 0;
+    c->sl_cap = 0;
     dfree(c->runs);
     dfree(c->cnt);
     c->sort_cap = 0;
@@ -657,78 +662,90 @@ void rebuild(ibmg_ctx* c) {
                 lb.E.val = c->e_val;
             }
         }
-        // per-level big-block face indices and inverses
+        // big-block E' row ranges, slabs and inverses of every level: one
+        // launch each over the level-major block numbering
+        BSetup S{};
         for (int l = 0; l + 1 < c->nlev; ++l) {
             LevelBuf& lb = c->lev[l];
             if (lb.nbig == 0) continue;
+            if (S.nlev == kBSLevels) throw InvalidArg("too many levels with big blocks");
             if (lb.ainv_cap < lb.nbig) {
                 dfree(lb.Ainv);
                 dfree(lb.rr);
+                dfree(lb.sl_rp);
                 lb.ainv_cap = int(grow_cap(lb.nbig, lb.ainv_cap));
                 lb.Ainv = dalloc<double>(size_t(lb.ainv_cap) * 3136);
                 lb.rr = dalloc<int2>(size_t(lb.ainv_cap) * 40);
-            }
-            LAUNCH(c, k_block_rows, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.FL, lb.E, lb.blk_ids, lb.nbig, lb.rr,
-                   lb.bq);
-            if (lb.sl_off == nullptr || lb.ainv_cap > lb.blk_slab_cap) {
-                dfree(lb.sl_rp);
-                dfree(lb.sl_off);
                 lb.sl_rp = dalloc<int>(size_t(lb.ainv_cap) * 48);
-                lb.sl_off = dalloc<int>(size_t(lb.ainv_cap) + 1);
-                lb.blk_slab_cap = lb.ainv_cap;
             }
-            CK(cudaMemsetAsync(c->cnt, 0, sizeof(int) * (lb.nbig + 1), c->s));
-            LAUNCH(c, k_slab_count, nblk(lb.nbig, 128), 128, 0, lb.nbig, lb.blk_ids, lb.rr, lb.sl_rp, c->cnt,
-                   c->counters + l * kCtr + 19);
-            size_t bytes = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, lb.sl_off, lb.nbig + 1, c->s);
-            ensure_cub(c, bytes);
-            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, lb.sl_off, lb.nbig + 1, c->s));
-            CK(cudaMemcpyAsync(c->counters + l * kCtr + 28, lb.sl_off + lb.nbig, sizeof(int), cudaMemcpyDeviceToDevice,
-                               c->s));
+            const int k = S.nlev++;
+            S.lev[k] = l;
+            S.L[k] = lb.L;
+            S.FL[k] = lb.FL;
+            S.E[k] = lb.E;
+            S.blk_ids[k] = lb.blk_ids;
+            S.rr[k] = lb.rr;
+            S.bq[k] = lb.bq;
+            S.sl_rp[k] = lb.sl_rp;
+            S.start[k + 1] = S.start[k] + lb.nbig;
         }
-        {
+        const int nball = S.start[S.nlev];
+        if (nball) {
+            if (c->slo_cap < nball + 1) {
+                dfree(c->sl_off);
+                c->slo_cap = int(grow_cap(nball + 1, c->slo_cap));
+                c->sl_off = dalloc<int>(size_t(c->slo_cap));
+            }
+            LAUNCH(c, k_block_rows, nblk(size_t(nball) * 40), 256, 0, S);
+            CK(cudaMemsetAsync(c->cnt + nball, 0, sizeof(int), c->s));
+            LAUNCH(c, k_slab_count, nblk(nball, 128), 128, 0, S, c->cnt, c->counters, kCtr);
+            size_t bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, c->sl_off, nball + 1, c->s);
+            ensure_cub(c, bytes);
+            CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, c->sl_off, nball + 1, c->s));
+            CK(cudaMemcpyAsync(c->counters + kCtrSlabTot, c->sl_off + nball, sizeof(int), cudaMemcpyDeviceToDevice,
+                               c->s));
             // all levels' box inverses in one launch (each CTA is a latency-bound
             // 56-step Gauss-Jordan; one launch overlaps the levels)
             BInvLevels BL{};
-            int tot = 0;
-            for (int l = 0; l + 1 < c->nlev; ++l) {
-                LevelBuf& lb = c->lev[l];
-                if (lb.nbig == 0) continue;
-                const int k = BL.nlev++;
+            for (int k = 0; k < S.nlev; ++k) {
+                const LevelBuf& lb = c->lev[S.lev[k]];
                 BL.L[k] = lb.L;
                 BL.E[k] = lb.E;
                 BL.blk_ids[k] = lb.blk_ids;
                 BL.rr[k] = lb.rr;
                 BL.Ainv[k] = lb.Ainv;
-                BL.start[k] = tot;
-                tot += lb.nbig;
+                BL.start[k] = S.start[k];
             }
-            BL.start[BL.nlev] = tot;
-            if (tot) LAUNCH(c, k_block_inverse, tot, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
-        }
-        {
-            std::vector<int> hc(size_t(c->nlev) * kCtr);
-            CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
+            BL.nlev = S.nlev;
+            BL.start[S.nlev] = nball;
+            LAUNCH(c, k_block_inverse, nball, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
+            std::vector<int> hc2(size_t(c->nlev) * kCtr);
+            CK(cudaMemcpyAsync(hc2.data(), c->counters, sizeof(int) * hc2.size(), cudaMemcpyDeviceToHost, c->s));
             tr.mark("launched inverses");
             CK(cudaStreamSynchronize(c->s));
             tr.mark("synced slab sizes");
-            for (int l = 0; l + 1 < c->nlev; ++l) {
-                LevelBuf& lb = c->lev[l];
-                if (lb.nbig == 0) continue;
-                const int* h = &hc[size_t(l) * kCtr];
-                if (h[19] > kSlabCap)
-                    throw InvalidArg("E' rows of a big block exceed the shared-memory slab (" + std::to_string(h[19]) +
-                                     " > " + std::to_string(kSlabCap) + " entries) on level " + std::to_string(l));
-                if (h[28] > lb.sl_cap) {
-                    dfree(lb.sl_col);
-                    dfree(lb.sl_val);
-                    lb.sl_cap = grow_cap(h[28], lb.sl_cap);
-                    lb.sl_col = dalloc<int>(size_t(lb.sl_cap));
-                    lb.sl_val = dalloc<double>(size_t(lb.sl_cap));
-                }
-                LAUNCH(c, k_slab_fill, nblk(size_t(lb.nbig) * 40), 256, 0, lb.L, lb.nbig, lb.blk_ids, lb.rr, lb.E,
-                       lb.sl_off, lb.sl_rp, lb.sl_col, lb.sl_val, 0);
+            for (int k = 0; k < S.nlev; ++k) {
+                const int mx = hc2[size_t(S.lev[k]) * kCtr + 19];
+                if (mx > kSlabCap)
+                    throw InvalidArg("E' rows of a big block exceed the shared-memory slab (" + std::to_string(mx) +
+                                     " > " + std::to_string(kSlabCap) + " entries) on level " +
+                                     std::to_string(S.lev[k]));
+            }
+            const long stot = hc2[kCtrSlabTot];
+            if (stot > c->sl_cap) {
+                dfree(c->sl_col);
+                dfree(c->sl_val);
+                c->sl_cap = grow_cap(stot, c->sl_cap);
+                c->sl_col = dalloc<int>(size_t(c->sl_cap));
+                c->sl_val = dalloc<double>(size_t(c->sl_cap));
+            }
+            LAUNCH(c, k_slab_fill, nblk(size_t(nball) * 40), 256, 0, S, c->sl_off, c->sl_col, c->sl_val);
+            for (int k = 0; k < S.nlev; ++k) {
+                LevelBuf& lb = c->lev[S.lev[k]];
+                lb.sl_off = c->sl_off + S.start[k];
+                lb.sl_col = c->sl_col;
+                lb.sl_val = c->sl_val;
             }
         }
     }

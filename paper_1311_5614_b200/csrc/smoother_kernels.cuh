@@ -832,13 +832,38 @@ __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict_
 
 // E' row range (begin, end) of each of the 40 velocity DOFs of every big block
 // ((0, 0) if the face has no E' row), and the block -> list position map bq.
-__global__ void k_block_rows(Lev L, FaceList FL, EMat E, const int* __restrict__ blk_ids, int nbig,
-                             int2* __restrict__ rr, int* __restrict__ bq) {
+// Big-block setup for every level with big blocks in one launch each
+// (DESIGN.md §3.4): blocks are numbered level-major, start[] the prefix.
+constexpr int kBSLevels = 16;
+struct BSetup {
+    int nlev;
+    int lev[kBSLevels];  // level index (counters)
+    Lev L[kBSLevels];
+    FaceList FL[kBSLevels];
+    EMat E[kBSLevels];
+    const int* blk_ids[kBSLevels];
+    int2* rr[kBSLevels];
+    int* bq[kBSLevels];
+    int* sl_rp[kBSLevels];
+    int start[kBSLevels + 1];
+};
+__device__ __forceinline__ int bs_level(const BSetup& S, int qg) {
+    int k = 0;
+    while (qg >= S.start[k + 1]) ++k;
+    return k;
+}
+
+// E' row ranges of the 40 velocity DOFs of every block (binary search of the
+// face list; (0, 0) for faces without an E' row).
+__global__ void k_block_rows(BSetup S) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nbig * 40) return;
-    const int q = idx / 40, t = idx % 40, n = L.n, nbk = n >> 2;
-    const int B = blk_ids[q];
-    if (t == 0) bq[B] = q;
+    if (idx >= S.start[S.nlev] * 40) return;
+    const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
+    const Lev& L = S.L[k];
+    const FaceList& FL = S.FL[k];
+    const int n = L.n, nbk = n >> 2;
+    const int B = S.blk_ids[k][q];
+    if (t == 0) S.bq[k][B] = q;
     int f, i, j;
     block_dof(t, 4 * (B % nbk), 4 * (B / nbk), f, i, j);
     const int key = f * L.nn + wr(i, n) + wr(j, n) * n;
@@ -847,17 +872,18 @@ __global__ void k_block_rows(Lev L, FaceList FL, EMat E, const int* __restrict__
         const int mid = (lo + hi) >> 1;
         if (FL.face[mid] < key) lo = mid + 1; else hi = mid;
     }
-    rr[idx] = (lo < FL.nf && FL.face[lo] == key) ? make_int2(E.rp[lo], E.rp[lo + 1]) : make_int2(0, 0);
+    S.rr[k][(size_t)q * 40 + t] =
+        (lo < FL.nf && FL.face[lo] == key) ? make_int2(S.E[k].rp[lo], S.E[k].rp[lo + 1]) : make_int2(0, 0);
 }
 
-// Slab packing (setup): row pointers + padded entry counts, then the entries
-// with pre-encoded columns.  tile_mode: columns inside the 20x20 region of the
-// block's 16x16 tile become shared-memory indices comp*400 + lj*20 + li, others
-// -(flat+1); otherwise (single-CTA coarse levels) the flat index itself.
-__global__ void k_slab_count(int nbig, const int* __restrict__ blk_ids, const int2* __restrict__ rr,
-                             int* __restrict__ rp, int* __restrict__ cnt, int* __restrict__ maxcnt) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nbig) return;
+// Slab packing: row pointers + padded entry counts (cnt, level-major), the
+// owner block id in rp[47]; the longest slab per level into counter 19.
+__global__ void k_slab_count(BSetup S, int* __restrict__ cnt, int* __restrict__ counters, int ctr_stride) {
+    const int qg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qg >= S.start[S.nlev]) return;
+    const int k = bs_level(S, qg), q = qg - S.start[k];
+    const int2* rr = S.rr[k];
+    int* rp = S.sl_rp[k];
     int rel = 0;
     for (int t = 0; t < 40; ++t) {
         rp[(size_t)q * 48 + t] = rel;
@@ -865,43 +891,23 @@ __global__ void k_slab_count(int nbig, const int* __restrict__ blk_ids, const in
         rel += r.y - r.x;
     }
     for (int t = 40; t < 47; ++t) rp[(size_t)q * 48 + t] = rel;
-    rp[(size_t)q * 48 + 47] = blk_ids[q];  // owner block id (used by the coarse kernel)
-    cnt[q] = (rel + 3) & ~3;
-    atomicMax(maxcnt, rel);
+    rp[(size_t)q * 48 + 47] = S.blk_ids[k][q];  // owner block id (used by the coarse kernel)
+    cnt[qg] = (rel + 3) & ~3;
+    atomicMax(counters + S.lev[k] * ctr_stride + 19, rel);
 }
 
-__global__ void k_slab_fill(Lev L, int nbig, const int* __restrict__ blk_ids, const int2* __restrict__ rr, EMat E,
-                            const int* __restrict__ off, const int* __restrict__ rp, int* __restrict__ col,
-                            double* __restrict__ val, int tile_mode) {
+// The entries, at off[qg] (level-major offsets), columns as flat indices.
+__global__ void k_slab_fill(BSetup S, const int* __restrict__ off, int* __restrict__ col, double* __restrict__ val) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nbig * 40) return;
-    const int q = idx / 40, t = idx % 40, n = L.n, nn = L.nn, nbk = n >> 2;
-    const int B = blk_ids[q];
-    const int x0 = ((B % nbk) >> 2) * 16, y0 = ((B / nbk) >> 2) * 16;
-    const int2 r = rr[idx];
-    int o = off[q] + rp[(size_t)q * 48 + t];
+    if (idx >= S.start[S.nlev] * 40) return;
+    const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
+    const int2 r = S.rr[k][idx - S.start[k] * 40];
+    const EMat& E = S.E[k];
+    int o = off[qg] + S.sl_rp[k][(size_t)q * 48 + t];
     for (int e = r.x; e < r.y; ++e, ++o) {
-        const int c = E.col[e];
-        int enc = c;
-        if (tile_mode) {
-            const int comp = c >= nn, f = c - comp * nn;
-            const int li = wr((f & (n - 1)) - x0 + 2, n), lj = wr(f / n - y0 + 2, n);
-            enc = (li < kReg && lj < kReg) ? comp * kReg * kReg + lj * kReg + li : -(c + 1);
-        }
-        col[o] = enc;
+        col[o] = E.col[e];
         val[o] = E.val[e];
     }
-}
-
-// Block sort keys: colour (bx mod 4) + 4 (by mod 4) for big blocks, 16 otherwise.
-__global__ void k_block_keys(int nbk, const uint8_t* __restrict__ big, int* keys, int* vals, int* counts) {
-    const int B = blockIdx.x * blockDim.x + threadIdx.x;
-    if (B >= nbk * nbk) return;
-    const int bx = B % nbk, by = B / nbk;
-    const int key = big[B] ? (bx & 3) + 4 * (by & 3) : 16;
-    keys[B] = key;
-    vals[B] = B;
-    atomicAdd(&counts[key], 1);
 }
 
 }  // namespace ibmg
