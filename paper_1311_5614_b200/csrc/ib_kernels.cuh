@@ -176,11 +176,25 @@ __global__ void k_face_levels(const unsigned* __restrict__ ukeys, const int* __r
     }
 }
 
+// Per-level block arrays (flags, conflict masks) of the levels with big
+// blocks, contiguous and level-major: level l's blocks start at boff[l].
+struct BlkLevels {
+    int nlev;  // levels 0 .. nlev-1 (all but the coarsest)
+    int n[20];
+    int boff[21];
+};
+
 // Big-block marking: a 4x4 block is big when any face of it
 // lies in the support of any point's left or right window on the level.
-__global__ void k_mark_big(int npts, Win W, int n, uint8_t* flags) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= npts * 64) return;
+// Thread per (level, point, window slot, tap).
+__global__ void k_mark_big(int npts, WinLevels WL, BlkLevels BK, uint8_t* __restrict__ flags_all) {
+    const long per = (long)npts * 64;
+    const long qq = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (qq >= per * BK.nlev) return;
+    const int l = int(qq / per), q = int(qq - l * per);
+    const Win& W = WL.win[l];
+    const int n = BK.n[l];
+    uint8_t* flags = flags_all + BK.boff[l];
     const int k = q >> 6, s = (q >> 4) & 3, e = q & 15;
     if (W.w[(size_t)k * 64 + s * 16 + e] == 0.0) return;
     const int4 o = (s < 2) ? W.orgL[k] : W.orgR[k];
@@ -239,9 +253,15 @@ __device__ __forceinline__ int canon_off(int d, int nbk) { return wr(d + nbk / 2
 //  * the E' reach: the extent (face index units) of the union of the L_k and
 //    R_{k-1}, R_k, R_{k+1} supports, max into *reach (same-colour blocks are
 //    >= 8 cells apart only when it is <= 7, checked at setup).
-__global__ void k_block_pairs(int npts, Win W, Pts P, int n, unsigned* __restrict__ mask, int* __restrict__ reach) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= npts * 2) return;
+__global__ void k_block_pairs(int npts, WinLevels WL, BlkLevels BK, Pts P, unsigned* __restrict__ mask_all,
+                              int* __restrict__ counters, int ctr_stride) {
+    const int qq = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qq >= npts * 2 * BK.nlev) return;
+    const int l = qq / (npts * 2), q = qq - l * npts * 2;
+    const Win& W = WL.win[l];
+    const int n = BK.n[l];
+    unsigned* mask = mask_all + BK.boff[l];
+    int* reach = counters + l * ctr_stride + 18;
     const int k = q >> 1, comp = q & 1, nbk = n >> 2;
     int lo_i = 1 << 30, hi_i = -(1 << 30), lo_j = 1 << 30, hi_j = -(1 << 30);
     const WinSupport Ls = window_support(W, k, comp, lo_i, hi_i, lo_j, hi_j);
@@ -273,10 +293,14 @@ __global__ void k_block_pairs(int npts, Win W, Pts P, int n, unsigned* __restric
 // B = A + (dx, dy) (periodic) is big, is not A itself, and conflicts with A —
 // canonical Chebyshev offset 1, or 2 with the pair bit set — and bit 12
 // (the zero offset) marking A big; 0 for blocks that are not big.
-__global__ void k_block_conflicts(int n, const uint8_t* __restrict__ big, unsigned* __restrict__ mask) {
-    const int nbk = n >> 2;
-    const int A = blockIdx.x * blockDim.x + threadIdx.x;
-    if (A >= nbk * nbk) return;
+__global__ void k_block_conflicts(BlkLevels BK, const uint8_t* __restrict__ big_all, unsigned* __restrict__ mask_all) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= BK.boff[BK.nlev]) return;
+    int l = 0;
+    while (g >= BK.boff[l + 1]) ++l;
+    const int nbk = BK.n[l] >> 2, A = g - BK.boff[l];
+    const uint8_t* big = big_all + BK.boff[l];
+    unsigned* mask = mask_all + BK.boff[l];
     if (!big[A]) {
         mask[A] = 0u;
         return;

@@ -77,7 +77,7 @@ struct LevelBuf {
     int fl_cap = 0;
     EMat E{};
     int maxrow = 0;          // longest face list (selects the E'-row assembly kernel)
-    uint8_t* big = nullptr;
+    uint8_t* big = nullptr;     // views into the ctx's all-level block arrays
     unsigned* cmask = nullptr;  // length-2 conflict bits per block (k_block_pairs)
     int nbig = 0;
     int* blk_ids = nullptr;  // big blocks sorted by colour, ascending id within
@@ -128,6 +128,10 @@ struct ibmg_ctx {
     // setup scratch
     int *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *vals2 = nullptr, *runs = nullptr, *cnt = nullptr;
     int *fl_face = nullptr, *fl_off = nullptr, *fl_ent = nullptr;  // batched face lists (all levels)
+    BlkLevels blk_levels{};                                        // block-array layout (all but coarsest)
+    uint8_t* big_all = nullptr;
+    unsigned* cmask_all = nullptr;
+    unsigned* h_cm_all = nullptr;  // pinned
     int *e_cnt = nullptr, *e_rp = nullptr, *e_col = nullptr;       // batched E' rows (all levels)
     double* e_val = nullptr;
     long e_cap = 0;
@@ -249,9 +253,7 @@ void alloc_levels(ibmg_ctx* c) {
         lb.b = dalloc<double>(m);
         lb.r = dalloc<double>(m);
         if (n > p.coarsest_n) {
-            lb.big = dalloc<uint8_t>(size_t(n / 4) * (n / 4));
-            lb.cmask = dalloc<unsigned>(size_t(n / 4) * (n / 4));
-            CK(cudaMallocHost(&lb.h_cm, sizeof(unsigned) * (n / 4) * (n / 4)));
+
             lb.bq = dalloc<int>(size_t(n / 4) * (n / 4));
             if (n >= 4 * kTile) {
                 lb.tflags = dalloc<unsigned>(size_t(n / kTile) * (n / kTile));
@@ -262,6 +264,23 @@ void alloc_levels(ibmg_ctx* c) {
         if (n <= p.coarsest_n) break;
     }
     c->nlev = int(c->lev.size());
+    // block flags / conflict masks of the levels with big blocks, contiguous
+    BlkLevels& BK = c->blk_levels;
+    BK.nlev = c->nlev - 1;
+    for (int l = 0; l < BK.nlev; ++l) {
+        const int nbk = c->lev[l].L.n / 4;
+        BK.n[l] = c->lev[l].L.n;
+        BK.boff[l + 1] = BK.boff[l] + nbk * nbk;
+    }
+    const size_t nb = std::max(size_t(BK.boff[BK.nlev]), size_t(1));
+    c->big_all = dalloc<uint8_t>(nb);
+    c->cmask_all = dalloc<unsigned>(nb);
+    CK(cudaMallocHost(&c->h_cm_all, sizeof(unsigned) * nb));
+    for (int l = 0; l < BK.nlev; ++l) {
+        c->lev[l].big = c->big_all + BK.boff[l];
+        c->lev[l].cmask = c->cmask_all + BK.boff[l];
+        c->lev[l].h_cm = c->h_cm_all + BK.boff[l];
+    }
     c->lc = 0;
     while (c->lev[c->lc].L.n > kCoarseMaxN) ++c->lc;
     static_assert(kCoarseMaxN == 2 * kTile, "multi-tile kernels run the levels n >= 64");
@@ -576,24 +595,20 @@ void rebuild(ibmg_ctx* c) {
             c->launches += 2;  // account the CUB launches coarsely (sort+rle+scan)
         }
         // big-block marking, colour sort, reach
-        for (int l = 0; l + 1 < c->nlev; ++l) {
-            LevelBuf& lb = c->lev[l];
-            const int nbk = lb.L.n / 4;
-            CK(cudaMemsetAsync(lb.big, 0, size_t(nbk) * nbk, c->s));
-            LAUNCH(c, k_mark_big, nblk(size_t(npts) * 64), 256, 0, npts, lb.W, lb.L.n, lb.big);
-            CK(cudaMemsetAsync(lb.cmask, 0, sizeof(unsigned) * nbk * nbk, c->s));
-            LAUNCH(c, k_block_pairs, nblk(size_t(npts) * 2, 128), 128, 0, npts, lb.W, c->P, lb.L.n, lb.cmask,
-                   c->counters + l * kCtr + 18);
-            LAUNCH(c, k_block_conflicts, nblk(size_t(nbk) * nbk), 256, 0, lb.L.n, lb.big, lb.cmask);
+        {
+            const BlkLevels& BK = c->blk_levels;
+            const size_t nb = size_t(BK.boff[BK.nlev]);
+            CK(cudaMemsetAsync(c->big_all, 0, nb, c->s));
+            CK(cudaMemsetAsync(c->cmask_all, 0, sizeof(unsigned) * nb, c->s));
+            LAUNCH(c, k_mark_big, nblk(size_t(npts) * 64 * BK.nlev), 256, 0, npts, WL, BK, c->big_all);
+            LAUNCH(c, k_block_pairs, nblk(size_t(npts) * 2 * BK.nlev, 128), 128, 0, npts, WL, BK, c->P, c->cmask_all,
+                   c->counters, kCtr);
+            LAUNCH(c, k_block_conflicts, nblk(nb), 256, 0, BK, c->big_all, c->cmask_all);
+            // conflict masks (big flag in bit 12) of every level in one copy
+            CK(cudaMemcpyAsync(c->h_cm_all, c->cmask_all, sizeof(unsigned) * nb, cudaMemcpyDeviceToHost, c->s));
         }
         std::vector<int> hc(size_t(c->nlev) * kCtr);
         CK(cudaMemcpyAsync(hc.data(), c->counters, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost, c->s));
-        // conflict masks (big flag in bit 12) of every level in the same round trip
-        for (int l = 0; l + 1 < c->nlev; ++l) {
-            const int nbk = c->lev[l].L.n / 4;
-            CK(cudaMemcpyAsync(c->lev[l].h_cm, c->lev[l].cmask, sizeof(unsigned) * nbk * nbk, cudaMemcpyDeviceToHost,
-                               c->s));
-        }
         tr.mark("launched marks");
         CK(cudaStreamSynchronize(c->s));
         tr.mark("synced marks");
@@ -1216,9 +1231,7 @@ void ibmg_destroy(ibmg_ctx* c) {
         dfree(lb.w);
         dfree(lb.b);
         dfree(lb.r);
-        dfree(lb.big);
-        dfree(lb.cmask);
-        if (lb.h_cm) cudaFreeHost(lb.h_cm);
+
         dfree(lb.bq);
         dfree(lb.tflags);
     }
@@ -1232,6 +1245,9 @@ void ibmg_destroy(ibmg_ctx* c) {
     dfree(c->stage_b);
     dfree(c->partial);
     dfree(c->ticket);
+    dfree(c->big_all);
+    dfree(c->cmask_all);
+    if (c->h_cm_all) cudaFreeHost(c->h_cm_all);
     dfree(c->tail_cnt);
     dfree(c->dh);
     dfree(c->ones);
