@@ -210,20 +210,23 @@ template <class WA, class LocA, class GlobA, class BA, class WAdd>
 __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slot, int bi, int bj, const WA& W,
                                                const LocA& wloc, const GlobA& wglob, const BA& Bv, WAdd&& wadd,
                                                BigScratch& S, int gt, unsigned long long* dbg = nullptr) {
+    // stencil row and E' row dots are computed into registers first and
+    // stored after both, so their global gathers are in flight together (one
+    // L2 round trip for the residual instead of two)
+    double sres = 0.0, wcur = 0.0, s0 = 0.0;
     if (gt < 56) {
         int f, i, j;
         block_dof(gt, bi, bj, f, i, j);
         i = wr(i, L.n);
         j = wr(j, L.n);
-        S.sr[gt] = Bv(f, i, j) - stokes_row(L, W, f, i, j);
-        S.wold[gt] = W(f, i, j);  // current value, reused for the correction (no re-read)
+        sres = Bv(f, i, j) - stokes_row(L, W, f, i, j);
+        wcur = W(f, i, j);  // current value, reused for the correction (no re-read)
     }
-    // E' row dots: 3 threads per row (strided entries), the column gathers
-    // batched 8 at a time (independent loads in flight), fixed-order combine
+    // E' row dots: 3 threads per row (strided entries), up to 24 column
+    // gathers in flight per thread, fixed-order combine
     if (gt < 120) {
         const int r = gt % 40, p = gt / 40;
         const int e1 = slot.rp[r + 1];
-        double s0 = 0.0;
         for (int e = slot.rp[r] + p; e < e1; e += 72) {  // one round of up to 24 gathers per thread
             int cc[24];
             double vv[24], xx[24];
@@ -239,8 +242,12 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
 #pragma unroll
             for (int m = 0; m < 24; ++m) s0 += vv[m] * xx[m];
         }
-        S.epart[p][r] = s0;
     }
+    if (gt < 56) {
+        S.sr[gt] = sres;
+        S.wold[gt] = wcur;
+    }
+    if (gt < 120) S.epart[gt / 40][gt % 40] = s0;
     if (dbg && gt == 0) dbg[0] = gtimer();
     __syncthreads();
     if (dbg && gt == 0) dbg[1] = gtimer();
