@@ -32,6 +32,7 @@ struct CoarseArgs {
     const double* Acoarse;   // bordered inverse, col-major (3nn+1)^2
     const double* b_in;
     double* w_out;
+    double* w_fine;  // optional: w of the next finer level (n = 2 * lv[0].L.n) += P w_out
 };
 
 struct SW {
@@ -210,6 +211,17 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
         for (int s = 0; s < A.nu2; ++s) coarse_sweep(C, wl[l], bl[l], slot, S, A.trace, nm);
     }
     for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) A.w_out[q] = wl[0][q];
+    if (A.w_fine) {  // prolongation-add to the finer level (K3) from shared memory
+        const int nf = 2 * A.lv[0].L.n, nnf = nf * nf;
+        SW E{wl[0], A.lv[0].L.n, A.lv[0].L.nn};
+        for (int q = t; q < nnf; q += nt) {
+            double du, dv, dp;
+            prolong_rows(nf, E, q % nf, q / nf, du, dv, dp);
+            A.w_fine[q] += du;
+            A.w_fine[nnf + q] += dv;
+            A.w_fine[2 * nnf + q] += dp;
+        }
+    }
     cmark(A.trace, nm);
 }
 

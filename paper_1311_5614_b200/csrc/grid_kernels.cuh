@@ -155,9 +155,15 @@ __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const dou
 // restricted residual, R E' w = sum_k L^{l+1}_k F_k, is added afterwards by
 // k_face_gather on the coarse face list.
 __device__ __forceinline__ void residual_restrict_cell(const Lev& F, const double* __restrict__ b,
-                                                       const double* __restrict__ w, double* __restrict__ bc, int q) {
+                                                       const double* __restrict__ w, double* __restrict__ bc,
+                                                       double* __restrict__ wc_zero, int q) {
     const int nc = F.n >> 1, nnc = nc * nc;
     if (q >= nnc) return;
+    if (wc_zero) {  // the coarse level's zero initial guess, in the same pass
+        wc_zero[q] = 0.0;
+        wc_zero[nnc + q] = 0.0;
+        wc_zero[2 * nnc + q] = 0.0;
+    }
     const int I = q % nc, J = q / nc;
     const int i = 2 * I, j = 2 * J, n = F.n, nn = F.nn;
     GAcc acc{w, n, nn};
@@ -190,8 +196,10 @@ __device__ __forceinline__ void residual_restrict_cell(const Lev& F, const doubl
 }
 
 __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
-                                    double* __restrict__ bc, PForce pf, Gather G, int ngrid) {
-    fused_launch(pf, G, ngrid, [&](int blk) { residual_restrict_cell(F, b, w, bc, blk * blockDim.x + threadIdx.x); });
+                                    double* __restrict__ bc, double* __restrict__ wc_zero, PForce pf, Gather G,
+                                    int ngrid) {
+    fused_launch(pf, G, ngrid,
+                 [&](int blk) { residual_restrict_cell(F, b, w, bc, wc_zero, blk * blockDim.x + threadIdx.x); });
 }
 
 // Plain restriction of a vector (ibmg_restrict).
@@ -392,11 +400,15 @@ __global__ void k_multi_axpy_add(const double* __restrict__ Z, size_t stride, in
 }
 
 // dst = src * (1 / sqrt(*nrm2))  or  src / scalar when nrm2 == nullptr
+// dst = src / s (s = sqrt(*nrm2) or scalar); zero[] (optional, same length)
+// is cleared in the same pass (the next V-cycle's zero initial guess).
 __global__ void k_scale_by_norm(const double* __restrict__ src, double* __restrict__ dst, size_t m,
-                                const double* __restrict__ nrm2, double scalar) {
+                                const double* __restrict__ nrm2, double scalar, double* __restrict__ zero) {
     const double s = nrm2 ? sqrt(*nrm2) : scalar;
-    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
         dst[q] = src[q] / s;
+        if (zero) zero[q] = 0.0;
+    }
 }
 
 // p -= mean(p)  (project_pressure_mean, fields.cpp:78-85); sum precomputed in *sum.

@@ -934,7 +934,7 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     ++c->launches;
 }
 
-CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
+CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out, double* w_fine = nullptr) {
     CoarseArgs A{};
     A.nl = c->nlev - c->lc;
     A.nu1 = c->prm.nu1;
@@ -954,6 +954,7 @@ CoarseArgs coarse_args(ibmg_ctx* c, const double* b_in, double* w_out) {
     A.Acoarse = c->Acoarse;
     A.b_in = b_in;
     A.w_out = w_out;
+    A.w_fine = w_fine;
     return A;
 }
 
@@ -964,8 +965,8 @@ size_t coarse_smem(ibmg_ctx* c) {
     return (kCoarseThreads / kGroup) * sizeof(ESlot) + d * sizeof(double);
 }
 
-void coarse_cycle(ibmg_ctx* c, const double* b, double* w) {
-    CoarseArgs A = coarse_args(c, b, w);
+void coarse_cycle(ibmg_ctx* c, const double* b, double* w, double* w_fine = nullptr) {
+    CoarseArgs A = coarse_args(c, b, w, w_fine);
     LAUNCH(c, k_coarse_cycle, 1, kCoarseThreads, coarse_smem(c), A);
 }
 
@@ -982,7 +983,7 @@ void pressure_mean_zero(ibmg_ctx* c, double* x) {
 // constant pressure is in the null space of the periodic operator, so the
 // mean is removed once from the solution instead (oracle
 // vcycle).
-void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true) {
+void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z_zeroed = false) {
     if (c->lc == 0) {
         coarse_cycle(c, b, z);
     } else {
@@ -990,20 +991,24 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true) {
         if (alias) CK(cudaMemcpyAsync(c->lev[0].b, b, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
         auto bl = [&](int l) -> const double* { return l == 0 && !alias ? b : c->lev[l].b; };
         auto wl = [&](int l) -> double* { return l == 0 ? z : c->lev[l].w; };
+        // zero initial guesses: level 0 by the caller (z_zeroed) or here, the
+        // coarser levels inside the residual-restriction pass above them
+        if (!z_zeroed) CK(cudaMemsetAsync(z, 0, sizeof(double) * c->M, c->s));
         for (int l = 0; l < c->lc; ++l) {
             LevelBuf& lb = c->lev[l];
             LevelBuf& nx = c->lev[l + 1];
-            CK(cudaMemsetAsync(wl(l), 0, sizeof(double) * 3 * lb.L.nn, c->s));
             for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
             const PForce pf = pforce(c, lb, wl(l), nx.FL.nf > 0);
             const int ng = int(nblk(nx.L.nn));
             const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
-            LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, bl(l), wl(l), nx.b, pf, G, ng);
+            LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, bl(l), wl(l), nx.b, wl(l + 1), pf, G,
+                   ng);
         }
-        coarse_cycle(c, c->lev[c->lc].b, wl(c->lc));
+        // the coarse kernel also prolongs its correction into level lc-1
+        coarse_cycle(c, c->lev[c->lc].b, wl(c->lc), wl(c->lc - 1));
         for (int l = c->lc - 1; l >= 0; --l) {
             LevelBuf& lb = c->lev[l];
-            LAUNCH(c, k_prolong_add, nblk(lb.L.nn), 256, 0, lb.L.n, wl(l + 1), wl(l));
+            if (l < c->lc - 1) LAUNCH(c, k_prolong_add, nblk(lb.L.nn), 256, 0, lb.L.n, wl(l + 1), wl(l));
             for (int s = 0; s < c->prm.nu2; ++s) sweep_level(c, l, bl(l), wl(l));
         }
     }
@@ -1066,14 +1071,14 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
     const double* r = b;
     int it = 0, restarts = 0;
     while (true) {
-        LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, nullptr, beta);
+        LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, nullptr, beta, c->Z);
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = beta;
         int kdim = 0;
         for (int j = 0; j < m; ++j) {
             double* Vj = c->V + c->Mst * j;
             double* Zj = c->Z + c->Mst * j;
-            vcycle(c, Vj, Zj, false);
+            vcycle(c, Vj, Zj, false, true);
             apply_level(c, 0, Zj, c->wv);
             // CGS2 in three fused sweeps: h1 = V^T w | w -= V h1, h2 = V^T w | w -= V h2, ||w||^2
             cgs_sweep(c, 0, j + 1, nullptr, c->wv, hoff);
@@ -1101,7 +1106,8 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
             kdim = j + 1;
             if (!std::isfinite(g[j + 1])) throw CudaError("FGMRES: non-finite residual estimate");
             if (std::fabs(g[j + 1]) <= tol || it >= c->prm.max_iters || hnext == 0.0) break;
-            LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + c->Mst * (j + 1), M, nullptr, hnext);
+            LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + c->Mst * (j + 1), M, nullptr, hnext,
+                   c->Z + c->Mst * (j + 1));
         }
         for (int i = kdim - 1; i >= 0; --i) {
             double s = g[i];
