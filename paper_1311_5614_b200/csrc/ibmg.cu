@@ -148,6 +148,7 @@ struct ibmg_ctx {
     double *V = nullptr, *Z = nullptr, *wv = nullptr, *xv = nullptr, *rv = nullptr, *bv = nullptr;
     double *partial = nullptr, *dh = nullptr, *ones = nullptr, *stage_a = nullptr, *stage_b = nullptr;
     unsigned* ticket = nullptr;  // last-CTA ticket of the fused CGS sweeps
+    cudaEvent_t ev_dots = nullptr;  // FGMRES: the iteration's dots have reached the host
     unsigned long long* tail_cnt = nullptr;  // producer counter of the fused gathers
     unsigned long long tail_base = 0;        // its value after the last enqueued launch
     double* hpin = nullptr;    // pinned host mirror of dh
@@ -300,6 +301,7 @@ void alloc_levels(ibmg_ctx* c) {
     c->stage_a = dalloc<double>(c->M);
     c->stage_b = dalloc<double>(c->M);
     c->partial = dalloc<double>(size_t(std::max(kRedBlocks, kCgsBlocks)) * (m + 2));
+    CK(cudaEventCreateWithFlags(&c->ev_dots, cudaEventDisableTiming));
     c->ticket = dalloc<unsigned>(1);
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     c->tail_cnt = dalloc<unsigned long long>(1);
@@ -983,7 +985,10 @@ void pressure_mean_zero(ibmg_ctx* c, double* x) {
 // constant pressure is in the null space of the periodic operator, so the
 // mean is removed once from the solution instead (oracle
 // vcycle).
-void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z_zeroed = false) {
+// first_sweep_done: the first level-0 pre-smoothing sweep was already
+// launched (vcycle_head, speculatively, by FGMRES).
+void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z_zeroed = false,
+            bool first_sweep_done = false) {
     if (c->lc == 0) {
         coarse_cycle(c, b, z);
     } else {
@@ -997,7 +1002,7 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z
         for (int l = 0; l < c->lc; ++l) {
             LevelBuf& lb = c->lev[l];
             LevelBuf& nx = c->lev[l + 1];
-            for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
+            for (int s = (l == 0 && first_sweep_done) ? 1 : 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
             const PForce pf = pforce(c, lb, wl(l), nx.FL.nf > 0);
             const int ng = int(nblk(nx.L.nn));
             const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
@@ -1013,6 +1018,14 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z
         }
     }
     if (project) pressure_mean_zero(c, z);
+}
+
+// The head of a V-cycle whose level-0 guess z is already zero: the first
+// pre-smoothing sweep.  Returns whether it launched anything.
+bool vcycle_head(ibmg_ctx* c, const double* b, double* z) {
+    if (c->lc == 0 || c->prm.nu1 == 0 || b == z) return false;
+    sweep_level(c, 0, b, z);
+    return true;
 }
 
 // dots[0..k) = V_i . w, written to c->dh + off (accumulate when acc)
@@ -1075,17 +1088,28 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = beta;
         int kdim = 0;
+        bool head_done = false;
         for (int j = 0; j < m; ++j) {
             double* Vj = c->V + c->Mst * j;
             double* Zj = c->Z + c->Mst * j;
-            vcycle(c, Vj, Zj, false, true);
+            vcycle(c, Vj, Zj, false, true, head_done);
             apply_level(c, 0, Zj, c->wv);
             // CGS2 in three fused sweeps: h1 = V^T w | w -= V h1, h2 = V^T w | w -= V h2, ||w||^2
             cgs_sweep(c, 0, j + 1, nullptr, c->wv, hoff);
             cgs_sweep(c, 1, j + 1, c->dh + hoff, c->wv, h2off);
             cgs_sweep(c, 2, j + 1, c->dh + h2off, c->wv, h2off + j + 1);
             CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (2 * (m + 2)), cudaMemcpyDeviceToHost, c->s));
-            CK(cudaStreamSynchronize(c->s));
+            CK(cudaEventRecord(c->ev_dots, c->s));
+            // while the host reads the dots: the next basis vector V_{j+1} =
+            // w / ||w|| (norm on the device) and the first sweep of its V-cycle,
+            // speculatively (discarded if this iteration converges)
+            head_done = false;
+            if (j + 1 < m) {
+                LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + c->Mst * (j + 1), M, c->dh + h2off + j + 1,
+                       0.0, c->Z + c->Mst * (j + 1));
+                head_done = vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1));
+            }
+            CK(cudaEventSynchronize(c->ev_dots));
             for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = c->hpin[hoff + i] + c->hpin[h2off + i];
             const double hnext = std::sqrt(c->hpin[h2off + j + 1]);
             H[size_t(j + 1) * m + j] = hnext;
@@ -1106,8 +1130,6 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
             kdim = j + 1;
             if (!std::isfinite(g[j + 1])) throw CudaError("FGMRES: non-finite residual estimate");
             if (std::fabs(g[j + 1]) <= tol || it >= c->prm.max_iters || hnext == 0.0) break;
-            LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + c->Mst * (j + 1), M, nullptr, hnext,
-                   c->Z + c->Mst * (j + 1));
         }
         for (int i = kdim - 1; i >= 0; --i) {
             double s = g[i];
@@ -1251,6 +1273,7 @@ void ibmg_destroy(ibmg_ctx* c) {
     dfree(c->stage_b);
     dfree(c->partial);
     dfree(c->ticket);
+    if (c->ev_dots) cudaEventDestroy(c->ev_dots);
     dfree(c->big_all);
     dfree(c->cmask_all);
     if (c->h_cm_all) cudaFreeHost(c->h_cm_all);
