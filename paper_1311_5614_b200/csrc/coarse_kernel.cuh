@@ -129,6 +129,7 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
 }
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char dsm[];
     ESlot* slot = reinterpret_cast<ESlot*>(dsm);
     double* sm = reinterpret_cast<double*>(dsm + (kCoarseThreads / kGroup) * sizeof(ESlot));

@@ -61,6 +61,16 @@ struct Pts {
 
 __host__ __device__ __forceinline__ int wr(int i, int n) { return i & (n - 1); }
 
+// Programmatic dependent launch: every kernel of the library is launched with
+// programmatic stream serialization (ibmg.cu launch_k), lets the next kernel
+// in the stream be scheduled at once, and waits for the previous kernel's
+// completion (and memory flush) before touching any data.  The dependent's
+// CTAs are resident when its prerequisite finishes: no launch gap.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 // Enumerate the 56 DOFs of a 4x4 big block at cell origin (bi, bj):
 // u faces (a in 0..4, b in 0..3), v faces (a in 0..3, b in 0..4), p (4x4).
 __device__ __forceinline__ void block_dof(int t, int bi, int bj, int& field, int& i, int& j) {

@@ -121,6 +121,7 @@ __device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, 
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
 __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out, PForce pf, Gather G,
                                int ngrid) {
+    pdl_enter();
     fused_launch(pf, G, ngrid, [&](int b) {
         const int q = b * blockDim.x + threadIdx.x;
         if (q >= L.nn) return;
@@ -137,6 +138,7 @@ __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __re
 // r = b - S w (E' part added by k_face_gather with sign +1).
 __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const double* __restrict__ w,
                                   double* __restrict__ r, PForce pf, Gather G, int ngrid) {
+    pdl_enter();
     fused_launch(pf, G, ngrid, [&](int blk) {
         const int q = blk * blockDim.x + threadIdx.x;
         if (q >= L.nn) return;
@@ -198,12 +200,14 @@ __device__ __forceinline__ void residual_restrict_cell(const Lev& F, const doubl
 __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
                                     double* __restrict__ bc, double* __restrict__ wc_zero, PForce pf, Gather G,
                                     int ngrid) {
+    pdl_enter();
     fused_launch(pf, G, ngrid,
                  [&](int blk) { residual_restrict_cell(F, b, w, bc, wc_zero, blk * blockDim.x + threadIdx.x); });
 }
 
 // Plain restriction of a vector (ibmg_restrict).
 __global__ void k_restrict(int nf, const double* __restrict__ rf, double* __restrict__ rc) {
+    pdl_enter();
     const int nc = nf >> 1, nnc = nc * nc, nnf = nf * nf;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nnc) return;
@@ -251,6 +255,7 @@ __device__ __forceinline__ void prolong_rows(int nf, const Acc& ec, int i, int j
 }
 
 __global__ void k_prolong_add(int nf, const double* __restrict__ ec, double* __restrict__ wf) {
+    pdl_enter();
     const int nnf = nf * nf;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nnf) return;
@@ -277,6 +282,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // (y = blockIdx.y indexes the vector; V vectors are `stride` doubles apart).
 __global__ void k_multidot_partial(const double* __restrict__ V, size_t stride, const double* __restrict__ w,
                                    size_t m, double* __restrict__ partial) {
+    pdl_enter();
     const double* v = V + stride * blockIdx.y;
     double s = 0.0;
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
@@ -294,6 +300,7 @@ __global__ void k_multidot_partial(const double* __restrict__ V, size_t stride, 
 
 // out[y] (+)= sum_x partial[y][x]; mode 0: store, 1: accumulate (CGS2 second pass).
 __global__ void k_finish_dots(const double* __restrict__ partial, int nblk, double* __restrict__ out, int accumulate) {
+    pdl_enter();
     double s = 0.0;
     for (int x = threadIdx.x; x < nblk; x += 32) s += partial[blockIdx.x * nblk + x];
     s = warp_sum(s);
@@ -313,6 +320,7 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
     k_cgs_sweep(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
                 double* __restrict__ w, size_t m, double* __restrict__ partial, double* __restrict__ out,
                 unsigned* __restrict__ ticket) {
+    pdl_enter();
     constexpr int NACC = MODE == 2 ? 1 : KMAX;
     __shared__ double hs[KMAX];
     __shared__ double red[kRedThreads / 32][NACC];
@@ -382,6 +390,7 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
 // w -= sum_{i<k} h[i] V_i   (one pass over w and the V's).
 __global__ void k_multi_axpy_sub(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
                                  double* __restrict__ w, size_t m) {
+    pdl_enter();
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
         double s = w[q];
         for (int i = 0; i < k; ++i) s -= h[i] * V[stride * i + q];
@@ -392,6 +401,7 @@ __global__ void k_multi_axpy_sub(const double* __restrict__ V, size_t stride, in
 // x += sum_{i<k} y[i] Z_i
 __global__ void k_multi_axpy_add(const double* __restrict__ Z, size_t stride, int k, const double* __restrict__ y,
                                  double* __restrict__ x, size_t m) {
+    pdl_enter();
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
         double s = x[q];
         for (int i = 0; i < k; ++i) s += y[i] * Z[stride * i + q];
@@ -404,6 +414,7 @@ __global__ void k_multi_axpy_add(const double* __restrict__ Z, size_t stride, in
 // is cleared in the same pass (the next V-cycle's zero initial guess).
 __global__ void k_scale_by_norm(const double* __restrict__ src, double* __restrict__ dst, size_t m,
                                 const double* __restrict__ nrm2, double scalar, double* __restrict__ zero) {
+    pdl_enter();
     const double s = nrm2 ? sqrt(*nrm2) : scalar;
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
         dst[q] = src[q] / s;
@@ -413,6 +424,7 @@ __global__ void k_scale_by_norm(const double* __restrict__ src, double* __restri
 
 // p -= mean(p)  (project_pressure_mean, fields.cpp:78-85); sum precomputed in *sum.
 __global__ void k_sub_mean(double* __restrict__ p, size_t nn, const double* __restrict__ sum) {
+    pdl_enter();
     const double mean = *sum / (double)nn;
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < nn; q += (size_t)gridDim.x * blockDim.x)
         p[q] -= mean;
@@ -420,12 +432,14 @@ __global__ void k_sub_mean(double* __restrict__ p, size_t nn, const double* __re
 
 // b = [(rho/dt) u ; 0]
 __global__ void k_rhs_mass(const double* __restrict__ u, double* __restrict__ b, size_t nn, double rho_dt) {
+    pdl_enter();
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < 3 * nn; q += (size_t)gridDim.x * blockDim.x)
         b[q] = q < 2 * nn ? rho_dt * u[q] : 0.0;
 }
 
 // r = b - r  (residual from an applied operator)
 __global__ void k_b_minus(const double* __restrict__ b, double* __restrict__ r, size_t m) {
+    pdl_enter();
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
         r[q] = b[q] - r[q];
 }

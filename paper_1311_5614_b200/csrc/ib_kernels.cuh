@@ -62,6 +62,7 @@ __device__ __forceinline__ int cell_prolong(int c, int* J, double* w) {
 // level l's times P (W*P*...*P) — the factored form of the reference's
 // recursive Galerkin R*E*P (transfers.cpp:286-293, PAPER Eq. 20).
 __global__ void k_windows(int npts, const double* __restrict__ X, WinLevels WL, double h0, int* err) {
+    pdl_enter();
     // one thread per (point, patch s): s = 0 Lu, 1 Lv, 2 Ru, 3 Rv; the 16-entry
     // patch and its origin stay in registers from level to level
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -140,6 +141,7 @@ struct FaceBase {
     int n[20];
 };
 __global__ void k_face_keys(int npts, WinLevels WL, FaceBase FB, unsigned* keys, int* vals) {
+    pdl_enter();
     const long items = (long)npts * 32;
     const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= items * FB.nlev) return;
@@ -160,6 +162,7 @@ __global__ void k_face_keys(int npts, WinLevels WL, FaceBase FB, unsigned* keys,
 __global__ void k_face_levels(const unsigned* __restrict__ ukeys, const int* __restrict__ nruns,
                               const int* __restrict__ off, FaceBase FB, int* __restrict__ face,
                               int* __restrict__ counters, int ctr_stride) {
+    pdl_enter();
     const int nr = *nruns;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nr; q += gridDim.x * blockDim.x) {
         const unsigned key = ukeys[q];
@@ -188,6 +191,7 @@ struct BlkLevels {
 // lies in the support of any point's left or right window on the level.
 // Thread per (level, point, window slot, tap).
 __global__ void k_mark_big(int npts, WinLevels WL, BlkLevels BK, uint8_t* __restrict__ flags_all) {
+    pdl_enter();
     const long per = (long)npts * 64;
     const long qq = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (qq >= per * BK.nlev) return;
@@ -255,6 +259,7 @@ __device__ __forceinline__ int canon_off(int d, int nbk) { return wr(d + nbk / 2
 //    >= 8 cells apart only when it is <= 7, checked at setup).
 __global__ void k_block_pairs(int npts, WinLevels WL, BlkLevels BK, Pts P, unsigned* __restrict__ mask_all,
                               int* __restrict__ counters, int ctr_stride) {
+    pdl_enter();
     const int qq = blockIdx.x * blockDim.x + threadIdx.x;
     if (qq >= npts * 2 * BK.nlev) return;
     const int l = qq / (npts * 2), q = qq - l * npts * 2;
@@ -294,6 +299,7 @@ __global__ void k_block_pairs(int npts, WinLevels WL, BlkLevels BK, Pts P, unsig
 // canonical Chebyshev offset 1, or 2 with the pair bit set — and bit 12
 // (the zero offset) marking A big; 0 for blocks that are not big.
 __global__ void k_block_conflicts(BlkLevels BK, const uint8_t* __restrict__ big_all, unsigned* __restrict__ mask_all) {
+    pdl_enter();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= BK.boff[BK.nlev]) return;
     int l = 0;
@@ -323,6 +329,7 @@ __global__ void k_block_conflicts(BlkLevels BK, const uint8_t* __restrict__ big_
 // Stand-alone face gather (spread of given forces): face_gather_warp per warp.
 __global__ void k_face_gather(FaceList FL, Win W, const double* __restrict__ F, double* __restrict__ out,
                               int nn, double sign) {
+    pdl_enter();
     face_gather_warp(FL, W, F, out, nn, sign, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
 }
 
@@ -407,6 +414,7 @@ __global__ void __launch_bounds__(32 * kEWarps) k_erows(ERows R, const int* __re
                                                          Pts P, int pass, int* __restrict__ cnt,
                                                          const int* __restrict__ rp, int* __restrict__ col,
                                                          double* __restrict__ val) {
+    pdl_enter();
     __shared__ double patch[kEWarps][256];
     __shared__ double fin[256];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -450,6 +458,7 @@ __global__ void __launch_bounds__(32 * kEWarps) k_erows(ERows R, const int* __re
 // Fiber force density of the RHS times the spread quadrature:
 // F_k ds^2 = kappa (X_{k-1} + X_{k+1} - 2 X_k)/ds^2 * ds^2  (fiber.cpp:34-55, 93).
 __global__ void k_rhs_force(Pts P, const double* __restrict__ X, double* __restrict__ F) {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= P.n) return;
     const int km = P.kprev[k], kp = P.knext[k];
@@ -461,6 +470,7 @@ __global__ void k_rhs_force(Pts P, const double* __restrict__ X, double* __restr
 
 // Plain spread input scaling: F_k ds_m^2 (ds^2 quadrature, fiber.cpp:93).
 __global__ void k_scale_dsq(Pts P, const double* __restrict__ Fin, double* __restrict__ F) {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= P.n) return;
     F[2 * k] = Fin[2 * k] * P.dsq[k];
@@ -470,6 +480,7 @@ __global__ void k_scale_dsq(Pts P, const double* __restrict__ Fin, double* __res
 // interpolate (fiber.cpp:116-140): U_k = h^2 sum W u; optionally X += dt U.
 __global__ void k_interp(Win W, int npts, int n, double h, const double* __restrict__ u, double* __restrict__ U,
                          double* __restrict__ X, double dt) {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= npts) return;
     GAcc acc{u, n, n * n};

@@ -148,6 +148,7 @@ struct ibmg_ctx {
     double *V = nullptr, *Z = nullptr, *wv = nullptr, *xv = nullptr, *rv = nullptr, *bv = nullptr;
     double *partial = nullptr, *dh = nullptr, *ones = nullptr, *stage_a = nullptr, *stage_b = nullptr;
     unsigned* ticket = nullptr;  // last-CTA ticket of the fused CGS sweeps
+    bool pdl = true;             // programmatic dependent launch (IBMG_NO_PDL=1: off)
     cudaEvent_t ev_dots = nullptr;  // FGMRES: the iteration's dots have reached the host
     unsigned long long* tail_cnt = nullptr;  // producer counter of the fused gathers
     unsigned long long tail_base = 0;        // its value after the last enqueued launch
@@ -202,13 +203,40 @@ void prof_collect(ibmg_ctx* c) {
     c->prof_pending.clear();
 }
 
+// Every library kernel is launched with programmatic stream serialization
+// (common.cuh pdl_enter): the next kernel's CTAs are scheduled while the
+// previous one runs and start the moment it completes.  IBMG_NO_PDL=1 turns
+// it off (plain stream order).
+template <typename... KArgs, typename... Args>
+void launch_k(ibmg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, bool coop, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (c->pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 #define LAUNCH(ctx, kern, grid, block, smem, ...)                          \
     do {                                                                   \
         if ((ctx)->prof) prof_begin((ctx), #kern);                         \
-        kern<<<(grid), (block), (smem), (ctx)->s>>>(__VA_ARGS__);          \
+        launch_k((ctx), kern, dim3(grid), dim3(block), (smem), false, __VA_ARGS__); \
         if ((ctx)->prof) prof_end((ctx));                                  \
         ++(ctx)->launches;                                                 \
-        CK(cudaGetLastError());                                            \
         if ((ctx)->prof && (ctx)->prof_pending.size() > 4096) prof_collect(ctx); \
     } while (0)
 
@@ -916,10 +944,9 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     if (n <= kDataflowMaxN) {
         // latency regime: the whole sweep as one dataflow kernel
         DfArgs A{L, SL, BC, BigDeps{lb.pred, lb.poff, lb.flags, ++lb.epoch}, lb.tflags, lb.big, b, w, c->trace};
-        void* args[] = {&A};
         if (c->prof) prof_begin(c, "k_sweep_df");
-        CK(cudaLaunchCooperativeKernel((const void*)k_sweep_df, dim3(c->grid_limit > 0 ? std::min(c->grid_limit, c->df_grid_max) : c->df_grid_max), dim3(32 * kDfWarps), args,
-                                       kDfSmem, c->s));
+        launch_k(c, k_sweep_df, dim3(c->grid_limit > 0 ? std::min(c->grid_limit, c->df_grid_max) : c->df_grid_max),
+                 dim3(32 * kDfWarps), kDfSmem, true, A);
         if (c->prof) prof_end(c);
         ++c->launches;
         return;
@@ -929,9 +956,8 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     if (lb.nbig == 0) return;
     const int grid = std::min(widest, c->grid_limit > 0 ? std::min(c->grid_limit, c->big_grid_max) : c->big_grid_max);
     BigDeps DP{lb.pred, lb.poff, lb.flags, ++lb.epoch};
-    void* args[] = {&L, &SL, &BC, &DP, (void*)&b, (void*)&w};
     if (c->prof) prof_begin(c, "k_big_phase");
-    CK(cudaLaunchCooperativeKernel((const void*)k_big_phase, dim3(grid), dim3(kBigThreads), args, kBigSmem, c->s));
+    launch_k(c, k_big_phase, dim3(grid), dim3(kBigThreads), kBigSmem, true, L, SL, BC, DP, b, w);
     if (c->prof) prof_end(c);
     ++c->launches;
 }
@@ -1221,6 +1247,7 @@ int ibmg_create(const ibmg_params* p, ibmg_ctx** out) {
     if (p->restart < 1 || p->restart > 31 || p->max_iters < 1 || !(p->rtol > 0 && p->rtol < 1)) return IBMG_INVALID;
     if (p->nu1 < 0 || p->nu2 < 0 || p->nu1 + p->nu2 < 1) return IBMG_INVALID;
     ibmg_ctx* c = new ibmg_ctx;
+    c->pdl = std::getenv("IBMG_NO_PDL") == nullptr;
     c->prm = *p;
     try {
         CK(cudaSetDevice(p->device));

@@ -93,6 +93,7 @@ struct TileBG {  // b read through L1 (read-only in the kernel): local coords of
 // memory (9.6 KB per warp -> ~23 resident warps per SM), b is read through L1.
 __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double* __restrict__ b,
                                                      double* __restrict__ w, const uint8_t* __restrict__ big) {
+    pdl_enter();
     __shared__ __align__(16) double sw[3 * kReg * kReg];
     const int n = L.n, nn = L.nn, lane = threadIdx.x;
     const int half = (n / kTile) >> 1;
@@ -450,6 +451,7 @@ constexpr int kBigThreads = 128;
 constexpr size_t kBigSmem = 2 * sizeof(ESlot);
 __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC, BigDeps DP,
                                                             const double* __restrict__ b, double* w) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char dsm[];
     ESlot* slot = reinterpret_cast<ESlot*>(dsm);
     __shared__ BigScratch S;
@@ -532,6 +534,7 @@ __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
 }
 
 __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char dsm[];
     SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
     __shared__ BigScratch S;
@@ -759,6 +762,7 @@ struct BInvLevels {
 };
 
 __global__ void k_block_inverse(BInvLevels BL, int* err) {
+    pdl_enter();
     extern __shared__ double M[];  // 56 x gj_ld(56)
     __shared__ double col[56];
     int lv = 0;
@@ -806,6 +810,7 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
 // Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
 // pressure constraint), 49 x 49, inverted; stored col-major.
 __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict__ Ainv, int* err) {
+    pdl_enter();
     extern __shared__ double M[];
     __shared__ double col[64];
     const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = gj_ld(m), t = threadIdx.x, nt = blockDim.x;
@@ -863,6 +868,7 @@ __device__ __forceinline__ int bs_level(const BSetup& S, int qg) {
 // E' row ranges of the 40 velocity DOFs of every block (binary search of the
 // face list; (0, 0) for faces without an E' row).
 __global__ void k_block_rows(BSetup S) {
+    pdl_enter();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= S.start[S.nlev] * 40) return;
     const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
@@ -886,6 +892,7 @@ __global__ void k_block_rows(BSetup S) {
 // Slab packing: row pointers + padded entry counts (cnt, level-major), the
 // owner block id in rp[47]; the longest slab per level into counter 19.
 __global__ void k_slab_count(BSetup S, int* __restrict__ cnt, int* __restrict__ counters, int ctr_stride) {
+    pdl_enter();
     const int qg = blockIdx.x * blockDim.x + threadIdx.x;
     if (qg >= S.start[S.nlev]) return;
     const int k = bs_level(S, qg), q = qg - S.start[k];
@@ -905,6 +912,7 @@ __global__ void k_slab_count(BSetup S, int* __restrict__ cnt, int* __restrict__ 
 
 // The entries, at off[qg] (level-major offsets), columns as flat indices.
 __global__ void k_slab_fill(BSetup S, const int* __restrict__ off, int* __restrict__ col, double* __restrict__ val) {
+    pdl_enter();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= S.start[S.nlev] * 40) return;
     const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
