@@ -133,6 +133,44 @@ int ibmg_profile_report(ibmg_ctx* ctx, char* buf, int cap);
 /* The context's CUDA stream (cudaStream_t), for callers timing with events. */
 void* ibmg_stream(const ibmg_ctx* ctx);
 
+/* ---- Slab partition of one problem (BASELINE north_star: large
+ * fine grids slab-partitioned across 2/4/8 GPUs with NVLink halo exchange per
+ * smoothing sweep and coarse-level agglomeration).  No reference counterpart:
+ * the reference is single-threaded CPU code; the group takes the
+ * same calls as a context (SPEC.md:349 v_cycle, :474 gmres_solve, :548
+ * step_implicit) on host whole-grid vectors.
+ *
+ * nslabs y-slabs of the fine grid, slab r on devices[r] (slabs may share a
+ * GPU; distinct GPUs need peer access).  A level is distributed while each
+ * slab has >= max(min_rows, 24) rows, a multiple of 32, and >= min_cells
+ * cells; coarser levels are agglomerated (every slab runs them on the whole
+ * level).  Every colour pass on a distributed level is followed by a seam
+ * merge and a 24-row halo push between neighbouring slabs; FGMRES dots are
+ * summed over the slabs in rank order. */
+typedef struct ibmg_group ibmg_group;
+
+/* Host-only plan (no GPU needed): returns the number of distributed levels
+ * (-1 on invalid arguments) and, if rows_out != NULL, the owned rows
+ * rows_out[(r * nlev + l) * 2 + {0, 1}] = [y0, y1) of slab r on level l. */
+int ibmg_slab_plan(int N, int coarsest_n, int nslabs, int min_rows, long min_cells, int* rows_out);
+int ibmg_group_create(const ibmg_params* params, int nslabs, const int* devices, int min_rows, long min_cells,
+                      ibmg_group** out);
+void ibmg_group_destroy(ibmg_group* group);
+const char* ibmg_group_last_error(const ibmg_group* group);
+int ibmg_group_distributed_levels(const ibmg_group* group);
+long long ibmg_group_kernel_launches(const ibmg_group* group);
+/* Number of halo exchanges / allgathers issued (evidence for tests and bench). */
+long long ibmg_group_exchanges(const ibmg_group* group);
+/* As ibmg_set_structures, on every slab (host arrays). */
+int ibmg_group_set_structures(ibmg_group* group, int n_mem, const int* nb, const double* kappa, const double* ds,
+                              const double* X);
+/* One distributed sweep on a distributed level (host whole-level b, w; w in place). */
+int ibmg_group_sweep(ibmg_group* group, int level, const double* b, double* w);
+/* As ibmg_vcycle / ibmg_solve / ibmg_step with host whole-grid vectors. */
+int ibmg_group_vcycle(ibmg_group* group, const double* b, double* z);
+int ibmg_group_solve(ibmg_group* group, const double* b, double* x, ibmg_stats* stats);
+int ibmg_group_step(ibmg_group* group, double* u, double* p, double* X, ibmg_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

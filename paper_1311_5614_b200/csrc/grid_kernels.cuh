@@ -63,6 +63,9 @@ struct Gather {
     int nblk;
     unsigned long long* cnt;    // monotone per-context counter
     unsigned long long target;  // its value once this launch's producers are done
+    // slab mode: only faces in rows [jlo, jhi) of the level are
+    // gathered (the owned rows of a slab); lg = log2(n)
+    int lg = 0, jlo = 0, jhi = 1 << 30;
 };
 constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point / per face
 
@@ -104,6 +107,10 @@ __device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, 
             while (ld_acquire_u64(G.cnt) < G.target) __nanosleep(32);
         __syncthreads();
         const int q = (bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5);
+        if (q < G.FL.nf && (G.jlo > 0 || G.jhi < (1 << 30))) {
+            const int row = (G.FL.face[q] & (G.nn - 1)) >> G.lg;
+            if (row < G.jlo || row >= G.jhi) return;
+        }
         face_gather_warp(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, threadIdx.x & 31);
         return;
     }
@@ -119,12 +126,13 @@ __device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, 
 }
 
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
+// Grid CTAs cover cells [q0, q1) (a slab's owned rows; 0, nn for the level).
 __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out, PForce pf, Gather G,
-                               int ngrid) {
+                               int ngrid, int q0, int q1) {
     pdl_enter();
     fused_launch(pf, G, ngrid, [&](int b) {
-        const int q = b * blockDim.x + threadIdx.x;
-        if (q >= L.nn) return;
+        const int q = q0 + b * blockDim.x + threadIdx.x;
+        if (q >= q1) return;
         const int i = q & (L.n - 1), j = q >> L.lg;
         GAcc acc{w, L.n, L.nn};
         double ru, rv, rp;
@@ -137,11 +145,11 @@ __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __re
 
 // r = b - S w (E' part added by k_face_gather with sign +1).
 __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const double* __restrict__ w,
-                                  double* __restrict__ r, PForce pf, Gather G, int ngrid) {
+                                  double* __restrict__ r, PForce pf, Gather G, int ngrid, int q0, int q1) {
     pdl_enter();
     fused_launch(pf, G, ngrid, [&](int blk) {
-        const int q = blk * blockDim.x + threadIdx.x;
-        if (q >= L.nn) return;
+        const int q = q0 + blk * blockDim.x + threadIdx.x;
+        if (q >= q1) return;
         const int i = q & (L.n - 1), j = q >> L.lg;
         GAcc acc{w, L.n, L.nn};
         double ru, rv, rp;
@@ -158,9 +166,9 @@ __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const dou
 // k_face_gather on the coarse face list.
 __device__ __forceinline__ void residual_restrict_cell(const Lev& F, const double* __restrict__ b,
                                                        const double* __restrict__ w, double* __restrict__ bc,
-                                                       double* __restrict__ wc_zero, int q) {
+                                                       double* __restrict__ wc_zero, int q, int q1) {
     const int nc = F.n >> 1, nnc = nc * nc;
-    if (q >= nnc) return;
+    if (q >= q1) return;
     if (wc_zero) {  // the coarse level's zero initial guess, in the same pass
         wc_zero[q] = 0.0;
         wc_zero[nnc + q] = 0.0;
@@ -199,10 +207,11 @@ __device__ __forceinline__ void residual_restrict_cell(const Lev& F, const doubl
 
 __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
                                     double* __restrict__ bc, double* __restrict__ wc_zero, PForce pf, Gather G,
-                                    int ngrid) {
+                                    int ngrid, int q0, int q1) {
     pdl_enter();
-    fused_launch(pf, G, ngrid,
-                 [&](int blk) { residual_restrict_cell(F, b, w, bc, wc_zero, blk * blockDim.x + threadIdx.x); });
+    fused_launch(pf, G, ngrid, [&](int blk) {
+        residual_restrict_cell(F, b, w, bc, wc_zero, q0 + blk * blockDim.x + threadIdx.x, q1);
+    });
 }
 
 // Plain restriction of a vector (ibmg_restrict).
@@ -254,11 +263,11 @@ __device__ __forceinline__ void prolong_rows(int nf, const Acc& ec, int i, int j
     dp = ec(2, i >> 1, j >> 1);
 }
 
-__global__ void k_prolong_add(int nf, const double* __restrict__ ec, double* __restrict__ wf) {
+__global__ void k_prolong_add(int nf, const double* __restrict__ ec, double* __restrict__ wf, int q0, int q1) {
     pdl_enter();
     const int nnf = nf * nf;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nnf) return;
+    const int q = q0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= q1) return;
     const int i = q % nf, j = q / nf;
     GAcc acc{ec, nf >> 1, (nf >> 1) * (nf >> 1)};
     double du, dv, dp;
@@ -422,11 +431,12 @@ __global__ void k_scale_by_norm(const double* __restrict__ src, double* __restri
     }
 }
 
-// p -= mean(p)  (project_pressure_mean, fields.cpp:78-85); sum precomputed in *sum.
-__global__ void k_sub_mean(double* __restrict__ p, size_t nn, const double* __restrict__ sum) {
+// p -= mean(p)  (project_pressure_mean, fields.cpp:78-85); sum over all
+// `total` cells precomputed in *sum; this launch covers `count` of them.
+__global__ void k_sub_mean(double* __restrict__ p, size_t count, size_t total, const double* __restrict__ sum) {
     pdl_enter();
-    const double mean = *sum / (double)nn;
-    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < nn; q += (size_t)gridDim.x * blockDim.x)
+    const double mean = *sum / (double)total;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (size_t)gridDim.x * blockDim.x)
         p[q] -= mean;
 }
 
@@ -442,6 +452,38 @@ __global__ void k_b_minus(const double* __restrict__ b, double* __restrict__ r, 
     pdl_enter();
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
         r[q] = b[q] - r[q];
+}
+
+// ---------------- slab partition ----------------
+constexpr int kMaxSlabs = 8;
+struct RankPtrs {
+    const double* p[kMaxSlabs];
+};
+
+// out[i] = sum_r src.p[r][i] in rank order (the allreduce of the per-slab
+// partial dots: every slab sums the same values in the same order, so all
+// slabs hold bitwise identical results).
+__global__ void k_sum_ranks(RankPtrs src, int nranks, int len, double* __restrict__ out) {
+    pdl_enter();
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < nranks; ++r) s += src.p[r][i];
+        out[i] = s;
+    }
+}
+
+// Seam row merge: the v faces of a slab's first row are also box DOFs of the
+// boxes just below it (the neighbour slab's top cells).  After a colour pass,
+// the entries the neighbour changed (its copy differs from the snapshot taken
+// before the pass) replace ours; same-colour boxes never share a DOF, so
+// each entry was written by at most one side.
+__global__ void k_seam_merge(double* __restrict__ row, const double* __restrict__ theirs,
+                             const double* __restrict__ old, int n) {
+    pdl_enter();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double t = theirs[i];
+    if (t != old[i]) row[i] = t;
 }
 
 }  // namespace ibmg

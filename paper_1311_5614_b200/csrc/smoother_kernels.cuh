@@ -91,13 +91,15 @@ struct TileBG {  // b read through L1 (read-only in the kernel): local coords of
 // Plain phase of one tile colour on a large level (n > 512, bandwidth regime):
 // one warp per 16x16 tile; only the w region (2-cell halo) is staged in shared
 // memory (9.6 KB per warp -> ~23 resident warps per SM), b is read through L1.
+// ty0 (even): first tile row of the launch (a slab's first tile row; 0 for
+// the whole level).
 __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double* __restrict__ b,
-                                                     double* __restrict__ w, const uint8_t* __restrict__ big) {
+                                                     double* __restrict__ w, const uint8_t* __restrict__ big, int ty0) {
     pdl_enter();
     __shared__ __align__(16) double sw[3 * kReg * kReg];
     const int n = L.n, nn = L.nn, lane = threadIdx.x;
     const int half = (n / kTile) >> 1;
-    const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = 2 * (blockIdx.x / half) + (tc >> 1);
+    const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = ty0 + 2 * (blockIdx.x / half) + (tc >> 1);
     const int x0 = tx * kTile, y0 = ty * kTile;
     for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs
         const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
@@ -479,9 +481,11 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
         next_item(c, q, nc, nq);
         if (nc < BC.ncol) eslot_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
         cp_async_commit();
-        // wait for the predecessors of block q (one thread per predecessor)
-        for (int e = DP.poff[q] + t; e < DP.poff[q + 1]; e += kBigThreads)
-            while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(8);
+        // wait for the predecessors of block q (one thread per predecessor);
+        // poff == nullptr: one colour per launch (slab mode), nothing to wait for
+        if (DP.poff)
+            for (int e = DP.poff[q] + t; e < DP.poff[q + 1]; e += kBigThreads)
+                while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(8);
         cp_async_wait<1>();
         __syncthreads();
         const ESlot& sl = slot[k & 1];
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
                      },
                      S, t, [] { __syncthreads(); });
         __syncthreads();
-        if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
+        if (t == 0 && DP.flags) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(DP.flags + q, DP.epoch);
         }
         ++k;

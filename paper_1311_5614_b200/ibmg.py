@@ -46,7 +46,10 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_vcycle", "ibmg_coarse_solve", "ibmg_big_blocks", "ibmg_build_rhs", "ibmg_interpolate",
            "ibmg_spread", "ibmg_solve", "ibmg_step", "ibmg_kernel_launches", "ibmg_stream", "ibmg_profile",
            "ibmg_profile_report", "ibmg_elasticity_triplets", "ibmg_debug_sweep_trace", "ibmg_set_grid_limit",
-           "ibmg_debug_coarse_trace"]
+           "ibmg_debug_coarse_trace", "ibmg_slab_plan", "ibmg_group_create", "ibmg_group_destroy",
+           "ibmg_group_last_error", "ibmg_group_distributed_levels", "ibmg_group_kernel_launches",
+           "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
+           "ibmg_group_solve", "ibmg_group_step"]
 
 
 def lib_path() -> str:
@@ -98,6 +101,21 @@ def lib(build_if_missing: bool = True):
     L.ibmg_debug_coarse_trace.argtypes = [vp, vp, vp, vp, C.c_long]
     L.ibmg_profile.argtypes = [vp, ip]
     L.ibmg_profile_report.argtypes = [vp, C.c_char_p, ip]
+    L.ibmg_slab_plan.argtypes = [ip, ip, ip, ip, C.c_long, vp]
+    L.ibmg_group_create.argtypes = [C.POINTER(Params), ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
+    L.ibmg_group_destroy.argtypes = [vp]
+    L.ibmg_group_last_error.restype = C.c_char_p
+    L.ibmg_group_last_error.argtypes = [vp]
+    L.ibmg_group_distributed_levels.argtypes = [vp]
+    L.ibmg_group_kernel_launches.restype = C.c_longlong
+    L.ibmg_group_kernel_launches.argtypes = [vp]
+    L.ibmg_group_exchanges.restype = C.c_longlong
+    L.ibmg_group_exchanges.argtypes = [vp]
+    L.ibmg_group_set_structures.argtypes = [vp, ip, vp, vp, vp, vp]
+    L.ibmg_group_sweep.argtypes = [vp, ip, dp, dp]
+    L.ibmg_group_vcycle.argtypes = [vp, dp, dp]
+    L.ibmg_group_solve.argtypes = [vp, dp, dp, C.POINTER(Stats)]
+    L.ibmg_group_step.argtypes = [vp, dp, dp, dp, C.POINTER(Stats)]
     _LIB = L
     return L
 
@@ -307,3 +325,103 @@ class SaddleSystem:
     @property
     def stream(self):
         return self._L.ibmg_stream(self._h)
+
+
+def slab_plan(N, nslabs, min_rows=64, min_cells=1 << 16, coarsest_n=4):
+    """(la, rows) of the slab partition (host-only, no GPU): la = number of
+    distributed levels, rows[r][l] = (y0, y1) owned by slab r on level l."""
+    L = lib()
+    nlev = int(np.log2(N // coarsest_n)) + 1
+    rows = np.zeros((nslabs, nlev, 2), np.int32)
+    la = L.ibmg_slab_plan(N, coarsest_n, nslabs, min_rows, min_cells, rows.ctypes.data)
+    if la < 0:
+        raise ValueError("slab_plan: invalid arguments")
+    return la, rows
+
+
+class SlabGroup:
+    """One problem slab-partitioned over `nslabs` contexts:
+    y-slabs of the fine grid on `devices` (slabs may share a GPU), halo
+    exchange + seam merge after every colour pass, agglomerated coarse levels,
+    FGMRES dots allreduced in rank order.  Host (numpy) whole-grid vectors."""
+
+    def __init__(self, N, nslabs, devices=None, rho=1.0, mu=1.0, dt=1e-2, nu1=1, nu2=1, restart=30,
+                 max_iters=600, rtol=1e-10, min_rows=64, min_cells=1 << 16):
+        self._L = lib()
+        p = Params(N, rho, mu, dt, nu1, nu2, restart, max_iters, rtol, 4, 0 if devices is None else devices[0])
+        dev = (C.c_int * nslabs)(*(devices if devices is not None else [0] * nslabs))
+        h = C.c_void_p()
+        rc = self._L.ibmg_group_create(C.byref(p), nslabs, dev, min_rows, min_cells, C.byref(h))
+        if rc != 0 or not h.value:
+            raise RuntimeError(f"ibmg_group_create failed (status {rc})")
+        self._h = h
+        self.N, self.nslabs, self.npts = N, nslabs, 0
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.ibmg_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, rc, ok=(0,)):
+        if rc in ok:
+            return rc
+        msg = self._L.ibmg_group_last_error(self._h).decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+    @property
+    def distributed_levels(self):
+        return self._L.ibmg_group_distributed_levels(self._h)
+
+    @property
+    def kernel_launches(self):
+        return int(self._L.ibmg_group_kernel_launches(self._h))
+
+    @property
+    def exchanges(self):
+        return int(self._L.ibmg_group_exchanges(self._h))
+
+    def set_structures(self, nb, kappa, ds, X):
+        nb = np.ascontiguousarray(nb, np.int32)
+        kappa = np.ascontiguousarray(kappa, np.float64)
+        ds = np.ascontiguousarray(ds, np.float64)
+        X = np.ascontiguousarray(X, np.float64).reshape(-1)
+        self._chk(self._L.ibmg_group_set_structures(self._h, len(nb), nb.ctypes.data, kappa.ctypes.data,
+                                                    ds.ctypes.data, X.ctypes.data))
+        self.npts = int(nb.sum())
+        return self
+
+    @classmethod
+    def from_problem(cls, prob, nslabs, **kw):
+        g = cls(prob.N, nslabs, rho=prob.rho, mu=prob.mu, dt=prob.dt, **kw)
+        return g.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
+
+    def sweep(self, b, w, level=0):
+        b = np.ascontiguousarray(b, np.float64)
+        w = np.array(w, np.float64)
+        self._chk(self._L.ibmg_group_sweep(self._h, level, b.ctypes.data, w.ctypes.data))
+        return w
+
+    def v_cycle(self, b):
+        b = np.ascontiguousarray(b, np.float64)
+        z = np.empty_like(b)
+        self._chk(self._L.ibmg_group_vcycle(self._h, b.ctypes.data, z.ctypes.data))
+        return z
+
+    def gmres_solve(self, b):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty_like(b)
+        st = Stats()
+        self._chk(self._L.ibmg_group_solve(self._h, b.ctypes.data, x.ctypes.data, C.byref(st)), ok=(0, 2))
+        return x, st.as_dict()
+
+    def step_implicit(self, u, p, X):
+        st = Stats()
+        for a in (u, p, X):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+                raise ValueError("group step: C-contiguous float64 numpy arrays")
+        self._chk(self._L.ibmg_group_step(self._h, u.ctypes.data, p.ctypes.data, X.ctypes.data, C.byref(st)),
+                  ok=(0, 2))
+        return st.as_dict()
