@@ -153,8 +153,19 @@ typedef struct ibmg_group ibmg_group;
  * (-1 on invalid arguments) and, if rows_out != NULL, the owned rows
  * rows_out[(r * nlev + l) * 2 + {0, 1}] = [y0, y1) of slab r on level l. */
 int ibmg_slab_plan(int N, int coarsest_n, int nslabs, int min_rows, long min_cells, int* rows_out);
+/* In-process group: all nslabs slabs in this process, slab r on devices[r]
+ * (NULL: params->device); exchanges are peer copies ordered by CUDA events.
+ * min_rows < 0 is a test mode that distributes levels even for one slab. */
 int ibmg_group_create(const ibmg_params* params, int nslabs, const int* devices, int min_rows, long min_cells,
                       ibmg_group** out);
+/* NCCL group: one slab per process (torchrun, one rank per GPU on
+ * params->device); halos / seams by ncclSend/ncclRecv, dots by ncclAllReduce,
+ * agglomeration by ncclAllGather, stream-ordered.  nccl_id: the 128-byte
+ * ncclUniqueId from ibmg_nccl_unique_id on rank 0, broadcast by the caller.
+ * Host outputs (vcycle/solve/step/sweep) are whole on every rank. */
+int ibmg_nccl_unique_id(void* id_out);
+int ibmg_group_create_nccl(const ibmg_params* params, int rank, int nranks, const void* nccl_id, int min_rows,
+                           long min_cells, ibmg_group** out);
 void ibmg_group_destroy(ibmg_group* group);
 const char* ibmg_group_last_error(const ibmg_group* group);
 int ibmg_group_distributed_levels(const ibmg_group* group);

@@ -36,7 +36,7 @@ def stale(target, deps) -> bool:
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(HERE, "csrc", d) for d in DEPS] + [os.path.join(ROOT, "include", "ibmg_gpu.h")]
     if force or stale(LIB, deps):
-        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(HERE, "csrc", s) for s in SRCS]
+        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(HERE, "csrc", s) for s in SRCS] + ["-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

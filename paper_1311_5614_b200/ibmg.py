@@ -49,7 +49,7 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_debug_coarse_trace", "ibmg_slab_plan", "ibmg_group_create", "ibmg_group_destroy",
            "ibmg_group_last_error", "ibmg_group_distributed_levels", "ibmg_group_kernel_launches",
            "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
-           "ibmg_group_solve", "ibmg_group_step"]
+           "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl"]
 
 
 def lib_path() -> str:
@@ -103,6 +103,8 @@ def lib(build_if_missing: bool = True):
     L.ibmg_profile_report.argtypes = [vp, C.c_char_p, ip]
     L.ibmg_slab_plan.argtypes = [ip, ip, ip, ip, C.c_long, vp]
     L.ibmg_group_create.argtypes = [C.POINTER(Params), ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
+    L.ibmg_group_create_nccl.argtypes = [C.POINTER(Params), ip, ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
+    L.ibmg_nccl_unique_id.argtypes = [vp]
     L.ibmg_group_destroy.argtypes = [vp]
     L.ibmg_group_last_error.restype = C.c_char_p
     L.ibmg_group_last_error.argtypes = [vp]
@@ -346,14 +348,23 @@ class SlabGroup:
     FGMRES dots allreduced in rank order.  Host (numpy) whole-grid vectors."""
 
     def __init__(self, N, nslabs, devices=None, rho=1.0, mu=1.0, dt=1e-2, nu1=1, nu2=1, restart=30,
-                 max_iters=600, rtol=1e-10, min_rows=64, min_cells=1 << 16):
+                 max_iters=600, rtol=1e-10, min_rows=64, min_cells=1 << 16, nccl=None):
+        """nccl=(rank, device, unique_id bytes): this process holds slab `rank`
+        of an NCCL group of `nslabs` ranks (see nccl_group); otherwise all
+        slabs live in this process on `devices` (default: all on GPU 0)."""
         self._L = lib()
-        p = Params(N, rho, mu, dt, nu1, nu2, restart, max_iters, rtol, 4, 0 if devices is None else devices[0])
-        dev = (C.c_int * nslabs)(*(devices if devices is not None else [0] * nslabs))
         h = C.c_void_p()
-        rc = self._L.ibmg_group_create(C.byref(p), nslabs, dev, min_rows, min_cells, C.byref(h))
+        if nccl is not None:
+            rank, device, uid = nccl
+            p = Params(N, rho, mu, dt, nu1, nu2, restart, max_iters, rtol, 4, device)
+            buf = C.create_string_buffer(bytes(uid), 128)
+            rc = self._L.ibmg_group_create_nccl(C.byref(p), rank, nslabs, buf, min_rows, min_cells, C.byref(h))
+        else:
+            p = Params(N, rho, mu, dt, nu1, nu2, restart, max_iters, rtol, 4, 0 if devices is None else devices[0])
+            dev = (C.c_int * nslabs)(*(devices if devices is not None else [0] * nslabs))
+            rc = self._L.ibmg_group_create(C.byref(p), nslabs, dev, min_rows, min_cells, C.byref(h))
         if rc != 0 or not h.value:
-            raise RuntimeError(f"ibmg_group_create failed (status {rc})")
+            raise RuntimeError(f"slab group creation failed (status {rc})")
         self._h = h
         self.N, self.nslabs, self.npts = N, nslabs, 0
 
@@ -370,6 +381,24 @@ class SlabGroup:
             return rc
         msg = self._L.ibmg_group_last_error(self._h).decode()
         raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = C.create_string_buffer(128)
+        if lib().ibmg_nccl_unique_id(buf) != 0:
+            raise RuntimeError("ncclGetUniqueId failed")
+        return buf.raw
+
+    @classmethod
+    def nccl_group(cls, N, device=None, **kw):
+        """One slab per torch.distributed rank (torchrun): rank 0 makes the NCCL
+        id, every rank receives it through the process group's broadcast."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        dev = int(os.environ.get("LOCAL_RANK", "0")) if device is None else device
+        return cls(N, world, nccl=(rank, dev, obj[0]), **kw)
 
     @property
     def distributed_levels(self):

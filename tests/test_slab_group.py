@@ -103,3 +103,30 @@ def test_group_steps_match_single(P):
         assert abs(sg["iters"] - ss["iters"]) <= 1
     assert rel(ug, us) < 1e-8 and rel(pg, ps) < 1e-8 and rel(Xg, Xs) < 1e-8
     assert g.kernel_launches > 0
+
+
+@pytest.mark.parametrize("transport", ["inprocess", "nccl"])
+def test_one_slab_test_mode_exchanges_with_itself(c2, transport):
+    """min_rows < 0 distributes levels even for one slab: every seam, halo,
+    allgather and allreduce then targets the slab itself (NCCL: self send/recv,
+    world-size-1 collectives).  Results must equal the one-context solver."""
+    prob, s = c2
+    kw = dict(min_rows=-1, min_cells=0)
+    if transport == "nccl":
+        g = SlabGroup(prob.N, 1, nccl=(0, 0, SlabGroup.nccl_unique_id()), rho=prob.rho, mu=prob.mu, dt=prob.dt, **kw)
+        g.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
+    else:
+        g = SlabGroup.from_problem(prob, 1, **kw)
+    assert g.distributed_levels == 3  # 256, 128, 64
+    n = prob.N
+    for l in range(3):
+        m = s.level_n(l)
+        b, w = rand(3 * m * m, 60 + l), rand(3 * m * m, 70 + l)
+        assert np.array_equal(g.sweep(b, w, level=l), s.sweep(b, w.copy(), level=l)), l
+    b = rand(3 * n * n, 80)
+    assert rel(g.v_cycle(b), s.v_cycle(b)) < 1e-13
+    rhs = s.build_rhs(rand(2 * n * n, 81))
+    xs, ss = s.gmres_solve(rhs)
+    xg, sg = g.gmres_solve(rhs)
+    assert sg["converged"] and sg["iters"] == ss["iters"]
+    assert rel(xg, xs) < 1e-10
