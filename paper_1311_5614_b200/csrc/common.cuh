@@ -61,6 +61,25 @@ struct Pts {
 
 __host__ __device__ __forceinline__ int wr(int i, int n) { return i & (n - 1); }
 
+// Slab partition (slab_group.cuh): halo depth in rows, and the
+// neighbour copies a colour pass mirrors its boundary writes into (peer
+// stores over NVLink, or plain stores when the slabs share a GPU).  A write of
+// row j (wrapped) also goes to the previous slab when j is among the first
+// kHaloRows owned rows, and to the next slab when j is among the last
+// kHaloRows owned rows or is row y1 (the next slab's first v row, a face of
+// this slab's top boxes).  prv == nullptr: no mirroring (one context).
+constexpr int kHaloRows = 24;
+struct Mirror {
+    double* prv = nullptr;
+    double* nxt = nullptr;
+    int y0 = 0, y1 = 0;
+    __device__ __forceinline__ void store(size_t off, int j, int n, double v) const {
+        if (prv == nullptr) return;
+        if (wr(j - y0, n) < kHaloRows) __stcg(prv + off, v);
+        if (wr(j - (y1 - kHaloRows), n) <= kHaloRows) __stcg(nxt + off, v);
+    }
+};
+
 // Programmatic dependent launch: every kernel of the library is launched with
 // programmatic stream serialization (ibmg.cu launch_k), lets the next kernel
 // in the stream be scheduled at once, and waits for the previous kernel's

@@ -156,6 +156,7 @@ struct ibmg_ctx {
     size_t M = 0;              // 3 N^2
     size_t Mk = 0;             // Krylov vector length: M, or 3 rows N for a slab
     int krows = 0;             // fine rows held by the Krylov vectors (N unless a slab)
+    std::vector<int> own_y0, own_y1;  // slab: owned rows per distributed level (setup skips other blocks)
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
     bool have_structs = false;
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
@@ -764,6 +765,10 @@ void rebuild(ibmg_ctx* c) {
                 BL.rr[k] = lb.rr;
                 BL.Ainv[k] = lb.Ainv;
                 BL.start[k] = S.start[k];
+                const int l = S.lev[k];
+                const bool own = l < int(c->own_y0.size());
+                BL.bylo[k] = own ? c->own_y0[l] / 4 : 0;
+                BL.byhi[k] = own ? c->own_y1[l] / 4 : lb.L.n / 4;
             }
             BL.nlev = S.nlev;
             BL.start[S.nlev] = nball;
@@ -955,12 +960,12 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
         return;
     }
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
-    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big, 0);
+    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big, 0, Mirror{});
     if (lb.nbig == 0) return;
     const int grid = std::min(widest, c->grid_limit > 0 ? std::min(c->grid_limit, c->big_grid_max) : c->big_grid_max);
     BigDeps DP{lb.pred, lb.poff, lb.flags, ++lb.epoch};
     if (c->prof) prof_begin(c, "k_big_phase");
-    launch_k(c, k_big_phase, dim3(grid), dim3(kBigThreads), kBigSmem, true, L, SL, BC, DP, b, w);
+    launch_k(c, k_big_phase, dim3(grid), dim3(kBigThreads), kBigSmem, true, L, SL, BC, DP, b, w, Mirror{});
     if (c->prof) prof_end(c);
     ++c->launches;
 }

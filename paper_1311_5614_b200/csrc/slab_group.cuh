@@ -22,6 +22,9 @@
 //       in the pass (k_seam_merge against a snapshot taken before it);
 //   (2) the halo push: each slab's first and last kHalo owned rows (3 planes)
 //       go to the neighbours' copies.
+// In-process groups do both inside the pass kernels (peer stores of the
+// boundary rows into the neighbours' copies, common.cuh Mirror) and only
+// synchronise with the neighbours afterwards; NCCL groups exchange after it.
 // The colour passes are those of the single-GPU schedule (4 tile colours,
 // then the big-block colours one launch each), so a distributed sweep equals
 // the one-context sweep bit for bit (tests/test_slab_group.py).
@@ -95,7 +98,7 @@ const NcclApi& nccl() {
     return *a;
 }
 
-constexpr int kHalo = 24;   // >= 2 E' reaches (<= 7 cells, checked at setup) + restriction stencil
+constexpr int kHalo = kHaloRows;  // >= 2 E' reaches (<= 7 cells, checked at setup) + restriction stencil
 constexpr int kStash = 64;  // doubles per partial-dot stash slot (>= restart + 1)
 
 struct SlabPlan {
@@ -368,27 +371,64 @@ std::pair<int, int> owned_blocks(ibmg_group* g, int r, int l, int col) {
     return {lo, hi};
 }
 
+// In-process groups fuse the exchange into the colour passes: a pass kernel
+// mirrors every write of its boundary rows (and of the next slab's seam row)
+// into the neighbours' copies with peer stores (common.cuh Mirror), so a pass
+// is followed only by an event barrier with the two neighbours.  NCCL groups
+// (no peer pointers) snapshot the seam row and exchange after the pass.
+bool fused_exchange(ibmg_group* g) { return !g->comm && g->plan.P > 1; }
+
+Mirror mirror(ibmg_group* g, int r, int l) {
+    if (!fused_exchange(g)) return Mirror{};
+    const int P = g->plan.P;
+    Mirror M;
+    M.prv = lvec(g, (r + P - 1) % P, l, VW);
+    M.nxt = lvec(g, (r + 1) % P, l, VW);
+    M.y0 = g->plan.y0(r, l);
+    M.y1 = g->plan.y1(r, l);
+    return M;
+}
+
+// every slab's stream waits for its neighbours' work so far
+void neighbour_barrier(ibmg_group* g) {
+    const int P = g->plan.P;
+    ++g->exchanges;
+    each(g, [&](int r, ibmg_ctx* c) { CK(cudaEventRecord(pr(g, r).ea, c->s)); });
+    each(g, [&](int r, ibmg_ctx* c) {
+        CK(cudaStreamWaitEvent(c->s, pr(g, (r + P - 1) % P).ea, 0));
+        CK(cudaStreamWaitEvent(c->s, pr(g, (r + 1) % P).ea, 0));
+    });
+}
+
+void before_pass(ibmg_group* g, int l) {
+    if (!fused_exchange(g)) seam_snapshot(g, l);
+}
+void after_pass(ibmg_group* g, int l) {
+    if (fused_exchange(g)) neighbour_barrier(g);
+    else exchange(g, l, VW, true);
+}
+
 // one multicolour sweep of a distributed level: the single-GPU pass order
 // (4 tile colours, then the big-block colours), each pass over the slab's own
-// tiles / blocks, each followed by the seam merge and the halo push
+// tiles / blocks, each followed by the exchange with the neighbour slabs
 void sweep_group(ibmg_group* g, int l) {
     const int n = g->plan.n[l], half = (n / kTile) / 2;
     const int rows = n / g->plan.P;
     for (int tc = 0; tc < 4; ++tc) {
-        seam_snapshot(g, l);
+        before_pass(g, l);
         each(g, [&](int r, ibmg_ctx* c) {
             LevelBuf& lb = c->lev[l];
             LAUNCH(c, k_plain_tiles, half * (rows / (2 * kTile)), 32, 0, lb.L, tc, (const double*)lb.b, lb.w,
-                   (const uint8_t*)lb.big, g->plan.y0(r, l) / kTile);
+                   (const uint8_t*)lb.big, g->plan.y0(r, l) / kTile, mirror(g, r, l));
         });
-        exchange(g, l, VW, true);
+        after_pass(g, l);
     }
     // every slab holds the same colouring (redundant setup), so the colour
     // count and the skip decision below are identical on all ranks
     const LevelBuf& l0 = g->c[0]->lev[l];
     for (int col = 0; col < l0.ncol; ++col) {
         if (l0.coff[col + 1] == l0.coff[col]) continue;
-        seam_snapshot(g, l);
+        before_pass(g, l);
         each(g, [&](int r, ibmg_ctx* c) {
             const std::pair<int, int> q = owned_blocks(g, r, l, col);
             if (q.second <= q.first) return;
@@ -401,11 +441,11 @@ void sweep_group(ibmg_group* g, int l) {
             const int grid = std::min(q.second - q.first, c->big_grid_max);
             if (c->prof) prof_begin(c, "k_big_phase");
             launch_k(c, k_big_phase, dim3(grid), dim3(kBigThreads), kBigSmem, true, lb.L, slabs(lb), BC, DP,
-                     (const double*)lb.b, lb.w);
+                     (const double*)lb.b, lb.w, mirror(g, r, l));
             if (c->prof) prof_end(c);
             ++c->launches;
         });
-        exchange(g, l, VW, true);
+        after_pass(g, l);
     }
 }
 
@@ -723,6 +763,10 @@ void group_alloc(ibmg_group* g, const ibmg_params* p, int nlocal) {
         ibmg_ctx* c = nullptr;
         const int rc = create_ctx(&q, g->rows, &c);
         if (rc != IBMG_OK) throw CudaError("slab context creation failed (status " + std::to_string(rc) + ")");
+        for (int l = 0; l < g->plan.la; ++l) {  // box inverses of its own blocks only
+            c->own_y0.push_back(g->plan.y0(g->r0 + i, l));
+            c->own_y1.push_back(g->plan.y1(g->r0 + i, l));
+        }
         g->c.push_back(c);
     }
     for (int i = 0; i < nlocal; ++i)

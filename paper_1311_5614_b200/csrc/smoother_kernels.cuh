@@ -94,7 +94,8 @@ struct TileBG {  // b read through L1 (read-only in the kernel): local coords of
 // ty0 (even): first tile row of the launch (a slab's first tile row; 0 for
 // the whole level).
 __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double* __restrict__ b,
-                                                     double* __restrict__ w, const uint8_t* __restrict__ big, int ty0) {
+                                                     double* __restrict__ w, const uint8_t* __restrict__ big, int ty0,
+                                                     Mirror M) {
     pdl_enter();
     __shared__ __align__(16) double sw[3 * kReg * kReg];
     const int n = L.n, nn = L.nn, lane = threadIdx.x;
@@ -121,11 +122,20 @@ __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double*
     }
     // write set: u faces i in [x0, x0+16], v faces j in [y0, y0+16], p cells
     for (int q = lane; q < 17 * 17; q += 32) {
-        const int a = q % 17, bb = q / 17;
-        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-        if (bb < 16) w[gi] = W(0, a, bb);
-        if (a < 16) w[nn + gi] = W(1, a, bb);
-        if (a < 16 && bb < 16) w[2 * nn + gi] = W(2, a, bb);
+        const int a = q % 17, bb = q / 17, j = wr(y0 + bb, n);
+        const size_t gi = wr(x0 + a, n) + (size_t)j * n;
+        if (bb < 16) {
+            w[gi] = W(0, a, bb);
+            M.store(gi, j, n, W(0, a, bb));
+        }
+        if (a < 16) {
+            w[nn + gi] = W(1, a, bb);
+            M.store(nn + gi, j, n, W(1, a, bb));
+        }
+        if (a < 16 && bb < 16) {
+            w[2 * nn + gi] = W(2, a, bb);
+            M.store(2 * nn + gi, j, n, W(2, a, bb));
+        }
     }
 }
 
@@ -452,7 +462,7 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 constexpr int kBigThreads = 128;
 constexpr size_t kBigSmem = 2 * sizeof(ESlot);
 __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC, BigDeps DP,
-                                                            const double* __restrict__ b, double* w) {
+                                                            const double* __restrict__ b, double* w, Mirror M) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char dsm[];
     ESlot* slot = reinterpret_cast<ESlot*>(dsm);
@@ -492,7 +502,9 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
         const int Bk = sl.rp[47];
         big_block_es(L, sl, SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, B,
                      [&](int f, int i, int j, double old, double d) {
-                         __stcg(w + (size_t)f * L.nn + i + (size_t)j * L.n, old + d);
+                         const size_t off = (size_t)f * L.nn + i + (size_t)j * L.n;
+                         __stcg(w + off, old + d);
+                         M.store(off, j, L.n, old + d);
                      },
                      S, t, [] { __syncthreads(); });
         __syncthreads();
@@ -763,6 +775,7 @@ struct BInvLevels {
     double* Ainv[20];
     int start[21];
     int nlev;
+    int bylo[20], byhi[20];  // block rows to invert (a slab's own rows; 0, n/4 = all)
 };
 
 __global__ void k_block_inverse(BInvLevels BL, int* err) {
@@ -779,6 +792,7 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
     const int q = blockIdx.x - BL.start[lv], t = threadIdx.x, nt = blockDim.x, n = L.n;
     const int B = blk_ids[q], nbk = n >> 2;
     const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
+    if (B / nbk < BL.bylo[lv] || B / nbk >= BL.byhi[lv]) return;  // another slab's block
     constexpr int LD = gj_ld(56);
     for (int idx = t; idx < 56 * LD; idx += nt) {
         const int i = idx / LD, j = idx % LD;

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--spread", action="store_true", help="slab r on GPU r % device_count")
     ap.add_argument("--min-cells", type=int, default=1 << 16)
     ap.add_argument("--skip-single", action="store_true")
+    ap.add_argument("--single-only", action="store_true")
     a = ap.parse_args()
     prob = {"C2": lambda: configs.config2(1e6), "C3": configs.config3, "C4": configs.config4}[a.config]()
     n = prob.N
@@ -46,6 +47,9 @@ def main():
         res["single"] = (u, p, X)
         s.close()
         del s
+    if a.single_only:
+        print(json.dumps(out))
+        return
     devs = None
     if a.spread:
         import torch
