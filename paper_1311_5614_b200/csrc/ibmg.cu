@@ -160,6 +160,8 @@ struct ibmg_ctx {
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
     bool have_structs = false;
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
+    int pp_grid_max = 1;    // co-resident CTAs of the persistent plain phase
+    bool tiles_pp = true;   // persistent double-buffered plain phase (IBMG_TILES_PP=0: one CTA per tile)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int grid_limit = 0;     // optional cap on the persistent kernels' grids (concurrent contexts)
     unsigned long long* trace = nullptr;  // debug task timeline of the dataflow sweep
@@ -935,6 +937,18 @@ void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double
 
 Slabs slabs(const LevelBuf& lb) { return Slabs{lb.Ainv, lb.sl_rp, lb.sl_off, lb.sl_col, lb.sl_val}; }
 
+// One tile-colour pass of the plain phase over `ntiles` tiles starting at tile
+// row ty0 (bandwidth regime: persistent double-buffered kernel by default).
+void plain_pass(ibmg_ctx* c, LevelBuf& lb, int tc, const double* b, double* w, int ty0, int ntiles, const Mirror& M) {
+    if (c->tiles_pp) {
+        const int lim = c->grid_limit > 0 ? std::min(c->grid_limit, c->pp_grid_max) : c->pp_grid_max;
+        LAUNCH(c, k_plain_tiles_pp, std::min(ntiles, lim), 32, kPPSmem, lb.L, tc, b, w, (const uint8_t*)lb.big, ty0,
+               ntiles, M);
+    } else {
+        LAUNCH(c, k_plain_tiles, ntiles, 32, 0, lb.L, tc, b, w, (const uint8_t*)lb.big, ty0, M);
+    }
+}
+
 // One multicolour sweep of a multi-tile level (n >= 32): the plain phase as
 // 4 tile-colour launches (one warp per 16x16 tile), then the big phase as one
 // cooperative persistent launch over the 16 level-wide colours.
@@ -960,7 +974,7 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
         return;
     }
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
-    for (int tc = 0; tc < 4; ++tc) LAUNCH(c, k_plain_tiles, per, 32, 0, lb.L, tc, b, w, lb.big, 0, Mirror{});
+    for (int tc = 0; tc < 4; ++tc) plain_pass(c, lb, tc, b, w, 0, per, Mirror{});
     if (lb.nbig == 0) return;
     const int grid = std::min(widest, c->grid_limit > 0 ? std::min(c->grid_limit, c->big_grid_max) : c->big_grid_max);
     BigDeps DP{lb.pred, lb.poff, lb.flags, ++lb.epoch};
@@ -1262,6 +1276,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (krows < 1 || krows > p->N) return IBMG_INVALID;
     ibmg_ctx* c = new ibmg_ctx;
     c->pdl = std::getenv("IBMG_NO_PDL") == nullptr;
+    if (const char* e = std::getenv("IBMG_TILES_PP")) c->tiles_pp = std::atoi(e) != 0;
     c->prm = *p;
     c->krows = krows;
     try {
@@ -1275,6 +1290,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_phase, kBigThreads, kBigSmem));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
             c->big_grid_max = std::max(1, per_sm * sms);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_tiles_pp, 32, kPPSmem));
+            c->pp_grid_max = std::max(1, per_sm * sms);
             CK(cudaFuncSetAttribute(k_sweep_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df, 32 * kDfWarps, kDfSmem));
             c->df_grid_max = std::max(1, per_sm * sms);

@@ -418,8 +418,7 @@ void sweep_group(ibmg_group* g, int l) {
         before_pass(g, l);
         each(g, [&](int r, ibmg_ctx* c) {
             LevelBuf& lb = c->lev[l];
-            LAUNCH(c, k_plain_tiles, half * (rows / (2 * kTile)), 32, 0, lb.L, tc, (const double*)lb.b, lb.w,
-                   (const uint8_t*)lb.big, g->plan.y0(r, l) / kTile, mirror(g, r, l));
+            plain_pass(c, lb, tc, lb.b, lb.w, g->plan.y0(r, l) / kTile, half * (rows / (2 * kTile)), mirror(g, r, l));
         });
         after_pass(g, l);
     }

@@ -68,13 +68,33 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // ---- plain phase, multi-tile levels (n >= 32): one warp per 16x16 tile.
 constexpr int kTile = 16, kReg = kTile + 4;  // region with a 2-cell halo
+// Row stride of the staged w region.  An odd stride would halve the shared-
+// memory wavefronts of the passes (the 32 cells of a colour pass all have
+// one word parity at an even stride: 4 wavefronts per fp64 access instead of
+// 2), but needs 8-byte staging copies; measured on B200 that is slower
+// (C4 plain phase 123 -> 160 ms, C2 step 7.77 -> 8.02 ms), so rows stay
+// 16-byte aligned.
+constexpr int kRegS = kReg, kRegP = kReg * kRegS;
 
 struct TileW {
-    double* s;  // [3][kReg][kReg], local coords li, lj in [-2, 18)
+    double* s;  // [3][kReg][kRegS], local coords li, lj in [-2, 18)
     __device__ __forceinline__ double& operator()(int f, int i, int j) const {
-        return s[f * kReg * kReg + (j + 2) * kReg + (i + 2)];
+        return s[f * kRegP + (j + 2) * kRegS + (i + 2)];
     }
 };
+// w region of a tile (2-cell halo, 3 planes) into the TileW layout with
+// 16-byte cp.async (L1-allocating: w is not written by the launch).
+__device__ __forceinline__ void stage_w_region(double* sw, const double* __restrict__ w, int n, int nn, int x0, int y0,
+                                               int lane) {
+    static_assert(kRegS % 2 == 0, "16-byte staging needs 16-byte aligned rows");
+    for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs
+        const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
+        const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
+        const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
+        cp_async16(&sw[f * kRegP + bb * kRegS + 2 * a2], w + (size_t)f * nn + gi);
+    }
+}
+
 struct TileB {
     const double* s;  // [3][17][17], local coords in [0, 17)
     __device__ __forceinline__ double operator()(int f, int i, int j) const { return s[f * 289 + j * 17 + i]; }
@@ -97,17 +117,12 @@ __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double*
                                                      double* __restrict__ w, const uint8_t* __restrict__ big, int ty0,
                                                      Mirror M) {
     pdl_enter();
-    __shared__ __align__(16) double sw[3 * kReg * kReg];
+    __shared__ __align__(16) double sw[3 * kRegP];
     const int n = L.n, nn = L.nn, lane = threadIdx.x;
     const int half = (n / kTile) >> 1;
     const int tx = 2 * (blockIdx.x % half) + (tc & 1), ty = ty0 + 2 * (blockIdx.x / half) + (tc >> 1);
     const int x0 = tx * kTile, y0 = ty * kTile;
-    for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs
-        const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
-        const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
-        const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-        cp_async16(&sw[f * kReg * kReg + bb * kReg + 2 * a2], w + (size_t)f * nn + gi);
-    }
+    stage_w_region(sw, w, n, nn, x0, y0, lane);
     cp_async_commit();
     const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
     const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
@@ -137,6 +152,88 @@ __global__ void __launch_bounds__(32) k_plain_tiles(Lev L, int tc, const double*
             M.store(2 * nn + gi, j, n, W(2, a, bb));
         }
     }
+}
+
+// Persistent, double-buffered plain phase (bandwidth regime): each one-warp
+// CTA walks the tiles of the colour with a grid stride and stages BOTH the w
+// region (2-cell halo) and the b region of the NEXT tile with cp.async while
+// it relaxes the current one, so every resident warp keeps a tile's loads in
+// flight and the 8 passes run on shared memory only.  Per tile the arithmetic
+// is plain_cell on the same values as k_plain_tiles (bitwise identical).
+constexpr int kPPBw = 3 * kRegP;           // w region doubles
+constexpr int kPPBb = 3 * 289;              // b region doubles (17 x 17, odd stride)
+constexpr int kPPBuf = (kPPBw + kPPBb + 1) / 2 * 2;  // even: both buffers 16-byte aligned
+constexpr size_t kPPSmem = 2 * kPPBuf * sizeof(double);
+__device__ __forceinline__ void pp_issue(double* buf, const double* __restrict__ w, const double* __restrict__ b, int n,
+                                         int nn, int x0, int y0, int lane) {
+    stage_w_region(buf, w, n, nn, x0, y0, lane);
+    for (int qq = lane; qq < 289; qq += 32) {
+        const int a = qq % 17, bb = qq / 17;
+        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+        cp_async8(&buf[kPPBw + qq], b + gi);
+        cp_async8(&buf[kPPBw + 289 + qq], b + nn + gi);
+        cp_async8(&buf[kPPBw + 578 + qq], b + 2 * nn + gi);
+    }
+}
+
+__global__ void __launch_bounds__(32) k_plain_tiles_pp(Lev L, int tc, const double* __restrict__ b,
+                                                        double* __restrict__ w, const uint8_t* __restrict__ big,
+                                                        int ty0, int ntiles, Mirror M) {
+    pdl_enter();
+    extern __shared__ __align__(16) double pps[];
+    const int n = L.n, nn = L.nn, lane = threadIdx.x;
+    const int half = (n / kTile) >> 1;
+    auto origin = [&](int t, int& x0, int& y0) {
+        x0 = (2 * (t % half) + (tc & 1)) * kTile;
+        y0 = (ty0 + 2 * (t / half) + (tc >> 1)) * kTile;
+    };
+    int t = blockIdx.x;
+    if (t >= ntiles) return;
+    int x0, y0;
+    origin(t, x0, y0);
+    pp_issue(pps, w, b, n, nn, x0, y0, lane);
+    cp_async_commit();
+    for (int k = 0; t < ntiles; t += gridDim.x, ++k) {
+        const int tn = t + gridDim.x;
+        int xn = 0, yn = 0;
+        if (tn < ntiles) {
+            origin(tn, xn, yn);
+            pp_issue(pps + ((k + 1) & 1) * kPPBuf, w, b, n, nn, xn, yn, lane);
+        }
+        cp_async_commit();
+        const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
+        const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
+        cp_async_wait<1>();
+        __syncwarp();
+        double* buf = pps + (k & 1) * kPPBuf;
+        TileW W{buf};
+        TileB B{buf + kPPBw};
+        for (int pc = 0; pc < 8; ++pc) {
+            const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
+            if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
+            __syncwarp();
+        }
+        for (int q = lane; q < 17 * 17; q += 32) {
+            const int a = q % 17, bb = q / 17, j = wr(y0 + bb, n);
+            const size_t gi = wr(x0 + a, n) + (size_t)j * n;
+            if (bb < 16) {
+                w[gi] = W(0, a, bb);
+                M.store(gi, j, n, W(0, a, bb));
+            }
+            if (a < 16) {
+                w[nn + gi] = W(1, a, bb);
+                M.store(nn + gi, j, n, W(1, a, bb));
+            }
+            if (a < 16 && bb < 16) {
+                w[2 * nn + gi] = W(2, a, bb);
+                M.store(2 * nn + gi, j, n, W(2, a, bb));
+            }
+        }
+        __syncwarp();  // this buffer is refilled two tiles later
+        x0 = xn;
+        y0 = yn;
+    }
+    cp_async_wait<0>();
 }
 
 // Global accessor for plain loads (no __ldg: the big phase writes w in-kernel).
@@ -541,7 +638,7 @@ struct DfArgs {
     double* w;
     unsigned long long* trace;  // debug: per-task globaltimer stamps (nullptr in production)
 };
-constexpr size_t kDfTileBytes = (3 * kReg * kReg + 3 * 289) * sizeof(double);
+constexpr size_t kDfTileBytes = (3 * kRegP + 3 * 289) * sizeof(double);
 constexpr size_t kDfSmem = 2 * sizeof(SlabSlot) + kDfWarps * ((kDfTileBytes + 15) / 16 * 16);
 
 __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
@@ -558,7 +655,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
     const int n = L.n, nn = L.nn, t = threadIdx.x, wid = t >> 5, lane = t & 31, G = gridDim.x;
     const int nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1, nbk = n >> 2;
     double* sw = reinterpret_cast<double*>(dsm + 2 * sizeof(SlabSlot) + wid * ((kDfTileBytes + 15) / 16 * 16));
-    double* sb = sw + 3 * kReg * kReg;
+    double* sb = sw + 3 * kRegP;
     const unsigned epoch = A.DP.epoch;
     // first big slab streams in while the plain tasks run
     int c = 0, q = -1;
@@ -594,7 +691,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
             const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
             const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
             const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-            cp_async16_cg(&sw[f * kReg * kReg + bb * kReg + 2 * a2], A.w + (size_t)f * nn + gi);
+            cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], A.w + (size_t)f * nn + gi);
         }
         for (int qq = lane; qq < 289; qq += 32) {
             const int a = qq % 17, bb = qq / 17;
