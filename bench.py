@@ -152,14 +152,29 @@ def measured_traffic(config, kernel):
         return None
 
 
+def cgs_bytes(step_iters, restart, M):
+    """Compulsory bytes of the fused CGS2 sweeps of FGMRES steps with the given
+    Arnoldi-step counts: at basis index j the three sweeps read V_0..V_j and w
+    (j + 2 vectors) and read+write w twice more (2 (j + 3)), 8 B per DOF."""
+    tot = 0
+    for it in step_iters:
+        j = 0
+        for _ in range(it):
+            tot += (3 * j + 8) * 8 * M
+            j = j + 1 if j + 1 < restart else 0
+    return tot
+
+
 def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     """Algorithmic (compulsory fp64) bytes of all launches of `name` in the
     profiled pass (SURVEY.md §8d per-cell figures x cells)."""
+    if "k_cgs_sweep" in name:
+        return cgs_bytes(ctxinfo["step_iters"], 30, 3 * ctxinfo["N"] ** 2)
     lv = ctxinfo["levels"]  # list of (n, nbig) for multi-tile levels (n >= 32)
     sweeps = 2  # V(1,1)
     N = ctxinfo["N"]
     big_bytes = 3136 * 8 + 2000 * 12 + 56 * 24  # inverse + E' slab (~2000 entries x 12 B) + block w/b traffic
-    if name == "k_plain_tiles":  # levels n > 512: 4 tile-colour launches cover every cell once per sweep
+    if name.startswith("k_plain_tiles"):  # levels n > 512: 4 tile-colour launches cover every cell once per sweep
         return sum(72 * n * n * sweeps for n, _ in lv if n > 512) * vcycles
     if name == "k_big_phase":
         return sum(big_bytes * nb * sweeps for n, nb in lv if n > 512) * vcycles
@@ -254,7 +269,7 @@ def run_ours(args, rank, world):
     if rank == 0:
         # profiled pass (live CUDA-event timing per kernel): first step of each kappa
         prof_tot = {}
-        pv, pit, prs = 0, 0, 0
+        pv, pit, prs, step_iters = 0, 0, 0, []
         for kb in range(len(probs)):
             u.zero_()
             p.zero_()
@@ -270,6 +285,7 @@ def run_ours(args, rank, world):
                 a[1] += cnt
             pv += st["iters"]
             pit += st["iters"]
+            step_iters.append(st["iters"])
             prs += st["restarts"]
         step_prof_ms = sum(v[0] for v in prof_tot.values())
         ranked = sorted(prof_tot.items(), key=lambda kv: -kv[1][0])
@@ -284,7 +300,7 @@ def run_ours(args, rank, world):
         for l, (nl, _) in enumerate(levels):
             nbig = np.mean([int(c.big_blocks(l).sum()) for c in ctxs])
             lv_info.append((nl, nbig))
-        info = {"N": N_GRID, "levels": lv_info}
+        info = {"N": N_GRID, "levels": lv_info, "step_iters": step_iters}
         peak, peak_kind = measured_peak_hbm()
         roof = None
         for name, (tms, cnt) in ranked:
@@ -430,6 +446,9 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--batch", type=int, default=512, help="C5: number of independent N=256 problems")
     ap.add_argument("--workers", type=int, default=16, help="C5: concurrent solver contexts per GPU")
+    ap.add_argument("--slabs", type=int, default=0,
+                    help="C3/C4: slab-partition the problem (DESIGN.md §7): P slabs over the visible GPUs in this "
+                         "process (P2P-fused exchange), or under torchrun one slab per rank over NCCL")
     args = ap.parse_args()
     if args.config == "C5":
         return main_batch(args)
@@ -458,6 +477,8 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    if args.slabs:
+        return run_slabs(args, rank, world)
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -489,6 +510,76 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_slabs(args, rank, world):
+    """One problem slab-partitioned.  world == 1: `--slabs` slabs
+    in this process, slab r on GPU r mod device_count (exchanges fused into the
+    smoother kernels as peer stores); torchrun: one slab per rank over NCCL.
+    Each step goes through the group's public call with host arrays, so the
+    value is end to end (H2D of u^n, X^n, D2H of u, p, X inside), wall clock
+    after the group's device synchronisation, max over ranks."""
+    import torch
+    from paper_1311_5614_b200.ibmg import SlabGroup
+    from paper_1311_5614_b200 import dist as D
+    prob = WL["blocks"][0]
+    N = prob.N
+    kw = dict(rho=prob.rho, mu=prob.mu, dt=prob.dt)
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("gloo")
+        g = SlabGroup.nccl_group(N, **kw)
+        nslab, devs, mode = world, world, "NCCL, one slab per rank"
+    else:
+        nd = max(1, torch.cuda.device_count())
+        devices = [r % nd for r in range(args.slabs)]
+        g = SlabGroup(N, args.slabs, devices=devices, **kw)
+        nslab, devs, mode = args.slabs, len(set(devices)), "in-process, P2P-fused exchange"
+    g.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
+    u, p, X = np.zeros(2 * N * N), np.zeros(N * N), prob.X.reshape(-1).copy()
+    for _ in range(args.warmup):
+        u[:] = 0.0
+        X[:] = prob.X.reshape(-1)
+        g.step_implicit(u, p, X)
+    wall, stats = [], []
+    l0 = g.kernel_launches
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for s in range(args.steps):
+            if s % WL["per"] == 0:
+                u[:] = 0.0
+                X[:] = prob.X.reshape(-1)
+            t0 = time.perf_counter()
+            st = g.step_implicit(u, p, X)
+            wall.append((time.perf_counter() - t0) * 1e3)
+            stats.append(st)
+    tmax, _, _ = D.reduce_stats([float(sum(wall))])
+    if rank == 0:
+        v = float(tmax[0]) / args.steps
+        vc = sum(st["iters"] for st in stats)
+        line = {
+            "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": devs, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded geometry, u0 = 0)",
+            "config": dict(workload_config(), parallelism=f"slab partition x{nslab} on {devs} GPU(s), {mode}",
+                           distributed_levels=g.distributed_levels,
+                           timing="end to end through ibmg_group_step (host arrays), wall clock, max over ranks"),
+            "dof_vcycles_per_s": 3 * N * N * vc / (sum(wall) * 1e-3),
+            "vcycles_per_step": vc / args.steps,
+            "setup_ms_mean": round(float(np.mean([st["setup_ms"] for st in stats])), 3),
+            "solve_ms_mean": round(float(np.mean([st["solve_ms"] for st in stats])), 3),
+            "converged": all(st["converged"] for st in stats),
+            "gpu_launches": g.kernel_launches - l0,
+            "exchanges": g.exchanges,
+            "clocks": clk.summary(),
+            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 8 * (2 * N * N + X.size) * nslab,
+                    "d2h_bytes_per_step": 8 * (3 * N * N + X.size)},
+        }
+        print(json.dumps(line), flush=True)
+    g.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -193,16 +193,23 @@ __global__ void __launch_bounds__(32) k_plain_tiles_pp(Lev L, int tc, const doub
     origin(t, x0, y0);
     pp_issue(pps, w, b, n, nn, x0, y0, lane);
     cp_async_commit();
+    // big-block flags of a tile: loaded one tile ahead (their latency hides
+    // behind the current tile instead of stalling the ballot)
+    auto flag = [&](int xa, int ya) {
+        return lane < 16 ? big[(xa >> 2) + (lane & 3) + ((ya >> 2) + (lane >> 2)) * (n >> 2)] : (uint8_t)0;
+    };
+    uint8_t fcur = flag(x0, y0);
     for (int k = 0; t < ntiles; t += gridDim.x, ++k) {
         const int tn = t + gridDim.x;
         int xn = 0, yn = 0;
+        uint8_t fnext = 0;
         if (tn < ntiles) {
             origin(tn, xn, yn);
             pp_issue(pps + ((k + 1) & 1) * kPPBuf, w, b, n, nn, xn, yn, lane);
+            fnext = flag(xn, yn);
         }
         cp_async_commit();
-        const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * (n >> 2)];
-        const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
+        const unsigned bigmask = __ballot_sync(0xffffffffu, fcur != 0);
         cp_async_wait<1>();
         __syncwarp();
         double* buf = pps + (k & 1) * kPPBuf;
@@ -232,6 +239,7 @@ __global__ void __launch_bounds__(32) k_plain_tiles_pp(Lev L, int tc, const doub
         __syncwarp();  // this buffer is refilled two tiles later
         x0 = xn;
         y0 = yn;
+        fcur = fnext;
     }
     cp_async_wait<0>();
 }
