@@ -123,7 +123,9 @@ int ibmg_step(ibmg_ctx* ctx, double* u, double* p, double* X, ibmg_stats* stats,
 long long ibmg_kernel_launches(const ibmg_ctx* ctx);
 /* Cap the grid of the persistent cooperative kernels (0 = all SMs).  For many
  * concurrent contexts on one GPU (batches of independent problems, C5) a cap of
- * ~SMs/contexts lets their sweeps run side by side instead of serialising. */
+ * ~SMs/contexts lets their sweeps run side by side instead of serialising.  A
+ * cap > 0 also turns programmatic dependent launch off for the context (its
+ * early-resident waiting CTAs would take SMs from the other contexts). */
 int ibmg_set_grid_limit(ibmg_ctx* ctx, int max_ctas);
 /* Per-kernel CUDA-event timing on the context stream (bench roofline evidence):
  * enable=1 starts (and clears) the accumulation; report writes JSON

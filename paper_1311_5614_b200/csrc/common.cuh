@@ -152,23 +152,52 @@ struct GAcc {
     }
 };
 
-// out[face q] += sign * sum_{(k, l) in list(q)} l * F[k][comp]: one warp per
-// face (lists run to hundreds of entries on coarse levels), lanes strided over
-// the entries, fixed butterfly reduction (deterministic spread: no atomics).
-__device__ __forceinline__ void face_gather_warp(const FaceList& FL, const Win& W, const double* __restrict__ F,
-                                                 double* __restrict__ out, int nn, double sign, int q, int lane) {
-    if (q >= FL.nf) return;
-    const int face = FL.face[q];
-    const int comp = face >= nn;
+// out[face q] += sign * sum_{(k, l) in list(q)} l * F[k][comp]: a group of SUB
+// lanes per face (SUB = 32 on coarse levels, whose lists run to thousands of
+// entries; SUB = 8 where every list is <= 32 entries), lanes strided over the
+// entries, then a fixed xor-tree over the group (deterministic spread: no
+// atomics).  All 32 lanes must call it (inactive groups pass active = false).
+template <int SUB>
+__device__ __forceinline__ void face_gather_sub(const FaceList& FL, const Win& W, const double* __restrict__ F,
+                                                double* __restrict__ out, int nn, double sign, int q, bool active,
+                                                int gl) {
     double s = 0.0;
-    for (int e = FL.off[q] + lane; e < FL.off[q + 1]; e += 32) {
-        const int v = FL.ent[e];
-        const int k = v >> 5;
-        s += W.w[(size_t)k * 64 + (v & 31)] * F[2 * k + comp];
+    int face = 0;
+    if (active) {
+        face = FL.face[q];
+        const int comp = face >= nn;
+        const int e1 = FL.off[q + 1];
+        int e = FL.off[q] + gl;
+        // 4 entries per lane in flight (the per-lane summation order is unchanged)
+        for (; e + 3 * SUB < e1; e += 4 * SUB) {
+            int v[4];
+            double a[4], f[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = FL.ent[e + SUB * u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = v[u] >> 5;
+                a[u] = W.w[(size_t)k * 64 + (v[u] & 31)];
+                f[u] = F[2 * k + comp];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s += a[u] * f[u];
+        }
+        for (; e < e1; e += SUB) {
+            const int v = FL.ent[e];
+            const int k = v >> 5;
+            s += W.w[(size_t)k * 64 + (v & 31)] * F[2 * k + comp];
+        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[face] += sign * s;
+    for (int o = SUB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (active && gl == 0) out[face] += sign * s;
+}
+
+// one warp per face (k_face_gather: RHS forces, spread)
+__device__ __forceinline__ void face_gather_warp(const FaceList& FL, const Win& W, const double* __restrict__ F,
+                                                 double* __restrict__ out, int nn, double sign, int q, int lane) {
+    face_gather_sub<32>(FL, W, F, out, nn, sign, q, q < FL.nf, lane);
 }
 
 }  // namespace ibmg

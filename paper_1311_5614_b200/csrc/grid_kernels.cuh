@@ -66,6 +66,7 @@ struct Gather {
     // slab mode: only faces in rows [jlo, jhi) of the level are
     // gathered (the owned rows of a slab); lg = log2(n)
     int lg = 0, jlo = 0, jhi = 1 << 30;
+    int sub = 32;  // lanes per face (8 when every list of the level is <= 32 entries)
 };
 constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point / per face
 
@@ -106,12 +107,15 @@ __device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, 
         if (threadIdx.x == 0)
             while (ld_acquire_u64(G.cnt) < G.target) __nanosleep(32);
         __syncthreads();
-        const int q = (bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5);
-        if (q < G.FL.nf && (G.jlo > 0 || G.jhi < (1 << 30))) {
+        const int lane = threadIdx.x & 31;
+        const int q = ((bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5)) * (32 / G.sub) + lane / G.sub;
+        bool active = q < G.FL.nf;
+        if (active && (G.jlo > 0 || G.jhi < (1 << 30))) {
             const int row = (G.FL.face[q] & (G.nn - 1)) >> G.lg;
-            if (row < G.jlo || row >= G.jhi) return;
+            active = row >= G.jlo && row < G.jhi;
         }
-        face_gather_warp(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, threadIdx.x & 31);
+        if (G.sub == 8) face_gather_sub<8>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane & 7);
+        else face_gather_sub<32>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane);
         return;
     }
     if (bid < pf.nblk) point_force_warp(pf, bid);
@@ -163,54 +167,42 @@ __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const dou
 // Fused residual + restriction (K2): coarse b = R (b - S w) per coarse cell
 // (restrict_saddle, transfers.cpp:107-134; periodic).  The E' part of the
 // restricted residual, R E' w = sum_k L^{l+1}_k F_k, is added afterwards by
-// k_face_gather on the coarse face list.
-__device__ __forceinline__ void residual_restrict_cell(const Lev& F, const double* __restrict__ b,
+// the launch's face-gather CTAs on the coarse face list.  One thread per
+// (coarse cell, component): the 6 (u, v) or 4 (p) fine residual rows of one
+// component (stokes_row, the same expressions as stokes_rows), ~3x fewer
+// registers than a thread per cell with all 16 (occupancy-bound otherwise).
+__device__ __forceinline__ void residual_restrict_comp(const Lev& F, const double* __restrict__ b,
                                                        const double* __restrict__ w, double* __restrict__ bc,
-                                                       double* __restrict__ wc_zero, int q, int q1) {
+                                                       double* __restrict__ wc_zero, int q, int q1, int comp) {
     const int nc = F.n >> 1, nnc = nc * nc;
     if (q >= q1) return;
-    if (wc_zero) {  // the coarse level's zero initial guess, in the same pass
-        wc_zero[q] = 0.0;
-        wc_zero[nnc + q] = 0.0;
-        wc_zero[2 * nnc + q] = 0.0;
-    }
+    if (wc_zero) wc_zero[(size_t)comp * nnc + q] = 0.0;  // the coarse level's zero initial guess
     const int I = q % nc, J = q / nc;
     const int i = 2 * I, j = 2 * J, n = F.n, nn = F.nn;
     GAcc acc{w, n, nn};
-    auto ru_at = [&](int a, int bb) {
+    auto r_at = [&](int f, int a, int bb) {
         a = wr(a, n);
         bb = wr(bb, n);
-        double ru, rv, rp;
-        stokes_rows(F, acc, a, bb, ru, rv, rp);
-        return b[a + bb * n] - ru;
+        return b[(size_t)f * nn + a + bb * n] - stokes_row(F, acc, f, a, bb);
     };
-    auto rv_at = [&](int a, int bb) {
-        a = wr(a, n);
-        bb = wr(bb, n);
-        double ru, rv, rp;
-        stokes_rows(F, acc, a, bb, ru, rv, rp);
-        return b[nn + a + bb * n] - rv;
-    };
-    auto rp_at = [&](int a, int bb) {
-        a = wr(a, n);
-        bb = wr(bb, n);
-        double ru, rv, rp;
-        stokes_rows(F, acc, a, bb, ru, rv, rp);
-        return b[2 * nn + a + bb * n] - rp;
-    };
-    bc[q] = 0.125 * (ru_at(i - 1, j) + 2.0 * ru_at(i, j) + ru_at(i + 1, j) + ru_at(i - 1, j + 1) +
-                     2.0 * ru_at(i, j + 1) + ru_at(i + 1, j + 1));
-    bc[nnc + q] = 0.125 * (rv_at(i, j - 1) + 2.0 * rv_at(i, j) + rv_at(i, j + 1) + rv_at(i + 1, j - 1) +
-                           2.0 * rv_at(i + 1, j) + rv_at(i + 1, j + 1));
-    bc[2 * nnc + q] = 0.25 * (rp_at(i, j) + rp_at(i + 1, j) + rp_at(i, j + 1) + rp_at(i + 1, j + 1));
+    if (comp == 0)
+        bc[q] = 0.125 * (r_at(0, i - 1, j) + 2.0 * r_at(0, i, j) + r_at(0, i + 1, j) + r_at(0, i - 1, j + 1) +
+                         2.0 * r_at(0, i, j + 1) + r_at(0, i + 1, j + 1));
+    else if (comp == 1)
+        bc[nnc + q] = 0.125 * (r_at(1, i, j - 1) + 2.0 * r_at(1, i, j) + r_at(1, i, j + 1) + r_at(1, i + 1, j - 1) +
+                               2.0 * r_at(1, i + 1, j) + r_at(1, i + 1, j + 1));
+    else
+        bc[2 * nnc + q] = 0.25 * (r_at(2, i, j) + r_at(2, i + 1, j) + r_at(2, i, j + 1) + r_at(2, i + 1, j + 1));
 }
 
+// Grid CTAs: ngrid = 3 x CTAs-per-component over coarse cells [q0, q1).
 __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const double* __restrict__ w,
                                     double* __restrict__ bc, double* __restrict__ wc_zero, PForce pf, Gather G,
                                     int ngrid, int q0, int q1) {
     pdl_enter();
     fused_launch(pf, G, ngrid, [&](int blk) {
-        residual_restrict_cell(F, b, w, bc, wc_zero, q0 + blk * blockDim.x + threadIdx.x, q1);
+        const int nbc = ngrid / 3, comp = blk / nbc;
+        residual_restrict_comp(F, b, w, bc, wc_zero, q0 + (blk - comp * nbc) * blockDim.x + threadIdx.x, q1, comp);
     });
 }
 

@@ -910,8 +910,9 @@ PForce pforce(ibmg_ctx* c, const LevelBuf& lb, const double* w, bool active) {
 // the launch's pf.nblk + ngrid producer CTAs (grid_kernels.cuh fused_launch).
 Gather gather(ibmg_ctx* c, const LevelBuf& to, double* out, double sign, const PForce& pf, int ngrid) {
     Gather G{to.FL, to.W, c->F, out, to.L.nn, sign, 0, c->tail_cnt, 0ull};
+    G.sub = to.maxrow <= 32 ? 8 : 32;
     if (pf.nblk) {
-        G.nblk = int(nblk(to.FL.nf, kPfPerCta));
+        G.nblk = int(nblk(to.FL.nf, kPfPerCta * (32 / G.sub)));
         c->tail_base += (unsigned long long)(pf.nblk + ngrid);
         G.target = c->tail_base;
     }
@@ -1052,7 +1053,7 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z
             LevelBuf& nx = c->lev[l + 1];
             for (int s = (l == 0 && first_sweep_done) ? 1 : 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
             const PForce pf = pforce(c, lb, wl(l), nx.FL.nf > 0);
-            const int ng = int(nblk(nx.L.nn));
+            const int ng = 3 * int(nblk(nx.L.nn));
             const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
             LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, bl(l), wl(l), nx.b, wl(l + 1), pf, G,
                    ng, 0, nx.L.nn);
@@ -1368,6 +1369,10 @@ int ibmg_set_grid_limit(ibmg_ctx* c, int max_ctas) {
     return api(c, [&]() -> int {
         if (max_ctas < 0) throw InvalidArg("grid limit must be >= 0");
         c->grid_limit = max_ctas;
+        // contexts sharing a GPU: programmatic dependent launch would keep each
+        // context's next kernel resident (waiting) on SMs the other contexts
+        // could use (measured on C5: 1.74 -> 2.30 ms per problem with it on)
+        if (max_ctas > 0) c->pdl = false;
         return IBMG_OK;
     });
 }

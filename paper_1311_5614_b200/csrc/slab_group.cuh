@@ -455,7 +455,7 @@ void restrict_group(ibmg_group* g, int l) {
         LevelBuf& nx = c->lev[l + 1];
         const int nc = nx.L.n, yc0 = g->plan.y0(r, l) / 2, yc1 = g->plan.y1(r, l) / 2;
         const PForce pf = pforce(c, lb, lb.w, nx.FL.nf > 0);
-        const int ng = int(nblk(size_t(yc1 - yc0) * nc));
+        const int ng = 3 * int(nblk(size_t(yc1 - yc0) * nc));
         Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
         G.lg = nx.L.lg;
         G.jlo = yc0;
@@ -494,7 +494,7 @@ void vtail(ibmg_ctx* c, int la) {
         LevelBuf& nx = c->lev[l + 1];
         for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, lb.b, lb.w);
         const PForce pf = pforce(c, lb, lb.w, nx.FL.nf > 0);
-        const int ng = int(nblk(nx.L.nn));
+        const int ng = 3 * int(nblk(nx.L.nn));
         const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
         LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, (const double*)lb.b,
                (const double*)lb.w, nx.b, nx.w, pf, G, ng, 0, nx.L.nn);
