@@ -123,6 +123,17 @@ class SaddleSystem {
         return x;
     }
 
+    // iteration_matrix_spectrum: Arnoldi Hessenberg matrix of
+    // E = I - V(0, A .) on mean-zero pressure, (m_done + 1) x m_done row-major
+    // (leading block of the (m+1) x m buffer); its eigenvalues are the Ritz values.
+    std::vector<double> iteration_matrix_hessenberg(int m, unsigned long long seed, int* m_done) const {
+        std::vector<double> H(size_t(m + 1) * m);
+        int done = 0;
+        check(ibmg_vcycle_spectrum(ctx_, m, seed, H.data(), &done), ctx_);
+        if (m_done) *m_done = done;
+        return H;
+    }
+
     // step_implicit: u (2N^2) in/out, p (N^2) out, X in/out
     SolveStats step_implicit(std::span<double> u, std::span<double> p, std::span<double> X) {
         if (int(u.size()) != n_vel() || int(p.size()) != N_ * N_ || X.size() != 2 * npts_)

@@ -115,6 +115,13 @@ int ibmg_spread(ibmg_ctx* ctx, const double* F, double* f, int ptr_kind);
  * one V-cycle as right preconditioner, x0 = 0. */
 int ibmg_solve(ibmg_ctx* ctx, const double* b, double* x, ibmg_stats* stats, int ptr_kind);
 
+/* Replaces iteration_matrix_spectrum (§5.2): Arnoldi of
+ * dimension m (<= restart) on the multigrid error-propagation operator
+ * E x = x - V(0, A x), restricted to mean-zero pressure, from a seeded random
+ * start.  H: host (m+1) x m row-major Hessenberg matrix (its eigenvalues are
+ * the Ritz values; rho = max modulus); *m_done = steps completed. */
+int ibmg_vcycle_spectrum(ibmg_ctx* ctx, int m, unsigned long long seed, double* H, int* m_done);
+
 /* Replaces step_implicit: rebuild at X^n, RHS, solve,
  * X^{n+1} = X^n + dt S^T u^{n+1}.  u: 2N^2 in/out, p: N^2 out, X in/out. */
 int ibmg_step(ibmg_ctx* ctx, double* u, double* p, double* X, ibmg_stats* stats, int ptr_kind);

@@ -1648,6 +1648,62 @@ int ibmg_spread(ibmg_ctx* c, const double* Fin, double* f, int ptr_kind) {
     });
 }
 
+// Arnoldi probe of the multigrid iteration matrix (PAPER.md
+// §5.2): E x = x - V(0, A x) on the mean-zero-pressure subspace (V-cycle
+// linear in b from a zero guess), m Arnoldi steps from a seeded random start
+// with the fused CGS2 sweeps of FGMRES.  H (host, (m+1) x m, row-major) gets
+// the Hessenberg matrix; its eigenvalues are the Ritz values, rho = max |.|.
+int ibmg_vcycle_spectrum(ibmg_ctx* c, int m, unsigned long long seed, double* H, int* m_done) {
+    return api(c, [&]() -> int {
+        if (m < 1 || m > c->prm.restart || !H) throw InvalidArg("spectrum: 1 <= m <= restart and H required");
+        const size_t M = c->M, nn = size_t(c->prm.N) * c->prm.N;
+        const int hoff = 0, h2off = c->prm.restart + 2;
+        // seeded start vector (splitmix64 -> U[-1, 1)), pressure mean removed on the device
+        std::vector<double> x0(M);
+        unsigned long long z = seed;
+        for (size_t i = 0; i < M; ++i) {
+            z += 0x9E3779B97F4A7C15ull;
+            unsigned long long t = z;
+            t = (t ^ (t >> 30)) * 0xBF58476D1CE4E5B9ull;
+            t = (t ^ (t >> 27)) * 0x94D049BB133111EBull;
+            t ^= t >> 31;
+            x0[i] = double(t >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+        }
+        CK(cudaMemcpyAsync(c->stage_a, x0.data(), sizeof(double) * M, cudaMemcpyHostToDevice, c->s));
+        pressure_mean_zero(c, c->stage_a);
+        multidot(c, c->stage_a, 1, c->stage_a, h2off, 0);
+        LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, (const double*)c->stage_a, c->V, M, (const double*)(c->dh + h2off),
+               0.0, (double*)nullptr);
+        std::fill(H, H + size_t(m + 1) * m, 0.0);
+        int done = 0;
+        for (int j = 0; j < m; ++j) {
+            double* Vj = c->V + c->Mst * j;
+            double* w = c->stage_b;
+            apply_level(c, 0, Vj, c->wv);
+            vcycle(c, c->wv, w, true);                                      // w = V(0, A v_j), mean-zero p
+            LAUNCH(c, k_b_minus, nblk(M), 256, 0, (const double*)Vj, w, M);  // w = v_j - w
+            pressure_mean_zero(c, w);  // E restricted to mean-zero p: the constant mode (E c = c) stays out
+            cgs_sweep(c, 0, j + 1, nullptr, w, hoff);
+            cgs_sweep(c, 1, j + 1, c->dh + hoff, w, h2off);
+            cgs_sweep(c, 2, j + 1, c->dh + h2off, w, h2off + j + 1);
+            CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (2 * (c->prm.restart + 2)), cudaMemcpyDeviceToHost,
+                               c->s));
+            CK(cudaStreamSynchronize(c->s));
+            for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = c->hpin[hoff + i] + c->hpin[h2off + i];
+            const double hn = std::sqrt(c->hpin[h2off + j + 1]);
+            H[size_t(j + 1) * m + j] = hn;
+            done = j + 1;
+            if (!(hn > 1e-300)) break;  // invariant subspace
+            if (j + 1 < m)
+                LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, (const double*)w, c->V + c->Mst * (j + 1), M,
+                       (const double*)(c->dh + h2off + j + 1), 0.0, (double*)nullptr);
+        }
+        (void)nn;
+        if (m_done) *m_done = done;
+        return IBMG_OK;
+    });
+}
+
 int ibmg_solve(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st, int ptr_kind) {
     ibmg_stats local{};
     if (!st) st = &local;

@@ -49,7 +49,8 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_debug_coarse_trace", "ibmg_slab_plan", "ibmg_group_create", "ibmg_group_destroy",
            "ibmg_group_last_error", "ibmg_group_distributed_levels", "ibmg_group_kernel_launches",
            "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
-           "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl"]
+           "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl",
+           "ibmg_vcycle_spectrum"]
 
 
 def lib_path() -> str:
@@ -102,6 +103,7 @@ def lib(build_if_missing: bool = True):
     L.ibmg_profile.argtypes = [vp, ip]
     L.ibmg_profile_report.argtypes = [vp, C.c_char_p, ip]
     L.ibmg_slab_plan.argtypes = [ip, ip, ip, ip, C.c_long, vp]
+    L.ibmg_vcycle_spectrum.argtypes = [vp, ip, C.c_ulonglong, vp, C.POINTER(C.c_int)]
     L.ibmg_group_create.argtypes = [C.POINTER(Params), ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
     L.ibmg_group_create_nccl.argtypes = [C.POINTER(Params), ip, ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
     L.ibmg_nccl_unique_id.argtypes = [vp]
@@ -303,6 +305,17 @@ class SaddleSystem:
         (up, k), (pp, _), (Xp, _) = _ptr(u), _ptr(p), _ptr(X)
         self._chk(self._L.ibmg_step(self._h, up, pp, Xp, C.byref(st), k), ok=(0, 2))
         return st.as_dict()
+
+    def iteration_matrix_spectrum(self, m=30, seed=1):
+        """Arnoldi probe of E = I - V(0, A .): returns (ritz, H),
+        Ritz values sorted by decreasing modulus; rho = abs(ritz[0])."""
+        H = np.zeros((m + 1) * m)
+        done = C.c_int()
+        self._chk(self._L.ibmg_vcycle_spectrum(self._h, m, seed, H.ctypes.data, C.byref(done)))
+        k = done.value
+        Hm = H.reshape(m + 1, m)[:k, :k]
+        ritz = np.linalg.eigvals(Hm)  # host: eigenvalues of the k x k Hessenberg matrix
+        return ritz[np.argsort(-np.abs(ritz))], H.reshape(m + 1, m)[: k + 1, :k]
 
     @property
     def kernel_launches(self):
