@@ -72,6 +72,12 @@ int ibmg_set_structures(ibmg_ctx* ctx, int n_mem, const int* nb, const double* k
 int ibmg_num_levels(const ibmg_ctx* ctx);
 int ibmg_level_n(const ibmg_ctx* ctx, int level);
 
+/* Time scheme of the IB coupling: implicit = 1 (default) puts
+ * E' = dt S K S^T on the left (step_implicit); implicit = 0 drops it (E' = 0 on
+ * every level, pure Stokes + mass solve) while ibmg_step / ibmg_build_rhs keep
+ * the spread spring forces S F(X^n) on the right: step_explicit (Eqs. 9-12). */
+int ibmg_set_scheme(ibmg_ctx* ctx, int implicit);
+
 /* Replaces SaddleSystem::apply (saddle.cpp:19-38) on level `level` (0 = fine). */
 int ibmg_apply(ibmg_ctx* ctx, int level, const double* w, double* out, int ptr_kind);
 /* Replaces SaddleSystem::residual (saddle.cpp:48-54): r = b - A w, norm optional. */

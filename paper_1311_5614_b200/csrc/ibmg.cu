@@ -157,6 +157,9 @@ struct ibmg_ctx {
     size_t Mk = 0;             // Krylov vector length: M, or 3 rows N for a slab
     int krows = 0;             // fine rows held by the Krylov vectors (N unless a slab)
     std::vector<int> own_y0, own_y1;  // slab: owned rows per distributed level (setup skips other blocks)
+    bool implicit_ib = true;          // false: explicit IB scheme (E' = 0 on the left, forces on the right)
+    std::vector<int> h_nb;            // last structures (re-applied by ibmg_set_scheme)
+    std::vector<double> h_kappa, h_ds, h_X;
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
     bool have_structs = false;
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
@@ -658,7 +661,8 @@ void rebuild(ibmg_ctx* c) {
             lb.FL.ent = c->fl_ent;
             if (l + 1 < c->nlev) {
                 const int reach = h[18];
-                if (reach > 7)
+                // (explicit scheme: E' = 0, nothing couples through the windows)
+                if (reach > 7 && c->implicit_ib)
                     throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 8-cell same-colour gap on level " +
                                      std::to_string(l) + " (Lagrangian spacing too large)");
                 colour_big_blocks(c, lb, lb.h_cm);
@@ -842,7 +846,7 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
         for (int k = 0; k < hnb[m]; ++k) {
             kp[o + k] = o + (k == 0 ? hnb[m] - 1 : k - 1);
             kn[o + k] = o + (k == hnb[m] - 1 ? 0 : k + 1);
-            cE[o + k] = c->prm.dt * hk[m] * h0 * h0;
+            cE[o + k] = c->implicit_ib ? c->prm.dt * hk[m] * h0 * h0 : 0.0;
             kap[o + k] = hk[m];
             ids2[o + k] = 1.0 / (hds[m] * hds[m]);
             dsq[o + k] = hds[m] * hds[m];
@@ -894,6 +898,9 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
     CK(cudaStreamSynchronize(c->s));
     rebuild(c);
     c->have_structs = true;
+    c->h_nb = hnb;
+    c->h_kappa = hk;
+    c->h_ds = hds;
 }
 
 // ---------------- operators ----------------
@@ -1408,6 +1415,18 @@ int ibmg_set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kap
     return api(c, [&]() -> int {
         if (n_mem > 0 && (!nb || !kappa || !ds || !X)) throw InvalidArg("null structure arrays");
         set_structures(c, n_mem, nb, kappa, ds, X, ptr_kind);
+        return IBMG_OK;
+    });
+}
+
+int ibmg_set_scheme(ibmg_ctx* c, int implicit) {
+    return api(c, [&]() -> int {
+        c->implicit_ib = implicit != 0;
+        if (c->have_structs && c->npts) {  // re-upload the E' coefficients at the current X
+            std::vector<double> X(2 * size_t(c->npts));
+            CK(cudaMemcpy(X.data(), c->X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost));
+            set_structures(c, c->nmem, c->h_nb.data(), c->h_kappa.data(), c->h_ds.data(), X.data(), IBMG_PTR_HOST);
+        }
         return IBMG_OK;
     });
 }

@@ -50,7 +50,7 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_group_last_error", "ibmg_group_distributed_levels", "ibmg_group_kernel_launches",
            "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
            "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl",
-           "ibmg_vcycle_spectrum"]
+           "ibmg_vcycle_spectrum", "ibmg_set_scheme"]
 
 
 def lib_path() -> str:
@@ -104,6 +104,7 @@ def lib(build_if_missing: bool = True):
     L.ibmg_profile_report.argtypes = [vp, C.c_char_p, ip]
     L.ibmg_slab_plan.argtypes = [ip, ip, ip, ip, C.c_long, vp]
     L.ibmg_vcycle_spectrum.argtypes = [vp, ip, C.c_ulonglong, vp, C.POINTER(C.c_int)]
+    L.ibmg_set_scheme.argtypes = [vp, ip]
     L.ibmg_group_create.argtypes = [C.POINTER(Params), ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
     L.ibmg_group_create_nccl.argtypes = [C.POINTER(Params), ip, ip, vp, ip, C.c_long, C.POINTER(C.c_void_p)]
     L.ibmg_nccl_unique_id.argtypes = [vp]
@@ -192,6 +193,8 @@ class SaddleSystem:
         self._chk(self._L.ibmg_set_structures(self._h, len(nb), nb.ctypes.data, kappa.ctypes.data,
                                               ds.ctypes.data, xp, kind))
         self.npts = int(nb.sum())
+        self._nb, self._ds = nb.astype(np.int64), ds
+        self._X_host = np.array(X.detach().cpu().numpy() if hasattr(X, "detach") else X, np.float64).reshape(-1)
         return self
 
     @classmethod
@@ -199,6 +202,13 @@ class SaddleSystem:
         s = cls(prob.N, prob.rho, prob.mu, prob.dt, **kw)
         s.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
         return s
+
+    def set_scheme(self, implicit=True):
+        """implicit=True: E' = dt S K S^T on the left (step_implicit); False: the
+        explicit IB scheme: pure Stokes(+mass) on the left,
+        spread spring forces S F(X^n) on the right."""
+        self._chk(self._L.ibmg_set_scheme(self._h, int(bool(implicit))))
+        self._implicit = bool(implicit)
 
     @property
     def num_levels(self):
@@ -299,8 +309,21 @@ class SaddleSystem:
         self._chk(self._L.ibmg_solve(self._h, bp, xp, C.byref(st), k), ok=(0, 2))
         return x, st.as_dict()
 
+    def step_explicit(self, u, p, X):
+        """One explicit IB step in place on (u, p, X): forces at
+        X^n spread to the right-hand side, Stokes(+mass) solve, X^{n+1} = X^n +
+        dt S^T u^{n+1}."""
+        if getattr(self, "_implicit", True):
+            self.set_scheme(False)
+        return self._step(u, p, X)
+
     def step_implicit(self, u, p, X):
         """One backward-Euler implicit step in place on (u, p, X); returns stats."""
+        if not getattr(self, "_implicit", True):
+            self.set_scheme(True)
+        return self._step(u, p, X)
+
+    def _step(self, u, p, X):
         st = Stats()
         (up, k), (pp, _), (Xp, _) = _ptr(u), _ptr(p), _ptr(X)
         self._chk(self._L.ibmg_step(self._h, up, pp, Xp, C.byref(st), k), ok=(0, 2))
@@ -467,3 +490,51 @@ class SlabGroup:
         self._chk(self._L.ibmg_group_step(self._h, u.ctypes.data, p.ctypes.data, X.ctypes.data, C.byref(st)),
                   ok=(0, 2))
         return st.as_dict()
+
+
+def fiber_force_unit(X, nb, ds):
+    """A_f X per unit stiffness (fiber.cpp:34-55): (X_{k+1} - 2 X_k + X_{k-1}) / ds_m^2
+    on each closed membrane; X is (npts, 2)."""
+    X = np.asarray(X, np.float64).reshape(-1, 2)
+    F = np.empty_like(X)
+    o = 0
+    for m, d in zip(nb, ds):
+        Xm = X[o:o + m]
+        F[o:o + m] = (np.roll(Xm, -1, axis=0) - 2.0 * Xm + np.roll(Xm, 1, axis=0)) / (d * d)
+        o += m
+    return F
+
+
+def estimate_alpha_exp(sys_, tol=1e-6, max_iter=1000, seed=0):
+    """alpha_exp = 2 / |lambda_max| of M X = interpolate(stokes_solve(spread(A_f X)))
+    by power iteration (§4.1, Table 1): the critical
+    dt * kappa of the explicit IB scheme.  The Stokes(+mass) solves are FGMRES on
+    the GPU with E' off; A_f is the unit-stiffness spring operator at the
+    context's current X.  Returns (alpha_exp, lambda_max, iterations)."""
+    was = getattr(sys_, "_implicit", True)
+    sys_.set_scheme(False)
+    try:
+        nb, ds = sys_._nb, sys_._ds
+        X0 = sys_._X_host.reshape(-1, 2)
+        N = sys_.N
+        rng = np.random.default_rng(seed)
+        x = rng.uniform(-1.0, 1.0, X0.shape)
+        x /= np.linalg.norm(x)
+        lam_prev = None
+        for it in range(1, max_iter + 1):
+            F = fiber_force_unit(x, nb, ds)
+            f = sys_.spread(F.reshape(-1))
+            b = np.concatenate([f, np.zeros(N * N)])
+            u, _ = sys_.gmres_solve(b)
+            y = sys_.interpolate(u[: 2 * N * N]).reshape(-1, 2)
+            lam = float(np.sum(x * y))
+            nrm = np.linalg.norm(y)
+            if nrm == 0.0:
+                raise RuntimeError("estimate_alpha_exp: zero operator")
+            x = y / nrm
+            if lam_prev is not None and abs(lam - lam_prev) <= tol * abs(lam):
+                return 2.0 / abs(lam), lam, it
+            lam_prev = lam
+        raise RuntimeError("estimate_alpha_exp: power iteration did not converge")
+    finally:
+        sys_.set_scheme(was)
