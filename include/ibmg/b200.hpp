@@ -16,6 +16,8 @@
 // extensions (D1-D3); the packed vectors are [u | v | p] on the periodic grid.
 #pragma once
 
+#include <istream>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -171,6 +173,43 @@ inline std::vector<double> restrict_saddle(const SaddleSystem& s, int level, std
 }
 inline void prolong_saddle_add(const SaddleSystem& s, int level, std::span<const double> ec, std::span<double> wf) {
     check(ibmg_prolong_add(s.handle(), level, ec.data(), wf.data(), IBMG_PTR_HOST), s.handle());
+}
+
+// Mesh text format of the reference (write_fiber_mesh / read_fiber_mesh,
+// fiber.cpp:142-166): header "m1 m2 ds periodic_s1", then "k l x y" per node at
+// 17 significant digits.  A structure set is one block per closed membrane.
+inline void write_fiber_mesh(std::ostream& os, std::span<const double> X, double ds, bool periodic = true) {
+    const size_t m1 = X.size() / 2;
+    const auto prec = os.precision(17);
+    os << m1 << ' ' << 1 << ' ' << ds << ' ' << (periodic ? 1 : 0) << '\n';
+    for (size_t k = 0; k < m1; ++k) os << k << ' ' << 0 << ' ' << X[2 * k] << ' ' << X[2 * k + 1] << '\n';
+    os.precision(prec);
+}
+
+struct MeshBlock {
+    int m1 = 0, m2 = 0;
+    double ds = 0.0;
+    bool periodic = true;
+    std::vector<double> X;  // (x, y) interleaved, l-major
+};
+
+// Next block of the stream; false at end of input.  Errors as the reference's
+// reader (std::runtime_error).
+inline bool read_fiber_mesh(std::istream& is, MeshBlock& out) {
+    int m1 = 0, m2 = 0, per = 0;
+    double ds = 0.0;
+    if (!(is >> m1)) return false;
+    if (!(is >> m2 >> ds >> per)) throw std::runtime_error("read_fiber_mesh: bad header");
+    out = MeshBlock{m1, m2, ds, per != 0, std::vector<double>(2 * size_t(m1) * m2)};
+    for (long q = 0; q < long(m1) * m2; ++q) {
+        int k = 0, l = 0;
+        double x = 0.0, y = 0.0;
+        if (!(is >> k >> l >> x >> y)) throw std::runtime_error("read_fiber_mesh: bad node line");
+        if (k < 0 || k >= m1 || l < 0 || l >= m2) throw std::runtime_error("read_fiber_mesh: node index out of range");
+        out.X[2 * (size_t(l) * m1 + k)] = x;
+        out.X[2 * (size_t(l) * m1 + k) + 1] = y;
+    }
+    return true;
 }
 
 }  // namespace ibmg::b200

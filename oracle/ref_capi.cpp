@@ -205,3 +205,35 @@ int ref_saddle_apply(int n, int m1, double ds, const double* X, double gamma, do
 }
 
 }  // extern "C"
+
+// Mesh text IO through the reference's own writer/reader (fiber.cpp:142-166).
+#include <sstream>
+#include <string>
+extern "C" {
+long ref_write_fiber_mesh(int m1, double ds, const double* X, char* buf, long cap) {
+    try {
+        std::ostringstream os;
+        write_fiber_mesh(os, mesh(m1, ds, X));
+        const std::string s = os.str();
+        if (buf && cap > long(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+        return long(s.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+int ref_read_fiber_mesh(const char* text, int* m1, double* ds, double* X, int cap) {
+    try {
+        std::istringstream is(text);
+        const FiberMesh M = read_fiber_mesh(is);
+        *m1 = M.m1;
+        *ds = M.ds;
+        for (int k = 0; k < M.m1 && k < cap; ++k) {
+            X[2 * k] = M.X.at(k, 0).x;
+            X[2 * k + 1] = M.X.at(k, 0).y;
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+}
