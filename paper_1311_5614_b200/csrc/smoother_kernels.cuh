@@ -806,6 +806,9 @@ __host__ __device__ constexpr int gj_ld(int m) { return 2 * m + 1; }
 __device__ void gauss_jordan(double* M, int m, double* col, int* err) {
     // thread mapping for the elimination: row r = t % 64, column quarter t / 64
     // (no division per element); rows >= m idle.  Requires blockDim = 256, m <= 64.
+    // Per pivot step: warp 0 finds the pivot and snapshots column k (as it will
+    // read after the swap) | swap + scale by the reciprocal | eliminate, 4
+    // independent updates in flight per thread: 3 barriers.
     const int ld = gj_ld(m), t = threadIdx.x;
     const int r = t & 63, cq = t >> 6, q = (2 * m + 3) / 4, c0 = cq * q, c1 = min(2 * m, c0 + q);
     __shared__ int piv;
@@ -823,6 +826,8 @@ __device__ void gauss_jordan(double* M, int m, double* col, int* err) {
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
             }
+            // column k after the swap of rows k and bi
+            for (int i = t; i < m; i += 32) col[i] = M[(i == bi ? k : (i == k ? bi : i)) * ld + k];
             if (t == 0) {
                 piv = bi;
                 pinv = M[bi * ld + k];
@@ -835,20 +840,30 @@ __device__ void gauss_jordan(double* M, int m, double* col, int* err) {
             if (t == 0) atomicOr(err, 2);
             return;
         }
+        const double ipv = 1.0 / pv;
         // swap rows k and p and scale the new pivot row in one pass
         for (int j = t; j < 2 * m; j += blockDim.x) {
             const double a = M[k * ld + j], bp = M[p * ld + j];
-            M[k * ld + j] = bp / pv;
+            M[k * ld + j] = bp * ipv;
             if (p != k) M[p * ld + j] = a;
         }
-        __syncthreads();
-        if (t < m) col[t] = M[t * ld + k];
         __syncthreads();
         if (r < m && r != k) {
             const double f = col[r];
             double* Mr = M + r * ld;
             const double* Mk = M + k * ld;
-            for (int j = c0; j < c1; ++j) Mr[j] -= f * Mk[j];
+            int j = c0;
+            for (; j + 4 <= c1; j += 4) {
+                double x[4], y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    x[u] = Mr[j + u];
+                    y[u] = Mk[j + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) Mr[j + u] = x[u] - f * y[u];
+            }
+            for (; j < c1; ++j) Mr[j] -= f * Mk[j];
         }
         __syncthreads();
     }
