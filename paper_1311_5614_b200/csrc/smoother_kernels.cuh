@@ -686,6 +686,17 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         const int tx = 2 * (i % half) + (tc & 1), ty = 2 * (i / half) + (tc >> 1);
         const int x0 = tx * kTile, y0 = ty * kTile;
         const unsigned long long t_a = A.trace ? gtimer() : 0;
+        // b and the big-block flags are read-only in the sweep: staged before the
+        // dependency wait (off the critical path of the tile-colour chain)
+        for (int qq = lane; qq < 289; qq += 32) {
+            const int a = qq % 17, bb = qq / 17;
+            const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+            cp_async8(&sb[qq], A.b + gi);
+            cp_async8(&sb[289 + qq], A.b + nn + gi);
+            cp_async8(&sb[578 + qq], A.b + 2 * nn + gi);
+        }
+        cp_async_commit();
+        const bool isbig = lane < 16 && A.big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * nbk];
         if (lane < 8) {  // adjacent tiles of smaller tile colour
             const int d = lane < 4 ? lane : lane + 1;  // skip the centre of the 3x3
             const int ax = wr(tx + d % 3 - 1, nt), ay = wr(ty + d / 3 - 1, nt);
@@ -701,15 +712,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
             const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
             cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], A.w + (size_t)f * nn + gi);
         }
-        for (int qq = lane; qq < 289; qq += 32) {
-            const int a = qq % 17, bb = qq / 17;
-            const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-            cp_async8(&sb[qq], A.b + gi);
-            cp_async8(&sb[289 + qq], A.b + nn + gi);
-            cp_async8(&sb[578 + qq], A.b + 2 * nn + gi);
-        }
         cp_async_commit();
-        const bool isbig = lane < 16 && A.big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * nbk];
         const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
         cp_async_wait<0>();
         __syncwarp();
