@@ -706,11 +706,14 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         }
         __syncwarp();
         const unsigned long long t_b = A.trace ? gtimer() : 0;
-        for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs, L2 only
-            const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
-            const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
-            const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-            cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], A.w + (size_t)f * nn + gi);
+        if (lane < 30) {  // 16-byte pairs, L2 only: lane -> (pair lane % 10, rows lane / 10 + 3 k)
+            const int a2 = lane % 10, r0 = lane / 10;
+            const int xg = wr(x0 - 2 + 2 * a2, n);
+            for (int row = r0; row < 3 * kReg; row += 3) {  // row = f * kReg + bb
+                const int f = row / kReg, bb = row - f * kReg;
+                const size_t gi = xg + (size_t)wr(y0 - 2 + bb, n) * n;
+                cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], A.w + (size_t)f * nn + gi);
+            }
         }
         cp_async_commit();
         const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
@@ -725,12 +728,21 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
             __syncwarp();
         }
         const unsigned long long t_p = A.trace ? gtimer() : 0;
-        for (int qq = lane; qq < 17 * 17; qq += 32) {
-            const int a = qq % 17, bb = qq / 17;
-            const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-            if (bb < 16) __stcg(A.w + gi, W(0, a, bb));
-            if (a < 16) __stcg(A.w + nn + gi, W(1, a, bb));
-            if (a < 16 && bb < 16) __stcg(A.w + 2 * nn + gi, W(2, a, bb));
+        {  // write set: u faces i in [x0, x0+16], v faces j in [y0, y0+16], p cells.
+           // Half-warps take alternate rows, lane & 15 the column (few index
+           // operations: one warp per scheduler here, every instruction's latency
+           // is on the tile chain); lanes 0..15 then store the u column x0 + 16.
+            const int a = lane & 15, h = lane >> 4;
+            const int xa = wr(x0 + a, n);
+            for (int bb = h; bb < 17; bb += 2) {
+                const size_t gi = xa + (size_t)wr(y0 + bb, n) * n;
+                if (bb < 16) {
+                    __stcg(A.w + gi, W(0, a, bb));
+                    __stcg(A.w + 2 * nn + gi, W(2, a, bb));
+                }
+                __stcg(A.w + nn + gi, W(1, a, bb));
+            }
+            if (lane < 16) __stcg(A.w + wr(x0 + 16, n) + (size_t)wr(y0 + lane, n) * n, W(0, 16, lane));
         }
         __syncwarp();
         if (lane == 0) {  // warp-synchronous stores + st.release.gpu (cumulative) publish the tile
