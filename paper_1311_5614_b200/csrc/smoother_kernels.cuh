@@ -87,11 +87,13 @@ struct TileW {
 __device__ __forceinline__ void stage_w_region(double* sw, const double* __restrict__ w, int n, int nn, int x0, int y0,
                                                int lane) {
     static_assert(kRegS % 2 == 0, "16-byte staging needs 16-byte aligned rows");
-    for (int qq = lane; qq < 3 * kReg * (kReg / 2); qq += 32) {  // 16-byte pairs
-        const int f = qq / (kReg * kReg / 2), r = qq % (kReg * kReg / 2);
-        const int a2 = r % (kReg / 2), bb = r / (kReg / 2);
-        const size_t gi = wr(x0 - 2 + 2 * a2, n) + (size_t)wr(y0 - 2 + bb, n) * n;
-        cp_async16(&sw[f * kRegP + bb * kRegS + 2 * a2], w + (size_t)f * nn + gi);
+    if (lane < 30) {  // 16-byte pairs: lane -> (pair lane % 10, rows lane / 10 + 3 k)
+        const int a2 = lane % 10, r0 = lane / 10;
+        const int xg = wr(x0 - 2 + 2 * a2, n);
+        for (int row = r0; row < 3 * kReg; row += 3) {  // row = f * kReg + bb
+            const int f = row / kReg, bb = row - f * kReg;
+            cp_async16(&sw[f * kRegP + bb * kRegS + 2 * a2], w + (size_t)f * nn + xg + (size_t)wr(y0 - 2 + bb, n) * n);
+        }
     }
 }
 
@@ -167,12 +169,15 @@ constexpr size_t kPPSmem = 2 * kPPBuf * sizeof(double);
 __device__ __forceinline__ void pp_issue(double* buf, const double* __restrict__ w, const double* __restrict__ b, int n,
                                          int nn, int x0, int y0, int lane) {
     stage_w_region(buf, w, n, nn, x0, y0, lane);
-    for (int qq = lane; qq < 289; qq += 32) {
-        const int a = qq % 17, bb = qq / 17;
-        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-        cp_async8(&buf[kPPBw + qq], b + gi);
-        cp_async8(&buf[kPPBw + 289 + qq], b + nn + gi);
-        cp_async8(&buf[kPPBw + 578 + qq], b + 2 * nn + gi);
+    if (lane < 17) {  // b region 17 x 17: lane = column, one row per step
+        const int xb = wr(x0 + lane, n);
+        for (int bb = 0; bb < 17; ++bb) {
+            const size_t gi = xb + (size_t)wr(y0 + bb, n) * n;
+            const int sq = bb * 17 + lane;
+            cp_async8(&buf[kPPBw + sq], b + gi);
+            cp_async8(&buf[kPPBw + 289 + sq], b + nn + gi);
+            cp_async8(&buf[kPPBw + 578 + sq], b + 2 * nn + gi);
+        }
     }
 }
 
@@ -220,20 +225,27 @@ __global__ void __launch_bounds__(32) k_plain_tiles_pp(Lev L, int tc, const doub
             if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
             __syncwarp();
         }
-        for (int q = lane; q < 17 * 17; q += 32) {
-            const int a = q % 17, bb = q / 17, j = wr(y0 + bb, n);
-            const size_t gi = wr(x0 + a, n) + (size_t)j * n;
-            if (bb < 16) {
-                w[gi] = W(0, a, bb);
-                M.store(gi, j, n, W(0, a, bb));
-            }
-            if (a < 16) {
+        {  // write set (as k_plain_tiles): half-warps take alternate rows, lane & 15
+           // the column; lanes 0..15 then store the u column x0 + 16
+            const int a = lane & 15, h = lane >> 4;
+            const int xa = wr(x0 + a, n);
+            for (int bb = h; bb < 17; bb += 2) {
+                const int j = wr(y0 + bb, n);
+                const size_t gi = xa + (size_t)j * n;
+                if (bb < 16) {
+                    w[gi] = W(0, a, bb);
+                    M.store(gi, j, n, W(0, a, bb));
+                    w[2 * nn + gi] = W(2, a, bb);
+                    M.store(2 * nn + gi, j, n, W(2, a, bb));
+                }
                 w[nn + gi] = W(1, a, bb);
                 M.store(nn + gi, j, n, W(1, a, bb));
             }
-            if (a < 16 && bb < 16) {
-                w[2 * nn + gi] = W(2, a, bb);
-                M.store(2 * nn + gi, j, n, W(2, a, bb));
+            if (lane < 16) {
+                const int j = wr(y0 + lane, n);
+                const size_t gi = wr(x0 + 16, n) + (size_t)j * n;
+                w[gi] = W(0, 16, lane);
+                M.store(gi, j, n, W(0, 16, lane));
             }
         }
         __syncwarp();  // this buffer is refilled two tiles later
