@@ -66,3 +66,25 @@ def test_product_path_never_loads_the_oracle():
             assert not re.search(r"import oracle|from oracle|libibmg_oracle|orc_", src), f
     for f in os.listdir(os.path.join(pkg, "csrc")):
         assert "orc_" not in open(os.path.join(pkg, "csrc", f)).read(), f
+
+
+@pytest.mark.parametrize("nslabs,N,restart", [(0, 64, 30), (9, 64, 30), (3, 64, 30), (2, 12, 30), (2, 64, 64)])
+def test_group_create_rejects_invalid_params(nslabs, N, restart):
+    """Slab groups validate like contexts (status 1, no handle), before any CUDA call."""
+    p = ibmg.Params(N, 1.0, 1.0, 1e-2, 1, 1, restart, 100, 1e-10, 4, 0)
+    h = C.c_void_p()
+    L = ibmg.lib()
+    dev = (C.c_int * 9)(*([0] * 9))
+    assert L.ibmg_group_create(C.byref(p), nslabs, dev, 64, 0, C.byref(h)) == 1 and not h.value
+    assert L.ibmg_group_create_nccl(C.byref(p), 0, nslabs, b"\0" * 128, 64, 0, C.byref(h)) == 1 and not h.value
+
+
+def test_group_null_handles():
+    L = ibmg.lib()
+    assert L.ibmg_group_distributed_levels(None) == -1
+    assert L.ibmg_group_kernel_launches(None) == -1
+    assert L.ibmg_group_last_error(None) == b"null group"
+    x = np.zeros(4)
+    assert L.ibmg_group_vcycle(None, x.ctypes.data, x.ctypes.data) == 1
+    assert L.ibmg_vcycle_spectrum(None, 4, 1, x.ctypes.data, None) == 1
+    assert L.ibmg_set_scheme(None, 0) == 1
