@@ -1675,7 +1675,7 @@ int ibmg_spread(ibmg_ctx* c, const double* Fin, double* f, int ptr_kind) {
 int ibmg_vcycle_spectrum(ibmg_ctx* c, int m, unsigned long long seed, double* H, int* m_done) {
     return api(c, [&]() -> int {
         if (m < 1 || m > c->prm.restart || !H) throw InvalidArg("spectrum: 1 <= m <= restart and H required");
-        const size_t M = c->M, nn = size_t(c->prm.N) * c->prm.N;
+        const size_t M = c->M;
         const int hoff = 0, h2off = c->prm.restart + 2;
         // seeded start vector (splitmix64 -> U[-1, 1)), pressure mean removed on the device
         std::vector<double> x0(M);
@@ -1717,7 +1717,6 @@ int ibmg_vcycle_spectrum(ibmg_ctx* c, int m, unsigned long long seed, double* H,
                 LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, (const double*)w, c->V + c->Mst * (j + 1), M,
                        (const double*)(c->dh + h2off + j + 1), 0.0, (double*)nullptr);
         }
-        (void)nn;
         if (m_done) *m_done = done;
         return IBMG_OK;
     });
