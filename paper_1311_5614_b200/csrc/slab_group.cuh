@@ -66,31 +66,30 @@ struct NcclApi {
     decltype(&ncclAllGather) AllGather = nullptr;
 };
 
-const NcclApi* nccl_api() {
+const NcclApi* nccl_load() {
     static NcclApi api;
-    static bool tried = false, ok = false;
-    if (!tried) {
-        tried = true;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-        if (h) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return nullptr;
 #define IBMG_NCCL_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
-            IBMG_NCCL_SYM(GetUniqueId);
-            IBMG_NCCL_SYM(CommInitRank);
-            IBMG_NCCL_SYM(CommDestroy);
-            IBMG_NCCL_SYM(GetErrorString);
-            IBMG_NCCL_SYM(GroupStart);
-            IBMG_NCCL_SYM(GroupEnd);
-            IBMG_NCCL_SYM(Send);
-            IBMG_NCCL_SYM(Recv);
-            IBMG_NCCL_SYM(AllReduce);
-            IBMG_NCCL_SYM(AllGather);
+    IBMG_NCCL_SYM(GetUniqueId);
+    IBMG_NCCL_SYM(CommInitRank);
+    IBMG_NCCL_SYM(CommDestroy);
+    IBMG_NCCL_SYM(GetErrorString);
+    IBMG_NCCL_SYM(GroupStart);
+    IBMG_NCCL_SYM(GroupEnd);
+    IBMG_NCCL_SYM(Send);
+    IBMG_NCCL_SYM(Recv);
+    IBMG_NCCL_SYM(AllReduce);
+    IBMG_NCCL_SYM(AllGather);
 #undef IBMG_NCCL_SYM
-            ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GetErrorString && api.GroupStart &&
-                 api.GroupEnd && api.Send && api.Recv && api.AllReduce && api.AllGather;
-        }
-    }
+    const bool ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GetErrorString && api.GroupStart &&
+                    api.GroupEnd && api.Send && api.Recv && api.AllReduce && api.AllGather;
     return ok ? &api : nullptr;
+}
+const NcclApi* nccl_api() {
+    static const NcclApi* api = nccl_load();  // thread-safe one-time initialisation
+    return api;
 }
 const NcclApi& nccl() {
     const NcclApi* a = nccl_api();
