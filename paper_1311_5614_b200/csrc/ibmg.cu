@@ -710,6 +710,7 @@ void rebuild(ibmg_ctx* c) {
             }
             LAUNCH(c, k_erows, grid, 32 * kEWarps, 0, R, c->fl_face, c->fl_off, c->fl_ent, c->P, 1, c->e_cnt,
                    c->e_rp, c->e_col, c->e_val);
+            tr.mark("launched erows fill");
             for (int l = 0; l < c->nlev; ++l) {
                 LevelBuf& lb = c->lev[l];
                 lb.E.rp = c->e_rp + R.start[l];
@@ -751,15 +752,18 @@ void rebuild(ibmg_ctx* c) {
                 c->slo_cap = int(grow_cap(nball + 1, c->slo_cap));
                 c->sl_off = dalloc<int>(size_t(c->slo_cap));
             }
+            tr.mark("built block levels");
             LAUNCH(c, k_block_rows, nblk(size_t(nball) * 40), 256, 0, S);
             CK(cudaMemsetAsync(c->cnt + nball, 0, sizeof(int), c->s));
             LAUNCH(c, k_slab_count, nblk(nball, 128), 128, 0, S, c->cnt, c->counters, kCtr);
+            tr.mark("launched slab count");
             size_t bytes = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cnt, c->sl_off, nball + 1, c->s);
             ensure_cub(c, bytes);
             CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, c->sl_off, nball + 1, c->s));
             CK(cudaMemcpyAsync(c->counters + kCtrSlabTot, c->sl_off + nball, sizeof(int), cudaMemcpyDeviceToDevice,
                                c->s));
+            tr.mark("scanned slabs");
             // all levels' box inverses in one launch (each CTA is a latency-bound
             // 56-step Gauss-Jordan; one launch overlaps the levels)
             BInvLevels BL{};

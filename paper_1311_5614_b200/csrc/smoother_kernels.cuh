@@ -824,75 +824,106 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
 
 // ---- setup: dense local matrices and their inverses --------------------------
 
-// Gauss-Jordan with partial pivoting on an m x 2m augmented matrix in shared
-// memory (row-major, ld = 2m).  Ties in the pivot search go to the lowest row.
-// Row stride of the augmented matrices: 2m + 1 (odd) keeps the per-row
-// accesses of a warp on distinct shared-memory banks.
-__host__ __device__ constexpr int gj_ld(int m) { return 2 * m + 1; }
+// Dense local inverses: the m x m matrix is assembled in shared memory (row
+// stride m + 1, odd: a warp's per-row accesses hit distinct banks) and
+// inverted by gauss_jordan below.
+__host__ __device__ constexpr int gj_ld(int m) { return m + 1; }
 
-__device__ void gauss_jordan(double* M, int m, double* col, int* err) {
-    // thread mapping for the elimination: row r = t % 64, column quarter t / 64
-    // (no division per element); rows >= m idle.  Requires blockDim = 256, m <= 64.
-    // Per pivot step: warp 0 finds the pivot and snapshots column k (as it will
-    // read after the swap) | swap + scale by the reciprocal | eliminate, 4
-    // independent updates in flight per thread: 3 barriers.
-    const int ld = gj_ld(m), t = threadIdx.x;
-    const int r = t & 63, cq = t >> 6, q = (2 * m + 3) / 4, c0 = cq * q, c1 = min(2 * m, c0 + q);
-    __shared__ int piv;
-    __shared__ double pinv;
+__device__ void gauss_jordan(const double* __restrict__ M, int m, double* __restrict__ out, int* err) {
+    // Gauss-Jordan with partial pivoting on [A | I], register-resident: thread
+    // (row r = t & 63, quarter cq = t >> 6) holds columns [cq Q, cq Q + Q) of
+    // row r, Q = ceil(2m / 4) <= 28.  Rows are not swapped: step k takes the
+    // unused row with the largest |a_rk| (lowest index on ties) as pivot row,
+    // scales it by the reciprocal and eliminates column k from every other row
+    // (the arithmetic of the row-swapping variant); the inverse's row k is row
+    // piv(k) of the right half.  Per step only column k and the pivot row pass
+    // through shared memory, double-buffered by step parity: 3 barriers.
+    // M: the assembled A (row stride gj_ld(m)); out: inverse, column-major.
+    // Requires blockDim = 256, m <= 56.
+    constexpr int QMAX = 28;
+    __shared__ double colk[2][64];
+    __shared__ double prow[2][4 * QMAX];
+    __shared__ int used[64], stepof[64];
+    __shared__ int sp;
+    __shared__ double spv;
+    const int ld = gj_ld(m), t = threadIdx.x, r = t & 63, cq = t >> 6;
+    const int Q = (2 * m + 3) / 4, c0 = cq * Q;
+    const bool active = r < m;
+    double a[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) {
+        const int c = c0 + j;
+        a[j] = (!active || j >= Q || c >= 2 * m) ? 0.0 : (c < m ? M[r * ld + c] : (c - m == r ? 1.0 : 0.0));
+    }
+    if (t < 64) used[t] = 0;
+    __syncthreads();
     for (int k = 0; k < m; ++k) {
+        const int b = k & 1, kq = k / Q, kj = k - kq * Q;
+        if (active && cq == kq) {
+            double v = 0.0;
+#pragma unroll
+            for (int j = 0; j < QMAX; ++j)
+                if (j == kj) v = a[j];
+            colk[b][r] = v;
+        }
+        __syncthreads();
         if (t < 32) {
             double best = -1.0;
-            int bi = k;
-            for (int i = k + t; i < m; i += 32) {
-                const double v = fabs(M[i * ld + k]);
-                if (v > best) { best = v; bi = i; }
+            int bi = 64;
+            for (int i = t; i < m; i += 32) {
+                const double v = fabs(colk[b][i]);
+                if (!used[i] && v > best) {
+                    best = v;
+                    bi = i;
+                }
             }
             for (int o = 16; o > 0; o >>= 1) {
                 const double ob = __shfl_xor_sync(0xffffffffu, best, o);
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
             }
-            // column k after the swap of rows k and bi
-            for (int i = t; i < m; i += 32) col[i] = M[(i == bi ? k : (i == k ? bi : i)) * ld + k];
             if (t == 0) {
-                piv = bi;
-                pinv = M[bi * ld + k];
+                sp = bi;
+                spv = bi < m ? colk[b][bi] : 0.0;
+                if (bi < m) {
+                    used[bi] = 1;
+                    stepof[bi] = k;
+                }
             }
         }
         __syncthreads();
-        const int p = piv;
-        const double pv = pinv;
+        const int p = sp;
+        const double pv = spv;
         if (pv == 0.0) {
             if (t == 0) atomicOr(err, 2);
             return;
         }
-        const double ipv = 1.0 / pv;
-        // swap rows k and p and scale the new pivot row in one pass
-        for (int j = t; j < 2 * m; j += blockDim.x) {
-            const double a = M[k * ld + j], bp = M[p * ld + j];
-            M[k * ld + j] = bp * ipv;
-            if (p != k) M[p * ld + j] = a;
-        }
-        __syncthreads();
-        if (r < m && r != k) {
-            const double f = col[r];
-            double* Mr = M + r * ld;
-            const double* Mk = M + k * ld;
-            int j = c0;
-            for (; j + 4 <= c1; j += 4) {
-                double x[4], y[4];
+        if (active && r == p) {
+            const double ipv = 1.0 / pv;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    x[u] = Mr[j + u];
-                    y[u] = Mk[j + u];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) Mr[j + u] = x[u] - f * y[u];
+            for (int j = 0; j < QMAX; ++j) {
+                a[j] *= ipv;
+                if (j < Q) prow[b][c0 + j] = a[j];
             }
-            for (; j < c1; ++j) Mr[j] -= f * Mk[j];
         }
         __syncthreads();
+        if (active && r != p) {
+            const double f = colk[b][r];
+#pragma unroll
+            for (int j = 0; j < QMAX; ++j)
+                if (j < Q) a[j] -= f * prow[b][c0 + j];
+        }
+    }
+    if (active) {
+        const int k = stepof[r];
+#pragma unroll
+        for (int j = 0; j < QMAX; ++j) {
+            const int c = c0 + j;
+            if (j < Q && c >= m && c < 2 * m) out[(size_t)(c - m) * m + k] = a[j];
+        }
     }
 }
 
@@ -928,7 +959,6 @@ struct BInvLevels {
 __global__ void k_block_inverse(BInvLevels BL, int* err) {
     pdl_enter();
     extern __shared__ double M[];  // 56 x gj_ld(56)
-    __shared__ double col[56];
     int lv = 0;
     while (lv + 1 < BL.nlev && (int)blockIdx.x >= BL.start[lv + 1]) ++lv;
     const Lev L = BL.L[lv];
@@ -941,10 +971,7 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
     const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
     if (B / nbk < BL.bylo[lv] || B / nbk >= BL.byhi[lv]) return;  // another slab's block
     constexpr int LD = gj_ld(56);
-    for (int idx = t; idx < 56 * LD; idx += nt) {
-        const int i = idx / LD, j = idx % LD;
-        M[idx] = (j == 56 + i) ? 1.0 : 0.0;
-    }
+    for (int idx = t; idx < 56 * LD; idx += nt) M[idx] = 0.0;
     __syncthreads();
     if (t < 56) {
         int f, i, j;
@@ -965,11 +992,7 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
         }
     }
     __syncthreads();
-    gauss_jordan(M, 56, col, err);
-    for (int idx = t; idx < 56 * 56; idx += nt) {
-        const int c = idx / 56, r = idx % 56;
-        Ainv[(size_t)q * 3136 + idx] = M[r * LD + 56 + c];
-    }
+    gauss_jordan(M, 56, Ainv + (size_t)q * 3136, err);
 }
 
 // Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
@@ -977,12 +1000,8 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
 __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict__ Ainv, int* err) {
     pdl_enter();
     extern __shared__ double M[];
-    __shared__ double col[64];
     const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = gj_ld(m), t = threadIdx.x, nt = blockDim.x;
-    for (int idx = t; idx < m * ld; idx += nt) {
-        const int i = idx / ld, j = idx % ld;
-        M[idx] = (j == m + i) ? 1.0 : 0.0;
-    }
+    for (int idx = t; idx < m * ld; idx += nt) M[idx] = 0.0;
     __syncthreads();
     if (t < 3 * nn) {
         const int f = t / nn, i = (t % nn) % n, j = (t % nn) / n;
@@ -1000,11 +1019,7 @@ __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict_
         for (int e = E.rp[q]; e < E.rp[q + 1]; ++e) M[r * ld + E.col[e]] -= E.val[e];
     }
     __syncthreads();
-    gauss_jordan(M, m, col, err);
-    for (int idx = t; idx < m * m; idx += nt) {
-        const int c = idx / m, r = idx % m;
-        Ainv[idx] = M[r * ld + m + c];
-    }
+    gauss_jordan(M, m, Ainv, err);
 }
 
 // E' row range (begin, end) of each of the 40 velocity DOFs of every big block
