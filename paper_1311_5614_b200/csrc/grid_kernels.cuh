@@ -206,6 +206,141 @@ __global__ void k_residual_restrict(Lev F, const double* __restrict__ b, const d
     });
 }
 
+// Tiled residual + restriction for levels whose coarse side is >= 32 (the
+// bandwidth regime; same arithmetic, term order and results as
+// residual_restrict_comp).  A grid CTA owns a 32 x 8 tile of coarse cells: it
+// stages the fine w region [x0-2, x0+66) x [y0-2, y0+17) of all three fields
+// into shared memory with 16-byte cp.async (every fine value crosses HBM once
+// per launch, up to the 2-cell halo), loads its b values straight from
+// global, and each thread then forms the 16 fine residual rows of one coarse
+// cell from double2 shared loads (lane I reads columns 2I.., 16 B apart: no
+// bank conflicts).  Tiles with rows past q1 (slab ends) skip those rows.
+constexpr int kRrTx = 32, kRrTy = 8;
+constexpr int kRrW = 2 * kRrTx + 4, kRrH = 2 * kRrTy + 3;
+struct RrSmem {
+    double s[3][kRrH][kRrW];
+};
+
+__device__ __forceinline__ void rr_cp16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+__device__ __forceinline__ void residual_restrict_tile(const Lev& F, const double* __restrict__ b,
+                                                       const double* __restrict__ w, double* __restrict__ bc,
+                                                       double* __restrict__ wc_zero, int blk, int q0, int q1,
+                                                       RrSmem& S) {
+    const int n = F.n, nn = F.nn, nc = n >> 1, nnc = nc * nc;
+    const int ntx = nc / kRrTx, Jb = q0 / nc, Je = q1 / nc;
+    const int ty = blk / ntx, tx = blk - ty * ntx;
+    const int x0 = 2 * tx * kRrTx, y0 = 2 * (Jb + ty * kRrTy);
+    constexpr int kPairs = kRrW / 2;
+    for (int e = threadIdx.x; e < 3 * kRrH * kPairs; e += blockDim.x) {
+        const int f = e / (kRrH * kPairs), rem = e - f * (kRrH * kPairs);
+        const int r = rem / kPairs, pc = rem - r * kPairs;
+        rr_cp16(&S.s[f][r][2 * pc], w + (size_t)f * nn + wr(x0 - 2 + 2 * pc, n) + (size_t)wr(y0 - 2 + r, n) * n);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int I = threadIdx.x & 31, J = threadIdx.x >> 5;
+    const int Ic = tx * kRrTx + I, Jc = Jb + ty * kRrTy + J;
+    const bool act = Jc < Je;
+    const int q = Ic + Jc * nc;
+    // b values of the cell's residual rows (fine x 2Ic-2.., rows as below)
+    double2 bu[2][2], bv[3], bp[2];
+    if (act) {
+        const int xm = wr(2 * Ic - 2, n), xc = 2 * Ic;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const size_t row = (size_t)(2 * Jc + k) * n;
+            bu[k][0] = __ldg(reinterpret_cast<const double2*>(b + row + xm));
+            bu[k][1] = __ldg(reinterpret_cast<const double2*>(b + row + xc));
+            bp[k] = __ldg(reinterpret_cast<const double2*>(b + 2 * (size_t)nn + row + xc));
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            bv[k] = __ldg(reinterpret_cast<const double2*>(b + nn + (size_t)wr(2 * Jc - 1 + k, n) * n + xc));
+        if (wc_zero) {
+            wc_zero[q] = 0.0;
+            wc_zero[nnc + q] = 0.0;
+            wc_zero[2 * nnc + q] = 0.0;
+        }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    if (!act) return;
+    const double d = F.d, cc = F.c, g = F.g;
+    auto ld2 = [&](int f, int r, int c) { return *reinterpret_cast<const double2*>(&S.s[f][r][c]); };
+    const int c0 = 2 * I;  // smem column of fine x = 2Ic - 2
+    // ---- u: smem rows 2J+1 .. 2J+4 (fine y 2Jc-1 .. 2Jc+2), columns c0 .. c0+5
+    double u[4][6];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+            const double2 t = ld2(0, 2 * J + 1 + k, c0 + 2 * h);
+            u[k][2 * h] = t.x;
+            u[k][2 * h + 1] = t.y;
+        }
+    double pu[2][4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double2 t = ld2(2, 2 * J + 2 + k, c0 + 2 * h);
+            pu[k][2 * h] = t.x;
+            pu[k][2 * h + 1] = t.y;
+        }
+    // u residual at fine (2Ic - 2 + ci, 2Jc + k - 1), ci in 1..3, k in 1..2
+    auto ru = [&](int k, int ci) {
+        const double bb = (ci & 1) ? ((ci == 1) ? bu[k - 1][0].y : bu[k - 1][1].y) : bu[k - 1][1].x;
+        return bb - (d * u[k][ci] - cc * (u[k][ci - 1] + u[k][ci + 1] + u[k - 1][ci] + u[k + 1][ci]) +
+                     g * (pu[k - 1][ci] - pu[k - 1][ci - 1]));
+    };
+    bc[q] = 0.125 * (ru(1, 1) + 2.0 * ru(1, 2) + ru(1, 3) + ru(2, 1) + 2.0 * ru(2, 2) + ru(2, 3));
+    // ---- p rows: u(x+1, y) - u(x, y) and v(x, y+1) - v(x, y), fine (2Ic + a, 2Jc + bb)
+    double v[5][6];
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+            const double2 t = ld2(1, 2 * J + k, c0 + 2 * h);
+            v[k][2 * h] = t.x;
+            v[k][2 * h + 1] = t.y;
+        }
+    auto rp = [&](int a, int bb) {
+        const double2 t = bp[bb];
+        const double bval = a ? t.y : t.x;
+        return bval - (-g * (u[1 + bb][3 + a] - u[1 + bb][2 + a]) - g * (v[3 + bb][2 + a] - v[2 + bb][2 + a]));
+    };
+    bc[2 * nnc + q] = 0.25 * (rp(0, 0) + rp(1, 0) + rp(0, 1) + rp(1, 1));
+    // ---- v: smem rows 2J .. 2J+4 (fine y 2Jc-2 .. 2Jc+2); residual rows k in 1..3
+    double pv[4][2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double2 t = ld2(2, 2 * J + k, c0 + 2);
+        pv[k][0] = t.x;
+        pv[k][1] = t.y;
+    }
+    auto rv = [&](int k, int ci) {
+        const double bb = (ci == 2) ? bv[k - 1].x : bv[k - 1].y;
+        return bb - (d * v[k][ci] - cc * (v[k - 1][ci] + v[k + 1][ci] + v[k][ci - 1] + v[k][ci + 1]) +
+                     g * (pv[k][ci - 2] - pv[k - 1][ci - 2]));
+    };
+    bc[nnc + q] = 0.125 * (rv(1, 2) + 2.0 * rv(2, 2) + rv(3, 2) + rv(1, 3) + 2.0 * rv(2, 3) + rv(3, 3));
+}
+
+// Grid CTAs: ngrid = (nc / 32) x ceil(rows / 8) tiles over coarse rows
+// [q0 / nc, q1 / nc) (q0, q1 whole coarse rows; nc >= 32).
+__global__ void __launch_bounds__(256) k_residual_restrict_t(Lev F, const double* __restrict__ b,
+                                                             const double* __restrict__ w, double* __restrict__ bc,
+                                                             double* __restrict__ wc_zero, PForce pf, Gather G,
+                                                             int ngrid, int q0, int q1) {
+    __shared__ __align__(16) RrSmem S;
+    pdl_enter();
+    fused_launch(pf, G, ngrid,
+                 [&](int blk) { residual_restrict_tile(F, b, w, bc, wc_zero, blk, q0, q1, S); });
+}
+
 // Plain restriction of a vector (ibmg_restrict).
 __global__ void k_restrict(int nf, const double* __restrict__ rf, double* __restrict__ rc) {
     pdl_enter();

@@ -165,6 +165,7 @@ struct ibmg_ctx {
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
     int pp_grid_max = 1;    // co-resident CTAs of the persistent plain phase
     bool tiles_pp = true;   // persistent double-buffered plain phase (IBMG_TILES_PP=0: one CTA per tile)
+    bool rr_tiled = true;   // tiled residual + restriction where the coarse side is >= 32 (IBMG_RR_TILED=0: off)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int grid_limit = 0;     // optional cap on the persistent kernels' grids (concurrent contexts)
     unsigned long long* trace = nullptr;  // debug task timeline of the dataflow sweep
@@ -1040,6 +1041,33 @@ void pressure_mean_zero(ibmg_ctx* c, double* x) {
     LAUNCH(c, k_sub_mean, nblk(nn), 256, 0, x + 2 * nn, nn, nn, c->dh + 2 * (c->prm.restart + 2));
 }
 
+// Coarse b (rows [yc0, yc1) of level l+1) = R (b - A_l w) and, when wcz is
+// given, the coarse zero initial guess: one fused launch (stencil CTAs, point
+// forces, face gather on the coarse face list).  The stencil part is tiled
+// (k_residual_restrict_t) where the coarse side is >= 32.  slab: gather only
+// the faces of the owned coarse rows.
+void residual_restrict(ibmg_ctx* c, int l, const double* b, const double* w, double* wcz, int yc0, int yc1,
+                       bool slab) {
+    LevelBuf& lb = c->lev[l];
+    LevelBuf& nx = c->lev[l + 1];
+    const int nc = nx.L.n;
+    const PForce pf = pforce(c, lb, w, nx.FL.nf > 0);
+    const bool tiled = c->rr_tiled && nc >= kRrTx;
+    const int ng = tiled ? (nc / kRrTx) * ((yc1 - yc0 + kRrTy - 1) / kRrTy) : 3 * int(nblk(size_t(yc1 - yc0) * nc));
+    Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
+    if (slab) {
+        G.lg = nx.L.lg;
+        G.jlo = yc0;
+        G.jhi = yc1;
+    }
+    if (tiled)
+        LAUNCH(c, k_residual_restrict_t, pf.nblk + ng + G.nblk, 256, 0, lb.L, b, w, nx.b, wcz, pf, G, ng, yc0 * nc,
+               yc1 * nc);
+    else
+        LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, b, w, nx.b, wcz, pf, G, ng, yc0 * nc,
+               yc1 * nc);
+}
+
 // z = V(nu1,nu2)(0, b): Algorithm 1 from a zero guess.
 // Level 0 reads b and works in z directly.  project = false inside FGMRES: a
 // constant pressure is in the null space of the periodic operator, so the
@@ -1063,11 +1091,7 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z
             LevelBuf& lb = c->lev[l];
             LevelBuf& nx = c->lev[l + 1];
             for (int s = (l == 0 && first_sweep_done) ? 1 : 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
-            const PForce pf = pforce(c, lb, wl(l), nx.FL.nf > 0);
-            const int ng = 3 * int(nblk(nx.L.nn));
-            const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
-            LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, bl(l), wl(l), nx.b, wl(l + 1), pf, G,
-                   ng, 0, nx.L.nn);
+            residual_restrict(c, l, bl(l), wl(l), wl(l + 1), 0, nx.L.n, false);
         }
         // the coarse kernel also prolongs its correction into level lc-1
         coarse_cycle(c, c->lev[c->lc].b, wl(c->lc), wl(c->lc - 1));
@@ -1289,6 +1313,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     ibmg_ctx* c = new ibmg_ctx;
     c->pdl = std::getenv("IBMG_NO_PDL") == nullptr;
     if (const char* e = std::getenv("IBMG_TILES_PP")) c->tiles_pp = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_RR_TILED")) c->rr_tiled = std::atoi(e) != 0;
     c->prm = *p;
     c->krows = krows;
     try {

@@ -452,15 +452,8 @@ void restrict_group(ibmg_group* g, int l) {
     each(g, [&](int r, ibmg_ctx* c) {
         LevelBuf& lb = c->lev[l];
         LevelBuf& nx = c->lev[l + 1];
-        const int nc = nx.L.n, yc0 = g->plan.y0(r, l) / 2, yc1 = g->plan.y1(r, l) / 2;
-        const PForce pf = pforce(c, lb, lb.w, nx.FL.nf > 0);
-        const int ng = 3 * int(nblk(size_t(yc1 - yc0) * nc));
-        Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
-        G.lg = nx.L.lg;
-        G.jlo = yc0;
-        G.jhi = yc1;
-        LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, (const double*)lb.b,
-               (const double*)lb.w, nx.b, (double*)nullptr, pf, G, ng, yc0 * nc, yc1 * nc);
+        const int yc0 = g->plan.y0(r, l) / 2, yc1 = g->plan.y1(r, l) / 2;
+        residual_restrict(c, l, lb.b, lb.w, nullptr, yc0, yc1, true);
         CK(cudaMemsetAsync(nx.w, 0, sizeof(double) * 3 * size_t(nx.L.nn), c->s));
     });
     if (l + 1 < g->plan.la) exchange(g, l + 1, VB, false);
@@ -492,11 +485,7 @@ void vtail(ibmg_ctx* c, int la) {
         LevelBuf& lb = c->lev[l];
         LevelBuf& nx = c->lev[l + 1];
         for (int s = 0; s < c->prm.nu1; ++s) sweep_level(c, l, lb.b, lb.w);
-        const PForce pf = pforce(c, lb, lb.w, nx.FL.nf > 0);
-        const int ng = 3 * int(nblk(nx.L.nn));
-        const Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
-        LAUNCH(c, k_residual_restrict, pf.nblk + ng + G.nblk, 256, 0, lb.L, (const double*)lb.b,
-               (const double*)lb.w, nx.b, nx.w, pf, G, ng, 0, nx.L.nn);
+        residual_restrict(c, l, lb.b, lb.w, nx.w, 0, nx.L.n, false);
     }
     coarse_cycle(c, c->lev[c->lc].b, c->lev[c->lc].w, c->lev[c->lc - 1].w);
     for (int l = c->lc - 1; l >= la; --l) {
