@@ -92,6 +92,8 @@ struct LevelBuf {
     int poff_cap = 0;
     unsigned epoch = 0;
     unsigned* tflags = nullptr;  // per-tile completion epochs (dataflow sweep)
+    unsigned tepoch = 0;         // tile epoch of the band-major plain phase (n > 512; never reset)
+    int* pdf_seg = nullptr;      // its segment order: (tile row << 2) | tile colour per half row
     int2* rr = nullptr;
     int* bq = nullptr;
     // per-block slabs (inverse + encoded E' rows) and big-tile lists
@@ -167,6 +169,9 @@ struct ibmg_ctx {
     bool tiles_pp = true;   // persistent double-buffered plain phase (IBMG_TILES_PP=0: one CTA per tile)
     bool rr_tiled = true;   // tiled residual + restriction where the coarse side is >= 32 (IBMG_RR_TILED=0: off)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
+    int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
+    bool plain_df = true;   // n > 512: band-major plain dataflow launch (IBMG_PLAIN_DF=0: 4 tile-colour launches)
+    int pdf_skew = 0;       // its band skew in steps (0: from the grid; IBMG_PDF_SKEW)
     int grid_limit = 0;     // optional cap on the persistent kernels' grids (concurrent contexts)
     unsigned long long* trace = nullptr;  // debug task timeline of the dataflow sweep
     // live per-kernel CUDA-event timing (bench roofline); off on the timed path
@@ -281,6 +286,28 @@ void ensure_cub(ibmg_ctx* c, size_t bytes) {
     }
 }
 
+// Segment order of the band-major plain dataflow phase (k_plain_df) on a
+// level with nt x nt tiles: a segment is the half row of tiles of one colour
+// in one tile row.  With A_g, B_g = colours 0, 1 of tile row 2g and C_g, D_g =
+// colours 2, 3 of tile row 2g + 1, step s holds A_s, B_{s-k}, C_{s-2k-1},
+// D_{s-3k-1} (those that exist).  Every dependency (B_g <- A_g; C_g <- A, B
+// of rows 2g and 2g + 2; D_g <- those and C_g) lies >= k steps earlier, so
+// with k steps >= the grid's warps no task waits on one started beside it,
+// while the live rows stay a few MB-scale bands (L2-resident).  k >= the
+// number of row pairs degenerates to the tile-colour-major order.
+std::vector<int> plain_df_order(int nt, int grid, int skew) {
+    const int ng = nt / 2, half = nt / 2;
+    const int k = skew > 0 ? skew : std::max(1, (grid + 4 * half - 1) / (4 * half));
+    std::vector<int> seg;
+    seg.reserve(2 * nt);
+    for (int st = 0; int(seg.size()) < 2 * nt; ++st) {
+        const int g[4] = {st, st - k, st - 2 * k - 1, st - 3 * k - 1};
+        for (int tc = 0; tc < 4; ++tc)
+            if (g[tc] >= 0 && g[tc] < ng) seg.push_back(((2 * g[tc] + (tc >> 1)) << 2) | tc);
+    }
+    return seg;
+}
+
 void alloc_levels(ibmg_ctx* c) {
     const ibmg_params& p = c->prm;
     for (int n = p.N;; n /= 2) {
@@ -296,6 +323,11 @@ void alloc_levels(ibmg_ctx* c) {
             if (n >= 4 * kTile) {
                 lb.tflags = dalloc<unsigned>(size_t(n / kTile) * (n / kTile));
                 CK(cudaMemset(lb.tflags, 0, sizeof(unsigned) * (n / kTile) * (n / kTile)));
+            }
+            if (n > kDataflowMaxN) {
+                const std::vector<int> seg = plain_df_order(n / kTile, c->pdf_grid_max, c->pdf_skew);
+                lb.pdf_seg = dalloc<int>(seg.size());
+                CK(cudaMemcpy(lb.pdf_seg, seg.data(), sizeof(int) * seg.size(), cudaMemcpyHostToDevice));
             }
         }
         c->lev.push_back(lb);
@@ -542,6 +574,10 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
         lb.poff = dalloc<int>(size_t(lb.poff_cap));
         lb.flags = dalloc<unsigned>(size_t(lb.poff_cap));
         CK(cudaMemset(lb.flags, 0, sizeof(unsigned) * lb.poff_cap));
+        // the dataflow sweep's tile flags share this epoch: restart them too
+        // (a stale tile epoch equal to a new sweep's would read as published)
+        if (lb.tflags && lb.L.n <= kDataflowMaxN)
+            CK(cudaMemset(lb.tflags, 0, sizeof(unsigned) * (lb.L.n / kTile) * (lb.L.n / kTile)));
         lb.epoch = 0;
     }
     // the host copies stay alive in the level until the next rebuild (which
@@ -987,7 +1023,16 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
         return;
     }
     const int ntile = n / kTile, per = (ntile / 2) * (ntile / 2);
-    for (int tc = 0; tc < 4; ++tc) plain_pass(c, lb, tc, b, w, 0, per, Mirror{});
+    if (c->plain_df) {
+        const int lim = c->grid_limit > 0 ? std::min(c->grid_limit, c->pdf_grid_max) : c->pdf_grid_max;
+        if (c->prof) prof_begin(c, "k_plain_df");
+        launch_k(c, k_plain_df, dim3(std::min(lim, 4 * per)), dim3(32), kPdfSmem, true, L, b, w,
+                 (const uint8_t*)lb.big, lb.tflags, ++lb.tepoch, (const int*)lb.pdf_seg);
+        if (c->prof) prof_end(c);
+        ++c->launches;
+    } else {
+        for (int tc = 0; tc < 4; ++tc) plain_pass(c, lb, tc, b, w, 0, per, Mirror{});
+    }
     if (lb.nbig == 0) return;
     const int grid = std::min(widest, c->grid_limit > 0 ? std::min(c->grid_limit, c->big_grid_max) : c->big_grid_max);
     BigDeps DP{lb.pred, lb.poff, lb.flags, ++lb.epoch};
@@ -1314,6 +1359,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     c->pdl = std::getenv("IBMG_NO_PDL") == nullptr;
     if (const char* e = std::getenv("IBMG_TILES_PP")) c->tiles_pp = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_RR_TILED")) c->rr_tiled = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
     c->prm = *p;
     c->krows = krows;
     try {
@@ -1332,6 +1379,9 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             CK(cudaFuncSetAttribute(k_sweep_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df, 32 * kDfWarps, kDfSmem));
             c->df_grid_max = std::max(1, per_sm * sms);
+            CK(cudaFuncSetAttribute(k_plain_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPdfSmem)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_df, 32, kPdfSmem));
+            c->pdf_grid_max = std::max(1, per_sm * sms);
         }
         alloc_levels(c);
         CK(cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem(c))));
@@ -1363,6 +1413,7 @@ void ibmg_destroy(ibmg_ctx* c) {
 
         dfree(lb.bq);
         dfree(lb.tflags);
+        dfree(lb.pdf_seg);
     }
     dfree(c->V);
     dfree(c->Z);

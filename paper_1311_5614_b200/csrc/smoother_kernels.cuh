@@ -666,6 +666,119 @@ __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
+// One plain tile task of a dataflow sweep (one warp): stage b and the
+// big-block flags, wait for the adjacent tiles of smaller tile colour, stage
+// the w region (L2 only: neighbours were written by other SMs), run the 8
+// colour passes in shared memory, write back with L2 stores and publish the
+// tile's epoch.  sw / sb: the warp's w region and b region buffers.
+// trace: debug timeline slot of the task (nullptr in production).
+__device__ __forceinline__ void df_plain_tile(const Lev& L, const double* __restrict__ b, double* __restrict__ w,
+                                              const uint8_t* __restrict__ big, unsigned* tflags, unsigned epoch,
+                                              int tx, int ty, int tc, double* sw, double* sb,
+                                              unsigned long long* trace) {
+    const int n = L.n, nn = L.nn, lane = threadIdx.x & 31, nt = n / kTile, nbk = n >> 2;
+    const int x0 = tx * kTile, y0 = ty * kTile;
+    const unsigned long long t_a = trace ? gtimer() : 0;
+    // b and the big-block flags are read-only in the sweep: staged before the
+    // dependency wait (off the critical path of the tile-colour chain)
+    for (int qq = lane; qq < 289; qq += 32) {
+        const int a = qq % 17, bb = qq / 17;
+        const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+        cp_async8(&sb[qq], b + gi);
+        cp_async8(&sb[289 + qq], b + nn + gi);
+        cp_async8(&sb[578 + qq], b + 2 * nn + gi);
+    }
+    cp_async_commit();
+    const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * nbk];
+    if (lane < 8) {  // adjacent tiles of smaller tile colour
+        const int d = lane < 4 ? lane : lane + 1;  // skip the centre of the 3x3
+        const int ax = wr(tx + d % 3 - 1, nt), ay = wr(ty + d / 3 - 1, nt);
+        const int ac = (ax & 1) + 2 * (ay & 1);
+        if (ac < tc)
+            while (ld_acquire(tflags + ax + ay * nt) != epoch) __nanosleep(8);
+    }
+    __syncwarp();
+    const unsigned long long t_b = trace ? gtimer() : 0;
+    if (lane < 30) {  // 16-byte pairs, L2 only: lane -> (pair lane % 10, rows lane / 10 + 3 k)
+        const int a2 = lane % 10, r0 = lane / 10;
+        const int xg = wr(x0 - 2 + 2 * a2, n);
+        for (int row = r0; row < 3 * kReg; row += 3) {  // row = f * kReg + bb
+            const int f = row / kReg, bb = row - f * kReg;
+            const size_t gi = xg + (size_t)wr(y0 - 2 + bb, n) * n;
+            cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], w + (size_t)f * nn + gi);
+        }
+    }
+    cp_async_commit();
+    const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
+    cp_async_wait<0>();
+    __syncwarp();
+    const unsigned long long t_s = trace ? gtimer() : 0;
+    TileW W{sw};
+    TileB B{sb};
+    for (int pc = 0; pc < 8; ++pc) {
+        const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
+        if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
+        __syncwarp();
+    }
+    const unsigned long long t_p = trace ? gtimer() : 0;
+    {  // write set: u faces i in [x0, x0+16], v faces j in [y0, y0+16], p cells.
+       // Half-warps take alternate rows, lane & 15 the column (few index
+       // operations: one warp per scheduler here, every instruction's latency
+       // is on the tile chain); lanes 0..15 then store the u column x0 + 16.
+        const int a = lane & 15, h = lane >> 4;
+        const int xa = wr(x0 + a, n);
+        for (int bb = h; bb < 17; bb += 2) {
+            const size_t gi = xa + (size_t)wr(y0 + bb, n) * n;
+            if (bb < 16) {
+                __stcg(w + gi, W(0, a, bb));
+                __stcg(w + 2 * nn + gi, W(2, a, bb));
+            }
+            __stcg(w + nn + gi, W(1, a, bb));
+        }
+        if (lane < 16) __stcg(w + wr(x0 + 16, n) + (size_t)wr(y0 + lane, n) * n, W(0, 16, lane));
+    }
+    __syncwarp();
+    if (lane == 0) {  // warp-synchronous stores + st.release.gpu (cumulative) publish the tile
+        st_release(tflags + tx + ty * nt, epoch);
+        if (trace) {
+            unsigned long long* r = trace;
+            r[0] = t_a;
+            r[1] = t_b;
+            r[2] = gtimer();
+            r[3] = blockIdx.x;
+            r[4] = t_s;
+            r[5] = t_p;
+        }
+    }
+}
+
+// ---- plain phase of a large level (n > 512) as one band-major dataflow launch
+// The same tile tasks and dependencies as k_sweep_df's plain part (so the
+// result is the oracle's tile-colour-ordered schedule), but the tasks run in
+// skewed tile-row bands (ibmg.cu plain_df_order: seg[] maps each half row of
+// tasks to its tile row and colour) instead of colour by colour.  Every
+// tile's smaller-colour neighbours come earlier in that order, so it is a
+// valid task order for the DAG.  The live rows are a few bands, mostly
+// L2-resident: a tile's halo was written recently by its neighbours, and w
+// and b cross HBM about once per sweep instead of once per tile colour plus
+// halos (4 separate tile-colour launches).  One-warp CTAs, one w and one b
+// region per warp; cooperative launch (all CTAs co-resident) => no deadlock.
+constexpr size_t kPdfSmem = (kDfTileBytes + 15) / 16 * 16;
+__global__ void __launch_bounds__(32) k_plain_df(Lev L, const double* __restrict__ b, double* __restrict__ w,
+                                                  const uint8_t* __restrict__ big, unsigned* tflags, unsigned epoch,
+                                                  const int* __restrict__ seg) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char pdm[];
+    double* sw = reinterpret_cast<double*>(pdm);
+    double* sb = sw + 3 * kRegP;
+    const int nt = L.n / kTile, half = nt >> 1, ntiles = nt * nt;
+    for (int task = blockIdx.x; task < ntiles; task += gridDim.x) {
+        const int s = task / half, i = task - s * half;
+        const int sg = __ldg(seg + s), ty = sg >> 2, tc = sg & 3;
+        df_plain_tile(L, b, w, big, tflags, epoch, 2 * i + (tc & 1), ty, tc, sw, sb, nullptr);
+    }
+}
+
 __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -692,83 +805,11 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
     next_item(-1, 0, c, q);
     if (c < A.BC.ncol) slab_issue(slot[0], A.SL, q, t, 32 * kDfWarps);
     cp_async_commit();
-    // ---- plain tasks: warp per tile
+    // ---- plain tasks: warp per tile, tile-colour-major order
     for (int task = blockIdx.x * kDfWarps + wid; task < ntiles; task += G * kDfWarps) {
         const int tc = task / per, i = task % per;
-        const int tx = 2 * (i % half) + (tc & 1), ty = 2 * (i / half) + (tc >> 1);
-        const int x0 = tx * kTile, y0 = ty * kTile;
-        const unsigned long long t_a = A.trace ? gtimer() : 0;
-        // b and the big-block flags are read-only in the sweep: staged before the
-        // dependency wait (off the critical path of the tile-colour chain)
-        for (int qq = lane; qq < 289; qq += 32) {
-            const int a = qq % 17, bb = qq / 17;
-            const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
-            cp_async8(&sb[qq], A.b + gi);
-            cp_async8(&sb[289 + qq], A.b + nn + gi);
-            cp_async8(&sb[578 + qq], A.b + 2 * nn + gi);
-        }
-        cp_async_commit();
-        const bool isbig = lane < 16 && A.big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * nbk];
-        if (lane < 8) {  // adjacent tiles of smaller tile colour
-            const int d = lane < 4 ? lane : lane + 1;  // skip the centre of the 3x3
-            const int ax = wr(tx + d % 3 - 1, nt), ay = wr(ty + d / 3 - 1, nt);
-            const int ac = (ax & 1) + 2 * (ay & 1);
-            if (ac < tc)
-                while (ld_acquire(A.tflags + ax + ay * nt) != epoch) __nanosleep(8);
-        }
-        __syncwarp();
-        const unsigned long long t_b = A.trace ? gtimer() : 0;
-        if (lane < 30) {  // 16-byte pairs, L2 only: lane -> (pair lane % 10, rows lane / 10 + 3 k)
-            const int a2 = lane % 10, r0 = lane / 10;
-            const int xg = wr(x0 - 2 + 2 * a2, n);
-            for (int row = r0; row < 3 * kReg; row += 3) {  // row = f * kReg + bb
-                const int f = row / kReg, bb = row - f * kReg;
-                const size_t gi = xg + (size_t)wr(y0 - 2 + bb, n) * n;
-                cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], A.w + (size_t)f * nn + gi);
-            }
-        }
-        cp_async_commit();
-        const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
-        cp_async_wait<0>();
-        __syncwarp();
-        const unsigned long long t_s = A.trace ? gtimer() : 0;
-        TileW W{sw};
-        TileB B{sb};
-        for (int pc = 0; pc < 8; ++pc) {
-            const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
-            if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
-            __syncwarp();
-        }
-        const unsigned long long t_p = A.trace ? gtimer() : 0;
-        {  // write set: u faces i in [x0, x0+16], v faces j in [y0, y0+16], p cells.
-           // Half-warps take alternate rows, lane & 15 the column (few index
-           // operations: one warp per scheduler here, every instruction's latency
-           // is on the tile chain); lanes 0..15 then store the u column x0 + 16.
-            const int a = lane & 15, h = lane >> 4;
-            const int xa = wr(x0 + a, n);
-            for (int bb = h; bb < 17; bb += 2) {
-                const size_t gi = xa + (size_t)wr(y0 + bb, n) * n;
-                if (bb < 16) {
-                    __stcg(A.w + gi, W(0, a, bb));
-                    __stcg(A.w + 2 * nn + gi, W(2, a, bb));
-                }
-                __stcg(A.w + nn + gi, W(1, a, bb));
-            }
-            if (lane < 16) __stcg(A.w + wr(x0 + 16, n) + (size_t)wr(y0 + lane, n) * n, W(0, 16, lane));
-        }
-        __syncwarp();
-        if (lane == 0) {  // warp-synchronous stores + st.release.gpu (cumulative) publish the tile
-            st_release(A.tflags + tx + ty * nt, epoch);
-            if (A.trace) {
-                unsigned long long* r = A.trace + 6 * task;
-                r[0] = t_a;
-                r[1] = t_b;
-                r[2] = gtimer();
-                r[3] = blockIdx.x;
-                r[4] = t_s;
-                r[5] = t_p;
-            }
-        }
+        df_plain_tile(L, A.b, A.w, A.big, A.tflags, epoch, 2 * (i % half) + (tc & 1), 2 * (i / half) + (tc >> 1), tc,
+                      sw, sb, A.trace ? A.trace + 6 * task : nullptr);
     }
     __syncthreads();
     // ---- big tasks: CTA per block, colour order
