@@ -174,13 +174,13 @@ def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     sweeps = 2  # V(1,1)
     N = ctxinfo["N"]
     big_bytes = 3136 * 8 + 2000 * 12 + 56 * 24  # inverse + E' slab (~2000 entries x 12 B) + block w/b traffic
-    if name.startswith("k_plain_tiles"):  # levels n > 512: 4 tile-colour launches cover every cell once per sweep
+    if name.startswith("k_plain_tiles") or name == "k_plain_df":  # levels n > 512: every cell once per sweep
         return sum(72 * n * n * sweeps for n, _ in lv if n > 512) * vcycles
     if name == "k_big_phase":
         return sum(big_bytes * nb * sweeps for n, nb in lv if n > 512) * vcycles
     if name == "k_sweep_df":  # levels 64 <= n <= 512: the whole sweep (plain cells + big blocks)
         return sum((72 * n * n + big_bytes * nb) * sweeps for n, nb in lv if 64 <= n <= 512) * vcycles
-    if name == "k_residual_restrict":
+    if name.startswith("k_residual_restrict"):
         return sum(54 * n * n for n, _ in lv) * vcycles
     if name == "k_prolong_add":
         return sum(54 * n * n for n, _ in lv) * vcycles

@@ -226,10 +226,12 @@ __device__ __forceinline__ void rr_cp16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
+// e (optional): E'_l w on the level's velocity faces (dense, zero off the
+// E-active faces; k_residual_restrict_e), added to b in the residual rows.
 __device__ __forceinline__ void residual_restrict_tile(const Lev& F, const double* __restrict__ b,
                                                        const double* __restrict__ w, double* __restrict__ bc,
                                                        double* __restrict__ wc_zero, int blk, int q0, int q1,
-                                                       RrSmem& S) {
+                                                       RrSmem& S, const double* __restrict__ e = nullptr) {
     const int n = F.n, nn = F.nn, nc = n >> 1, nnc = nc * nc;
     const int ntx = nc / kRrTx, Jb = q0 / nc, Je = q1 / nc;
     const int ty = blk / ntx, tx = blk - ty * ntx;
@@ -259,6 +261,25 @@ __device__ __forceinline__ void residual_restrict_tile(const Lev& F, const doubl
 #pragma unroll
         for (int k = 0; k < 3; ++k)
             bv[k] = __ldg(reinterpret_cast<const double2*>(b + nn + (size_t)wr(2 * Jc - 1 + k, n) * n + xc));
+        if (e) {  // b + E'w on the u and v rows (e is written by this launch: L2 loads)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const size_t row = (size_t)(2 * Jc + k) * n;
+                const double2 e0 = __ldcg(reinterpret_cast<const double2*>(e + row + xm));
+                const double2 e1 = __ldcg(reinterpret_cast<const double2*>(e + row + xc));
+                bu[k][0].x += e0.x;
+                bu[k][0].y += e0.y;
+                bu[k][1].x += e1.x;
+                bu[k][1].y += e1.y;
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double2 ev =
+                    __ldcg(reinterpret_cast<const double2*>(e + nn + (size_t)wr(2 * Jc - 1 + k, n) * n + xc));
+                bv[k].x += ev.x;
+                bv[k].y += ev.y;
+            }
+        }
         if (wc_zero) {
             wc_zero[q] = 0.0;
             wc_zero[nnc + q] = 0.0;
@@ -339,6 +360,54 @@ __global__ void __launch_bounds__(256) k_residual_restrict_t(Lev F, const double
     pdl_enter();
     fused_launch(pf, G, ngrid,
                  [&](int blk) { residual_restrict_tile(F, b, w, bc, wc_zero, blk, q0, q1, S); });
+}
+
+// Variant for levels where the Lagrangian points far outnumber the E-active
+// faces (coarse levels of many-structure grids): the E' part of the residual
+// comes from the level's assembled rows (E'_l w, CSR, elasticity.cpp:88-107
+// restated per level) instead of the factored point forces + coarse face
+// gather, whose cost scales with the points.  Launch = [R.nblk row CTAs: a
+// warp per E' row (lane-strided sum + fixed xor tree: deterministic) writing
+// e[face] | tile CTAs: wait until every row CTA has signalled, then the tiled
+// residual + restriction with b + e].  Row CTAs come first in dispatch order,
+// so the waiting tiles never block them.
+__device__ __forceinline__ double warp_sum_xor(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+struct ERes {
+    FaceList FL;
+    EMat E;
+    double* e;                  // dense level vector (velocity part), zero off the face list
+    int nblk;                   // row CTAs (8 rows each)
+    unsigned long long* cnt;    // monotone per-context counter
+    unsigned long long target;  // its value once this launch's row CTAs are done
+};
+__global__ void __launch_bounds__(256) k_residual_restrict_e(Lev F, const double* __restrict__ b,
+                                                             const double* __restrict__ w, double* __restrict__ bc,
+                                                             double* __restrict__ wc_zero, ERes R, int q0, int q1) {
+    __shared__ __align__(16) RrSmem S;
+    pdl_enter();
+    if ((int)blockIdx.x < R.nblk) {
+        const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+        if (row < R.FL.nf) {
+            double s = 0.0;
+            for (int k = R.E.rp[row] + lane; k < R.E.rp[row + 1]; k += 32) s += R.E.val[k] * w[R.E.col[k]];
+            s = warp_sum_xor(s);
+            if (lane == 0) __stcg(R.e + R.FL.face[row], s);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(R.cnt, 1ull);
+        }
+        return;
+    }
+    if (threadIdx.x == 0)
+        while (ld_acquire_u64(R.cnt) < R.target) __nanosleep(32);
+    __syncthreads();
+    residual_restrict_tile(F, b, w, bc, wc_zero, blockIdx.x - R.nblk, q0, q1, S, R.e);
 }
 
 // Plain restriction of a vector (ibmg_restrict).

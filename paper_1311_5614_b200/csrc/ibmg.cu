@@ -94,6 +94,8 @@ struct LevelBuf {
     unsigned* tflags = nullptr;  // per-tile completion epochs (dataflow sweep)
     unsigned tepoch = 0;         // tile epoch of the band-major plain phase (n > 512; never reset)
     int* pdf_seg = nullptr;      // its segment order: (tile row << 2) | tile colour per half row
+    bool rr_csr = false;         // restriction from this level takes E' w from the assembled rows
+    double* escr = nullptr;      // its E'w scratch (2 nn, zero off the face list)
     int2* rr = nullptr;
     int* bq = nullptr;
     // per-block slabs (inverse + encoded E' rows) and big-tile lists
@@ -168,6 +170,8 @@ struct ibmg_ctx {
     int pp_grid_max = 1;    // co-resident CTAs of the persistent plain phase
     bool tiles_pp = true;   // persistent double-buffered plain phase (IBMG_TILES_PP=0: one CTA per tile)
     bool rr_tiled = true;   // tiled residual + restriction where the coarse side is >= 32 (IBMG_RR_TILED=0: off)
+    bool rr_csr = true;     // ... with E' from the assembled rows on point-dense levels (IBMG_RR_CSR=0: off)
+    double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
     bool plain_df = true;   // n > 512: band-major plain dataflow launch (IBMG_PLAIN_DF=0: 4 tile-colour launches)
@@ -205,12 +209,25 @@ void prof_begin(ibmg_ctx* c, const char* name) {
 void prof_end(ibmg_ctx* c) { CK(cudaEventRecord(c->prof_pending.back().b, c->s)); }
 void prof_collect(ibmg_ctx* c) {
     CK(cudaStreamSynchronize(c->s));
+    // "(idle)": device time between consecutive profiled kernels (launch gaps
+    // and host round trips; event-record overhead included)
+    const ibmg_ctx::ProfRec* prev = nullptr;
     for (auto& r : c->prof_pending) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, r.a, r.b));
         auto& acc = c->prof_acc[r.name];
         acc.first += ms;
         acc.second += 1;
+        if (prev) {
+            float gap = 0.f;
+            CK(cudaEventElapsedTime(&gap, prev->b, r.a));
+            auto& g = c->prof_acc["(idle)"];
+            g.first += gap;
+            g.second += 1;
+        }
+        prev = &r;
+    }
+    for (auto& r : c->prof_pending) {
         c->ev_pool.push_back(r.a);
         c->ev_pool.push_back(r.b);
     }
@@ -855,6 +872,17 @@ void rebuild(ibmg_ctx* c) {
         LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
                c->err_flag);
     }
+    // levels whose restriction takes E' from the assembled rows (points far
+    // outnumber the level's E-active faces): zero their E'w scratch (the face
+    // set changed; only active faces are written afterwards)
+    for (int l = 0; l + 1 < c->nlev; ++l) {
+        LevelBuf& lb = c->lev[l];
+        lb.rr_csr = c->rr_tiled && c->rr_csr && npts > 0 && lb.FL.nf > 0 && lb.L.n >= 2 * kRrTx &&
+                    c->rr_csr_ratio * lb.FL.nf < double(npts);
+        if (!lb.rr_csr) continue;
+        if (!lb.escr) lb.escr = dalloc<double>(2 * size_t(lb.L.nn));
+        CK(cudaMemsetAsync(lb.escr, 0, sizeof(double) * 2 * size_t(lb.L.nn), c->s));
+    }
     tr.mark("launched slabs");
     check_err_flag(c, "rebuild");
     tr.mark("done");
@@ -1096,6 +1124,14 @@ void residual_restrict(ibmg_ctx* c, int l, const double* b, const double* w, dou
     LevelBuf& lb = c->lev[l];
     LevelBuf& nx = c->lev[l + 1];
     const int nc = nx.L.n;
+    if (lb.rr_csr && !slab) {
+        const int ng = (nc / kRrTx) * ((yc1 - yc0 + kRrTy - 1) / kRrTy);
+        ERes R{lb.FL, lb.E, lb.escr, int(nblk(lb.FL.nf, 8)), c->tail_cnt, 0ull};
+        c->tail_base += (unsigned long long)R.nblk;
+        R.target = c->tail_base;
+        LAUNCH(c, k_residual_restrict_e, R.nblk + ng, 256, 0, lb.L, b, w, nx.b, wcz, R, yc0 * nc, yc1 * nc);
+        return;
+    }
     const PForce pf = pforce(c, lb, w, nx.FL.nf > 0);
     const bool tiled = c->rr_tiled && nc >= kRrTx;
     const int ng = tiled ? (nc / kRrTx) * ((yc1 - yc0 + kRrTy - 1) / kRrTy) : 3 * int(nblk(size_t(yc1 - yc0) * nc));
@@ -1359,6 +1395,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     c->pdl = std::getenv("IBMG_NO_PDL") == nullptr;
     if (const char* e = std::getenv("IBMG_TILES_PP")) c->tiles_pp = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_RR_TILED")) c->rr_tiled = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_RR_CSR")) c->rr_csr = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_RR_CSR_RATIO")) c->rr_csr_ratio = std::atof(e);
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
     c->prm = *p;
@@ -1414,6 +1452,7 @@ void ibmg_destroy(ibmg_ctx* c) {
         dfree(lb.bq);
         dfree(lb.tflags);
         dfree(lb.pdf_seg);
+        dfree(lb.escr);
     }
     dfree(c->V);
     dfree(c->Z);

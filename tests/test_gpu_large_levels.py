@@ -56,3 +56,21 @@ def test_tiled_restriction_matches(c3, monkeypatch):
     assert rel(z_t, z_u) < 1e-13
     o = O.Oracle(c3, threads=16)
     assert rel(z_t, o.vcycle(b)) < 1e-10
+
+
+@pytest.mark.parametrize("which", ["c3", "dense"])
+def test_restriction_from_assembled_rows(c3, which, monkeypatch):
+    """Point-dense levels take E' w from the assembled rows (IBMG_RR_CSR):
+    same V-cycle as the factored point-force path to round-off, and the
+    oracle's.  'dense': 4096 points on one ellipse at N = 128, so even the
+    fine level's restriction uses the rows."""
+    prob = c3 if which == "c3" else configs.small_problem(N=128, nb=4096, kappa=1e4)
+    n = prob.N
+    b = rand(3 * n * n, 34)
+    b[2 * n * n:] -= b[2 * n * n:].mean()
+    g_r = system(prob, monkeypatch, IBMG_RR_CSR="1")
+    g_p = system(prob, monkeypatch, IBMG_RR_CSR="0")
+    z_r, z_p = g_r.v_cycle(b), g_p.v_cycle(b)
+    assert rel(z_r, z_p) < 1e-12
+    o = O.Oracle(prob, threads=16)
+    assert rel(z_r, o.vcycle(b)) < 1e-10
