@@ -147,6 +147,104 @@ __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __re
     });
 }
 
+__device__ __forceinline__ void rr_cp16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// Tiled operator apply for levels with n >= 64 (bandwidth regime; the same
+// expressions and term order as stokes_rows).  A grid CTA owns 64 x 16 cells:
+// the w region [x0-2, x0+66) x [y0-1, y0+17) of all three fields is staged in
+// shared memory with 16-byte cp.async, and each thread forms the 2 x 2 cells
+// (x0+2I.., y0+2J..) from double2 shared loads and writes them as double2
+// rows (coalesced).  Rows past q1 (slab ends) are skipped.
+constexpr int kApTx = 64, kApTy = 16;
+constexpr int kApW = kApTx + 4, kApH = kApTy + 2;
+struct ApSmem {
+    double s[3][kApH][kApW];
+};
+__device__ __forceinline__ void apply_tile(const Lev& L, const double* __restrict__ w, double* __restrict__ out,
+                                           int blk, int q0, int q1, ApSmem& S) {
+    const int n = L.n, nn = L.nn;
+    const int ntx = n / kApTx, jb = q0 / n, je = q1 / n;
+    const int ty = blk / ntx, tx = blk - ty * ntx;
+    const int x0 = tx * kApTx, y0 = jb + ty * kApTy;
+    constexpr int kPairs = kApW / 2;
+    for (int e = threadIdx.x; e < 3 * kApH * kPairs; e += blockDim.x) {
+        const int f = e / (kApH * kPairs), rem = e - f * (kApH * kPairs);
+        const int r = rem / kPairs, pc = rem - r * kPairs;
+        rr_cp16(&S.s[f][r][2 * pc], w + (size_t)f * nn + wr(x0 - 2 + 2 * pc, n) + (size_t)wr(y0 - 1 + r, n) * n);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    const int I = threadIdx.x & 31, J = threadIdx.x >> 5;
+    const int x = x0 + 2 * I, y = y0 + 2 * J;
+    if (y >= je) return;
+    const double d = L.d, cc = L.c, g = L.g;
+    auto ld2 = [&](int f, int r, int c) { return *reinterpret_cast<const double2*>(&S.s[f][r][c]); };
+    const int c0 = 2 * I;  // smem column of x - 2; smem row 2J of y - 1
+    double u[4][6], p[3][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+            const double2 t = ld2(0, 2 * J + k, c0 + 2 * h);
+            u[k][2 * h] = t.x;
+            u[k][2 * h + 1] = t.y;
+        }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double2 t = ld2(2, 2 * J + k, c0 + 2 * h);
+            p[k][2 * h] = t.x;
+            p[k][2 * h + 1] = t.y;
+        }
+    // cells (ci, k) = (x - 2 + ci, y - 1 + k), ci in 2..3, k in 1..2
+    double ru[2][2], rpu[2][2];
+#pragma unroll
+    for (int k = 1; k <= 2; ++k)
+#pragma unroll
+        for (int ci = 2; ci <= 3; ++ci) {
+            ru[k - 1][ci - 2] = d * u[k][ci] - cc * (u[k][ci - 1] + u[k][ci + 1] + u[k - 1][ci] + u[k + 1][ci]) +
+                                g * (p[k][ci] - p[k][ci - 1]);
+            rpu[k - 1][ci - 2] = -g * (u[k][ci + 1] - u[k][ci]);
+        }
+    double v[4][6];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+            const double2 t = ld2(1, 2 * J + k, c0 + 2 * h);
+            v[k][2 * h] = t.x;
+            v[k][2 * h + 1] = t.y;
+        }
+#pragma unroll
+    for (int k = 1; k <= 2; ++k) {
+        const int yy = y + k - 1;
+        if (yy >= je) break;
+        double rv[2], rp[2];
+#pragma unroll
+        for (int ci = 2; ci <= 3; ++ci) {
+            rv[ci - 2] = d * v[k][ci] - cc * (v[k - 1][ci] + v[k + 1][ci] + v[k][ci - 1] + v[k][ci + 1]) +
+                         g * (p[k][ci] - p[k - 1][ci]);
+            rp[ci - 2] = rpu[k - 1][ci - 2] - g * (v[k + 1][ci] - v[k][ci]);
+        }
+        const size_t o = x + (size_t)yy * n;
+        *reinterpret_cast<double2*>(out + o) = make_double2(ru[k - 1][0], ru[k - 1][1]);
+        *reinterpret_cast<double2*>(out + nn + o) = make_double2(rv[0], rv[1]);
+        *reinterpret_cast<double2*>(out + 2 * (size_t)nn + o) = make_double2(rp[0], rp[1]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_stokes_apply_t(Lev L, const double* __restrict__ w, double* __restrict__ out,
+                                                        PForce pf, Gather G, int ngrid, int q0, int q1) {
+    __shared__ __align__(16) ApSmem S;
+    pdl_enter();
+    fused_launch(pf, G, ngrid, [&](int blk) { apply_tile(L, w, out, blk, q0, q1, S); });
+}
+
 // r = b - S w (E' part added by k_face_gather with sign +1).
 __global__ void k_stokes_residual(Lev L, const double* __restrict__ b, const double* __restrict__ w,
                                   double* __restrict__ r, PForce pf, Gather G, int ngrid, int q0, int q1) {
@@ -221,10 +319,6 @@ struct RrSmem {
     double s[3][kRrH][kRrW];
 };
 
-__device__ __forceinline__ void rr_cp16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
 
 // e (optional): E'_l w on the level's velocity faces (dense, zero off the
 // E-active faces; k_residual_restrict_e), added to b in the residual rows.

@@ -171,6 +171,7 @@ struct ibmg_ctx {
     bool tiles_pp = true;   // persistent double-buffered plain phase (IBMG_TILES_PP=0: one CTA per tile)
     bool rr_tiled = true;   // tiled residual + restriction where the coarse side is >= 32 (IBMG_RR_TILED=0: off)
     bool rr_csr = true;     // ... with E' from the assembled rows on point-dense levels (IBMG_RR_CSR=0: off)
+    bool ap_tiled = true;   // tiled operator apply where n >= 64 (IBMG_AP_TILED=0: off)
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
@@ -995,13 +996,29 @@ Gather gather(ibmg_ctx* c, const LevelBuf& to, double* out, double sign, const P
     return G;
 }
 
-// out = A_l w on level l: stencil, point forces and the face gather in one launch.
-void apply_level(ibmg_ctx* c, int l, const double* w, double* out) {
+// out (rows [y0, y1) of level l) = A_l w: stencil, point forces and the face
+// gather in one launch; the stencil part tiled (k_stokes_apply_t) where
+// n >= 64.  slab: gather only the faces of the owned rows.
+void apply_rows(ibmg_ctx* c, int l, const double* w, double* out, int y0, int y1, bool slab) {
     LevelBuf& lb = c->lev[l];
+    const int n = lb.L.n;
     const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
-    const int ng = int(nblk(lb.L.nn));
-    const Gather G = gather(c, lb, out, -1.0, pf, ng);
-    LAUNCH(c, k_stokes_apply, pf.nblk + ng + G.nblk, 256, 0, lb.L, w, out, pf, G, ng, 0, lb.L.nn);
+    const bool tiled = c->ap_tiled && n >= kApTx;
+    const int ng = tiled ? (n / kApTx) * ((y1 - y0 + kApTy - 1) / kApTy) : int(nblk(size_t(y1 - y0) * n));
+    Gather G = gather(c, lb, out, -1.0, pf, ng);
+    if (slab) {
+        G.lg = lb.L.lg;
+        G.jlo = y0;
+        G.jhi = y1;
+    }
+    if (tiled)
+        LAUNCH(c, k_stokes_apply_t, pf.nblk + ng + G.nblk, 256, 0, lb.L, w, out, pf, G, ng, y0 * n, y1 * n);
+    else
+        LAUNCH(c, k_stokes_apply, pf.nblk + ng + G.nblk, 256, 0, lb.L, w, out, pf, G, ng, y0 * n, y1 * n);
+}
+
+void apply_level(ibmg_ctx* c, int l, const double* w, double* out) {
+    apply_rows(c, l, w, out, 0, c->lev[l].L.n, false);
 }
 
 void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double* r) {
@@ -1397,6 +1414,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_RR_TILED")) c->rr_tiled = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_RR_CSR")) c->rr_csr = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_RR_CSR_RATIO")) c->rr_csr_ratio = std::atof(e);
+    if (const char* e = std::getenv("IBMG_AP_TILED")) c->ap_tiled = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
     c->prm = *p;

@@ -462,16 +462,7 @@ void restrict_group(ibmg_group* g, int l) {
 
 // out (owned rows of level 0) = A w, w valid on the owned rows + halo
 void apply_owned(ibmg_group* g, int r, const double* w, double* out) {
-    ibmg_ctx* c = cx(g, r);
-    LevelBuf& lb = c->lev[0];
-    const int n = lb.L.n, y0 = g->plan.y0(r, 0), y1 = g->plan.y1(r, 0);
-    const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
-    const int ng = int(nblk(size_t(y1 - y0) * n));
-    Gather G = gather(c, lb, out, -1.0, pf, ng);
-    G.lg = lb.L.lg;
-    G.jlo = y0;
-    G.jhi = y1;
-    LAUNCH(c, k_stokes_apply, pf.nblk + ng + G.nblk, 256, 0, lb.L, w, out, pf, G, ng, y0 * n, y1 * n);
+    apply_rows(cx(g, r), 0, w, out, g->plan.y0(r, 0), g->plan.y1(r, 0), true);
 }
 
 // The V-cycle below the distributed levels on one slab: levels la..nlev-1

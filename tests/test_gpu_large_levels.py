@@ -74,3 +74,16 @@ def test_restriction_from_assembled_rows(c3, which, monkeypatch):
     assert rel(z_r, z_p) < 1e-12
     o = O.Oracle(prob, threads=16)
     assert rel(z_r, o.vcycle(b)) < 1e-10
+
+
+def test_tiled_apply_matches(c3, monkeypatch):
+    """k_stokes_apply_t (64 x 16 cell tiles) = the cell-per-thread apply
+    (IBMG_AP_TILED=0) = the oracle's operator, on the C3 fine level."""
+    n = c3.N
+    w = rand(3 * n * n, 35)
+    g_t = system(c3, monkeypatch, IBMG_AP_TILED="1")
+    g_u = system(c3, monkeypatch, IBMG_AP_TILED="0")
+    a_t, a_u = g_t.apply(w), g_u.apply(w)
+    assert rel(a_t, a_u) < 1e-14
+    o = O.Oracle(c3, threads=16)
+    assert rel(a_t, o.apply(w)) < 1e-12
