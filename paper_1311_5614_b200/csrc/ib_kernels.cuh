@@ -57,6 +57,20 @@ __device__ __forceinline__ int cell_prolong(int c, int* J, double* w) {
     J[0] = c >> 1; w[0] = 0.75; J[1] = (c & 1) ? (c >> 1) + 1 : (c >> 1) - 1; w[1] = 0.25; return 2;
 }
 
+// Weight of fine index fi in coarse index ci for a 1-D transfer kind:
+// 0 face-restrict {1/8, 1/4, 1/8}, 1 cell-restrict (1), 2 face-prolong
+// (1 or 1/2, 1/2), 3 cell-prolong (3/4, 1/4); see face_restrict etc. above.
+__device__ __forceinline__ double transfer_weight(int kind, int fi, int ci) {
+    const int h = fi >> 1;
+    const bool odd = fi & 1;
+    if (kind == 1) return ci == h ? 1.0 : 0.0;
+    if (kind == 3) return ci == h ? 0.75 : (ci == (odd ? h + 1 : h - 1) ? 0.25 : 0.0);
+    const double w_even = kind == 0 ? 0.25 : 1.0, w_odd = kind == 0 ? 0.125 : 0.5;
+    if (!odd) return ci == h ? w_even : 0.0;
+    return (ci == h || ci == h + 1) ? w_odd : 0.0;  // (fi - 1) / 2 = h, (fi + 1) / 2 = h + 1
+}
+__device__ __forceinline__ double transfer_total(int kind) { return kind == 0 ? 0.25 : 1.0; }
+
 // Windows of every point on every level, one thread per point.  Level l+1's
 // left window is R applied to level l's (R*...*R*W^T), the right window is
 // level l's times P (W*P*...*P) — the factored form of the reference's
@@ -91,39 +105,49 @@ __global__ void k_windows(int npts, const double* __restrict__ X, WinLevels WL, 
         org[0] = ox;
         org[1] = oy;
         if (l + 1 >= WL.nlev) break;
-        double nxt[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) nxt[e] = 0.0;
+        // next patch = Wx^T cur Wy with the separable 1-D transfer weights
+        // (gather form: static register indexing, no scatter into a local
+        // array).  kind: 0 face-restrict, 1 cell-restrict, 2 face-prolong,
+        // 3 cell-prolong; x and y kinds per patch type as in the reference's
+        // R (transfers.cpp:117-127) and P (transfers.cpp:141-205).
+        const int kx = s == 0 ? 0 : s == 1 ? 1 : s == 2 ? 2 : 3;
+        const int ky = s == 0 ? 1 : s == 1 ? 0 : s == 2 ? 3 : 2;
         int nx, ny;
         if (s == 0) { nx = ox >> 1; ny = oy >> 1; }             // left u: face-restrict x, cell-restrict y
         else if (s == 1) { nx = ox >> 1; ny = oy >> 1; }        // left v: cell-restrict x, face-restrict y
         else if (s == 2) { nx = ox >> 1; ny = (oy - 1) >> 1; }  // right u: face-prolong x, cell-prolong y
         else { nx = (ox - 1) >> 1; ny = oy >> 1; }              // right v: cell-prolong x, face-prolong y
-        int I[2], J[2];
-        double wi[2], wj[2];
-        for (int b = 0; b < 4; ++b)
-            for (int a = 0; a < 4; ++a) {
-                const double v = cur[b * 4 + a];
-                if (v == 0.0) continue;
-                if (s == 0) {
-                    const int ni = face_restrict(ox + a, I, wi);
-                    const int J0 = (oy + b) >> 1;
-                    for (int p2 = 0; p2 < ni; ++p2) patch_add(nxt, I[p2] - nx, J0 - ny, v * wi[p2], err);
-                } else if (s == 1) {
-                    const int nj = face_restrict(oy + b, J, wj);
-                    const int I0 = (ox + a) >> 1;
-                    for (int q2 = 0; q2 < nj; ++q2) patch_add(nxt, I0 - nx, J[q2] - ny, v * wj[q2], err);
-                } else if (s == 2) {
-                    const int ni = face_prolong(ox + a, I, wi);
-                    const int nj = cell_prolong(oy + b, J, wj);
-                    for (int p2 = 0; p2 < ni; ++p2)
-                        for (int q2 = 0; q2 < nj; ++q2) patch_add(nxt, I[p2] - nx, J[q2] - ny, v * (wi[p2] * wj[q2]), err);
-                } else {
-                    const int nj = face_prolong(oy + b, J, wj);
-                    const int ni = cell_prolong(ox + a, I, wi);
-                    for (int q2 = 0; q2 < nj; ++q2)
-                        for (int p2 = 0; p2 < ni; ++p2) patch_add(nxt, I[p2] - nx, J[q2] - ny, v * (wj[q2] * wi[p2]), err);
+        double tx[4][4], ty[4][4];
+        bool bad = false;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double cs = 0.0, rs = 0.0, sx = 0.0, sy = 0.0;
+#pragma unroll
+            for (int A = 0; A < 4; ++A) {
+                tx[a][A] = transfer_weight(kx, ox + a, nx + A);
+                ty[a][A] = transfer_weight(ky, oy + a, ny + A);
+                sx += tx[a][A];
+                sy += ty[a][A];
+                cs += fabs(cur[A * 4 + a]);  // column a
+                rs += fabs(cur[a * 4 + A]);  // row a
+            }
+            bad |= (cs != 0.0 && sx != transfer_total(kx)) || (rs != 0.0 && sy != transfer_total(ky));
+        }
+        if (bad) atomicOr(err, 1);  // a weight falls outside the 4x4 patch
+        double nxt[16];
+#pragma unroll
+        for (int B = 0; B < 4; ++B)
+#pragma unroll
+            for (int A = 0; A < 4; ++A) {
+                double acc = 0.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) t += tx[a][A] * cur[b * 4 + a];
+                    acc += ty[b][B] * t;
                 }
+                nxt[B * 4 + A] = acc;
             }
 #pragma unroll
         for (int e = 0; e < 16; ++e) cur[e] = nxt[e];

@@ -1891,12 +1891,12 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
         if (c->npts)
             CK(cudaMemcpyAsync(c->X, X, sizeof(double) * 2 * c->npts,
                                ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
-        rebuild(c);
         const double* du = u;
-        if (ptr_kind != IBMG_PTR_DEVICE) {
+        if (ptr_kind != IBMG_PTR_DEVICE) {  // u^n upload first: the rebuild does not touch stage_a
             CK(cudaMemcpyAsync(c->stage_a, u, sizeof(double) * 2 * nn, cudaMemcpyHostToDevice, c->s));
             du = c->stage_a;
         }
+        rebuild(c);
         build_rhs(c, du, c->bv);
         CK(cudaStreamSynchronize(c->s));
         const double t1 = now_ms();
