@@ -117,6 +117,8 @@ struct ibmg_ctx {
     ibmg_params prm{};
     std::string err;
     cudaStream_t s = nullptr;
+    cudaStream_t s2 = nullptr;                       // setup side stream (coarsest inverse)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sizes = nullptr;
     int nlev = 0, lc = 0;  // levels [lc, nlev) run in the single-CTA coarse kernel
     std::vector<LevelBuf> lev;
     long long launches = 0;
@@ -144,6 +146,8 @@ struct ibmg_ctx {
     int slo_cap = 0;
     long sl_cap = 0;
     int* hpin_i = nullptr;  // pinned int scratch (row counts)
+    bool err_pending = false;  // hpin_i[4] holds a rebuild's error flags, not yet checked
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // setup timing of ibmg_step
     size_t sort_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -396,7 +400,7 @@ void alloc_levels(ibmg_ctx* c) {
     CK(cudaMemset(c->tail_cnt, 0, sizeof(unsigned long long)));
     c->dh = dalloc<double>(2 * (m + 2) + 8);
     CK(cudaMallocHost(&c->hpin, sizeof(double) * (2 * (m + 2) + 8)));
-    CK(cudaMallocHost(&c->hpin_i, sizeof(int) * 16));
+    CK(cudaMallocHost(&c->hpin_i, sizeof(int) * (16 + 20 * kCtr)));
     c->ones = dalloc<double>(size_t(p.N) * p.N);
     {
         std::vector<double> one(size_t(p.N) * p.N, 1.0);
@@ -630,9 +634,34 @@ struct SetupTrace {
     }
 };
 
-void rebuild(ibmg_ctx* c) {
+// k_coarse_inverse on the setup side stream, forked from and joined back into
+// the solver stream by events (the join is in rebuild()).
+void coarse_inverse_forked(ibmg_ctx* c) {
+    LevelBuf& lb = c->lev.back();
+    const int m = 3 * lb.L.nn + 1;
+    CK(cudaEventRecord(c->ev_fork, c->s));
+    CK(cudaStreamWaitEvent(c->s2, c->ev_fork, 0));
+    std::swap(c->s, c->s2);
+    LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
+           c->err_flag);
+    std::swap(c->s, c->s2);
+    CK(cudaEventRecord(c->ev_join, c->s2));
+}
+
+// Error flags of a rebuild whose check was deferred (ibmg_step): read with the
+// solve's first host round trip instead of a dedicated one.
+void check_deferred_err(ibmg_ctx* c) {
+    if (!c->err_pending) return;
+    c->err_pending = false;
+    const int h = c->hpin_i[4];
+    if (h & 1) throw InvalidArg("rebuild: window patch overflow (structure too coarse for 4x4 windows)");
+    if (h & 2) throw CudaError("rebuild: singular local box matrix");
+}
+
+void rebuild(ibmg_ctx* c, bool defer_check = false) {
     const int npts = c->npts;
     const SetupTrace tr;
+    bool coarse_forked = false, side_used = false;
     CK(cudaMemsetAsync(c->err_flag, 0, sizeof(int), c->s));
     CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * kCtr, c->s));
     if (npts == 0) {
@@ -751,11 +780,16 @@ void rebuild(ibmg_ctx* c) {
             cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->e_cnt, c->e_rp, total + 1, c->s);
             ensure_cub(c, bytes);
             CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->e_cnt, c->e_rp, total + 1, c->s));
-            CK(cudaMemcpyAsync(c->hpin_i, c->e_rp + total, sizeof(int), cudaMemcpyDeviceToHost, c->s));
-            tr.mark("launched erows count");
-            CK(cudaStreamSynchronize(c->s));
-            tr.mark("synced nnz");
-            const long nnz = c->hpin_i[0];
+            // a row holds at most 256 entries (16 x 16 patch): when that bound is
+            // small, size the arrays by it and skip the host round trip for nnz
+            long nnz = 256L * total;
+            if (nnz * 12 > (256L << 20)) {
+                CK(cudaMemcpyAsync(c->hpin_i, c->e_rp + total, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+                tr.mark("launched erows count");
+                CK(cudaStreamSynchronize(c->s));
+                tr.mark("synced nnz");
+                nnz = c->hpin_i[0];
+            }
             if (nnz > c->e_cap) {
                 dfree(c->e_col);
                 dfree(c->e_val);
@@ -772,6 +806,10 @@ void rebuild(ibmg_ctx* c) {
                 lb.E.col = c->e_col;
                 lb.E.val = c->e_val;
             }
+            // the bordered coarsest inverse needs only the coarsest E' rows: it
+            // runs on the side stream, beside the big-block setup below
+            coarse_inverse_forked(c);
+            coarse_forked = true;
         }
         // big-block E' row ranges, slabs and inverses of every level: one
         // launch each over the level-major block numbering
@@ -837,11 +875,14 @@ void rebuild(ibmg_ctx* c) {
             }
             BL.nlev = S.nlev;
             BL.start[S.nlev] = nball;
+            // slab sizes to the host, then the inverses: the host waits for the
+            // copy only, while the inverses run
+            int* hc2 = c->hpin_i + 8;
+            CK(cudaMemcpyAsync(hc2, c->counters, sizeof(int) * size_t(c->nlev) * kCtr, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaEventRecord(c->ev_sizes, c->s));
             LAUNCH(c, k_block_inverse, nball, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
-            std::vector<int> hc2(size_t(c->nlev) * kCtr);
-            CK(cudaMemcpyAsync(hc2.data(), c->counters, sizeof(int) * hc2.size(), cudaMemcpyDeviceToHost, c->s));
             tr.mark("launched inverses");
-            CK(cudaStreamSynchronize(c->s));
+            CK(cudaEventSynchronize(c->ev_sizes));
             tr.mark("synced slab sizes");
             for (int k = 0; k < S.nlev; ++k) {
                 const int mx = hc2[size_t(S.lev[k]) * kCtr + 19];
@@ -858,7 +899,14 @@ void rebuild(ibmg_ctx* c) {
                 c->sl_col = dalloc<int>(size_t(c->sl_cap));
                 c->sl_val = dalloc<double>(size_t(c->sl_cap));
             }
+            // the slab fill does not depend on the inverses: side stream (joined
+            // at the end of rebuild)
+            CK(cudaStreamWaitEvent(c->s2, c->ev_sizes, 0));
+            std::swap(c->s, c->s2);
             LAUNCH(c, k_slab_fill, nblk(size_t(nball) * 40), 256, 0, S, c->sl_off, c->sl_col, c->sl_val);
+            std::swap(c->s, c->s2);
+            CK(cudaEventRecord(c->ev_join, c->s2));
+            side_used = true;
             for (int k = 0; k < S.nlev; ++k) {
                 LevelBuf& lb = c->lev[S.lev[k]];
                 lb.sl_off = c->sl_off + S.start[k];
@@ -867,7 +915,8 @@ void rebuild(ibmg_ctx* c) {
             }
         }
     }
-    {
+    if (coarse_forked || side_used) CK(cudaStreamWaitEvent(c->s, c->ev_join, 0));
+    if (!coarse_forked) {
         LevelBuf& lb = c->lev.back();
         const int m = 3 * lb.L.nn + 1;
         LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
@@ -885,7 +934,12 @@ void rebuild(ibmg_ctx* c) {
         CK(cudaMemsetAsync(lb.escr, 0, sizeof(double) * 2 * size_t(lb.L.nn), c->s));
     }
     tr.mark("launched slabs");
-    check_err_flag(c, "rebuild");
+    if (defer_check) {
+        CK(cudaMemcpyAsync(c->hpin_i + 4, c->err_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+        c->err_pending = true;
+    } else {
+        check_err_flag(c, "rebuild");
+    }
     tr.mark("done");
 }
 
@@ -1252,21 +1306,17 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
     st->iters = st->restarts = st->converged = 0;
     st->relres = 0.0;
     CK(cudaMemsetAsync(x, 0, sizeof(double) * M, c->s));
-    // ||b||
-    multidot(c, b, 1, b, hoff, 0);
-    CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double), cudaMemcpyDeviceToHost, c->s));
-    CK(cudaStreamSynchronize(c->s));
-    const double bnorm = std::sqrt(c->hpin[0]);
-    if (bnorm == 0.0) {
-        st->converged = 1;
-        return IBMG_OK;
-    }
-    const double tol = c->prm.rtol * bnorm;
-    double beta = bnorm;
+    // ||b||^2 into its own slot; V_0 = b / ||b|| with the norm on the device.
+    // The host reads ||b|| with the first Arnoldi step's dots (no round trip
+    // of its own); bnorm < 0 until then.
+    const int bslot = 2 * (m + 2) + 4;
+    multidot(c, b, 1, b, bslot, 0);
+    double bnorm = -1.0, tol = 0.0, beta = 0.0;
     const double* r = b;
     int it = 0, restarts = 0;
     while (true) {
-        LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, nullptr, beta, c->Z);
+        if (bnorm < 0.0) LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, c->dh + bslot, 0.0, c->Z);
+        else LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, nullptr, beta, c->Z);
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = beta;
         int kdim = 0;
@@ -1280,7 +1330,8 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
             cgs_sweep(c, 0, j + 1, nullptr, c->wv, hoff);
             cgs_sweep(c, 1, j + 1, c->dh + hoff, c->wv, h2off);
             cgs_sweep(c, 2, j + 1, c->dh + h2off, c->wv, h2off + j + 1);
-            CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (2 * (m + 2)), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (bnorm < 0.0 ? bslot + 1 : 2 * (m + 2)),
+                               cudaMemcpyDeviceToHost, c->s));
             CK(cudaEventRecord(c->ev_dots, c->s));
             // while the host reads the dots: the next basis vector V_{j+1} =
             // w / ||w|| (norm on the device) and the first sweep of its V-cycle,
@@ -1292,6 +1343,18 @@ int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
                 head_done = vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1));
             }
             CK(cudaEventSynchronize(c->ev_dots));
+            if (bnorm < 0.0) {  // first read: ||b||, and a deferred rebuild check
+                check_deferred_err(c);
+                bnorm = std::sqrt(c->hpin[bslot]);
+                if (bnorm == 0.0) {  // x = 0 (the launched work is discarded)
+                    CK(cudaStreamSynchronize(c->s));
+                    st->converged = 1;
+                    return IBMG_OK;
+                }
+                tol = c->prm.rtol * bnorm;
+                beta = bnorm;
+                g[0] = beta;
+            }
             for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = c->hpin[hoff + i] + c->hpin[h2off + i];
             const double hnext = std::sqrt(c->hpin[h2off + j + 1]);
             H[size_t(j + 1) * m + j] = hnext;
@@ -1422,6 +1485,12 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     try {
         CK(cudaSetDevice(p->device));
         CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_sizes, cudaEventDisableTiming));
+        CK(cudaEventCreate(&c->ev_t0));
+        CK(cudaEventCreate(&c->ev_t1));
         CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
         CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * gj_ld(49) * 8));
         CK(cudaFuncSetAttribute(k_big_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
@@ -1501,6 +1570,12 @@ void ibmg_destroy(ibmg_ctx* c) {
     }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->s) cudaStreamDestroy(c->s);
+    if (c->s2) cudaStreamDestroy(c->s2);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_sizes) cudaEventDestroy(c->ev_sizes);
+    if (c->ev_t0) cudaEventDestroy(c->ev_t0);
+    if (c->ev_t1) cudaEventDestroy(c->ev_t1);
     delete c;
 }
 
@@ -1896,11 +1971,13 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
             CK(cudaMemcpyAsync(c->stage_a, u, sizeof(double) * 2 * nn, cudaMemcpyHostToDevice, c->s));
             du = c->stage_a;
         }
-        rebuild(c);
+        CK(cudaEventRecord(c->ev_t0, c->s));
+        rebuild(c, true);
         build_rhs(c, du, c->bv);
-        CK(cudaStreamSynchronize(c->s));
+        CK(cudaEventRecord(c->ev_t1, c->s));
         const double t1 = now_ms();
         const int rc = fgmres(c, c->bv, c->xv, st);
+        check_deferred_err(c);
         CK(cudaStreamSynchronize(c->s));
         const double t2 = now_ms();
         if (c->npts)
@@ -1911,7 +1988,9 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
         CK(cudaMemcpyAsync(p, c->xv + 2 * nn, sizeof(double) * nn, k, c->s));
         if (c->npts) CK(cudaMemcpyAsync(X, c->X, sizeof(double) * 2 * c->npts, k, c->s));
         CK(cudaStreamSynchronize(c->s));
-        st->setup_ms = t1 - t0;
+        float setup_ms = 0.f;  // device time of the rebuild + RHS (events)
+        CK(cudaEventElapsedTime(&setup_ms, c->ev_t0, c->ev_t1));
+        st->setup_ms = setup_ms;
         st->solve_ms = t2 - t1;
         st->total_ms = now_ms() - t0;
         return rc;
