@@ -165,11 +165,27 @@ def cgs_bytes(step_iters, restart, M):
     return tot
 
 
+def ortho_bytes(step_iters, restart, M, which):
+    """Compulsory bytes of the two-pass orthogonalisation (k_ortho_dots /
+    k_ortho_update) at basis index j: the dots read V_0..V_j and w (j + 2
+    vectors); the update reads them and writes V_j and w (j + 4)."""
+    tot = 0
+    for it in step_iters:
+        j = 0
+        for _ in range(it):
+            tot += ((j + 2) if which == "dots" else (j + 4)) * 8 * M
+            j = j + 1 if j + 1 < restart else 0
+    return tot
+
+
 def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     """Algorithmic (compulsory fp64) bytes of all launches of `name` in the
     profiled pass (SURVEY.md §8d per-cell figures x cells)."""
     if "k_cgs_sweep" in name:
         return cgs_bytes(ctxinfo["step_iters"], 30, 3 * ctxinfo["N"] ** 2)
+    if "k_ortho_dots" in name or "k_ortho_update" in name:
+        return ortho_bytes(ctxinfo["step_iters"], 30, 3 * ctxinfo["N"] ** 2,
+                           "dots" if "dots" in name else "update")
     lv = ctxinfo["levels"]  # list of (n, nbig) for multi-tile levels (n >= 32)
     sweeps = 2  # V(1,1)
     N = ctxinfo["N"]

@@ -686,6 +686,185 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
     if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// ---- two-pass (lagged) CGS2 orthogonalisation of FGMRES ----
+// At Arnoldi step j the basis slot V_j holds q, orthogonalised once against
+// V_0..V_{j-1} and normalised; w = A M q.  Pass 1 (k_ortho_dots) reads
+// V_0..V_j and w once: b_i = V_i.w, a_i = V_i.q (i < j), gamma = q.w,
+// delta = q.q; its last CTA forms nu = sqrt(delta - |a|^2) (q's norm after
+// the second orthogonalisation), h = (gamma - a.b) / nu (= v_j.w),
+// s = h / nu and c_i = b_i - a_i s.  Pass 2 (k_ortho_update) reads
+// V_0..V_j and w once more and writes v_j = (q - sum a_i V_i) / nu into V_j
+// (q's re-orthogonalisation, lagged by one step) and w1 = w - sum c_i V_i - s q
+// (w projected once against V_0..V_j), plus |w1|^2.  Two passes over the
+// basis per step instead of CGS2's three; in exact arithmetic the same
+// Arnoldi basis.  dh layout (ld = restart + 2): [b | gamma] at 0,
+// [a | delta] at ld, c at 4 ld, scalars at 5 ld: 1/nu, s, nu, h, |w1|^2.
+// 3 CTAs per SM (2 for KMAX 32) of 256 threads: room for the unrolled loads
+template <int KMAX>
+constexpr int ortho_dots_blocks() { return KMAX > 16 ? 2 * 148 : 3 * 148; }
+template <int KMAX>
+__global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
+    k_ortho_dots(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ w, size_t m,
+                 double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
+    pdl_enter();
+    constexpr int KH = KMAX / 2;  // i-range per thread half
+    __shared__ double red[kRedThreads / 32][2 * KH];
+    __shared__ double fin[2 * KMAX];
+    __shared__ double s_coef;
+    const int th = threadIdx.x & 127, half = threadIdx.x >> 7;
+    const int kh = (k + 1) >> 1, i0 = half * kh, ni = min(kh, k - i0);
+    const double* qv_ptr = V + stride * (k - 1);
+    // few basis vectors per thread => several elements per iteration, so
+    // every thread keeps enough loads in flight at small k
+    constexpr int UNR = KH <= 4 ? 4 : 1;
+    constexpr int BAT = KH < 8 ? KH : 8;
+    double aw[KH], aq[KH];
+#pragma unroll
+    for (int i = 0; i < KH; ++i) aw[i] = aq[i] = 0.0;
+    const size_t step = (size_t)gridDim.x * 128;
+    for (size_t q0 = (size_t)blockIdx.x * 128 + th; q0 < m; q0 += step * UNR) {
+        double x[UNR], qq[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const size_t q = q0 + u * step;
+            x[u] = q < m ? w[q] : 0.0;
+            qq[u] = q < m ? qv_ptr[q] : 0.0;
+        }
+#pragma unroll
+        for (int b0 = 0; b0 < KH; b0 += BAT) {
+            double v[BAT][UNR];
+#pragma unroll
+            for (int i = 0; i < BAT; ++i)
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const size_t q = q0 + u * step;
+                    v[i][u] = (b0 + i < ni && q < m) ? __ldcs(V + stride * (i0 + b0 + i) + q) : 0.0;
+                }
+#pragma unroll
+            for (int i = 0; i < BAT; ++i)
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    aw[b0 + i] += v[i][u] * x[u];
+                    aq[b0 + i] += v[i][u] * qq[u];
+                }
+        }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < KH; ++i) {
+        const double tw = warp_sum(aw[i]), tq = warp_sum(aq[i]);
+        if (lane == 0) {
+            red[wid][i] = tw;
+            red[wid][KH + i] = tq;
+        }
+    }
+    __syncthreads();
+    // dot d: which = d / k (0: with w, 1: with q), index i = d % k
+    for (int d = threadIdx.x; d < 2 * k; d += blockDim.x) {
+        const int which = d / k, i = d - which * k, hh = i / kh, sl = i - hh * kh;
+        double t = 0.0;
+        for (int ww = 4 * hh; ww < 4 * hh + 4; ++ww) t += red[ww][which * KH + sl];
+        partial[(size_t)d * gridDim.x + blockIdx.x] = t;
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int d = wid; d < 2 * k; d += kRedThreads / 32) {
+        double t = 0.0;
+        for (int x = lane; x < (int)gridDim.x; x += 32) t += __ldcg(partial + (size_t)d * gridDim.x + x);
+        t = warp_sum(t);
+        if (lane == 0) fin[d] = t;
+    }
+    __syncthreads();
+    const double* bw = fin;      // b_i (i < k-1), gamma = bw[k-1]
+    const double* aqd = fin + k; // a_i (i < k-1), delta = aqd[k-1]
+    if (wid == 0) {
+        double na = 0.0, ab = 0.0;
+        for (int i = lane; i < k - 1; i += 32) {
+            na += aqd[i] * aqd[i];
+            ab += aqd[i] * bw[i];
+        }
+        na = warp_sum(na);
+        ab = warp_sum(ab);
+        if (lane == 0) {
+            const double nu = sqrt(aqd[k - 1] - na), h = (bw[k - 1] - ab) / nu;
+            dh[5 * ld] = 1.0 / nu;
+            dh[5 * ld + 1] = h / nu;
+            dh[5 * ld + 2] = nu;
+            dh[5 * ld + 3] = h;
+            s_coef = h / nu;  // s for the coefficients below
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        dh[i] = bw[i];
+        dh[ld + i] = aqd[i];
+        if (i < k - 1) dh[4 * ld + i] = bw[i] - aqd[i] * s_coef;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
+    k_ortho_update(double* __restrict__ V, size_t stride, int k, double* __restrict__ w, size_t m,
+                   double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
+    pdl_enter();
+    __shared__ double as[KMAX], cs[KMAX];
+    __shared__ double red[kRedThreads / 32];
+    if (threadIdx.x < KMAX) {
+        const bool on = (int)threadIdx.x < k - 1;
+        as[threadIdx.x] = on ? dh[ld + threadIdx.x] : 0.0;
+        cs[threadIdx.x] = on ? dh[4 * ld + threadIdx.x] : 0.0;
+    }
+    __syncthreads();
+    const double inu = dh[5 * ld], sq = dh[5 * ld + 1];
+    double* qv_ptr = V + stride * (k - 1);
+    double acc = 0.0;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
+        double v[KMAX];
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) v[i] = (i < k - 1) ? __ldcs(V + stride * i + q) : 0.0;
+        const double qq = qv_ptr[q];
+        double x = w[q], t = qq;
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) {
+            t -= as[i] * v[i];
+            x -= cs[i] * v[i];
+        }
+        x -= sq * qq;
+        qv_ptr[q] = t * inu;
+        w[q] = x;
+        acc += x * x;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    acc = warp_sum(acc);
+    if (lane == 0) red[wid] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int ww = 0; ww < kRedThreads / 32; ++ww) t += red[ww];
+        partial[blockIdx.x] = t;
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (wid == 0) {
+        double t = 0.0;
+        for (int x = lane; x < (int)gridDim.x; x += 32) t += __ldcg(partial + x);
+        t = warp_sum(t);
+        if (lane == 0) dh[5 * ld + 4] = t;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
 // w -= sum_{i<k} h[i] V_i   (one pass over w and the V's).
 __global__ void k_multi_axpy_sub(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ h,
                                  double* __restrict__ w, size_t m) {

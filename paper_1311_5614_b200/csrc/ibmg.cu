@@ -176,6 +176,7 @@ struct ibmg_ctx {
     bool rr_tiled = true;   // tiled residual + restriction where the coarse side is >= 32 (IBMG_RR_TILED=0: off)
     bool rr_csr = true;     // ... with E' from the assembled rows on point-dense levels (IBMG_RR_CSR=0: off)
     bool ap_tiled = true;   // tiled operator apply where n >= 64 (IBMG_AP_TILED=0: off)
+    bool ortho2 = true;     // FGMRES with the two-pass lagged CGS2 (IBMG_CGS2=1: three-sweep CGS2)
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
@@ -392,14 +393,14 @@ void alloc_levels(ibmg_ctx* c) {
     c->bv = dalloc<double>(c->M);
     c->stage_a = dalloc<double>(c->M);
     c->stage_b = dalloc<double>(c->M);
-    c->partial = dalloc<double>(size_t(std::max(kRedBlocks, kCgsBlocks)) * (m + 2));
+    c->partial = dalloc<double>(size_t(std::max(kRedBlocks, kCgsBlocks)) * 2 * (m + 2));
     CK(cudaEventCreateWithFlags(&c->ev_dots, cudaEventDisableTiming));
     c->ticket = dalloc<unsigned>(1);
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     c->tail_cnt = dalloc<unsigned long long>(1);
     CK(cudaMemset(c->tail_cnt, 0, sizeof(unsigned long long)));
-    c->dh = dalloc<double>(2 * (m + 2) + 8);
-    CK(cudaMallocHost(&c->hpin, sizeof(double) * (2 * (m + 2) + 8)));
+    c->dh = dalloc<double>(7 * (m + 2) + 8);
+    CK(cudaMallocHost(&c->hpin, sizeof(double) * (7 * (m + 2) + 8)));
     CK(cudaMallocHost(&c->hpin_i, sizeof(int) * (16 + 20 * kCtr)));
     c->ones = dalloc<double>(size_t(p.N) * p.N);
     {
@@ -1296,9 +1297,177 @@ double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Two-pass orthogonalisation launches (grid_kernels.cuh k_ortho_dots /
+// k_ortho_update): k = j + 1 basis slots, the last one holding q.
+template <int KM>
+void ortho_dots_k(ibmg_ctx* c, int k, double* w) {
+    LAUNCH(c, (k_ortho_dots<KM>), ortho_dots_blocks<KM>(), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
+           c->partial, c->dh, c->prm.restart + 2, c->ticket);
+}
+template <int KM>
+void ortho_update_k(ibmg_ctx* c, int k, double* w) {
+    LAUNCH(c, (k_ortho_update<KM>), kCgsBlocks, kRedThreads, 0, c->V, c->Mst, k, w, c->Mk, c->partial, c->dh,
+           c->prm.restart + 2, c->ticket);
+}
+void ortho_dots(ibmg_ctx* c, int k, double* w) {
+    if (k <= 8) ortho_dots_k<8>(c, k, w);
+    else if (k <= 16) ortho_dots_k<16>(c, k, w);
+    else ortho_dots_k<32>(c, k, w);
+}
+void ortho_update(ibmg_ctx* c, int k, double* w) {
+    if (k - 1 <= 8) ortho_update_k<8>(c, k, w);
+    else if (k - 1 <= 16) ortho_update_k<16>(c, k, w);
+    else if (k - 1 <= 24) ortho_update_k<24>(c, k, w);
+    else ortho_update_k<32>(c, k, w);
+}
+
+// Givens QR of the (kdim + 1) x kdim Hessenberg H (row-major, m columns) and
+// back substitution: y = argmin |g0 e_1 - H y|; returns |residual estimate|.
+double hessenberg_lsq(const std::vector<double>& Hin, int m, int kdim, double g0, std::vector<double>& y) {
+    std::vector<double> H(Hin), g(kdim + 1, 0.0), cs(kdim), sn(kdim);
+    g[0] = g0;
+    for (int j = 0; j < kdim; ++j) {
+        for (int i = 0; i < j; ++i) {
+            const double a = H[size_t(i) * m + j], b = H[size_t(i + 1) * m + j];
+            H[size_t(i) * m + j] = cs[i] * a + sn[i] * b;
+            H[size_t(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+        }
+        const double a = H[size_t(j) * m + j], b = H[size_t(j + 1) * m + j];
+        const double den = std::hypot(a, b);
+        cs[j] = a / den;
+        sn[j] = b / den;
+        H[size_t(j) * m + j] = den;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+    }
+    for (int i = kdim - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int k = i + 1; k < kdim; ++k) s -= H[size_t(i) * m + k] * y[k];
+        y[i] = s / H[size_t(i) * m + i];
+    }
+    return std::fabs(g[kdim]);
+}
+
+// FGMRES(m) as fgmres() below, with the two-pass lagged CGS2 (k_ortho_*):
+// per Arnoldi step one V-cycle on q_j, one apply, two passes over the basis.
+// Column j of H is exact only after step j + 1 (q_{j+1}'s re-orthogonalisation
+// coefficients a, nu): the convergence check runs a Givens QR over the
+// columns as known (b, h, |w1|: round-off away from the exact ones), and the
+// least-squares solution is taken from the corrected H (last column with
+// a = 0, nu = 1: its correction is at round-off level).
+int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
+    const int m = c->prm.restart, ld = m + 2;
+    const int SC = 5 * ld, bslot = 6 * ld + 2;
+    const size_t M = c->M;
+    std::vector<double> Hx(size_t(m + 1) * m, 0.0), Ha(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m);
+    st->iters = st->restarts = st->converged = 0;
+    st->relres = 0.0;
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * M, c->s));
+    multidot(c, b, 1, b, bslot, 0);
+    double bnorm = -1.0, tol = 0.0, beta = 0.0;
+    const double* r = b;
+    int it = 0, restarts = 0;
+    while (true) {
+        if (bnorm < 0.0) LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, c->dh + bslot, 0.0, c->Z);
+        else LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, r, c->V, M, nullptr, beta, c->Z);
+        std::fill(g.begin(), g.end(), 0.0);
+        std::fill(Hx.begin(), Hx.end(), 0.0);
+        g[0] = beta;
+        int kdim = 0;
+        double nu0 = 1.0, beta_j = 0.0;  // beta_j: the norm q_j was scaled by
+        bool head_done = false;
+        for (int j = 0; j < m; ++j) {
+            double* Vj = c->V + c->Mst * j;
+            double* Zj = c->Z + c->Mst * j;
+            vcycle(c, Vj, Zj, false, true, head_done);
+            apply_level(c, 0, Zj, c->wv);
+            ortho_dots(c, j + 1, c->wv);
+            ortho_update(c, j + 1, c->wv);
+            CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (bslot + 1), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaEventRecord(c->ev_dots, c->s));
+            head_done = false;
+            if (j + 1 < m) {  // q_{j+1} = w1 / |w1| and its first sweep, speculatively
+                LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + c->Mst * (j + 1), M, c->dh + SC + 4, 0.0,
+                       c->Z + c->Mst * (j + 1));
+                head_done = vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1));
+            }
+            CK(cudaEventSynchronize(c->ev_dots));
+            const double* hp = c->hpin;
+            if (bnorm < 0.0) {  // first read: ||b||, and a deferred rebuild check
+                check_deferred_err(c);
+                bnorm = std::sqrt(hp[bslot]);
+                if (bnorm == 0.0) {
+                    CK(cudaStreamSynchronize(c->s));
+                    st->converged = 1;
+                    return IBMG_OK;
+                }
+                tol = c->prm.rtol * bnorm;
+                beta = bnorm;
+                g[0] = beta;
+            }
+            if (j == 0) beta_j = beta;
+            const double nu = hp[SC + 2], h = hp[SC + 3], bnext = std::sqrt(hp[SC + 4]);
+            // exact column j-1 (q_j's re-orthogonalisation): + beta_j a, bottom beta_j nu
+            if (j == 0) {
+                nu0 = nu;
+            } else {
+                for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j - 1] += beta_j * hp[ld + i];
+                Hx[size_t(j) * m + j - 1] = beta_j * nu;
+            }
+            // column j as known now
+            for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j] = hp[i];
+            Hx[size_t(j) * m + j] = h;
+            Hx[size_t(j + 1) * m + j] = bnext;
+            // running QR of the known columns (convergence check)
+            for (int i = 0; i <= j + 1; ++i) Ha[size_t(i) * m + j] = Hx[size_t(i) * m + j];
+            for (int i = 0; i < j; ++i) {
+                const double a = Ha[size_t(i) * m + j], cc = Ha[size_t(i + 1) * m + j];
+                Ha[size_t(i) * m + j] = cs[i] * a + sn[i] * cc;
+                Ha[size_t(i + 1) * m + j] = -sn[i] * a + cs[i] * cc;
+            }
+            const double a = Ha[size_t(j) * m + j], cc = Ha[size_t(j + 1) * m + j];
+            const double den = std::hypot(a, cc);
+            cs[j] = a / den;
+            sn[j] = cc / den;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++it;
+            kdim = j + 1;
+            beta_j = bnext;
+            if (!std::isfinite(g[j + 1])) throw CudaError("FGMRES: non-finite residual estimate");
+            if (std::fabs(g[j + 1]) <= tol || it >= c->prm.max_iters || bnext == 0.0) break;
+        }
+        // r = beta q_0 = beta nu0 v_0: least squares on the corrected H
+        hessenberg_lsq(Hx, m, kdim, beta * nu0, y);
+        std::copy(y.begin(), y.begin() + kdim, c->hpin);
+        CK(cudaMemcpyAsync(c->dh + 4 * ld, c->hpin, sizeof(double) * kdim, cudaMemcpyHostToDevice, c->s));
+        LAUNCH(c, k_multi_axpy_add, nblk(M), 256, 0, c->Z, c->Mst, kdim, c->dh + 4 * ld, x, M);
+        // true residual
+        apply_level(c, 0, x, c->rv);
+        LAUNCH(c, k_b_minus, nblk(M), 256, 0, b, c->rv, M);
+        multidot(c, c->rv, 1, c->rv, 0, 0);
+        CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        beta = std::sqrt(c->hpin[0]);
+        r = c->rv;
+        if (beta <= tol) {
+            st->converged = 1;
+            break;
+        }
+        if (it >= c->prm.max_iters) break;
+        ++restarts;
+    }
+    pressure_mean_zero(c, x);
+    st->iters = it;
+    st->restarts = restarts;
+    st->relres = beta / bnorm;
+    return st->converged ? IBMG_OK : IBMG_NOT_CONVERGED;
+}
+
 // FGMRES(m) with one V-cycle as right preconditioner, x0 = 0, CGS2, true
 // residual check at each restart (oracle fgmres()).
 int fgmres(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
+    if (c->ortho2) return fgmres2(c, b, x, st);
     const int m = c->prm.restart;
     const size_t M = c->M;
     const int hoff = 0, h2off = m + 2;  // dh layout: [h (m+1)] [h2 (m+1)] [scratch]
@@ -1478,6 +1647,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_RR_CSR")) c->rr_csr = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_RR_CSR_RATIO")) c->rr_csr_ratio = std::atof(e);
     if (const char* e = std::getenv("IBMG_AP_TILED")) c->ap_tiled = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_CGS2")) c->ortho2 = std::atoi(e) == 0;
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
     c->prm = *p;
