@@ -810,8 +810,9 @@ __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
 
 template <int KMAX>
 __global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
-    k_ortho_update(double* __restrict__ V, size_t stride, int k, double* __restrict__ w, size_t m,
-                   double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
+    k_ortho_update(double* __restrict__ V, size_t stride, int k, const double* __restrict__ w,
+                   double* __restrict__ w1out, double* __restrict__ zero, size_t m, double* __restrict__ partial,
+                   double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
     pdl_enter();
     __shared__ double as[KMAX], cs[KMAX];
     __shared__ double red[kRedThreads / 32];
@@ -837,7 +838,8 @@ __global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
         }
         x -= sq * qq;
         qv_ptr[q] = t * inu;
-        w[q] = x;
+        w1out[q] = x;
+        if (zero) zero[q] = 0.0;
         acc += x * x;
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

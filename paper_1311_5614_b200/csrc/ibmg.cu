@@ -1305,20 +1305,20 @@ void ortho_dots_k(ibmg_ctx* c, int k, double* w) {
            c->partial, c->dh, c->prm.restart + 2, c->ticket);
 }
 template <int KM>
-void ortho_update_k(ibmg_ctx* c, int k, double* w) {
-    LAUNCH(c, (k_ortho_update<KM>), kCgsBlocks, kRedThreads, 0, c->V, c->Mst, k, w, c->Mk, c->partial, c->dh,
-           c->prm.restart + 2, c->ticket);
+void ortho_update_k(ibmg_ctx* c, int k, const double* w, double* w1out, double* zero) {
+    LAUNCH(c, (k_ortho_update<KM>), kCgsBlocks, kRedThreads, 0, c->V, c->Mst, k, w, w1out, zero, c->Mk, c->partial,
+           c->dh, c->prm.restart + 2, c->ticket);
 }
 void ortho_dots(ibmg_ctx* c, int k, double* w) {
     if (k <= 8) ortho_dots_k<8>(c, k, w);
     else if (k <= 16) ortho_dots_k<16>(c, k, w);
     else ortho_dots_k<32>(c, k, w);
 }
-void ortho_update(ibmg_ctx* c, int k, double* w) {
-    if (k - 1 <= 8) ortho_update_k<8>(c, k, w);
-    else if (k - 1 <= 16) ortho_update_k<16>(c, k, w);
-    else if (k - 1 <= 24) ortho_update_k<24>(c, k, w);
-    else ortho_update_k<32>(c, k, w);
+void ortho_update(ibmg_ctx* c, int k, const double* w, double* w1out, double* zero) {
+    if (k - 1 <= 8) ortho_update_k<8>(c, k, w, w1out, zero);
+    else if (k - 1 <= 16) ortho_update_k<16>(c, k, w, w1out, zero);
+    else if (k - 1 <= 24) ortho_update_k<24>(c, k, w, w1out, zero);
+    else ortho_update_k<32>(c, k, w, w1out, zero);
 }
 
 // Givens QR of the (kdim + 1) x kdim Hessenberg H (row-major, m columns) and
@@ -1374,7 +1374,7 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
         std::fill(Hx.begin(), Hx.end(), 0.0);
         g[0] = beta;
         int kdim = 0;
-        double nu0 = 1.0, beta_j = 0.0;  // beta_j: the norm q_j was scaled by
+        double nu0 = 1.0;
         bool head_done = false;
         for (int j = 0; j < m; ++j) {
             double* Vj = c->V + c->Mst * j;
@@ -1382,15 +1382,14 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
             vcycle(c, Vj, Zj, false, true, head_done);
             apply_level(c, 0, Zj, c->wv);
             ortho_dots(c, j + 1, c->wv);
-            ortho_update(c, j + 1, c->wv);
+            // q_{j+1} = w1 (unnormalised) straight into the next slot, Z_{j+1} = 0
+            const bool more = j + 1 < m;
+            ortho_update(c, j + 1, c->wv, more ? c->V + c->Mst * (j + 1) : c->rv,
+                         more ? c->Z + c->Mst * (j + 1) : nullptr);
             CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (bslot + 1), cudaMemcpyDeviceToHost, c->s));
             CK(cudaEventRecord(c->ev_dots, c->s));
-            head_done = false;
-            if (j + 1 < m) {  // q_{j+1} = w1 / |w1| and its first sweep, speculatively
-                LAUNCH(c, k_scale_by_norm, nblk(M), 256, 0, c->wv, c->V + c->Mst * (j + 1), M, c->dh + SC + 4, 0.0,
-                       c->Z + c->Mst * (j + 1));
-                head_done = vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1));
-            }
+            // the next V-cycle's first sweep, speculatively
+            head_done = more && vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1));
             CK(cudaEventSynchronize(c->ev_dots));
             const double* hp = c->hpin;
             if (bnorm < 0.0) {  // first read: ||b||, and a deferred rebuild check
@@ -1405,14 +1404,13 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
                 beta = bnorm;
                 g[0] = beta;
             }
-            if (j == 0) beta_j = beta;
             const double nu = hp[SC + 2], h = hp[SC + 3], bnext = std::sqrt(hp[SC + 4]);
-            // exact column j-1 (q_j's re-orthogonalisation): + beta_j a, bottom beta_j nu
+            // exact column j-1: q_j = w1 = sum a_i V_i + nu v_j
             if (j == 0) {
                 nu0 = nu;
             } else {
-                for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j - 1] += beta_j * hp[ld + i];
-                Hx[size_t(j) * m + j - 1] = beta_j * nu;
+                for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j - 1] += hp[ld + i];
+                Hx[size_t(j) * m + j - 1] = nu;
             }
             // column j as known now
             for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j] = hp[i];
@@ -1433,7 +1431,6 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
             g[j] = cs[j] * g[j];
             ++it;
             kdim = j + 1;
-            beta_j = bnext;
             if (!std::isfinite(g[j + 1])) throw CudaError("FGMRES: non-finite residual estimate");
             if (std::fabs(g[j + 1]) <= tol || it >= c->prm.max_iters || bnext == 0.0) break;
         }
