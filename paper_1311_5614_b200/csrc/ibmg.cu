@@ -750,11 +750,8 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
                 if (reach > 7 && c->implicit_ib)
                     throw InvalidArg("E' reach " + std::to_string(reach) + " exceeds the 8-cell same-colour gap on level " +
                                      std::to_string(l) + " (Lagrangian spacing too large)");
-                colour_big_blocks(c, lb, lb.h_cm);
-                tr.mark(("coloured level " + std::to_string(l) + " nbig " + std::to_string(lb.nbig)).c_str());
             }
         }
-        tr.mark("coloured");
         // assembled E'_l rows of every level (count, one scan, fill): row q is
         // run q of the batched face lists; per-level views follow
         {
@@ -812,6 +809,13 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             coarse_inverse_forked(c);
             coarse_forked = true;
         }
+        // big-block colouring on the host, while the GPU assembles the E' rows
+        for (int l = 0; l + 1 < c->nlev; ++l) {
+            LevelBuf& lb = c->lev[l];
+            colour_big_blocks(c, lb, lb.h_cm);
+            tr.mark(("coloured level " + std::to_string(l) + " nbig " + std::to_string(lb.nbig)).c_str());
+        }
+        tr.mark("coloured");
         // big-block E' row ranges, slabs and inverses of every level: one
         // launch each over the level-major block numbering
         BSetup S{};

@@ -11,7 +11,7 @@ from paper_1311_5614_b200 import configs  # noqa: E402
 from paper_1311_5614_b200.ibmg import SaddleSystem  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
-prob = configs.config2(1e4) if cfg == "C2" else configs.config3()
+prob = {"C2": lambda: configs.config2(1e4), "C3": configs.config3, "C4": configs.config4}[cfg]()
 g = SaddleSystem.from_problem(prob)
 for _ in range(3):
     g.set_structures(prob.nb, prob.kappa, prob.ds, prob.X)
