@@ -20,8 +20,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-fi
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launches.log 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 python tools/profile_solve.py C4 > /dev/null 2>&1 || exit 1
-ncu --metrics $M --clock-control none -k regex:"k_plain_df|k_big_phase|k_cgs_sweep|k_residual_restrict|k_stokes_apply|k_prolong_add|k_scale_by_norm" \
-    -c 60 --csv --log-file $O/c4_traffic.csv python tools/profile_solve.py C4 > $O/ncu_c4.log 2>&1
+ncu --metrics $M --clock-control none -k regex:"k_plain_df|k_big_phase|k_ortho|k_residual_restrict|k_stokes_apply|k_prolong_add|k_scale_by_norm" \
+    -c 90 --csv --log-file $O/c4_traffic.csv python tools/profile_solve.py C4 > $O/ncu_c4.log 2>&1
 python tools/profile_vcycle.py 256 3 > /dev/null 2>&1 || exit 1
 ncu --metrics $M --clock-control none -k regex:k_sweep_df -c 6 --csv --log-file $O/c2_sweep_df.csv \
     python tools/profile_vcycle.py 256 3 > /dev/null 2>&1
