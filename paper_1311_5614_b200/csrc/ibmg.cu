@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -106,7 +107,9 @@ struct LevelBuf {
 
     double* Ainv = nullptr;
     int ainv_cap = 0;
-    std::vector<int> h_ids, h_pred, h_poff;  // host sources of the async uploads above
+    std::vector<int> h_ids, h_pred, h_poff;  // host results of the colouring
+    int* h_up = nullptr;                     // pinned staging of their uploads (async, no stream sync)
+    size_t h_up_cap = 0;
     std::vector<int> h_pos;                  // block -> list position scratch (colouring)
     unsigned* h_cm = nullptr;                // pinned mirror of cmask
 };
@@ -603,15 +606,27 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
             CK(cudaMemset(lb.tflags, 0, sizeof(unsigned) * (lb.L.n / kTile) * (lb.L.n / kTile)));
         lb.epoch = 0;
     }
-    // the host copies stay alive in the level until the next rebuild (which
-    // starts after rebuild()'s final synchronisation), so no sync here
     lb.h_ids = std::move(ids);
     lb.h_pred = std::move(pred);
     lb.h_poff = std::move(poff);
-    if (nbig) CK(cudaMemcpyAsync(lb.blk_ids, lb.h_ids.data(), sizeof(int) * nbig, cudaMemcpyHostToDevice, c->s));
+    // uploads from a pinned staging buffer: truly asynchronous (a pageable
+    // source would synchronise the stream first).  The buffer is rewritten
+    // only by the next rebuild, after the solve's synchronisations.
+    const size_t need = size_t(nbig) + lb.h_pred.size() + size_t(nbig + 1);
+    if (lb.h_up_cap < need) {
+        if (lb.h_up) CK(cudaFreeHost(lb.h_up));
+        lb.h_up_cap = size_t(grow_cap(long(need), long(lb.h_up_cap)));
+        CK(cudaMallocHost(&lb.h_up, sizeof(int) * lb.h_up_cap));
+    }
+    int* up = lb.h_up;
+    std::copy(lb.h_ids.begin(), lb.h_ids.end(), up);
+    std::copy(lb.h_pred.begin(), lb.h_pred.end(), up + nbig);
+    std::copy(lb.h_poff.begin(), lb.h_poff.end(), up + nbig + lb.h_pred.size());
+    if (nbig) CK(cudaMemcpyAsync(lb.blk_ids, up, sizeof(int) * nbig, cudaMemcpyHostToDevice, c->s));
     if (!lb.h_pred.empty())
-        CK(cudaMemcpyAsync(lb.pred, lb.h_pred.data(), sizeof(int) * lb.h_pred.size(), cudaMemcpyHostToDevice, c->s));
-    CK(cudaMemcpyAsync(lb.poff, lb.h_poff.data(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(lb.pred, up + nbig, sizeof(int) * lb.h_pred.size(), cudaMemcpyHostToDevice, c->s));
+    CK(cudaMemcpyAsync(lb.poff, up + nbig + lb.h_pred.size(), sizeof(int) * (nbig + 1), cudaMemcpyHostToDevice,
+                       c->s));
 }
 
 void check_err_flag(ibmg_ctx* c, const char* where) {
@@ -809,11 +824,26 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             coarse_inverse_forked(c);
             coarse_forked = true;
         }
-        // big-block colouring on the host, while the GPU assembles the E' rows
-        for (int l = 0; l + 1 < c->nlev; ++l) {
-            LevelBuf& lb = c->lev[l];
-            colour_big_blocks(c, lb, lb.h_cm);
-            tr.mark(("coloured level " + std::to_string(l) + " nbig " + std::to_string(lb.nbig)).c_str());
+        // big-block colouring on the host, while the GPU assembles the E' rows;
+        // levels are independent: on large problems the coarser levels colour
+        // on worker threads beside level 0
+        {
+            long blocks = 0;
+            for (int l = 0; l + 1 < c->nlev; ++l) blocks += long(c->lev[l].L.n / 4) * (c->lev[l].L.n / 4);
+            std::vector<std::future<void>> jobs;
+            if (blocks >= (1L << 20))
+                for (int l = 1; l + 1 < c->nlev; ++l)
+                    jobs.push_back(std::async(std::launch::async, [c, l] {
+                        CK(cudaSetDevice(c->prm.device));
+                        colour_big_blocks(c, c->lev[l], c->lev[l].h_cm);
+                    }));
+            for (int l = 0; l + 1 < c->nlev; ++l) {
+                if (l > 0 && !jobs.empty()) break;
+                LevelBuf& lb = c->lev[l];
+                colour_big_blocks(c, lb, lb.h_cm);
+                tr.mark(("coloured level " + std::to_string(l) + " nbig " + std::to_string(lb.nbig)).c_str());
+            }
+            for (auto& j : jobs) j.get();
         }
         tr.mark("coloured");
         // big-block E' row ranges, slabs and inverses of every level: one
@@ -1709,6 +1739,7 @@ void ibmg_destroy(ibmg_ctx* c) {
 
         dfree(lb.bq);
         dfree(lb.tflags);
+        if (lb.h_up) cudaFreeHost(lb.h_up);
         dfree(lb.pdf_seg);
         dfree(lb.escr);
     }
