@@ -141,6 +141,11 @@ struct ibmg_ctx {
     uint8_t* big_all = nullptr;
     unsigned* cmask_all = nullptr;
     unsigned* h_cm_all = nullptr;  // pinned
+    // box inverses in canonical (block-id) order, computed during the colouring
+    int *cflag = nullptr, *crank = nullptr, *cids = nullptr, *ctotal = nullptr;
+    int2* crr = nullptr;
+    double* cainv = nullptr;
+    int ccap = 0;  // inverses the canonical buffers hold (grown after a step that needed more)
     int *e_cnt = nullptr, *e_rp = nullptr, *e_col = nullptr;       // batched E' rows (all levels)
     double* e_val = nullptr;
     long e_cap = 0;
@@ -180,6 +185,8 @@ struct ibmg_ctx {
     bool rr_csr = true;     // ... with E' from the assembled rows on point-dense levels (IBMG_RR_CSR=0: off)
     bool ap_tiled = true;   // tiled operator apply where n >= 64 (IBMG_AP_TILED=0: off)
     bool ortho2 = true;     // FGMRES with the two-pass lagged CGS2 (IBMG_CGS2=1: three-sweep CGS2)
+    int canon_inv = -1;     // box inverses in block-id order during the colouring: -1 auto (large
+                            // levels), IBMG_CANON_INV=1 on, 0 off
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
@@ -372,6 +379,10 @@ void alloc_levels(ibmg_ctx* c) {
     c->big_all = dalloc<uint8_t>(nb);
     c->cmask_all = dalloc<unsigned>(nb);
     CK(cudaMallocHost(&c->h_cm_all, sizeof(unsigned) * nb));
+    c->cflag = dalloc<int>(nb);
+    c->crank = dalloc<int>(nb);
+    c->cids = dalloc<int>(nb);
+    c->ctotal = dalloc<int>(1);
     for (int l = 0; l < BK.nlev; ++l) {
         c->lev[l].big = c->big_all + BK.boff[l];
         c->lev[l].cmask = c->cmask_all + BK.boff[l];
@@ -678,6 +689,10 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
     const int npts = c->npts;
     const SetupTrace tr;
     bool coarse_forked = false, side_used = false;
+    // canonical-order box inverses: single contexts (slab contexts invert
+    // their own rows only) with the option on
+    const bool canon = c->canon_inv != 0 && c->own_y0.empty() &&
+                       (c->canon_inv > 0 || c->blk_levels.boff[c->blk_levels.nlev] >= (1 << 18));
     CK(cudaMemsetAsync(c->err_flag, 0, sizeof(int), c->s));
     CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * kCtr, c->s));
     if (npts == 0) {
@@ -743,6 +758,15 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             LAUNCH(c, k_block_pairs, nblk(size_t(npts) * 2 * BK.nlev, 128), 128, 0, npts, WL, BK, c->P, c->cmask_all,
                    c->counters, kCtr);
             LAUNCH(c, k_block_conflicts, nblk(nb), 256, 0, BK, c->big_all, c->cmask_all);
+            if (canon) {  // canonical numbering of the big blocks (the colouring's vertex order)
+                LAUNCH(c, k_canon_flags, nblk(nb), 256, 0, (const unsigned*)c->cmask_all, int(nb), c->cflag);
+                size_t bytes = 0;
+                cub::DeviceScan::ExclusiveSum(nullptr, bytes, c->cflag, c->crank, int(nb), c->s);
+                ensure_cub(c, bytes);
+                CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cflag, c->crank, int(nb), c->s));
+                LAUNCH(c, k_canon_list, nblk(nb), 256, 0, (const unsigned*)c->cmask_all, int(nb),
+                       (const int*)c->crank, c->cids, c->ctotal);
+            }
             // conflict masks (big flag in bit 12) of every level in one copy
             CK(cudaMemcpyAsync(c->h_cm_all, c->cmask_all, sizeof(unsigned) * nb, cudaMemcpyDeviceToHost, c->s));
         }
@@ -823,6 +847,28 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             // runs on the side stream, beside the big-block setup below
             coarse_inverse_forked(c);
             coarse_forked = true;
+            if (canon && c->ccap > 0) {  // box inverses of every big block while the host
+                                         // colours them (side stream, after the coarsest inverse)
+                CanonInv C{};
+                const BlkLevels& BK = c->blk_levels;
+                C.nlev = BK.nlev;
+                for (int l = 0; l <= BK.nlev; ++l) C.boff[l] = BK.boff[l];
+                for (int l = 0; l < BK.nlev; ++l) {
+                    C.L[l] = c->lev[l].L;
+                    C.FL[l] = c->lev[l].FL;
+                    C.E[l] = c->lev[l].E;
+                }
+                C.ids = c->cids;
+                C.total = c->ctotal;
+                C.rr = c->crr;
+                C.Ainv = c->cainv;
+                C.cap = c->ccap;
+                std::swap(c->s, c->s2);
+                LAUNCH(c, k_canon_rows, 8 * 148, 256, 0, C);
+                LAUNCH(c, k_canon_inverse, c->ccap, 256, 56 * gj_ld(56) * sizeof(double), C, c->err_flag);
+                std::swap(c->s, c->s2);
+                CK(cudaEventRecord(c->ev_join, c->s2));
+            }
         }
         // big-block colouring on the host, while the GPU assembles the E' rows;
         // levels are independent: on large problems the coarser levels colour
@@ -915,7 +961,35 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             int* hc2 = c->hpin_i + 8;
             CK(cudaMemcpyAsync(hc2, c->counters, sizeof(int) * size_t(c->nlev) * kCtr, cudaMemcpyDeviceToHost, c->s));
             CK(cudaEventRecord(c->ev_sizes, c->s));
-            LAUNCH(c, k_block_inverse, nball, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
+            if (canon && nball <= c->ccap) {  // move the canonical inverses to list order (side
+                                              // stream: after them and after the list upload)
+                CK(cudaStreamWaitEvent(c->s2, c->ev_sizes, 0));
+                APerm P{};
+                P.nlev = S.nlev;
+                for (int k = 0; k < S.nlev; ++k) {
+                    const LevelBuf& lb = c->lev[S.lev[k]];
+                    P.boff[k] = c->blk_levels.boff[S.lev[k]];
+                    P.blk_ids[k] = lb.blk_ids;
+                    P.Ainv[k] = lb.Ainv;
+                    P.start[k] = S.start[k];
+                }
+                P.start[S.nlev] = nball;
+                std::swap(c->s, c->s2);
+                LAUNCH(c, k_ainv_permute, std::min(nball, 8 * 148), 256, 0, P, (const int*)c->crank,
+                       (const double*)c->cainv);
+                std::swap(c->s, c->s2);
+                CK(cudaEventRecord(c->ev_join, c->s2));
+                side_used = true;
+            } else {
+                LAUNCH(c, k_block_inverse, nball, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
+                if (canon) {  // size the canonical buffers for the next steps
+                    dfree(c->crr);
+                    dfree(c->cainv);
+                    c->ccap = int(grow_cap(nball, c->ccap));
+                    c->crr = dalloc<int2>(size_t(c->ccap) * 40);
+                    c->cainv = dalloc<double>(size_t(c->ccap) * 3136);
+                }
+            }
             tr.mark("launched inverses");
             CK(cudaEventSynchronize(c->ev_sizes));
             tr.mark("synced slab sizes");
@@ -1679,6 +1753,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_RR_CSR_RATIO")) c->rr_csr_ratio = std::atof(e);
     if (const char* e = std::getenv("IBMG_AP_TILED")) c->ap_tiled = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_CGS2")) c->ortho2 = std::atoi(e) == 0;
+    if (const char* e = std::getenv("IBMG_CANON_INV")) c->canon_inv = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
     c->prm = *p;
@@ -1705,6 +1780,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             CK(cudaFuncSetAttribute(k_sweep_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df, 32 * kDfWarps, kDfSmem));
             c->df_grid_max = std::max(1, per_sm * sms);
+            CK(cudaFuncSetAttribute(k_canon_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    56 * gj_ld(56) * 8));
             CK(cudaFuncSetAttribute(k_plain_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPdfSmem)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_df, 32, kPdfSmem));
             c->pdf_grid_max = std::max(1, per_sm * sms);
@@ -1756,6 +1833,12 @@ void ibmg_destroy(ibmg_ctx* c) {
     if (c->ev_dots) cudaEventDestroy(c->ev_dots);
     dfree(c->big_all);
     dfree(c->cmask_all);
+    dfree(c->cflag);
+    dfree(c->crank);
+    dfree(c->cids);
+    dfree(c->ctotal);
+    dfree(c->crr);
+    dfree(c->cainv);
     if (c->h_cm_all) cudaFreeHost(c->h_cm_all);
     dfree(c->tail_cnt);
     dfree(c->dh);

@@ -997,20 +997,13 @@ struct BInvLevels {
     int bylo[20], byhi[20];  // block rows to invert (a slab's own rows; 0, n/4 = all)
 };
 
-__global__ void k_block_inverse(BInvLevels BL, int* err) {
-    pdl_enter();
-    extern __shared__ double M[];  // 56 x gj_ld(56)
-    int lv = 0;
-    while (lv + 1 < BL.nlev && (int)blockIdx.x >= BL.start[lv + 1]) ++lv;
-    const Lev L = BL.L[lv];
-    const EMat E = BL.E[lv];
-    const int* __restrict__ blk_ids = BL.blk_ids[lv];
-    const int2* __restrict__ rr = BL.rr[lv];
-    double* __restrict__ Ainv = BL.Ainv[lv];
-    const int q = blockIdx.x - BL.start[lv], t = threadIdx.x, nt = blockDim.x, n = L.n;
-    const int B = blk_ids[q], nbk = n >> 2;
+// Assemble the 56x56 box matrix of block B (cell-block index, n/4 per row)
+// from the Stokes rows and the E' rows (rr40: the 40 velocity rows' ranges in
+// E) into M, and invert it into out (column-major).  256 threads.
+__device__ __forceinline__ void box_inverse(const Lev& L, const EMat& E, const int2* __restrict__ rr40, int B,
+                                            double* __restrict__ out, int* err, double* M) {
+    const int t = threadIdx.x, nt = blockDim.x, n = L.n, nbk = n >> 2;
     const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
-    if (B / nbk < BL.bylo[lv] || B / nbk >= BL.byhi[lv]) return;  // another slab's block
     constexpr int LD = gj_ld(56);
     for (int idx = t; idx < 56 * LD; idx += nt) M[idx] = 0.0;
     __syncthreads();
@@ -1025,15 +1018,27 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
     }
     __syncthreads();
     if (t < 40) {
-        const int2 r = rr[(size_t)q * 40 + t];
+        const int2 r = rr40[t];
         for (int e = r.x; e < r.y; ++e) {
-                const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
+            const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
             const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
             if (c >= 0) M[t * LD + c] -= E.val[e];
         }
     }
     __syncthreads();
-    gauss_jordan(M, 56, Ainv + (size_t)q * 3136, err);
+    gauss_jordan(M, 56, out, err);
+    __syncthreads();
+}
+
+__global__ void k_block_inverse(BInvLevels BL, int* err) {
+    pdl_enter();
+    extern __shared__ double M[];  // 56 x gj_ld(56)
+    int lv = 0;
+    while (lv + 1 < BL.nlev && (int)blockIdx.x >= BL.start[lv + 1]) ++lv;
+    const int q = blockIdx.x - BL.start[lv], nbk = BL.L[lv].n >> 2;
+    const int B = BL.blk_ids[lv][q];
+    if (B / nbk < BL.bylo[lv] || B / nbk >= BL.byhi[lv]) return;  // another slab's block
+    box_inverse(BL.L[lv], BL.E[lv], BL.rr[lv] + (size_t)q * 40, B, BL.Ainv[lv] + (size_t)q * 3136, err, M);
 }
 
 // Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
@@ -1086,18 +1091,10 @@ __device__ __forceinline__ int bs_level(const BSetup& S, int qg) {
     return k;
 }
 
-// E' row ranges of the 40 velocity DOFs of every block (binary search of the
+// E' row range of velocity DOF t (0..39) of block B (binary search of the
 // face list; (0, 0) for faces without an E' row).
-__global__ void k_block_rows(BSetup S) {
-    pdl_enter();
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= S.start[S.nlev] * 40) return;
-    const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
-    const Lev& L = S.L[k];
-    const FaceList& FL = S.FL[k];
+__device__ __forceinline__ int2 block_row_range(const Lev& L, const FaceList& FL, const EMat& E, int B, int t) {
     const int n = L.n, nbk = n >> 2;
-    const int B = S.blk_ids[k][q];
-    if (t == 0) S.bq[k][B] = q;
     int f, i, j;
     block_dof(t, 4 * (B % nbk), 4 * (B / nbk), f, i, j);
     const int key = f * L.nn + wr(i, n) + wr(j, n) * n;
@@ -1106,8 +1103,94 @@ __global__ void k_block_rows(BSetup S) {
         const int mid = (lo + hi) >> 1;
         if (FL.face[mid] < key) lo = mid + 1; else hi = mid;
     }
-    S.rr[k][(size_t)q * 40 + t] =
-        (lo < FL.nf && FL.face[lo] == key) ? make_int2(S.E[k].rp[lo], S.E[k].rp[lo + 1]) : make_int2(0, 0);
+    return (lo < FL.nf && FL.face[lo] == key) ? make_int2(E.rp[lo], E.rp[lo + 1]) : make_int2(0, 0);
+}
+
+// E' row ranges of the 40 velocity DOFs of every block.
+__global__ void k_block_rows(BSetup S) {
+    pdl_enter();
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= S.start[S.nlev] * 40) return;
+    const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
+    const int B = S.blk_ids[k][q];
+    if (t == 0) S.bq[k][B] = q;
+    S.rr[k][(size_t)q * 40 + t] = block_row_range(S.L[k], S.FL[k], S.E[k], B, t);
+}
+
+// ---- box inverses in canonical (block-id) order, before the colouring -------
+// The inverse of a big block does not depend on its colour: the canonical
+// pass numbers the big blocks of all levels in level-major block-id order
+// (a scan of the conflict masks; the colouring's vertex order), assembles
+// their E' row ranges and inverts them while the host colours the blocks.
+// k_ainv_permute then moves each inverse to its colour-sorted list position.
+struct CanonInv {
+    int nlev;        // levels with blocks (all but the coarsest)
+    int boff[21];    // level offsets in the level-major block numbering
+    Lev L[20];
+    FaceList FL[20];
+    EMat E[20];
+    const int* ids;    // canonical index -> level-major block index
+    const int* total;  // device: number of big blocks, all levels
+    int2* rr;          // [cap][40]
+    double* Ainv;      // [cap][3136]
+    int cap;
+};
+__device__ __forceinline__ int canon_level(const CanonInv& C, int e) {
+    int l = 0;
+    while (l + 1 < C.nlev && e >= C.boff[l + 1]) ++l;
+    return l;
+}
+__global__ void k_canon_flags(const unsigned* __restrict__ cm, int nb, int* __restrict__ flag) {
+    pdl_enter();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nb) flag[i] = cm[i] != 0u;
+}
+__global__ void k_canon_list(const unsigned* __restrict__ cm, int nb, const int* __restrict__ rank,
+                             int* __restrict__ ids, int* __restrict__ total) {
+    pdl_enter();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb) return;
+    if (cm[i]) ids[rank[i]] = i;
+    if (i == nb - 1) *total = rank[i] + (cm[i] != 0u);
+}
+__global__ void k_canon_rows(CanonInv C) {
+    pdl_enter();
+    const long tot = (long)min(*C.total, C.cap) * 40;
+    for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
+        const int g = int(idx / 40), t = int(idx % 40), e = C.ids[g], l = canon_level(C, e);
+        C.rr[idx] = block_row_range(C.L[l], C.FL[l], C.E[l], e - C.boff[l], t);
+    }
+}
+// one CTA per canonical block; the grid is the buffer capacity (>= the block
+// count of the previous step), CTAs past the current count exit
+__global__ void k_canon_inverse(CanonInv C, int* err) {
+    pdl_enter();
+    extern __shared__ double M[];
+    const int g = blockIdx.x;
+    if (g >= min(*C.total, C.cap)) return;
+    const int e = C.ids[g], l = canon_level(C, e);
+    box_inverse(C.L[l], C.E[l], C.rr + (size_t)g * 40, e - C.boff[l], C.Ainv + (size_t)g * 3136, err, M);
+}
+struct APerm {
+    int nlev;
+    int boff[kBSLevels];  // level-major offset of each listed level
+    const int* blk_ids[kBSLevels];
+    double* Ainv[kBSLevels];
+    int start[kBSLevels + 1];
+};
+// Ainv[level][q] = canonical inverse of list position q's block (256 threads
+// per inverse, 16-byte copies).
+__global__ void k_ainv_permute(APerm P, const int* __restrict__ rank, const double* __restrict__ Ac) {
+    pdl_enter();
+    for (int qg = blockIdx.x; qg < P.start[P.nlev]; qg += gridDim.x) {
+        int k = 0;
+        while (qg >= P.start[k + 1]) ++k;
+        const int q = qg - P.start[k];
+        const int g = rank[P.boff[k] + P.blk_ids[k][q]];
+        const double2* src = reinterpret_cast<const double2*>(Ac + (size_t)g * 3136);
+        double2* dst = reinterpret_cast<double2*>(P.Ainv[k] + (size_t)q * 3136);
+        for (int i = threadIdx.x; i < 3136 / 2; i += blockDim.x) dst[i] = __ldcs(src + i);
+    }
 }
 
 // Slab packing: row pointers + padded entry counts (cnt, level-major), the
