@@ -573,11 +573,12 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // exactly the colour-ordered Gauss-Seidel schedule while blocks that do not
 // depend on each other run ahead.  The cooperative launch makes all CTAs
 // co-resident, and dependencies only point to smaller colours, so the waits
-// cannot deadlock.  Only the E' rows of the CTA's next block are
-// double-buffered in shared memory (2 x 31 KB -> 3 CTAs/SM); the 25 KB inverse
-// streams straight into registers at the start of each block.
+// cannot deadlock.  The E' rows of a block go through one 31 KB shared-memory
+// slot, refilled with the next block's rows once they are consumed (4 CTAs/SM,
+// register-limited); the 25 KB inverse streams straight into registers at the
+// start of each block.
 constexpr int kBigThreads = 128;
-constexpr size_t kBigSmem = 2 * sizeof(ESlot);
+constexpr size_t kBigSmem = sizeof(ESlot);
 __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigColours BC, BigDeps DP,
                                                             const double* __restrict__ b, double* w, Mirror M) {
     pdl_enter();
@@ -606,24 +607,30 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
     while (c < BC.ncol) {
         int nc, nq;
         next_item(c, q, nc, nq);
-        if (nc < BC.ncol) eslot_issue(slot[(k + 1) & 1], SL, nq, t, kBigThreads);
-        cp_async_commit();
         // wait for the predecessors of block q (one thread per predecessor);
         // poff == nullptr: one colour per launch (slab mode), nothing to wait for
         if (DP.poff)
             for (int e = DP.poff[q] + t; e < DP.poff[q + 1]; e += kBigThreads)
                 while (ld_acquire(DP.flags + DP.pred[e]) != DP.epoch) __nanosleep(8);
-        cp_async_wait<1>();
+        cp_async_wait<0>();
         __syncthreads();
-        const ESlot& sl = slot[k & 1];
+        const ESlot& sl = slot[0];
         const int Bk = sl.rp[47];
+        // one E'-row slot: refilled with the next block's rows as soon as this
+        // block's rows are consumed (overlapping the matvec, the write-back,
+        // the publish and the next dependency wait); one slot keeps 4 CTAs
+        // per SM resident instead of 3
         big_block_es(L, sl, SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W, FlatCG{w}, B,
                      [&](int f, int i, int j, double old, double d) {
                          const size_t off = (size_t)f * L.nn + i + (size_t)j * L.n;
                          __stcg(w + off, old + d);
                          M.store(off, j, L.n, old + d);
                      },
-                     S, t, [] { __syncthreads(); });
+                     S, t, [] { __syncthreads(); },
+                     [&] {
+                         if (nc < BC.ncol) eslot_issue(slot[0], SL, nq, t, kBigThreads);
+                         cp_async_commit();
+                     });
         __syncthreads();
         if (t == 0 && DP.flags) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(DP.flags + q, DP.epoch);
