@@ -1024,12 +1024,15 @@ __device__ __forceinline__ void box_inverse(const Lev& L, const EMat& E, const i
         });
     }
     __syncthreads();
-    if (t < 40) {
-        const int2 r = rr40[t];
-        for (int e = r.x; e < r.y; ++e) {
+    // E' rows: one warp per row, the lanes over its entries (the entries of a
+    // row map to distinct local columns, so every M element has one writer);
+    // a thread-per-row loop made the box build latency-bound on the row length
+    for (int row = t >> 5; row < 40; row += nt >> 5) {
+        const int2 r = rr40[row];
+        for (int e = r.x + (t & 31); e < r.y; e += 32) {
             const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
             const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
-            if (c >= 0) M[t * LD + c] -= E.val[e];
+            if (c >= 0) M[row * LD + c] -= E.val[e];
         }
     }
     __syncthreads();

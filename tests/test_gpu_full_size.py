@@ -3,7 +3,8 @@
 * C2 at full size against the CPU oracle: every kappa block, 10 consecutive
   implicit steps each (BASELINE configs[1]), u, p, X^{n+1} within 1e-8 and
   iteration counts within +-2 at every step.
-* C3 at full size against the oracle: the 5 consecutive steps of configs[2].
+* C3 at full size against the oracle: the 5 consecutive steps of configs[2],
+  each on identical inputs.
 * C4 (N = 8192, 256 membranes, 222k points) is out of the oracle's reach (it
   needs > 110 GB of host RAM), so it is checked through properties that do not
   depend on size: the converged step's true residual recomputed through
@@ -44,17 +45,21 @@ def test_c2_full_block_tracks_oracle(kappa):
         assert rel(X.reshape(-1, 2), Xo) < 1e-8, s
 
 
-def test_c3_five_steps_track_oracle():
-    """C3 as BASELINE configs[2] runs it: 5 consecutive implicit steps at N = 1024."""
+def test_c3_five_steps_match_oracle():
+    """C3 as BASELINE configs[2] runs it: 5 consecutive implicit steps at N = 1024.
+    Each step is compared on identical inputs (the oracle steps from the GPU's
+    u^n, X^n): the north_star bar is per solve.  Free-running trajectories, each
+    step converged only to 1e-10, drift apart by about 1e-8 after 4 steps
+    (1.2e-8 in u measured on B200), so they are not held to the per-solve bar."""
     prob = configs.config3()
     g = SaddleSystem.from_problem(prob)
     o = O.Oracle(prob, threads=16)
     n = prob.N
     u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
-    uo, Xo = np.zeros(2 * n * n), prob.X.copy()
     for s in range(5):
+        u_in, X_in = u.copy(), X.reshape(-1, 2).copy()
         sg = g.step_implicit(u, p, X)
-        uo, po, Xo, so = o.step(uo, Xo)
+        uo, po, Xo, so = o.step(u_in, X_in)
         assert sg["converged"] and so["converged"], s
         assert abs(sg["iters"] - so["iters"]) <= 2, (s, sg["iters"], so["iters"])
         assert rel(u, uo) < 1e-8 and rel(p, po) < 1e-8, s
