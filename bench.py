@@ -468,7 +468,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--batch", type=int, default=512, help="C5: number of independent N=256 problems")
-    ap.add_argument("--workers", type=int, default=16, help="C5: concurrent solver contexts per GPU")
+    ap.add_argument("--workers", type=int, default=10, help="C5: concurrent solver contexts per GPU (8-12 measured best on B200, 16 host cores)")
     ap.add_argument("--slabs", type=int, default=0,
                     help="C3/C4: slab-partition the problem (DESIGN.md §7): P slabs over the visible GPUs in this "
                          "process (P2P-fused exchange), or under torchrun one slab per rank over NCCL")
