@@ -370,8 +370,9 @@ def run_batch(args, rank, world):
     W = min(args.workers, len(mine))
     ctxs = [SaddleSystem(256, 1.0, 1.0, 1e-3, device=dev) for _ in range(W)]
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    glim = args.ctx_grid if args.ctx_grid > 0 else max(8, (2 * sms) // W)
     for c in ctxs:  # share the SMs among the concurrent contexts
-        c.set_grid_limit(max(8, (2 * sms) // W))
+        c.set_grid_limit(glim)
     n2 = 256 * 256
 
     def work(w, host, out):
@@ -468,6 +469,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--batch", type=int, default=512, help="C5: number of independent N=256 problems")
+    ap.add_argument("--ctx-grid", type=int, default=0, help="C5: CTA cap per context (0: 2 x SMs / workers)")
     ap.add_argument("--workers", type=int, default=10, help="C5: concurrent solver contexts per GPU (8-12 measured best on B200, 16 host cores)")
     ap.add_argument("--slabs", type=int, default=0,
                     help="C3/C4: slab-partition the problem (DESIGN.md §7): P slabs over the visible GPUs in this "
