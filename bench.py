@@ -1,27 +1,35 @@
 #!/usr/bin/env python
 """bench.py — implicit IB step solve time on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], "C2"): periodic unit square, MAC grid
-N=256, fp64, rho = mu = 1, dt = 1e-3; one ellipse centred (0.5, 0.5), semi-axes
-0.3 / 0.15, Nb = 512 equal-arclength points, zero-rest-length springs with
-kappa in {1e2, 1e4, 1e6}; 10 consecutive backward-Euler steps per kappa from
-u = 0, each solved by FGMRES(30) preconditioned by one V(1,1) cycle (multicolour
-Vanka + big boxes, coarsening to 4x4) to relative residual 1e-10.
+Workload (default "C3": BASELINE.json configs[2], the largest configuration
+quoted single-GPU): periodic unit square, MAC grid N=1024, fp64, rho = mu = 1,
+dt = 1e-3; 16 circular membranes (seed 0, r ~ U[0.03, 0.06], spacing h/2,
+kappa 10^U[3, 6]); 5 consecutive backward-Euler steps from u = 0, each solved
+by FGMRES(30) preconditioned by one V(1,1) cycle (multicolour Vanka + big
+boxes, coarsening to 4x4) to relative residual 1e-10.  --config C2 runs
+configs[1] (N=256, kappa {1e2, 1e4, 1e6} x 10 steps), C4 the N=8192 problem
+on one GPU, C5 the batch of 512 N=256 problems.
 
-A bench "step" is one implicit step of that 30-step sequence (step s uses kappa
-index (s // 10) % 3; the state resets at the start of each kappa block).
+A bench "step" is one implicit step.  The configured steps of every block
+(C2: one block per kappa) are visited round-robin, each block advancing its
+own trajectory and restarting from u = 0, X^0 after its last configured step,
+so any --steps >= (blocks x steps per block) times every configured step
+(C3: --steps 5 covers the whole 5-step trajectory; the driver's 20 cover it
+four times).
   value  : device time per implicit step (ms), CUDA events on the solver's
            stream, inputs resident in HBM, L2 flushed (256 MiB write) between
            steps, max over ranks.
   e2e    : the same steps through the C ABI with HOST buffers (pinned; H2D of
            u^n, X^n and D2H of u, p, X inside the timed region), wall clock.
   roofline: live per-kernel CUDA-event timing (ibmg_profile) of the dominant
-           kernel in a separate profiled pass of the first step of each kappa.
+           kernel over one profiled pass of every configured step.
   cpu_baseline: the CPU oracle (oracle/, kind "port": the reference ships no
-           solver) on all host threads, 2 steps per kappa.
---impl reference runs that oracle port on the same sequence (rank 0 only).
-Multi-GPU (torchrun): C2 does not shard; every rank runs an independent replica
-("replicas only"); scaling "weak".
+           solver) on all host threads, a bounded sample.
+  secondary.C4: the N=8192 problem on this GPU (1 timed step): ms/step, the
+           V-cycle roofline fraction and the dominant kernel's.
+--impl reference runs that oracle port on the same schedule (rank 0 only).
+Multi-GPU (torchrun): C2/C3 do not shard; every rank runs an independent
+replica ("replicas only"); scaling "weak".
 """
 from __future__ import annotations
 
@@ -68,20 +76,27 @@ THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_p
 
 
 def workload_config():
+    """The `config` object of both arms (identical dicts: no arm-specific text)."""
     probs, per, desc = WL["blocks"], WL["per"], WL["desc"]
     N = probs[0].N
     return {
         "workload": desc, "name": WL["name"], "N": N, "Nb": [p.npts for p in probs],
         "kappas": [p.kappa if len(p.kappa) > 1 else p.kappa[0] for p in probs], "steps_per_block": per,
         "dt": probs[0].dt, "dof": 3 * N * N,
+        "step_order": "blocks round-robin, each block's trajectory restarted after its last configured step",
         "l2": "flushed between timed steps (256 MiB write)",
     }
 
 
+DATA = "synthetic (seeded BASELINE.json geometry, u0 = 0)"
+
+
 def step_schedule(total):
-    """(block index, reset?) for steps 0..total-1 of the repeating workload sequence."""
+    """(block, step index in block) for bench steps 0..total-1: blocks are
+    visited round-robin (C2: kappa 1e2, 1e4, 1e6, 1e2, ...), each advancing
+    its own trajectory; index 0 restarts it from u = 0, X^0."""
     per, nblocks = WL["per"], len(WL["blocks"])
-    return [((s // per) % nblocks, s % per == 0) for s in range(total)]
+    return [(s % nblocks, (s // nblocks) % per) for s in range(total)]
 
 
 class ClockSampler:
@@ -205,6 +220,57 @@ def kernel_algorithmic_bytes(name, ctxinfo, vcycles, fgmres_iters, restarts):
     return None
 
 
+def profile_pass(ctxs, states_reset, sched):
+    """Live per-kernel CUDA-event timing (ibmg_profile) over the steps of
+    `sched`; returns ({kernel: [ms, launches]}, per-step iterations, restarts)."""
+    prof_tot, step_iters, prs = {}, [], 0
+    for c in ctxs:
+        c.profile(True)
+    for kb, si in sched:
+        u, p, X = states_reset(kb, si)
+        st = ctxs[kb].step_implicit(u, p, X)
+        step_iters.append(st["iters"])
+        prs += st["restarts"]
+    for c in ctxs:
+        for k, (tms, cnt) in c.profile_report().items():
+            a = prof_tot.setdefault(k, [0.0, 0])
+            a[0] += tms
+            a[1] += cnt
+        c.profile(False)
+    return prof_tot, step_iters, prs
+
+
+def roofline_of(prof_tot, ctxs, N_GRID, step_iters, restarts, wl_name):
+    """The dominant kernel with a byte model: achieved GB/s on algorithmic bytes."""
+    pv = sum(step_iters)
+    step_prof_ms = sum(v[0] for v in prof_tot.values())
+    ranked = sorted(prof_tot.items(), key=lambda kv: -kv[1][0])
+    c0 = ctxs[0]
+    lv_info = []
+    for l in range(c0.num_levels):
+        nl = c0.level_n(l)
+        if nl >= 32:
+            lv_info.append((nl, float(np.mean([int(c.big_blocks(l).sum()) for c in ctxs]))))
+    info = {"N": N_GRID, "levels": lv_info, "step_iters": step_iters}
+    peak, peak_kind = measured_peak_hbm()
+    roof = None
+    for name, (tms, cnt) in ranked:
+        byts = kernel_algorithmic_bytes(name, info, pv, pv, restarts)
+        if byts is None:
+            continue
+        avg_s = tms / cnt * 1e-3
+        ach = byts / cnt / avg_s / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": measured_traffic(wl_name, name),
+                "traffic_unit": "B/launch (ncu, profiles/traffic.json)", "peak_source": peak_kind,
+                "bytes_per_launch": byts / cnt, "avg_launch_us": round(avg_s * 1e6, 3),
+                "share_of_step": round(tms / step_prof_ms, 4), "launches": cnt}
+        break
+    shares = {k: {"ms": round(v[0], 4), "launches": v[1], "share": round(v[0] / step_prof_ms, 4)}
+              for k, v in ranked[:14]}
+    return roof, shares
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_1311_5614_b200.ibmg import SaddleSystem
@@ -216,28 +282,32 @@ def run_ours(args, rank, world):
     ctxs = [SaddleSystem.from_problem(p, device=dev) for p in probs]
     n2 = N_GRID * N_GRID
     NBs = [p.npts for p in probs]
-    X0 = [torch.tensor(p.X.reshape(-1), dtype=torch.float64, device=f"cuda:{dev}") for p in probs]
-    u = torch.zeros(2 * n2, dtype=torch.float64, device=f"cuda:{dev}")
-    p = torch.zeros(n2, dtype=torch.float64, device=f"cuda:{dev}")
-    X = torch.empty(max(x.numel() for x in X0), dtype=torch.float64, device=f"cuda:{dev}")
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
-    streams = [torch.cuda.ExternalStream(c.stream, device=f"cuda:{dev}") for c in ctxs]
+    D = f"cuda:{dev}"
+    X0 = [torch.tensor(p.X.reshape(-1), dtype=torch.float64, device=D) for p in probs]
+    # one trajectory state per block (C2: per kappa), advanced round-robin
+    U = [torch.zeros(2 * n2, dtype=torch.float64, device=D) for _ in probs]
+    P = [torch.zeros(n2, dtype=torch.float64, device=D) for _ in probs]
+    Xs = [x.clone() for x in X0]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=D)
+    streams = [torch.cuda.ExternalStream(c.stream, device=D) for c in ctxs]
+
+    def state(kb, si):
+        if si == 0:  # restart this block's trajectory
+            U[kb].zero_()
+            P[kb].zero_()
+            Xs[kb].copy_(X0[kb])
+        return U[kb], P[kb], Xs[kb]
 
     def run(total, timed):
-        nonlocal X
         ms, iters, setup, restarts, conv = [], [], [], [], True
-        for kb, reset in step_schedule(total):
-            Xk = X[: X0[kb].numel()]
-            if reset:
-                u.zero_()
-                p.zero_()
-                Xk.copy_(X0[kb])
+        for kb, si in step_schedule(total):
+            u, p, X = state(kb, si)
             flush.zero_()
             torch.cuda.synchronize()
             if timed:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(streams[kb])
-            st = ctxs[kb].step_implicit(u, p, Xk)
+            st = ctxs[kb].step_implicit(u, p, X)
             if timed:
                 e1.record(streams[kb])
                 e1.synchronize()
@@ -259,87 +329,38 @@ def run_ours(args, rank, world):
     launches = sum(c.kernel_launches for c in ctxs) - launches0
     if world > 1:
         torch.distributed.barrier()
-    from paper_1311_5614_b200 import dist as D
-    tmax, tsum, _ = D.reduce_stats([float(sum(ms)), float(sum(iters))], device=f"cuda:{dev}")
+    from paper_1311_5614_b200 import dist as Dd
+    tmax, tsum, _ = Dd.reduce_stats([float(sum(ms)), float(sum(iters))], device=D)
     total_ms_max, vcyc_all = float(tmax[0]), float(tsum[1])
 
     # e2e: same steps through the C ABI with host buffers in pinned memory
     # (numpy views of page-locked torch tensors; the H2D / D2H copies run inside)
-    e2e_ms = []
-
     def pinned(n):
         return torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
 
-    uh = pinned(2 * n2)
-    ph = pinned(n2)
-    Xbuf = pinned(max(int(p_.X.size) for p_ in probs))
-    Xh = None
-    for kb, reset in step_schedule(args.steps):
-        if reset:
-            uh[:] = 0.0
-            ph[:] = 0.0
-            Xh = Xbuf[: probs[kb].X.size]
-            Xh[:] = probs[kb].X.reshape(-1)
+    Uh = [pinned(2 * n2) for _ in probs]
+    Ph = [pinned(n2) for _ in probs]
+    Xh = [pinned(int(p_.X.size)) for p_ in probs]
+    e2e_ms = []
+    for kb, si in step_schedule(args.steps):
+        if si == 0:
+            Uh[kb][:] = 0.0
+            Ph[kb][:] = 0.0
+            Xh[kb][:] = probs[kb].X.reshape(-1)
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctxs[kb].step_implicit(uh, ph, Xh)
+        ctxs[kb].step_implicit(Uh[kb], Ph[kb], Xh[kb])
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     h2d = 8 * (2 * n2 + 2 * int(np.mean(NBs)))
     d2h = 8 * (2 * n2 + n2 + 2 * int(np.mean(NBs)))
 
     result = None
     if rank == 0:
-        # profiled pass (live CUDA-event timing per kernel): first step of each kappa
-        prof_tot = {}
-        pv, pit, prs, step_iters = 0, 0, 0, []
-        for kb in range(len(probs)):
-            u.zero_()
-            p.zero_()
-            Xk = X[: X0[kb].numel()]
-            Xk.copy_(X0[kb])
-            ctxs[kb].profile(True)
-            st = ctxs[kb].step_implicit(u, p, Xk)
-            rep = ctxs[kb].profile_report()
-            ctxs[kb].profile(False)
-            for k, (tms, cnt) in rep.items():
-                a = prof_tot.setdefault(k, [0.0, 0])
-                a[0] += tms
-                a[1] += cnt
-            pv += st["iters"]
-            pit += st["iters"]
-            step_iters.append(st["iters"])
-            prs += st["restarts"]
-        step_prof_ms = sum(v[0] for v in prof_tot.values())
-        ranked = sorted(prof_tot.items(), key=lambda kv: -kv[1][0])
-        levels = []
-        c0 = ctxs[0]
-        for l in range(c0.num_levels):
-            nl = c0.level_n(l)
-            if nl >= 32:
-                levels.append((nl, None))
-        # big-block counts per level per kappa context (averaged)
-        lv_info = []
-        for l, (nl, _) in enumerate(levels):
-            nbig = np.mean([int(c.big_blocks(l).sum()) for c in ctxs])
-            lv_info.append((nl, nbig))
-        info = {"N": N_GRID, "levels": lv_info, "step_iters": step_iters}
-        peak, peak_kind = measured_peak_hbm()
-        roof = None
-        for name, (tms, cnt) in ranked:
-            byts = kernel_algorithmic_bytes(name, info, pv, pit, prs)
-            if byts is None:
-                continue
-            avg_s = tms / cnt * 1e-3
-            ach = byts / cnt / avg_s / 1e9
-            roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 4), "traffic": measured_traffic(WL["name"], name),
-                    "traffic_unit": "B/launch (ncu, profiles/traffic.json)", "peak_source": peak_kind,
-                    "bytes_per_launch": byts / cnt, "avg_launch_us": round(avg_s * 1e6, 3),
-                    "share_of_step": round(tms / step_prof_ms, 4), "launches": cnt}
-            break
-        kernel_shares = {k: {"ms": round(v[0], 4), "launches": v[1], "share": round(v[0] / step_prof_ms, 4)}
-                         for k, v in ranked[:12]}
+        # profiled pass (live CUDA-event timing per kernel) over every configured step
+        sched = [(kb, si) for si in range(WL["per"]) for kb in range(len(probs))]
+        prof_tot, step_iters, prs = profile_pass(ctxs, state, sched)
+        roof, kernel_shares = roofline_of(prof_tot, ctxs, N_GRID, step_iters, prs, WL["name"])
         result = {
             "total_ms_max": total_ms_max, "vcyc_all": vcyc_all, "ms": ms, "iters": iters, "setup": setup,
             "launches": launches, "clocks": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h,
@@ -348,6 +369,62 @@ def run_ours(args, rank, world):
     for c in ctxs:
         c.close()
     return result
+
+
+def run_secondary_c4(dev, steps=1, warmup=1):
+    """The N=8192 configuration (BASELINE configs[3]) on this one GPU: device
+    time per implicit step (CUDA events, inputs in HBM), its DOF.V-cycles/s
+    roofline fraction and the dominant kernel's roofline from a profiled step."""
+    import torch
+    from paper_1311_5614_b200 import configs
+    from paper_1311_5614_b200.ibmg import SaddleSystem
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < 130 * 2**30:
+        return {"skipped": f"needs ~130 GiB free device memory, {free / 2**30:.0f} GiB free"}
+    prob = configs.config4()
+    D = f"cuda:{dev}"
+    ctx = SaddleSystem.from_problem(prob, device=dev)
+    n2 = prob.N ** 2
+    u = torch.zeros(2 * n2, dtype=torch.float64, device=D)
+    p = torch.zeros(n2, dtype=torch.float64, device=D)
+    X0 = torch.tensor(prob.X.reshape(-1), dtype=torch.float64, device=D)
+    X = X0.clone()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=D)
+
+    def one():
+        u.zero_()
+        X.copy_(X0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = ctx.step_implicit(u, p, X)
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), st
+
+    for _ in range(warmup):
+        one()
+    ms, its = [], []
+    for _ in range(steps):
+        t, st = one()
+        ms.append(t)
+        its.append(st["iters"])
+    v = float(np.mean(ms))
+    peak, _ = measured_peak_hbm()
+    dofv = 3 * n2 * float(np.mean(its)) / (v * 1e-3)
+
+    def reset(kb, si):
+        u.zero_()
+        X.copy_(X0)
+        return u, p, X
+
+    prof_tot, step_iters, prs = profile_pass([ctx], reset, [(0, 0)])
+    roof, shares = roofline_of(prof_tot, [ctx], prob.N, step_iters, prs, "C4")
+    ctx.close()
+    return {"config": "C4: periodic N=8192 fp64, 256 membranes (seed 1), dt=1e-4, one implicit step, 1 GPU",
+            "ms_per_step": round(v, 3), "steps": steps, "warmup": warmup, "vcycles_per_step": float(np.mean(its)),
+            "dof_vcycles_per_s": dofv, "vcycle_roofline_frac": round(dofv * 112 / (peak * 1e9), 4),
+            "roofline": roof, "kernels": {k: v_ for k, v_ in list(shares.items())[:8]}}
 
 
 def run_batch(args, rank, world):
@@ -412,8 +489,8 @@ def run_batch(args, rank, world):
         wall = (time.perf_counter() - t0) * 1e3
         return max(e0.elapsed_time(e1), wall), [r for o in outs for r in o]
 
-    # warm-up: one problem per worker
-    saved = args.batch
+    # warm-up: one pass over this rank's whole shard (every worker context
+    # grows its buffers to its problems' sizes), untimed
     run(False)
     launches0 = sum(c.kernel_launches for c in ctxs)
     with ClockSampler(dev) as clk:
@@ -425,35 +502,37 @@ def run_batch(args, rank, world):
     ms, e2e_ms, nprob, vcyc, conv = float(tmax[0]), float(tmax[1]), float(tsum[2]), float(tsum[3]), bool(tmin[4])
     for c in ctxs:
         c.close()
-    args.batch = saved
     return {"ms": ms, "e2e_ms": e2e_ms, "nprob": nprob, "vcyc": vcyc, "conv": conv, "launches": launches,
-            "clocks": clk.summary(), "workers": W}
+            "clocks": clk.summary(), "workers": W, "warmup_problems": len(mine)}
 
 
 def cpu_oracle_steps(steps_sched, threads):
+    """The oracle on a schedule of (block, step index in block), one trajectory
+    state per block (as the GPU arm)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     probs = WL["blocks"]
     N_GRID = probs[0].N
     ctxs = [O.Oracle(pr, threads=threads) for pr in probs]
     ms, iters = [], []
-    u = X = None
-    for kb, reset in steps_sched:
-        if reset or u is None:
-            u = np.zeros(2 * N_GRID * N_GRID)
-            X = probs[kb].X.copy()
+    st_u = [None] * len(probs)
+    st_X = [None] * len(probs)
+    for kb, si in steps_sched:
+        if si == 0 or st_u[kb] is None:
+            st_u[kb] = np.zeros(2 * N_GRID * N_GRID)
+            st_X[kb] = probs[kb].X.copy()
         t0 = time.perf_counter()
-        u, p, X, st = ctxs[kb].step(u, X)
+        st_u[kb], p, st_X[kb], st = ctxs[kb].step(st_u[kb], st_X[kb])
         ms.append((time.perf_counter() - t0) * 1e3)
         iters.append(st["iters"])
     return ms, iters
 
 
 def cpu_baseline(threads):
-    sched = []
-    per = 2 if WL["name"] == "C2" else 1
-    for kb in range(len(WL["blocks"])):
-        sched += [(kb, True)] + [(kb, False)] * (per - 1)
+    """Bounded sample (10-30 s of CPU work): C2 the first 2 steps of each kappa,
+    C3 the first configured step, C1 all."""
+    per = {"C2": 2, "C3": 1}.get(WL["name"], 1)
+    sched = [(kb, si) for kb in range(len(WL["blocks"])) for si in range(per)]
     ms, iters = cpu_oracle_steps(sched, threads)
     return {"value": round(float(np.mean(ms)), 3), "unit": "ms", "cores": threads, "kind": "port",
             "sample": f"first {per} implicit {WL['name']} step(s) of each block ({len(sched)} steps, {sum(iters)} "
@@ -463,11 +542,12 @@ def cpu_baseline(threads):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C4 one-GPU secondary measurement")
     ap.add_argument("--batch", type=int, default=512, help="C5: number of independent N=256 problems")
     ap.add_argument("--ctx-grid", type=int, default=0, help="C5: CTA cap per context (0: 2 x SMs / workers)")
     ap.add_argument("--workers", type=int, default=10, help="C5: concurrent solver contexts per GPU (8-12 measured best on B200, 16 host cores)")
@@ -492,12 +572,15 @@ def main():
         v = float(np.mean(ms))
         line = {"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 geometry)", "impl": "reference",
-                "config": dict(workload_config(), parallelism="CPU oracle port, OpenMP over independent boxes"),
+                "vs_baseline": None, "dtype": "f64", "data": DATA, "impl": "reference",
+                "config": workload_config(),
+                "parallelism": f"CPU oracle port, OpenMP over independent boxes ({threads} threads)",
                 "dof_vcycles_per_s": 3 * WL["blocks"][0].N ** 2 * sum(iters) / (sum(ms) * 1e-3),
+                "vcycles_per_step": round(sum(iters) / len(iters), 2),
                 "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "port",
-                                 "sample": f"{args.steps} C2 implicit steps ({sum(iters)} V-cycles) on the CPU oracle "
-                                           "(the reference ships no solver; SURVEY.md §0)"},
+                                 "sample": f"{args.steps} {WL['name']} implicit steps ({sum(iters)} V-cycles) on the "
+                                           "CPU oracle, same step schedule as the GPU arm (the reference ships no "
+                                           "solver; SURVEY.md §0)"},
                 "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -513,13 +596,13 @@ def main():
     if rank == 0:
         ms_step = res["total_ms_max"] / args.steps
         dofv = 3 * N_GRID ** 2 * res["vcyc_all"] / (res["total_ms_max"] * 1e-3)
-        line_extra = {}
         peak, _ = measured_peak_hbm()
         line = {
             "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 geometry, u0 = 0)",
-            "config": dict(workload_config(), parallelism=f"replicas x{world} ({args.config} runs one problem per GPU)"),
+            "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": workload_config(),
+            "parallelism": f"replicas x{world} ({args.config} runs one problem per GPU)",
             "dof_vcycles_per_s": dofv,
             "dof_vcycles_roofline_frac": dofv * 112 / (peak * 1e9 * world),
             "vcycles_per_step": round(res["vcyc_all"] / world / args.steps, 2),
@@ -532,6 +615,11 @@ def main():
             "roofline": res["roofline"],
             "kernels": res["kernels"],
         }
+        if world == 1 and not args.no_secondary and args.config != "C4":
+            try:
+                line["secondary"] = {"C4": run_secondary_c4(int(os.environ.get("LOCAL_RANK", "0")))}
+            except Exception as e:  # reported, never fatal for the headline
+                line["secondary"] = {"C4": {"error": str(e)[:200]}}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
@@ -650,7 +738,7 @@ def main_batch(args):
     if rank == 0:
         ms_per = r["ms"] / r["nprob"]
         line = {"metric": METRIC, "value": round(ms_per, 4), "unit": "ms", "n_gpus": world,
-                "steps": int(r["nprob"]), "warmup": r["workers"], "ms_per_step": round(ms_per, 4),
+                "steps": int(r["nprob"]), "warmup": r["warmup_problems"], "ms_per_step": round(ms_per, 4),
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded C5 geometry)", "config": cfg,
                 "problems_per_s": r["nprob"] / (r["ms"] * 1e-3),

@@ -147,6 +147,13 @@ int ibmg_profile(ibmg_ctx* ctx, int enable);
 int ibmg_profile_report(ibmg_ctx* ctx, char* buf, int cap);
 /* The context's CUDA stream (cudaStream_t), for callers timing with events. */
 void* ibmg_stream(const ibmg_ctx* ctx);
+/* Stream ordering of device-pointer inputs: every call given IBMG_PTR_DEVICE
+ * arrays first makes the context's stream wait on an event recorded on this
+ * caller stream (cudaStream_t; NULL = the legacy default stream, the default),
+ * so inputs still being produced there are read only after their producers.
+ * Outputs are complete when a call returns (the context stream is
+ * synchronised), so no ordering is needed on the way out. */
+int ibmg_set_input_stream(ibmg_ctx* ctx, void* stream);
 
 /* ---- Slab partition of one problem (BASELINE north_star: large
  * fine grids slab-partitioned across 2/4/8 GPUs with NVLink halo exchange per

@@ -119,6 +119,7 @@ Csr spgemm(const Csr& A, const Csr& B) {
 struct DenseLu {
     int m = 0;
     std::vector<double> a;  // row-major m x m, factors in place
+    std::vector<double> a0; // (plain-cell cache) the matrix before factoring
     std::vector<int> piv;
     bool factor() {
         piv.resize(m);
@@ -376,6 +377,11 @@ struct Level {
     std::vector<char> big;              // per 4x4 block
     std::vector<Pass> passes;
     std::vector<DenseLu> blk;               // factors per block (big only)
+    // plain-cell 5x5 factors, cached per level per step: the
+    // level's common matrix (constant-coefficient stencil) factored once; a
+    // plain cell whose extracted matrix differs in any bit keeps its own
+    DenseLu plain_lu;
+    std::map<int, DenseLu> plain_own;
     DenseLu coarse;                         // coarsest bordered LU
     std::vector<double> w, b, r;
 };
@@ -711,13 +717,43 @@ void build(Ctx& C) {
         mark_big(L, npts);
         build_schedule(L, kprev, knext);
         L.blk.assign(L.big.size(), DenseLu{});
-        int d[56];
-        for (size_t bkk = 0; bkk < L.big.size(); ++bkk) {
+        // independent per block / per cell: OpenMP (each factor is the same
+        // sequential arithmetic whichever thread runs it)
+        int bad = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(| : bad)
+        for (long bkk = 0; bkk < long(L.big.size()); ++bkk) {
             if (!L.big[bkk]) continue;
+            int d[56];
             const int m = box_dofs(L, true, int(bkk), d);
             extract(L.A, d, m, L.blk[bkk]);
-            if (!L.blk[bkk].factor()) throw std::runtime_error("big-box local matrix singular");
+            if (!L.blk[bkk].factor()) bad |= 1;
         }
+        if (bad) throw std::runtime_error("big-box local matrix singular");
+        L.plain_own.clear();
+        L.plain_lu = DenseLu{};
+        std::vector<int> plain;
+        for (const Pass& ps : L.passes)
+            if (!ps.big) plain.insert(plain.end(), ps.items.begin(), ps.items.end());
+        if (!plain.empty()) {
+            int d[56];
+            const int m = box_dofs(L, false, plain[0], d);
+            extract(L.A, d, m, L.plain_lu);
+            L.plain_lu.a0 = L.plain_lu.a;
+            if (!L.plain_lu.factor()) throw std::runtime_error("plain-cell local matrix singular");
+        }
+#pragma omp parallel for schedule(static) reduction(| : bad)
+        for (long t = 1; t < long(plain.size()); ++t) {
+            int d[56];
+            const int m = box_dofs(L, false, plain[t], d);
+            DenseLu lu;
+            extract(L.A, d, m, lu);
+            if (std::memcmp(lu.a.data(), L.plain_lu.a0.data(), sizeof(double) * 25) != 0) {
+                if (!lu.factor()) bad |= 1;
+#pragma omp critical(plain_own)
+                L.plain_own.emplace(plain[t], std::move(lu));
+            }
+        }
+        if (bad) throw std::runtime_error("plain-cell local matrix singular");
     }
 }
 
@@ -746,11 +782,9 @@ void sweep(const Level& L, const double* b, double* w) {
             for (int a = 0; a < m; ++a) rr[a] = b[d[a]] - L.A.row_dot(d[a], w);
             if (ps.big) {
                 L.blk[item].solve(rr);
-            } else {
-                DenseLu lu;
-                extract(L.A, d, m, lu);
-                lu.factor();
-                lu.solve(rr);
+            } else {  // the cached factors (identical arithmetic to factoring here)
+                auto it = L.plain_own.find(item);
+                (it == L.plain_own.end() ? L.plain_lu : it->second).solve(rr);
             }
             for (int a = 0; a < m; ++a) w[d[a]] += rr[a];
         }

@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
 
 // ---- two-pass (lagged) CGS2 orthogonalisation of FGMRES ----
 // At Arnoldi step j the basis slot V_j holds q, orthogonalised once against
-// V_0..V_{j-1} and normalised; w = A M q.  Pass 1 (k_ortho_dots) reads
+// V_0..V_{j-1} (unnormalised: the previous update pass writes w1 there); w = A M q.  Pass 1 (k_ortho_dots) reads
 // V_0..V_j and w once: b_i = V_i.w, a_i = V_i.q (i < j), gamma = q.w,
 // delta = q.q; its last CTA forms nu = sqrt(delta - |a|^2) (q's norm after
 // the second orthogonalisation), h = (gamma - a.b) / nu (= v_j.w),
@@ -791,12 +791,18 @@ __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
         na = warp_sum(na);
         ab = warp_sum(ab);
         if (lane == 0) {
-            const double nu = sqrt(aqd[k - 1] - na), h = (bw[k - 1] - ab) / nu;
-            dh[5 * ld] = 1.0 / nu;
-            dh[5 * ld + 1] = h / nu;
+            // |q - V a|^2 = delta - |a|^2, clamped: near a Krylov breakdown the
+            // difference can round below zero.  nu <= 1e-14 |q| is a breakdown
+            // (q in span V): nu = 0 is published (v_j = 0, w projected on
+            // V_{<j} only) and fgmres2 ends the cycle at the previous column.
+            const double delta = aqd[k - 1], nu2 = fmax(delta - na, 0.0);
+            const bool brk = !(nu2 > 1e-28 * delta);
+            const double nu = brk ? 0.0 : sqrt(nu2), h = brk ? 0.0 : (bw[k - 1] - ab) / nu;
+            dh[5 * ld] = brk ? 0.0 : 1.0 / nu;
+            dh[5 * ld + 1] = brk ? 0.0 : h / nu;
             dh[5 * ld + 2] = nu;
             dh[5 * ld + 3] = h;
-            s_coef = h / nu;  // s for the coefficients below
+            s_coef = brk ? 0.0 : h / nu;  // s for the coefficients below
         }
     }
     __syncthreads();

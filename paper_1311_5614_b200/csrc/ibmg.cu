@@ -156,6 +156,12 @@ struct ibmg_ctx {
     int* hpin_i = nullptr;  // pinned int scratch (row counts)
     bool err_pending = false;  // hpin_i[4] holds a rebuild's error flags, not yet checked
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // setup timing of ibmg_step
+    // caller stream that produces device-pointer inputs (ibmg_set_input_stream;
+    // default: the legacy default stream).  Every call taking device pointers
+    // makes c->s wait on an event recorded there, so a producer still running
+    // on the caller's stream is ordered before the context reads its inputs.
+    cudaStream_t in_stream = nullptr;
+    cudaEvent_t ev_in = nullptr;
     size_t sort_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -355,7 +361,7 @@ void alloc_levels(ibmg_ctx* c) {
             lb.bq = dalloc<int>(size_t(n / 4) * (n / 4));
             if (n >= 4 * kTile) {
                 lb.tflags = dalloc<unsigned>(size_t(n / kTile) * (n / kTile));
-                CK(cudaMemset(lb.tflags, 0, sizeof(unsigned) * (n / kTile) * (n / kTile)));
+                CK(cudaMemsetAsync(lb.tflags, 0, sizeof(unsigned) * (n / kTile) * (n / kTile), c->s));
             }
             if (n > kDataflowMaxN) {
                 const std::vector<int> seg = plain_df_order(n / kTile, c->pdf_grid_max, c->pdf_skew);
@@ -610,11 +616,12 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
         lb.pred = dalloc<int>(size_t(lb.pred_cap));
         lb.poff = dalloc<int>(size_t(lb.poff_cap));
         lb.flags = dalloc<unsigned>(size_t(lb.poff_cap));
-        CK(cudaMemset(lb.flags, 0, sizeof(unsigned) * lb.poff_cap));
+        // stream-ordered (c->s): the next sweep on c->s must see zeroed epochs
+        CK(cudaMemsetAsync(lb.flags, 0, sizeof(unsigned) * lb.poff_cap, c->s));
         // the dataflow sweep's tile flags share this epoch: restart them too
         // (a stale tile epoch equal to a new sweep's would read as published)
         if (lb.tflags && lb.L.n <= kDataflowMaxN)
-            CK(cudaMemset(lb.tflags, 0, sizeof(unsigned) * (lb.L.n / kTile) * (lb.L.n / kTile)));
+            CK(cudaMemsetAsync(lb.tflags, 0, sizeof(unsigned) * (lb.L.n / kTile) * (lb.L.n / kTile), c->s));
         lb.epoch = 0;
     }
     lb.h_ids = std::move(ids);
@@ -1115,7 +1122,7 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
         c->keys2 = dalloc<int>(scap);
         c->vals2 = dalloc<int>(scap);
         c->cnt = dalloc<int>(scap + 1);
-        CK(cudaMemset(c->cnt, 0, sizeof(int) * (scap + 1)));
+        CK(cudaMemsetAsync(c->cnt, 0, sizeof(int) * (scap + 1), c->s));
         c->sort_cap = scap;
     }
     c->P.n = tot;
@@ -1513,6 +1520,11 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
                 g[0] = beta;
             }
             const double nu = hp[SC + 2], h = hp[SC + 3], bnext = std::sqrt(hp[SC + 4]);
+            if (j > 0 && !(nu > 0.0)) {  // breakdown: q_j in span V_{<j}, the space is invariant
+                for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j - 1] += hp[ld + i];
+                Hx[size_t(j) * m + j - 1] = 0.0;
+                break;  // least squares over columns 0..j-1 (kdim = j), then the true residual
+            }
             // exact column j-1: q_j = w1 = sum a_i V_i + nu v_j
             if (j == 0) {
                 nu0 = nu;
@@ -1690,9 +1702,17 @@ void build_rhs(ibmg_ctx* c, const double* u, double* b) {
 }
 
 // ---------------- host/device staging for the C ABI ----------------
+// Order the caller's device-pointer inputs before this context's stream.
+void wait_inputs(ibmg_ctx* c, int kind) {
+    if (kind != IBMG_PTR_DEVICE) return;
+    CK(cudaEventRecord(c->ev_in, c->in_stream));
+    CK(cudaStreamWaitEvent(c->s, c->ev_in, 0));
+}
+
 struct Stage {
     ibmg_ctx* c;
     int kind;
+    Stage(ibmg_ctx* c_, int kind_) : c(c_), kind(kind_) { wait_inputs(c, kind); }
     const double* in(const double* p, size_t n, double* buf) {
         if (kind == IBMG_PTR_DEVICE) return p;
         CK(cudaMemcpyAsync(buf, p, n * sizeof(double), cudaMemcpyHostToDevice, c->s));
@@ -1767,6 +1787,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
         CK(cudaEventCreateWithFlags(&c->ev_sizes, cudaEventDisableTiming));
         CK(cudaEventCreate(&c->ev_t0));
         CK(cudaEventCreate(&c->ev_t1));
+        CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
         CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * gj_ld(49) * 8));
         CK(cudaFuncSetAttribute(k_big_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
@@ -1861,6 +1882,7 @@ void ibmg_destroy(ibmg_ctx* c) {
     if (c->ev_sizes) cudaEventDestroy(c->ev_sizes);
     if (c->ev_t0) cudaEventDestroy(c->ev_t0);
     if (c->ev_t1) cudaEventDestroy(c->ev_t1);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
     delete c;
 }
 
@@ -1907,10 +1929,18 @@ int ibmg_profile_report(ibmg_ctx* c, char* buf, int cap) {
 }
 void* ibmg_stream(const ibmg_ctx* c) { return c ? (void*)c->s : nullptr; }
 
+int ibmg_set_input_stream(ibmg_ctx* c, void* stream) {
+    return api(c, [&]() -> int {
+        c->in_stream = static_cast<cudaStream_t>(stream);
+        return IBMG_OK;
+    });
+}
+
 int ibmg_set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, const double* ds,
                         const double* X, int ptr_kind) {
     return api(c, [&]() -> int {
         if (n_mem > 0 && (!nb || !kappa || !ds || !X)) throw InvalidArg("null structure arrays");
+        wait_inputs(c, ptr_kind);
         set_structures(c, n_mem, nb, kappa, ds, X, ptr_kind);
         return IBMG_OK;
     });
@@ -2224,6 +2254,7 @@ int ibmg_solve(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st, int ptr_
     if (!st) st = &local;
     return api(c, [&]() -> int {
         const double t0 = now_ms();
+        wait_inputs(c, ptr_kind);
         const double* db = ptr_kind == IBMG_PTR_DEVICE ? b : nullptr;
         if (!db) {
             CK(cudaMemcpyAsync(c->bv, b, sizeof(double) * c->M, cudaMemcpyHostToDevice, c->s));
@@ -2246,6 +2277,7 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
     return api(c, [&]() -> int {
         if (!c->have_structs) throw InvalidArg("ibmg_step: call ibmg_set_structures first");
         const double t0 = now_ms();
+        wait_inputs(c, ptr_kind);
         const size_t nn = size_t(c->prm.N) * c->prm.N;
         // X^n in, lagged operators rebuilt at X^n
         if (c->npts)

@@ -50,7 +50,7 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_group_last_error", "ibmg_group_distributed_levels", "ibmg_group_kernel_launches",
            "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
            "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl",
-           "ibmg_vcycle_spectrum", "ibmg_set_scheme"]
+           "ibmg_vcycle_spectrum", "ibmg_set_scheme", "ibmg_set_input_stream"]
 
 
 def lib_path() -> str:
@@ -93,6 +93,7 @@ def lib(build_if_missing: bool = True):
     L.ibmg_kernel_launches.argtypes = [vp]
     L.ibmg_stream.restype = C.c_void_p
     L.ibmg_stream.argtypes = [vp]
+    L.ibmg_set_input_stream.argtypes = [vp, vp]
     L.ibmg_debug_sweep_trace.restype = C.c_long
     L.ibmg_debug_sweep_trace.argtypes = [vp, ip, vp, vp, vp, C.c_long]
     L.ibmg_elasticity_triplets.restype = C.c_long
@@ -163,6 +164,7 @@ class SaddleSystem:
         if rc != 0 or not h.value:
             raise RuntimeError(f"ibmg_create failed (status {rc}); is a CUDA device available?")
         self._h = h
+        self._in_stream = 0
         self.N, self.rho, self.mu, self.dt = N, rho, mu, dt
         self.npts = 0
 
@@ -173,6 +175,19 @@ class SaddleSystem:
 
     def __del__(self):
         self.close()
+
+    def _p(self, a):
+        """(pointer, kind) of `a`; for a CUDA tensor the context is first told the
+        caller's current torch stream (ibmg_set_input_stream), so its inputs are
+        read after their producers on that stream."""
+        ptr, kind = _ptr(a)
+        if kind == IBMG_PTR_DEVICE:
+            import torch
+            sp = torch.cuda.current_stream(a.device).cuda_stream
+            if sp != self._in_stream:
+                self._chk(self._L.ibmg_set_input_stream(self._h, C.c_void_p(sp)))
+                self._in_stream = sp
+        return ptr, kind
 
     def _chk(self, rc, ok=(0,)):
         if rc in ok:
@@ -189,7 +204,7 @@ class SaddleSystem:
         ds = np.ascontiguousarray(ds, np.float64)
         if isinstance(X, np.ndarray):
             X = np.ascontiguousarray(X, np.float64).reshape(-1)
-        xp, kind = _ptr(X)
+        xp, kind = self._p(X)
         self._chk(self._L.ibmg_set_structures(self._h, len(nb), nb.ctypes.data, kappa.ctypes.data,
                                               ds.ctypes.data, xp, kind))
         self.npts = int(nb.sum())
@@ -223,43 +238,43 @@ class SaddleSystem:
 
     def apply(self, w, out=None, level=0):
         out = _empty_like(w, self._size(level)) if out is None else out
-        (wp, k), (op, _) = _ptr(w), _ptr(out)
+        (wp, k), (op, _) = self._p(w), self._p(out)
         self._chk(self._L.ibmg_apply(self._h, level, wp, op, k))
         return out
 
     def residual(self, b, w, level=0):
         r = _empty_like(w, self._size(level))
         nrm = C.c_double()
-        (bp, k), (wp, _), (rp, _) = _ptr(b), _ptr(w), _ptr(r)
+        (bp, k), (wp, _), (rp, _) = self._p(b), self._p(w), self._p(r)
         self._chk(self._L.ibmg_residual(self._h, level, bp, wp, rp, C.byref(nrm), k))
         return r, nrm.value
 
     def sweep(self, b, w, level=0):
         """One multicolour box sweep, in place on w (returns w)."""
-        (bp, k), (wp, _) = _ptr(b), _ptr(w)
+        (bp, k), (wp, _) = self._p(b), self._p(w)
         self._chk(self._L.ibmg_sweep(self._h, level, bp, wp, k))
         return w
 
     def v_cycle(self, b):
         z = _empty_like(b, self._size(0))
-        (bp, k), (zp, _) = _ptr(b), _ptr(z)
+        (bp, k), (zp, _) = self._p(b), self._p(z)
         self._chk(self._L.ibmg_vcycle(self._h, bp, zp, k))
         return z
 
     def coarsest_solve(self, b):
         x = _empty_like(b, self._size(self.num_levels - 1))
-        (bp, k), (xp, _) = _ptr(b), _ptr(x)
+        (bp, k), (xp, _) = self._p(b), self._p(x)
         self._chk(self._L.ibmg_coarse_solve(self._h, bp, xp, k))
         return x
 
     def restrict_saddle(self, rf, level=0):
         rc = _empty_like(rf, self._size(level + 1))
-        (fp, k), (cp, _) = _ptr(rf), _ptr(rc)
+        (fp, k), (cp, _) = self._p(rf), self._p(rc)
         self._chk(self._L.ibmg_restrict(self._h, level, fp, cp, k))
         return rc
 
     def prolong_saddle_add(self, ec, wf, level=0):
-        (ep, k), (wp, _) = _ptr(ec), _ptr(wf)
+        (ep, k), (wp, _) = self._p(ec), self._p(wf)
         self._chk(self._L.ibmg_prolong_add(self._h, level, ep, wp, k))
         return wf
 
@@ -285,19 +300,19 @@ class SaddleSystem:
 
     def build_rhs(self, u_n):
         b = _empty_like(u_n, 3 * self.N * self.N)
-        (up, k), (bp, _) = _ptr(u_n), _ptr(b)
+        (up, k), (bp, _) = self._p(u_n), self._p(b)
         self._chk(self._L.ibmg_build_rhs(self._h, up, bp, k))
         return b
 
     def interpolate(self, u):
         U = _empty_like(u, 2 * self.npts)
-        (up, k), (Up, _) = _ptr(u), _ptr(U)
+        (up, k), (Up, _) = self._p(u), self._p(U)
         self._chk(self._L.ibmg_interpolate(self._h, up, Up, k))
         return U
 
     def spread(self, F):
         f = _empty_like(F, 2 * self.N * self.N)
-        (Fp, k), (fp, _) = _ptr(F), _ptr(f)
+        (Fp, k), (fp, _) = self._p(F), self._p(f)
         self._chk(self._L.ibmg_spread(self._h, Fp, fp, k))
         return f
 
@@ -305,7 +320,7 @@ class SaddleSystem:
         """FGMRES(restart) with one V-cycle right preconditioner; returns (x, stats)."""
         x = _empty_like(b, self._size(0)) if x is None else x
         st = Stats()
-        (bp, k), (xp, _) = _ptr(b), _ptr(x)
+        (bp, k), (xp, _) = self._p(b), self._p(x)
         self._chk(self._L.ibmg_solve(self._h, bp, xp, C.byref(st), k), ok=(0, 2))
         return x, st.as_dict()
 
@@ -325,7 +340,7 @@ class SaddleSystem:
 
     def _step(self, u, p, X):
         st = Stats()
-        (up, k), (pp, _), (Xp, _) = _ptr(u), _ptr(p), _ptr(X)
+        (up, k), (pp, _), (Xp, _) = self._p(u), self._p(p), self._p(X)
         self._chk(self._L.ibmg_step(self._h, up, pp, Xp, C.byref(st), k), ok=(0, 2))
         return st.as_dict()
 

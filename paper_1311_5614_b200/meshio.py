@@ -26,13 +26,20 @@ def write_fiber_mesh(f, X, ds, periodic=True):
         f.write(f"{k} 0 {_g(x)} {_g(y)}\n")
 
 
-def read_fiber_mesh(f):
-    """Next mesh block of a stream: (X (m1 * m2, 2), ds, periodic, m1, m2), or None at EOF."""
+class _Stop(Exception):
+    pass
+
+
+def read_fiber_mesh(f, stop=None):
+    """Next mesh block of a stream: (X (m1 * m2, 2), ds, periodic, m1, m2), or None at EOF
+    (or at a line equal to `stop`, which is consumed)."""
     head = ""
     while not head.strip():
         head = f.readline()
         if head == "":
             return None
+    if stop is not None and head.strip() == stop:
+        raise _Stop
     parts = head.split()
     if len(parts) != 4:
         raise RuntimeError("read_fiber_mesh: bad header")
@@ -57,10 +64,15 @@ def write_structures(f, nb, ds, X):
         o += m
 
 
-def read_structures(f):
+def read_structures(f, stop=None):
+    """Mesh blocks until EOF (or until a `stop` line, consumed; then
+    f.stopped is not set but the caller knows the section that follows)."""
     nb, ds, Xs = [], [], []
     while True:
-        blk = read_fiber_mesh(f)
+        try:
+            blk = read_fiber_mesh(f, stop)
+        except _Stop:
+            break
         if blk is None:
             break
         X, d, _, m1, m2 = blk
@@ -90,14 +102,36 @@ def read_field(f):
     return x.reshape(-1), N
 
 
-def save_checkpoint(path, u, p, X, nb, ds, N):
+def save_checkpoint(path, u, p, X, nb, ds, N, kappa=None, rho=None, mu=None, dt=None):
+    """Field, then the membranes in the reference write_fiber_mesh format (byte-
+    identical blocks), then a trailing 'params' section with what a restart
+    needs beyond the meshes: the solver parameters rho, mu, dt and one kappa
+    per membrane ('nan' where not given).  The reference format has no such
+    section; read_fiber_mesh stops at it (not a mesh header)."""
+    nmem = len(nb)
+    kap = [float("nan")] * nmem if kappa is None else [float(k) for k in np.asarray(kappa).reshape(-1)]
+    if len(kap) != nmem:
+        raise ValueError("one kappa per membrane")
     with open(path, "w") as f:
         write_field(f, np.concatenate([np.asarray(u).reshape(-1), np.asarray(p).reshape(-1)]), N)
         write_structures(f, nb, ds, X)
+        f.write("params\n")
+        f.write(" ".join(_g(float("nan") if v is None else float(v)) for v in (rho, mu, dt)) + "\n")
+        f.write(f"{nmem}\n")
+        for k in kap:
+            f.write(_g(k) + "\n")
 
 
-def load_checkpoint(path):
+def load_checkpoint(path, with_params=False):
+    """(u, p, X, nb, ds, N), plus {'kappa', 'rho', 'mu', 'dt'} when with_params."""
     with open(path) as f:
         x, N = read_field(f)
-        nb, ds, X = read_structures(f)
-    return x[: 2 * N * N].copy(), x[2 * N * N:].copy(), X, nb, ds, N
+        nb, ds, X = read_structures(f, stop="params")
+        prm = {"kappa": None, "rho": None, "mu": None, "dt": None}
+        rest = f.readline()
+        if rest.strip():  # the params section follows (its header line was consumed)
+            rho, mu, dt = (float(t) for t in rest.split())
+            nmem = int(f.readline())
+            prm = {"kappa": np.array([float(f.readline()) for _ in range(nmem)]), "rho": rho, "mu": mu, "dt": dt}
+    out = (x[: 2 * N * N].copy(), x[2 * N * N:].copy(), X, nb, ds, N)
+    return out + (prm,) if with_params else out

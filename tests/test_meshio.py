@@ -48,6 +48,26 @@ def test_checkpoint_round_trip(tmp_path):
     assert np.array_equal(u2, u) and np.array_equal(p2, p) and np.array_equal(X2, prob.X.reshape(-1, 2))
 
 
+def test_checkpoint_restores_run_parameters(tmp_path):
+    """kappa per membrane and rho, mu, dt survive the round trip (a trailing
+    'params' section after the reference-format mesh blocks)."""
+    prob = configs.config3()
+    N = 16
+    u, p = np.zeros(2 * N * N), np.zeros(N * N)
+    path = tmp_path / "ck.txt"
+    meshio.save_checkpoint(path, u, p, prob.X, prob.nb, prob.ds, N, kappa=prob.kappa, rho=prob.rho, mu=prob.mu,
+                           dt=prob.dt)
+    *_, nb2, ds2, N2, prm = meshio.load_checkpoint(path, with_params=True)
+    assert nb2 == list(prob.nb) and ds2 == list(prob.ds)
+    assert np.array_equal(prm["kappa"], np.asarray(prob.kappa, np.float64).reshape(-1))
+    assert (prm["rho"], prm["mu"], prm["dt"]) == (prob.rho, prob.mu, prob.dt)
+    # the mesh blocks stay byte-identical to the reference writer's
+    text = open(path).read()
+    f = io.StringIO()
+    meshio.write_structures(f, prob.nb, prob.ds, prob.X)
+    assert f.getvalue() in text
+
+
 def test_cpp_facade_round_trips_reference_file(tmp_path):
     """include/ibmg/b200.hpp's reader + writer reproduce the reference's file."""
     import shutil
