@@ -1,4 +1,5 @@
-"""Task timeline of one dataflow sweep (debug): where the critical path goes."""
+"""Task timeline of one dataflow sweep per level (debug): where the critical path goes.
+usage: python tools/trace_sweep.py [C2|C3]"""
 import ctypes as C
 import os
 import sys
@@ -10,13 +11,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1311_5614_b200 import configs  # noqa: E402
 from paper_1311_5614_b200.ibmg import SaddleSystem  # noqa: E402
 
-prob = configs.config2(1e4)
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+prob = configs.config3() if cfg == "C3" else configs.config2(1e4)
 g = SaddleSystem.from_problem(prob)
 L = g._L
-b = torch.tensor(g.build_rhs(np.zeros(2 * 256 * 256)), device="cuda")
+N = prob.N
+b = torch.tensor(g.build_rhs(np.zeros(2 * N * N)), device="cuda")
 w = torch.zeros_like(b)
-for level in (0, 1, 2):
+for level in range(g.num_levels):
     n = g.level_n(level)
+    if n > 512 or n < 64:
+        continue
     nb = 3 * n * n
     bl, wl = b[:nb].clone(), w[:nb].clone()
     words = L.ibmg_debug_sweep_trace(g._h, level, bl.data_ptr(), wl.data_ptr(), None, 0)
