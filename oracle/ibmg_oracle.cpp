@@ -850,7 +850,9 @@ int fgmres(Ctx& C, const double* bptr, double* xptr, orc_stats* st, double* hist
     const size_t M = L.b.size();
     const int m = C.prm.restart;
     std::vector<double> b(bptr, bptr + M), x(M, 0.0), r(M), w(M);
-    std::vector<std::vector<double>> V(m + 1, std::vector<double>(M)), Z(m, std::vector<double>(M));
+    // basis vectors allocated on first use: a solve that converges in k steps
+    // touches k + 1 V and k Z vectors (C4: 35 of 61 x 1.6 GB)
+    std::vector<std::vector<double>> V(m + 1), Z(m);
     std::vector<double> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), h1(m + 1);
     const double bnorm = std::sqrt(dotv(b, b));
     int it = 0, restarts = 0, hn = 0;
@@ -867,11 +869,13 @@ int fgmres(Ctx& C, const double* bptr, double* xptr, orc_stats* st, double* hist
     double beta = bnorm;
     const double tol = C.prm.rtol * bnorm;
     while (true) {
+        V[0].resize(M);
         for (size_t q = 0; q < M; ++q) V[0][q] = r[q] / beta;
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = beta;
         int j = 0, kdim = 0;
         for (; j < m; ++j) {
+            Z[j].resize(M);
             vcycle(C, V[j].data(), Z[j].data(), false);
             apply_level(L, Z[j].data(), w.data());
             for (int pass = 0; pass < 2; ++pass) {
@@ -901,6 +905,7 @@ int fgmres(Ctx& C, const double* bptr, double* xptr, orc_stats* st, double* hist
             kdim = j + 1;
             if (hist && hn < hist_len) hist[hn++] = std::fabs(g[j + 1]) / bnorm;
             if (std::fabs(g[j + 1]) <= tol || it >= C.prm.max_iters || hnext == 0.0) break;
+            V[j + 1].resize(M);
             for (size_t q = 0; q < M; ++q) V[j + 1][q] = w[q] / hnext;
         }
         for (int i = kdim - 1; i >= 0; --i) {

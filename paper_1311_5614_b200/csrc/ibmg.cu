@@ -23,6 +23,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "../../include/ibmg_gpu.h"
+#include "cluster_kernel.cuh"
 #include "coarse_kernel.cuh"
 #include "common.cuh"
 #include "grid_kernels.cuh"
@@ -69,6 +70,7 @@ inline long grow_cap(long need, long cap) { return std::max<long>(need + need / 
 
 constexpr int kMaxColours = 32;
 constexpr int kDataflowMaxN = 512;  // levels swept by the single dataflow kernel
+static_assert(kMaxColours == kClMaxColours, "cluster kernel colour table");
 
 struct LevelBuf {
     Lev L{};
@@ -112,6 +114,13 @@ struct LevelBuf {
     size_t h_up_cap = 0;
     std::vector<int> h_pos;                  // block -> list position scratch (colouring)
     unsigned* h_cm = nullptr;                // pinned mirror of cmask
+    // cluster kernel (P-levels): big-block list positions per owner rank in
+    // colour order, and their colour offsets per rank (cluster_lists)
+    int* cl_q = nullptr;
+    int* cl_off = nullptr;
+    int cl_cap = 0;
+    int* h_cl = nullptr;  // pinned staging of their upload
+    int h_cl_cap = 0;
 };
 
 }  // namespace
@@ -123,6 +132,12 @@ struct ibmg_ctx {
     cudaStream_t s2 = nullptr;                       // setup side stream (coarsest inverse)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sizes = nullptr;
     int nlev = 0, lc = 0;  // levels [lc, nlev) run in the single-CTA coarse kernel
+    // levels [lt, nlev) run in the 16-CTA cluster kernel (k_cluster_cycle,
+    // n <= 128) when cl_ok; IBMG_CLUSTER=0 keeps the dataflow sweeps + coarse kernel
+    int lt = 0;
+    bool cl_ok = false;
+    int cl_smem = 0, cl_uoff = 0;
+    std::vector<int> cl_woff, cl_boff;
     std::vector<LevelBuf> lev;
     long long launches = 0;
     // structures
@@ -647,6 +662,8 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
                        c->s));
 }
 
+void cluster_lists(ibmg_ctx* c);
+
 void check_err_flag(ibmg_ctx* c, const char* where) {
     int h = 0;
     CK(cudaMemcpyAsync(&h, c->err_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s));
@@ -898,6 +915,7 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             }
             for (auto& j : jobs) j.get();
         }
+        cluster_lists(c);
         tr.mark("coloured");
         // big-block E' row ranges, slabs and inverses of every level: one
         // launch each over the level-major block numbering
@@ -1293,6 +1311,166 @@ void coarse_cycle(ibmg_ctx* c, const double* b, double* w, double* w_fine = null
     LAUNCH(c, k_coarse_cycle, 1, kCoarseThreads, coarse_smem(c), A);
 }
 
+// ---- cluster kernel (cluster_kernel.cuh): levels [lt, nlev) in one 16-CTA cluster
+// Shared-memory layout per CTA: for each cluster level its w and b (P-level:
+// the 3 (n/4)^2 region; Q-level: the whole 3 n^2 level), then the union region.
+void setup_cluster(ibmg_ctx* c) {
+    c->cl_ok = false;
+    if (const char* e = std::getenv("IBMG_CLUSTER"))
+        if (std::atoi(e) == 0) return;
+    int lt = 0;
+    while (lt < c->nlev && c->lev[lt].L.n > kClMaxN) ++lt;
+    const int nl = c->nlev - lt;
+    if (nl < 1 || nl > kClMaxLev) return;
+    c->lt = lt;
+    c->cl_woff.assign(c->nlev, 0);
+    c->cl_boff.assign(c->nlev, 0);
+    int off = 0;
+    for (int l = lt; l < c->nlev; ++l) {
+        const int n = c->lev[l].L.n;
+        const int m = n >= 4 * kTile ? 3 * (n / kClCX) * (n / kClCY) : 3 * n * n;
+        c->cl_woff[l] = off;
+        off += m;
+        c->cl_boff[l] = off;
+        off += m;
+    }
+    off = (off + 1) & ~1;  // 16-byte aligned union region (cp.async E' slots)
+    c->cl_uoff = off;
+    off += kClUnionD;
+    c->cl_smem = off * int(sizeof(double));
+    if (c->cl_smem + int(sizeof(BigScratch)) * kClGroups > 227 * 1024) return;
+    CK(cudaFuncSetAttribute(k_cluster_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, c->cl_smem));
+    CK(cudaFuncSetAttribute(k_cluster_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kCl);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = size_t(c->cl_smem);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_cluster_cycle, &cfg) != cudaSuccess || ncl < 1) {
+        (void)cudaGetLastError();
+        return;
+    }
+    c->cl_ok = true;
+}
+
+// Per P-level (n >= 64) of the cluster kernel: the big-block list positions of
+// each owner rank (the CTA whose region holds the block) in colour order, and
+// the per-rank colour offsets; uploaded from pinned staging (async).
+void cluster_lists(ibmg_ctx* c) {
+    if (!c->cl_ok) return;
+    for (int l = c->lt; l + 1 < c->nlev; ++l) {
+        LevelBuf& lb = c->lev[l];
+        const int n = lb.L.n;
+        if (n < 4 * kTile || lb.nbig == 0) continue;
+        const int nbk = n / 4, Rx = n / kClCX, Ry = n / kClCY, nc = lb.ncol, nbig = lb.nbig;
+        const int need = nbig + kCl * (nc + 1);
+        if (lb.cl_cap < need) {
+            dfree(lb.cl_q);
+            lb.cl_cap = int(grow_cap(need, lb.cl_cap));
+            lb.cl_q = dalloc<int>(size_t(lb.cl_cap));
+        }
+        if (lb.h_cl_cap < need) {
+            if (lb.h_cl) CK(cudaFreeHost(lb.h_cl));
+            lb.h_cl_cap = int(grow_cap(need, lb.h_cl_cap));
+            CK(cudaMallocHost(&lb.h_cl, sizeof(int) * size_t(lb.h_cl_cap)));
+        }
+        int* hq = lb.h_cl;
+        int* ho = lb.h_cl + nbig;
+        std::vector<int> own(nbig);
+        std::fill(ho, ho + kCl * (nc + 1), 0);
+        for (int col = 0; col < nc; ++col)
+            for (int q = lb.coff[col]; q < lb.coff[col + 1]; ++q) {
+                const int B = lb.h_ids[q];
+                own[q] = (4 * (B % nbk)) / Rx + kClCX * ((4 * (B / nbk)) / Ry);
+                ++ho[own[q] * (nc + 1) + col + 1];
+            }
+        int run = 0;  // exclusive offsets, rank-major then colour
+        for (int r = 0; r < kCl; ++r) {
+            ho[r * (nc + 1)] = run;
+            for (int col = 0; col < nc; ++col) {
+                run += ho[r * (nc + 1) + col + 1];
+                ho[r * (nc + 1) + col + 1] = run;
+            }
+        }
+        std::vector<int> fill(kCl * (nc + 1));
+        for (int r = 0; r < kCl; ++r)
+            for (int col = 0; col < nc; ++col) fill[r * (nc + 1) + col] = ho[r * (nc + 1) + col];
+        for (int col = 0; col < nc; ++col)
+            for (int q = lb.coff[col]; q < lb.coff[col + 1]; ++q) hq[fill[own[q] * (nc + 1) + col]++] = q;
+        CK(cudaMemcpyAsync(lb.cl_q, hq, sizeof(int) * size_t(need), cudaMemcpyHostToDevice, c->s));
+        lb.cl_off = lb.cl_q + nbig;
+    }
+}
+
+ClArgs cluster_args(ibmg_ctx* c, const double* b_in, double* w_out, double* w_fine) {
+    ClArgs A{};
+    A.nl = c->nlev - c->lt;
+    A.nu1 = c->prm.nu1;
+    A.nu2 = c->prm.nu2;
+    for (int l = c->lt; l < c->nlev; ++l) {
+        LevelBuf& lb = c->lev[l];
+        ClLev& C = A.lv[l - c->lt];
+        C.L = lb.L;
+        C.FL = lb.FL;
+        C.E = lb.E;
+        C.SL = slabs(lb);
+        C.big = lb.big;
+        C.nbig = l + 1 < c->nlev ? lb.nbig : 0;
+        C.ncol = l + 1 < c->nlev ? lb.ncol : 0;
+        std::copy(lb.coff, lb.coff + kMaxColours + 1, C.coff);
+        const int n = lb.L.n;
+        C.part = n >= 4 * kTile;
+        C.Rx = C.part ? n / kClCX : n;
+        C.Ry = C.part ? n / kClCY : n;
+        C.lgRx = C.part ? lb.L.lg - 2 : lb.L.lg;
+        C.lgRy = C.part ? lb.L.lg - 2 : lb.L.lg;
+        C.own_q = lb.cl_q;
+        C.own_off = lb.cl_off;
+        C.w_off = c->cl_woff[l];
+        C.b_off = c->cl_boff[l];
+    }
+    A.Acoarse = c->Acoarse;
+    A.b_in = b_in;
+    A.w_out = w_out;
+    A.w_fine = w_fine;
+    A.u_off = c->cl_uoff;
+    return A;
+}
+
+void cluster_cycle(ibmg_ctx* c, const double* b, double* w, double* w_fine) {
+    ClArgs A = cluster_args(c, b, w, w_fine);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kCl);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = size_t(c->cl_smem);
+    cfg.stream = c->s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = kCl;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+    if (c->pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    if (c->prof) prof_begin(c, "k_cluster_cycle");
+    CK(cudaLaunchKernelEx(&cfg, k_cluster_cycle, A));
+    if (c->prof) prof_end(c);
+    ++c->launches;
+}
+
 void pressure_mean_zero(ibmg_ctx* c, double* x) {
     const size_t nn = size_t(c->prm.N) * c->prm.N;
     dim3 g(kRedBlocks, 1);
@@ -1345,7 +1523,29 @@ void residual_restrict(ibmg_ctx* c, int l, const double* b, const double* w, dou
 // launched (vcycle_head, speculatively, by FGMRES).
 void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z_zeroed = false,
             bool first_sweep_done = false) {
-    if (c->lc == 0) {
+    if (c->cl_ok && c->lt == 0) {
+        // the whole V-cycle in the cluster kernel (it reads all of b before it
+        // writes z, so b == z is safe)
+        cluster_cycle(c, b, z, nullptr);
+    } else if (c->cl_ok) {
+        const bool alias = b == z;
+        if (alias) CK(cudaMemcpyAsync(c->lev[0].b, b, sizeof(double) * c->M, cudaMemcpyDeviceToDevice, c->s));
+        auto bl = [&](int l) -> const double* { return l == 0 && !alias ? b : c->lev[l].b; };
+        auto wl = [&](int l) -> double* { return l == 0 ? z : c->lev[l].w; };
+        if (!z_zeroed) CK(cudaMemsetAsync(z, 0, sizeof(double) * c->M, c->s));
+        for (int l = 0; l < c->lt; ++l) {
+            LevelBuf& nx = c->lev[l + 1];
+            for (int s = (l == 0 && first_sweep_done) ? 1 : 0; s < c->prm.nu1; ++s) sweep_level(c, l, bl(l), wl(l));
+            residual_restrict(c, l, bl(l), wl(l), wl(l + 1), 0, nx.L.n, false);
+        }
+        // levels lt.. in one cluster launch, which also prolongs into level lt-1
+        cluster_cycle(c, c->lev[c->lt].b, wl(c->lt), wl(c->lt - 1));
+        for (int l = c->lt - 1; l >= 0; --l) {
+            LevelBuf& lb = c->lev[l];
+            if (l < c->lt - 1) LAUNCH(c, k_prolong_add, nblk(lb.L.nn), 256, 0, lb.L.n, wl(l + 1), wl(l), 0, lb.L.nn);
+            for (int s = 0; s < c->prm.nu2; ++s) sweep_level(c, l, bl(l), wl(l));
+        }
+    } else if (c->lc == 0) {
         coarse_cycle(c, b, z);
     } else {
         const bool alias = b == z;
@@ -1375,7 +1575,7 @@ void vcycle(ibmg_ctx* c, const double* b, double* z, bool project = true, bool z
 // The head of a V-cycle whose level-0 guess z is already zero: the first
 // pre-smoothing sweep.  Returns whether it launched anything.
 bool vcycle_head(ibmg_ctx* c, const double* b, double* z) {
-    if (c->lc == 0 || c->prm.nu1 == 0 || b == z) return false;
+    if (c->lc == 0 || (c->cl_ok && c->lt == 0) || c->prm.nu1 == 0 || b == z) return false;
     sweep_level(c, 0, b, z);
     return true;
 }
@@ -1809,6 +2009,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
         }
         alloc_levels(c);
         CK(cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem(c))));
+        setup_cluster(c);
         c->npts = 0;
         rebuild(c);
     } catch (const std::exception& e) {
@@ -1840,6 +2041,8 @@ void ibmg_destroy(ibmg_ctx* c) {
         if (lb.h_up) cudaFreeHost(lb.h_up);
         dfree(lb.pdf_seg);
         dfree(lb.escr);
+        dfree(lb.cl_q);
+        if (lb.h_cl) cudaFreeHost(lb.h_cl);
     }
     dfree(c->V);
     dfree(c->Z);

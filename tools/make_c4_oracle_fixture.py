@@ -35,7 +35,7 @@ def main():
     mem = meminfo_gb()
     threads = os.cpu_count() or 1
     print(f"MemTotal {mem:.0f} GiB, {threads} threads", flush=True)
-    if mem < 200:
+    if mem < 150:
         print("not enough host memory for the C4 oracle", flush=True)
         return 2
     prob = configs.config4()
