@@ -106,6 +106,14 @@ long ibmg_elasticity_triplets(ibmg_ctx* ctx, int level, int* rows, int* cols, do
  * per-task globaltimer stamps (device b, w); returns the trace length in words. */
 long ibmg_debug_sweep_trace(ibmg_ctx* ctx, int level, const double* b, double* w, unsigned long long* out, long cap);
 
+/* Debug only: one cluster-kernel launch (device b, w at the first cluster level)
+ * with (globaltimer, tag) stamps of CTA 0 after each cluster barrier; returns the
+ * stamp count. */
+long ibmg_debug_cluster_trace(ibmg_ctx* ctx, const double* b, double* w, unsigned long long* out, long cap);
+/* First level of the 16-CTA cluster kernel (levels n <= 128), or -1 when the
+ * cluster path is off (IBMG_CLUSTER=0 or no cluster launch on the device). */
+int ibmg_cluster_level(const ibmg_ctx* ctx);
+
 /* Debug only: one coarse-cycle launch (device b, w at the first coarse-kernel
  * level) with thread-0 globaltimer phase stamps; returns the stamp count. */
 long ibmg_debug_coarse_trace(ibmg_ctx* ctx, const double* b, double* w, unsigned long long* out, long cap);

@@ -45,8 +45,24 @@ __device__ __forceinline__ unsigned cl_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
-__device__ __forceinline__ void cl_sync() {
+// debug timeline (ibmg_debug_cluster_trace): CTA 0 thread 0 stamps
+// (globaltimer, tag) after each cluster barrier; cl_tr == nullptr in production
+__shared__ unsigned long long* cl_tr;
+__shared__ int cl_nm;
+__shared__ int cl_gen;  // ClArgs.gen (DView)
+__device__ __forceinline__ void cl_mark(int tag) {
+    if (cl_tr && threadIdx.x == 0) {
+        if (cl_nm < 2000) {
+            cl_tr[2 * cl_nm] = gtimer();
+            cl_tr[2 * cl_nm + 1] = (unsigned long long)tag;
+        }
+        ++cl_nm;
+    }
+}
+// tag: level * 10000 + phase * 100 + index (see tools/trace_cluster.py)
+__device__ __forceinline__ void cl_sync(int tag = 0) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (tag) cl_mark(tag);
 }
 // generic address of the same shared-memory location in CTA `rank` of the cluster
 template <class T>
@@ -66,6 +82,7 @@ struct DView {
     int n, nn, lg;
     int part, Rx, Ry, lgRx, lgRy;
     unsigned me;
+    int gen;  // 1: every partitioned access through mapa + a generic load (no local/remote branch)
     __device__ __forceinline__ unsigned owner(int i, int j) const { return (i >> lgRx) + kClCX * (j >> lgRy); }
     __device__ __forceinline__ int loff(int f, int i, int j) const {  // i, j wrapped
         return part ? f * (Rx * Ry) + (i & (Rx - 1)) + (j & (Ry - 1)) * Rx : f * nn + i + j * n;
@@ -74,6 +91,7 @@ struct DView {
         const int k = loff(f, i, j);
         if (!part) return in_smem(loc)[k];
         const unsigned o = owner(i, j);
+        if (gen) return *cl_map(loc + k, o);
         if (o == me) return in_smem(loc)[k];
         return *cl_map(loc + k, o);
     }
@@ -118,6 +136,8 @@ struct ClArgs {
     double* w_out;          // its correction (global)
     double* w_fine;         // optional: w of the next finer level += P w_out
     int u_off;              // union region (doubles): 2 E' slots | tile buffers, residual, E' dots
+    unsigned long long* trace;  // debug timeline (nullptr in production)
+    int gen;                    // DView.gen
 };
 
 // union region layout (doubles)
@@ -130,7 +150,7 @@ constexpr int kClUnionD = (kClGroups * kClSlotD > kClTileD + kClResD + kClEDots)
                                                                                     : kClTileD + kClResD + kClEDots;
 
 __device__ __forceinline__ DView cl_view(const ClLev& C, double* base, int off, unsigned me) {
-    return DView{base + off, C.L.n, C.L.nn, C.L.lg, C.part, C.Rx, C.Ry, C.lgRx, C.lgRy, me};
+    return DView{base + off, C.L.n, C.L.nn, C.L.lg, C.part, C.Rx, C.Ry, C.lgRx, C.lgRy, me, cl_gen};
 }
 
 // ---- plain phase of a P-level: the tile colours in order, one cluster step each
@@ -180,7 +200,7 @@ __device__ void cl_plain_p(const ClLev& C, const DView& W, const DView& B, doubl
                 }
                 __syncthreads();
             }
-        cl_sync();
+        cl_sync(C.L.lg * 10000 + 100 + tc);
     }
 }
 
@@ -254,7 +274,7 @@ __device__ void cl_big(const ClLev& C, const DView& W, const DView& B, double* u
             k = nk;
             q = nq;
         }
-        cl_sync();
+        cl_sync(C.L.lg * 10000 + 300 + colour);
     }
     cp_async_wait<0>();
 }
@@ -265,7 +285,7 @@ __device__ __forceinline__ void cl_sweep(const ClLev& C, double* sm, double* un,
         cl_plain_p(C, W, B, un, me);
     } else {
         cl_plain_q(C, sm + C.w_off, sm + C.b_off);
-        cl_sync();  // every copy's plain phase reads the pre-big-phase values
+        cl_sync(C.L.lg * 10000 + 200);  // every copy's plain phase reads the pre-big-phase values
     }
     cl_big(C, W, B, un, S, me);
 }
@@ -303,7 +323,7 @@ __device__ void cl_restrict(const ClLev& C, const ClLev& D, double* sm, double* 
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) rs[R.loff(f, i, j)] += s;
         }
-        cl_sync();  // every region's residual is complete
+        cl_sync(C.L.lg * 10000 + 400);  // every region's residual is complete
     } else {
         double* ed = in_smem(un + kClTileD + kClResD);
         SW Wl{in_smem(sm + C.w_off), n, nn};
@@ -324,7 +344,7 @@ __device__ void cl_restrict(const ClLev& C, const ClLev& D, double* sm, double* 
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane < kCl) *cl_map(ed + fq, lane) = s;
         }
-        cl_sync();  // every copy holds every row's dot
+        cl_sync(C.L.lg * 10000 + 500);  // every copy holds every row's dot
         for (int fq = t; fq < C.FL.nf; fq += kClThreads) rs[__ldg(C.FL.face + fq)] += ed[fq];
         __syncthreads();
         R.part = 0;
@@ -365,7 +385,7 @@ __device__ void cl_restrict(const ClLev& C, const ClLev& D, double* sm, double* 
     }
     const int wcount = 3 * (D.part ? D.Rx * D.Ry : nnc);
     for (int q = t; q < wcount; q += kClThreads) wc[q] = 0.0;
-    cl_sync();  // the coarse level is complete everywhere
+    cl_sync(C.L.lg * 10000 + 600);  // the coarse level is complete everywhere
 }
 
 // Level C += P (level D's w) on C's cells of this CTA (its region, or all).
@@ -393,7 +413,7 @@ __device__ void cl_prolong(const ClLev& C, const ClLev& D, double* sm, unsigned 
             w[2 * nn + q] += dp;
         }
     }
-    if (C.part) cl_sync();  // the next sweep stages neighbours' regions
+    if (C.part) cl_sync(C.L.lg * 10000 + 700);  // the next sweep stages neighbours' regions
     else __syncthreads();
 }
 
@@ -402,6 +422,13 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_cycle(ClArgs A) {
     extern __shared__ __align__(16) double csm[];
     __shared__ BigScratch S[kClGroups];
     const unsigned me = cl_rank();
+    if (threadIdx.x == 0) {
+        cl_tr = me == 0 ? A.trace : nullptr;
+        cl_nm = 0;
+        cl_gen = A.gen;
+    }
+    __syncthreads();
+    cl_mark(1);
     double* sm = csm;
     double* un = csm + A.u_off;
     const int t = threadIdx.x;
@@ -424,7 +451,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_cycle(ClArgs A) {
                 w[q] = 0.0;
             }
         }
-        cl_sync();
+        cl_sync(800);
     }
     for (int l = 0; l + 1 < A.nl; ++l) {
         for (int s = 0; s < A.nu1; ++s) cl_sweep(A.lv[l], sm, un, S, me);
@@ -441,6 +468,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_cycle(ClArgs A) {
             w[q] = s;
         }
         __syncthreads();
+        cl_mark(1000);
     }
     for (int l = A.nl - 2; l >= 0; --l) {
         cl_prolong(A.lv[l], A.lv[l + 1], sm, me);
@@ -470,7 +498,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_cycle(ClArgs A) {
             A.w_fine[2 * nnf + q] += dp;
         }
     }
-    cl_sync();  // no CTA exits while others may still read its shared memory
+    cl_sync(900);  // no CTA exits while others may still read its shared memory
 }
 
 }  // namespace ibmg

@@ -136,7 +136,7 @@ struct ibmg_ctx {
     // n <= 128) when cl_ok; IBMG_CLUSTER=0 keeps the dataflow sweeps + coarse kernel
     int lt = 0;
     bool cl_ok = false;
-    int cl_smem = 0, cl_uoff = 0;
+    int cl_smem = 0, cl_uoff = 0, cl_gen = 0;  // cl_gen: IBMG_CL_GEN (DView access mode)
     std::vector<int> cl_woff, cl_boff;
     std::vector<LevelBuf> lev;
     long long launches = 0;
@@ -210,6 +210,9 @@ struct ibmg_ctx {
                             // levels), IBMG_CANON_INV=1 on, 0 off
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
+    int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
+    bool spec_full = true;  // FGMRES: whole next V-cycle enqueued behind the dots (IBMG_SPEC=0: first sweep only)
+    bool df_es = true;      // dataflow sweep with the E'-row slot + register inverse, 2 CTAs/SM (IBMG_DF_ES=0: slab slots)
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
     bool plain_df = true;   // n > 512: band-major plain dataflow launch (IBMG_PLAIN_DF=0: 4 tile-colour launches)
     int pdf_skew = 0;       // its band skew in steps (0: from the grid; IBMG_PDF_SKEW)
@@ -378,7 +381,7 @@ void alloc_levels(ibmg_ctx* c) {
                 lb.tflags = dalloc<unsigned>(size_t(n / kTile) * (n / kTile));
                 CK(cudaMemsetAsync(lb.tflags, 0, sizeof(unsigned) * (n / kTile) * (n / kTile), c->s));
             }
-            if (n > kDataflowMaxN) {
+            if (n > c->df_maxn) {
                 const std::vector<int> seg = plain_df_order(n / kTile, c->pdf_grid_max, c->pdf_skew);
                 lb.pdf_seg = dalloc<int>(seg.size());
                 CK(cudaMemcpy(lb.pdf_seg, seg.data(), sizeof(int) * seg.size(), cudaMemcpyHostToDevice));
@@ -635,7 +638,7 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
         CK(cudaMemsetAsync(lb.flags, 0, sizeof(unsigned) * lb.poff_cap, c->s));
         // the dataflow sweep's tile flags share this epoch: restart them too
         // (a stale tile epoch equal to a new sweep's would read as published)
-        if (lb.tflags && lb.L.n <= kDataflowMaxN)
+        if (lb.tflags && lb.L.n <= c->df_maxn)
             CK(cudaMemsetAsync(lb.tflags, 0, sizeof(unsigned) * (lb.L.n / kTile) * (lb.L.n / kTile), c->s));
         lb.epoch = 0;
     }
@@ -1037,7 +1040,7 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             // at the end of rebuild)
             CK(cudaStreamWaitEvent(c->s2, c->ev_sizes, 0));
             std::swap(c->s, c->s2);
-            LAUNCH(c, k_slab_fill, nblk(size_t(nball) * 40), 256, 0, S, c->sl_off, c->sl_col, c->sl_val);
+            LAUNCH(c, k_slab_fill, nblk(size_t(nball) * 40 * 32), 256, 0, S, c->sl_off, c->sl_col, c->sl_val);
             std::swap(c->s, c->s2);
             CK(cudaEventRecord(c->ev_join, c->s2));
             side_used = true;
@@ -1245,12 +1248,13 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     for (int k = 0; k < lb.ncol; ++k) widest = std::max(widest, lb.coff[k + 1] - lb.coff[k]);
     Lev L = lb.L;
     Slabs SL = slabs(lb);
-    if (n <= kDataflowMaxN) {
+    if (n <= c->df_maxn) {
         // latency regime: the whole sweep as one dataflow kernel
         DfArgs A{L, SL, BC, BigDeps{lb.pred, lb.poff, lb.flags, ++lb.epoch}, lb.tflags, lb.big, b, w, c->trace};
         if (c->prof) prof_begin(c, "k_sweep_df");
-        launch_k(c, k_sweep_df, dim3(c->grid_limit > 0 ? std::min(c->grid_limit, c->df_grid_max) : c->df_grid_max),
-                 dim3(32 * kDfWarps), kDfSmem, true, A);
+        const dim3 grid(c->grid_limit > 0 ? std::min(c->grid_limit, c->df_grid_max) : c->df_grid_max);
+        if (c->df_es) launch_k(c, k_sweep_df<true>, grid, dim3(32 * kDfWarps), kDfSmemES, true, A);
+        else launch_k(c, k_sweep_df<false>, grid, dim3(32 * kDfWarps), kDfSmem, true, A);
         if (c->prof) prof_end(c);
         ++c->launches;
         return;
@@ -1441,6 +1445,8 @@ ClArgs cluster_args(ibmg_ctx* c, const double* b_in, double* w_out, double* w_fi
     A.w_out = w_out;
     A.w_fine = w_fine;
     A.u_off = c->cl_uoff;
+    A.trace = c->trace;
+    A.gen = c->cl_gen;
     return A;
 }
 
@@ -1690,11 +1696,13 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
         g[0] = beta;
         int kdim = 0;
         double nu0 = 1.0;
-        bool head_done = false;
+        // what of column j's V-cycle is already enqueued: 0 nothing, 1 its first
+        // sweep, 2 all of it (launched speculatively behind step j-1's dots)
+        int pre = 0;
         for (int j = 0; j < m; ++j) {
             double* Vj = c->V + c->Mst * j;
             double* Zj = c->Z + c->Mst * j;
-            vcycle(c, Vj, Zj, false, true, head_done);
+            if (pre < 2) vcycle(c, Vj, Zj, false, true, pre == 1);
             apply_level(c, 0, Zj, c->wv);
             ortho_dots(c, j + 1, c->wv);
             // q_{j+1} = w1 (unnormalised) straight into the next slot, Z_{j+1} = 0
@@ -1703,8 +1711,21 @@ int fgmres2(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st) {
                          more ? c->Z + c->Mst * (j + 1) : nullptr);
             CK(cudaMemcpyAsync(c->hpin, c->dh, sizeof(double) * (bslot + 1), cudaMemcpyDeviceToHost, c->s));
             CK(cudaEventRecord(c->ev_dots, c->s));
-            // the next V-cycle's first sweep, speculatively
-            head_done = more && vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1));
+            // the next V-cycle, speculatively, while the host waits for the dots:
+            // all of it when step j is not expected to converge (the estimate
+            // |g_j| times the last reduction factor stays above 4 tol; a miss
+            // costs one discarded V-cycle), else its first sweep
+            pre = 0;
+            if (more) {
+                const bool likely_last = j >= 1 && bnorm > 0.0 && std::fabs(g[j]) * (std::fabs(g[j]) / std::fabs(g[j - 1])) <= 4.0 * tol;
+                const bool room = it + 1 < c->prm.max_iters;
+                if (c->spec_full && room && !likely_last && j >= 1) {
+                    vcycle(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1), false, true, false);
+                    pre = 2;
+                } else if (vcycle_head(c, c->V + c->Mst * (j + 1), c->Z + c->Mst * (j + 1))) {
+                    pre = 1;
+                }
+            }
             CK(cudaEventSynchronize(c->ev_dots));
             const double* hp = c->hpin;
             if (bnorm < 0.0) {  // first read: ||b||, and a deferred rebuild check
@@ -1976,6 +1997,10 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_CANON_INV")) c->canon_inv = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
+    if (const char* e = std::getenv("IBMG_DF_MAXN")) c->df_maxn = std::atoi(e);
+    if (const char* e = std::getenv("IBMG_DF_ES")) c->df_es = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_SPEC")) c->spec_full = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_CL_GEN")) c->cl_gen = std::atoi(e);
     c->prm = *p;
     c->krows = krows;
     try {
@@ -1998,8 +2023,12 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             c->big_grid_max = std::max(1, per_sm * sms);
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_tiles_pp, 32, kPPSmem));
             c->pp_grid_max = std::max(1, per_sm * sms);
-            CK(cudaFuncSetAttribute(k_sweep_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df, 32 * kDfWarps, kDfSmem));
+            CK(cudaFuncSetAttribute(k_sweep_df<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
+            CK(cudaFuncSetAttribute(k_sweep_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmemES)));
+            if (c->df_es)
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<true>, 32 * kDfWarps, kDfSmemES));
+            else
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<false>, 32 * kDfWarps, kDfSmem));
             c->df_grid_max = std::max(1, per_sm * sms);
             CK(cudaFuncSetAttribute(k_canon_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     56 * gj_ld(56) * 8));
@@ -2091,6 +2120,7 @@ void ibmg_destroy(ibmg_ctx* c) {
 
 const char* ibmg_last_error(const ibmg_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int ibmg_num_levels(const ibmg_ctx* c) { return c ? c->nlev : -1; }
+int ibmg_cluster_level(const ibmg_ctx* c) { return c ? (c->cl_ok ? c->lt : -1) : -2; }
 int ibmg_level_n(const ibmg_ctx* c, int l) { return (c && l >= 0 && l < c->nlev) ? c->lev[l].L.n : -1; }
 long long ibmg_kernel_launches(const ibmg_ctx* c) { return c ? c->launches : -1; }
 
@@ -2302,6 +2332,30 @@ long ibmg_debug_coarse_trace(ibmg_ctx* c, const double* b, double* w, unsigned l
         cudaFree(d);
         return 64;
     } catch (const std::exception& e) {
+        fail(c, e, -1);
+        return -1;
+    }
+}
+
+// Debug: one cluster-kernel launch (device b, w at the first cluster level)
+// with CTA-0 (globaltimer, tag) stamps after each cluster barrier; returns
+// the number of stamps, or -1.  Not part of the solver path.
+long ibmg_debug_cluster_trace(ibmg_ctx* c, const double* b, double* w, unsigned long long* out, long cap) {
+    try {
+        if (!c || !c->cl_ok) return -1;
+        CK(cudaSetDevice(c->prm.device));
+        const long words = 4000;
+        unsigned long long* d = dalloc<unsigned long long>(words);
+        CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * words, c->s));
+        c->trace = d;
+        cluster_cycle(c, b, w, nullptr);
+        c->trace = nullptr;
+        CK(cudaStreamSynchronize(c->s));
+        if (out) CK(cudaMemcpy(out, d, sizeof(unsigned long long) * std::min(words, cap), cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        return words / 2;
+    } catch (const std::exception& e) {
+        c->trace = nullptr;
         fail(c, e, -1);
         return -1;
     }

@@ -786,15 +786,24 @@ __global__ void __launch_bounds__(32) k_plain_df(Lev L, const double* __restrict
     }
 }
 
-__global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
+// ES = false: the double-buffered SlabSlot variant (inverse staged in shared
+// memory, 1 CTA per SM).  ES = true: one E'-row slot refilled as soon as a
+// block's rows are consumed and the 25 KB inverse streamed from L2 into
+// registers (k_big_phase's scheme): 97 KB per CTA, 2 CTAs (two big blocks and
+// 8 tile warps in flight) per SM.  Same arithmetic, bitwise identical results.
+constexpr size_t kDfTileStride = (kDfTileBytes + 15) / 16 * 16;
+constexpr size_t kDfSmemES = sizeof(ESlot) + kDfWarps * kDfTileStride;
+template <bool ES>
+__global__ void __launch_bounds__(32 * kDfWarps, ES ? 2 : 1) k_sweep_df(DfArgs A) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char dsm[];
     SlabSlot* slot = reinterpret_cast<SlabSlot*>(dsm);
+    ESlot* eslot = reinterpret_cast<ESlot*>(dsm);
     __shared__ BigScratch S;
     const Lev& L = A.L;
-    const int n = L.n, nn = L.nn, t = threadIdx.x, wid = t >> 5, lane = t & 31, G = gridDim.x;
+    const int n = L.n, nn = L.nn, t = threadIdx.x, wid = t >> 5, G = gridDim.x;
     const int nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1, nbk = n >> 2;
-    double* sw = reinterpret_cast<double*>(dsm + 2 * sizeof(SlabSlot) + wid * ((kDfTileBytes + 15) / 16 * 16));
+    double* sw = reinterpret_cast<double*>(dsm + (ES ? sizeof(ESlot) : 2 * sizeof(SlabSlot)) + wid * kDfTileStride);
     double* sb = sw + 3 * kRegP;
     const unsigned epoch = A.DP.epoch;
     // first big slab streams in while the plain tasks run
@@ -810,7 +819,10 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         }
     };
     next_item(-1, 0, c, q);
-    if (c < A.BC.ncol) slab_issue(slot[0], A.SL, q, t, 32 * kDfWarps);
+    if (c < A.BC.ncol) {
+        if (ES) eslot_issue(*eslot, A.SL, q, t, 32 * kDfWarps);
+        else slab_issue(slot[0], A.SL, q, t, 32 * kDfWarps);
+    }
     cp_async_commit();
     // ---- plain tasks: warp per tile, tile-colour-major order
     for (int task = blockIdx.x * kDfWarps + wid; task < ntiles; task += G * kDfWarps) {
@@ -826,8 +838,10 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
     while (c < A.BC.ncol) {
         int nc, nq;
         next_item(c, q, nc, nq);
-        if (nc < A.BC.ncol) slab_issue(slot[(k + 1) & 1], A.SL, nq, t, 32 * kDfWarps);
-        cp_async_commit();
+        if (!ES) {
+            if (nc < A.BC.ncol) slab_issue(slot[(k + 1) & 1], A.SL, nq, t, 32 * kDfWarps);
+            cp_async_commit();
+        }
         const int Bk = A.SL.rp[(size_t)q * 48 + 47];
         const int bi = 4 * (Bk % nbk), bj = 4 * (Bk / nbk);
         const unsigned long long t_a = A.trace ? gtimer() : 0;
@@ -841,15 +855,24 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_sweep_df(DfArgs A) {
         }
         __syncthreads();
         const unsigned long long t_b = A.trace ? gtimer() : 0;
-        cp_async_wait<1>();
+        if (ES) cp_async_wait<0>();
+        else cp_async_wait<1>();
         __syncthreads();
         const unsigned long long t_c = A.trace ? gtimer() : 0;
-        unsigned long long* dbgp = A.trace ? A.trace + 6 * ntiles + 9 * q + 6 : nullptr;
-        big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg,
-                       [&](int f, int i, int j, double old, double d) {
-                           __stcg(A.w + (size_t)f * nn + i + (size_t)j * n, old + d);
-                       },
-                       S, t, dbgp);
+        auto wadd = [&](int f, int i, int j, double old, double d) {
+            __stcg(A.w + (size_t)f * nn + i + (size_t)j * n, old + d);
+        };
+        if (ES) {
+            big_block_es<0>(L, *eslot, A.SL.Ainv + (size_t)q * 3136, bi, bj, Wg, FlatCG{A.w}, Bg, wadd, S, t,
+                            [] { __syncthreads(); },
+                            [&] {
+                                if (nc < A.BC.ncol) eslot_issue(*eslot, A.SL, nq, t, 32 * kDfWarps);
+                                cp_async_commit();
+                            });
+        } else {
+            unsigned long long* dbgp = A.trace ? A.trace + 6 * ntiles + 9 * q + 6 : nullptr;
+            big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg, wadd, S, t, dbgp);
+        }
         __syncthreads();
         if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(A.DP.flags + q, epoch);
@@ -1224,18 +1247,21 @@ __global__ void k_slab_count(BSetup S, int* __restrict__ cnt, int* __restrict__ 
     atomicMax(counters + S.lev[k] * ctr_stride + 19, rel);
 }
 
-// The entries, at off[qg] (level-major offsets), columns as flat indices.
+// The entries, at off[qg] (level-major offsets), columns as flat indices: one
+// warp per (block, row), the lanes over the row's entries (coalesced; rows of
+// the coarse Galerkin levels run to hundreds of entries).
 __global__ void k_slab_fill(BSetup S, const int* __restrict__ off, int* __restrict__ col, double* __restrict__ val) {
     pdl_enter();
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= S.start[S.nlev] * 40) return;
-    const int qg = idx / 40, t = idx % 40, k = bs_level(S, qg), q = qg - S.start[k];
-    const int2 r = S.rr[k][idx - S.start[k] * 40];
+    const long idx = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (idx >= (long)S.start[S.nlev] * 40) return;
+    const int qg = int(idx / 40), t = int(idx % 40), k = bs_level(S, qg), q = qg - S.start[k];
+    const int2 r = S.rr[k][idx - (long)S.start[k] * 40];
     const EMat& E = S.E[k];
-    int o = off[qg] + S.sl_rp[k][(size_t)q * 48 + t];
-    for (int e = r.x; e < r.y; ++e, ++o) {
-        col[o] = E.col[e];
-        val[o] = E.val[e];
+    const int o = off[qg] + S.sl_rp[k][(size_t)q * 48 + t] - r.x;
+    for (int e = r.x + lane; e < r.y; e += 32) {
+        col[o + e] = E.col[e];
+        val[o + e] = E.val[e];
     }
 }
 

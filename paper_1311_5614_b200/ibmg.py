@@ -50,7 +50,8 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_group_last_error", "ibmg_group_distributed_levels", "ibmg_group_kernel_launches",
            "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
            "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl",
-           "ibmg_vcycle_spectrum", "ibmg_set_scheme", "ibmg_set_input_stream"]
+           "ibmg_vcycle_spectrum", "ibmg_set_scheme", "ibmg_set_input_stream", "ibmg_debug_cluster_trace",
+           "ibmg_cluster_level"]
 
 
 def lib_path() -> str:
@@ -94,6 +95,9 @@ def lib(build_if_missing: bool = True):
     L.ibmg_stream.restype = C.c_void_p
     L.ibmg_stream.argtypes = [vp]
     L.ibmg_set_input_stream.argtypes = [vp, vp]
+    L.ibmg_debug_cluster_trace.restype = C.c_long
+    L.ibmg_debug_cluster_trace.argtypes = [vp, vp, vp, vp, C.c_long]
+    L.ibmg_cluster_level.argtypes = [vp]
     L.ibmg_debug_sweep_trace.restype = C.c_long
     L.ibmg_debug_sweep_trace.argtypes = [vp, ip, vp, vp, vp, C.c_long]
     L.ibmg_elasticity_triplets.restype = C.c_long
@@ -356,6 +360,11 @@ class SaddleSystem:
         return ritz[np.argsort(-np.abs(ritz))], H.reshape(m + 1, m)[: k + 1, :k]
 
     @property
+    def cluster_level(self):
+        """First level run by the 16-CTA cluster kernel, or -1 (cluster path off)."""
+        return self._L.ibmg_cluster_level(self._h)
+
+    @property
     def kernel_launches(self):
         return int(self._L.ibmg_kernel_launches(self._h))
 
@@ -454,6 +463,11 @@ class SlabGroup:
     @property
     def distributed_levels(self):
         return self._L.ibmg_group_distributed_levels(self._h)
+
+    @property
+    def cluster_level(self):
+        """First level run by the 16-CTA cluster kernel, or -1 (cluster path off)."""
+        return self._L.ibmg_cluster_level(self._h)
 
     @property
     def kernel_launches(self):

@@ -48,9 +48,10 @@ for level in range(g.num_levels):
         print("  big wait-deps / wait-slab / solve (us): mean %.2f / %.2f / %.2f; end at %.2f" % (
             np.mean(bigs[:, 1] - bigs[:, 0]) / 1e3, np.mean(bigs[:, 2] - bigs[:, 1]) / 1e3,
             np.mean(bigs[:, 3] - bigs[:, 2]) / 1e3, (bigs[:, 3].max() - t0) / 1e3))
-        print("  solve phases (us): residual %.2f | sync %.2f | matvec+sync %.2f | write+publish %.2f" % (
-            np.mean(bigs[:, 6] - bigs[:, 2]) / 1e3, np.mean(bigs[:, 7] - bigs[:, 6]) / 1e3,
-            np.mean(bigs[:, 8] - bigs[:, 7]) / 1e3, np.mean(bigs[:, 3] - bigs[:, 8]) / 1e3))
+        if bigs[:, 6].any():  # per-phase stamps (slab-slot variant only: IBMG_DF_ES=0)
+            print("  solve phases (us): residual %.2f | sync %.2f | matvec+sync %.2f | write+publish %.2f" % (
+                np.mean(bigs[:, 6] - bigs[:, 2]) / 1e3, np.mean(bigs[:, 7] - bigs[:, 6]) / 1e3,
+                np.mean(bigs[:, 8] - bigs[:, 7]) / 1e3, np.mean(bigs[:, 3] - bigs[:, 8]) / 1e3))
         for col in range(int(bigs[:, 4].max()) + 1):
             m = bigs[:, 4] == col
             print(f"    colour {col}: {m.sum():3d} blocks, start {(bigs[m,0].min()-t0)/1e3:7.2f} done {(bigs[m,3].max()-t0)/1e3:7.2f} us")
