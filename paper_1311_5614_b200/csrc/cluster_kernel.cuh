@@ -14,8 +14,8 @@
 //   tile is staged (local + DSMEM) into one warp's shared buffers, relaxed by
 //   the 8 conflict-free cell colours (i + 2j) mod 8 (plain_cell, the same
 //   arithmetic as k_sweep_df) and written back to the owners.  Big phase: the
-//   big 4x4 blocks in colour order, each by its owner CTA (2 groups of 128
-//   threads), stencil and E' columns read through the distributed view.
+//   big 4x4 blocks in colour order, spread over the cluster's 32 groups of
+//   128 threads, stencil and E' columns read through the distributed view.
 // * "Q-levels" (n <= 32, replicated): every CTA holds the whole level and runs
 //   the plain phase redundantly (identical arithmetic in every copy); the big
 //   blocks of a colour are spread over the 32 groups of the cluster and each
@@ -49,7 +49,6 @@ __device__ __forceinline__ unsigned cl_rank() {
 // (globaltimer, tag) after each cluster barrier; cl_tr == nullptr in production
 __shared__ unsigned long long* cl_tr;
 __shared__ int cl_nm;
-__shared__ int cl_gen;  // ClArgs.gen (DView)
 __device__ __forceinline__ void cl_mark(int tag) {
     if (cl_tr && threadIdx.x == 0) {
         if (cl_nm < 2000) {
@@ -82,7 +81,6 @@ struct DView {
     int n, nn, lg;
     int part, Rx, Ry, lgRx, lgRy;
     unsigned me;
-    int gen;  // 1: every partitioned access through mapa + a generic load (no local/remote branch)
     __device__ __forceinline__ unsigned owner(int i, int j) const { return (i >> lgRx) + kClCX * (j >> lgRy); }
     __device__ __forceinline__ int loff(int f, int i, int j) const {  // i, j wrapped
         return part ? f * (Rx * Ry) + (i & (Rx - 1)) + (j & (Ry - 1)) * Rx : f * nn + i + j * n;
@@ -90,10 +88,9 @@ struct DView {
     __device__ __forceinline__ double get(int f, int i, int j) const {  // wrapped coordinates
         const int k = loff(f, i, j);
         if (!part) return in_smem(loc)[k];
-        const unsigned o = owner(i, j);
-        if (gen) return *cl_map(loc + k, o);
-        if (o == me) return in_smem(loc)[k];
-        return *cl_map(loc + k, o);
+        // one generic load through mapa, local or remote (no divergent branch:
+        // a warp's loads issue back to back)
+        return *cl_map(loc + k, owner(i, j));
     }
     __device__ __forceinline__ double operator()(int f, int i, int j) const { return get(f, wr(i, n), wr(j, n)); }
     __device__ __forceinline__ double operator[](int flat) const {  // flat = f nn + i + j n
@@ -121,8 +118,6 @@ struct ClLev {
     EMat E;
     Slabs SL;
     const uint8_t* big;
-    const int* own_q;    // P-levels: list positions of the big blocks, per owner rank in colour order
-    const int* own_off;  // [rank * (ncol + 1) + c]
     int nbig, ncol, part, Rx, Ry, lgRx, lgRy;
     int coff[kClMaxColours + 1];
     int w_off, b_off;  // shared-memory offsets (doubles) of w and b (this CTA's part or copy)
@@ -137,7 +132,6 @@ struct ClArgs {
     double* w_fine;         // optional: w of the next finer level += P w_out
     int u_off;              // union region (doubles): 2 E' slots | tile buffers, residual, E' dots
     unsigned long long* trace;  // debug timeline (nullptr in production)
-    int gen;                    // DView.gen
 };
 
 // union region layout (doubles)
@@ -150,7 +144,7 @@ constexpr int kClUnionD = (kClGroups * kClSlotD > kClTileD + kClResD + kClEDots)
                                                                                     : kClTileD + kClResD + kClEDots;
 
 __device__ __forceinline__ DView cl_view(const ClLev& C, double* base, int off, unsigned me) {
-    return DView{base + off, C.L.n, C.L.nn, C.L.lg, C.part, C.Rx, C.Ry, C.lgRx, C.lgRy, me, cl_gen};
+    return DView{base + off, C.L.n, C.L.nn, C.L.lg, C.part, C.Rx, C.Ry, C.lgRx, C.lgRy, me};
 }
 
 // ---- plain phase of a P-level: the tile colours in order, one cluster step each
@@ -168,14 +162,33 @@ __device__ void cl_plain_p(const ClLev& C, const DView& W, const DView& B, doubl
                 const int gx = X0 / kTile + tx, gy = Y0 / kTile + ty;
                 if ((gx & 1) + 2 * (gy & 1) != tc) continue;
                 const int x0 = gx * kTile, y0 = gy * kTile;
-                // stage the w region (2-cell halo) and the b region: local or DSMEM
-                for (int q = t; q < 3 * kReg * kReg; q += kClThreads) {
+                // stage the w region (2-cell halo) and the b region: local or
+                // DSMEM; every thread's loads are issued before its stores
+                constexpr int NW = (3 * kReg * kReg + kClThreads - 1) / kClThreads;
+                constexpr int NB = (3 * 289 + kClThreads - 1) / kClThreads;
+                double vw[NW], vb[NB];
+#pragma unroll
+                for (int u = 0; u < NW; ++u) {
+                    const int q = t + u * kClThreads;
                     const int f = q / (kReg * kReg), rem = q - f * kReg * kReg, bb = rem / kReg, a = rem - bb * kReg;
-                    sw[f * kRegP + bb * kRegS + a] = W.get(f, wr(x0 - 2 + a, n), wr(y0 - 2 + bb, n));
+                    vw[u] = q < 3 * kReg * kReg ? W.get(f, wr(x0 - 2 + a, n), wr(y0 - 2 + bb, n)) : 0.0;
                 }
-                for (int q = t; q < 3 * 289; q += kClThreads) {
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    const int q = t + u * kClThreads;
                     const int f = q / 289, rem = q - f * 289, bb = rem / 17, a = rem - bb * 17;
-                    sb[f * 289 + bb * 17 + a] = B.get(f, wr(x0 + a, n), wr(y0 + bb, n));
+                    vb[u] = q < 3 * 289 ? B.get(f, wr(x0 + a, n), wr(y0 + bb, n)) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < NW; ++u) {
+                    const int q = t + u * kClThreads;
+                    const int f = q / (kReg * kReg), rem = q - f * kReg * kReg, bb = rem / kReg, a = rem - bb * kReg;
+                    if (q < 3 * kReg * kReg) sw[f * kRegP + bb * kRegS + a] = vw[u];
+                }
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    const int q = t + u * kClThreads;
+                    if (q < 3 * 289) sb[q] = vb[u];
                 }
                 __syncthreads();
                 if (wid == 0) {  // the 8 conflict-free colours on the staged tile (as df_plain_tile)
@@ -222,23 +235,21 @@ __device__ void cl_plain_q(const ClLev& C, double* w, const double* b) {
 }
 
 // ---- big phase (P or Q): colour classes in order, one cluster step each.
-// P: a CTA relaxes the blocks of its region (own_q lists); Q: block k of a
-// colour goes to group k mod 32 of the cluster.  A group's next block (in
-// the same or a later colour) has its E' rows refilled into the group's slot
-// as soon as the current block's rows are consumed.
+// Block k of a colour goes to group k mod 32 of the cluster.  A group's next
+// block (in the same or a later colour) has its E' rows refilled into the
+// group's slot as soon as the current block's rows are consumed, and its
+// inverse loaded into registers right after the current block's matvec.
 __device__ void cl_big(const ClLev& C, const DView& W, const DView& B, double* un, BigScratch* S, unsigned me) {
     if (C.nbig == 0) return;
     const Lev& L = C.L;
     const int t = threadIdx.x, g = t / kGroup, gt = t % kGroup, nbk = L.n >> 2;
     ESlot* slot = reinterpret_cast<ESlot*>(in_smem(un)) + g;
     const int gid = int(me) * kClGroups + g;  // Q: this group's rank in the cluster
-    // k-th item of this group in colour c (or -1): a list position
+    // k-th item of this group in colour c (or -1): a list position.  Block m of
+    // a colour goes to group m mod 32 of the cluster (P-levels too: DSMEM
+    // makes every region reachable, and owner-computes left most groups idle
+    // where the structure crosses few regions)
     auto item = [&](int c, int k) -> int {
-        if (C.part) {
-            const int o0 = __ldg(C.own_off + me * (C.ncol + 1) + c), o1 = __ldg(C.own_off + me * (C.ncol + 1) + c + 1);
-            const int e = o0 + g + kClGroups * k;
-            return e < o1 ? __ldg(C.own_q + e) : -1;
-        }
         const int q = C.coff[c] + gid + kCl * kClGroups * k;
         return q < C.coff[c + 1] ? q : -1;
     };
@@ -253,7 +264,11 @@ __device__ void cl_big(const ClLev& C, const DView& W, const DView& B, double* u
     };
     int c = 0, k = -1, q = -1;
     advance(c, k, q);
-    if (c < C.ncol) eslot_issue(*slot, C.SL, q, gt, kGroup);
+    double av[28];  // this thread's part of the group's next inverse, loaded a block ahead
+    if (c < C.ncol) {
+        eslot_issue(*slot, C.SL, q, gt, kGroup);
+        load_inverse_part(av, C.SL.Ainv + (size_t)q * 3136, gt);
+    }
     cp_async_commit();
     auto gsync = [g] { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kGroup)); };
     for (int colour = 0; colour < C.ncol; ++colour) {
@@ -263,12 +278,14 @@ __device__ void cl_big(const ClLev& C, const DView& W, const DView& B, double* u
             cp_async_wait<0>();
             gsync();
             const int Bk = slot->rp[47];
-            big_block_es<0>(L, *slot, C.SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), W, W, B,
+            big_block_es<0>(L, *slot, nullptr, 4 * (Bk % nbk), 4 * (Bk / nbk), W, W, B,
                             [&](int f, int i, int j, double old, double d) { W.put(f, i, j, old + d); }, S[g], gt,
-                            gsync, [&] {
+                            gsync,
+                            [&] {
                                 if (nc < C.ncol) eslot_issue(*slot, C.SL, nq, gt, kGroup);
                                 cp_async_commit();
-                            });
+                            },
+                            av, nc < C.ncol ? C.SL.Ainv + (size_t)nq * 3136 : nullptr);
             gsync();
             c = nc;
             k = nk;
@@ -311,17 +328,26 @@ __device__ void cl_restrict(const ClLev& C, const ClLev& D, double* sm, double* 
             rs[2 * RR + q] = B.get(2, i, j) - rp;
         }
         __syncthreads();
-        // E' rows of the faces this CTA owns: a warp per row, fixed-order xor tree
-        for (int fq = wid; fq < C.FL.nf; fq += kClWarps) {
-            const int face = __ldg(C.FL.face + fq), f = face >> (2 * L.lg), rem = face & (nn - 1);
-            const int i = rem & (n - 1), j = rem >> L.lg;
-            if (W.owner(i, j) != me) continue;
-            double s = 0.0;
-            for (int e = __ldg(C.E.rp + fq) + lane; e < __ldg(C.E.rp + fq + 1); e += 32)
-                s += __ldg(C.E.val + e) * W[__ldg(C.E.col + e)];
+        // E' rows of the faces this CTA owns: a warp reads 32 faces at once,
+        // ballots the owned ones and sums each of their rows (lanes over the
+        // entries, fixed-order xor tree)
+        for (int base = wid * 32; base < C.FL.nf; base += kClWarps * 32) {
+            const int fq = base + lane;
+            const int face = fq < C.FL.nf ? __ldg(C.FL.face + fq) : 0, rem = face & (nn - 1);
+            const bool mine = fq < C.FL.nf && W.owner(rem & (n - 1), rem >> L.lg) == me;
+            unsigned m = __ballot_sync(0xffffffffu, mine);
+            while (m) {
+                const int bl = __ffs(m) - 1;
+                m &= m - 1;
+                const int fr = base + bl, fc = __shfl_sync(0xffffffffu, face, bl);
+                const int f = fc >> (2 * L.lg), rr = fc & (nn - 1);
+                double s = 0.0;
+                for (int e = __ldg(C.E.rp + fr) + lane; e < __ldg(C.E.rp + fr + 1); e += 32)
+                    s += __ldg(C.E.val + e) * W[__ldg(C.E.col + e)];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) rs[R.loff(f, i, j)] += s;
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) rs[R.loff(f, rr & (n - 1), rr >> L.lg)] += s;
+            }
         }
         cl_sync(C.L.lg * 10000 + 400);  // every region's residual is complete
     } else {
@@ -425,7 +451,6 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cluster_cycle(ClArgs A) {
     if (threadIdx.x == 0) {
         cl_tr = me == 0 ? A.trace : nullptr;
         cl_nm = 0;
-        cl_gen = A.gen;
     }
     __syncthreads();
     cl_mark(1);

@@ -114,13 +114,6 @@ struct LevelBuf {
     size_t h_up_cap = 0;
     std::vector<int> h_pos;                  // block -> list position scratch (colouring)
     unsigned* h_cm = nullptr;                // pinned mirror of cmask
-    // cluster kernel (P-levels): big-block list positions per owner rank in
-    // colour order, and their colour offsets per rank (cluster_lists)
-    int* cl_q = nullptr;
-    int* cl_off = nullptr;
-    int cl_cap = 0;
-    int* h_cl = nullptr;  // pinned staging of their upload
-    int h_cl_cap = 0;
 };
 
 }  // namespace
@@ -136,7 +129,7 @@ struct ibmg_ctx {
     // n <= 128) when cl_ok; IBMG_CLUSTER=0 keeps the dataflow sweeps + coarse kernel
     int lt = 0;
     bool cl_ok = false;
-    int cl_smem = 0, cl_uoff = 0, cl_gen = 0;  // cl_gen: IBMG_CL_GEN (DView access mode)
+    int cl_smem = 0, cl_uoff = 0;
     std::vector<int> cl_woff, cl_boff;
     std::vector<LevelBuf> lev;
     long long launches = 0;
@@ -665,8 +658,6 @@ void colour_big_blocks(ibmg_ctx* c, LevelBuf& lb, const unsigned* cm) {
                        c->s));
 }
 
-void cluster_lists(ibmg_ctx* c);
-
 void check_err_flag(ibmg_ctx* c, const char* where) {
     int h = 0;
     CK(cudaMemcpyAsync(&h, c->err_flag, sizeof(int), cudaMemcpyDeviceToHost, c->s));
@@ -918,7 +909,6 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             }
             for (auto& j : jobs) j.get();
         }
-        cluster_lists(c);
         tr.mark("coloured");
         // big-block E' row ranges, slabs and inverses of every level: one
         // launch each over the level-major block numbering
@@ -1364,55 +1354,6 @@ void setup_cluster(ibmg_ctx* c) {
     c->cl_ok = true;
 }
 
-// Per P-level (n >= 64) of the cluster kernel: the big-block list positions of
-// each owner rank (the CTA whose region holds the block) in colour order, and
-// the per-rank colour offsets; uploaded from pinned staging (async).
-void cluster_lists(ibmg_ctx* c) {
-    if (!c->cl_ok) return;
-    for (int l = c->lt; l + 1 < c->nlev; ++l) {
-        LevelBuf& lb = c->lev[l];
-        const int n = lb.L.n;
-        if (n < 4 * kTile || lb.nbig == 0) continue;
-        const int nbk = n / 4, Rx = n / kClCX, Ry = n / kClCY, nc = lb.ncol, nbig = lb.nbig;
-        const int need = nbig + kCl * (nc + 1);
-        if (lb.cl_cap < need) {
-            dfree(lb.cl_q);
-            lb.cl_cap = int(grow_cap(need, lb.cl_cap));
-            lb.cl_q = dalloc<int>(size_t(lb.cl_cap));
-        }
-        if (lb.h_cl_cap < need) {
-            if (lb.h_cl) CK(cudaFreeHost(lb.h_cl));
-            lb.h_cl_cap = int(grow_cap(need, lb.h_cl_cap));
-            CK(cudaMallocHost(&lb.h_cl, sizeof(int) * size_t(lb.h_cl_cap)));
-        }
-        int* hq = lb.h_cl;
-        int* ho = lb.h_cl + nbig;
-        std::vector<int> own(nbig);
-        std::fill(ho, ho + kCl * (nc + 1), 0);
-        for (int col = 0; col < nc; ++col)
-            for (int q = lb.coff[col]; q < lb.coff[col + 1]; ++q) {
-                const int B = lb.h_ids[q];
-                own[q] = (4 * (B % nbk)) / Rx + kClCX * ((4 * (B / nbk)) / Ry);
-                ++ho[own[q] * (nc + 1) + col + 1];
-            }
-        int run = 0;  // exclusive offsets, rank-major then colour
-        for (int r = 0; r < kCl; ++r) {
-            ho[r * (nc + 1)] = run;
-            for (int col = 0; col < nc; ++col) {
-                run += ho[r * (nc + 1) + col + 1];
-                ho[r * (nc + 1) + col + 1] = run;
-            }
-        }
-        std::vector<int> fill(kCl * (nc + 1));
-        for (int r = 0; r < kCl; ++r)
-            for (int col = 0; col < nc; ++col) fill[r * (nc + 1) + col] = ho[r * (nc + 1) + col];
-        for (int col = 0; col < nc; ++col)
-            for (int q = lb.coff[col]; q < lb.coff[col + 1]; ++q) hq[fill[own[q] * (nc + 1) + col]++] = q;
-        CK(cudaMemcpyAsync(lb.cl_q, hq, sizeof(int) * size_t(need), cudaMemcpyHostToDevice, c->s));
-        lb.cl_off = lb.cl_q + nbig;
-    }
-}
-
 ClArgs cluster_args(ibmg_ctx* c, const double* b_in, double* w_out, double* w_fine) {
     ClArgs A{};
     A.nl = c->nlev - c->lt;
@@ -1435,8 +1376,6 @@ ClArgs cluster_args(ibmg_ctx* c, const double* b_in, double* w_out, double* w_fi
         C.Ry = C.part ? n / kClCY : n;
         C.lgRx = C.part ? lb.L.lg - 2 : lb.L.lg;
         C.lgRy = C.part ? lb.L.lg - 2 : lb.L.lg;
-        C.own_q = lb.cl_q;
-        C.own_off = lb.cl_off;
         C.w_off = c->cl_woff[l];
         C.b_off = c->cl_boff[l];
     }
@@ -1446,7 +1385,6 @@ ClArgs cluster_args(ibmg_ctx* c, const double* b_in, double* w_out, double* w_fi
     A.w_fine = w_fine;
     A.u_off = c->cl_uoff;
     A.trace = c->trace;
-    A.gen = c->cl_gen;
     return A;
 }
 
@@ -2000,7 +1938,6 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_DF_MAXN")) c->df_maxn = std::atoi(e);
     if (const char* e = std::getenv("IBMG_DF_ES")) c->df_es = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_SPEC")) c->spec_full = std::atoi(e) != 0;
-    if (const char* e = std::getenv("IBMG_CL_GEN")) c->cl_gen = std::atoi(e);
     c->prm = *p;
     c->krows = krows;
     try {
@@ -2070,8 +2007,6 @@ void ibmg_destroy(ibmg_ctx* c) {
         if (lb.h_up) cudaFreeHost(lb.h_up);
         dfree(lb.pdf_seg);
         dfree(lb.escr);
-        dfree(lb.cl_q);
-        if (lb.h_cl) cudaFreeHost(lb.h_cl);
     }
     dfree(c->V);
     dfree(c->Z);

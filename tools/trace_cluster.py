@@ -1,5 +1,5 @@
 """Phase timeline of one k_cluster_cycle launch (debug): CTA 0's stamps after
-each cluster barrier.  usage: python tools/trace_cluster.py [C2|C3|C1] [gen]"""
+each cluster barrier.  usage: python tools/trace_cluster.py [C2|C3|C1]"""
 import os
 import sys
 
@@ -7,8 +7,6 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-if len(sys.argv) > 2:
-    os.environ["IBMG_CL_GEN"] = sys.argv[2]
 from paper_1311_5614_b200 import configs  # noqa: E402
 from paper_1311_5614_b200.ibmg import SaddleSystem  # noqa: E402
 
