@@ -126,7 +126,7 @@ struct ibmg_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sizes = nullptr;
     int nlev = 0, lc = 0;  // levels [lc, nlev) run in the single-CTA coarse kernel
     // levels [lt, nlev) run in the 16-CTA cluster kernel (k_cluster_cycle,
-    // n <= 128) when cl_ok; IBMG_CLUSTER=0 keeps the dataflow sweeps + coarse kernel
+    // n <= 128) when cl_ok (opt-in, IBMG_CLUSTER=1); else the dataflow sweeps + coarse kernel
     int lt = 0;
     bool cl_ok = false;
     int cl_smem = 0, cl_uoff = 0;
@@ -1310,8 +1310,13 @@ void coarse_cycle(ibmg_ctx* c, const double* b, double* w, double* w_fine = null
 // the 3 (n/4)^2 region; Q-level: the whole 3 n^2 level), then the union region.
 void setup_cluster(ibmg_ctx* c) {
     c->cl_ok = false;
-    if (const char* e = std::getenv("IBMG_CLUSTER"))
-        if (std::atoi(e) == 0) return;
+    // opt-in (IBMG_CLUSTER=1): measured slower than the dataflow sweeps + the
+    // single-CTA coarse kernel on B200 (C2 7.59 vs 6.06 ms, C3 23.8 vs 20.5 ms
+    // per step): per-colour block latency, not synchronisation,
+    // bounds these levels, and 16 SMs give the latency-bound E' row gathers
+    // of the residual a ninth of the whole GPU's memory parallelism
+    const char* e = std::getenv("IBMG_CLUSTER");
+    if (!e || std::atoi(e) == 0) return;
     int lt = 0;
     while (lt < c->nlev && c->lev[lt].L.n > kClMaxN) ++lt;
     const int nl = c->nlev - lt;

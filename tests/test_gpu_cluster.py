@@ -1,8 +1,9 @@
 """The cluster-resident bottom of the V-cycle (k_cluster_cycle, levels with
-n <= 128 in one 16-CTA thread-block cluster, DSMEM; cluster_kernel.cuh)
-against the launch-per-phase path it replaces (k_sweep_df dataflow sweeps,
-restriction / prolongation launches, single-CTA k_coarse_cycle; selected with
-IBMG_CLUSTER=0 at context creation) and against the CPU oracle.
+n <= 128 in one 16-CTA thread-block cluster, DSMEM; cluster_kernel.cuh;
+opt-in with IBMG_CLUSTER=1 at context creation, measured slower than the
+default on B200) against the default launch-per-phase path
+(k_sweep_df dataflow sweeps, restriction / prolongation launches,
+single-CTA k_coarse_cycle) and against the CPU oracle.
 
 The partitioned levels relax tiles and big blocks with the same arithmetic as
 k_sweep_df; the replicated levels and the restrictions sum E' rows in a
@@ -76,8 +77,8 @@ def test_cluster_step_matches_old_path(name):
 
 
 def test_cluster_path_is_selected():
-    """The default context runs the cluster kernel (one launch per V-cycle for
-    N <= 128, fewer launches than the old path for N = 256)."""
+    """IBMG_CLUSTER=1 runs the cluster kernel (fewer launches than the default
+    path for N = 256); the default context does not."""
     prob = CASES["C2k6"]()
     g1, g0 = make(prob, True), make(prob, False)
     b = g1.build_rhs(rand(2 * prob.N ** 2, seed=5))
@@ -88,5 +89,6 @@ def test_cluster_path_is_selected():
     g1.profile(True)
     g1.v_cycle(b)
     assert "k_cluster_cycle" in g1.profile_report()
+    assert g1.cluster_level >= 0 and g0.cluster_level == -1
     g1.close()
     g0.close()
