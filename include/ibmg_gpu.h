@@ -146,7 +146,10 @@ long long ibmg_kernel_launches(const ibmg_ctx* ctx);
  * concurrent contexts on one GPU (batches of independent problems, C5) a cap of
  * ~SMs/contexts lets their sweeps run side by side instead of serialising.  A
  * cap > 0 also turns programmatic dependent launch off for the context (its
- * early-resident waiting CTAs would take SMs from the other contexts). */
+ * early-resident waiting CTAs would take SMs from the other contexts), and the
+ * latency-hiding extras whose discarded work costs the other contexts
+ * throughput: the speculative V-cycle behind the FGMRES dots and the
+ * canonical-order box inverses. */
 int ibmg_set_grid_limit(ibmg_ctx* ctx, int max_ctas);
 /* Per-kernel CUDA-event timing on the context stream (bench roofline evidence):
  * enable=1 starts (and clears) the accumulation; report writes JSON

@@ -2073,6 +2073,14 @@ int ibmg_set_grid_limit(ibmg_ctx* c, int max_ctas) {
         // context's next kernel resident (waiting) on SMs the other contexts
         // could use (measured on C5: 1.74 -> 2.30 ms per problem with it on)
         if (max_ctas > 0) c->pdl = false;
+        // throughput mode: work that only hides latency costs the other
+        // contexts' throughput (C5, 10 contexts: the speculative V-cycle behind
+        // the FGMRES dots 1.75 -> 1.60 ms per problem when off, the canonical-
+        // order inverses' extra passes 1.75 -> 1.69)
+        if (max_ctas > 0) {
+            c->spec_full = false;
+            if (!std::getenv("IBMG_CANON_INV")) c->canon_inv = 0;
+        }
         return IBMG_OK;
     });
 }
