@@ -204,6 +204,7 @@ struct ibmg_ctx {
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
+    bool gj_regs = true;    // box inverses: 64-thread register Gauss-Jordan (IBMG_GJ256=1: 256-thread [A|I] form)
     bool spec_full = true;  // FGMRES: whole next V-cycle enqueued behind the dots (IBMG_SPEC=0: first sweep only)
     bool df_es = true;      // dataflow sweep with the E'-row slot + register inverse, 2 CTAs/SM (IBMG_DF_ES=0: slab slots)
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
@@ -884,7 +885,10 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
                 C.cap = c->ccap;
                 std::swap(c->s, c->s2);
                 LAUNCH(c, k_canon_rows, 8 * 148, 256, 0, C);
-                LAUNCH(c, k_canon_inverse, c->ccap, 256, 56 * gj_ld(56) * sizeof(double), C, c->err_flag);
+                if (c->gj_regs)
+                    LAUNCH(c, k_canon_inverse<true>, c->ccap, 64, 56 * gj_ld(56) * sizeof(double), C, c->err_flag);
+                else
+                    LAUNCH(c, k_canon_inverse<false>, c->ccap, 256, 56 * gj_ld(56) * sizeof(double), C, c->err_flag);
                 std::swap(c->s, c->s2);
                 CK(cudaEventRecord(c->ev_join, c->s2));
             }
@@ -1000,7 +1004,10 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
                 CK(cudaEventRecord(c->ev_join, c->s2));
                 side_used = true;
             } else {
-                LAUNCH(c, k_block_inverse, nball, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
+                if (c->gj_regs)
+                    LAUNCH(c, k_block_inverse<true>, nball, 64, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
+                else
+                    LAUNCH(c, k_block_inverse<false>, nball, 256, 56 * gj_ld(56) * sizeof(double), BL, c->err_flag);
                 if (canon) {  // size the canonical buffers for the next steps
                     dfree(c->crr);
                     dfree(c->cainv);
@@ -1944,6 +1951,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_DF_MAXN")) c->df_maxn = std::atoi(e);
     if (const char* e = std::getenv("IBMG_DF_ES")) c->df_es = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_SPEC")) c->spec_full = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_GJ256")) c->gj_regs = std::atoi(e) == 0;
     c->prm = *p;
     c->krows = krows;
     try {
@@ -1956,7 +1964,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
         CK(cudaEventCreate(&c->ev_t0));
         CK(cudaEventCreate(&c->ev_t1));
         CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
-        CK(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
+        CK(cudaFuncSetAttribute(k_block_inverse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
+        CK(cudaFuncSetAttribute(k_block_inverse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
         CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * gj_ld(49) * 8));
         CK(cudaFuncSetAttribute(k_big_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
         {
@@ -1973,7 +1982,9 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             else
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<false>, 32 * kDfWarps, kDfSmem));
             c->df_grid_max = std::max(1, per_sm * sms);
-            CK(cudaFuncSetAttribute(k_canon_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(k_canon_inverse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    56 * gj_ld(56) * 8));
+            CK(cudaFuncSetAttribute(k_canon_inverse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     56 * gj_ld(56) * 8));
             CK(cudaFuncSetAttribute(k_plain_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPdfSmem)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_df, 32, kPdfSmem));

@@ -1027,6 +1027,120 @@ struct BInvLevels {
     int bylo[20], byhi[20];  // block rows to invert (a slab's own rows; 0, n/4 = all)
 };
 
+// In-place Gauss-Jordan with partial pivoting, register-resident: 64 threads,
+// thread t < 56 holds row t of the 56 x 56 matrix.  Step k takes the unused
+// row with the largest |a_rk| (lowest index on ties) as pivot row p, scales it
+// (a_pk <- 1 / a_pk) and eliminates column k from every other row
+// (a_rk <- -a_rk / a_pk): the in-place inversion of the row-permuted matrix,
+// with no row moved.  The register row is rotated by one column per step, so
+// the pivot column is always element 0 (no dynamic register indexing, a short
+// loop) and after 56 steps every column is back in place.  Per step: a warp
+// argmax, two 64-thread barriers, the pivot row through shared memory.
+// 2 warps and ~150 registers per matrix: ~7 matrices in flight per SM, where
+// the 256-thread [A | I] form (gauss_jordan) is barrier-bound at 3.
+// M: the assembled A (row stride gj_ld(56)); out: inverse, column-major.
+__device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M, double* __restrict__ out, int* err) {
+    constexpr int m = 56, LD = gj_ld(56);
+    __shared__ double prow[m];
+    __shared__ double cand_v[2];
+    __shared__ int cand_i[2];
+    __shared__ int stepof[64], pivrow[m];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const bool act = t < m;
+    double a[m];
+#pragma unroll
+    for (int c = 0; c < m; ++c) a[c] = act ? M[t * LD + c] : 0.0;
+    bool used = !act;
+    for (int k = 0; k < m; ++k) {
+        double v = used ? -1.0 : fabs(a[0]);
+        int idx = used ? 64 : t;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov > v || (ov == v && oi < idx)) {
+                v = ov;
+                idx = oi;
+            }
+        }
+        if (lane == 0) {
+            cand_v[wid] = v;
+            cand_i[wid] = idx;
+        }
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        const double v1 = cand_v[1];
+        const int i1 = cand_i[1];
+        int p = cand_i[0];
+        if (v1 > cand_v[0] || (v1 == cand_v[0] && i1 < p)) p = i1;
+        if (p >= m || a[0] == 0.0 && t == p) {  // no usable pivot: singular
+            if (t == 0) atomicOr(err, 2);
+            return;
+        }
+        if (t == p) {
+            const double inv = 1.0 / a[0];
+#pragma unroll
+            for (int c = 1; c < m; ++c) a[c] *= inv;
+            a[0] = inv;
+#pragma unroll
+            for (int c = 0; c < m; ++c) prow[c] = a[c];
+            used = true;
+            stepof[t] = k;
+            pivrow[k] = t;
+        }
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (act && t != p) {
+            const double f = a[0];
+#pragma unroll
+            for (int c = 1; c < m; ++c) a[c] -= f * prow[c];
+            a[0] = -f * prow[0];
+        }
+        // rotate: element i <- column (k + 1 + i) mod 56
+        const double a0 = a[0];
+#pragma unroll
+        for (int c = 0; c + 1 < m; ++c) a[c] = a[c + 1];
+        a[m - 1] = a0;
+        asm volatile("bar.sync 1, 64;" ::: "memory");  // prow / cand reuse
+    }
+    // A^{-1}[r][c] = X[pivrow[r]][stepof[c]]: the thread of physical row q
+    // (r = stepof[q]) writes column pivrow[j] of the inverse from its a[j]
+    if (act) {
+        const int r = stepof[t];
+#pragma unroll
+        for (int j = 0; j < m; ++j) out[(size_t)pivrow[j] * m + r] = a[j];
+    }
+}
+
+// Assemble the 56x56 box matrix of block B into M (shared, row stride
+// gj_ld(56)) from the Stokes rows and the E' rows (rr40: the 40 velocity rows'
+// ranges in E); any block size (64 threads for the register inverse).
+__device__ __forceinline__ void box_assemble(const Lev& L, const EMat& E, const int2* __restrict__ rr40, int B,
+                                             double* M) {
+    const int t = threadIdx.x, nt = blockDim.x, n = L.n, nbk = n >> 2;
+    const int bi = 4 * (B % nbk), bj = 4 * (B / nbk);
+    constexpr int LD = gj_ld(56);
+    for (int idx = t; idx < 56 * LD; idx += nt) M[idx] = 0.0;
+    __syncthreads();
+    if (t < 56) {
+        int f, i, j;
+        block_dof(t, bi, bj, f, i, j);
+        const int a = i - bi, bb = j - bj;
+        stokes_row_entries(L, f, [&](int f2, int da, int db, double v) {
+            const int c = block_local(f2, a + da, bb + db);
+            if (c >= 0) M[t * LD + c] += v;
+        });
+    }
+    __syncthreads();
+    for (int row = t >> 5; row < 40; row += nt >> 5) {
+        const int2 r = rr40[row];
+        for (int e = r.x + (t & 31); e < r.y; e += 32) {
+            const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
+            const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
+            if (c >= 0) M[row * LD + c] -= E.val[e];
+        }
+    }
+    __syncthreads();
+}
+
 // Assemble the 56x56 box matrix of block B (cell-block index, n/4 per row)
 // from the Stokes rows and the E' rows (rr40: the 40 velocity rows' ranges in
 // E) into M, and invert it into out (column-major).  256 threads.
@@ -1063,7 +1177,10 @@ __device__ __forceinline__ void box_inverse(const Lev& L, const EMat& E, const i
     __syncthreads();
 }
 
-__global__ void k_block_inverse(BInvLevels BL, int* err) {
+// RG = true: 64-thread CTAs, register Gauss-Jordan (default); false: 256
+// threads, gauss_jordan (IBMG_GJ256=1).
+template <bool RG>
+__global__ void __launch_bounds__(RG ? 64 : 256, RG ? 4 : 1) k_block_inverse(BInvLevels BL, int* err) {
     pdl_enter();
     extern __shared__ double M[];  // 56 x gj_ld(56)
     int lv = 0;
@@ -1071,7 +1188,12 @@ __global__ void k_block_inverse(BInvLevels BL, int* err) {
     const int q = blockIdx.x - BL.start[lv], nbk = BL.L[lv].n >> 2;
     const int B = BL.blk_ids[lv][q];
     if (B / nbk < BL.bylo[lv] || B / nbk >= BL.byhi[lv]) return;  // another slab's block
-    box_inverse(BL.L[lv], BL.E[lv], BL.rr[lv] + (size_t)q * 40, B, BL.Ainv[lv] + (size_t)q * 3136, err, M);
+    if (RG) {
+        box_assemble(BL.L[lv], BL.E[lv], BL.rr[lv] + (size_t)q * 40, B, M);
+        gauss_jordan56_regs(M, BL.Ainv[lv] + (size_t)q * 3136, err);
+    } else {
+        box_inverse(BL.L[lv], BL.E[lv], BL.rr[lv] + (size_t)q * 40, B, BL.Ainv[lv] + (size_t)q * 3136, err, M);
+    }
 }
 
 // Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
@@ -1196,13 +1318,19 @@ __global__ void k_canon_rows(CanonInv C) {
 }
 // one CTA per canonical block; the grid is the buffer capacity (>= the block
 // count of the previous step), CTAs past the current count exit
-__global__ void k_canon_inverse(CanonInv C, int* err) {
+template <bool RG>
+__global__ void __launch_bounds__(RG ? 64 : 256, RG ? 4 : 1) k_canon_inverse(CanonInv C, int* err) {
     pdl_enter();
     extern __shared__ double M[];
     const int g = blockIdx.x;
     if (g >= min(*C.total, C.cap)) return;
     const int e = C.ids[g], l = canon_level(C, e);
-    box_inverse(C.L[l], C.E[l], C.rr + (size_t)g * 40, e - C.boff[l], C.Ainv + (size_t)g * 3136, err, M);
+    if (RG) {
+        box_assemble(C.L[l], C.E[l], C.rr + (size_t)g * 40, e - C.boff[l], M);
+        gauss_jordan56_regs(M, C.Ainv + (size_t)g * 3136, err);
+    } else {
+        box_inverse(C.L[l], C.E[l], C.rr + (size_t)g * 40, e - C.boff[l], C.Ainv + (size_t)g * 3136, err, M);
+    }
 }
 struct APerm {
     int nlev;
