@@ -1130,12 +1130,48 @@ __device__ __forceinline__ void box_assemble(const Lev& L, const EMat& E, const 
         });
     }
     __syncthreads();
-    for (int row = t >> 5; row < 40; row += nt >> 5) {
-        const int2 r = rr40[row];
-        for (int e = r.x + (t & 31); e < r.y; e += 32) {
-            const int cidx = E.col[e], comp = cidx >= L.nn, f2 = cidx - comp * L.nn;
+    // E' rows: the 40 rows' entries as one flattened range (row starts in
+    // shared memory), 8 independent loads in flight per thread (the entries of
+    // a row map to distinct local columns: every M element has one writer)
+    __shared__ int rs[41];
+    __shared__ int2 rrs[40];
+    if (t < 40) rrs[t] = rr40[t];
+    __syncthreads();
+    if (t == 0) {
+        int acc = 0;
+        for (int r = 0; r < 40; ++r) {
+            rs[r] = acc;
+            acc += rrs[r].y - rrs[r].x;
+        }
+        rs[40] = acc;
+    }
+    __syncthreads();
+    const int tot = rs[40];
+    for (int e0 = t; e0 < tot; e0 += 8 * nt) {
+        int row[8], idx[8], cidx[8];
+        double val[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * nt;
+            int lo = 0, hi = 40;  // last row with rs[row] <= e
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (rs[mid] <= e) lo = mid; else hi = mid;
+            }
+            row[u] = e < tot ? lo : -1;
+            idx[u] = e < tot ? rrs[lo].x + (e - rs[lo]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            cidx[u] = row[u] >= 0 ? __ldg(E.col + idx[u]) : 0;
+            val[u] = row[u] >= 0 ? __ldg(E.val + idx[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (row[u] < 0) continue;
+            const int comp = cidx[u] >= L.nn, f2 = cidx[u] - comp * L.nn;
             const int c = block_local(comp, wr((f2 & (n - 1)) - bi, n), wr(f2 / n - bj, n));
-            if (c >= 0) M[row * LD + c] -= E.val[e];
+            if (c >= 0) M[row[u] * LD + c] -= val[u];
         }
     }
     __syncthreads();
