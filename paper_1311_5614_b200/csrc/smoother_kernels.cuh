@@ -1032,16 +1032,19 @@ struct BInvLevels {
 // row with the largest |a_rk| (lowest index on ties) as pivot row p, scales it
 // (a_pk <- 1 / a_pk) and eliminates column k from every other row
 // (a_rk <- -a_rk / a_pk): the in-place inversion of the row-permuted matrix,
-// with no row moved.  The register row is rotated by one column per step, so
-// the pivot column is always element 0 (no dynamic register indexing, a short
-// loop) and after 56 steps every column is back in place.  Per step: a warp
-// argmax, two 64-thread barriers, the pivot row through shared memory.
+// with no row moved.  Steps run in rounds of 8 with the pivot column at a
+// static register index, and the register row rotates by 8 columns per round
+// (no dynamic register indexing, a short loop): after 56 steps every column
+// is back in place.  Per step: a warp argmax, two 64-thread barriers, the
+// unscaled pivot row through shared memory (every thread scales its own
+// update by f / a_pk).
 // 2 warps and ~150 registers per matrix: ~7 matrices in flight per SM, where
 // the 256-thread [A | I] form (gauss_jordan) is barrier-bound at 3.
 // M: the assembled A (row stride gj_ld(56)); out: inverse, column-major.
 __device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M, double* __restrict__ out, int* err) {
     constexpr int m = 56, LD = gj_ld(56);
-    __shared__ double prow[m];
+    __shared__ double prow[m];  // the pivot row, unscaled
+    __shared__ double pinv;
     __shared__ double cand_v[2];
     __shared__ int cand_i[2];
     __shared__ int stepof[64], pivrow[m];
@@ -1051,56 +1054,67 @@ __device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M
 #pragma unroll
     for (int c = 0; c < m; ++c) a[c] = act ? M[t * LD + c] : 0.0;
     bool used = !act;
-    for (int k = 0; k < m; ++k) {
-        double v = used ? -1.0 : fabs(a[0]);
-        int idx = used ? 64 : t;
+    // 7 rounds of 8 steps: inside a round the pivot column is a[s] (static),
+    // after it the row rotates by 8 columns
+    for (int k8 = 0; k8 < m / 8; ++k8) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-            if (ov > v || (ov == v && oi < idx)) {
-                v = ov;
-                idx = oi;
+        for (int s = 0; s < 8; ++s) {
+            double v = used ? -1.0 : fabs(a[s]);
+            int idx = used ? 64 : t;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (ov > v || (ov == v && oi < idx)) {
+                    v = ov;
+                    idx = oi;
+                }
+            }
+            if (lane == 0) {
+                cand_v[wid] = v;
+                cand_i[wid] = idx;
+            }
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            const double v1 = cand_v[1];
+            const int i1 = cand_i[1];
+            int p = cand_i[0];
+            if (v1 > cand_v[0] || (v1 == cand_v[0] && i1 < p)) p = i1;
+            if (p >= m || (v1 > cand_v[0] ? v1 : cand_v[0]) == 0.0) {  // no usable pivot: singular
+                if (t == 0) atomicOr(err, 2);
+                return;
+            }
+            if (t == p) {
+#pragma unroll
+                for (int c = 0; c < m; ++c) prow[c] = a[c];
+                pinv = 1.0 / a[s];
+                used = true;
+                stepof[t] = 8 * k8 + s;
+                pivrow[8 * k8 + s] = t;
+            }
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            const double inv = pinv;
+            if (t == p) {
+#pragma unroll
+                for (int c = 0; c < m; ++c)
+                    if (c != s) a[c] *= inv;
+                a[s] = inv;
+            } else if (act) {
+                const double g = a[s] * inv;
+#pragma unroll
+                for (int c = 0; c < m; ++c)
+                    if (c != s) a[c] -= g * prow[c];
+                a[s] = -g;
             }
         }
-        if (lane == 0) {
-            cand_v[wid] = v;
-            cand_i[wid] = idx;
-        }
-        asm volatile("bar.sync 1, 64;" ::: "memory");
-        const double v1 = cand_v[1];
-        const int i1 = cand_i[1];
-        int p = cand_i[0];
-        if (v1 > cand_v[0] || (v1 == cand_v[0] && i1 < p)) p = i1;
-        if (p >= m || a[0] == 0.0 && t == p) {  // no usable pivot: singular
-            if (t == 0) atomicOr(err, 2);
-            return;
-        }
-        if (t == p) {
-            const double inv = 1.0 / a[0];
+        double r8[8];
 #pragma unroll
-            for (int c = 1; c < m; ++c) a[c] *= inv;
-            a[0] = inv;
+        for (int c = 0; c < 8; ++c) r8[c] = a[c];
 #pragma unroll
-            for (int c = 0; c < m; ++c) prow[c] = a[c];
-            used = true;
-            stepof[t] = k;
-            pivrow[k] = t;
-        }
-        asm volatile("bar.sync 1, 64;" ::: "memory");
-        if (act && t != p) {
-            const double f = a[0];
+        for (int c = 0; c + 8 < m; ++c) a[c] = a[c + 8];
 #pragma unroll
-            for (int c = 1; c < m; ++c) a[c] -= f * prow[c];
-            a[0] = -f * prow[0];
-        }
-        // rotate: element i <- column (k + 1 + i) mod 56
-        const double a0 = a[0];
-#pragma unroll
-        for (int c = 0; c + 1 < m; ++c) a[c] = a[c + 1];
-        a[m - 1] = a0;
-        asm volatile("bar.sync 1, 64;" ::: "memory");  // prow / cand reuse
+        for (int c = 0; c < 8; ++c) a[m - 8 + c] = r8[c];
     }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
     // A^{-1}[r][c] = X[pivrow[r]][stepof[c]]: the thread of physical row q
     // (r = stepof[q]) writes column pivrow[j] of the inverse from its a[j]
     if (act) {
