@@ -1037,7 +1037,8 @@ struct BInvLevels {
 // (no dynamic register indexing, a short loop): after 56 steps every column
 // is back in place.  Per step: a warp argmax, two 64-thread barriers, the
 // unscaled pivot row through shared memory (every thread scales its own
-// update by f / a_pk).
+// update by f / a_pk); the pivot search is one warp max-reduce (redux) of a
+// packed magnitude / row key per warp.
 // 2 warps and ~150 registers per matrix: ~7 matrices in flight per SM, where
 // the 256-thread [A | I] form (gauss_jordan) is barrier-bound at 3.
 // M: the assembled A (row stride gj_ld(56)); out: inverse, column-major.
@@ -1045,7 +1046,6 @@ __device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M
     constexpr int m = 56, LD = gj_ld(56);
     __shared__ double prow[m];  // the pivot row, unscaled
     __shared__ double pinv;
-    __shared__ double cand_v[2];
     __shared__ int cand_i[2];
     __shared__ int stepof[64], pivrow[m];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -1059,27 +1059,18 @@ __device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M
     for (int k8 = 0; k8 < m / 8; ++k8) {
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-            double v = used ? -1.0 : fabs(a[s]);
-            int idx = used ? 64 : t;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-                if (ov > v || (ov == v && oi < idx)) {
-                    v = ov;
-                    idx = oi;
-                }
-            }
-            if (lane == 0) {
-                cand_v[wid] = v;
-                cand_i[wid] = idx;
-            }
+            // pivot key: the high word of |a_rk| (sign, exponent, 20 mantissa bits:
+            // monotone in |a_rk|) with its 6 low bits replaced by 63 - row, so
+            // one integer max picks the largest magnitude (to 14 mantissa bits)
+            // and the lowest row on ties; used rows bid 0
+            const unsigned hi = (unsigned)(__double_as_longlong(fabs(a[s])) >> 32);
+            const unsigned key = used ? 0u : ((hi & ~63u) | unsigned(63 - t));
+            const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+            if (lane == 0) cand_i[wid] = (int)wmax;
             asm volatile("bar.sync 1, 64;" ::: "memory");
-            const double v1 = cand_v[1];
-            const int i1 = cand_i[1];
-            int p = cand_i[0];
-            if (v1 > cand_v[0] || (v1 == cand_v[0] && i1 < p)) p = i1;
-            if (p >= m || (v1 > cand_v[0] ? v1 : cand_v[0]) == 0.0) {  // no usable pivot: singular
+            const unsigned best = max((unsigned)cand_i[0], (unsigned)cand_i[1]);
+            const int p = 63 - int(best & 63u);
+            if ((best >> 6) == 0u) {  // no nonzero pivot left: singular
                 if (t == 0) atomicOr(err, 2);
                 return;
             }
