@@ -1029,7 +1029,8 @@ struct BInvLevels {
 
 // In-place Gauss-Jordan with partial pivoting, register-resident: 64 threads,
 // thread t < 56 holds row t of the 56 x 56 matrix.  Step k takes the unused
-// row with the largest |a_rk| (lowest index on ties) as pivot row p, scales it
+// row with the largest |a_rk| (to 14 mantissa bits; lowest index on ties) as
+// pivot row p, scales it
 // (a_pk <- 1 / a_pk) and eliminates column k from every other row
 // (a_rk <- -a_rk / a_pk): the in-place inversion of the row-permuted matrix,
 // with no row moved.  Steps run in rounds of 8 with the pivot column at a
