@@ -285,7 +285,7 @@ __device__ void cl_big(const ClLev& C, const DView& W, const DView& B, double* u
                                 if (nc < C.ncol) eslot_issue(*slot, C.SL, nq, gt, kGroup);
                                 cp_async_commit();
                             },
-                            av, nc < C.ncol ? C.SL.Ainv + (size_t)nq * 3136 : nullptr);
+                            av, nc < C.ncol ? C.SL.Ainv + (size_t)nq * 3136 : nullptr, SlabTail{&C.SL, q});
             gsync();
             c = nc;
             k = nk;

@@ -117,7 +117,7 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
                                  if (nc < C.ncol) eslot_issue(slot[g], C.SL, nq, gt, kGroup);
                                  cp_async_commit();
                              },
-                             av, nc < C.ncol ? C.SL.Ainv + (size_t)nq * 3136 : nullptr);
+                             av, nc < C.ncol ? C.SL.Ainv + (size_t)nq * 3136 : nullptr, SlabTail{&C.SL, qq});
                 cc = nc;
                 qq = nq;
             }

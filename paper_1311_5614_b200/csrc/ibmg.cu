@@ -1019,13 +1019,9 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             tr.mark("launched inverses");
             CK(cudaEventSynchronize(c->ev_sizes));
             tr.mark("synced slab sizes");
-            for (int k = 0; k < S.nlev; ++k) {
-                const int mx = hc2[size_t(S.lev[k]) * kCtr + 19];
-                if (mx > kSlabCap)
-                    throw InvalidArg("E' rows of a big block exceed the shared-memory slab (" + std::to_string(mx) +
-                                     " > " + std::to_string(kSlabCap) + " entries) on level " +
-                                     std::to_string(S.lev[k]));
-            }
+            // blocks with more E' entries than a shared-memory slot holds (kSlabCap,
+            // counter 19 = the longest) read the rest from the slab arrays in
+            // global memory (SlabTail): no size limit
             const long stot = hc2[kCtrSlabTot];
             if (stot > c->sl_cap) {
                 dfree(c->sl_col);

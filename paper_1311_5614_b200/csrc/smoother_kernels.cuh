@@ -318,13 +318,34 @@ struct Slabs {
     const double* val;
 };
 
+// The E' entries of block q past kSlabCap (structures denser than ~h/3
+// point spacing give blocks more entries than a shared-memory slot holds)
+// stay in the slab arrays in global memory: a thread whose row runs past the
+// slot adds them after its slot entries, in its own stride class and
+// ascending order (blocks within the slot keep their exact summation order).
+struct SlabTail {
+    const Slabs* SL;  // nullptr: every entry is in the slot
+    int q;
+    template <class LocA>
+    __device__ __forceinline__ double sum(int e0, int e1, int stride, const LocA& wloc) const {
+        double s = 0.0;
+        if (SL == nullptr || e1 <= kSlabCap) return s;
+        const int o = __ldg(SL->off + q);
+        int e = e0;
+        if (e < kSlabCap) e += (kSlabCap - e + stride - 1) / stride * stride;
+        for (; e < e1; e += stride) s += __ldg(SL->val + o + e) * wloc[__ldg(SL->col + o + e)];
+        return s;
+    }
+};
+
 
 __device__ __forceinline__ void slab_issue(SlabSlot& slot, const Slabs& SL, int q, int t, int nt) {
     const char* A = reinterpret_cast<const char*>(SL.Ainv + (size_t)q * 3136);
     char* dA = reinterpret_cast<char*>(slot.A);
     for (int c = t; c < 3136 * 8 / 16; c += nt) cp_async16(dA + 16 * c, A + 16 * c);
     if (t < 12) cp_async16(reinterpret_cast<char*>(slot.rp) + 16 * t, reinterpret_cast<const char*>(SL.rp + (size_t)q * 48) + 16 * t);
-    const int o = SL.off[q], cnt = SL.off[q + 1] - o;
+    // entries past kSlabCap stay in global memory (slab_entry)
+    const int o = SL.off[q], cnt = min(SL.off[q + 1] - o, kSlabCap);
     const char* cv = reinterpret_cast<const char*>(SL.val + o);
     const char* cc = reinterpret_cast<const char*>(SL.col + o);
     for (int c = t; c < cnt / 2; c += nt) cp_async16(reinterpret_cast<char*>(slot.val) + 16 * c, cv + 16 * c);
@@ -339,7 +360,8 @@ __device__ __forceinline__ void slab_issue(SlabSlot& slot, const Slabs& SL, int 
 template <class WA, class LocA, class GlobA, class BA, class WAdd>
 __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slot, int bi, int bj, const WA& W,
                                                const LocA& wloc, const GlobA& wglob, const BA& Bv, WAdd&& wadd,
-                                               BigScratch& S, int gt, unsigned long long* dbg = nullptr) {
+                                               BigScratch& S, int gt, unsigned long long* dbg = nullptr,
+                                               SlabTail tail = SlabTail{nullptr, 0}) {
     // stencil row and E' row dots are computed into registers first and
     // stored after both, so their global gathers are in flight together (one
     // L2 round trip for the residual instead of two)
@@ -356,7 +378,7 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
     // gathers in flight per thread, fixed-order combine
     if (gt < 120) {
         const int r = gt % 40, p = gt / 40;
-        const int e1 = slot.rp[r + 1];
+        const int e1 = min(slot.rp[r + 1], kSlabCap);
         for (int e = slot.rp[r] + p; e < e1; e += 72) {  // one round of up to 24 gathers per thread
             int cc[24];
             double vv[24], xx[24];
@@ -372,6 +394,7 @@ __device__ __forceinline__ void big_block_slab(const Lev& L, const SlabSlot& slo
 #pragma unroll
             for (int m = 0; m < 24; ++m) s0 += vv[m] * xx[m];
         }
+        s0 += tail.sum(slot.rp[r] + p, slot.rp[r + 1], 3, wloc);
     }
     if (gt < 56) {
         S.sr[gt] = sres;
@@ -414,7 +437,8 @@ static_assert(sizeof(ESlot) % 16 == 0, "slot alignment");
 
 __device__ __forceinline__ void eslot_issue(ESlot& slot, const Slabs& SL, int q, int t, int nt) {
     if (t < 12) cp_async16(reinterpret_cast<char*>(slot.rp) + 16 * t, reinterpret_cast<const char*>(SL.rp + (size_t)q * 48) + 16 * t);
-    const int o = SL.off[q], cnt = SL.off[q + 1] - o;
+    // entries past kSlabCap stay in global memory (slab_entry)
+    const int o = SL.off[q], cnt = min(SL.off[q + 1] - o, kSlabCap);
     const char* cv = reinterpret_cast<const char*>(SL.val + o);
     const char* cc = reinterpret_cast<const char*>(SL.col + o);
     for (int c = t; c < cnt / 2; c += nt) cp_async16(reinterpret_cast<char*>(slot.val) + 16 * c, cv + 16 * c);
@@ -450,7 +474,8 @@ template <int EDOT = 0, class WA, class LocA, class BA, class WAdd, class Sync, 
 __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, const double* __restrict__ A_q, int bi,
                                              int bj, const WA& W, const LocA& wloc, const BA& Bv, WAdd&& wadd,
                                              BigScratch& S, int gt, Sync&& gsync, After after_rows = After{},
-                                             double* avp = nullptr, const double* __restrict__ A_next = nullptr) {
+                                             double* avp = nullptr, const double* __restrict__ A_next = nullptr,
+                                             SlabTail tail = SlabTail{nullptr, 0}) {
     double avl[28];
     double (&av)[28] = avp ? *reinterpret_cast<double(*)[28]>(avp) : avl;
     const int row = gt % 56, cg = gt / 56;
@@ -465,7 +490,7 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
     }
     if (EDOT == 0 && gt < 120) {  // E' row dots: 3 threads per row, 24 gathers per round
         const int r = gt % 40, p = gt / 40;
-        const int e1 = slot.rp[r + 1];
+        const int e1 = min(slot.rp[r + 1], kSlabCap);
         double s0 = 0.0;
         for (int e = slot.rp[r] + p; e < e1; e += 72) {  // one round of up to 24 gathers per thread
             double vv[24], xx[24];
@@ -478,11 +503,11 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
 #pragma unroll
             for (int m = 0; m < 24; ++m) s0 += vv[m] * xx[m];
         }
-        S.epart[p][r] = s0;
+        S.epart[p][r] = s0 + tail.sum(slot.rp[r] + p, slot.rp[r + 1], 3, wloc);
     }
     if (EDOT == 1 && gt >= 64 && gt < 104) {  // E' row dots: one thread per row
         const int r = gt - 64;
-        const int e1 = slot.rp[r + 1];
+        const int e1 = min(slot.rp[r + 1], kSlabCap);
         double s0 = 0.0, s1 = 0.0;
         for (int e = slot.rp[r]; e < e1; e += 8) {
             double vv[8], xx[8];
@@ -498,7 +523,7 @@ __device__ __forceinline__ void big_block_es(const Lev& L, const ESlot& slot, co
                 s1 += vv[m + 1] * xx[m + 1];
             }
         }
-        S.epart[0][r] = s0 + s1;
+        S.epart[0][r] = (s0 + s1) + tail.sum(slot.rp[r], slot.rp[r + 1], 1, wloc);
     }
     gsync();
     after_rows();
@@ -630,7 +655,8 @@ __global__ void __launch_bounds__(kBigThreads) k_big_phase(Lev L, Slabs SL, BigC
                      [&] {
                          if (nc < BC.ncol) eslot_issue(slot[0], SL, nq, t, kBigThreads);
                          cp_async_commit();
-                     });
+                     },
+                     nullptr, nullptr, SlabTail{&SL, q});
         __syncthreads();
         if (t == 0 && DP.flags) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag
             st_release(DP.flags + q, DP.epoch);
@@ -868,10 +894,12 @@ __global__ void __launch_bounds__(32 * kDfWarps, ES ? 2 : 1) k_sweep_df(DfArgs A
                             [&] {
                                 if (nc < A.BC.ncol) eslot_issue(*eslot, A.SL, nq, t, 32 * kDfWarps);
                                 cp_async_commit();
-                            });
+                            },
+                            nullptr, nullptr, SlabTail{&A.SL, q});
         } else {
             unsigned long long* dbgp = A.trace ? A.trace + 6 * ntiles + 9 * q + 6 : nullptr;
-            big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg, wadd, S, t, dbgp);
+            big_block_slab(L, slot[k & 1], bi, bj, Wg, FlatCG{A.w}, FlatCG{A.w}, Bg, wadd, S, t, dbgp,
+                           SlabTail{&A.SL, q});
         }
         __syncthreads();
         if (t == 0) {  // bar.sync + st.release.gpu order the CTA's w stores before the flag

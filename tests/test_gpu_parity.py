@@ -263,3 +263,4 @@ def test_invalid_arguments_raise_value_error():
         g.set_structures([2], [1.0], [0.01], np.zeros((2, 2)))  # FiberMesh: m1 >= 3
     with pytest.raises(ValueError):
         g.sweep(np.zeros(3 * 64 * 64), np.zeros(3 * 64 * 64), level=3)  # coarse-kernel level
+
