@@ -70,6 +70,7 @@ inline long grow_cap(long need, long cap) { return std::max<long>(need + need / 
 
 constexpr int kMaxColours = 32;
 constexpr int kDataflowMaxN = 512;  // levels swept by the single dataflow kernel
+constexpr int kDfEsMinBig = 512;    // auto: E'-row-slot dataflow sweep from this many big blocks
 static_assert(kMaxColours == kClMaxColours, "cluster kernel colour table");
 
 struct LevelBuf {
@@ -199,14 +200,17 @@ struct ibmg_ctx {
     bool rr_csr = true;     // ... with E' from the assembled rows on point-dense levels (IBMG_RR_CSR=0: off)
     bool ap_tiled = true;   // tiled operator apply where n >= 64 (IBMG_AP_TILED=0: off)
     bool ortho2 = true;     // FGMRES with the two-pass lagged CGS2 (IBMG_CGS2=1: three-sweep CGS2)
-    int canon_inv = -1;     // box inverses in block-id order during the colouring: default on
-                            // (single contexts), IBMG_CANON_INV=0 off
+    int canon_inv = -1;     // box inverses in block-id order during the colouring: -1 auto (>= 2^15
+                            // blocks over all levels, single contexts), IBMG_CANON_INV=1 on, 0 off
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
     bool gj_regs = true;    // box inverses: 64-thread register Gauss-Jordan (IBMG_GJ256=1: 256-thread [A|I] form)
-    bool spec_full = true;  // FGMRES: whole next V-cycle enqueued behind the dots (IBMG_SPEC=0: first sweep only)
-    bool df_es = true;      // dataflow sweep with the E'-row slot + register inverse, 2 CTAs/SM (IBMG_DF_ES=0: slab slots)
+    bool spec_full = false; // FGMRES: whole next V-cycle enqueued behind the dots (IBMG_SPEC=1); measured no gain
+                            // (C3 19.9 ms either way, C2 6.23 vs 6.17): default = its first sweep only
+    int df_es = -1;         // dataflow sweep with the E'-row slot + register inverse, 2 CTAs/SM: -1 auto
+                            // (levels with >= kDfEsMinBig big blocks), IBMG_DF_ES=1 every level, 0 none
+    int df_grid_max_es = 1; // its co-resident CTAs
     int pdf_grid_max = 1;   // co-resident CTAs of the band-major plain dataflow phase
     bool plain_df = true;   // n > 512: band-major plain dataflow launch (IBMG_PLAIN_DF=0: 4 tile-colour launches)
     int pdf_skew = 0;       // its band skew in steps (0: from the grid; IBMG_PDF_SKEW)
@@ -710,9 +714,11 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
     bool coarse_forked = false, side_used = false;
     // canonical-order box inverses: single contexts (slab contexts invert
     // their own rows only) with the option on
-    // (measured faster at every size: C3 21.1 -> 20.1 ms, C2 6.14 -> 6.10 ms per
-    // step, C4 auto-on since round 1; IBMG_CANON_INV=0 turns it off)
-    const bool canon = c->canon_inv != 0 && c->own_y0.empty();
+    // auto: on from 2^15 blocks over all levels (C3 21.1 -> 20.1 ms, C4 since
+    // round 1; on C2, 5.5k blocks, the extra passes cost ~1%: off);
+    // IBMG_CANON_INV=0/1 forces it
+    const bool canon = c->canon_inv != 0 && c->own_y0.empty() &&
+                       (c->canon_inv > 0 || c->blk_levels.boff[c->blk_levels.nlev] >= (1 << 15));
     CK(cudaMemsetAsync(c->err_flag, 0, sizeof(int), c->s));
     CK(cudaMemsetAsync(c->counters, 0, sizeof(int) * c->nlev * kCtr, c->s));
     if (npts == 0) {
@@ -1246,8 +1252,13 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
         // latency regime: the whole sweep as one dataflow kernel
         DfArgs A{L, SL, BC, BigDeps{lb.pred, lb.poff, lb.flags, ++lb.epoch}, lb.tflags, lb.big, b, w, c->trace};
         if (c->prof) prof_begin(c, "k_sweep_df");
-        const dim3 grid(c->grid_limit > 0 ? std::min(c->grid_limit, c->df_grid_max) : c->df_grid_max);
-        if (c->df_es) launch_k(c, k_sweep_df<true>, grid, dim3(32 * kDfWarps), kDfSmemES, true, A);
+        // the E'-row-slot variant (2 CTAs/SM) pays where big blocks outnumber one
+        // CTA per SM (C3 level 512: 68 -> 57 us per sweep); on levels with fewer
+        // the slab-slot variant's shorter block latency wins (C2: 6.39 vs 6.24 ms)
+        const bool es = c->df_es > 0 || (c->df_es < 0 && lb.nbig >= kDfEsMinBig);
+        const int gmax = es ? c->df_grid_max_es : c->df_grid_max;
+        const dim3 grid(c->grid_limit > 0 ? std::min(c->grid_limit, gmax) : gmax);
+        if (es) launch_k(c, k_sweep_df<true>, grid, dim3(32 * kDfWarps), kDfSmemES, true, A);
         else launch_k(c, k_sweep_df<false>, grid, dim3(32 * kDfWarps), kDfSmem, true, A);
         if (c->prof) prof_end(c);
         ++c->launches;
@@ -1945,7 +1956,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_PDF_SKEW")) c->pdf_skew = std::atoi(e);
     if (const char* e = std::getenv("IBMG_DF_MAXN")) c->df_maxn = std::atoi(e);
-    if (const char* e = std::getenv("IBMG_DF_ES")) c->df_es = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_DF_ES")) c->df_es = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("IBMG_SPEC")) c->spec_full = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_GJ256")) c->gj_regs = std::atoi(e) == 0;
     c->prm = *p;
@@ -1973,10 +1984,9 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             c->pp_grid_max = std::max(1, per_sm * sms);
             CK(cudaFuncSetAttribute(k_sweep_df<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmem)));
             CK(cudaFuncSetAttribute(k_sweep_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDfSmemES)));
-            if (c->df_es)
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<true>, 32 * kDfWarps, kDfSmemES));
-            else
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<false>, 32 * kDfWarps, kDfSmem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<true>, 32 * kDfWarps, kDfSmemES));
+            c->df_grid_max_es = std::max(1, per_sm * sms);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_df<false>, 32 * kDfWarps, kDfSmem));
             c->df_grid_max = std::max(1, per_sm * sms);
             CK(cudaFuncSetAttribute(k_canon_inverse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     56 * gj_ld(56) * 8));
