@@ -224,19 +224,17 @@ def profile_pass(ctxs, states_reset, sched):
     """Live per-kernel CUDA-event timing (ibmg_profile) over the steps of
     `sched`; returns ({kernel: [ms, launches]}, per-step iterations, restarts)."""
     prof_tot, step_iters, prs = {}, [], 0
-    for c in ctxs:
-        c.profile(True)
     for kb, si in sched:
         u, p, X = states_reset(kb, si)
+        ctxs[kb].profile(True)  # per step: "(idle)" is the device gap inside a step only
         st = ctxs[kb].step_implicit(u, p, X)
-        step_iters.append(st["iters"])
-        prs += st["restarts"]
-    for c in ctxs:
-        for k, (tms, cnt) in c.profile_report().items():
+        for k, (tms, cnt) in ctxs[kb].profile_report().items():
             a = prof_tot.setdefault(k, [0.0, 0])
             a[0] += tms
             a[1] += cnt
-        c.profile(False)
+        ctxs[kb].profile(False)
+        step_iters.append(st["iters"])
+        prs += st["restarts"]
     return prof_tot, step_iters, prs
 
 
