@@ -128,8 +128,9 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
     cmark(tr, nm);  // big phase done
 }
 
-__global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
-    pdl_enter();
+// The body of one coarse cycle (A in parameter space, or one problem's
+// arguments in global memory for the batched kernel, batch.cuh).
+__device__ __forceinline__ void coarse_cycle_body(const CoarseArgs& A) {
     extern __shared__ __align__(16) unsigned char dsm[];
     ESlot* slot = reinterpret_cast<ESlot*>(dsm);
     double* sm = reinterpret_cast<double*>(dsm + (kCoarseThreads / kGroup) * sizeof(ESlot));
@@ -224,6 +225,11 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
         }
     }
     cmark(A.trace, nm);
+}
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
+    pdl_enter();
+    coarse_cycle_body(A);
 }
 
 }  // namespace ibmg

@@ -99,10 +99,10 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
-// Dispatch of a fused launch; `grid(b)` runs grid CTA b.
+// Dispatch of a fused launch; `grid(b)` runs grid CTA b.  bid: this CTA's
+// index in the launch (blockIdx.x; the batched kernels pass their own).
 template <class GridFn>
-__device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, int ngrid, GridFn&& grid) {
-    const int bid = blockIdx.x;
+__device__ __forceinline__ void fused_launch_at(const PForce& pf, const Gather& G, int ngrid, int bid, GridFn&& grid) {
     if (bid >= pf.nblk + ngrid) {  // gather CTA
         if (threadIdx.x == 0)
             while (ld_acquire_u64(G.cnt) < G.target) __nanosleep(32);
@@ -127,6 +127,10 @@ __device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, 
             atomicAdd(G.cnt, 1ull);
         }
     }
+}
+template <class GridFn>
+__device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, int ngrid, GridFn&& grid) {
+    fused_launch_at(pf, G, ngrid, (int)blockIdx.x, grid);
 }
 
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
@@ -478,13 +482,12 @@ struct ERes {
     unsigned long long* cnt;    // monotone per-context counter
     unsigned long long target;  // its value once this launch's row CTAs are done
 };
-__global__ void __launch_bounds__(256) k_residual_restrict_e(Lev F, const double* __restrict__ b,
-                                                             const double* __restrict__ w, double* __restrict__ bc,
-                                                             double* __restrict__ wc_zero, ERes R, int q0, int q1) {
-    __shared__ __align__(16) RrSmem S;
-    pdl_enter();
-    if ((int)blockIdx.x < R.nblk) {
-        const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+__device__ __forceinline__ void residual_restrict_e_at(const Lev& F, const double* __restrict__ b,
+                                                       const double* __restrict__ w, double* __restrict__ bc,
+                                                       double* __restrict__ wc_zero, const ERes& R, int q0, int q1,
+                                                       int bid, RrSmem& S) {
+    if (bid < R.nblk) {
+        const int row = bid * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
         if (row < R.FL.nf) {
             double s = 0.0;
             for (int k = R.E.rp[row] + lane; k < R.E.rp[row + 1]; k += 32) s += R.E.val[k] * w[R.E.col[k]];
@@ -501,7 +504,14 @@ __global__ void __launch_bounds__(256) k_residual_restrict_e(Lev F, const double
     if (threadIdx.x == 0)
         while (ld_acquire_u64(R.cnt) < R.target) __nanosleep(32);
     __syncthreads();
-    residual_restrict_tile(F, b, w, bc, wc_zero, blockIdx.x - R.nblk, q0, q1, S, R.e);
+    residual_restrict_tile(F, b, w, bc, wc_zero, bid - R.nblk, q0, q1, S, R.e);
+}
+__global__ void __launch_bounds__(256) k_residual_restrict_e(Lev F, const double* __restrict__ b,
+                                                             const double* __restrict__ w, double* __restrict__ bc,
+                                                             double* __restrict__ wc_zero, ERes R, int q0, int q1) {
+    __shared__ __align__(16) RrSmem S;
+    pdl_enter();
+    residual_restrict_e_at(F, b, w, bc, wc_zero, R, q0, q1, (int)blockIdx.x, S);
 }
 
 // Plain restriction of a vector (ibmg_restrict).
@@ -702,11 +712,13 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
 // 3 CTAs per SM (2 for KMAX 32) of 256 threads: room for the unrolled loads
 template <int KMAX>
 constexpr int ortho_dots_blocks() { return KMAX > 16 ? 2 * 148 : 3 * 148; }
+// bid / nb: this CTA's index and the CTA count of the pass (bid and
+// nb; the batched kernel passes its own)
 template <int KMAX>
-__global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
-    k_ortho_dots(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ w, size_t m,
-                 double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
-    pdl_enter();
+__device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size_t stride, int k,
+                                              const double* __restrict__ w, size_t m, double* __restrict__ partial,
+                                              double* __restrict__ dh, int ld, unsigned* __restrict__ ticket, int bid,
+                                              int nb) {
     constexpr int KH = KMAX / 2;  // i-range per thread half
     __shared__ double red[kRedThreads / 32][2 * KH];
     __shared__ double fin[2 * KMAX];
@@ -721,8 +733,8 @@ __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
     double aw[KH], aq[KH];
 #pragma unroll
     for (int i = 0; i < KH; ++i) aw[i] = aq[i] = 0.0;
-    const size_t step = (size_t)gridDim.x * 128;
-    for (size_t q0 = (size_t)blockIdx.x * 128 + th; q0 < m; q0 += step * UNR) {
+    const size_t step = (size_t)nb * 128;
+    for (size_t q0 = (size_t)bid * 128 + th; q0 < m; q0 += step * UNR) {
         double x[UNR], qq[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -764,18 +776,18 @@ __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
         const int which = d / k, i = d - which * k, hh = i / kh, sl = i - hh * kh;
         double t = 0.0;
         for (int ww = 4 * hh; ww < 4 * hh + 4; ++ww) t += red[ww][which * KH + sl];
-        partial[(size_t)d * gridDim.x + blockIdx.x] = t;
+        partial[(size_t)d * nb + bid] = t;
     }
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == nb - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
     for (int d = wid; d < 2 * k; d += kRedThreads / 32) {
         double t = 0.0;
-        for (int x = lane; x < (int)gridDim.x; x += 32) t += __ldcg(partial + (size_t)d * gridDim.x + x);
+        for (int x = lane; x < (int)nb; x += 32) t += __ldcg(partial + (size_t)d * nb + x);
         t = warp_sum(t);
         if (lane == 0) fin[d] = t;
     }
@@ -815,11 +827,19 @@ __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
 }
 
 template <int KMAX>
-__global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
-    k_ortho_update(double* __restrict__ V, size_t stride, int k, const double* __restrict__ w,
-                   double* __restrict__ w1out, double* __restrict__ zero, size_t m, double* __restrict__ partial,
-                   double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
+__global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
+    k_ortho_dots(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ w, size_t m,
+                 double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
     pdl_enter();
+    ortho_dots_at<KMAX>(V, stride, k, w, m, partial, dh, ld, ticket, (int)blockIdx.x, (int)gridDim.x);
+}
+
+template <int KMAX>
+__device__ __forceinline__ void ortho_update_at(double* __restrict__ V, size_t stride, int k,
+                                                const double* __restrict__ w, double* __restrict__ w1out,
+                                                double* __restrict__ zero, size_t m, double* __restrict__ partial,
+                                                double* __restrict__ dh, int ld, unsigned* __restrict__ ticket, int bid,
+                                                int nb) {
     __shared__ double as[KMAX], cs[KMAX];
     __shared__ double red[kRedThreads / 32];
     if (threadIdx.x < KMAX) {
@@ -831,7 +851,7 @@ __global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
     const double inu = dh[5 * ld], sq = dh[5 * ld + 1];
     double* qv_ptr = V + stride * (k - 1);
     double acc = 0.0;
-    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x) {
+    for (size_t q = (size_t)bid * blockDim.x + threadIdx.x; q < m; q += (size_t)nb * blockDim.x) {
         double v[KMAX];
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) v[i] = (i < k - 1) ? __ldcs(V + stride * i + q) : 0.0;
@@ -855,22 +875,31 @@ __global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int ww = 0; ww < kRedThreads / 32; ++ww) t += red[ww];
-        partial[blockIdx.x] = t;
+        partial[bid] = t;
     }
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == nb - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
     if (wid == 0) {
         double t = 0.0;
-        for (int x = lane; x < (int)gridDim.x; x += 32) t += __ldcg(partial + x);
+        for (int x = lane; x < (int)nb; x += 32) t += __ldcg(partial + x);
         t = warp_sum(t);
         if (lane == 0) dh[5 * ld + 4] = t;
     }
     if (threadIdx.x == 0) *ticket = 0u;
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kRedThreads, 4 / (KMAX > 16 ? 2 : 1))
+    k_ortho_update(double* __restrict__ V, size_t stride, int k, const double* __restrict__ w,
+                   double* __restrict__ w1out, double* __restrict__ zero, size_t m, double* __restrict__ partial,
+                   double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
+    pdl_enter();
+    ortho_update_at<KMAX>(V, stride, k, w, w1out, zero, m, partial, dh, ld, ticket, (int)blockIdx.x, (int)gridDim.x);
 }
 
 // w -= sum_{i<k} h[i] V_i   (one pass over w and the V's).
