@@ -504,6 +504,71 @@ def run_batch(args, rank, world):
             "clocks": clk.summary(), "workers": W, "warmup_problems": len(mine)}
 
 
+def run_batch_lockstep(args, rank, world):
+    """C5 through the lockstep batch (ibmg_batch_*): this rank's
+    problems in chunks of `slots`, sorted by kappa (similar iteration counts
+    keep the lockstep rounds full); per chunk: set_structures per slot, then one
+    batched step.  Device arrays for the value, host arrays for e2e; wall clock
+    around host-synchronous steps (every step returns after its results are
+    back), max over ranks."""
+    import torch
+    from paper_1311_5614_b200 import configs
+    from paper_1311_5614_b200 import dist as D
+    from paper_1311_5614_b200.ibmg import BatchSystem
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    mine = D.shard(args.batch, rank, world)
+    probs = {i: configs.config5_problem(i) for i in mine}
+    order = sorted(mine, key=lambda i: probs[i].kappa[0])
+    S = max(1, min(args.slots, len(order)))
+    B = BatchSystem(256, S, 1.0, 1.0, 1e-3, device=dev)
+    n2 = 256 * 256
+    Dv = f"cuda:{dev}"
+
+    def run(host, sub):
+        if host:
+            us = [np.zeros(2 * n2) for _ in range(S)]
+            ps = [np.zeros(n2) for _ in range(S)]
+        else:
+            us = [torch.zeros(2 * n2, dtype=torch.float64, device=Dv) for _ in range(S)]
+            ps = [torch.zeros(n2, dtype=torch.float64, device=Dv) for _ in range(S)]
+        res = []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for c0 in range(0, len(sub), S):
+            chunk = sub[c0:c0 + S]
+            Xs = []
+            for k, i in enumerate(chunk):
+                pr = probs[i]
+                B.set_structures(k, pr.nb, pr.kappa, pr.ds, pr.X)
+                if host:
+                    us[k][:] = 0.0
+                    Xs.append(pr.X.reshape(-1).copy())
+                else:
+                    us[k].zero_()
+                    Xs.append(torch.tensor(pr.X.reshape(-1), dtype=torch.float64, device=Dv))
+            sts = B.step_implicit(us[:len(chunk)], ps[:len(chunk)], Xs)
+            res += [(i, st["iters"], bool(st["converged"])) for i, st in zip(chunk, sts)]
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3, res
+
+    run(False, order[:S])  # warm-up: one chunk
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = B.kernel_launches
+    with ClockSampler(dev) as clk:
+        ms, res = run(False, order)
+    launches = B.kernel_launches - launches0
+    e2e_ms, _ = run(True, order)
+    tmax, tsum, tmin = D.reduce_stats([ms, e2e_ms, len(res), sum(r[1] for r in res), all(r[2] for r in res)],
+                                      device=Dv)
+    B.close()
+    return {"ms": float(tmax[0]), "e2e_ms": float(tmax[1]), "nprob": float(tsum[2]), "vcyc": float(tsum[3]),
+            "conv": bool(tmin[4]), "launches": launches, "clocks": clk.summary(), "workers": S,
+            "warmup_problems": min(S, len(order))}
+
+
 def cpu_oracle_steps(steps_sched, threads):
     """The oracle on a schedule of (block, step index in block), one trajectory
     state per block (as the GPU arm)."""
@@ -548,7 +613,10 @@ def main():
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 one-GPU secondary measurement")
     ap.add_argument("--batch", type=int, default=512, help="C5: number of independent N=256 problems")
     ap.add_argument("--ctx-grid", type=int, default=0, help="C5: CTA cap per context (0: 2 x SMs / workers)")
-    ap.add_argument("--workers", type=int, default=10, help="C5: concurrent solver contexts per GPU (8-12 measured best on B200, 16 host cores)")
+    ap.add_argument("--workers", type=int, default=10, help="C5 --c5-mode contexts: concurrent solver contexts per GPU (8-12 measured best on B200, 16 host cores)")
+    ap.add_argument("--c5-mode", default="batch", choices=["batch", "contexts"],
+                    help="C5: lockstep batch (ibmg_batch_*) or concurrent single-problem contexts")
+    ap.add_argument("--slots", type=int, default=32, help="C5 --c5-mode batch: problems per lockstep batch")
     ap.add_argument("--slabs", type=int, default=0,
                     help="C3/C4: slab-partition the problem (DESIGN.md §7): P slabs over the visible GPUs in this "
                          "process (P2P-fused exchange), or under torchrun one slab per rank over NCCL")
@@ -702,8 +770,10 @@ def main_batch(args):
     threads = os.cpu_count() or 1
     desc = (f"C5: batch of {args.batch} independent problems, periodic N=256 fp64, one ellipse each (seed 5+i, "
             "semi-axes U[0.1,0.35], Nb=512, kappa 10^U[1,6]), dt=1e-3, one implicit step each, FGMRES(30)+V(1,1)")
-    cfg = {"workload": desc, "name": "C5", "N": 256, "batch": args.batch, "dof": 3 * 256 * 256,
-           "parallelism": f"batch sharded over {world} GPU(s) (replicas), {args.workers} concurrent contexts/GPU"}
+    cfg = {"workload": desc, "name": "C5", "N": 256, "batch": args.batch, "dof": 3 * 256 * 256}
+    par = (f"batch sharded over {world} GPU(s) (replicas), " +
+           (f"lockstep batches of {args.slots} problems/GPU (ibmg_batch)" if args.c5_mode == "batch"
+            else f"{args.workers} concurrent contexts/GPU"))
     if args.impl == "reference":
         if rank != 0:
             return
@@ -721,7 +791,8 @@ def main_batch(args):
         print(json.dumps({"metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
                           "steps": sample, "warmup": 0, "ms_per_step": round(v, 3), "higher_is_better": False,
                           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                          "impl": "reference", "config": cfg, "problems_per_s": 1e3 / v,
+                          "impl": "reference", "config": cfg, "parallelism": f"CPU oracle port ({threads} threads)",
+                          "problems_per_s": 1e3 / v,
                           "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "port",
                                            "sample": f"{sample} C5 problems (oracle port, ms per problem)"},
                           "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0,
@@ -732,13 +803,13 @@ def main_batch(args):
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
-    r = run_batch(args, rank, world)
+    r = run_batch_lockstep(args, rank, world) if args.c5_mode == "batch" else run_batch(args, rank, world)
     if rank == 0:
         ms_per = r["ms"] / r["nprob"]
         line = {"metric": METRIC, "value": round(ms_per, 4), "unit": "ms", "n_gpus": world,
                 "steps": int(r["nprob"]), "warmup": r["warmup_problems"], "ms_per_step": round(ms_per, 4),
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded C5 geometry)", "config": cfg,
+                "data": "synthetic (seeded C5 geometry)", "config": cfg, "parallelism": par,
                 "problems_per_s": r["nprob"] / (r["ms"] * 1e-3),
                 "dof_vcycles_per_s": 3 * 256 * 256 * r["vcyc"] / (r["ms"] * 1e-3),
                 "vcycles_per_problem": r["vcyc"] / r["nprob"], "converged": r["conv"],

@@ -215,6 +215,30 @@ int ibmg_group_vcycle(ibmg_group* group, const double* b, double* z);
 int ibmg_group_solve(ibmg_group* group, const double* b, double* x, ibmg_stats* stats);
 int ibmg_group_step(ibmg_group* group, double* u, double* p, double* X, ibmg_stats* stats);
 
+/* ---- Batch of independent problems stepped in lockstep (C5).
+ * No reference counterpart (the reference solves one system per call): the
+ * batch takes the reference's step_implicit for `count`
+ * problems at once.  nslots contexts of one grid size (64 <= N <= 512); every
+ * slot gets its own structures; ibmg_batch_step runs the rebuilds per slot
+ * and then ONE launch per smoother / transfer / Krylov phase for all slots
+ * (tile and block tasks of all problems in one dataflow DAG, the problem index
+ * in the grid), FGMRES advancing every unconverged problem one Arnoldi step
+ * per round.  Results equal the single-context step's (same arithmetic per
+ * problem). */
+typedef struct ibmg_batch ibmg_batch;
+int ibmg_batch_create(const ibmg_params* params, int nslots, ibmg_batch** out);
+void ibmg_batch_destroy(ibmg_batch* batch);
+const char* ibmg_batch_last_error(const ibmg_batch* batch);
+long long ibmg_batch_kernel_launches(const ibmg_batch* batch);
+void* ibmg_batch_stream(const ibmg_batch* batch);
+/* As ibmg_set_structures for slot `slot` (host arrays; the rebuild happens in the step). */
+int ibmg_batch_set_structures(ibmg_batch* batch, int slot, int n_mem, const int* nb, const double* kappa,
+                              const double* ds, const double* X);
+/* One implicit step of slots 0..count-1: u[k] (2N^2 in/out), p[k] (N^2 out), X[k]
+ * (in/out), host or device pointers; stats[k] per problem (may be NULL). */
+int ibmg_batch_step(ibmg_batch* batch, int count, double* const* u, double* const* p, double* const* X,
+                    ibmg_stats* stats, int ptr_kind);
+
 #ifdef __cplusplus
 }
 #endif

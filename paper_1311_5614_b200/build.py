@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libibmg_b200.so")
 SRCS = ["ibmg.cu"]
-DEPS = ["ibmg.cu", "common.cuh", "cluster_kernel.cuh", "grid_kernels.cuh", "ib_kernels.cuh", "smoother_kernels.cuh", "coarse_kernel.cuh",
+DEPS = ["ibmg.cu", "common.cuh", "cluster_kernel.cuh", "batch.cuh", "grid_kernels.cuh", "ib_kernels.cuh", "smoother_kernels.cuh", "coarse_kernel.cuh",
         "slab_group.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]

@@ -130,7 +130,7 @@ __device__ void coarse_sweep(const CLev& C, double* w, const double* b, ESlot* s
 
 // The body of one coarse cycle (A in parameter space, or one problem's
 // arguments in global memory for the batched kernel, batch.cuh).
-__device__ __forceinline__ void coarse_cycle_body(const CoarseArgs& A) {
+__device__ __forceinline__ void coarse_cycle_body(const CoarseArgs& A, double* w_fine) {
     extern __shared__ __align__(16) unsigned char dsm[];
     ESlot* slot = reinterpret_cast<ESlot*>(dsm);
     double* sm = reinterpret_cast<double*>(dsm + (kCoarseThreads / kGroup) * sizeof(ESlot));
@@ -213,15 +213,15 @@ __device__ __forceinline__ void coarse_cycle_body(const CoarseArgs& A) {
         for (int s = 0; s < A.nu2; ++s) coarse_sweep(C, wl[l], bl[l], slot, S, A.trace, nm);
     }
     for (int q = t; q < 3 * A.lv[0].L.nn; q += nt) A.w_out[q] = wl[0][q];
-    if (A.w_fine) {  // prolongation-add to the finer level (K3) from shared memory
+    if (w_fine) {  // prolongation-add to the finer level (K3) from shared memory
         const int nf = 2 * A.lv[0].L.n, nnf = nf * nf;
         SW E{wl[0], A.lv[0].L.n, A.lv[0].L.nn};
         for (int q = t; q < nnf; q += nt) {
             double du, dv, dp;
             prolong_rows(nf, E, q % nf, q / nf, du, dv, dp);
-            A.w_fine[q] += du;
-            A.w_fine[nnf + q] += dv;
-            A.w_fine[2 * nnf + q] += dp;
+            w_fine[q] += du;
+            w_fine[nnf + q] += dv;
+            w_fine[2 * nnf + q] += dp;
         }
     }
     cmark(A.trace, nm);
@@ -229,7 +229,7 @@ __device__ __forceinline__ void coarse_cycle_body(const CoarseArgs& A) {
 
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_cycle(CoarseArgs A) {
     pdl_enter();
-    coarse_cycle_body(A);
+    coarse_cycle_body(A, A.w_fine);
 }
 
 }  // namespace ibmg

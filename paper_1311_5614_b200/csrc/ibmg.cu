@@ -193,6 +193,7 @@ struct ibmg_ctx {
     std::vector<double> h_kappa, h_ds, h_X;
     size_t Mst = 0;            // padded stride of the Krylov basis vectors
     bool have_structs = false;
+    bool built_dirty = false;  // ibmg_set_structures deferred the rebuild to the next call that needs it
     int big_grid_max = 1;   // co-resident CTAs of the cooperative big phase
     int pp_grid_max = 1;    // co-resident CTAs of the persistent plain phase
     bool tiles_pp = true;   // persistent double-buffered plain phase (IBMG_TILES_PP=0: one CTA per tile)
@@ -1081,7 +1082,7 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
 }
 
 void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, const double* ds, const double* X,
-                    int ptr_kind) {
+                    int ptr_kind, bool defer = false) {
     if (n_mem < 0) throw InvalidArg("n_mem must be >= 0");
     std::vector<int> hnb(nb, nb + n_mem);
     std::vector<double> hk(kappa, kappa + n_mem), hds(ds, ds + n_mem);
@@ -1157,7 +1158,11 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
         CK(cudaMemcpyAsync(c->X, X, sizeof(double) * 2 * tot,
                            ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
     CK(cudaStreamSynchronize(c->s));
-    rebuild(c);
+    // deferred (single contexts): ibmg_step rebuilds at X^n anyway, so a
+    // set_structures + step pair (a batch of problems through one context)
+    // builds once; any other call builds first (ensure_built)
+    if (defer) c->built_dirty = true;
+    else rebuild(c);
     c->have_structs = true;
     c->h_nb = hnb;
     c->h_kappa = hk;
@@ -1881,6 +1886,13 @@ void build_rhs(ibmg_ctx* c, const double* u, double* b) {
 }
 
 // ---------------- host/device staging for the C ABI ----------------
+// The per-step operators of the current structures (deferred by ibmg_set_structures).
+void ensure_built(ibmg_ctx* c) {
+    if (!c->built_dirty) return;
+    c->built_dirty = false;
+    rebuild(c);
+}
+
 // Order the caller's device-pointer inputs before this context's stream.
 void wait_inputs(ibmg_ctx* c, int kind) {
     if (kind != IBMG_PTR_DEVICE) return;
@@ -1891,7 +1903,10 @@ void wait_inputs(ibmg_ctx* c, int kind) {
 struct Stage {
     ibmg_ctx* c;
     int kind;
-    Stage(ibmg_ctx* c_, int kind_) : c(c_), kind(kind_) { wait_inputs(c, kind); }
+    Stage(ibmg_ctx* c_, int kind_) : c(c_), kind(kind_) {
+        ensure_built(c);
+        wait_inputs(c, kind);
+    }
     const double* in(const double* p, size_t n, double* buf) {
         if (kind == IBMG_PTR_DEVICE) return p;
         CK(cudaMemcpyAsync(buf, p, n * sizeof(double), cudaMemcpyHostToDevice, c->s));
@@ -2140,7 +2155,7 @@ int ibmg_set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kap
     return api(c, [&]() -> int {
         if (n_mem > 0 && (!nb || !kappa || !ds || !X)) throw InvalidArg("null structure arrays");
         wait_inputs(c, ptr_kind);
-        set_structures(c, n_mem, nb, kappa, ds, X, ptr_kind);
+        set_structures(c, n_mem, nb, kappa, ds, X, ptr_kind, true);
         return IBMG_OK;
     });
 }
@@ -2264,6 +2279,7 @@ int ibmg_big_blocks(ibmg_ctx* c, int level, int* flags) {
     try {
         if (!c || level < 0 || level + 1 >= c->nlev) return -1;
         CK(cudaSetDevice(c->prm.device));
+        ensure_built(c);
         const int nbk = c->lev[level].L.n / 4;
         std::vector<uint8_t> h(size_t(nbk) * nbk);
         CK(cudaMemcpy(h.data(), c->lev[level].big, h.size(), cudaMemcpyDeviceToHost));
@@ -2288,6 +2304,7 @@ long ibmg_debug_coarse_trace(ibmg_ctx* c, const double* b, double* w, unsigned l
     try {
         if (!c) return -1;
         CK(cudaSetDevice(c->prm.device));
+        ensure_built(c);
         unsigned long long* d = dalloc<unsigned long long>(64);
         CK(cudaMemset(d, 0, sizeof(unsigned long long) * 64));
         CoarseArgs A = coarse_args(c, b, w);
@@ -2310,6 +2327,7 @@ long ibmg_debug_cluster_trace(ibmg_ctx* c, const double* b, double* w, unsigned 
     try {
         if (!c || !c->cl_ok) return -1;
         CK(cudaSetDevice(c->prm.device));
+        ensure_built(c);
         const long words = 4000;
         unsigned long long* d = dalloc<unsigned long long>(words);
         CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * words, c->s));
@@ -2331,6 +2349,7 @@ long ibmg_debug_sweep_trace(ibmg_ctx* c, int level, const double* b, double* w, 
     try {
         if (!c || level < 0 || level >= c->lc) return -1;
         CK(cudaSetDevice(c->prm.device));
+        ensure_built(c);
         LevelBuf& lb = c->lev[level];
         const int nt = lb.L.n / kTile;
         const long words = 6L * nt * nt + 9L * lb.nbig;
@@ -2355,6 +2374,7 @@ long ibmg_elasticity_triplets(ibmg_ctx* c, int level, int* rows, int* cols, doub
     try {
         if (!c || level < 0 || level >= c->nlev) return -1;
         CK(cudaSetDevice(c->prm.device));
+        ensure_built(c);
         LevelBuf& lb = c->lev[level];
         const int nf = lb.FL.nf;
         if (nf == 0) return 0;
@@ -2425,6 +2445,7 @@ int ibmg_spread(ibmg_ctx* c, const double* Fin, double* f, int ptr_kind) {
 int ibmg_vcycle_spectrum(ibmg_ctx* c, int m, unsigned long long seed, double* H, int* m_done) {
     return api(c, [&]() -> int {
         if (m < 1 || m > c->prm.restart || !H) throw InvalidArg("spectrum: 1 <= m <= restart and H required");
+        ensure_built(c);
         const size_t M = c->M;
         const int hoff = 0, h2off = c->prm.restart + 2;
         // seeded start vector (splitmix64 -> U[-1, 1)), pressure mean removed on the device
@@ -2477,6 +2498,7 @@ int ibmg_solve(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st, int ptr_
     if (!st) st = &local;
     return api(c, [&]() -> int {
         const double t0 = now_ms();
+        ensure_built(c);
         wait_inputs(c, ptr_kind);
         const double* db = ptr_kind == IBMG_PTR_DEVICE ? b : nullptr;
         if (!db) {
@@ -2513,6 +2535,7 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
         }
         CK(cudaEventRecord(c->ev_t0, c->s));
         rebuild(c, true);
+        c->built_dirty = false;
         build_rhs(c, du, c->bv);
         CK(cudaEventRecord(c->ev_t1, c->s));
         const double t1 = now_ms();
@@ -2540,3 +2563,4 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
 }  // extern "C"
 
 #include "slab_group.cuh"
+#include "batch.cuh"

@@ -51,7 +51,8 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_group_exchanges", "ibmg_group_set_structures", "ibmg_group_sweep", "ibmg_group_vcycle",
            "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl",
            "ibmg_vcycle_spectrum", "ibmg_set_scheme", "ibmg_set_input_stream", "ibmg_debug_cluster_trace",
-           "ibmg_cluster_level"]
+           "ibmg_cluster_level", "ibmg_batch_create", "ibmg_batch_destroy", "ibmg_batch_last_error",
+           "ibmg_batch_kernel_launches", "ibmg_batch_stream", "ibmg_batch_set_structures", "ibmg_batch_step"]
 
 
 def lib_path() -> str:
@@ -98,6 +99,16 @@ def lib(build_if_missing: bool = True):
     L.ibmg_debug_cluster_trace.restype = C.c_long
     L.ibmg_debug_cluster_trace.argtypes = [vp, vp, vp, vp, C.c_long]
     L.ibmg_cluster_level.argtypes = [vp]
+    L.ibmg_batch_create.argtypes = [C.POINTER(Params), ip, C.POINTER(C.c_void_p)]
+    L.ibmg_batch_destroy.argtypes = [vp]
+    L.ibmg_batch_last_error.restype = C.c_char_p
+    L.ibmg_batch_last_error.argtypes = [vp]
+    L.ibmg_batch_kernel_launches.restype = C.c_longlong
+    L.ibmg_batch_kernel_launches.argtypes = [vp]
+    L.ibmg_batch_stream.restype = C.c_void_p
+    L.ibmg_batch_stream.argtypes = [vp]
+    L.ibmg_batch_set_structures.argtypes = [vp, ip, ip, vp, vp, vp, vp]
+    L.ibmg_batch_step.argtypes = [vp, ip, vp, vp, vp, vp, ip]
     L.ibmg_debug_sweep_trace.restype = C.c_long
     L.ibmg_debug_sweep_trace.argtypes = [vp, ip, vp, vp, vp, C.c_long]
     L.ibmg_elasticity_triplets.restype = C.c_long
@@ -387,6 +398,70 @@ class SaddleSystem:
     @property
     def stream(self):
         return self._L.ibmg_stream(self._h)
+
+
+class BatchSystem:
+    """`nslots` independent problems of one grid size (64 <= N <= 512) stepped in
+    lockstep (C ABI ibmg_batch_*, DESIGN.md §7): per slot its own structures;
+    step_implicit runs the rebuilds per slot, then one launch per smoother /
+    transfer / Krylov phase for all slots.  Each problem's result equals the
+    single-context step_implicit's."""
+
+    def __init__(self, N, nslots, rho=1.0, mu=1.0, dt=1e-2, nu1=1, nu2=1, restart=30, max_iters=600,
+                 rtol=1e-10, device=0):
+        self._L = lib()
+        p = Params(N, rho, mu, dt, nu1, nu2, restart, max_iters, rtol, 4, device)
+        h = C.c_void_p()
+        rc = self._L.ibmg_batch_create(C.byref(p), int(nslots), C.byref(h))
+        if rc != 0 or not h.value:
+            raise RuntimeError(f"ibmg_batch_create failed (status {rc})")
+        self._h = h
+        self.N, self.nslots = N, nslots
+        self._in_stream = 0
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.ibmg_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, rc, ok=(0,)):
+        if rc in ok:
+            return rc
+        msg = self._L.ibmg_batch_last_error(self._h).decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+    def set_structures(self, slot, nb, kappa, ds, X):
+        nb = np.ascontiguousarray(nb, np.int32)
+        kappa = np.ascontiguousarray(kappa, np.float64)
+        ds = np.ascontiguousarray(ds, np.float64)
+        X = np.ascontiguousarray(X, np.float64).reshape(-1)
+        self._chk(self._L.ibmg_batch_set_structures(self._h, int(slot), len(nb), nb.ctypes.data, kappa.ctypes.data,
+                                                    ds.ctypes.data, X.ctypes.data))
+
+    def step_implicit(self, us, ps, Xs):
+        """One implicit step of slots 0..len(us)-1 in place on the per-problem
+        (u, p, X) arrays (all numpy, or all CUDA tensors); returns the stats."""
+        n = len(us)
+        if not (len(ps) == n == len(Xs)):
+            raise ValueError("one u, p, X per problem")
+        ptrs = [[_ptr(a) for a in arrs] for arrs in (us, ps, Xs)]
+        kinds = {k for arr in ptrs for _, k in arr}
+        if len(kinds) != 1:
+            raise ValueError("all arrays host or all device")
+        kind = kinds.pop()
+        arr = [(C.c_void_p * n)(*[pt for pt, _ in a]) for a in ptrs]
+        st = (Stats * n)()
+        self._chk(self._L.ibmg_batch_step(self._h, n, arr[0], arr[1], arr[2], st, kind), ok=(0, 2))
+        return [s.as_dict() for s in st]
+
+    @property
+    def kernel_launches(self):
+        return int(self._L.ibmg_batch_kernel_launches(self._h))
 
 
 def slab_plan(N, nslabs, min_rows=64, min_cells=1 << 16, coarsest_n=4):
