@@ -507,10 +507,15 @@ def run_batch(args, rank, world):
 def run_batch_lockstep(args, rank, world):
     """C5 through the lockstep batch (ibmg_batch_*): this rank's
     problems in chunks of `slots`, sorted by kappa (similar iteration counts
-    keep the lockstep rounds full); per chunk: set_structures per slot, then one
-    batched step.  Device arrays for the value, host arrays for e2e; wall clock
-    around host-synchronous steps (every step returns after its results are
+    keep the lockstep rounds full).  Two batch objects alternate: while one
+    solves chunk i (the batched FGMRES), a second host thread sets the
+    structures of chunk i+1 on the other and prepares it (upload, rebuild at
+    X^n with the host colouring, RHS), so the setup overlaps the solves.
+    Device arrays for the value, host arrays for e2e; wall clock around the
+    whole host-synchronous pipeline (every solve returns after its results are
     back), max over ranks."""
+    import threading as th
+
     import torch
     from paper_1311_5614_b200 import configs
     from paper_1311_5614_b200 import dist as D
@@ -522,51 +527,72 @@ def run_batch_lockstep(args, rank, world):
     probs = {i: configs.config5_problem(i) for i in mine}
     order = sorted(mine, key=lambda i: probs[i].kappa[0])
     S = max(1, min(args.slots, len(order)))
-    B = BatchSystem(256, S, 1.0, 1.0, 1e-3, device=dev)
+    Bs = [BatchSystem(256, S, 1.0, 1.0, 1e-3, device=dev) for _ in range(2)]
     n2 = 256 * 256
     Dv = f"cuda:{dev}"
 
-    def run(host, sub):
+    def arrays(host):
         if host:
-            us = [np.zeros(2 * n2) for _ in range(S)]
-            ps = [np.zeros(n2) for _ in range(S)]
-        else:
-            us = [torch.zeros(2 * n2, dtype=torch.float64, device=Dv) for _ in range(S)]
-            ps = [torch.zeros(n2, dtype=torch.float64, device=Dv) for _ in range(S)]
+            return ([np.zeros(2 * n2) for _ in range(S)], [np.zeros(n2) for _ in range(S)],
+                    [np.zeros(2 * 512) for _ in range(S)])
+        return ([torch.zeros(2 * n2, dtype=torch.float64, device=Dv) for _ in range(S)],
+                [torch.zeros(n2, dtype=torch.float64, device=Dv) for _ in range(S)],
+                [torch.zeros(2 * 512, dtype=torch.float64, device=Dv) for _ in range(S)])
+
+    def run(host, sub):
+        chunks = [sub[c0:c0 + S] for c0 in range(0, len(sub), S)]
+        bufs = [arrays(host), arrays(host)]
+        views = [None, None]
         res = []
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for c0 in range(0, len(sub), S):
-            chunk = sub[c0:c0 + S]
-            Xs = []
-            for k, i in enumerate(chunk):
-                pr = probs[i]
+
+        def prepare(i):
+            B, (us, ps, Xs) = Bs[i % 2], bufs[i % 2]
+            ch = chunks[i]
+            xv = []
+            for k, pi in enumerate(ch):
+                pr = probs[pi]
                 B.set_structures(k, pr.nb, pr.kappa, pr.ds, pr.X)
+                m = pr.X.size
                 if host:
                     us[k][:] = 0.0
-                    Xs.append(pr.X.reshape(-1).copy())
+                    Xs[k][:m] = pr.X.reshape(-1)
                 else:
                     us[k].zero_()
-                    Xs.append(torch.tensor(pr.X.reshape(-1), dtype=torch.float64, device=Dv))
-            sts = B.step_implicit(us[:len(chunk)], ps[:len(chunk)], Xs)
-            res += [(i, st["iters"], bool(st["converged"])) for i, st in zip(chunk, sts)]
+                    Xs[k][:m].copy_(torch.from_numpy(pr.X.reshape(-1)))
+                xv.append(Xs[k][:m])
+            views[i % 2] = (us[:len(ch)], ps[:len(ch)], xv)
+            B.prepare(views[i % 2][0], xv)
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        prepare(0)
+        for i in range(len(chunks)):
+            nxt = th.Thread(target=prepare, args=(i + 1,)) if i + 1 < len(chunks) else None
+            if nxt:
+                nxt.start()
+            us, ps, xv = views[i % 2]
+            sts = Bs[i % 2].solve(us, ps, xv)
+            res += [(pi, st["iters"], bool(st["converged"])) for pi, st in zip(chunks[i], sts)]
+            if nxt:
+                nxt.join()
         torch.cuda.synchronize()
         return (time.perf_counter() - t0) * 1e3, res
 
-    run(False, order[:S])  # warm-up: one chunk
+    run(False, order[:2 * S])  # warm-up: two chunks (both batch objects)
     if world > 1:
         torch.distributed.barrier()
-    launches0 = B.kernel_launches
+    launches0 = sum(B.kernel_launches for B in Bs)
     with ClockSampler(dev) as clk:
         ms, res = run(False, order)
-    launches = B.kernel_launches - launches0
+    launches = sum(B.kernel_launches for B in Bs) - launches0
     e2e_ms, _ = run(True, order)
     tmax, tsum, tmin = D.reduce_stats([ms, e2e_ms, len(res), sum(r[1] for r in res), all(r[2] for r in res)],
                                       device=Dv)
-    B.close()
+    for B in Bs:
+        B.close()
     return {"ms": float(tmax[0]), "e2e_ms": float(tmax[1]), "nprob": float(tsum[2]), "vcyc": float(tsum[3]),
             "conv": bool(tmin[4]), "launches": launches, "clocks": clk.summary(), "workers": S,
-            "warmup_problems": min(S, len(order))}
+            "warmup_problems": min(2 * S, len(order))}
 
 
 def cpu_oracle_steps(steps_sched, threads):

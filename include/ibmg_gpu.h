@@ -238,6 +238,12 @@ int ibmg_batch_set_structures(ibmg_batch* batch, int slot, int n_mem, const int*
  * (in/out), host or device pointers; stats[k] per problem (may be NULL). */
 int ibmg_batch_step(ibmg_batch* batch, int count, double* const* u, double* const* p, double* const* X,
                     ibmg_stats* stats, int ptr_kind);
+/* ibmg_batch_step in two phases, so that one thread can prepare (upload,
+ * rebuild at X^n, RHS: host colouring + setup kernels) the next batch while
+ * another solves this one: prepare(count, u, X) then solve(count, u, p, X). */
+int ibmg_batch_prepare(ibmg_batch* batch, int count, double* const* u, double* const* X, int ptr_kind);
+int ibmg_batch_solve(ibmg_batch* batch, int count, double* const* u, double* const* p, double* const* X,
+                     ibmg_stats* stats, int ptr_kind);
 
 #ifdef __cplusplus
 }

@@ -279,6 +279,8 @@ struct ibmg_batch {
     int bt_off[ibmg::kBMaxLev + 1] = {0};
     double* d_dh = nullptr;
     double* h_dh = nullptr;  // pinned
+    int prepared = 0;        // slots rebuilt by ibmg_batch_prepare, awaiting ibmg_batch_solve
+    double prep_ms = 0.0;
 };
 
 namespace {
@@ -760,18 +762,19 @@ int ibmg_batch_set_structures(ibmg_batch* B, int slot, int n_mem, const int* nb,
     });
 }
 
-// One implicit step of problems 0..count-1 (SPEC.md:548-552 each), in lockstep:
-// u[k] (2N^2 in/out), p[k] (N^2 out), X[k] (in/out) host or device arrays.
-int ibmg_batch_step(ibmg_batch* B, int count, double* const* u, double* const* p, double* const* X,
-                    ibmg_stats* stats, int ptr_kind) {
+// Phase 1 of a batch step: X^n and u^n in, every slot's operators rebuilt at
+// X^n and its RHS built, on the slots' own streams (another thread may run
+// ibmg_batch_solve of ANOTHER batch meanwhile: the host colouring and the
+// rebuild kernels overlap that batch's solve).
+int ibmg_batch_prepare(ibmg_batch* B, int count, double* const* u, double* const* X, int ptr_kind) {
     using namespace ibmg;
     return bapi(B, [&]() -> int {
-        if (count < 1 || count > int(B->ctx.size()) || !u || !p || !X) throw InvalidArg("batch step arguments");
+        if (count < 1 || count > int(B->ctx.size()) || !u || !X) throw InvalidArg("batch prepare arguments");
         const double t0 = now_ms();
         const size_t nn = size_t(B->prm.N) * B->prm.N;
         for (int k = 0; k < count; ++k) {
             ibmg_ctx* c = B->ctx[k];
-            if (!c->have_structs) throw InvalidArg("ibmg_batch_step: set the structures of every slot first");
+            if (!c->have_structs) throw InvalidArg("ibmg_batch_prepare: set the structures of every slot first");
             wait_inputs(c, ptr_kind);
             const cudaMemcpyKind kin = ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
             if (c->npts) CK(cudaMemcpyAsync(c->X, X[k], sizeof(double) * 2 * c->npts, kin, c->s));
@@ -780,9 +783,25 @@ int ibmg_batch_step(ibmg_batch* B, int count, double* const* u, double* const* p
             c->built_dirty = false;
             build_rhs(c, c->stage_a, c->bv);
             CK(cudaEventRecord(B->ev_ready[k], c->s));
-            CK(cudaStreamWaitEvent(B->s, B->ev_ready[k], 0));
         }
+        B->prepared = count;
+        B->prep_ms = now_ms() - t0;
+        return IBMG_OK;
+    });
+}
+
+// Phase 2: the lockstep solve of the prepared slots, X^{n+1} = X^n + dt S*u,
+// results out (u[k] 2N^2, p[k] N^2, X[k]).
+int ibmg_batch_solve(ibmg_batch* B, int count, double* const* u, double* const* p, double* const* X,
+                     ibmg_stats* stats, int ptr_kind) {
+    using namespace ibmg;
+    return bapi(B, [&]() -> int {
+        if (count < 1 || count != B->prepared || !u || !p || !X)
+            throw InvalidArg("batch solve: call ibmg_batch_prepare with the same count first");
+        B->prepared = 0;
         const double t1 = now_ms();
+        const size_t nn = size_t(B->prm.N) * B->prm.N;
+        for (int k = 0; k < count; ++k) CK(cudaStreamWaitEvent(B->s, B->ev_ready[k], 0));
         batch_table(B, count);
         std::vector<ibmg_stats> st;
         batch_fgmres(B, count, st);
@@ -799,19 +818,32 @@ int ibmg_batch_step(ibmg_batch* B, int count, double* const* u, double* const* p
             });
         }
         CK(cudaStreamSynchronize(B->s));
+        // the slots' own streams follow the batch stream (their next rebuild
+        // must not overwrite what this solve used)
+        CK(cudaEventRecord(B->ev_done, B->s));
+        for (int k = 0; k < count; ++k) CK(cudaStreamWaitEvent(B->ctx[k]->s, B->ev_done, 0));
         const double t2 = now_ms();
         int rc = IBMG_OK;
         for (int k = 0; k < count; ++k) {
             if (stats) {
                 stats[k] = st[k];
-                stats[k].setup_ms = (t1 - t0) / count;
+                stats[k].setup_ms = B->prep_ms / count;
                 stats[k].solve_ms = (t2 - t1) / count;
-                stats[k].total_ms = (t2 - t0) / count;
+                stats[k].total_ms = (B->prep_ms + t2 - t1) / count;
             }
             if (!st[k].converged) rc = IBMG_NOT_CONVERGED;
         }
         return rc;
     });
+}
+
+// One implicit step of problems 0..count-1 (SPEC.md:548-552 each), in lockstep:
+// u[k] (2N^2 in/out), p[k] (N^2 out), X[k] (in/out) host or device arrays.
+int ibmg_batch_step(ibmg_batch* B, int count, double* const* u, double* const* p, double* const* X,
+                    ibmg_stats* stats, int ptr_kind) {
+    const int rc = ibmg_batch_prepare(B, count, u, X, ptr_kind);
+    if (rc != IBMG_OK) return rc;
+    return ibmg_batch_solve(B, count, u, p, X, stats, ptr_kind);
 }
 
 }  // extern "C"

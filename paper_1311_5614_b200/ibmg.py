@@ -52,7 +52,8 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_group_solve", "ibmg_group_step", "ibmg_nccl_unique_id", "ibmg_group_create_nccl",
            "ibmg_vcycle_spectrum", "ibmg_set_scheme", "ibmg_set_input_stream", "ibmg_debug_cluster_trace",
            "ibmg_cluster_level", "ibmg_batch_create", "ibmg_batch_destroy", "ibmg_batch_last_error",
-           "ibmg_batch_kernel_launches", "ibmg_batch_stream", "ibmg_batch_set_structures", "ibmg_batch_step"]
+           "ibmg_batch_kernel_launches", "ibmg_batch_stream", "ibmg_batch_set_structures", "ibmg_batch_step",
+           "ibmg_batch_prepare", "ibmg_batch_solve"]
 
 
 def lib_path() -> str:
@@ -109,6 +110,8 @@ def lib(build_if_missing: bool = True):
     L.ibmg_batch_stream.argtypes = [vp]
     L.ibmg_batch_set_structures.argtypes = [vp, ip, ip, vp, vp, vp, vp]
     L.ibmg_batch_step.argtypes = [vp, ip, vp, vp, vp, vp, ip]
+    L.ibmg_batch_prepare.argtypes = [vp, ip, vp, vp, ip]
+    L.ibmg_batch_solve.argtypes = [vp, ip, vp, vp, vp, vp, ip]
     L.ibmg_debug_sweep_trace.restype = C.c_long
     L.ibmg_debug_sweep_trace.argtypes = [vp, ip, vp, vp, vp, C.c_long]
     L.ibmg_elasticity_triplets.restype = C.c_long
@@ -443,20 +446,37 @@ class BatchSystem:
         self._chk(self._L.ibmg_batch_set_structures(self._h, int(slot), len(nb), nb.ctypes.data, kappa.ctypes.data,
                                                     ds.ctypes.data, X.ctypes.data))
 
-    def step_implicit(self, us, ps, Xs):
-        """One implicit step of slots 0..len(us)-1 in place on the per-problem
-        (u, p, X) arrays (all numpy, or all CUDA tensors); returns the stats."""
-        n = len(us)
-        if not (len(ps) == n == len(Xs)):
-            raise ValueError("one u, p, X per problem")
-        ptrs = [[_ptr(a) for a in arrs] for arrs in (us, ps, Xs)]
+    @staticmethod
+    def _arrays(*lists):
+        n = len(lists[0])
+        if any(len(x) != n for x in lists):
+            raise ValueError("one array of each kind per problem")
+        ptrs = [[_ptr(a) for a in arrs] for arrs in lists]
         kinds = {k for arr in ptrs for _, k in arr}
         if len(kinds) != 1:
             raise ValueError("all arrays host or all device")
-        kind = kinds.pop()
-        arr = [(C.c_void_p * n)(*[pt for pt, _ in a]) for a in ptrs]
+        return n, kinds.pop(), [(C.c_void_p * n)(*[pt for pt, _ in a]) for a in ptrs]
+
+    def step_implicit(self, us, ps, Xs):
+        """One implicit step of slots 0..len(us)-1 in place on the per-problem
+        (u, p, X) arrays (all numpy, or all CUDA tensors); returns the stats."""
+        n, kind, arr = self._arrays(us, ps, Xs)
         st = (Stats * n)()
         self._chk(self._L.ibmg_batch_step(self._h, n, arr[0], arr[1], arr[2], st, kind), ok=(0, 2))
+        return [s.as_dict() for s in st]
+
+    def prepare(self, us, Xs):
+        """Phase 1 of step_implicit (upload, rebuild at X^n, RHS); releases the
+        GIL, so another thread can solve another batch meanwhile."""
+        n, kind, arr = self._arrays(us, Xs)
+        self._prep = (arr, kind)
+        self._chk(self._L.ibmg_batch_prepare(self._h, n, arr[0], arr[1], kind))
+
+    def solve(self, us, ps, Xs):
+        """Phase 2 of step_implicit for the prepared slots; returns the stats."""
+        n, kind, arr = self._arrays(us, ps, Xs)
+        st = (Stats * n)()
+        self._chk(self._L.ibmg_batch_solve(self._h, n, arr[0], arr[1], arr[2], st, kind), ok=(0, 2))
         return [s.as_dict() for s in st]
 
     @property
