@@ -280,6 +280,7 @@ struct ibmg_batch {
     double* d_dh = nullptr;
     double* h_dh = nullptr;  // pinned
     int prepared = 0;        // slots rebuilt by ibmg_batch_prepare, awaiting ibmg_batch_solve
+    int prep_threads = 4;    // host threads of ibmg_batch_prepare (IBMG_BATCH_THREADS)
     double prep_ms = 0.0;
 };
 
@@ -675,6 +676,7 @@ int ibmg_batch_create(const ibmg_params* p, int nslots, ibmg_batch** out) {
     ibmg_batch* B = new ibmg_batch;
     B->prm = *p;
     B->pdl = std::getenv("IBMG_NO_PDL") == nullptr;
+    if (const char* e = std::getenv("IBMG_BATCH_THREADS")) B->prep_threads = std::max(1, std::atoi(e));
     try {
         CK(cudaSetDevice(p->device));
         for (int k = 0; k < nslots; ++k) {
@@ -772,18 +774,43 @@ int ibmg_batch_prepare(ibmg_batch* B, int count, double* const* u, double* const
         if (count < 1 || count > int(B->ctx.size()) || !u || !X) throw InvalidArg("batch prepare arguments");
         const double t0 = now_ms();
         const size_t nn = size_t(B->prm.N) * B->prm.N;
-        for (int k = 0; k < count; ++k) {
-            ibmg_ctx* c = B->ctx[k];
-            if (!c->have_structs) throw InvalidArg("ibmg_batch_prepare: set the structures of every slot first");
-            wait_inputs(c, ptr_kind);
-            const cudaMemcpyKind kin = ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-            if (c->npts) CK(cudaMemcpyAsync(c->X, X[k], sizeof(double) * 2 * c->npts, kin, c->s));
-            CK(cudaMemcpyAsync(c->stage_a, u[k], sizeof(double) * 2 * nn, kin, c->s));
-            rebuild(c, true);
-            c->built_dirty = false;
-            build_rhs(c, c->stage_a, c->bv);
-            CK(cudaEventRecord(B->ev_ready[k], c->s));
+        for (int k = 0; k < count; ++k)
+            if (!B->ctx[k]->have_structs) throw InvalidArg("ibmg_batch_prepare: set the structures of every slot first");
+        // the slots' rebuilds (host colouring + setup kernels with their host
+        // round trips) on worker threads, slots round-robin: each context
+        // has its own streams and pinned buffers
+        auto work = [&](int w, int nw) {
+            CK(cudaSetDevice(B->prm.device));
+            for (int k = w; k < count; k += nw) {
+                ibmg_ctx* c = B->ctx[k];
+                wait_inputs(c, ptr_kind);
+                const cudaMemcpyKind kin =
+                    ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+                if (c->npts) CK(cudaMemcpyAsync(c->X, X[k], sizeof(double) * 2 * c->npts, kin, c->s));
+                CK(cudaMemcpyAsync(c->stage_a, u[k], sizeof(double) * 2 * nn, kin, c->s));
+                rebuild(c, true);
+                c->built_dirty = false;
+                build_rhs(c, c->stage_a, c->bv);
+                CK(cudaEventRecord(B->ev_ready[k], c->s));
+            }
+        };
+        const int nw = std::max(1, std::min(B->prep_threads, count));
+        std::vector<std::future<void>> jobs;
+        for (int w = 1; w < nw; ++w) jobs.push_back(std::async(std::launch::async, work, w, nw));
+        std::exception_ptr first;
+        try {
+            work(0, nw);
+        } catch (...) {
+            first = std::current_exception();
         }
+        for (auto& j : jobs) {
+            try {
+                j.get();
+            } catch (...) {
+                if (!first) first = std::current_exception();
+            }
+        }
+        if (first) std::rethrow_exception(first);
         B->prepared = count;
         B->prep_ms = now_ms() - t0;
         return IBMG_OK;
