@@ -578,7 +578,7 @@ def run_batch_lockstep(args, rank, world):
         torch.cuda.synchronize()
         return (time.perf_counter() - t0) * 1e3, res
 
-    run(False, order[:2 * S])  # warm-up: two chunks (both batch objects)
+    run(False, order)  # warm-up: one pass over the shard (every slot's buffers grown to its problems' sizes)
     if world > 1:
         torch.distributed.barrier()
     launches0 = sum(B.kernel_launches for B in Bs)
@@ -592,7 +592,7 @@ def run_batch_lockstep(args, rank, world):
         B.close()
     return {"ms": float(tmax[0]), "e2e_ms": float(tmax[1]), "nprob": float(tsum[2]), "vcyc": float(tsum[3]),
             "conv": bool(tmin[4]), "launches": launches, "clocks": clk.summary(), "workers": S,
-            "warmup_problems": min(2 * S, len(order))}
+            "warmup_problems": len(order)}
 
 
 def cpu_oracle_steps(steps_sched, threads):
@@ -642,7 +642,7 @@ def main():
     ap.add_argument("--workers", type=int, default=10, help="C5 --c5-mode contexts: concurrent solver contexts per GPU (8-12 measured best on B200, 16 host cores)")
     ap.add_argument("--c5-mode", default="batch", choices=["batch", "contexts"],
                     help="C5: lockstep batch (ibmg_batch_*) or concurrent single-problem contexts")
-    ap.add_argument("--slots", type=int, default=32, help="C5 --c5-mode batch: problems per lockstep batch")
+    ap.add_argument("--slots", type=int, default=64, help="C5 --c5-mode batch: problems per lockstep batch (32-64 measured best)")
     ap.add_argument("--slabs", type=int, default=0,
                     help="C3/C4: slab-partition the problem (DESIGN.md §7): P slabs over the visible GPUs in this "
                          "process (P2P-fused exchange), or under torchrun one slab per rank over NCCL")
