@@ -531,10 +531,13 @@ def run_batch_lockstep(args, rank, world):
     n2 = 256 * 256
     Dv = f"cuda:{dev}"
 
+    def pinned(n):  # page-locked host buffers (numpy views): truly asynchronous copies
+        return torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
+
     def arrays(host):
         if host:
-            return ([np.zeros(2 * n2) for _ in range(S)], [np.zeros(n2) for _ in range(S)],
-                    [np.zeros(2 * 512) for _ in range(S)])
+            return ([pinned(2 * n2) for _ in range(S)], [pinned(n2) for _ in range(S)],
+                    [pinned(2 * 512) for _ in range(S)])
         return ([torch.zeros(2 * n2, dtype=torch.float64, device=Dv) for _ in range(S)],
                 [torch.zeros(n2, dtype=torch.float64, device=Dv) for _ in range(S)],
                 [torch.zeros(2 * 512, dtype=torch.float64, device=Dv) for _ in range(S)])
