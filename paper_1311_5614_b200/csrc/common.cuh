@@ -160,7 +160,7 @@ struct GAcc {
 template <int SUB>
 __device__ __forceinline__ void face_gather_sub(const FaceList& FL, const Win& W, const double* __restrict__ F,
                                                 double* __restrict__ out, int nn, double sign, int q, bool active,
-                                                int gl) {
+                                                int gl, bool assign = false) {
     double s = 0.0;
     int face = 0;
     if (active) {
@@ -191,7 +191,10 @@ __device__ __forceinline__ void face_gather_sub(const FaceList& FL, const Win& W
     }
 #pragma unroll
     for (int o = SUB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (active && gl == 0) out[face] += sign * s;
+    if (active && gl == 0) {
+        if (assign) out[face] = sign * s;  // into a face scratch the grid CTAs add (gather-first launches)
+        else out[face] += sign * s;
+    }
 }
 
 // one warp per face (k_face_gather: RHS forces, spread)

@@ -67,6 +67,10 @@ struct Gather {
     // gathered (the owned rows of a slab); lg = log2(n)
     int lg = 0, jlo = 0, jhi = 1 << 30;
     int sub = 32;  // lanes per face (8 when every list of the level is <= 32 entries)
+    // gather-first launches (fused_launch_gf): the gather CTAs wait for the
+    // point-force CTAs only (target_pf) and write sign * sum into `out`, a
+    // face scratch; the grid CTAs add it after `target` (all gathers done)
+    unsigned long long target_pf = 0;
 };
 constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point / per face
 
@@ -133,6 +137,50 @@ __device__ __forceinline__ void fused_launch(const PForce& pf, const Gather& G, 
     fused_launch_at(pf, G, ngrid, (int)blockIdx.x, grid);
 }
 
+// Gather-first dispatch: [point-force CTAs | gather CTAs | grid CTAs].  The
+// gathers wait for the point forces only and write sign * L F into the face
+// scratch G.out (zero off the face list); the grid CTAs stream their cells
+// and, just before storing, wait until every gather has signalled
+// (G.target) and add the scratch.  The grid's bandwidth-bound work no longer
+// waits for a tail of gathers; every wait is on lower-index CTAs (dispatched
+// first), so it always makes progress.  Same values as fused_launch:
+// v + sign * s either way.
+template <class GridFn>
+__device__ __forceinline__ void fused_launch_gf(const PForce& pf, const Gather& G, int ngrid, int bid, GridFn&& grid) {
+    if (bid < pf.nblk) {
+        point_force_warp(pf, bid);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(G.cnt, 1ull);
+        }
+        return;
+    }
+    if (bid < pf.nblk + G.nblk) {
+        if (threadIdx.x == 0)
+            while (ld_acquire_u64(G.cnt) < G.target_pf) __nanosleep(32);
+        __syncthreads();
+        const int lane = threadIdx.x & 31;
+        const int q = ((bid - pf.nblk) * kPfPerCta + (threadIdx.x >> 5)) * (32 / G.sub) + lane / G.sub;
+        const bool active = q < G.FL.nf;
+        if (G.sub == 8) face_gather_sub<8>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane & 7, true);
+        else face_gather_sub<32>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane, true);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(G.cnt, 1ull);
+        }
+        return;
+    }
+    grid(bid - pf.nblk - G.nblk);
+}
+
+// A grid thread's wait for every gather of a gather-first launch.
+__device__ __forceinline__ void wait_gathers(const Gather& G) {
+    if (G.nblk)
+        while (ld_acquire_u64(G.cnt) < G.target) __nanosleep(20);
+}
+
 // out = S w (E' part added by k_face_gather). K1 of DESIGN.md §4.
 // Grid CTAs cover cells [q0, q1) (a slab's owned rows; 0, nn for the level).
 __global__ void k_stokes_apply(Lev L, const double* __restrict__ w, double* __restrict__ out, PForce pf, Gather G,
@@ -168,7 +216,7 @@ struct ApSmem {
     double s[3][kApH][kApW];
 };
 __device__ __forceinline__ void apply_tile(const Lev& L, const double* __restrict__ w, double* __restrict__ out,
-                                           int blk, int q0, int q1, ApSmem& S) {
+                                           int blk, int q0, int q1, ApSmem& S, const Gather* gf = nullptr) {
     const int n = L.n, nn = L.nn;
     const int ntx = n / kApTx, jb = q0 / n, je = q1 / n;
     const int ty = blk / ntx, tx = blk - ty * ntx;
@@ -236,8 +284,18 @@ __device__ __forceinline__ void apply_tile(const Lev& L, const double* __restric
             rp[ci - 2] = rpu[k - 1][ci - 2] - g * (v[k + 1][ci] - v[k][ci]);
         }
         const size_t o = x + (size_t)yy * n;
-        *reinterpret_cast<double2*>(out + o) = make_double2(ru[k - 1][0], ru[k - 1][1]);
-        *reinterpret_cast<double2*>(out + nn + o) = make_double2(rv[0], rv[1]);
+        double2 ou = make_double2(ru[k - 1][0], ru[k - 1][1]), ov = make_double2(rv[0], rv[1]);
+        if (gf && gf->nblk) {  // gather-first: + sign * L F from the face scratch
+            if (k == 1) wait_gathers(*gf);
+            const double2 eu = __ldcg(reinterpret_cast<const double2*>(gf->out + o));
+            const double2 ev = __ldcg(reinterpret_cast<const double2*>(gf->out + nn + o));
+            ou.x += eu.x;
+            ou.y += eu.y;
+            ov.x += ev.x;
+            ov.y += ev.y;
+        }
+        *reinterpret_cast<double2*>(out + o) = ou;
+        *reinterpret_cast<double2*>(out + nn + o) = ov;
         *reinterpret_cast<double2*>(out + 2 * (size_t)nn + o) = make_double2(rp[0], rp[1]);
     }
 }
@@ -247,6 +305,13 @@ __global__ void __launch_bounds__(256) k_stokes_apply_t(Lev L, const double* __r
     __shared__ __align__(16) ApSmem S;
     pdl_enter();
     fused_launch(pf, G, ngrid, [&](int blk) { apply_tile(L, w, out, blk, q0, q1, S); });
+}
+// gather-first variant: G.out is the level's face scratch, out the result
+__global__ void __launch_bounds__(256) k_stokes_apply_gf(Lev L, const double* __restrict__ w, double* __restrict__ out,
+                                                         PForce pf, Gather G, int ngrid) {
+    __shared__ __align__(16) ApSmem S;
+    pdl_enter();
+    fused_launch_gf(pf, G, ngrid, (int)blockIdx.x, [&](int blk) { apply_tile(L, w, out, blk, 0, L.nn, S, &G); });
 }
 
 // r = b - S w (E' part added by k_face_gather with sign +1).
@@ -329,7 +394,8 @@ struct RrSmem {
 __device__ __forceinline__ void residual_restrict_tile(const Lev& F, const double* __restrict__ b,
                                                        const double* __restrict__ w, double* __restrict__ bc,
                                                        double* __restrict__ wc_zero, int blk, int q0, int q1,
-                                                       RrSmem& S, const double* __restrict__ e = nullptr) {
+                                                       RrSmem& S, const double* __restrict__ e = nullptr,
+                                                       const Gather* gf = nullptr) {
     const int n = F.n, nn = F.nn, nc = n >> 1, nnc = nc * nc;
     const int ntx = nc / kRrTx, Jb = q0 / nc, Je = q1 / nc;
     const int ty = blk / ntx, tx = blk - ty * ntx;
@@ -415,7 +481,17 @@ __device__ __forceinline__ void residual_restrict_tile(const Lev& F, const doubl
         return bb - (d * u[k][ci] - cc * (u[k][ci - 1] + u[k][ci + 1] + u[k - 1][ci] + u[k + 1][ci]) +
                      g * (pu[k - 1][ci] - pu[k - 1][ci - 1]));
     };
-    bc[q] = 0.125 * (ru(1, 1) + 2.0 * ru(1, 2) + ru(1, 3) + ru(2, 1) + 2.0 * ru(2, 2) + ru(2, 3));
+    double ecu = 0.0, ecv = 0.0;
+    const bool gfa = gf && gf->nblk;
+    if (gfa) {  // gather-first: R E' w on the coarse faces, from the face scratch
+        wait_gathers(*gf);
+        ecu = __ldcg(gf->out + q);
+        ecv = __ldcg(gf->out + nnc + q);
+    }
+    {
+        const double v = 0.125 * (ru(1, 1) + 2.0 * ru(1, 2) + ru(1, 3) + ru(2, 1) + 2.0 * ru(2, 2) + ru(2, 3));
+        bc[q] = gfa ? v + ecu : v;
+    }
     // ---- p rows: u(x+1, y) - u(x, y) and v(x, y+1) - v(x, y), fine (2Ic + a, 2Jc + bb)
     double v[5][6];
 #pragma unroll
@@ -445,7 +521,23 @@ __device__ __forceinline__ void residual_restrict_tile(const Lev& F, const doubl
         return bb - (d * v[k][ci] - cc * (v[k - 1][ci] + v[k + 1][ci] + v[k][ci - 1] + v[k][ci + 1]) +
                      g * (pv[k][ci - 2] - pv[k - 1][ci - 2]));
     };
-    bc[nnc + q] = 0.125 * (rv(1, 2) + 2.0 * rv(2, 2) + rv(3, 2) + rv(1, 3) + 2.0 * rv(2, 3) + rv(3, 3));
+    {
+        const double v = 0.125 * (rv(1, 2) + 2.0 * rv(2, 2) + rv(3, 2) + rv(1, 3) + 2.0 * rv(2, 3) + rv(3, 3));
+        bc[nnc + q] = gfa ? v + ecv : v;
+    }
+}
+
+// gather-first variant (whole coarse level): G.out is the coarse level's face scratch
+__global__ void __launch_bounds__(256) k_residual_restrict_gf(Lev F, const double* __restrict__ b,
+                                                              const double* __restrict__ w, double* __restrict__ bc,
+                                                              double* __restrict__ wc_zero, PForce pf, Gather G,
+                                                              int ngrid) {
+    __shared__ __align__(16) RrSmem S;
+    pdl_enter();
+    const int nnc = F.nn >> 2;
+    fused_launch_gf(pf, G, ngrid, (int)blockIdx.x, [&](int blk) {
+        residual_restrict_tile(F, b, w, bc, wc_zero, blk, 0, nnc, S, nullptr, &G);
+    });
 }
 
 // Grid CTAs: ngrid = (nc / 32) x ceil(rows / 8) tiles over coarse rows

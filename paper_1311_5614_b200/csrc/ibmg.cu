@@ -206,6 +206,7 @@ struct ibmg_ctx {
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
+    bool gather_first = true;  // fused apply / restriction: gathers before the grid CTAs (IBMG_GF=0: after)
     bool gj_regs = true;    // box inverses: 64-thread register Gauss-Jordan (IBMG_GJ256=1: 256-thread [A|I] form)
     bool spec_full = false; // FGMRES: whole next V-cycle enqueued behind the dots (IBMG_SPEC=1); measured no gain
                             // (C3 19.9 ms either way, C2 6.23 vs 6.17): default = its first sweep only
@@ -907,12 +908,18 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
             long blocks = 0;
             for (int l = 0; l + 1 < c->nlev; ++l) blocks += long(c->lev[l].L.n / 4) * (c->lev[l].L.n / 4);
             std::vector<std::future<void>> jobs;
-            if (blocks >= (1L << 20))
+            if (blocks >= (1L << 20)) {  // C4: a worker per coarser level
                 for (int l = 1; l + 1 < c->nlev; ++l)
                     jobs.push_back(std::async(std::launch::async, [c, l] {
                         CK(cudaSetDevice(c->prm.device));
                         colour_big_blocks(c, c->lev[l], c->lev[l].h_cm);
                     }));
+            } else if (blocks >= (1L << 15)) {  // C3: one worker for all coarser levels
+                jobs.push_back(std::async(std::launch::async, [c] {
+                    CK(cudaSetDevice(c->prm.device));
+                    for (int l = 1; l + 1 < c->nlev; ++l) colour_big_blocks(c, c->lev[l], c->lev[l].h_cm);
+                }));
+            }
             for (int l = 0; l + 1 < c->nlev; ++l) {
                 if (l > 0 && !jobs.empty()) break;
                 LevelBuf& lb = c->lev[l];
@@ -1063,11 +1070,13 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
     // levels whose restriction takes E' from the assembled rows (points far
     // outnumber the level's E-active faces): zero their E'w scratch (the face
     // set changed; only active faces are written afterwards)
-    for (int l = 0; l + 1 < c->nlev; ++l) {
+    // (gather-first launches: every level with E-active faces keeps such a
+    // face scratch, the target of the coarse face gathers and of the apply's)
+    for (int l = 0; l < c->nlev; ++l) {
         LevelBuf& lb = c->lev[l];
-        lb.rr_csr = c->rr_tiled && c->rr_csr && npts > 0 && lb.FL.nf > 0 && lb.L.n >= 2 * kRrTx &&
-                    c->rr_csr_ratio * lb.FL.nf < double(npts);
-        if (!lb.rr_csr) continue;
+        lb.rr_csr = l + 1 < c->nlev && c->rr_tiled && c->rr_csr && npts > 0 && lb.FL.nf > 0 &&
+                    lb.L.n >= 2 * kRrTx && c->rr_csr_ratio * lb.FL.nf < double(npts);
+        if (!lb.rr_csr && !(c->gather_first && lb.FL.nf > 0)) continue;
         if (!lb.escr) lb.escr = dalloc<double>(2 * size_t(lb.L.nn));
         CK(cudaMemsetAsync(lb.escr, 0, sizeof(double) * 2 * size_t(lb.L.nn), c->s));
     }
@@ -1192,6 +1201,19 @@ Gather gather(ibmg_ctx* c, const LevelBuf& to, double* out, double sign, const P
     return G;
 }
 
+// Gather-first launches (grid_kernels.cuh fused_launch_gf): gathers onto
+// level `to`'s face list into its face scratch, after the pf.nblk point-force
+// CTAs; the grid CTAs wait for all of them.
+Gather gather_gf(ibmg_ctx* c, const LevelBuf& to, double sign, const PForce& pf) {
+    Gather G{to.FL, to.W, c->F, to.escr, to.L.nn, sign, 0, c->tail_cnt, 0ull};
+    G.sub = to.maxrow <= 32 ? 8 : 32;
+    G.nblk = int(nblk(to.FL.nf, kPfPerCta * (32 / G.sub)));
+    G.target_pf = c->tail_base + (unsigned long long)pf.nblk;
+    c->tail_base += (unsigned long long)(pf.nblk + G.nblk);
+    G.target = c->tail_base;
+    return G;
+}
+
 // out (rows [y0, y1) of level l) = A_l w: stencil, point forces and the face
 // gather in one launch; the stencil part tiled (k_stokes_apply_t) where
 // n >= 64.  slab: gather only the faces of the owned rows.
@@ -1201,6 +1223,13 @@ void apply_rows(ibmg_ctx* c, int l, const double* w, double* out, int y0, int y1
     const PForce pf = pforce(c, lb, w, lb.FL.nf > 0);
     const bool tiled = c->ap_tiled && n >= kApTx;
     const int ng = tiled ? (n / kApTx) * ((y1 - y0 + kApTy - 1) / kApTy) : int(nblk(size_t(y1 - y0) * n));
+    if (tiled && !slab && c->gather_first && pf.nblk) {
+        // gather-first: point forces, face gathers into the level's face
+        // scratch, then the tiles (which add it before their stores)
+        Gather G = gather_gf(c, lb, -1.0, pf);
+        LAUNCH(c, k_stokes_apply_gf, pf.nblk + G.nblk + ng, 256, 0, lb.L, w, out, pf, G, ng);
+        return;
+    }
     Gather G = gather(c, lb, out, -1.0, pf, ng);
     if (slab) {
         G.lg = lb.L.lg;
@@ -1469,6 +1498,11 @@ void residual_restrict(ibmg_ctx* c, int l, const double* b, const double* w, dou
     const PForce pf = pforce(c, lb, w, nx.FL.nf > 0);
     const bool tiled = c->rr_tiled && nc >= kRrTx;
     const int ng = tiled ? (nc / kRrTx) * ((yc1 - yc0 + kRrTy - 1) / kRrTy) : 3 * int(nblk(size_t(yc1 - yc0) * nc));
+    if (tiled && !slab && c->gather_first && pf.nblk && yc0 == 0 && yc1 == nc) {
+        Gather G = gather_gf(c, nx, 1.0, pf);
+        LAUNCH(c, k_residual_restrict_gf, pf.nblk + G.nblk + ng, 256, 0, lb.L, b, w, nx.b, wcz, pf, G, ng);
+        return;
+    }
     Gather G = gather(c, nx, nx.b, 1.0, pf, ng);
     if (slab) {
         G.lg = nx.L.lg;
@@ -1974,6 +2008,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_DF_ES")) c->df_es = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("IBMG_SPEC")) c->spec_full = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_GJ256")) c->gj_regs = std::atoi(e) == 0;
+    if (const char* e = std::getenv("IBMG_GF")) c->gather_first = std::atoi(e) != 0;
     c->prm = *p;
     c->krows = krows;
     try {

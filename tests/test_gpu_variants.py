@@ -9,6 +9,8 @@ arithmetic is identical, to round-off where it is not.
   same column as the non-speculative one: bitwise steps.
 * IBMG_CANON_INV: canonical-order inverses are the same inverses, permuted:
   bitwise.
+* IBMG_GF: gather-first fused apply / restriction add the same sign * L F to
+  the same grid value (v + s either way): bitwise.
 * IBMG_GJ256: the register-resident in-place Gauss-Jordan and the 256-thread
   [A | I] form invert the same boxes with different operation orders:
   round-off (the V-cycle to 1e-12, the step to 1e-10, same iterations).
@@ -50,6 +52,7 @@ def step(g, prob):
     ("IBMG_SPEC", 1, 0, True),
     ("IBMG_CANON_INV", 1, 0, True),
     ("IBMG_GJ256", 0, 1, False),
+    ("IBMG_GF", 1, 0, True),
 ])
 def test_variant_step(var, a, b, bitwise):
     prob = configs.config2(1e6)
