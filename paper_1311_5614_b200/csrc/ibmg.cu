@@ -206,7 +206,8 @@ struct ibmg_ctx {
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
-    bool gather_first = true;  // fused apply / restriction: gathers before the grid CTAs (IBMG_GF=0: after)
+    bool gather_first = false; // fused apply / restriction: gathers before the grid CTAs (IBMG_GF=1); measured
+                               // slower (C4 restriction 24 -> 40 ms: the grid CTAs wait holding their SMs)
     bool gj_regs = true;    // box inverses: 64-thread register Gauss-Jordan (IBMG_GJ256=1: 256-thread [A|I] form)
     bool spec_full = false; // FGMRES: whole next V-cycle enqueued behind the dots (IBMG_SPEC=1); measured no gain
                             // (C3 19.9 ms either way, C2 6.23 vs 6.17): default = its first sweep only

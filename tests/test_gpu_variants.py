@@ -52,7 +52,7 @@ def step(g, prob):
     ("IBMG_SPEC", 1, 0, True),
     ("IBMG_CANON_INV", 1, 0, True),
     ("IBMG_GJ256", 0, 1, False),
-    ("IBMG_GF", 1, 0, True),
+    ("IBMG_GF", 1, 0, True),  # (opt-in)
 ])
 def test_variant_step(var, a, b, bitwise):
     prob = configs.config2(1e6)
