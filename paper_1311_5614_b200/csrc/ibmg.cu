@@ -5,6 +5,7 @@
 // the sm_100a kernels of *_kernels.cuh; there is no CPU fallback: every
 // numerical operation of the hot path is a kernel on the context's stream.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -206,6 +207,7 @@ struct ibmg_ctx {
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
+    bool tma = true;        // TMA staging of the interior tiles' w regions in k_plain_df (IBMG_TMA=0: cp.async)
     bool gather_first = false; // fused apply / restriction: gathers before the grid CTAs (IBMG_GF=1); measured
                                // slower (C4 restriction 24 -> 40 ms: the grid CTAs wait holding their SMs)
     bool gj_regs = true;    // box inverses: 64-thread register Gauss-Jordan (IBMG_GJ256=1: 256-thread [A|I] form)
@@ -1257,6 +1259,46 @@ void residual_level(ibmg_ctx* c, int l, const double* b, const double* w, double
 
 Slabs slabs(const LevelBuf& lb) { return Slabs{lb.Ainv, lb.sl_rp, lb.sl_off, lb.sl_col, lb.sl_val}; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            (void)cudaGetLastError();
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// Tensor maps of the three planes of a level vector w (n x n doubles each),
+// box = a tile's w region (TmaPlanes, smoother_kernels.cuh).  use = 0 when
+// TMA staging is off (IBMG_TMA=0) or unavailable.
+TmaPlanes tma_planes(ibmg_ctx* c, const double* w, int n) {
+    TmaPlanes t{};
+    t.use = 0;
+    if (!c->tma) return t;
+    auto fn = tma_encode_fn();
+    if (!fn) return t;
+    const size_t nn = size_t(n) * n;
+    for (int f = 0; f < 3; ++f) {
+        const cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(n)};
+        const cuuint64_t strides[1] = {cuuint64_t(n) * sizeof(double)};
+        const cuuint32_t box[2] = {cuuint32_t(kReg), cuuint32_t(kReg)};
+        const cuuint32_t es[2] = {1, 1};
+        const CUresult r = fn(&t.m[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(w + f * nn), dims,
+                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return TmaPlanes{};
+    }
+    t.use = 1;
+    return t;
+}
+
 // One tile-colour pass of the plain phase over `ntiles` tiles starting at tile
 // row ty0 (bandwidth regime: persistent double-buffered kernel by default).
 void plain_pass(ibmg_ctx* c, LevelBuf& lb, int tc, const double* b, double* w, int ty0, int ntiles, const Mirror& M) {
@@ -1303,8 +1345,9 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
     if (c->plain_df) {
         const int lim = c->grid_limit > 0 ? std::min(c->grid_limit, c->pdf_grid_max) : c->pdf_grid_max;
         if (c->prof) prof_begin(c, "k_plain_df");
+        const TmaPlanes tp = tma_planes(c, w, n);
         launch_k(c, k_plain_df, dim3(std::min(lim, 4 * per)), dim3(32), kPdfSmem, true, L, b, w,
-                 (const uint8_t*)lb.big, lb.tflags, ++lb.tepoch, (const int*)lb.pdf_seg);
+                 (const uint8_t*)lb.big, lb.tflags, ++lb.tepoch, (const int*)lb.pdf_seg, tp);
         if (c->prof) prof_end(c);
         ++c->launches;
     } else {
@@ -2010,6 +2053,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_SPEC")) c->spec_full = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_GJ256")) c->gj_regs = std::atoi(e) == 0;
     if (const char* e = std::getenv("IBMG_GF")) c->gather_first = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_TMA")) c->tma = std::atoi(e) != 0;
     c->prm = *p;
     c->krows = krows;
     try {

@@ -8,6 +8,7 @@
 // (bx mod 4, by mod 4), one CTA per block, dense 56x56 inverse applied.
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "common.cuh"
 #include "grid_kernels.cuh"
@@ -74,7 +75,10 @@ constexpr int kTile = 16, kReg = kTile + 4;  // region with a 2-cell halo
 // 2), but needs 8-byte staging copies; measured on B200 that is slower
 // (C4 plain phase 123 -> 160 ms, C2 step 7.77 -> 8.02 ms), so rows stay
 // 16-byte aligned.
-constexpr int kRegS = kReg, kRegP = kReg * kRegS;
+#ifndef IBMG_REG_STRIDE
+#define IBMG_REG_STRIDE 20
+#endif
+constexpr int kRegS = IBMG_REG_STRIDE, kRegP = kReg * kRegS;  // (odd: 8-byte staging, 2-way passes)
 
 struct TileW {
     double* s;  // [3][kReg][kRegS], local coords li, lj in [-2, 18)
@@ -86,7 +90,13 @@ struct TileW {
 // 16-byte cp.async (L1-allocating: w is not written by the launch).
 __device__ __forceinline__ void stage_w_region(double* sw, const double* __restrict__ w, int n, int nn, int x0, int y0,
                                                int lane) {
-    static_assert(kRegS % 2 == 0, "16-byte staging needs 16-byte aligned rows");
+    if (kRegS % 2) {  // odd stride: 8-byte copies
+        for (int q = lane; q < 3 * kReg * kReg; q += 32) {
+            const int f = q / (kReg * kReg), r = q - f * (kReg * kReg), bb = r / kReg, a = r - bb * kReg;
+            cp_async8(&sw[f * kRegP + bb * kRegS + a], w + (size_t)f * nn + wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n);
+        }
+        return;
+    }
     if (lane < 30) {  // 16-byte pairs: lane -> (pair lane % 10, rows lane / 10 + 3 k)
         const int a2 = lane % 10, r0 = lane / 10;
         const int xg = wr(x0 - 2 + 2 * a2, n);
@@ -699,6 +709,41 @@ __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
+// ---- TMA staging of a tile's w region (Blackwell tensor memory accelerator)
+// One 2-D tensor map per plane of the level's w (rows of n doubles, box 20 x 20
+// = the tile plus its 2-cell halo, landing in the TileW layout, row stride 20):
+// an interior tile's w region is three cp.async.bulk.tensor copies issued by one
+// lane and completed on an mbarrier, instead of 20 16-byte cp.async per lane.
+// Tiles whose region wraps the periodic edge keep the cp.async path (TMA
+// fills out-of-bound boxes with zeros, not the periodic image).
+struct TmaPlanes {
+    CUtensorMap m[3];
+    int use;  // 0: no tensor maps (cp.async staging everywhere)
+};
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(mb)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* mb) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(mb))
+        : "memory");
+}
+
 // One plain tile task of a dataflow sweep (one warp): stage b and the
 // big-block flags, wait for the adjacent tiles of smaller tile colour, stage
 // the w region (L2 only: neighbours were written by other SMs), run the 8
@@ -708,7 +753,8 @@ __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
 __device__ __forceinline__ void df_plain_tile(const Lev& L, const double* __restrict__ b, double* __restrict__ w,
                                               const uint8_t* __restrict__ big, unsigned* tflags, unsigned epoch,
                                               int tx, int ty, int tc, double* sw, double* sb,
-                                              unsigned long long* trace) {
+                                              unsigned long long* trace, const TmaPlanes* tm = nullptr,
+                                              unsigned long long* mbar = nullptr, unsigned* mphase = nullptr) {
     const int n = L.n, nn = L.nn, lane = threadIdx.x & 31, nt = n / kTile, nbk = n >> 2;
     const int x0 = tx * kTile, y0 = ty * kTile;
     const unsigned long long t_a = trace ? gtimer() : 0;
@@ -732,7 +778,25 @@ __device__ __forceinline__ void df_plain_tile(const Lev& L, const double* __rest
     }
     __syncwarp();
     const unsigned long long t_b = trace ? gtimer() : 0;
-    if (lane < 30) {  // 16-byte pairs, L2 only: lane -> (pair lane % 10, rows lane / 10 + 3 k)
+    const bool tma = tm && kRegS == kReg && x0 >= 2 && y0 >= 2 && x0 + kTile + 2 <= n && y0 + kTile + 2 <= n;
+    if (tma) {  // interior tile: three tensor copies (see TmaPlanes)
+        if (lane == 0) {
+            // the neighbours' stores (generic proxy, acquired above) before the
+            // async-proxy reads; this warp's last reads of sw before its writes
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(mbar, 3u * kRegP * 8u);
+#pragma unroll
+            for (int f = 0; f < 3; ++f) tma_load_2d(sw + f * kRegP, &tm->m[f], x0 - 2, y0 - 2, mbar);
+        }
+    } else if (kRegS % 2) {  // odd stride: 8-byte copies (L2 only)
+        for (int q = lane; q < 3 * kReg * kReg; q += 32) {
+            const int f = q / (kReg * kReg), r = q - f * (kReg * kReg), bb = r / kReg, a = r - bb * kReg;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&sw[f * kRegP + bb * kRegS + a]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                         "l"(w + (size_t)f * nn + wr(x0 - 2 + a, n) + (size_t)wr(y0 - 2 + bb, n) * n));
+        }
+    } else if (lane < 30) {  // 16-byte pairs, L2 only: lane -> (pair lane % 10, rows lane / 10 + 3 k)
         const int a2 = lane % 10, r0 = lane / 10;
         const int xg = wr(x0 - 2 + 2 * a2, n);
         for (int row = r0; row < 3 * kReg; row += 3) {  // row = f * kReg + bb
@@ -744,6 +808,10 @@ __device__ __forceinline__ void df_plain_tile(const Lev& L, const double* __rest
     cp_async_commit();
     const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
     cp_async_wait<0>();
+    if (tma) {
+        mbar_wait(mbar, *mphase);
+        *mphase ^= 1u;
+    }
     __syncwarp();
     const unsigned long long t_s = trace ? gtimer() : 0;
     TileW W{sw};
@@ -796,19 +864,26 @@ __device__ __forceinline__ void df_plain_tile(const Lev& L, const double* __rest
 // and b cross HBM about once per sweep instead of once per tile colour plus
 // halos (4 separate tile-colour launches).  One-warp CTAs, one w and one b
 // region per warp; cooperative launch (all CTAs co-resident) => no deadlock.
-constexpr size_t kPdfSmem = (kDfTileBytes + 15) / 16 * 16;
+constexpr size_t kPdfSmem = (kDfTileBytes + 127) / 128 * 128;
 __global__ void __launch_bounds__(32) k_plain_df(Lev L, const double* __restrict__ b, double* __restrict__ w,
                                                   const uint8_t* __restrict__ big, unsigned* tflags, unsigned epoch,
-                                                  const int* __restrict__ seg) {
+                                                  const int* __restrict__ seg, const __grid_constant__ TmaPlanes tm) {
     pdl_enter();
-    extern __shared__ __align__(16) unsigned char pdm[];
+    extern __shared__ __align__(128) unsigned char pdm[];
+    __shared__ __align__(8) unsigned long long mbar;
     double* sw = reinterpret_cast<double*>(pdm);
     double* sb = sw + 3 * kRegP;
     const int nt = L.n / kTile, half = nt >> 1, ntiles = nt * nt;
+    unsigned phase = 0;
+    if (tm.use) {
+        if (threadIdx.x == 0) mbar_init(&mbar, 1);
+        __syncwarp();
+    }
     for (int task = blockIdx.x; task < ntiles; task += gridDim.x) {
         const int s = task / half, i = task - s * half;
         const int sg = __ldg(seg + s), ty = sg >> 2, tc = sg & 3;
-        df_plain_tile(L, b, w, big, tflags, epoch, 2 * i + (tc & 1), ty, tc, sw, sb, nullptr);
+        df_plain_tile(L, b, w, big, tflags, epoch, 2 * i + (tc & 1), ty, tc, sw, sb, nullptr,
+                      tm.use ? &tm : nullptr, &mbar, &phase);
     }
 }
 

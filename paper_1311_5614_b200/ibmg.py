@@ -57,7 +57,8 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # IBMG_LIB: another build of the same library (A/B of compile-time variants)
+    return os.environ.get("IBMG_LIB", _build.LIB)
 
 
 def lib(build_if_missing: bool = True):

@@ -69,6 +69,21 @@ def test_variant_step(var, a, b, bitwise):
     gb.close()
 
 
+def test_tma_staging_c3_bitwise():
+    """IBMG_TMA: the band-major plain phase (levels n > 512; C3's level 1024)
+    staging interior tiles' w regions with tensor copies moves the same bytes
+    into the same layout: the V-cycle and the step are bitwise equal."""
+    prob = configs.config3()
+    ga, gb = make(prob, IBMG_TMA=1), make(prob, IBMG_TMA=0)
+    b = ga.build_rhs(rand(2 * prob.N ** 2, seed=4))
+    assert np.array_equal(ga.v_cycle(b), gb.v_cycle(b))
+    ua, pa, Xa, sa = step(ga, prob)
+    ub, pb, Xb, sb = step(gb, prob)
+    assert sa["iters"] == sb["iters"] and np.array_equal(ua, ub) and np.array_equal(Xa, Xb)
+    ga.close()
+    gb.close()
+
+
 def test_register_gauss_jordan_vcycle_c3():
     """C3 (dense coarse levels, 4.8k boxes): the V-cycle with the register
     inverses equals the [A | I] inverses' to round-off."""
