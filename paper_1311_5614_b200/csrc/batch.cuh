@@ -161,6 +161,74 @@ __global__ void __launch_bounds__(32 * kDfWarps, ES ? 2 : 1)
     cp_async_wait<0>();
 }
 
+// Split form of a batched sweep (throughput regime: many problems): the
+// plain phase of every active problem as one launch of one-warp CTAs (13 per
+// SM by shared memory; tile tasks colour-major, problems interleaved), then
+// the big blocks as one launch of 128-thread CTAs (4 per SM: one E'-row slot,
+// the inverse streamed into registers; k_big_phase's scheme) over the batch's
+// colour-major task list.  The blocks no longer overlap the tiles, but twice
+// as many tasks are in flight per SM as in the one-launch sweep.
+__global__ void __launch_bounds__(32) k_plain_b(const BProb* __restrict__ P, int l, int j, unsigned eadd,
+                                                const int* __restrict__ act, int nA) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char pdm[];
+    double* sw = reinterpret_cast<double*>(pdm);
+    double* sb = sw + 3 * kRegP;
+    const int n = P[act[0]].lv[l].df.L.n, nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1;
+    for (int task = blockIdx.x; task < nA * ntiles; task += gridDim.x) {
+        const int b = act[task % nA], loc = task / nA;
+        const int tc = loc / per, i = loc - tc * per;
+        const BProb& PB = P[b];
+        const DfArgs& A = PB.lv[l].df;
+        const Lev L = A.L;
+        df_plain_tile(L, blev_b(PB, l, j), blev_w(PB, l, j), A.big, A.tflags, A.DP.epoch + eadd,
+                      2 * (i % half) + (tc & 1), 2 * (i / half) + (tc >> 1), tc, sw, sb, nullptr);
+    }
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_big_b(const BProb* __restrict__ P, int l, int j, unsigned eadd,
+                                                       const BTask* __restrict__ bt, int nbt) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char dsm[];
+    ESlot* slot = reinterpret_cast<ESlot*>(dsm);
+    __shared__ BigScratch S;
+    const int t = threadIdx.x, G = gridDim.x;
+    int k = blockIdx.x;
+    if (k < nbt) eslot_issue(*slot, P[bt[k].b].lv[l].df.SL, bt[k].q, t, kBigThreads);
+    cp_async_commit();
+    for (; k < nbt; k += G) {
+        const BTask it = bt[k];
+        const int kn = k + G;
+        const BProb& PB = P[it.b];
+        const DfArgs& A = PB.lv[l].df;
+        const Lev L = A.L;
+        const int n = L.n, nn = L.nn, nbk = n >> 2, q = it.q;
+        const unsigned epoch = A.DP.epoch + eadd;
+        double* w = blev_w(PB, l, j);
+        const double* bb = blev_b(PB, l, j);
+        for (int e = A.DP.poff[q] + t; e < A.DP.poff[q + 1]; e += kBigThreads)
+            while (ld_acquire(A.DP.flags + A.DP.pred[e]) != epoch) __nanosleep(8);
+        cp_async_wait<0>();
+        __syncthreads();
+        const int Bk = slot->rp[47];
+        GAccCG Wg{w, n, nn};
+        GAccB Bg{bb, n, nn};
+        big_block_es(L, *slot, A.SL.Ainv + (size_t)q * 3136, 4 * (Bk % nbk), 4 * (Bk / nbk), Wg, FlatCG{w}, Bg,
+                     [&](int f, int i, int jj, double old, double d) {
+                         __stcg(w + (size_t)f * nn + i + (size_t)jj * n, old + d);
+                     },
+                     S, t, [] { __syncthreads(); },
+                     [&] {
+                         if (kn < nbt) eslot_issue(*slot, P[bt[kn].b].lv[l].df.SL, bt[kn].q, t, kBigThreads);
+                         cp_async_commit();
+                     },
+                     nullptr, nullptr, SlabTail{&A.SL, q});
+        __syncthreads();
+        if (t == 0) st_release(A.DP.flags + q, epoch);
+    }
+    cp_async_wait<0>();
+}
+
 // Batched residual + restriction of level l (grid.y = active problem).
 __global__ void __launch_bounds__(256) k_rr_b(const BProb* __restrict__ P, int l, int j, const int* __restrict__ act) {
     __shared__ __align__(16) RrSmem S;
@@ -281,6 +349,9 @@ struct ibmg_batch {
     double* h_dh = nullptr;  // pinned
     int prepared = 0;        // slots rebuilt by ibmg_batch_prepare, awaiting ibmg_batch_solve
     int prep_threads = 4;    // host threads of ibmg_batch_prepare (IBMG_BATCH_THREADS)
+    bool split = true;       // split sweeps from split_min active problems (IBMG_BATCH_SPLIT=0: one launch)
+    int split_min = 8;
+    int pdf_grid = 1, big_grid = 1;
     double prep_ms = 0.0;
 };
 
@@ -421,6 +492,15 @@ void batch_sweep(ibmg_batch* B, int l, int j, unsigned eadd, int nA) {
     using namespace ibmg;
     const int nbt = B->bt_off[l + 1] - B->bt_off[l];
     const BTask* bt = B->d_bt + B->bt_off[l];
+    if (B->split && nA >= B->split_min) {  // throughput regime: split launches (k_plain_b / k_big_b)
+        const int nt = B->ctx[0]->lev[l].L.n / kTile;
+        launch_b(B, k_plain_b, dim3(std::min(B->pdf_grid, nA * nt * nt)), dim3(32), kPdfSmem, true,
+                 (const BProb*)B->dP, l, j, eadd, (const int*)B->d_act, nA);
+        if (nbt)
+            launch_b(B, k_big_b, dim3(std::min(B->big_grid, nbt)), dim3(kBigThreads), kBigSmem, true,
+                     (const BProb*)B->dP, l, j, eadd, bt, nbt);
+        return;
+    }
     // E'-row-slot variant (2 CTAs/SM) when the batch's blocks outnumber 1 CTA/SM (kDfEsMinBig)
     if (nbt >= kDfEsMinBig)
         launch_b(B, k_sweep_df_b<true>, dim3(B->df_grid_es), dim3(32 * kDfWarps), kDfSmemES, true,
@@ -704,6 +784,17 @@ int ibmg_batch_create(const ibmg_params* p, int nslots, ibmg_batch** out) {
         }
         CK(cudaFuncSetAttribute(k_coarse_cycle_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(coarse_smem(B->ctx[0]))));
+        CK(cudaFuncSetAttribute(k_plain_b, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPdfSmem)));
+        CK(cudaFuncSetAttribute(k_big_b, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
+        {
+            int per_sm = 0, sms = 0;
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_b, 32, kPdfSmem));
+            B->pdf_grid = std::max(1, per_sm * sms);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_b, kBigThreads, kBigSmem));
+            B->big_grid = std::max(1, per_sm * sms);
+        }
+        if (const char* e = std::getenv("IBMG_BATCH_SPLIT")) B->split = std::atoi(e) != 0;
         CK(cudaStreamCreateWithFlags(&B->s, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&B->ev_dots, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&B->ev_done, cudaEventDisableTiming));
