@@ -697,8 +697,12 @@ void coarse_inverse_forked(ibmg_ctx* c) {
     CK(cudaEventRecord(c->ev_fork, c->s));
     CK(cudaStreamWaitEvent(c->s2, c->ev_fork, 0));
     std::swap(c->s, c->s2);
-    LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
-           c->err_flag);
+    if (c->gj_regs && m <= 56)
+        LAUNCH(c, k_coarse_inverse<true>, 1, 64, size_t(56) * gj_ld(56) * sizeof(double), lb.L, lb.FL, lb.E,
+               c->Acoarse, c->err_flag);
+    else
+        LAUNCH(c, k_coarse_inverse<false>, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E,
+               c->Acoarse, c->err_flag);
     std::swap(c->s, c->s2);
     CK(cudaEventRecord(c->ev_join, c->s2));
 }
@@ -1067,8 +1071,12 @@ void rebuild(ibmg_ctx* c, bool defer_check = false) {
     if (!coarse_forked) {
         LevelBuf& lb = c->lev.back();
         const int m = 3 * lb.L.nn + 1;
-        LAUNCH(c, k_coarse_inverse, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E, c->Acoarse,
-               c->err_flag);
+        if (c->gj_regs && m <= 56)
+            LAUNCH(c, k_coarse_inverse<true>, 1, 64, size_t(56) * gj_ld(56) * sizeof(double), lb.L, lb.FL, lb.E,
+                   c->Acoarse, c->err_flag);
+        else
+            LAUNCH(c, k_coarse_inverse<false>, 1, 256, size_t(m) * gj_ld(m) * sizeof(double), lb.L, lb.FL, lb.E,
+                   c->Acoarse, c->err_flag);
     }
     // levels whose restriction takes E' from the assembled rows (points far
     // outnumber the level's E-active faces): zero their E'w scratch (the face
@@ -2068,7 +2076,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
         CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         CK(cudaFuncSetAttribute(k_block_inverse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
         CK(cudaFuncSetAttribute(k_block_inverse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
-        CK(cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * gj_ld(49) * 8));
+        CK(cudaFuncSetAttribute(k_coarse_inverse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 49 * gj_ld(49) * 8));
+        CK(cudaFuncSetAttribute(k_coarse_inverse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * gj_ld(56) * 8));
         CK(cudaFuncSetAttribute(k_big_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBigSmem)));
         {
             int per_sm = 0, sms = 0;

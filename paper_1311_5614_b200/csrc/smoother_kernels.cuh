@@ -1146,7 +1146,11 @@ struct BInvLevels {
 // 2 warps and ~150 registers per matrix: ~7 matrices in flight per SM, where
 // the 256-thread [A | I] form (gauss_jordan) is barrier-bound at 3.
 // M: the assembled A (row stride gj_ld(56)); out: inverse, column-major.
-__device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M, double* __restrict__ out, int* err) {
+// mo <= 56: the matrix is the leading mo x mo block of M, padded with the
+// identity (block-diagonal: the padding never pivots for the first mo columns
+// and stays apart); out gets the mo x mo inverse, column-major with ld mo.
+__device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M, double* __restrict__ out, int* err,
+                                                    int mo = 56) {
     constexpr int m = 56, LD = gj_ld(56);
     __shared__ double prow[m];  // the pivot row, unscaled
     __shared__ double pinv;
@@ -1156,7 +1160,7 @@ __device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M
     const bool act = t < m;
     double a[m];
 #pragma unroll
-    for (int c = 0; c < m; ++c) a[c] = act ? M[t * LD + c] : 0.0;
+    for (int c = 0; c < m; ++c) a[c] = !act ? 0.0 : (t < mo && c < mo) ? M[t * LD + c] : (c == t ? 1.0 : 0.0);
     bool used = !act;
     // 7 rounds of 8 steps: inside a round the pivot column is a[s] (static),
     // after it the row rotates by 8 columns
@@ -1214,8 +1218,11 @@ __device__ __forceinline__ void gauss_jordan56_regs(const double* __restrict__ M
     // (r = stepof[q]) writes column pivrow[j] of the inverse from its a[j]
     if (act) {
         const int r = stepof[t];
+        if (r < mo) {
 #pragma unroll
-        for (int j = 0; j < m; ++j) out[(size_t)pivrow[j] * m + r] = a[j];
+            for (int j = 0; j < m; ++j)
+                if (j < mo) out[(size_t)pivrow[j] * mo + r] = a[j];
+        }
     }
 }
 
@@ -1343,10 +1350,12 @@ __global__ void __launch_bounds__(RG ? 64 : 256, RG ? 4 : 1) k_block_inverse(BIn
 
 // Coarsest level (n = 4): dense bordered operator [A e; e^T 0] (mean-zero
 // pressure constraint), 49 x 49, inverted; stored col-major.
-__global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict__ Ainv, int* err) {
+template <bool RG>
+__global__ void __launch_bounds__(RG ? 64 : 256) k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict__ Ainv,
+                                                                   int* err) {
     pdl_enter();
     extern __shared__ double M[];
-    const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = gj_ld(m), t = threadIdx.x, nt = blockDim.x;
+    const int n = L.n, nn = L.nn, m = 3 * nn + 1, ld = RG ? gj_ld(56) : gj_ld(m), t = threadIdx.x, nt = blockDim.x;
     for (int idx = t; idx < m * ld; idx += nt) M[idx] = 0.0;
     __syncthreads();
     if (t < 3 * nn) {
@@ -1365,7 +1374,8 @@ __global__ void k_coarse_inverse(Lev L, FaceList FL, EMat E, double* __restrict_
         for (int e = E.rp[q]; e < E.rp[q + 1]; ++e) M[r * ld + E.col[e]] -= E.val[e];
     }
     __syncthreads();
-    gauss_jordan(M, m, Ainv, err);
+    if (RG) gauss_jordan56_regs(M, Ainv, err, m);  // m = 49 <= 56: identity-padded
+    else gauss_jordan(M, m, Ainv, err);
 }
 
 // E' row range (begin, end) of each of the 40 velocity DOFs of every big block
