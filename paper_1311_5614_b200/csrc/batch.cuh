@@ -537,13 +537,17 @@ void batch_vcycle(ibmg_batch* B, int j, int nA, std::vector<unsigned>& eadd) {
 template <int KM>
 void batch_ortho_k(ibmg_batch* B, int k, int ld, int more, int nA) {
     using namespace ibmg;
-    launch_b(B, k_ortho_dots_b<KM>, dim3(ortho_dots_blocks<KM>(), nA), dim3(kRedThreads), 0, false,
+    const size_t M = B->ctx[0]->Mk;
+    const bool sm = B->ctx[0]->small_ortho;
+    launch_b(B, k_ortho_dots_b<KM>, dim3(sm ? ortho_dots_grid<KM>(M) : ortho_dots_blocks<KM>(), nA), dim3(kRedThreads), 0, false,
              (const BProb*)B->dP, k, ld, (const int*)B->d_act);
 }
 template <int KM>
 void batch_update_k(ibmg_batch* B, int k, int ld, int more, int nA) {
     using namespace ibmg;
-    launch_b(B, k_ortho_update_b<KM>, dim3(kCgsBlocks, nA), dim3(kRedThreads), 0, false, (const BProb*)B->dP, k, ld,
+    const size_t M = B->ctx[0]->Mk;
+    const bool sm = B->ctx[0]->small_ortho;
+    launch_b(B, k_ortho_update_b<KM>, dim3(sm ? ortho_update_grid(M) : kCgsBlocks, nA), dim3(kRedThreads), 0, false, (const BProb*)B->dP, k, ld,
              more, (const int*)B->d_act);
 }
 void batch_ortho(ibmg_batch* B, int k, int ld, int more, int nA) {
