@@ -538,16 +538,16 @@ template <int KM>
 void batch_ortho_k(ibmg_batch* B, int k, int ld, int more, int nA) {
     using namespace ibmg;
     const size_t M = B->ctx[0]->Mk;
-    const bool sm = B->ctx[0]->small_ortho;
-    launch_b(B, k_ortho_dots_b<KM>, dim3(sm ? ortho_dots_grid<KM>(M) : ortho_dots_blocks<KM>(), nA), dim3(kRedThreads), 0, false,
+    const int pc = B->ctx[0]->ortho_per_cta;
+    launch_b(B, k_ortho_dots_b<KM>, dim3(ortho_dots_grid<KM>(M, pc), nA), dim3(kRedThreads), 0, false,
              (const BProb*)B->dP, k, ld, (const int*)B->d_act);
 }
 template <int KM>
 void batch_update_k(ibmg_batch* B, int k, int ld, int more, int nA) {
     using namespace ibmg;
     const size_t M = B->ctx[0]->Mk;
-    const bool sm = B->ctx[0]->small_ortho;
-    launch_b(B, k_ortho_update_b<KM>, dim3(sm ? ortho_update_grid(M) : kCgsBlocks, nA), dim3(kRedThreads), 0, false, (const BProb*)B->dP, k, ld,
+    const int pc = B->ctx[0]->ortho_per_cta;
+    launch_b(B, k_ortho_update_b<KM>, dim3(ortho_update_grid(M, pc), nA), dim3(kRedThreads), 0, false, (const BProb*)B->dP, k, ld,
              more, (const int*)B->d_act);
 }
 void batch_ortho(ibmg_batch* B, int k, int ld, int more, int nA) {

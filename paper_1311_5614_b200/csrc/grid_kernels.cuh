@@ -716,8 +716,9 @@ __global__ void k_finish_dots(const double* __restrict__ partial, int nblk, doub
 // Per-block partial sums are reduced in a fixed order (warp butterfly, then
 // the warps in index order), so the dots are deterministic.
 constexpr int kCgsBlocks = 592;  // 4 per SM; fixed => reduction order fixed
-inline int ortho_update_grid(size_t m) {
-    const int b = int(m / 4096);
+inline int ortho_update_grid(size_t m, int per_cta) {
+    if (per_cta <= 0) return kCgsBlocks;
+    const int b = int(m / size_t(per_cta));
     return b < 16 ? 16 : (b > kCgsBlocks ? kCgsBlocks : b);
 }
 template <int MODE, int KMAX>
@@ -809,14 +810,14 @@ __global__ void __launch_bounds__(kRedThreads, (MODE == 1 ? 2 : 4) / (KMAX > 16 
 template <int KMAX>
 constexpr int ortho_dots_blocks() { return KMAX > 16 ? 2 * 148 : 3 * 148; }
 // CTAs of the two passes for Krylov vectors of m doubles: the counts above
-// (kCgsBlocks for the update) on large vectors, about 4096 doubles per CTA
-// on small ones (C2 / C5: 48 CTAs with many loads in flight each, instead of
+// (kCgsBlocks for the update) on large vectors, about per_cta doubles per CTA
+// on small ones (C2 / C5: 96 CTAs with many loads in flight each, instead of
 // hundreds of CTAs doing one load round each).  A function of m only, so a
 // problem's reduction order is the same in a batch and in its own context.
-constexpr int kOrthoPerCta = 4096;
 template <int KMAX>
-inline int ortho_dots_grid(size_t m) {
-    const int b = int(m / kOrthoPerCta);
+inline int ortho_dots_grid(size_t m, int per_cta) {
+    if (per_cta <= 0) return ortho_dots_blocks<KMAX>();
+    const int b = int(m / size_t(per_cta));
     return b < 16 ? 16 : (b > ortho_dots_blocks<KMAX>() ? ortho_dots_blocks<KMAX>() : b);
 }
 // bid / nb: this CTA's index and the CTA count of the pass (bid and

@@ -207,7 +207,7 @@ struct ibmg_ctx {
     double rr_csr_ratio = 2.0;  // a level is point-dense when ratio x its E-active faces < points (IBMG_RR_CSR_RATIO)
     int df_grid_max = 1;    // co-resident CTAs of the dataflow sweep
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
-    bool small_ortho = true;  // CGS2 passes with ~4096 doubles per CTA on small vectors (IBMG_SMALL_ORTHO=0: fixed grids)
+    int ortho_per_cta = 2048;  // CGS2 grid: ~this many doubles per CTA on small vectors (IBMG_ORTHO_PER_CTA; 0: fixed grids)
     bool tma = true;        // TMA staging of the interior tiles' w regions in k_plain_df (IBMG_TMA=0: cp.async)
     bool gather_first = false; // fused apply / restriction: gathers before the grid CTAs (IBMG_GF=1); measured
                                // slower (C4 restriction 24 -> 40 ms: the grid CTAs wait holding their SMs)
@@ -1672,12 +1672,12 @@ double now_ms() {
 // k_ortho_update): k = j + 1 basis slots, the last one holding q.
 template <int KM>
 void ortho_dots_k(ibmg_ctx* c, int k, double* w) {
-    LAUNCH(c, (k_ortho_dots<KM>), c->small_ortho ? ortho_dots_grid<KM>(c->Mk) : ortho_dots_blocks<KM>(), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
+    LAUNCH(c, (k_ortho_dots<KM>), ortho_dots_grid<KM>(c->Mk, c->ortho_per_cta), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
            c->partial, c->dh, c->prm.restart + 2, c->ticket);
 }
 template <int KM>
 void ortho_update_k(ibmg_ctx* c, int k, const double* w, double* w1out, double* zero) {
-    LAUNCH(c, (k_ortho_update<KM>), c->small_ortho ? ortho_update_grid(c->Mk) : kCgsBlocks, kRedThreads, 0, c->V, c->Mst, k, w, w1out, zero, c->Mk, c->partial,
+    LAUNCH(c, (k_ortho_update<KM>), ortho_update_grid(c->Mk, c->ortho_per_cta), kRedThreads, 0, c->V, c->Mst, k, w, w1out, zero, c->Mk, c->partial,
            c->dh, c->prm.restart + 2, c->ticket);
 }
 void ortho_dots(ibmg_ctx* c, int k, double* w) {
@@ -2063,7 +2063,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_GJ256")) c->gj_regs = std::atoi(e) == 0;
     if (const char* e = std::getenv("IBMG_GF")) c->gather_first = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_TMA")) c->tma = std::atoi(e) != 0;
-    if (const char* e = std::getenv("IBMG_SMALL_ORTHO")) c->small_ortho = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_ORTHO_PER_CTA")) c->ortho_per_cta = std::atoi(e);
     c->prm = *p;
     c->krows = krows;
     try {
