@@ -4,6 +4,7 @@
 // Geometry is the reference's Dirichlet unit square: nx = ny = n, h = 1/n,
 // origin 0; vectors use the reference's packed interior ordering
 // (geometry.hpp:54-72); one closed fiber (m2 = 1, periodic_s1).
+#include <cmath>
 #include <cstring>
 #include <exception>
 #include <vector>
@@ -200,6 +201,82 @@ int ref_saddle_apply(int n, int m1, double ds, const double* X, double gamma, do
         SaddleSystem S(g, VelocityBC::zero(), alpha, std::move(E));
         DofMap dm(g);
         S.apply(std::span<const double>(w, dm.n_total()), std::span<double>(out, dm.n_total()));
+        return 0;
+    } catch (const std::exception&) { return 1; }
+}
+
+// ---- Dirichlet paper-mode pins (thick m1 x m2 mesh, walls included) -------
+namespace {
+FiberMesh mesh2(int m1, int m2, double ds, const double* X) {
+    FiberMesh M(m1, m2, ds, true);
+    for (int l = 0; l < m2; ++l)
+        for (int k = 0; k < m1; ++k) M.X.at(k, l) = Vec2{X[2 * (k + size_t(l) * m1)], X[2 * (k + size_t(l) * m1) + 1]};
+    return M;
+}
+VelocityBC lid_bc() {
+    return VelocityBC{[](double x, double y) { return y >= 1.0 ? (1.0 - std::cos(2.0 * 3.14159265358979323846 * x)) / 2.0 : 0.0; },
+                      [](double, double) { return 0.0; }};
+}
+}  // namespace
+
+// assemble_saddle_matrix (assembly.cpp:5-65) of SaddleSystem(g, bc, alpha, assemble_elasticity(mesh, g, 1)).
+long ref_assemble_saddle_m2(int n, int m1, int m2, double ds, const double* X, double alpha, int* rows, int* cols,
+                            double* vals, long cap) {
+    try {
+        GridGeometry g = geom(n);
+        ElasticityOperator E = (alpha > 0) ? assemble_elasticity(mesh2(m1, m2, ds, X), g, 1.0) : ElasticityOperator{};
+        SaddleSystem S(g, VelocityBC::zero(), alpha, std::move(E));
+        return dump(assemble_saddle_matrix(S), rows, cols, vals, cap);
+    } catch (const std::exception&) { return -1; }
+}
+
+// Galerkin-coarsened elasticity (transfers.cpp:286-293) `levels` times.  The v block
+// goes through the packed prolongation's wrong weight (transfers.cpp:202); the u block is exact.
+long ref_galerkin_elasticity_m2(int n, int m1, int m2, double ds, const double* X, int levels, int* rows, int* cols,
+                                double* vals, long cap) {
+    try {
+        GridGeometry g = geom(n);
+        SparseOperator E = assemble_elasticity(mesh2(m1, m2, ds, X), g, 1.0).matrix;
+        for (int l = 0; l < levels; ++l) {
+            E = galerkin_coarsen_elasticity(E, g);
+            g = g.coarsened();
+        }
+        return dump(E, rows, cols, vals, cap);
+    } catch (const std::exception&) { return -1; }
+}
+
+// build_rhs (saddle.cpp:96-104) with the lid-driven cavity data.
+int ref_build_rhs_lid(int n, int m1, int m2, double ds, const double* X, double gamma, double* out) {
+    try {
+        GridGeometry g = geom(n);
+        SaddleSystem S(g, lid_bc(), 0.0, ElasticityOperator{});
+        FiberMesh M = mesh2(m1, m2, ds, X);
+        std::vector<double> b = build_rhs(S, &M, gamma);
+        std::memcpy(out, b.data(), b.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception&) { return 1; }
+}
+
+// spread / interpolate on the thick mesh (fiber.cpp:89-140), packed velocities.
+int ref_spread_m2(int n, int m1, int m2, double ds, const double* X, const double* F, double* f_vel) {
+    try {
+        FiberMesh M = mesh2(m1, m2, ds, X);
+        LagrangianField L(m1, m2);
+        for (size_t q = 0; q < size_t(m1) * m2; ++q) L.val[q] = Vec2{F[2 * q], F[2 * q + 1]};
+        std::vector<double> f = pack_velocity(spread(M, L, geom(n)));
+        std::memcpy(f_vel, f.data(), f.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception&) { return 1; }
+}
+int ref_interpolate_m2(int n, int m1, int m2, double ds, const double* X, const double* vel, double* U) {
+    try {
+        DofMap dm(geom(n));
+        FiberMesh M = mesh2(m1, m2, ds, X);
+        LagrangianField L = interpolate(M, unpack_velocity(geom(n), std::span<const double>(vel, dm.n_vel())));
+        for (size_t q = 0; q < size_t(m1) * m2; ++q) {
+            U[2 * q] = L.val[q].x;
+            U[2 * q + 1] = L.val[q].y;
+        }
         return 0;
     } catch (const std::exception&) { return 1; }
 }

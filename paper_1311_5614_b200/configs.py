@@ -145,3 +145,36 @@ def config5_problem(index: int, N: int = 256, nb: int = 512) -> Problem:
 def small_problem(N=32, nb=64, kappa=1e2, dt=1e-2, a=0.3, b=0.15, cx=0.5, cy=0.5, rot=0.0) -> Problem:
     X, ds, _ = ellipse_points(cx, cy, a, b, nb, rot=rot)
     return Problem(f"small(N={N})", N, 1.0, 1.0, dt, [nb], [kappa], [ds], X, steps=1)
+
+
+# ---- paper-reproduction mode
+
+#: Table 1: largest stable alpha = gamma dt of the explicit scheme.
+PAPER_ALPHA_EXP = {32: 6.09, 64: 3.93, 128: 2.82, 256: 2.28}
+
+
+@dataclass
+class AnnulusMesh:
+    """Thick fiber mesh (fiber.hpp:36-50): node (k, l) at X[k + l * m1], closed in s1."""
+    N: int
+    m1: int
+    m2: int
+    ds: float
+    X: np.ndarray  # (m1 * m2, 2)
+
+
+def paper_annulus(N: int, centre=(0.5, 0.5), r: float = 0.25, w: float = 1.0 / 16) -> AnnulusMesh:
+    """The annulus of Eq. 21: X(s1, s2) = centre + (r + s2)(cos(s1/r), sin(s1/r)) with
+    M1 = 19N/8 nodes in s1, M2 = 3N/32 + 1 rings across the thickness w and
+    ds = 2 pi r / M1."""
+    if (19 * N) % 8 or (3 * N) % 32:
+        raise ValueError("M1 = 19N/8 and M2 = 3N/32 + 1 must be integers")
+    m1, m2 = 19 * N // 8, 3 * N // 32 + 1
+    ds = 2 * math.pi * r / m1
+    k = np.arange(m1)
+    X = np.empty((m2, m1, 2))
+    for l in range(m2):
+        rad = r + l * (w / (m2 - 1))
+        X[l, :, 0] = centre[0] + rad * np.cos(k * ds / r)
+        X[l, :, 1] = centre[1] + rad * np.sin(k * ds / r)
+    return AnnulusMesh(N, m1, m2, ds, X.reshape(-1, 2))
