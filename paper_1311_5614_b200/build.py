@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libibmg_b200.so")
-SRCS = ["ibmg.cu"]
-DEPS = ["ibmg.cu", "common.cuh", "cluster_kernel.cuh", "batch.cuh", "grid_kernels.cuh", "ib_kernels.cuh", "smoother_kernels.cuh", "coarse_kernel.cuh",
+SRCS = ["ibmg.cu", "paper_mode.cu"]
+DEPS = ["ibmg.cu", "paper_mode.cu", "common.cuh", "cluster_kernel.cuh", "batch.cuh", "grid_kernels.cuh", "ib_kernels.cuh", "smoother_kernels.cuh", "coarse_kernel.cuh",
         "slab_group.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
@@ -34,7 +34,7 @@ def stale(target, deps) -> bool:
 
 
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
-    deps = [os.path.join(HERE, "csrc", d) for d in DEPS] + [os.path.join(ROOT, "include", "ibmg_gpu.h")]
+    deps = [os.path.join(HERE, "csrc", d) for d in DEPS] + [os.path.join(ROOT, "include", "ibmg_gpu.h"), os.path.join(ROOT, "include", "ibmg_paper.h")]
     if force or stale(LIB, deps):
         cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(HERE, "csrc", s) for s in SRCS] + ["-ldl"]
         if verbose:

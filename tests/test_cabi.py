@@ -13,8 +13,8 @@ from paper_1311_5614_b200 import ibmg
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared():
-    src = open(os.path.join(ROOT, "include", "ibmg_gpu.h")).read()
+def declared(header="ibmg_gpu.h"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(ibmg_[a-z_]+)\s*\(", src)))
 
@@ -26,6 +26,26 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
     assert set(ibmg.EXPORTS) == set(names)
+
+
+def test_library_exports_the_paper_mode_abi():
+    """include/ibmg_paper.h: every symbol exported, arguments validated
+    like the reference's constructors before any CUDA call, null handles rejected."""
+    from paper_1311_5614_b200 import paper
+    L = paper.lib()
+    names = declared("ibmg_paper.h")
+    assert not [n for n in names if not hasattr(L, n)]
+    assert set(paper.EXPORTS) == set(names)
+    for bad in (dict(N=12), dict(N=4), dict(box=3), dict(box=32), dict(alpha=-1.0), dict(nu1=0, nu2=0),
+                dict(coarsest_n=3)):
+        p = dict(N=32, box=4, nu1=1, nu2=1, coarsest_n=4, alpha=1.0, device=0)
+        p.update(bad)
+        h = C.c_void_p()
+        assert L.ibmg_paper_create(C.byref(paper.PaperParams(**p)), C.byref(h)) == 1 and not h.value, bad
+    x = np.zeros(4)
+    assert L.ibmg_paper_num_levels(None) == -1 and L.ibmg_paper_level_n(None, 0) == -1
+    assert L.ibmg_paper_apply(None, 0, x.ctypes.data, x.ctypes.data) == 1
+    assert L.ibmg_paper_last_error(None) == b"null context"
 
 
 def test_library_is_sm100a():
