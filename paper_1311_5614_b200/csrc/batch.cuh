@@ -416,7 +416,7 @@ void batch_table(ibmg_batch* B, int count) {
                 BL.G = Gather{nx.FL, nx.W, c->F, nx.b, nx.L.nn, 1.0, 0, nullptr, 0ull};
                 BL.G.sub = nx.maxrow <= 32 ? 8 : 32;
                 if (BL.pf.nblk) {
-                    BL.G.nblk = int(nblk(nx.FL.nf, kPfPerCta * (32 / BL.G.sub)));
+                    BL.G.nblk = int(nblk(nx.FL.nf, gather_faces_per_cta(BL.G.sub)));
                     BL.G.target = (unsigned long long)(BL.pf.nblk + BL.ngrid);
                 }
                 BL.total = BL.pf.nblk + BL.ngrid + BL.G.nblk;
@@ -430,7 +430,7 @@ void batch_table(ibmg_batch* B, int count) {
         P.aG = Gather{l0.FL, l0.W, c->F, c->wv, l0.L.nn, -1.0, 0, nullptr, 0ull};
         P.aG.sub = l0.maxrow <= 32 ? 8 : 32;
         if (P.apf.nblk) {
-            P.aG.nblk = int(nblk(l0.FL.nf, kPfPerCta * (32 / P.aG.sub)));
+            P.aG.nblk = int(nblk(l0.FL.nf, gather_faces_per_cta(P.aG.sub)));
             P.aG.target = (unsigned long long)(P.apf.nblk + P.ang);
         }
         P.atotal = P.apf.nblk + P.ang + P.aG.nblk;

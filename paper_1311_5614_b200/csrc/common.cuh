@@ -197,6 +197,74 @@ __device__ __forceinline__ void face_gather_sub(const FaceList& FL, const Win& W
     }
 }
 
+// NF consecutive faces per 8-lane group, the loads of all NF chains issued together
+// (face -> offsets -> entries -> weights and forces).  Per face the arithmetic is
+// face_gather_sub<8>'s: lane gl adds entries off + gl, off + gl + 8, ... in order, then
+// the xor tree over the 8 lanes; lane f of the group updates face f.  Rows outside
+// [jlo, jhi) are skipped (slab mode).  All 32 lanes must call it.
+template <int NF>
+__device__ __forceinline__ void face_gather_multi(const FaceList& FL, const Win& W, const double* __restrict__ F,
+                                                  double* __restrict__ out, int nn, double sign, int q0, int gl,
+                                                  bool assign, int lg, int jlo, int jhi) {
+    double s[NF];
+    int face[NF], e[NF], e1[NF], comp[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        s[f] = 0.0;
+        face[f] = -1;
+        e[f] = e1[f] = 0;
+        comp[f] = 0;
+        if (q0 + f < FL.nf) {
+            face[f] = FL.face[q0 + f];
+            e[f] = FL.off[q0 + f] + gl;
+            e1[f] = FL.off[q0 + f + 1];
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+        if (face[f] >= 0) {
+            comp[f] = face[f] >= nn;
+            if (jlo > 0 || jhi < (1 << 30)) {
+                const int row = (face[f] & (nn - 1)) >> lg;
+                if (row < jlo || row >= jhi) face[f] = -1, e1[f] = 0;
+            }
+        }
+    while (true) {
+        int v[NF];
+        bool on[NF], any = false;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            on[f] = e[f] < e1[f];
+            any |= on[f];
+            v[f] = on[f] ? FL.ent[e[f]] : 0;
+        }
+        if (!any) break;
+        double a[NF], ff[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const int k = v[f] >> 5;
+            a[f] = on[f] ? W.w[(size_t)k * 64 + (v[f] & 31)] : 0.0;
+            ff[f] = on[f] ? F[2 * k + comp[f]] : 0.0;
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            if (on[f]) {
+                s[f] += a[f] * ff[f];
+                e[f] += 8;
+            }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) s[f] += __shfl_xor_sync(0xffffffffu, s[f], o);
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+        if (gl == f && face[f] >= 0) {
+            if (assign) out[face[f]] = sign * s[f];
+            else out[face[f]] += sign * s[f];
+        }
+}
+
 // one warp per face (k_face_gather: RHS forces, spread)
 __device__ __forceinline__ void face_gather_warp(const FaceList& FL, const Win& W, const double* __restrict__ F,
                                                  double* __restrict__ out, int nn, double sign, int q, int lane) {

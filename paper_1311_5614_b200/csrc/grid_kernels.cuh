@@ -72,29 +72,48 @@ struct Gather {
     // face scratch; the grid CTAs add it after `target` (all gathers done)
     unsigned long long target_pf = 0;
 };
-constexpr int kPfPerCta = 8;  // 256-thread CTAs, a warp per point / per face
+constexpr int kPfPerCta = 8;  // 256-thread CTAs: 8 warps
+// Latency-bound chains (origin -> weights / field values -> sum) need several in
+// flight per warp: a warp takes kPfPts consecutive points, an 8-lane group of a
+// gather CTA kGaFaces consecutive faces, every load of the batch issued before the
+// first use (the fused kernels carry the tiles' 30 KB of shared memory and 64
+// registers, so only 32 warps per SM are resident: at one chain per warp the C4
+// fine level's 222k points and 1.1M faces cost 0.10 + 0.31 ms per apply).
+constexpr int kPfPts = 4;
+constexpr int kGaFaces = 4;
+__host__ __device__ inline int pf_points_per_cta() { return kPfPerCta * kPfPts; }
+__host__ __device__ inline int gather_faces_per_cta(int sub) { return sub == 8 ? kPfPerCta * 4 * kGaFaces : kPfPerCta; }
 
 __device__ __forceinline__ void point_force_warp(const PForce& pf, int bid) {
-    const int k = bid * kPfPerCta + (threadIdx.x >> 5);
-    if (k >= pf.P.n) return;
+    const int k0 = (bid * kPfPerCta + (threadIdx.x >> 5)) * kPfPts;
+    if (k0 >= pf.P.n) return;
     const int lane = threadIdx.x & 31, comp = lane >> 4, e = lane & 15;
     const int n = pf.n;
     const double* wc = pf.w + (size_t)comp * n * n;
-    const int ks[3] = {pf.P.kprev[k], k, pf.P.knext[k]};
-    double u[3];
+    double u[kPfPts][3];
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        const int kk = ks[t];
-        const int4 o = pf.W.orgR[kk];
-        const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
-        u[t] = pf.W.w[(size_t)kk * 64 + (2 + comp) * 16 + e] *
-               __ldg(wc + wr(i0 + (e & 3), n) + (size_t)wr(j0 + (e >> 2), n) * n);
+    for (int q = 0; q < kPfPts; ++q) {
+        const int k = k0 + q < pf.P.n ? k0 + q : pf.P.n - 1;  // clamped: the tail repeats the last point (not stored)
+        const int ks[3] = {pf.P.kprev[k], k, pf.P.knext[k]};
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int kk = ks[t];
+            const int4 o = pf.W.orgR[kk];
+            const int i0 = comp ? o.z : o.x, j0 = comp ? o.w : o.y;
+            u[q][t] = pf.W.w[(size_t)kk * 64 + (2 + comp) * 16 + e] *
+                      __ldg(wc + wr(i0 + (e & 3), n) + (size_t)wr(j0 + (e >> 2), n) * n);
+        }
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
-        for (int t = 0; t < 3; ++t) u[t] += __shfl_xor_sync(0xffffffffu, u[t], o);
-    if (e == 0) pf.F[2 * k + comp] = pf.P.cE[k] * (u[0] - 2.0 * u[1] + u[2]);
+        for (int q = 0; q < kPfPts; ++q)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) u[q][t] += __shfl_xor_sync(0xffffffffu, u[q][t], o);
+    if (e == 0)
+#pragma unroll
+        for (int q = 0; q < kPfPts; ++q)
+            if (k0 + q < pf.P.n) pf.F[2 * (k0 + q) + comp] = pf.P.cE[k0 + q] * (u[q][0] - 2.0 * u[q][1] + u[q][2]);
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -112,14 +131,18 @@ __device__ __forceinline__ void fused_launch_at(const PForce& pf, const Gather& 
             while (ld_acquire_u64(G.cnt) < G.target) __nanosleep(32);
         __syncthreads();
         const int lane = threadIdx.x & 31;
-        const int q = ((bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5)) * (32 / G.sub) + lane / G.sub;
+        if (G.sub == 8) {
+            const int q = (((bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5)) * 4 + (lane >> 3)) * kGaFaces;
+            face_gather_multi<kGaFaces>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, lane & 7, false, G.lg, G.jlo, G.jhi);
+            return;
+        }
+        const int q = (bid - pf.nblk - ngrid) * kPfPerCta + (threadIdx.x >> 5);
         bool active = q < G.FL.nf;
         if (active && (G.jlo > 0 || G.jhi < (1 << 30))) {
             const int row = (G.FL.face[q] & (G.nn - 1)) >> G.lg;
             active = row >= G.jlo && row < G.jhi;
         }
-        if (G.sub == 8) face_gather_sub<8>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane & 7);
-        else face_gather_sub<32>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane);
+        face_gather_sub<32>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane);
         return;
     }
     if (bid < pf.nblk) point_force_warp(pf, bid);
@@ -161,10 +184,13 @@ __device__ __forceinline__ void fused_launch_gf(const PForce& pf, const Gather& 
             while (ld_acquire_u64(G.cnt) < G.target_pf) __nanosleep(32);
         __syncthreads();
         const int lane = threadIdx.x & 31;
-        const int q = ((bid - pf.nblk) * kPfPerCta + (threadIdx.x >> 5)) * (32 / G.sub) + lane / G.sub;
-        const bool active = q < G.FL.nf;
-        if (G.sub == 8) face_gather_sub<8>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane & 7, true);
-        else face_gather_sub<32>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, active, lane, true);
+        if (G.sub == 8) {
+            const int q = (((bid - pf.nblk) * kPfPerCta + (threadIdx.x >> 5)) * 4 + (lane >> 3)) * kGaFaces;
+            face_gather_multi<kGaFaces>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, lane & 7, true, 0, 0, 1 << 30);
+        } else {
+            const int q = (bid - pf.nblk) * kPfPerCta + (threadIdx.x >> 5);
+            face_gather_sub<32>(G.FL, G.W, G.F, G.out, G.nn, G.sign, q, q < G.FL.nf, lane, true);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();

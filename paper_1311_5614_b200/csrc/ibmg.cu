@@ -201,6 +201,7 @@ struct ibmg_ctx {
     bool rr_tiled = true;   // tiled residual + restriction where the coarse side is >= 32 (IBMG_RR_TILED=0: off)
     bool rr_csr = true;     // ... with E' from the assembled rows on point-dense levels (IBMG_RR_CSR=0: off)
     bool ap_tiled = true;   // tiled operator apply where n >= 64 (IBMG_AP_TILED=0: off)
+    int debug_e = 0;        // IBMG_DEBUG_E (timing experiments, results wrong): 1 no gather CTAs, 2 no point-force CTAs either
     bool ortho2 = true;     // FGMRES with the two-pass lagged CGS2 (IBMG_CGS2=1: three-sweep CGS2)
     int canon_inv = -1;     // box inverses in block-id order during the colouring: -1 auto (>= 2^15
                             // blocks over all levels, single contexts), IBMG_CANON_INV=1 on, 0 off
@@ -1196,7 +1197,8 @@ void set_structures(ibmg_ctx* c, int n_mem, const int* nb, const double* kappa, 
 // none when the level has no E'-active faces.
 PForce pforce(ibmg_ctx* c, const LevelBuf& lb, const double* w, bool active) {
     PForce pf{lb.W, c->P, lb.L.n, w, c->F, 0};
-    if (c->npts && active) pf.nblk = int(nblk(c->npts, kPfPerCta));
+    if (c->npts && active) pf.nblk = int(nblk(c->npts, pf_points_per_cta()));
+    if (c->debug_e >= 2) pf.nblk = 0;  // timing experiments only (IBMG_DEBUG_E): wrong results
     return pf;
 }
 
@@ -1205,8 +1207,8 @@ PForce pforce(ibmg_ctx* c, const LevelBuf& lb, const double* w, bool active) {
 Gather gather(ibmg_ctx* c, const LevelBuf& to, double* out, double sign, const PForce& pf, int ngrid) {
     Gather G{to.FL, to.W, c->F, out, to.L.nn, sign, 0, c->tail_cnt, 0ull};
     G.sub = to.maxrow <= 32 ? 8 : 32;
-    if (pf.nblk) {
-        G.nblk = int(nblk(to.FL.nf, kPfPerCta * (32 / G.sub)));
+    if (pf.nblk && c->debug_e == 0) {
+        G.nblk = int(nblk(to.FL.nf, gather_faces_per_cta(G.sub)));
         c->tail_base += (unsigned long long)(pf.nblk + ngrid);
         G.target = c->tail_base;
     }
@@ -1219,7 +1221,7 @@ Gather gather(ibmg_ctx* c, const LevelBuf& to, double* out, double sign, const P
 Gather gather_gf(ibmg_ctx* c, const LevelBuf& to, double sign, const PForce& pf) {
     Gather G{to.FL, to.W, c->F, to.escr, to.L.nn, sign, 0, c->tail_cnt, 0ull};
     G.sub = to.maxrow <= 32 ? 8 : 32;
-    G.nblk = int(nblk(to.FL.nf, kPfPerCta * (32 / G.sub)));
+    G.nblk = int(nblk(to.FL.nf, gather_faces_per_cta(G.sub)));
     G.target_pf = c->tail_base + (unsigned long long)pf.nblk;
     c->tail_base += (unsigned long long)(pf.nblk + G.nblk);
     G.target = c->tail_base;
@@ -2053,6 +2055,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_RR_CSR")) c->rr_csr = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_RR_CSR_RATIO")) c->rr_csr_ratio = std::atof(e);
     if (const char* e = std::getenv("IBMG_AP_TILED")) c->ap_tiled = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_DEBUG_E")) c->debug_e = std::atoi(e);
     if (const char* e = std::getenv("IBMG_CGS2")) c->ortho2 = std::atoi(e) == 0;
     if (const char* e = std::getenv("IBMG_CANON_INV")) c->canon_inv = std::atoi(e) != 0 ? 1 : 0;
     if (const char* e = std::getenv("IBMG_PLAIN_DF")) c->plain_df = std::atoi(e) != 0;
