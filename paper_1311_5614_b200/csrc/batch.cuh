@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, ES ? 2 : 1)
     const int n = P[act[0]].lv[l].df.L.n, nn = n * n;
     const int nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1, nbk = n >> 2;
     double* sw = reinterpret_cast<double*>(dsm + (ES ? sizeof(ESlot) : 2 * sizeof(SlabSlot)) + wid * kDfTileStride);
-    double* sb = sw + 3 * kRegP;
+    double* sb = sw + kDfWDoubles;
     int k = blockIdx.x;  // this CTA's big tasks: k, k + G, ...
     if (k < nbt) {
         const BTask it = bt[k];
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(32) k_plain_b(const BProb* __restrict__ P, int
     pdl_enter();
     extern __shared__ __align__(128) unsigned char pdm[];
     double* sw = reinterpret_cast<double*>(pdm);
-    double* sb = sw + 3 * kRegP;
+    double* sb = sw + kDfWDoubles;
     const int n = P[act[0]].lv[l].df.L.n, nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1;
     for (int task = blockIdx.x; task < nA * ntiles; task += gridDim.x) {
         const int b = act[task % nA], loc = task / nA;

@@ -86,6 +86,50 @@ struct TileW {
         return s[f * kRegP + (j + 2) * kRegS + (i + 2)];
     }
 };
+// Optional working layout of the dataflow tiles (df_plain_tile, compile with
+// -DIBMG_RELAYOUT=1): the region is staged with 16-byte copies / tensor copies at the
+// even row stride kRegS, then moved in place to the odd row stride kRegS + 1, where
+// the 32 cells of a colour pass (all of one column parity) spread over all 16 bank
+// pairs: 2 shared-memory wavefronts per fp64 access (the minimum) instead of 4.
+// Bitwise the same sweep; measured on B200 it does not pay (C4 plain phase 12.91 ->
+// 12.73 ms per 24 launches, C3 sweeps 1.298 -> 1.308 ms, C2 step 7.22 -> 7.31 ms, C5
+// 0.677 -> 0.691 ms per problem): the tile chain is bound by instruction latency at
+// one warp per tile, not by the shared-memory pipe.  Default off.
+#ifndef IBMG_RELAYOUT
+#define IBMG_RELAYOUT 0
+#endif
+constexpr int kRegSW = IBMG_RELAYOUT ? kRegS + 1 : kRegS, kRegPW = kReg * kRegSW;
+constexpr int kDfWDoubles = 3 * kRegPW;  // w region of a dataflow tile buffer; the b region follows
+struct TileWW {
+    double* s;  // [3][kReg][kRegSW]
+    __device__ __forceinline__ double& operator()(int f, int i, int j) const {
+        return s[f * kRegPW + (j + 2) * kRegSW + (i + 2)];
+    }
+};
+// In-place move of the staged region [3][kReg][kRegS] to [3][kReg][kRegSW] (one warp):
+// planes from the last to the first, a whole plane through registers, so no source
+// is overwritten before it is read (destinations only move up).
+__device__ __forceinline__ void relayout_region(double* sw, int lane) {
+    if (kRegSW == kRegS) return;
+    constexpr int kPer = (kReg * kReg + 31) / 32;
+#pragma unroll
+    for (int f = 2; f >= 0; --f) {
+        double v[kPer];
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int e = lane + 32 * t;
+            v[t] = e < kReg * kReg ? sw[f * kRegP + (e / kReg) * kRegS + e % kReg] : 0.0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int e = lane + 32 * t;
+            if (e < kReg * kReg) sw[f * kRegPW + (e / kReg) * kRegSW + e % kReg] = v[t];
+        }
+        __syncwarp();
+    }
+}
+
 // w region of a tile (2-cell halo, 3 planes) into the TileW layout with
 // 16-byte cp.async (L1-allocating: w is not written by the launch).
 __device__ __forceinline__ void stage_w_region(double* sw, const double* __restrict__ w, int n, int nn, int x0, int y0,
@@ -701,7 +745,7 @@ struct DfArgs {
     double* w;
     unsigned long long* trace;  // debug: per-task globaltimer stamps (nullptr in production)
 };
-constexpr size_t kDfTileBytes = (3 * kRegP + 3 * 289) * sizeof(double);
+constexpr size_t kDfTileBytes = (kDfWDoubles + 3 * 289) * sizeof(double);
 constexpr size_t kDfSmem = 2 * sizeof(SlabSlot) + kDfWarps * ((kDfTileBytes + 15) / 16 * 16);
 
 __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
@@ -813,8 +857,9 @@ __device__ __forceinline__ void df_plain_tile(const Lev& L, const double* __rest
         *mphase ^= 1u;
     }
     __syncwarp();
+    relayout_region(sw, lane);
     const unsigned long long t_s = trace ? gtimer() : 0;
-    TileW W{sw};
+    TileWW W{sw};
     TileB B{sb};
     for (int pc = 0; pc < 8; ++pc) {
         const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
@@ -872,7 +917,7 @@ __global__ void __launch_bounds__(32) k_plain_df(Lev L, const double* __restrict
     extern __shared__ __align__(128) unsigned char pdm[];
     __shared__ __align__(8) unsigned long long mbar;
     double* sw = reinterpret_cast<double*>(pdm);
-    double* sb = sw + 3 * kRegP;
+    double* sb = sw + kDfWDoubles;
     const int nt = L.n / kTile, half = nt >> 1, ntiles = nt * nt;
     unsigned phase = 0;
     if (tm.use) {
@@ -905,7 +950,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, ES ? 2 : 1) k_sweep_df(DfArgs A
     const int n = L.n, nn = L.nn, t = threadIdx.x, wid = t >> 5, G = gridDim.x;
     const int nt = n / kTile, ntiles = nt * nt, per = ntiles / 4, half = nt >> 1, nbk = n >> 2;
     double* sw = reinterpret_cast<double*>(dsm + (ES ? sizeof(ESlot) : 2 * sizeof(SlabSlot)) + wid * kDfTileStride);
-    double* sb = sw + 3 * kRegP;
+    double* sb = sw + kDfWDoubles;
     const unsigned epoch = A.DP.epoch;
     // first big slab streams in while the plain tasks run
     int c = 0, q = -1;
