@@ -57,6 +57,21 @@ def build_facade_test() -> str:
     return FACADE_BIN
 
 
+PAPER_FACADE_SRC = os.path.join(ROOT, "tests", "cpp", "facade_paper.cpp")
+PAPER_FACADE_BIN = os.path.join(ROOT, "tests", "cpp", "facade_paper")
+
+
+def build_paper_facade_test() -> str:
+    """C++ caller of the paper-mode facade (include/ibmg/b200_paper.hpp)."""
+    deps = [PAPER_FACADE_SRC, LIB, os.path.join(ROOT, "include", "ibmg", "b200_paper.hpp"),
+            os.path.join(ROOT, "include", "ibmg_paper.h")]
+    if stale(PAPER_FACADE_BIN, deps):
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+        subprocess.check_call([cxx, "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"), "-o", PAPER_FACADE_BIN,
+                               PAPER_FACADE_SRC, "-L", HERE, "-libmg_b200", "-Wl,-rpath," + HERE])
+    return PAPER_FACADE_BIN
+
+
 def build_oracle() -> None:
     subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
 
@@ -64,4 +79,5 @@ def build_oracle() -> None:
 if __name__ == "__main__":
     build_cuda(force="--force" in sys.argv, verbose=True)
     build_facade_test()
+    build_paper_facade_test()
     build_oracle()

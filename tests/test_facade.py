@@ -33,3 +33,18 @@ def test_facade_step_matches_oracle():
     assert abs(np.sum(u * u) - r["u2"]) <= 1e-8 * np.sum(u * u)
     assert abs(np.sum(p * p) - r["p2"]) <= 1e-8 * np.sum(p * p)
     assert abs(np.sum(Xn) - r["xsum"]) <= 1e-12 * abs(np.sum(Xn))
+
+
+def test_paper_facade_compiles_and_links():
+    exe = build.build_paper_facade_test()
+    assert "libibmg_b200.so" in subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+
+
+@pytest.mark.gpu
+def test_paper_facade_table2_cell():
+    """include/ibmg/b200_paper.hpp from C++: Table 2's b = 4, V(1,1), relative stiffness 100
+    cell (11 iterations) and the reference's size-mismatch exception."""
+    out = subprocess.run([build.build_paper_facade_test()], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    f = out.stdout.split()
+    assert abs(int(f[1]) - 11) <= 2 and f[3] == "1" and float(f[7]) <= 1e-6 and f[9] == "1" and int(f[11]) > 0
