@@ -120,6 +120,13 @@ class CavitySystem {
         check(ibmg_paper_interpolate(ctx_, vel.data(), U.data()));
         return U;
     }
+    // iteration_matrix_spectrum: the (m+1) x m Hessenberg matrix of m Arnoldi steps
+    // on the V-cycle's error propagator; rho = max |eig(H[:done, :done])|
+    std::vector<double> iteration_matrix_hessenberg(int m, unsigned long long seed, int* done = nullptr) const {
+        std::vector<double> H(size_t(m + 1) * m);
+        check(ibmg_paper_vcycle_spectrum(ctx_, m, seed, H.data(), done));
+        return H;
+    }
     double estimate_alpha_exp(double tol = 1e-4, int max_steps = 1000, int* steps = nullptr) const {
         double a = 0.0;
         check(ibmg_paper_alpha_exp(ctx_, tol, max_steps, &a, steps));

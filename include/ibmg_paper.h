@@ -93,6 +93,12 @@ int ibmg_paper_gmres_solve(ibmg_paper* ctx, const double* b, double* x, double r
 /* estimate_alpha_exp: power iteration on S* L^-1 S A_f. */
 int ibmg_paper_alpha_exp(ibmg_paper* ctx, double tol, int max_steps, double* alpha_exp, int* steps);
 
+/* iteration_matrix_spectrum: m Arnoldi steps (CGS2) on the error
+ * propagator E x = x - v_cycle(0, A x) restricted to mean-zero pressure, from the splitmix64 start
+ * vector of `seed`; H receives the (m+1) x m Hessenberg matrix (row-major), m_done the steps taken.
+ * The spectral radius estimate is max |eig(H[:m_done, :m_done])|. */
+int ibmg_paper_vcycle_spectrum(ibmg_paper* ctx, int m, unsigned long long seed, double* H, int* m_done);
+
 long long ibmg_paper_kernel_launches(const ibmg_paper* ctx);
 
 #ifdef __cplusplus

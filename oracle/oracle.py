@@ -103,6 +103,7 @@ def lib():
         L.porc_interp.argtypes = [C.c_void_p, dp, dp]
         for f in ("porc_mg_solve", "porc_gmres_solve"):
             getattr(L, f).argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_int, C.POINTER(PorcStats), C.c_void_p, C.c_int]
+        L.porc_vcycle_spectrum.argtypes = [C.c_void_p, C.c_int, C.c_ulonglong, dp, C.POINTER(C.c_int)]
         L.porc_alpha_exp.argtypes = [C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)]
         _LIB = L
     return _LIB
@@ -335,6 +336,15 @@ class PaperOracle:
 
     def gmres_solve(self, b, rtol=1e-6, max_iter=100):
         return self._solve(lib().porc_gmres_solve, b, rtol, max_iter)
+
+    def iteration_matrix_spectrum(self, m=60, seed=1):
+        """(Ritz values by descending modulus, Hessenberg (m+1) x m) of the V-cycle's error propagator."""
+        H = np.zeros((m + 1) * m)
+        k = C.c_int()
+        self._chk(lib().porc_vcycle_spectrum(self._ctx, m, seed, H, C.byref(k)))
+        H = H.reshape(m + 1, m)
+        ritz = np.linalg.eigvals(H[: k.value, : k.value])
+        return ritz[np.argsort(-np.abs(ritz))], H
 
     def alpha_exp(self, tol=1e-4, max_steps=1000):
         a, k = C.c_double(), C.c_int()

@@ -683,6 +683,51 @@ int porc_gmres_solve(void* ctx, const double* b, double* x, double rtol, int max
     PORC_TRY(ctx, porc::gmres_solve(*static_cast<Ctx*>(ctx), b, x, rtol, max_iter, st, hist, hist_len));
 }
 
+int porc_vcycle_spectrum(void* ctx, int m, unsigned long long seed, double* H, int* m_done) {
+    Ctx& C = *static_cast<Ctx*>(ctx);
+    PORC_TRY(ctx, {
+        if (m < 2) throw std::invalid_argument("SpectrumProbe: m >= 2");
+        const porc::Level& L = C.lev[0];
+        const int n = L.d.ntot();
+        std::vector<std::vector<double>> V(1, std::vector<double>(n));
+        unsigned long long z = seed;
+        for (double& v : V[0]) {  // splitmix64 -> U[-1, 1), as the GPU probe
+            z += 0x9E3779B97F4A7C15ull;
+            unsigned long long t = z;
+            t = (t ^ (t >> 30)) * 0xBF58476D1CE4E5B9ull;
+            t = (t ^ (t >> 27)) * 0x94D049BB133111EBull;
+            t ^= t >> 31;
+            v = double(t >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+        }
+        porc::project_pressure_mean(L.d, V[0].data());
+        const double n0 = std::sqrt(porc::dotv(V[0].data(), V[0].data(), n));
+        for (double& v : V[0]) v /= n0;
+        std::fill(H, H + size_t(m + 1) * m, 0.0);
+        std::vector<double> a(n), w(n), h1(m + 1), h2(m + 1);
+        int done = 0;
+        for (int j = 0; j < m; ++j) {
+            for (int i = 0; i < n; ++i) a[i] = L.A.row_dot(i, V[j].data());
+            porc::vcycle(C, a.data(), w.data());
+            for (int i = 0; i < n; ++i) w[i] = V[j][i] - w[i];
+            porc::project_pressure_mean(L.d, w.data());
+            for (int i = 0; i <= j; ++i) h1[i] = porc::dotv(V[i].data(), w.data(), n);
+            for (int i = 0; i <= j; ++i)
+                for (int q = 0; q < n; ++q) w[q] -= h1[i] * V[i][q];
+            for (int i = 0; i <= j; ++i) h2[i] = porc::dotv(V[i].data(), w.data(), n);
+            for (int i = 0; i <= j; ++i)
+                for (int q = 0; q < n; ++q) w[q] -= h2[i] * V[i][q];
+            const double hn = std::sqrt(porc::dotv(w.data(), w.data(), n));
+            for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = h1[i] + h2[i];
+            H[size_t(j + 1) * m + j] = hn;
+            done = j + 1;
+            if (!(hn > 1e-300)) break;
+            V.emplace_back(w);
+            for (double& v : V[j + 1]) v /= hn;
+        }
+        if (m_done) *m_done = done;
+    });
+}
+
 // power iteration on M X = S* L^-1 S A_f X,
 // where u = L^-1 f solves Lap u - grad p = -f, div u = 0 with homogeneous walls.
 int porc_alpha_exp(void* ctx, double tol, int max_steps, double* alpha_exp, int* steps) {

@@ -80,6 +80,11 @@ int porc_gmres_solve(void* ctx, const double* b, double* x, double rtol, int max
  * alpha = 0 and MG-GMRES at rtol 1e-10. */
 int porc_alpha_exp(void* ctx, double tol, int max_steps, double* alpha_exp, int* steps);
 
+/* iteration_matrix_spectrum: m Arnoldi steps (CGS2) on the error
+ * propagator E x = x - V(0, A x) restricted to mean-zero pressure, from the splitmix64 start vector
+ * of `seed`; H is the (m+1) x m Hessenberg matrix, row-major.  rho = max |eig(H[:m_done, :m_done])|. */
+int porc_vcycle_spectrum(void* ctx, int m, unsigned long long seed, double* H, int* m_done);
+
 #ifdef __cplusplus
 }
 #endif

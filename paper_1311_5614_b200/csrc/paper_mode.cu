@@ -1353,6 +1353,69 @@ int ibmg_paper_gmres_solve(ibmg_paper* c, const double* b, double* x, double rto
     return solve(c, true, b, x, rtol, max_iter, st, hist, hl);
 }
 
+// w = a - w (elementwise)
+__global__ void pm_k_a_minus(const double* __restrict__ a, double* __restrict__ w, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) w[i] = a[i] - w[i];
+}
+
+int ibmg_paper_vcycle_spectrum(ibmg_paper* c, int m, unsigned long long seed, double* H, int* m_done) {
+    PM_TRY(c, {
+        if (m < 2 || !H) throw std::invalid_argument("SpectrumProbe: m >= 2");
+        const int n = c->lev[0].g.ntot;
+        const size_t stride = (size_t)n;
+        c->V.need(stride * (m + 1));
+        c->va.need(n);
+        c->vb.need(n);
+        c->hd.need(std::max<size_t>(256, 2 * (size_t)(m + 2) + 16));
+        double* a = c->va.p;
+        double* w = c->vb.p;
+        double* h1d = c->hd.p;
+        double* h2d = c->hd.p + (m + 2);
+        double* nd = c->hd.p + 2 * (m + 2);
+        std::vector<double> x0(n), hh(2 * (m + 2) + 1);
+        unsigned long long z = seed;
+        for (double& v : x0) {
+            z += 0x9E3779B97F4A7C15ull;
+            unsigned long long t = z;
+            t = (t ^ (t >> 30)) * 0xBF58476D1CE4E5B9ull;
+            t = (t ^ (t >> 27)) * 0x94D049BB133111EBull;
+            t ^= t >> 31;
+            v = double(t >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+        }
+        PM_CUDA(cudaMemcpyAsync(w, x0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->s));
+        pm::pressure_mean(c, 0, w);
+        PM_LAUNCH(c, pm::k_multi_dot, 1, 1024, 0, (const double*)w, (size_t)0, (const double*)w, n, nd);
+        PM_LAUNCH(c, pm::k_scale, pm::nblk(n), 256, 0, (const double*)w, (const double*)nd, 1.0, c->V.p, n);
+        std::fill(H, H + size_t(m + 1) * m, 0.0);
+        int done = 0;
+        for (int j = 0; j < m; ++j) {
+            const double* vj = c->V.p + stride * j;
+            pm::apply(c, 0, vj, nullptr, a);
+            pm::vcycle(c, a, w);                                        // w = V(0, A v_j), mean-zero p
+            PM_LAUNCH(c, pm_k_a_minus, pm::nblk(n), 256, 0, vj, w, n);  // w = v_j - w
+            pm::pressure_mean(c, 0, w);
+            PM_LAUNCH(c, pm::k_multi_dot, j + 1, 256, 0, (const double*)c->V.p, stride, (const double*)w, n, h1d);
+            PM_LAUNCH(c, pm::k_multi_axpy, pm::nblk(n), 256, 0, (const double*)c->V.p, stride, j + 1, (const double*)h1d,
+                      -1.0, w, n);
+            PM_LAUNCH(c, pm::k_multi_dot, j + 1, 256, 0, (const double*)c->V.p, stride, (const double*)w, n, h2d);
+            PM_LAUNCH(c, pm::k_multi_axpy, pm::nblk(n), 256, 0, (const double*)c->V.p, stride, j + 1, (const double*)h2d,
+                      -1.0, w, n);
+            PM_LAUNCH(c, pm::k_multi_dot, 1, 1024, 0, (const double*)w, (size_t)0, (const double*)w, n, nd);
+            PM_CUDA(cudaMemcpyAsync(hh.data(), c->hd.p, sizeof(double) * (2 * (m + 2) + 1), cudaMemcpyDeviceToHost, c->s));
+            PM_CUDA(cudaStreamSynchronize(c->s));
+            const double hn = std::sqrt(hh[2 * (m + 2)]);
+            for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = hh[i] + hh[m + 2 + i];
+            H[size_t(j + 1) * m + j] = hn;
+            done = j + 1;
+            if (!(hn > 1e-300)) break;
+            PM_LAUNCH(c, pm::k_scale, pm::nblk(n), 256, 0, (const double*)w, (const double*)nd, 1.0,
+                      c->V.p + stride * (j + 1), n);
+        }
+        if (m_done) *m_done = done;
+    });
+}
+
 // power iteration on M X = S* L^-1 S A_f X, u = L^-1 f
 // solving Lap u - grad p = -f, div u = 0 with homogeneous walls (MG-GMRES at 1e-10 on the
 // alpha = 0 twin of this context).  The iteration vector lives on the device.

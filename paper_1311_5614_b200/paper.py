@@ -36,7 +36,7 @@ EXPORTS = ["ibmg_paper_create", "ibmg_paper_destroy", "ibmg_paper_last_error", "
            "ibmg_paper_level_reach", "ibmg_paper_apply", "ibmg_paper_residual", "ibmg_paper_restrict",
            "ibmg_paper_prolong_add", "ibmg_paper_sweep", "ibmg_paper_vcycle", "ibmg_paper_elasticity_triplets",
            "ibmg_paper_build_rhs", "ibmg_paper_spread", "ibmg_paper_interpolate", "ibmg_paper_mg_solve",
-           "ibmg_paper_gmres_solve", "ibmg_paper_alpha_exp", "ibmg_paper_kernel_launches"]
+           "ibmg_paper_gmres_solve", "ibmg_paper_alpha_exp", "ibmg_paper_vcycle_spectrum", "ibmg_paper_kernel_launches"]
 
 _BOUND = False
 
@@ -68,6 +68,7 @@ def lib():
         for f in ("mg_solve", "gmres_solve"):
             getattr(L, "ibmg_paper_" + f).argtypes = [vp, vp, vp, d, ip, C.POINTER(PaperStats), vp, ip]
         L.ibmg_paper_alpha_exp.argtypes = [vp, d, ip, C.POINTER(d), C.POINTER(ip)]
+        L.ibmg_paper_vcycle_spectrum.argtypes = [vp, ip, C.c_ulonglong, vp, C.POINTER(ip)]
         L.ibmg_paper_kernel_launches.restype = C.c_longlong
         L.ibmg_paper_kernel_launches.argtypes = [vp]
         _BOUND = True
@@ -221,6 +222,16 @@ class PaperSystem:
 
     def gmres_solve(self, b, rtol=1e-6, max_iter=100):
         return self._solve(lib().ibmg_paper_gmres_solve, b, rtol, max_iter)
+
+    def iteration_matrix_spectrum(self, m=60, seed=1):
+        """(Ritz values by descending modulus, Hessenberg (m+1) x m) of the V-cycle's error
+        propagator E = I - v_cycle(0, A .) on mean-zero pressure."""
+        H = np.zeros((m + 1) * m)
+        k = C.c_int()
+        self._chk(lib().ibmg_paper_vcycle_spectrum(self._h, m, seed, _p(H), C.byref(k)))
+        H = H.reshape(m + 1, m)
+        ritz = np.linalg.eigvals(H[: k.value, : k.value])
+        return ritz[np.argsort(-np.abs(ritz))], H
 
     def estimate_alpha_exp(self, tol=1e-4, max_steps=1000):
         a, k = C.c_double(), C.c_int()

@@ -177,6 +177,19 @@ def test_grid_refinement_big_and_small_boxes():
     assert not st["converged"] and st["iters"] == 100
 
 
+def test_spectrum_probe_matches_oracle_and_fig4():
+    """The Arnoldi probe of the V-cycle's error propagator: Hessenberg entries equal the
+    oracle's (same start vector, same CGS2) and the radii are Fig. 4's (0.24 / 0.85 +- 0.05)."""
+    mesh = configs.paper_annulus(32)
+    for rel_stiff, want in ((0, 0.24), (100, 0.85)):
+        alpha = rel_stiff * configs.PAPER_ALPHA_EXP[32]
+        g, o = PaperSystem(32, 1, 1, 1, alpha, mesh), O.PaperOracle(32, 1, 1, 1, alpha, mesh)
+        rg, Hg = g.iteration_matrix_spectrum(m=60, seed=1)
+        ro, Ho = o.iteration_matrix_spectrum(m=60, seed=1)
+        assert np.abs(Hg[:13, :12] - Ho[:13, :12]).max() < 1e-9
+        assert abs(abs(rg[0]) - want) <= 0.05 and abs(abs(rg[0]) - abs(ro[0])) < 1e-6
+
+
 def test_rejects_bad_input():
     g = PaperSystem(32, 4, 1, 1, 1.0)
     with pytest.raises(ValueError):
