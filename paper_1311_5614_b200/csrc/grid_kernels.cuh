@@ -848,7 +848,54 @@ inline int ortho_dots_grid(size_t m, int per_cta) {
 }
 // bid / nb: this CTA's index and the CTA count of the pass (bid and
 // nb; the batched kernel passes its own)
-template <int KMAX>
+// The coefficients of the update pass from the summed dots of pass 1 (bw: b_i and
+// gamma, aqd: a_i and delta, k entries each): run by the last CTA of k_ortho_dots, or
+// by k_ortho_finish once the slabs' sums are reduced (slab groups).  One CTA.
+__device__ __forceinline__ void ortho_finish(const double* bw, const double* aqd, int k, double* __restrict__ dh,
+                                             int ld, double* s_coef) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid == 0) {
+        double na = 0.0, ab = 0.0;
+        for (int i = lane; i < k - 1; i += 32) {
+            na += aqd[i] * aqd[i];
+            ab += aqd[i] * bw[i];
+        }
+        na = warp_sum(na);
+        ab = warp_sum(ab);
+        if (lane == 0) {
+            // |q - V a|^2 = delta - |a|^2, clamped: near a Krylov breakdown the
+            // difference can round below zero.  nu <= 1e-14 |q| is a breakdown
+            // (q in span V): nu = 0 is published (v_j = 0, w projected on
+            // V_{<j} only) and fgmres2 ends the cycle at the previous column.
+            const double delta = aqd[k - 1], nu2 = fmax(delta - na, 0.0);
+            const bool brk = !(nu2 > 1e-28 * delta);
+            const double nu = brk ? 0.0 : sqrt(nu2), h = brk ? 0.0 : (bw[k - 1] - ab) / nu;
+            dh[5 * ld] = brk ? 0.0 : 1.0 / nu;
+            dh[5 * ld + 1] = brk ? 0.0 : h / nu;
+            dh[5 * ld + 2] = nu;
+            dh[5 * ld + 3] = h;
+            *s_coef = brk ? 0.0 : h / nu;  // s for the coefficients below
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        dh[i] = bw[i];
+        dh[ld + i] = aqd[i];
+        if (i < k - 1) dh[4 * ld + i] = bw[i] - aqd[i] * *s_coef;
+    }
+}
+// Slab groups: the 2k raw sums of pass 1 live at dh[2 ld ..) (k_ortho_dots<KMAX, true>),
+// are summed over the slabs there, and this kernel forms the coefficients.
+__global__ void k_ortho_finish(int k, double* __restrict__ dh, int ld) {
+    pdl_enter();
+    __shared__ double fin[64];
+    __shared__ double s_coef;
+    for (int d = threadIdx.x; d < 2 * k; d += blockDim.x) fin[d] = dh[2 * ld + d];
+    __syncthreads();
+    ortho_finish(fin, fin + k, k, dh, ld, &s_coef);
+}
+
+template <int KMAX, bool RAW = false>
 __device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size_t stride, int k,
                                               const double* __restrict__ w, size_t m, double* __restrict__ partial,
                                               double* __restrict__ dh, int ld, unsigned* __restrict__ ticket, int bid,
@@ -926,46 +973,20 @@ __device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size
         if (lane == 0) fin[d] = t;
     }
     __syncthreads();
-    const double* bw = fin;      // b_i (i < k-1), gamma = bw[k-1]
-    const double* aqd = fin + k; // a_i (i < k-1), delta = aqd[k-1]
-    if (wid == 0) {
-        double na = 0.0, ab = 0.0;
-        for (int i = lane; i < k - 1; i += 32) {
-            na += aqd[i] * aqd[i];
-            ab += aqd[i] * bw[i];
-        }
-        na = warp_sum(na);
-        ab = warp_sum(ab);
-        if (lane == 0) {
-            // |q - V a|^2 = delta - |a|^2, clamped: near a Krylov breakdown the
-            // difference can round below zero.  nu <= 1e-14 |q| is a breakdown
-            // (q in span V): nu = 0 is published (v_j = 0, w projected on
-            // V_{<j} only) and fgmres2 ends the cycle at the previous column.
-            const double delta = aqd[k - 1], nu2 = fmax(delta - na, 0.0);
-            const bool brk = !(nu2 > 1e-28 * delta);
-            const double nu = brk ? 0.0 : sqrt(nu2), h = brk ? 0.0 : (bw[k - 1] - ab) / nu;
-            dh[5 * ld] = brk ? 0.0 : 1.0 / nu;
-            dh[5 * ld + 1] = brk ? 0.0 : h / nu;
-            dh[5 * ld + 2] = nu;
-            dh[5 * ld + 3] = h;
-            s_coef = brk ? 0.0 : h / nu;  // s for the coefficients below
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-        dh[i] = bw[i];
-        dh[ld + i] = aqd[i];
-        if (i < k - 1) dh[4 * ld + i] = bw[i] - aqd[i] * s_coef;
+    if (RAW) {  // slab groups: the raw sums, reduced over the slabs before k_ortho_finish
+        for (int d = threadIdx.x; d < 2 * k; d += blockDim.x) dh[2 * ld + d] = fin[d];
+    } else {
+        ortho_finish(fin, fin + k, k, dh, ld, &s_coef);
     }
     if (threadIdx.x == 0) *ticket = 0u;
 }
 
-template <int KMAX>
+template <int KMAX, bool RAW = false>
 __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
     k_ortho_dots(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ w, size_t m,
                  double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
     pdl_enter();
-    ortho_dots_at<KMAX>(V, stride, k, w, m, partial, dh, ld, ticket, (int)blockIdx.x, (int)gridDim.x);
+    ortho_dots_at<KMAX, RAW>(V, stride, k, w, m, partial, dh, ld, ticket, (int)blockIdx.x, (int)gridDim.x);
 }
 
 template <int KMAX>

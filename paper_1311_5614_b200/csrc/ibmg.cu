@@ -1687,6 +1687,17 @@ void ortho_dots(ibmg_ctx* c, int k, double* w) {
     else if (k <= 16) ortho_dots_k<16>(c, k, w);
     else ortho_dots_k<32>(c, k, w);
 }
+// slab groups: pass 1 leaving its 2k raw sums at dh[2 ld ..) (reduced over the slabs, then k_ortho_finish)
+template <int KM>
+void ortho_dots_raw_k(ibmg_ctx* c, int k, double* w) {
+    LAUNCH(c, (k_ortho_dots<KM, true>), ortho_dots_grid<KM>(c->Mk, c->ortho_per_cta), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
+           c->partial, c->dh, c->prm.restart + 2, c->ticket);
+}
+void ortho_dots_raw(ibmg_ctx* c, int k, double* w) {
+    if (k <= 8) ortho_dots_raw_k<8>(c, k, w);
+    else if (k <= 16) ortho_dots_raw_k<16>(c, k, w);
+    else ortho_dots_raw_k<32>(c, k, w);
+}
 void ortho_update(ibmg_ctx* c, int k, const double* w, double* w1out, double* zero) {
     if (k - 1 <= 8) ortho_update_k<8>(c, k, w, w1out, zero);
     else if (k - 1 <= 16) ortho_update_k<16>(c, k, w, w1out, zero);

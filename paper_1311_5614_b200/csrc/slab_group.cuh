@@ -678,6 +678,125 @@ int fgmres_group(ibmg_group* g, ibmg_stats* st) {
     return st->converged ? IBMG_OK : IBMG_NOT_CONVERGED;
 }
 
+// FGMRES(m) over the slabs with the two-pass lagged CGS2 of fgmres2():
+// per Arnoldi step every slab runs pass 1 on its rows and leaves the 2k raw sums in
+// dh, one reduction over the slabs sums them, k_ortho_finish forms the coefficients
+// (identically on every slab), pass 2 updates the slab's rows, and |w1|^2 is reduced:
+// two passes over the basis and two small reductions per step, against three passes
+// and three reductions in fgmres_group().  Host logic as fgmres2().
+int fgmres_group2(ibmg_group* g, ibmg_stats* st) {
+    const int m = g->prm.restart, ld = m + 2;
+    const int SC = 5 * ld, RAW = 2 * ld, bslot = 6 * ld + 2;
+    const size_t Mk = g->Mk;
+    std::vector<double> Hx(size_t(m + 1) * m, 0.0), Ha(size_t(m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), y(m);
+    st->iters = st->restarts = st->converged = 0;
+    st->relres = 0.0;
+    const Vecs kb = per_slab(g, [&](int r) { return pr(g, r).kb; });
+    const Vecs kx = per_slab(g, [&](int r) { return pr(g, r).kx; });
+    const Vecs kr = per_slab(g, [&](int r) { return pr(g, r).kr; });
+    const Vecs w = per_slab(g, [&](int r) { return cx(g, r)->stage_a; });
+    each(g, [&](int r, ibmg_ctx* c) { CK(cudaMemsetAsync(kx[r], 0, sizeof(double) * Mk, c->s)); });
+    gdot(g, kb, kb, Mk, bslot);
+    const double bnorm = std::sqrt(read0(g, bslot));
+    if (bnorm == 0.0) {
+        st->converged = 1;
+        return IBMG_OK;
+    }
+    const double tol = g->prm.rtol * bnorm;
+    double beta = bnorm;
+    const Vecs* rvec = &kb;
+    int it = 0, restarts = 0;
+    ibmg_ctx* c0 = g->c[0];
+    while (true) {
+        each(g, [&](int r, ibmg_ctx* c) {
+            LAUNCH(c, k_scale_by_norm, nblk(Mk), 256, 0, (const double*)(*rvec)[r], c->V, Mk, (const double*)nullptr,
+                   beta, (double*)nullptr);
+        });
+        std::fill(gv.begin(), gv.end(), 0.0);
+        std::fill(Hx.begin(), Hx.end(), 0.0);
+        gv[0] = beta;
+        int kdim = 0;
+        double nu0 = 1.0;
+        for (int j = 0; j < m; ++j) {
+            const Vecs Vj = per_slab(g, [&](int r) { return cx(g, r)->V + cx(g, r)->Mst * j; });
+            const Vecs Zj = per_slab(g, [&](int r) { return cx(g, r)->Z + cx(g, r)->Mst * j; });
+            vcycle_group(g, Vj, Zj);
+            each(g, [&](int r, ibmg_ctx* c) {
+                apply_owned(g, r, c->lev[0].w, c->wv);
+                pack(g, r, c->wv, w[r]);
+                ortho_dots_raw(c, j + 1, w[r]);
+            });
+            allreduce(g, RAW, 2 * (j + 1));
+            const bool more = j + 1 < m;
+            each(g, [&](int r, ibmg_ctx* c) {
+                LAUNCH(c, k_ortho_finish, 1, 64, 0, j + 1, c->dh, ld);
+                ortho_update(c, j + 1, w[r], more ? c->V + c->Mst * (j + 1) : kr[r], nullptr);
+            });
+            allreduce(g, SC + 4, 1);
+            CK(cudaSetDevice(g->dev[0]));
+            CK(cudaMemcpyAsync(c0->hpin, c0->dh, sizeof(double) * (SC + 5), cudaMemcpyDeviceToHost, c0->s));
+            CK(cudaEventRecord(c0->ev_dots, c0->s));
+            CK(cudaEventSynchronize(c0->ev_dots));
+            const double* hp = c0->hpin;
+            const double nu = hp[SC + 2], h = hp[SC + 3], bnext = std::sqrt(hp[SC + 4]);
+            if (j > 0 && !(nu > 0.0)) {  // breakdown: the space is invariant (fgmres2)
+                for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j - 1] += hp[ld + i];
+                Hx[size_t(j) * m + j - 1] = 0.0;
+                break;
+            }
+            if (j == 0) {
+                nu0 = nu;
+            } else {  // exact column j-1: q_j = sum a_i V_i + nu v_j
+                for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j - 1] += hp[ld + i];
+                Hx[size_t(j) * m + j - 1] = nu;
+            }
+            for (int i = 0; i < j; ++i) Hx[size_t(i) * m + j] = hp[i];
+            Hx[size_t(j) * m + j] = h;
+            Hx[size_t(j + 1) * m + j] = bnext;
+            for (int i = 0; i <= j + 1; ++i) Ha[size_t(i) * m + j] = Hx[size_t(i) * m + j];
+            for (int i = 0; i < j; ++i) {
+                const double a = Ha[size_t(i) * m + j], cc = Ha[size_t(i + 1) * m + j];
+                Ha[size_t(i) * m + j] = cs[i] * a + sn[i] * cc;
+                Ha[size_t(i + 1) * m + j] = -sn[i] * a + cs[i] * cc;
+            }
+            const double a = Ha[size_t(j) * m + j], cc = Ha[size_t(j + 1) * m + j];
+            const double den = std::hypot(a, cc);
+            cs[j] = a / den;
+            sn[j] = cc / den;
+            gv[j + 1] = -sn[j] * gv[j];
+            gv[j] = cs[j] * gv[j];
+            ++it;
+            kdim = j + 1;
+            if (!std::isfinite(gv[j + 1])) throw CudaError("FGMRES: non-finite residual estimate");
+            if (std::fabs(gv[j + 1]) <= tol || it >= g->prm.max_iters || bnext == 0.0) break;
+        }
+        hessenberg_lsq(Hx, m, kdim, beta * nu0, y);  // r = beta q_0 = beta nu0 v_0
+        each(g, [&](int r, ibmg_ctx* c) {
+            CK(cudaStreamSynchronize(c->s));  // this slab's hpin is free
+            std::copy(y.begin(), y.begin() + kdim, c->hpin);
+            CK(cudaMemcpyAsync(c->dh + 4 * ld, c->hpin, sizeof(double) * kdim, cudaMemcpyHostToDevice, c->s));
+            LAUNCH(c, k_multi_axpy_add, nblk(Mk), 256, 0, (const double*)c->Z, c->Mst, kdim,
+                   (const double*)(c->dh + 4 * ld), kx[r], Mk);
+        });
+        beta = std::sqrt(true_residual(g, kx, kb, kr));
+        rvec = &kr;
+        if (beta <= tol) {
+            st->converged = 1;
+            break;
+        }
+        if (it >= g->prm.max_iters) break;
+        ++restarts;
+    }
+    pressure_mean_zero_group(g, kx);
+    st->iters = it;
+    st->restarts = restarts;
+    st->relres = beta / bnorm;
+    return st->converged ? IBMG_OK : IBMG_NOT_CONVERGED;
+}
+
+// the group's Krylov solver: two-pass lagged CGS2 unless IBMG_CGS2=1 (three sweeps)
+int fgmres_slabs(ibmg_group* g, ibmg_stats* st) { return g->c[0]->ortho2 ? fgmres_group2(g, st) : fgmres_group(g, st); }
+
 // host whole-grid vector (3 planes) -> each local slab's compact rows
 void scatter_host(ibmg_group* g, const double* h, const Vecs& k) {
     const size_t N = size_t(g->prm.N), nn = N * N, w = size_t(g->rows) * N;
@@ -935,7 +1054,7 @@ int ibmg_group_solve(ibmg_group* g, const double* b, double* x, ibmg_stats* st) 
     return gapi(g, [&]() -> int {
         const double t0 = now_ms();
         scatter_host(g, b, per_slab(g, [&](int r) { return pr(g, r).kb; }));
-        const int rc = fgmres_group(g, st);
+        const int rc = fgmres_slabs(g, st);
         gather_host(g, per_slab(g, [&](int r) { return pr(g, r).kx; }), x);
         st->solve_ms = now_ms() - t0;
         st->total_ms = st->solve_ms;
@@ -961,7 +1080,7 @@ int ibmg_group_step(ibmg_group* g, double* u, double* p, double* X, ibmg_stats* 
         });
         each(g, [&](int, ibmg_ctx* c) { CK(cudaStreamSynchronize(c->s)); });
         const double t1 = now_ms();
-        const int rc = fgmres_group(g, st);
+        const int rc = fgmres_slabs(g, st);
         gather_host(g, per_slab(g, [&](int r) { return pr(g, r).kx; }), u, 2, p);
         const double t2 = now_ms();
         // X^{n+1} = X^n + dt S^T u^{n+1} on every slab (whole u^{n+1})
