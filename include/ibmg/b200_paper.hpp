@@ -54,9 +54,10 @@ class CavitySystem {
         int N = 32, box = 1, nu1 = 1, nu2 = 1;
         double alpha = 0.0;
         int device = 0;
+        int order = 0;  // 0 lexicographic (the paper), 1 multicolour (opt-in)
     };
     explicit CavitySystem(const Params& p) : dm_{p.N} {
-        ibmg_paper_params q{p.N, p.box, p.nu1, p.nu2, 4, p.alpha, p.device};
+        ibmg_paper_params q{p.N, p.box, p.nu1, p.nu2, 4, p.alpha, p.device, p.order};
         const int rc = ibmg_paper_create(&q, &ctx_);
         if (rc == 1) throw std::invalid_argument("CavitySystem: invalid parameters");
         if (rc != 0) throw std::runtime_error("CavitySystem: CUDA initialisation failed");

@@ -35,6 +35,9 @@ typedef struct {
     int coarsest_n; /* direct solve at this size (4) */
     double alpha;   /* gamma dt (SaddleSystem::alpha, saddle.hpp:23) */
     int device;     /* CUDA device ordinal */
+    int order;      /* 0: lexicographic sweep, the paper's smoother (dataflow pipeline); 1: multicolour ordering
+                       (the opt-in extension of SPEC.md:452): colour (bx mod (R+1)) + (R+1) (by mod (R+1)), R the
+                       level's coupling reach in boxes, one launch per colour */
 } ibmg_paper_params;
 
 typedef struct {

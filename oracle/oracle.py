@@ -32,7 +32,7 @@ class OrcStats(C.Structure):
 
 class PorcParams(C.Structure):
     _fields_ = [("N", C.c_int), ("box", C.c_int), ("nu1", C.c_int), ("nu2", C.c_int), ("coarsest_n", C.c_int),
-                ("alpha", C.c_double)]
+                ("alpha", C.c_double), ("order", C.c_int)]
 
 
 class PorcStats(C.Structure):
@@ -87,7 +87,7 @@ def lib():
         L.porc_set_mesh.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p]
         for f in ("porc_num_levels",):
             getattr(L, f).argtypes = [C.c_void_p]
-        for f in ("porc_level_n", "porc_level_dofs", "porc_level_boxes"):
+        for f in ("porc_level_n", "porc_level_dofs", "porc_level_boxes", "porc_level_reach"):
             getattr(L, f).argtypes = [C.c_void_p, C.c_int]
         L.porc_apply.argtypes = [C.c_void_p, C.c_int, dp, dp]
         L.porc_residual.argtypes = [C.c_void_p, C.c_int, dp, dp, dp]
@@ -238,9 +238,9 @@ class PaperOracle:
     """CPU oracle of the Dirichlet paper-reproduction mode (paper_oracle.h): cavity
     walls, thick fiber mesh, b x b box relaxation in lexicographic order."""
 
-    def __init__(self, N, box=1, nu1=1, nu2=1, alpha=0.0, mesh=None, coarsest_n=4):
+    def __init__(self, N, box=1, nu1=1, nu2=1, alpha=0.0, mesh=None, coarsest_n=4, order=0):
         self.N = N
-        p = PorcParams(N, box, nu1, nu2, coarsest_n, alpha)
+        p = PorcParams(N, box, nu1, nu2, coarsest_n, alpha, order)
         err = C.create_string_buffer(512)
         self._ctx = lib().porc_create(C.byref(p), err, 512)
         if not self._ctx:
@@ -275,6 +275,9 @@ class PaperOracle:
 
     def level_boxes(self, l=0):
         return lib().porc_level_boxes(self._ctx, l)
+
+    def level_reach(self, l=0):
+        return lib().porc_level_reach(self._ctx, l)
 
     def apply(self, w, level=0):
         out = np.empty_like(w)

@@ -242,9 +242,10 @@ struct Level {
     Dof d;
     double h = 0;
     Csr S, E, A;  // Stokes rows, elasticity (velocity block, alpha-free), S + alpha E
-    int b = 1, nb = 1;
+    int b = 1, nb = 1, reach = 1;
     bool whole = false;
     std::vector<Box> boxes;
+    std::vector<int> order;  // box visiting order of a sweep
     std::vector<double> w, rhs, r;
 };
 
@@ -308,6 +309,7 @@ void build(Ctx& C) {
         throw std::invalid_argument("N and coarsest_n must be powers of two with N >= 2 coarsest_n");
     if (C.P.box < 1 || (C.P.box & (C.P.box - 1))) throw std::invalid_argument("box must be a power of two");
     if (C.P.alpha < 0) throw std::invalid_argument("alpha must be >= 0");
+    if (C.P.order != 0 && C.P.order != 1) throw std::invalid_argument("order must be 0 (lexicographic) or 1 (multicolour)");
     C.lev.clear();
     for (int n = N; n >= C.P.coarsest_n; n /= 2) {
         Level L;
@@ -348,6 +350,43 @@ void build(Ctx& C) {
         L.w.assign(L.d.ntot(), 0.0);
         L.rhs.assign(L.d.ntot(), 0.0);
         L.r.assign(L.d.ntot(), 0.0);
+        // coupling reach in boxes: the largest Chebyshev distance between a box owning a row's DOF and
+        // a box owning one of its columns (a velocity lies on the faces of up to two cells)
+        {
+            auto span = [&](int dof, int* lo, int* hi) {  // box index ranges (x, y) of the cells touching dof
+                const int nu = L.d.nu(), nvel = L.d.nvel(), nn = L.d.n;
+                if (dof < nu) {
+                    const int i = dof % (nn - 1) + 1, j = dof / (nn - 1);
+                    lo[0] = (i - 1) / L.b, hi[0] = i / L.b, lo[1] = hi[1] = j / L.b;
+                } else if (dof < nvel) {
+                    const int i = (dof - nu) % nn, j = (dof - nu) / nn + 1;
+                    lo[0] = hi[0] = i / L.b, lo[1] = (j - 1) / L.b, hi[1] = j / L.b;
+                } else {
+                    lo[0] = hi[0] = ((dof - nvel) % nn) / L.b, lo[1] = hi[1] = ((dof - nvel) / nn) / L.b;
+                }
+            };
+            int reach = 0;
+            for (int r = 0; r < L.A.nr; ++r)
+                for (long k = L.A.rp[r]; k < L.A.rp[r + 1]; ++k) {
+                    if (L.A.v[k] == 0.0) continue;
+                    int rl[2], rh[2], cl[2], ch[2];
+                    span(r, rl, rh);
+                    span(L.A.ci[k], cl, ch);
+                    for (int x = 0; x < 2; ++x)
+                        reach = std::max(reach, std::max(std::abs(rl[x] - ch[x]), std::abs(rh[x] - cl[x])));
+                }
+            L.reach = std::max(reach, 1);
+        }
+        L.order.clear();
+        if (C.P.order == 1 && !L.whole) {
+            const int per = L.reach + 1;
+            for (int cy = 0; cy < per; ++cy)
+                for (int cx = 0; cx < per; ++cx)
+                    for (int by = cy; by < L.nb; by += per)
+                        for (int bx = cx; bx < L.nb; bx += per) L.order.push_back(bx + by * L.nb);
+        } else {
+            for (int q = 0; q < L.nb * L.nb; ++q) L.order.push_back(q);
+        }
         for (int by = 0; by < L.nb; ++by)
             for (int bx = 0; bx < L.nb; ++bx) {
                 Box& B = L.boxes[bx + size_t(by) * L.nb];
@@ -373,7 +412,8 @@ void residual_level(const Level& L, const double* b, const double* w, double* r)
 // the box, exact local solve, immediate correction.
 void sweep(const Level& L, const double* b, double* w) {
     std::vector<double> x;
-    for (const Box& B : L.boxes) {
+    for (int q : L.order) {
+        const Box& B = L.boxes[q];
         const int m = int(B.dofs.size());
         x.assign(B.lu.m, 0.0);
         for (int a = 0; a < m; ++a) x[a] = b[B.dofs[a]] - L.A.row_dot(B.dofs[a], w);
@@ -631,6 +671,7 @@ int porc_num_levels(void* ctx) { return int(static_cast<Ctx*>(ctx)->lev.size());
 int porc_level_n(void* ctx, int l) { return static_cast<Ctx*>(ctx)->lev.at(l).d.n; }
 int porc_level_dofs(void* ctx, int l) { return static_cast<Ctx*>(ctx)->lev.at(l).d.ntot(); }
 int porc_level_boxes(void* ctx, int l) { return static_cast<Ctx*>(ctx)->lev.at(l).nb; }
+int porc_level_reach(void* ctx, int l) { return static_cast<Ctx*>(ctx)->lev.at(l).reach; }
 
 int porc_apply(void* ctx, int l, const double* w, double* out) {
     PORC_TRY(ctx, {

@@ -30,6 +30,9 @@ typedef struct {
     int nu1, nu2;   /* pre / post sweeps */
     int coarsest_n; /* direct solve at this size (4) */
     double alpha;   /* gamma * dt, multiplies E in the momentum rows */
+    int order;      /* 0: lexicographic (the paper's smoother); 1: multicolour (SPEC.md:452 opt-in extension):
+                       colour (bx mod (R+1)) + (R+1) (by mod (R+1)) with R the level's coupling reach in boxes,
+                       colours in ascending order, lexicographic inside a colour */
 } porc_params;
 
 typedef struct {
@@ -52,6 +55,7 @@ int porc_num_levels(void* ctx);
 int porc_level_n(void* ctx, int level);
 int porc_level_dofs(void* ctx, int level);       /* (n-1) n + n (n-1) + n^2 */
 int porc_level_boxes(void* ctx, int level);      /* boxes per side */
+int porc_level_reach(void* ctx, int level);      /* coupling reach of the level operator in boxes */
 
 int porc_apply(void* ctx, int level, const double* w, double* out);
 int porc_residual(void* ctx, int level, const double* b, const double* w, double* r);

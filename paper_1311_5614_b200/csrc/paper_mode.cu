@@ -570,31 +570,17 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// One lexicographic box sweep (SPEC.md:427-431) as a dataflow pipeline; see the header.
-// sync[0] is the ticket counter, sync[1 + by] the number of boxes of row by published.
-__global__ void k_sweep(Geo g, Csr E, double alpha, int b, int nb, int mc, int whole, int reach,
-                        const double* __restrict__ Tinv, const double* __restrict__ rhs, double* __restrict__ w,
-                        int* __restrict__ sync) {
-    extern __shared__ double r[];  // mc
-    __shared__ int s_t;
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        const int t = atomicAdd(sync, 1);
-        s_t = t;
-        const int bx = t % nb, by = t / nb;
-        if (bx > 0)
-            while (ld_acquire(sync + 1 + by) < bx) {}
-        if (by > 0) {
-            const int need = min(nb, bx + reach + 1);
-            while (ld_acquire(sync + by) < need) {}
-        }
-    }
-    __syncthreads();
-    const int t = s_t, bx = t % nb, by = t / nb;
+// Relaxation of box t: residual rows of the box (matrix-free Stokes part
+// + E rows, read through L2: other CTAs wrote them), dense inverse, immediate correction.
+// r: mc doubles of shared memory.  Small boxes (blockDim = 32 mc): one warp per row, the
+// lanes share the E row (fixed xor-tree sum).
+__device__ __forceinline__ void box_relax(const Geo& g, const Csr& E, double alpha, int b, int nb, int mc, int t,
+                                          const double* __restrict__ Tinv, const double* __restrict__ rhs,
+                                          double* __restrict__ w, double* r) {
+    const int tid = threadIdx.x, bx = t % nb, by = t / nb;
     const Box B = box_geo(g.n, b, bx, by);
-    int d = tid < B.m ? box_dof(g, B, tid) : -1;
+    const int d = tid < B.m ? box_dof(g, B, tid) : -1;
     if (blockDim.x == 32 * mc) {
-        // small boxes: one warp per row, the lanes share the E row (fixed xor-tree sum)
         const int a = tid >> 5, lane = tid & 31;
         if (a < B.m) {
             const int da = box_dof(g, B, a);
@@ -617,15 +603,47 @@ __global__ void k_sweep(Geo g, Csr E, double alpha, int b, int nb, int mc, int w
     if (tid < B.m) {
         const double* T = Tinv + (size_t)t * mc * mc + tid;
         double s = 0.0;
-        const int lim = whole ? B.m : mc;  // the border column multiplies the zero constraint residual
-        for (int c = 0; c < lim; ++c) s += T[(size_t)c * mc] * r[c];
+        for (int c = 0; c < B.m; ++c) s += T[(size_t)c * mc] * r[c];  // (a whole-level box: the border column multiplies 0)
         w[d] = __ldcg(w + d) + s;
     }
+}
+
+// One lexicographic box sweep as a dataflow pipeline; see the header.
+// sync[0] is the ticket counter, sync[1 + by] the number of boxes of row by published.
+__global__ void k_sweep(Geo g, Csr E, double alpha, int b, int nb, int mc, int reach, const double* __restrict__ Tinv,
+                        const double* __restrict__ rhs, double* __restrict__ w, int* __restrict__ sync) {
+    extern __shared__ double r[];  // mc
+    __shared__ int s_t;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        const int t = atomicAdd(sync, 1);
+        s_t = t;
+        const int bx = t % nb, by = t / nb;
+        if (bx > 0)
+            while (ld_acquire(sync + 1 + by) < bx) {}
+        if (by > 0) {
+            const int need = min(nb, bx + reach + 1);
+            while (ld_acquire(sync + by) < need) {}
+        }
+    }
+    __syncthreads();
+    const int t = s_t;
+    box_relax(g, E, alpha, b, nb, mc, t, Tinv, rhs, w, r);
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        st_release(sync + 1 + by, bx + 1);
+        st_release(sync + 1 + t / nb, t % nb + 1);
     }
+}
+
+// One colour of the multicolour ordering (opt-in): the boxes (cx + per ix,
+// cy + per iy), per = reach + 1, are further apart than the coupling reach, so they
+// relax independently; the colours follow each other in stream order.
+__global__ void k_sweep_colour(Geo g, Csr E, double alpha, int b, int nb, int mc, int per, int cx, int cy, int ncx,
+                               const double* __restrict__ Tinv, const double* __restrict__ rhs, double* __restrict__ w) {
+    extern __shared__ double r[];  // mc
+    const int ix = blockIdx.x % ncx, iy = blockIdx.x / ncx;
+    box_relax(g, E, alpha, b, nb, mc, (cx + per * ix) + (cy + per * iy) * nb, Tinv, rhs, w, r);
 }
 
 // ---- vectors ----
@@ -861,6 +879,7 @@ void build(Ctx* c) {
         throw std::invalid_argument("box must be 1, 2, 4, 8 or 16");
     if (c->P.alpha < 0) throw std::invalid_argument("SaddleSystem: alpha must be >= 0");
     if (c->P.nu1 < 0 || c->P.nu2 < 0 || c->P.nu1 + c->P.nu2 < 1) throw std::invalid_argument("nu1 + nu2 must be >= 1");
+    if (c->P.order != 0 && c->P.order != 1) throw std::invalid_argument("order must be 0 (lexicographic) or 1 (multicolour)");
     PM_CUDA(cudaSetDevice(c->P.device));
     if (!c->s) PM_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
     if (!c->fail) PM_CUDA(cudaMalloc(&c->fail, sizeof(int)));
@@ -955,10 +974,20 @@ void apply(Ctx* c, int l, const double* w, const double* b, double* out) {
 void sweep(Ctx* c, int l, const double* rhs, double* w) {
     Level& L = c->lev[l];
     const double alpha = c->m1 > 0 ? c->P.alpha : 0.0;
-    PM_CUDA(cudaMemsetAsync(L.sync, 0, sizeof(int) * (L.nb + 1), c->s));
     const int nt = (L.mc <= 16 && alpha > 0.0) ? 32 * L.mc : (L.mc + 31) / 32 * 32;
-    PM_LAUNCH(c, k_sweep, L.nb * L.nb, nt, sizeof(double) * L.mc, L.g, L.E, alpha, L.b, L.nb, L.mc, L.whole, L.reach,
-              L.Tinv, rhs, w, L.sync);
+    if (c->P.order == 1 && !L.whole) {  // multicolour: (reach + 1)^2 launches
+        const int per = L.reach + 1;
+        for (int cy = 0; cy < per && cy < L.nb; ++cy)
+            for (int cx = 0; cx < per && cx < L.nb; ++cx) {
+                const int ncx = (L.nb - cx + per - 1) / per, ncy = (L.nb - cy + per - 1) / per;
+                PM_LAUNCH(c, k_sweep_colour, ncx * ncy, nt, sizeof(double) * L.mc, L.g, L.E, alpha, L.b, L.nb, L.mc, per,
+                          cx, cy, ncx, L.Tinv, rhs, w);
+            }
+        return;
+    }
+    PM_CUDA(cudaMemsetAsync(L.sync, 0, sizeof(int) * (L.nb + 1), c->s));
+    PM_LAUNCH(c, k_sweep, L.nb * L.nb, nt, sizeof(double) * L.mc, L.g, L.E, alpha, L.b, L.nb, L.mc, L.reach, L.Tinv, rhs,
+              w, L.sync);
 }
 void restrict_to(Ctx* c, int l, const double* rf, double* rc) {
     PM_LAUNCH(c, k_restrict, nblk(c->lev[l + 1].g.ntot), 256, 0, c->lev[l].g, c->lev[l + 1].g, rf, rc);

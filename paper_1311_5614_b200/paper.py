@@ -20,7 +20,7 @@ from . import ibmg as _ibmg
 
 class PaperParams(C.Structure):
     _fields_ = [("N", C.c_int), ("box", C.c_int), ("nu1", C.c_int), ("nu2", C.c_int), ("coarsest_n", C.c_int),
-                ("alpha", C.c_double), ("device", C.c_int)]
+                ("alpha", C.c_double), ("device", C.c_int), ("order", C.c_int)]
 
 
 class PaperStats(C.Structure):
@@ -86,10 +86,11 @@ def _f64(a):
 class PaperSystem:
     """The cavity SaddleSystem with its hierarchy and box smoothers on one GPU."""
 
-    def __init__(self, N, box=1, nu1=1, nu2=1, alpha=0.0, mesh=None, coarsest_n=4, device=0):
+    def __init__(self, N, box=1, nu1=1, nu2=1, alpha=0.0, mesh=None, coarsest_n=4, device=0, order=0):
+        """order 0: the paper's lexicographic sweep; 1: the multicolour ordering (SPEC.md:452 opt-in)."""
         self.N = N
         self._h = C.c_void_p()
-        rc = lib().ibmg_paper_create(C.byref(PaperParams(N, box, nu1, nu2, coarsest_n, alpha, device)),
+        rc = lib().ibmg_paper_create(C.byref(PaperParams(N, box, nu1, nu2, coarsest_n, alpha, device, order)),
                                      C.byref(self._h))
         if rc == 1:
             raise ValueError("ibmg_paper_create: invalid parameters")

@@ -37,8 +37,8 @@ def test_library_exports_the_paper_mode_abi():
     assert not [n for n in names if not hasattr(L, n)]
     assert set(paper.EXPORTS) == set(names)
     for bad in (dict(N=12), dict(N=4), dict(box=3), dict(box=32), dict(alpha=-1.0), dict(nu1=0, nu2=0),
-                dict(coarsest_n=3)):
-        p = dict(N=32, box=4, nu1=1, nu2=1, coarsest_n=4, alpha=1.0, device=0)
+                dict(coarsest_n=3), dict(order=2)):
+        p = dict(N=32, box=4, nu1=1, nu2=1, coarsest_n=4, alpha=1.0, device=0, order=0)
         p.update(bad)
         h = C.c_void_p()
         assert L.ibmg_paper_create(C.byref(paper.PaperParams(**p)), C.byref(h)) == 1 and not h.value, bad

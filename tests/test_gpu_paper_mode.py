@@ -190,6 +190,29 @@ def test_spectrum_probe_matches_oracle_and_fig4():
         assert abs(abs(rg[0]) - want) <= 0.05 and abs(abs(rg[0]) - abs(ro[0])) < 1e-6
 
 
+@pytest.mark.parametrize("box", [1, 2, 4, 8])
+def test_multicolour_ordering_matches_oracle(box):
+    """order = 1 (one launch per colour, boxes of a colour further apart than the coupling reach): every
+    level's sweep, the V-cycle and the solve equal the oracle's multicolour ordering."""
+    mesh = configs.paper_annulus(32)
+    g, o = PaperSystem(32, box, 1, 1, 609.0, mesh, order=1), O.PaperOracle(32, box, 1, 1, 609.0, mesh, order=1)
+    rng = np.random.default_rng(40 + box)
+    for l in range(g.nlevels):
+        assert g.level_reach(l) == o.level_reach(l)
+        b, w = rng.uniform(-1, 1, (2, g.level_dofs(l)))
+        ws = g.sweep(b, w, l)
+        assert rel(ws, o.sweep(b, w, l)) < 1e-10, (box, l)
+        assert np.array_equal(ws, g.sweep(b, w, l))
+    b = g.build_rhs(True, 609.0)
+    assert rel(g.v_cycle(b), o.vcycle(b)) < 1e-10
+    xg, sg, _ = g.gmres_solve(b, 1e-10, 200)
+    xo, so, _ = o.gmres_solve(b, 1e-10, 200)
+    assert sg["converged"] and abs(sg["iters"] - so["iters"]) <= 1 and rel(xg, xo) < 1e-8
+    # and it is a different (valid) smoother from the lexicographic one
+    gl = PaperSystem(32, box, 1, 1, 609.0, mesh)
+    assert rel(gl.v_cycle(b), g.v_cycle(b)) > 1e-6
+
+
 def test_rejects_bad_input():
     g = PaperSystem(32, 4, 1, 1, 1.0)
     with pytest.raises(ValueError):

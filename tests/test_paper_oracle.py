@@ -204,3 +204,23 @@ def test_fig4_spectral_radii(rel_stiff, want):
         it = o.mg_solve(o.rhs(True, alpha), 1e-6, 200)[1]["iters"]
         pred = np.log(1e-6) / np.log(abs(ritz[0]))
         assert abs(it / pred - 1) < 0.3 if rel_stiff <= 10 else 0.5 * pred < it <= pred
+
+
+def test_multicolour_ordering_keeps_the_counts():
+    """The opt-in multicolour box ordering (colours (bx mod (R+1), by mod (R+1)) with R the
+    coupling reach in boxes) against the paper's lexicographic one, Table 2's V(1,1) rows at h = 2^-6:
+    the same MG-GMRES counts (+-1) for boxes 4 and 8, no more iterations for single-cell boxes (9 / 24 / 60
+    against 9 / 33 / 74).  This is the ordering family of the production path's smoother (D12)."""
+    mesh = configs.paper_annulus(64)
+    for box in (1, 4, 8):
+        for rel_stiff in (10, 100, 500):
+            alpha = rel_stiff * configs.PAPER_ALPHA_EXP[64]
+            its = []
+            for order in (0, 1):
+                o = O.PaperOracle(64, box, 1, 1, alpha=alpha, mesh=mesh, order=order)
+                its.append(o.gmres_solve(o.rhs(True, alpha))[1]["iters"])
+            assert its[1] <= its[0] + 1, (box, rel_stiff, its)
+            if box > 1:
+                assert abs(its[1] - its[0]) <= 1, (box, rel_stiff, its)
+    o = O.PaperOracle(64, 1, 1, 1, alpha=393.0, mesh=mesh, order=1)
+    assert [o.level_reach(l) for l in range(o.nlevels)] == [5, 4, 3, 3, 1]
