@@ -294,12 +294,12 @@ __global__ void __launch_bounds__(256) k_apply_b(const BProb* __restrict__ P, in
     fused_launch_at(pf, G, PB.ang, bid, [&](int blk) { apply_tile(L0, w, PB.wv, blk, 0, L0.nn, S); });
 }
 
-template <int KMAX>
+template <int KMAX, bool FLAT = false>
 __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
     k_ortho_dots_b(const BProb* __restrict__ P, int k, int ld, const int* __restrict__ act) {
     pdl_enter();
     const BProb& PB = P[act[blockIdx.y]];
-    ortho_dots_at<KMAX>(PB.V, PB.Mst, k, PB.wv, PB.M, PB.partial, PB.dh, ld, PB.ticket, (int)blockIdx.x,
+    ortho_dots_at<KMAX, false, FLAT>(PB.V, PB.Mst, k, PB.wv, PB.M, PB.partial, PB.dh, ld, PB.ticket, (int)blockIdx.x,
                         (int)gridDim.x);
 }
 
@@ -534,12 +534,12 @@ void batch_vcycle(ibmg_batch* B, int j, int nA, std::vector<unsigned>& eadd) {
     }
 }
 
-template <int KM>
+template <int KM, bool FLAT = false>
 void batch_ortho_k(ibmg_batch* B, int k, int ld, int more, int nA) {
     using namespace ibmg;
     const size_t M = B->ctx[0]->Mk;
     const int pc = B->ctx[0]->ortho_per_cta;
-    launch_b(B, k_ortho_dots_b<KM>, dim3(ortho_dots_grid<KM>(M, pc), nA), dim3(kRedThreads), 0, false,
+    launch_b(B, (k_ortho_dots_b<KM, FLAT>), dim3(ortho_dots_grid<KM>(M, pc), nA), dim3(kRedThreads), 0, false,
              (const BProb*)B->dP, k, ld, (const int*)B->d_act);
 }
 template <int KM>
@@ -551,7 +551,8 @@ void batch_update_k(ibmg_batch* B, int k, int ld, int more, int nA) {
              more, (const int*)B->d_act);
 }
 void batch_ortho(ibmg_batch* B, int k, int ld, int more, int nA) {
-    if (k <= 8) batch_ortho_k<8>(B, k, ld, more, nA);
+    if (k <= ibmg::kOrthoFlatK) batch_ortho_k<8, true>(B, k, ld, more, nA);
+    else if (k <= 8) batch_ortho_k<8>(B, k, ld, more, nA);
     else if (k <= 16) batch_ortho_k<16>(B, k, ld, more, nA);
     else batch_ortho_k<32>(B, k, ld, more, nA);
     if (k - 1 <= 8) batch_update_k<8>(B, k, ld, more, nA);

@@ -895,17 +895,21 @@ __global__ void k_ortho_finish(int k, double* __restrict__ dh, int ld) {
     ortho_finish(fin, fin + k, k, dh, ld, &s_coef);
 }
 
-template <int KMAX, bool RAW = false>
+// FLAT (k <= KMAX / 2, chosen for k <= 4): no split of the basis range over the two
+// thread halves — every thread takes all k vectors of its own elements, so at small k
+// all 256 threads stream (the split leaves half of them idle at k = 1: 2.5 TB/s at C4).
+template <int KMAX, bool RAW = false, bool FLAT = false>
 __device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size_t stride, int k,
                                               const double* __restrict__ w, size_t m, double* __restrict__ partial,
                                               double* __restrict__ dh, int ld, unsigned* __restrict__ ticket, int bid,
                                               int nb) {
     constexpr int KH = KMAX / 2;  // i-range per thread half
+    constexpr int TPE = FLAT ? kRedThreads : 128;  // threads over distinct elements
     __shared__ double red[kRedThreads / 32][2 * KH];
     __shared__ double fin[2 * KMAX];
     __shared__ double s_coef;
-    const int th = threadIdx.x & 127, half = threadIdx.x >> 7;
-    const int kh = (k + 1) >> 1, i0 = half * kh, ni = min(kh, k - i0);
+    const int th = FLAT ? (int)threadIdx.x : (int)(threadIdx.x & 127), half = FLAT ? 0 : (int)(threadIdx.x >> 7);
+    const int kh = FLAT ? k : (k + 1) >> 1, i0 = half * kh, ni = min(kh, k - i0);
     const double* qv_ptr = V + stride * (k - 1);
     // few basis vectors per thread => several elements per iteration, so
     // every thread keeps enough loads in flight at small k
@@ -914,8 +918,8 @@ __device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size
     double aw[KH], aq[KH];
 #pragma unroll
     for (int i = 0; i < KH; ++i) aw[i] = aq[i] = 0.0;
-    const size_t step = (size_t)nb * 128;
-    for (size_t q0 = (size_t)bid * 128 + th; q0 < m; q0 += step * UNR) {
+    const size_t step = (size_t)nb * TPE;
+    for (size_t q0 = (size_t)bid * TPE + th; q0 < m; q0 += step * UNR) {
         double x[UNR], qq[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -954,9 +958,9 @@ __device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size
     __syncthreads();
     // dot d: which = d / k (0: with w, 1: with q), index i = d % k
     for (int d = threadIdx.x; d < 2 * k; d += blockDim.x) {
-        const int which = d / k, i = d - which * k, hh = i / kh, sl = i - hh * kh;
+        const int which = d / k, i = d - which * k, hh = FLAT ? 0 : i / kh, sl = i - hh * kh;
         double t = 0.0;
-        for (int ww = 4 * hh; ww < 4 * hh + 4; ++ww) t += red[ww][which * KH + sl];
+        for (int ww = FLAT ? 0 : 4 * hh; ww < (FLAT ? kRedThreads / 32 : 4 * hh + 4); ++ww) t += red[ww][which * KH + sl];
         partial[(size_t)d * nb + bid] = t;
     }
     __shared__ bool last;
@@ -981,13 +985,14 @@ __device__ __forceinline__ void ortho_dots_at(const double* __restrict__ V, size
     if (threadIdx.x == 0) *ticket = 0u;
 }
 
-template <int KMAX, bool RAW = false>
+template <int KMAX, bool RAW = false, bool FLAT = false>
 __global__ void __launch_bounds__(kRedThreads, KMAX > 16 ? 2 : 3)
     k_ortho_dots(const double* __restrict__ V, size_t stride, int k, const double* __restrict__ w, size_t m,
                  double* __restrict__ partial, double* __restrict__ dh, int ld, unsigned* __restrict__ ticket) {
     pdl_enter();
-    ortho_dots_at<KMAX, RAW>(V, stride, k, w, m, partial, dh, ld, ticket, (int)blockIdx.x, (int)gridDim.x);
+    ortho_dots_at<KMAX, RAW, FLAT>(V, stride, k, w, m, partial, dh, ld, ticket, (int)blockIdx.x, (int)gridDim.x);
 }
+constexpr int kOrthoFlatK = 4;  // k <= this: the FLAT pass 1 (single context, batch and slab groups alike)
 
 template <int KMAX>
 __device__ __forceinline__ void ortho_update_at(double* __restrict__ V, size_t stride, int k,

@@ -1672,9 +1672,9 @@ double now_ms() {
 
 // Two-pass orthogonalisation launches (grid_kernels.cuh k_ortho_dots /
 // k_ortho_update): k = j + 1 basis slots, the last one holding q.
-template <int KM>
+template <int KM, bool FLAT = false>
 void ortho_dots_k(ibmg_ctx* c, int k, double* w) {
-    LAUNCH(c, (k_ortho_dots<KM>), ortho_dots_grid<KM>(c->Mk, c->ortho_per_cta), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
+    LAUNCH(c, (k_ortho_dots<KM, false, FLAT>), ortho_dots_grid<KM>(c->Mk, c->ortho_per_cta), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
            c->partial, c->dh, c->prm.restart + 2, c->ticket);
 }
 template <int KM>
@@ -1683,18 +1683,20 @@ void ortho_update_k(ibmg_ctx* c, int k, const double* w, double* w1out, double* 
            c->dh, c->prm.restart + 2, c->ticket);
 }
 void ortho_dots(ibmg_ctx* c, int k, double* w) {
-    if (k <= 8) ortho_dots_k<8>(c, k, w);
+    if (k <= kOrthoFlatK) ortho_dots_k<8, true>(c, k, w);
+    else if (k <= 8) ortho_dots_k<8>(c, k, w);
     else if (k <= 16) ortho_dots_k<16>(c, k, w);
     else ortho_dots_k<32>(c, k, w);
 }
 // slab groups: pass 1 leaving its 2k raw sums at dh[2 ld ..) (reduced over the slabs, then k_ortho_finish)
-template <int KM>
+template <int KM, bool FLAT = false>
 void ortho_dots_raw_k(ibmg_ctx* c, int k, double* w) {
-    LAUNCH(c, (k_ortho_dots<KM, true>), ortho_dots_grid<KM>(c->Mk, c->ortho_per_cta), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
+    LAUNCH(c, (k_ortho_dots<KM, true, FLAT>), ortho_dots_grid<KM>(c->Mk, c->ortho_per_cta), kRedThreads, 0, (const double*)c->V, c->Mst, k, (const double*)w, c->Mk,
            c->partial, c->dh, c->prm.restart + 2, c->ticket);
 }
 void ortho_dots_raw(ibmg_ctx* c, int k, double* w) {
-    if (k <= 8) ortho_dots_raw_k<8>(c, k, w);
+    if (k <= kOrthoFlatK) ortho_dots_raw_k<8, true>(c, k, w);
+    else if (k <= 8) ortho_dots_raw_k<8>(c, k, w);
     else if (k <= 16) ortho_dots_raw_k<16>(c, k, w);
     else ortho_dots_raw_k<32>(c, k, w);
 }
