@@ -130,3 +130,31 @@ def test_one_slab_test_mode_exchanges_with_itself(c2, transport):
     xg, sg = g.gmres_solve(rhs)
     assert sg["converged"] and sg["iters"] == ss["iters"]
     assert rel(xg, xs) < 1e-10
+
+
+def test_group_three_sweep_cgs2_still_matches(c2):
+    """IBMG_CGS2=1 keeps the three-sweep CGS2 over the slabs (fgmres_group); the default is the
+    two-pass lagged CGS2 with the pass-1 sums reduced across the slabs (fgmres_group2).  Both
+    solve to the one-context result with the same iteration count (+-1)."""
+    import os
+    prob, s = c2
+    n = prob.N
+    rhs = s.build_rhs(rand(2 * n * n, 91))
+    xs, ss = s.gmres_solve(rhs)
+    for env in ("1", None):
+        old = os.environ.get("IBMG_CGS2")
+        if env is None:
+            os.environ.pop("IBMG_CGS2", None)
+        else:
+            os.environ["IBMG_CGS2"] = env
+        try:
+            g = SlabGroup.from_problem(prob, 2, min_cells=0)
+        finally:
+            if old is None:
+                os.environ.pop("IBMG_CGS2", None)
+            else:
+                os.environ["IBMG_CGS2"] = old
+        xg, sg = g.gmres_solve(rhs)
+        assert sg["converged"] and abs(sg["iters"] - ss["iters"]) <= 1, (env, sg, ss)
+        assert rel(xg, xs) < 1e-8
+        g.close()
