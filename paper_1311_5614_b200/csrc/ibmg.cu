@@ -125,6 +125,8 @@ struct ibmg_ctx {
     std::string err;
     cudaStream_t s = nullptr;
     cudaStream_t s2 = nullptr;                       // setup side stream (coarsest inverse)
+    cudaStream_t s_copy = nullptr;                   // ibmg_step with host arrays: u^n upload beside the rebuild
+    cudaEvent_t ev_copy = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sizes = nullptr;
     int nlev = 0, lc = 0;  // levels [lc, nlev) run in the single-CTA coarse kernel
     // levels [lt, nlev) run in the 16-CTA cluster kernel (k_cluster_cycle,
@@ -2086,6 +2088,8 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
         CK(cudaSetDevice(p->device));
         CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_sizes, cudaEventDisableTiming));
@@ -2189,6 +2193,8 @@ void ibmg_destroy(ibmg_ctx* c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->s) cudaStreamDestroy(c->s);
     if (c->s2) cudaStreamDestroy(c->s2);
+    if (c->s_copy) cudaStreamDestroy(c->s_copy);
+    if (c->ev_copy) cudaEventDestroy(c->ev_copy);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_sizes) cudaEventDestroy(c->ev_sizes);
@@ -2636,13 +2642,17 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
             CK(cudaMemcpyAsync(c->X, X, sizeof(double) * 2 * c->npts,
                                ptr_kind == IBMG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
         const double* du = u;
-        if (ptr_kind != IBMG_PTR_DEVICE) {  // u^n upload first: the rebuild does not touch stage_a
-            CK(cudaMemcpyAsync(c->stage_a, u, sizeof(double) * 2 * nn, cudaMemcpyHostToDevice, c->s));
+        if (ptr_kind != IBMG_PTR_DEVICE) {
+            // u^n upload on the copy stream, beside the rebuild (which needs only X^n and does not
+            // touch stage_a; the context stream is idle at entry: every call synchronises on return)
+            CK(cudaMemcpyAsync(c->stage_a, u, sizeof(double) * 2 * nn, cudaMemcpyHostToDevice, c->s_copy));
+            CK(cudaEventRecord(c->ev_copy, c->s_copy));
             du = c->stage_a;
         }
         CK(cudaEventRecord(c->ev_t0, c->s));
         rebuild(c, true);
         c->built_dirty = false;
+        if (ptr_kind != IBMG_PTR_DEVICE) CK(cudaStreamWaitEvent(c->s, c->ev_copy, 0));
         build_rhs(c, du, c->bv);
         CK(cudaEventRecord(c->ev_t1, c->s));
         const double t1 = now_ms();
