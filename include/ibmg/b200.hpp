@@ -136,6 +136,20 @@ class SaddleSystem {
         return H;
     }
 
+    // run_simulation: n_steps consecutive steps, the state resident on the device
+    // between them; returns the per-step stats of the steps taken (stops at a non-converged step)
+    std::vector<SolveStats> run_simulation(int n_steps, std::span<double> u, std::span<double> p, std::span<double> X) {
+        if ((int)u.size() != n_vel() || (int)p.size() != N_ * N_)
+            throw std::invalid_argument("run_simulation: size mismatch");
+        std::vector<ibmg_stats> st(n_steps > 0 ? n_steps : 1);
+        int done = 0;
+        check(ibmg_run_simulation(ctx_, n_steps, u.data(), p.data(), X.data(), st.data(), &done, IBMG_PTR_HOST), ctx_);
+        std::vector<SolveStats> out;
+        for (int k = 0; k < done; ++k)
+            out.push_back(SolveStats{st[k].iters, st[k].restarts, st[k].converged != 0, st[k].relres, st[k].setup_ms,
+                                     st[k].solve_ms, st[k].total_ms});
+        return out;
+    }
     // step_implicit: u (2N^2) in/out, p (N^2) out, X in/out
     SolveStats step_implicit(std::span<double> u, std::span<double> p, std::span<double> X) {
         if (int(u.size()) != n_vel() || int(p.size()) != N_ * N_ || X.size() != 2 * npts_)

@@ -139,6 +139,13 @@ int ibmg_vcycle_spectrum(ibmg_ctx* ctx, int m, unsigned long long seed, double* 
 /* Replaces step_implicit: rebuild at X^n, RHS, solve,
  * X^{n+1} = X^n + dt S^T u^{n+1}.  u: 2N^2 in/out, p: N^2 out, X in/out. */
 int ibmg_step(ibmg_ctx* ctx, double* u, double* p, double* X, ibmg_stats* stats, int ptr_kind);
+/* Replaces run_simulation: n_steps consecutive implicit (or, after
+ * ibmg_set_scheme(ctx, 0), explicit) steps with the state resident on the device between
+ * them — host arrays are uploaded once and read back once.  stats (optional) receives
+ * n_steps records, *steps_done the steps taken; the run stops at the first step that
+ * does not converge (status 2).  The results equal n_steps calls of ibmg_step bit for bit. */
+int ibmg_run_simulation(ibmg_ctx* ctx, int n_steps, double* u, double* p, double* X, ibmg_stats* stats,
+                        int* steps_done, int ptr_kind);
 
 /* Number of kernels this context has launched (evidence for bench's gpu_launches). */
 long long ibmg_kernel_launches(const ibmg_ctx* ctx);

@@ -125,6 +125,8 @@ struct ibmg_ctx {
     std::string err;
     cudaStream_t s = nullptr;
     cudaStream_t s2 = nullptr;                       // setup side stream (coarsest inverse)
+    double* sim = nullptr;                           // ibmg_run_simulation with host arrays: device state [u | p | X]
+    size_t sim_cap = 0;
     cudaStream_t s_copy = nullptr;                   // ibmg_step with host arrays: u^n upload beside the rebuild
     cudaEvent_t ev_copy = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sizes = nullptr;
@@ -2193,6 +2195,7 @@ void ibmg_destroy(ibmg_ctx* c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->s) cudaStreamDestroy(c->s);
     if (c->s2) cudaStreamDestroy(c->s2);
+    dfree(c->sim);
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
     if (c->ev_copy) cudaEventDestroy(c->ev_copy);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -2629,13 +2632,15 @@ int ibmg_solve(ibmg_ctx* c, const double* b, double* x, ibmg_stats* st, int ptr_
     });
 }
 
-int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int ptr_kind) {
-    ibmg_stats local{};
-    if (!st) st = &local;
-    return api(c, [&]() -> int {
+}  // extern "C"
+
+// One implicit step (the body of ibmg_step and of every step of ibmg_run_simulation).
+static int step_impl(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int ptr_kind) {
+    {
         if (!c->have_structs) throw InvalidArg("ibmg_step: call ibmg_set_structures first");
         const double t0 = now_ms();
-        wait_inputs(c, ptr_kind);
+        if (ptr_kind >= 0) wait_inputs(c, ptr_kind);
+        else ptr_kind = IBMG_PTR_DEVICE;  // device state of a running simulation: no caller stream to wait for
         const size_t nn = size_t(c->prm.N) * c->prm.N;
         // X^n in, lagged operators rebuilt at X^n
         if (c->npts)
@@ -2673,6 +2678,54 @@ int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int 
         st->setup_ms = setup_ms;
         st->solve_ms = t2 - t1;
         st->total_ms = now_ms() - t0;
+        return rc;
+    }
+}
+
+extern "C" {
+
+int ibmg_step(ibmg_ctx* c, double* u, double* p, double* X, ibmg_stats* st, int ptr_kind) {
+    ibmg_stats local{};
+    if (!st) st = &local;
+    return api(c, [&]() -> int { return step_impl(c, u, p, X, st, ptr_kind); });
+}
+
+int ibmg_run_simulation(ibmg_ctx* c, int n_steps, double* u, double* p, double* X, ibmg_stats* stats, int* steps_done,
+                        int ptr_kind) {
+    if (steps_done) *steps_done = 0;
+    return api(c, [&]() -> int {
+        if (n_steps < 0) throw InvalidArg("ibmg_run_simulation: n_steps >= 0");
+        if (!c->have_structs) throw InvalidArg("ibmg_run_simulation: call ibmg_set_structures first");
+        const size_t nn = size_t(c->prm.N) * c->prm.N, nx = 2 * size_t(c->npts);
+        double *du = u, *dp = p, *dX = X;
+        if (ptr_kind != IBMG_PTR_DEVICE) {  // the state stays on the device between the steps
+            if (c->sim_cap < 3 * nn + nx) {
+                dfree(c->sim);
+                c->sim_cap = 3 * nn + nx;
+                c->sim = dalloc<double>(c->sim_cap);
+            }
+            du = c->sim;
+            dp = c->sim + 2 * nn;
+            dX = c->sim + 3 * nn;
+            CK(cudaMemcpyAsync(du, u, sizeof(double) * 2 * nn, cudaMemcpyHostToDevice, c->s));
+            if (nx) CK(cudaMemcpyAsync(dX, X, sizeof(double) * nx, cudaMemcpyHostToDevice, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        }
+        int rc = IBMG_OK;
+        ibmg_stats local{};
+        for (int k = 0; k < n_steps; ++k) {
+            // inputs of step k are the context stream's own outputs of step k-1 (already ordered);
+            // the caller's stream matters for the first step only
+            rc = step_impl(c, du, dp, dX, stats ? stats + k : &local, k == 0 && ptr_kind == IBMG_PTR_DEVICE ? IBMG_PTR_DEVICE : -1);
+            if (steps_done) *steps_done = k + 1;
+            if (rc != IBMG_OK) break;
+        }
+        if (ptr_kind != IBMG_PTR_DEVICE && n_steps > 0) {
+            CK(cudaMemcpyAsync(u, du, sizeof(double) * 2 * nn, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaMemcpyAsync(p, dp, sizeof(double) * nn, cudaMemcpyDeviceToHost, c->s));
+            if (nx) CK(cudaMemcpyAsync(X, dX, sizeof(double) * nx, cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        }
         return rc;
     });
 }

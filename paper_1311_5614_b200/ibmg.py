@@ -53,7 +53,7 @@ EXPORTS = ["ibmg_create", "ibmg_destroy", "ibmg_last_error", "ibmg_set_structure
            "ibmg_vcycle_spectrum", "ibmg_set_scheme", "ibmg_set_input_stream", "ibmg_debug_cluster_trace",
            "ibmg_cluster_level", "ibmg_batch_create", "ibmg_batch_destroy", "ibmg_batch_last_error",
            "ibmg_batch_kernel_launches", "ibmg_batch_stream", "ibmg_batch_set_structures", "ibmg_batch_step",
-           "ibmg_batch_prepare", "ibmg_batch_solve"]
+           "ibmg_batch_prepare", "ibmg_batch_solve", "ibmg_run_simulation"]
 
 
 def lib_path() -> str:
@@ -93,6 +93,7 @@ def lib(build_if_missing: bool = True):
     L.ibmg_spread.argtypes = [vp, dp, dp, ip]
     L.ibmg_solve.argtypes = [vp, dp, dp, C.POINTER(Stats), ip]
     L.ibmg_step.argtypes = [vp, dp, dp, dp, C.POINTER(Stats), ip]
+    L.ibmg_run_simulation.argtypes = [vp, ip, dp, dp, dp, vp, C.POINTER(C.c_int), ip]
     L.ibmg_kernel_launches.restype = C.c_longlong
     L.ibmg_kernel_launches.argtypes = [vp]
     L.ibmg_stream.restype = C.c_void_p
@@ -356,6 +357,15 @@ class SaddleSystem:
         if not getattr(self, "_implicit", True):
             self.set_scheme(True)
         return self._step(u, p, X)
+
+    def run_simulation(self, n_steps, u, p, X):
+        """n_steps consecutive steps in place on (u, p, X) with the state resident on the device
+        between them (run_simulation); returns the per-step stats of the steps taken."""
+        st = (Stats * max(n_steps, 1))()
+        done = C.c_int()
+        (up, k), (pp, _), (Xp, _) = self._p(u), self._p(p), self._p(X)
+        self._chk(self._L.ibmg_run_simulation(self._h, n_steps, up, pp, Xp, st, C.byref(done), k), ok=(0, 2))
+        return [st[i].as_dict() for i in range(done.value)]
 
     def _step(self, u, p, X):
         st = Stats()

@@ -264,3 +264,27 @@ def test_invalid_arguments_raise_value_error():
     with pytest.raises(ValueError):
         g.sweep(np.zeros(3 * 64 * 64), np.zeros(3 * 64 * 64), level=3)  # coarse-kernel level
 
+
+
+def test_run_simulation_equals_repeated_steps():
+    """ibmg_run_simulation (run_simulation): the state stays on the device between
+    the steps; results are bit for bit those of n calls of ibmg_step, with host arrays and with
+    device tensors."""
+    import torch
+    prob = configs.config2(1e4, N=64, nb=128)
+    n = prob.N
+    g = SaddleSystem.from_problem(prob)
+    u, p, X = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+    its = [g.step_implicit(u, p, X)["iters"] for _ in range(3)]
+    g2 = SaddleSystem.from_problem(prob)
+    u2, p2, X2 = np.zeros(2 * n * n), np.zeros(n * n), prob.X.reshape(-1).copy()
+    sts = g2.run_simulation(3, u2, p2, X2)
+    assert [s["iters"] for s in sts] == its and all(s["converged"] for s in sts)
+    assert np.array_equal(u, u2) and np.array_equal(p, p2) and np.array_equal(X, X2)
+    g3 = SaddleSystem.from_problem(prob)
+    ud = torch.zeros(2 * n * n, dtype=torch.float64, device="cuda")
+    pd = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+    Xd = torch.tensor(prob.X.reshape(-1), dtype=torch.float64, device="cuda")
+    sts = g3.run_simulation(3, ud, pd, Xd)
+    assert len(sts) == 3 and np.array_equal(ud.cpu().numpy(), u) and np.array_equal(Xd.cpu().numpy(), X)
+    assert g3.run_simulation(0, ud, pd, Xd) == []
