@@ -353,6 +353,19 @@ def run_ours(args, rank, world):
     h2d = 8 * (2 * n2 + 2 * int(np.mean(NBs)))
     d2h = 8 * (2 * n2 + n2 + 2 * int(np.mean(NBs)))
 
+    # auxiliary: each block's whole configured trajectory through ibmg_run_simulation (the state stays on
+    # the device between the steps, host arrays cross PCIe once each way); wall clock per step
+    traj_ms = []
+    for kb in range(len(probs)):
+        Uh[kb][:] = 0.0
+        Ph[kb][:] = 0.0
+        Xh[kb][:] = probs[kb].X.reshape(-1)
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sts = ctxs[kb].run_simulation(WL["per"], Uh[kb], Ph[kb], Xh[kb])
+        traj_ms.append((time.perf_counter() - t0) * 1e3 / max(len(sts), 1))
+
     result = None
     if rank == 0:
         # profiled pass (live CUDA-event timing per kernel) over every configured step
@@ -361,7 +374,7 @@ def run_ours(args, rank, world):
         roof, kernel_shares = roofline_of(prof_tot, ctxs, N_GRID, step_iters, prs, WL["name"])
         result = {
             "total_ms_max": total_ms_max, "vcyc_all": vcyc_all, "ms": ms, "iters": iters, "setup": setup,
-            "launches": launches, "clocks": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h,
+            "launches": launches, "clocks": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "traj_ms": traj_ms,
             "roofline": roof, "kernels": kernel_shares, "converged": conv,
         }
     for c in ctxs:
@@ -712,6 +725,9 @@ def main():
             "clocks": res["clocks"],
             "e2e": {"value": round(float(np.mean(res["e2e_ms"])), 4), "unit": "ms",
                     "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},
+            "trajectory": {"api": "ibmg_run_simulation (state resident on the device between the steps; host "
+                                  "arrays cross PCIe once per trajectory)",
+                           "steps": WL["per"], "ms_per_step": round(float(np.mean(res["traj_ms"])), 4)},
             "roofline": res["roofline"],
             "kernels": res["kernels"],
         }
