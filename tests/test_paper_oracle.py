@@ -224,3 +224,25 @@ def test_multicolour_ordering_keeps_the_counts():
                 assert abs(its[1] - its[0]) <= 1, (box, rel_stiff, its)
     o = O.PaperOracle(64, 1, 1, 1, alpha=393.0, mesh=mesh, order=1)
     assert [o.level_reach(l) for l in range(o.nlevels)] == [5, 4, 3, 3, 1]
+
+
+def test_fig5_standalone_mg_failure_thresholds():
+    """Fig. 5(a): the stand-alone multigrid solver with boxes 2 and 4 fails
+    at about the same relative stiffness as single-cell boxes (between 100 and 200), with fewer iterations
+    before that; boxes 8 and 16 converge an order of magnitude further (still at 1000, not at 2000) with
+    very similar counts."""
+    mesh = configs.paper_annulus(32)
+
+    def mg(box, rel_stiff):
+        alpha = rel_stiff * configs.PAPER_ALPHA_EXP[32]
+        o = O.PaperOracle(32, box, 1, 1, alpha=alpha, mesh=mesh)
+        return o.mg_solve(o.rhs(True, alpha), 1e-6, 100)[1]
+
+    at100 = {b: mg(b, 100) for b in (1, 2, 4, 8, 16)}
+    assert all(s["converged"] for s in at100.values())
+    assert at100[1]["iters"] > at100[2]["iters"] > at100[4]["iters"] > at100[8]["iters"] >= at100[16]["iters"]
+    for b in (1, 2, 4):
+        assert not mg(b, 200)["converged"]
+    for b in (8, 16):
+        assert mg(b, 1000)["converged"] and not mg(b, 2000)["converged"]
+    assert abs(mg(8, 500)["iters"] - mg(16, 500)["iters"]) <= 5
