@@ -246,3 +246,24 @@ def test_fig5_standalone_mg_failure_thresholds():
     for b in (8, 16):
         assert mg(b, 1000)["converged"] and not mg(b, 2000)["converged"]
     assert abs(mg(8, 500)["iters"] - mg(16, 500)["iters"]) <= 5
+
+
+def test_fig6_grid_refinement():
+    """Fig. 6: MG-GMRES counts at fixed alpha on 32^2, 64^2, 128^2.
+    Non-stiff and mildly stiff (alpha = 6, 60): independent of the grid for every box size; moderately
+    stiff (alpha = 600): growing for single-cell boxes (29, 42, 49), nearly independent for box 8 (9, 10, 11)."""
+    def counts(alpha, box):
+        out = []
+        for N in (32, 64, 128):
+            o = O.PaperOracle(N, box, 1, 1, alpha=alpha, mesh=configs.paper_annulus(N))
+            st = o.gmres_solve(o.rhs(True, alpha), 1e-6, 100)[1]
+            assert st["converged"]
+            out.append(st["iters"])
+        return out
+
+    for alpha in (6.0, 60.0):
+        for box in (1, 4, 8):
+            c = counts(alpha, box)
+            assert max(c) - min(c) <= 3, (alpha, box, c)
+    small, big = counts(600.0, 1), counts(600.0, 8)
+    assert small[2] - small[0] >= 10 and big[2] - big[0] <= 3, (small, big)
