@@ -213,6 +213,19 @@ def test_multicolour_ordering_matches_oracle(box):
     assert rel(gl.v_cycle(b), g.v_cycle(b)) > 1e-6
 
 
+def test_solve_matches_oracle_at_128():
+    """h = 2^-7 (608 x 13 nodes, 49k unknowns, E with 2.4M entries assembled on the device): the same
+    MG-GMRES iteration count as the oracle and u, p to 1e-8 when both converge to 1e-10."""
+    N, alpha = 128, 100 * configs.PAPER_ALPHA_EXP[128]
+    g, o = pair(N, 4, alpha)
+    b = g.build_rhs(True, alpha)
+    assert rel(b, o.rhs(True, alpha)) < 1e-12
+    xg, sg, _ = g.gmres_solve(b, 1e-10, 200)
+    xo, so, _ = o.gmres_solve(b, 1e-10, 200)
+    assert sg["converged"] and so["converged"] and abs(sg["iters"] - so["iters"]) <= 1
+    assert rel(xg, xo) < 1e-8
+
+
 def test_rejects_bad_input():
     g = PaperSystem(32, 4, 1, 1, 1.0)
     with pytest.raises(ValueError):
