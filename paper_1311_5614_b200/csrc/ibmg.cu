@@ -214,6 +214,8 @@ struct ibmg_ctx {
     int df_maxn = kDataflowMaxN;  // levels n <= df_maxn: one dataflow launch per sweep (IBMG_DF_MAXN)
     int ortho_per_cta = 2048;  // CGS2 grid: ~this many doubles per CTA on small vectors (IBMG_ORTHO_PER_CTA; 0: fixed grids)
     bool tma = true;        // TMA staging of the interior tiles' w regions in k_plain_df (IBMG_TMA=0: cp.async)
+    bool pdf2 = true;       // warp-specialised plain phase k_plain_df2 (IBMG_PDF2=0: one warp per tile, k_plain_df)
+    int pdf2_grid_max = 0;
     bool gather_first = false; // fused apply / restriction: gathers before the grid CTAs (IBMG_GF=1); measured
                                // slower (C4 restriction 24 -> 40 ms: the grid CTAs wait holding their SMs)
     bool gj_regs = true;    // box inverses: 64-thread register Gauss-Jordan (IBMG_GJ256=1: 256-thread [A|I] form)
@@ -391,7 +393,8 @@ void alloc_levels(ibmg_ctx* c) {
                 CK(cudaMemsetAsync(lb.tflags, 0, sizeof(unsigned) * (n / kTile) * (n / kTile), c->s));
             }
             if (n > c->df_maxn) {
-                const std::vector<int> seg = plain_df_order(n / kTile, c->pdf_grid_max, c->pdf_skew);
+                const std::vector<int> seg =
+                    plain_df_order(n / kTile, c->pdf2 ? kPdf2NB * c->pdf2_grid_max : c->pdf_grid_max, c->pdf_skew);
                 lb.pdf_seg = dalloc<int>(seg.size());
                 CK(cudaMemcpy(lb.pdf_seg, seg.data(), sizeof(int) * seg.size(), cudaMemcpyHostToDevice));
             }
@@ -1361,6 +1364,11 @@ void sweep_level(ibmg_ctx* c, int l, const double* b, double* w) {
         const int lim = c->grid_limit > 0 ? std::min(c->grid_limit, c->pdf_grid_max) : c->pdf_grid_max;
         if (c->prof) prof_begin(c, "k_plain_df");
         const TmaPlanes tp = tma_planes(c, w, n);
+        if (c->pdf2) {
+            const int lim2 = c->grid_limit > 0 ? std::min(c->grid_limit, c->pdf2_grid_max) : c->pdf2_grid_max;
+            launch_k(c, k_plain_df2, dim3(std::min(lim2, 4 * per)), dim3(32 * kPdf2NB), kPdf2Smem, true, L, b, w,
+                     (const uint8_t*)lb.big, lb.tflags, ++lb.tepoch, (const int*)lb.pdf_seg, tp);
+        } else
         launch_k(c, k_plain_df, dim3(std::min(lim, 4 * per)), dim3(32), kPdfSmem, true, L, b, w,
                  (const uint8_t*)lb.big, lb.tflags, ++lb.tepoch, (const int*)lb.pdf_seg, tp);
         if (c->prof) prof_end(c);
@@ -2083,6 +2091,7 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
     if (const char* e = std::getenv("IBMG_GJ256")) c->gj_regs = std::atoi(e) == 0;
     if (const char* e = std::getenv("IBMG_GF")) c->gather_first = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_TMA")) c->tma = std::atoi(e) != 0;
+    if (const char* e = std::getenv("IBMG_PDF2")) c->pdf2 = std::atoi(e) != 0;
     if (const char* e = std::getenv("IBMG_ORTHO_PER_CTA")) c->ortho_per_cta = std::atoi(e);
     c->prm = *p;
     c->krows = krows;
@@ -2123,6 +2132,9 @@ int create_ctx(const ibmg_params* p, int krows, ibmg_ctx** out) {
             CK(cudaFuncSetAttribute(k_plain_df, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPdfSmem)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_df, 32, kPdfSmem));
             c->pdf_grid_max = std::max(1, per_sm * sms);
+            CK(cudaFuncSetAttribute(k_plain_df2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPdf2Smem)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_df2, 32 * kPdf2NB, kPdf2Smem));
+            c->pdf2_grid_max = std::max(1, per_sm * sms);
         }
         alloc_levels(c);
         CK(cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(coarse_smem(c))));

@@ -932,6 +932,133 @@ __global__ void __launch_bounds__(32) k_plain_df(Lev L, const double* __restrict
     }
 }
 
+// ---- warp-specialised band-major plain phase (k_plain_df2, opt-in IBMG_PDF2=1) ----
+// Same tasks, order and arithmetic as k_plain_df, two warps per CTA: the LOADER warp
+// stages tile t + 1 (b region, dependency waits, w region by tensor copies or cp.async)
+// into the second buffer while the COMPUTE warp runs the 8 colour passes, the write-back
+// and the publish of tile t.  full[s] / empty[s] mbarriers hand the buffers over.
+__device__ __forceinline__ void mbar_arrive(unsigned long long* mb) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+// arrive on mb once all cp.async copies this thread has issued so far have landed (no wait here)
+__device__ __forceinline__ void cp_async_arrive(unsigned long long* mb) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+#ifndef IBMG_PDF2_NC
+#define IBMG_PDF2_NC 3
+#endif
+#ifndef IBMG_PDF2_NL
+#define IBMG_PDF2_NL 1
+#endif
+constexpr int kPdf2NC = IBMG_PDF2_NC;        // compute warps per CTA
+constexpr int kPdf2NL = IBMG_PDF2_NL;        // loader warps per CTA (a loader stages ~1 tile per us: 81 8-byte b copies per lane)
+constexpr int kPdf2NB = kPdf2NC + kPdf2NL;   // tile buffers per CTA
+constexpr size_t kPdf2Buf = (kDfTileBytes + 127) / 128 * 128;
+constexpr size_t kPdf2Smem = kPdf2NB * kPdf2Buf;
+__global__ void __launch_bounds__(32 * kPdf2NB)
+    k_plain_df2(Lev L, const double* __restrict__ b, double* __restrict__ w, const uint8_t* __restrict__ big,
+                unsigned* tflags, unsigned epoch, const int* __restrict__ seg, const __grid_constant__ TmaPlanes tm) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char pdm[];
+    __shared__ __align__(8) unsigned long long full[kPdf2NB], empty[kPdf2NB];
+    const int n = L.n, nn = L.nn, lane = threadIdx.x & 31, role = threadIdx.x >> 5;  // roles < NL: loaders
+    const int nt = n / kTile, half = nt >> 1, ntiles = nt * nt, nbk = n >> 2;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kPdf2NB; ++q) {
+            mbar_init(&full[q], 33);  // 32 lanes' cp.async completions + lane 0's arrival (with the tensor bytes)
+            mbar_init(&empty[q], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int it = 0;
+    for (int task = blockIdx.x; task < ntiles; task += gridDim.x, ++it) {
+        // loader it % NL stages the CTA's it-th tile, compute warp it % NC relaxes it
+        if (role < kPdf2NL ? role != it % kPdf2NL : role - kPdf2NL != it % kPdf2NC) continue;
+        const int sl = it % kPdf2NB;
+        const unsigned ph = (it / kPdf2NB) & 1;
+        double* sw = reinterpret_cast<double*>(pdm + sl * kPdf2Buf);
+        double* sb = sw + kDfWDoubles;
+        const int sI = task / half, i = task - sI * half;
+        const int sg = __ldg(seg + sI), ty = sg >> 2, tc = sg & 3, tx = 2 * i + (tc & 1);
+        const int x0 = tx * kTile, y0 = ty * kTile;
+        if (role < kPdf2NL) {
+            // ---------------- loader ----------------
+            if (it >= kPdf2NB) mbar_wait(&empty[sl], ph ^ 1u);  // its previous tile's compute warp is done with it
+            for (int qq = lane; qq < 289; qq += 32) {
+                const int a = qq % 17, bb = qq / 17;
+                const size_t gi = wr(x0 + a, n) + (size_t)wr(y0 + bb, n) * n;
+                cp_async8(&sb[qq], b + gi);
+                cp_async8(&sb[289 + qq], b + nn + gi);
+                cp_async8(&sb[578 + qq], b + 2 * nn + gi);
+            }
+            if (lane < 8) {  // adjacent tiles of smaller tile colour
+                const int d = lane < 4 ? lane : lane + 1;
+                const int ax = wr(tx + d % 3 - 1, nt), ay = wr(ty + d / 3 - 1, nt);
+                const int ac = (ax & 1) + 2 * (ay & 1);
+                if (ac < tc)
+                    while (ld_acquire(tflags + ax + ay * nt) != epoch) __nanosleep(8);
+            }
+            __syncwarp();
+            // nothing below waits for a copy: the lanes' cp.async completions and the tensor bytes
+            // arrive on full[sl] by themselves, and the loader moves on to the next tile
+            const bool tma = tm.use && x0 >= 2 && y0 >= 2 && x0 + kTile + 2 <= n && y0 + kTile + 2 <= n;
+            if (!tma && lane < 30) {
+                const int a2 = lane % 10, r0 = lane / 10;
+                const int xg = wr(x0 - 2 + 2 * a2, n);
+                for (int row = r0; row < 3 * kReg; row += 3) {
+                    const int f = row / kReg, bb = row - f * kReg;
+                    const size_t gi = xg + (size_t)wr(y0 - 2 + bb, n) * n;
+                    cp_async16_cg(&sw[f * kRegP + bb * kRegS + 2 * a2], w + (size_t)f * nn + gi);
+                }
+            }
+            cp_async_arrive(&full[sl]);
+            if (lane == 0) {
+                if (tma) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&full[sl], 3u * kRegP * 8u);
+#pragma unroll
+                    for (int f = 0; f < 3; ++f) tma_load_2d(sw + f * kRegP, &tm.m[f], x0 - 2, y0 - 2, &full[sl]);
+                } else {
+                    mbar_arrive(&full[sl]);
+                }
+            }
+        } else {
+            // ---------------- compute ----------------
+            const bool isbig = lane < 16 && big[(x0 >> 2) + (lane & 3) + ((y0 >> 2) + (lane >> 2)) * nbk];
+            const unsigned bigmask = __ballot_sync(0xffffffffu, isbig);
+            mbar_wait(&full[sl], ph);
+            relayout_region(sw, lane);  // (-DIBMG_RELAYOUT=1: to the odd row stride; else nothing)
+            TileWW W{sw};
+            TileB B{sb};
+            for (int pc = 0; pc < 8; ++pc) {
+                const int lj = lane >> 1, li = ((pc - 2 * lj) & 7) + 8 * (lane & 1);
+                if (!((bigmask >> ((li >> 2) + 4 * (lj >> 2))) & 1)) plain_cell(L, W, B, li, lj);
+                __syncwarp();
+            }
+            {
+                const int a = lane & 15, h = lane >> 4;
+                const int xa = wr(x0 + a, n);
+                for (int bb = h; bb < 17; bb += 2) {
+                    const size_t gi = xa + (size_t)wr(y0 + bb, n) * n;
+                    if (bb < 16) {
+                        __stcg(w + gi, W(0, a, bb));
+                        __stcg(w + 2 * nn + gi, W(2, a, bb));
+                    }
+                    __stcg(w + nn + gi, W(1, a, bb));
+                }
+                if (lane < 16) __stcg(w + wr(x0 + 16, n) + (size_t)wr(y0 + lane, n) * n, W(0, 16, lane));
+            }
+            __syncwarp();
+            if (lane == 0) {
+                st_release(tflags + tx + ty * nt, epoch);
+                mbar_arrive(&empty[sl]);
+            }
+        }
+    }
+}
+
 // ES = false: the double-buffered SlabSlot variant (inverse staged in shared
 // memory, 1 CTA per SM).  ES = true: one E'-row slot refilled as soon as a
 // block's rows are consumed and the 25 KB inverse streamed from L2 into

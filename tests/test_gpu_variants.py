@@ -93,3 +93,19 @@ def test_register_gauss_jordan_vcycle_c3():
     assert rel(ga.v_cycle(b), gb.v_cycle(b)) < 1e-12
     ga.close()
     gb.close()
+
+
+def test_warp_specialised_plain_phase_c3_bitwise():
+    """IBMG_PDF2 (default 1): the band-major plain phase with a loader warp feeding three compute
+    warps per CTA (k_plain_df2) runs the same tasks in the same order with the same arithmetic as
+    the one-warp-per-tile kernel (IBMG_PDF2=0): the V-cycle and the step are bitwise equal (C3's
+    level 1024)."""
+    prob = configs.config3()
+    ga, gb = make(prob, IBMG_PDF2=1), make(prob, IBMG_PDF2=0)
+    b = ga.build_rhs(rand(2 * prob.N ** 2, seed=5))
+    assert np.array_equal(ga.v_cycle(b), gb.v_cycle(b))
+    ua, pa, Xa, sa = step(ga, prob)
+    ub, pb, Xb, sb = step(gb, prob)
+    assert sa["iters"] == sb["iters"] and np.array_equal(ua, ub) and np.array_equal(Xa, Xb)
+    ga.close()
+    gb.close()
