@@ -360,6 +360,7 @@ def run_ours(args, rank, world):
         Uh[kb][:] = 0.0
         Ph[kb][:] = 0.0
         Xh[kb][:] = probs[kb].X.reshape(-1)
+        ctxs[kb].run_simulation(0, Uh[kb], Ph[kb], Xh[kb])  # (the device state buffer is allocated on first use)
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
