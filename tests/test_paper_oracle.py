@@ -267,3 +267,25 @@ def test_fig6_grid_refinement():
             assert max(c) - min(c) <= 3, (alpha, box, c)
     small, big = counts(600.0, 1), counts(600.0, 8)
     assert small[2] - small[0] >= 10 and big[2] - big[0] <= 3, (small, big)
+
+
+def test_elasticity_symmetry_semidefiniteness_and_adjointness(orc32):
+    """SPEC.md:690 property suite on the thick annulus: the fine E = S A_f S* is symmetric and negative
+    semidefinite (A_f is a periodic second difference), spread and interpolate are adjoint with their
+    ds^2 / h^2 weights, and E applied as a matrix equals spread(A_f interpolate(.)) h^2 ds^2-consistently."""
+    E = csr(orc32.elasticity(0), (nvel, nvel))
+    assert abs(E - E.T).max() <= 1e-12 * abs(E).max()
+    rng = np.random.default_rng(17)
+    for _ in range(20):
+        x = rng.uniform(-1, 1, nvel)
+        assert x @ (E @ x) <= 1e-10 * abs(E).max()
+    mesh = configs.paper_annulus(n)
+    F = rng.uniform(-1, 1, 2 * mesh.m1 * mesh.m2)
+    vel = rng.uniform(-1, 1, nvel)
+    lhs = orc32.spread(F) @ vel * (1.0 / n) ** 2
+    rhs = F @ orc32.interp(vel).reshape(-1) * mesh.ds ** 2
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    # matrix-free twin (elasticity.cpp:109-117): E vel = spread(second difference(interpolate(vel)))
+    U = orc32.interp(vel).reshape(mesh.m2, mesh.m1, 2)
+    D = (np.roll(U, 1, axis=1) + np.roll(U, -1, axis=1) - 2 * U) / mesh.ds ** 2
+    assert rel(orc32.spread(D.reshape(-1)), E @ vel) < 1e-12
